@@ -1,0 +1,151 @@
+/* libkotgpu — C ABI of the B200-native semismooth-Newton kernel-OT solver.
+ *
+ * Drop-in boundary for the reference package `kot` (pure Python;
+ * /root/reference/pkg/src/kot).  The reference exposes no native ABI, so each
+ * entry point below replaces the Python call it cites; the Python host layer
+ * (paper_2310_14087_b200/) binds them with ctypes exactly as INTEGRATION.md
+ * shows.  Conventions:
+ *   - all arrays are caller-owned, C-contiguous (row-major) float64; inputs
+ *     are read-only and copied to the device, outputs are caller-allocated;
+ *   - every function returns a status (0 = ok) that maps 1:1 onto the
+ *     reference's exception classes; kot_last_error() gives the message
+ *     (thread-local);
+ *   - one handle per problem, each with its own CUDA stream; handles may be
+ *     used from different host threads concurrently; no global mutable state.
+ */
+#ifndef KOTGPU_H_
+#define KOTGPU_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  KOT_OK = 0,
+  KOT_EINVAL = 1,       /* ValueError                 problem.py:116-119, newton.py:61-71, solver.py:45-51 */
+  KOT_EINDEFINITE = 2,  /* IndefiniteKernelError      linalg.py:114 */
+  KOT_EEIG = 3,         /* EigenSolveError            linalg.py:70 */
+  KOT_ENUMERICS = 4,    /* SolverNumericsError        solver.py:28-33 (partial trace returned) */
+  KOT_ECG = 5,          /* FloatingPointError         linalg.py:146,156 */
+  KOT_ECUDA = 6,        /* CUDA runtime failure */
+  KOT_EASSERT = 7       /* AssertionError             psdcone.py:77 */
+};
+
+typedef struct kot_problem kot_problem;
+
+/* SolverConfig + NewtonConfig + EgConfig flattened (solver.py:36-51,
+ * newton.py:36-71, eg.py:18-24). */
+typedef struct {
+  double tau, kappa, alpha1, alpha2, beta0, beta1, beta2, theta_min, theta_max, theta0;
+  int cg_max, cg_restarts;
+  double cg_tol;
+  int has_cg_tol;
+  double eg_stepsize, residual_tol;
+  int max_iter, safeguard_every;
+} kot_solver_cfg;
+
+/* IterationRecord (solver.py:54-73) + n_pos and CG attempts. */
+typedef struct {
+  int iteration;
+  double res_accepted, res_ssn, res_eg;
+  int accepted_ssn;
+  double theta, mu;
+  int cg_iters, criterion_met;
+  double crit_lhs, crit_rhs, eg_ms, newton_ms, cg_ms, resid_ms, step_ms;
+  int n_pos, attempts;
+} kot_iter_record;
+
+/* SolverReport scalars (solver.py:89-101). */
+typedef struct {
+  int converged;     /* termination == "converged" (else "max_iter") */
+  int iterations;    /* len(trace) */
+  double residual_norm;
+  double ot_estimate; /* NaN if the instance carries no embedding sums */
+  double total_ms;
+} kot_report;
+
+/* on_iteration observer (solver.py:76-86, 170-181); host copies of w, r, dw. */
+typedef void (*kot_iter_cb)(void* user, int iteration, const double* w_gamma, const double* w_x,
+                            const double* r_gamma, const double* r_x, double mu, double theta,
+                            const double* dw_gamma, const double* dw_x, int criterion_met);
+
+/* ---- problem construction --------------------------------------------- */
+
+/* Upload a host ProblemData (problem.py:86-123; q is symmetrised as in :112). */
+int kot_problem_create(const double* q, const double* z, double q_sq, const double* r_upper,
+                       const double* embed /* nullable */, int l, double lambda1, double lambda2,
+                       double jitter, int device, kot_problem** out);
+
+/* assemble() on device (problem.py:135-169): Gaussian Grams, mean embeddings,
+ * embedding norms, pair Gram K and its jittered Cholesky factor. */
+int kot_assemble(const double* xs, int n_mu, const double* ys, int n_nu, const double* xt,
+                 const double* yt, int l, int d, double bandwidth_sq, double lambda1, double lambda2,
+                 int device, kot_problem** out);
+
+int kot_problem_info(const kot_problem* p, int* l, double* q_sq, double* jitter, double* lambda1,
+                     double* lambda2, int* has_embed);
+
+/* Download ProblemData fields (any pointer may be NULL). */
+int kot_problem_download(kot_problem* p, double* q, double* z, double* r_upper, double* embed,
+                         double* kmat);
+
+void kot_problem_destroy(kot_problem* p);
+
+const char* kot_last_error(void);
+
+/* ---- solve (solver.py:114-233, 236-289) -------------------------------- */
+
+int kot_solve(kot_problem* p, const kot_solver_cfg* cfg, kot_iter_cb cb, void* user,
+              double* gamma_out /* l */, double* x_out /* l*l, nullable */,
+              kot_iter_record* trace /* trace_cap */, int trace_cap, kot_report* out);
+
+int kot_solve_pure_eg(kot_problem* p, const kot_solver_cfg* cfg, double* gamma_out, double* x_out,
+                      kot_iter_record* trace, int trace_cap, kot_report* out);
+
+/* One loop body from host state (w, v, theta) at iteration k: the lock-step
+ * replay unit of the parity protocol. */
+int kot_iterate(kot_problem* p, const kot_solver_cfg* cfg, const double* w_gamma, const double* w_x,
+                const double* v_gamma, const double* v_x, double theta, int k, double* w_gamma_out,
+                double* w_x_out, double* v_gamma_out, double* v_x_out, double* theta_out,
+                kot_iter_record* rec);
+
+/* ---- operators (host buffers in/out; per-kernel parity) ----------------- */
+
+/* gram_matrix (kernels.py:61-73), square form: out = exp(-|a_i-a_j|^2/(2 bw)), unit diag. */
+int kot_gram(const double* pts, int n, int d, double bandwidth_sq, int device, double* out);
+/* cholesky_psd (linalg.py:91-114). */
+int kot_cholesky_psd(const double* k, int n, int device, double* r_upper, double* jitter);
+/* sym_eig (linalg.py:60-83): descending eigenvalues, eigvecs in columns, n_pos. */
+int kot_sym_eig(const double* z, int n, int device, double* vecs, double* vals, int* n_pos);
+/* proj_psd (psdcone.py:62-64). */
+int kot_proj_psd(const double* z, int n, int device, double* out);
+/* apply_eliminator / apply_proj_jacobian at the decomposition of z (psdcone.py:94-151).
+ * mode 0: eliminator with mu; mode 1: projection Jacobian.  path: -1 auto, 0 POS, 1 NONPOS. */
+int kot_spectral_apply(const double* z, int n, int device, int mode, double mu, int path,
+                       const double* s, double* out);
+int kot_phi_forward(kot_problem* p, const double* x, double* out);      /* problem.py:172-177 */
+int kot_phi_adjoint(kot_problem* p, const double* gamma, double* out);  /* problem.py:180-185 */
+/* residual_parts (problem.py:204-214): r1, r2, eigenvalues of Z, n_pos, ||r||. */
+int kot_residual_parts(kot_problem* p, const double* gamma, const double* x, double* r1, double* r2,
+                       double* eigvals, int* n_pos, double* res_norm);
+/* middle_operator (newton.py:116-128) at the context of w with damping theta. */
+int kot_middle_operator(kot_problem* p, const double* gamma, const double* x, double theta,
+                        const double* v, double* out, double* mu_out);
+/* newton_direction (newton.py:144-195) at w with damping theta. */
+int kot_newton_direction(kot_problem* p, const kot_solver_cfg* cfg, const double* gamma,
+                         const double* x, double theta, double* dgamma, double* dx, int* cg_iters,
+                         int* criterion_met, double* crit_lhs, double* crit_rhs);
+/* eg_step (eg.py:34-41). */
+int kot_eg_step(kot_problem* p, const double* gamma, const double* x, double stepsize,
+                double* gamma_out, double* x_out);
+/* objective (problem.py:192-196) and ot_estimate (problem.py:244-251). */
+int kot_objective(kot_problem* p, const double* gamma, double* out);
+int kot_ot_estimate(kot_problem* p, const double* gamma, double* out);
+
+/* Diagnostics: number of kernels libkotgpu launched since load (all handles). */
+long long kot_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KOTGPU_H_ */

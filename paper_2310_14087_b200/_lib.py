@@ -1,0 +1,171 @@
+"""ctypes binding of libkotgpu (C ABI in include/kotgpu.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (nvcc,
+``-gencode arch=compute_100a,code=sm_100a``).  There is no CPU fallback: if
+the library is missing every call raises, and on a machine without a B200 the
+calls fail with the CUDA error the runtime reports.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkotgpu.so")
+
+dptr = C.POINTER(C.c_double)
+iptr = C.POINTER(C.c_int)
+
+
+class SolverCfgC(C.Structure):
+    _fields_ = [(n, C.c_double) for n in (
+        "tau", "kappa", "alpha1", "alpha2", "beta0", "beta1", "beta2", "theta_min", "theta_max", "theta0")] + [
+        ("cg_max", C.c_int), ("cg_restarts", C.c_int), ("cg_tol", C.c_double), ("has_cg_tol", C.c_int),
+        ("eg_stepsize", C.c_double), ("residual_tol", C.c_double), ("max_iter", C.c_int),
+        ("safeguard_every", C.c_int)]
+
+
+class IterRecordC(C.Structure):
+    _fields_ = [("iteration", C.c_int), ("res_accepted", C.c_double), ("res_ssn", C.c_double),
+                ("res_eg", C.c_double), ("accepted_ssn", C.c_int), ("theta", C.c_double), ("mu", C.c_double),
+                ("cg_iters", C.c_int), ("criterion_met", C.c_int), ("crit_lhs", C.c_double),
+                ("crit_rhs", C.c_double), ("eg_ms", C.c_double), ("newton_ms", C.c_double),
+                ("cg_ms", C.c_double), ("resid_ms", C.c_double), ("step_ms", C.c_double),
+                ("n_pos", C.c_int), ("attempts", C.c_int)]
+
+
+class ReportC(C.Structure):
+    _fields_ = [("converged", C.c_int), ("iterations", C.c_int), ("residual_norm", C.c_double),
+                ("ot_estimate", C.c_double), ("total_ms", C.c_double)]
+
+
+IterCB = C.CFUNCTYPE(None, C.c_void_p, C.c_int, dptr, dptr, dptr, dptr, C.c_double, C.c_double, dptr, dptr,
+                     C.c_int)
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "kot_last_error": (C.c_char_p, []),
+    "kot_launch_count": (C.c_longlong, []),
+    "kot_problem_create": (C.c_int, [dptr, dptr, C.c_double, dptr, dptr, C.c_int, C.c_double, C.c_double,
+                                     C.c_double, C.c_int, C.POINTER(C.c_void_p)]),
+    "kot_assemble": (C.c_int, [dptr, C.c_int, dptr, C.c_int, dptr, dptr, C.c_int, C.c_int, C.c_double, C.c_double,
+                               C.c_double, C.c_int, C.POINTER(C.c_void_p)]),
+    "kot_problem_info": (C.c_int, [C.c_void_p, iptr, dptr, dptr, dptr, dptr, iptr]),
+    "kot_problem_download": (C.c_int, [C.c_void_p, dptr, dptr, dptr, dptr, dptr]),
+    "kot_problem_destroy": (None, [C.c_void_p]),
+    "kot_solve": (C.c_int, [C.c_void_p, C.POINTER(SolverCfgC), IterCB, C.c_void_p, dptr, dptr,
+                            C.POINTER(IterRecordC), C.c_int, C.POINTER(ReportC)]),
+    "kot_solve_pure_eg": (C.c_int, [C.c_void_p, C.POINTER(SolverCfgC), dptr, dptr, C.POINTER(IterRecordC),
+                                    C.c_int, C.POINTER(ReportC)]),
+    "kot_iterate": (C.c_int, [C.c_void_p, C.POINTER(SolverCfgC), dptr, dptr, dptr, dptr, C.c_double, C.c_int,
+                              dptr, dptr, dptr, dptr, dptr, C.POINTER(IterRecordC)]),
+    "kot_gram": (C.c_int, [dptr, C.c_int, C.c_int, C.c_double, C.c_int, dptr]),
+    "kot_cholesky_psd": (C.c_int, [dptr, C.c_int, C.c_int, dptr, dptr]),
+    "kot_sym_eig": (C.c_int, [dptr, C.c_int, C.c_int, dptr, dptr, iptr]),
+    "kot_proj_psd": (C.c_int, [dptr, C.c_int, C.c_int, dptr]),
+    "kot_spectral_apply": (C.c_int, [dptr, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, dptr, dptr]),
+    "kot_phi_forward": (C.c_int, [C.c_void_p, dptr, dptr]),
+    "kot_phi_adjoint": (C.c_int, [C.c_void_p, dptr, dptr]),
+    "kot_residual_parts": (C.c_int, [C.c_void_p, dptr, dptr, dptr, dptr, dptr, iptr, dptr]),
+    "kot_middle_operator": (C.c_int, [C.c_void_p, dptr, dptr, C.c_double, dptr, dptr, dptr]),
+    "kot_newton_direction": (C.c_int, [C.c_void_p, C.POINTER(SolverCfgC), dptr, dptr, C.c_double, dptr, dptr,
+                                       iptr, iptr, dptr, dptr]),
+    "kot_eg_step": (C.c_int, [C.c_void_p, dptr, dptr, C.c_double, dptr, dptr]),
+    "kot_objective": (C.c_int, [C.c_void_p, dptr, dptr]),
+    "kot_ot_estimate": (C.c_int, [C.c_void_p, dptr, dptr]),
+}
+
+_lib = None
+
+
+class LibraryMissing(ImportError):
+    pass
+
+
+def lib():
+    """Load libkotgpu.so (built in-tree); raise loudly if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise LibraryMissing(
+                f"{LIB_PATH} not found: build the CUDA library first "
+                "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+# ---------------------------------------------------------------- errors
+
+class EigenSolveError(RuntimeError):
+    """linalg.py:17-18."""
+
+
+class IndefiniteKernelError(RuntimeError):
+    """linalg.py:21-22."""
+
+
+class SolverNumericsError(RuntimeError):
+    """solver.py:28-33: carries the trace up to the failure."""
+
+    def __init__(self, message, trace):
+        super().__init__(message)
+        self.trace = trace
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def check(status: int, trace=None):
+    if status == 0:
+        return
+    msg = lib().kot_last_error().decode(errors="replace")
+    if status == 1:
+        raise ValueError(msg)
+    if status == 2:
+        raise IndefiniteKernelError(msg)
+    if status == 3:
+        raise EigenSolveError(msg)
+    if status == 4:
+        raise SolverNumericsError(msg, trace if trace is not None else [])
+    if status == 5:
+        raise FloatingPointError(msg)
+    if status == 7:
+        raise AssertionError(msg)
+    raise CudaError(msg)
+
+
+# --------------------------------------------------------------- helpers
+
+def f64(a, shape=None) -> np.ndarray:
+    out = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if shape is not None and out.shape != tuple(shape):
+        raise ValueError(f"expected shape {tuple(shape)}, got {out.shape}")
+    return out
+
+
+def ptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(dptr)
+
+
+def default_device() -> int:
+    return int(os.environ.get("KOT_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+
+
+def launch_count() -> int:
+    return int(lib().kot_launch_count())

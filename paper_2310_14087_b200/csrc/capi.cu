@@ -1,0 +1,420 @@
+// extern "C" boundary of libkotgpu (declared in include/kotgpu.h).
+// Every entry point maps kot::KotError onto a status code and stores the
+// message in a thread-local buffer (kot_last_error).
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/kotgpu.h"
+#include "ssn.cuh"
+
+namespace kot {
+std::atomic<long long> g_kot_launches{0};
+}
+
+struct kot_problem {
+  std::unique_ptr<kot::Problem> p;
+};
+
+static thread_local std::string g_last_error;
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return kot::KOT_OK;
+  } catch (const kot::KotError& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return kot::KOT_ECUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return kot::KOT_ECUDA;
+  }
+}
+
+static kot::SolverCfg to_cfg(const kot_solver_cfg* c) {
+  kot::SolverCfg s;
+  static_assert(sizeof(kot::SolverCfg) == sizeof(kot_solver_cfg), "cfg layout");
+  std::memcpy(&s, c, sizeof(s));
+  return s;
+}
+
+static void check_cfg(const kot::SolverCfg& c) {
+  using kot::kot_require;
+  kot_require(c.tau > 0.0 && c.tau < 1.0 && c.kappa > 0.0 && c.kappa < 1.0, kot::KOT_EINVAL,
+              "tau and kappa must lie in (0, 1)");
+  kot_require(c.alpha1 > 0.0 && c.alpha1 <= c.alpha2, kot::KOT_EINVAL, "need 0 < alpha1 <= alpha2");
+  kot_require(c.beta0 < 1.0 && 1.0 < c.beta2, kot::KOT_EINVAL, "need beta0 < 1 < beta2");
+  kot_require(c.theta_min > 0.0 && c.theta_min <= c.theta_max, kot::KOT_EINVAL, "need 0 < theta_min <= theta_max");
+  kot_require(c.cg_max >= 1 && c.cg_restarts >= 0, kot::KOT_EINVAL, "invalid CG budget");
+}
+
+static_assert(sizeof(kot::IterRecord) == sizeof(kot_iter_record), "record layout");
+
+extern "C" {
+
+const char* kot_last_error(void) { return g_last_error.c_str(); }
+
+long long kot_launch_count(void) { return kot::g_kot_launches.load(); }
+
+int kot_problem_create(const double* q, const double* z, double q_sq, const double* r_upper, const double* embed,
+                       int l, double lambda1, double lambda2, double jitter, int device, kot_problem** out) {
+  return guarded([&] {
+    auto h = new kot_problem();
+    try {
+      h->p = kot::problem_from_host(q, z, q_sq, r_upper, embed, l, lambda1, lambda2, jitter, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int kot_assemble(const double* xs, int n_mu, const double* ys, int n_nu, const double* xt, const double* yt, int l,
+                 int d, double bandwidth_sq, double lambda1, double lambda2, int device, kot_problem** out) {
+  return guarded([&] {
+    auto h = new kot_problem();
+    try {
+      h->p = kot::problem_assemble(xs, n_mu, ys, n_nu, xt, yt, l, d, bandwidth_sq, lambda1, lambda2, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int kot_problem_info(const kot_problem* h, int* l, double* q_sq, double* jitter, double* lambda1, double* lambda2,
+                     int* has_embed) {
+  return guarded([&] {
+    const kot::Problem& p = *h->p;
+    if (l) *l = p.n;
+    if (q_sq) *q_sq = p.q_sq;
+    if (jitter) *jitter = p.jitter;
+    if (lambda1) *lambda1 = p.l1;
+    if (lambda2) *lambda2 = p.l2;
+    if (has_embed) *has_embed = p.has_embed ? 1 : 0;
+  });
+}
+
+int kot_problem_download(kot_problem* h, double* q, double* z, double* r_upper, double* embed, double* kmat) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    const long nn = (long)p.n * p.n;
+    if (q) KOT_CUDA(cudaMemcpyAsync(q, p.Q, nn * 8, cudaMemcpyDeviceToHost, p.st));
+    if (z) KOT_CUDA(cudaMemcpyAsync(z, p.z, p.n * 8, cudaMemcpyDeviceToHost, p.st));
+    if (r_upper) KOT_CUDA(cudaMemcpyAsync(r_upper, p.R, nn * 8, cudaMemcpyDeviceToHost, p.st));
+    if (embed && p.has_embed) KOT_CUDA(cudaMemcpyAsync(embed, p.embed, p.n * 8, cudaMemcpyDeviceToHost, p.st));
+    if (kmat) {
+      kot::kot_require(p.Kmat != nullptr, kot::KOT_EINVAL, "pair Gram only available for assembled problems");
+      KOT_CUDA(cudaMemcpyAsync(kmat, p.Kmat, nn * 8, cudaMemcpyDeviceToHost, p.st));
+    }
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+  });
+}
+
+void kot_problem_destroy(kot_problem* h) { delete h; }
+
+int kot_solve(kot_problem* h, const kot_solver_cfg* cfg, kot_iter_cb cb, void* user, double* gamma_out,
+              double* x_out, kot_iter_record* trace, int trace_cap, kot_report* out) {
+  int status = guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    const kot::SolverCfg c = to_cfg(cfg);
+    check_cfg(c);
+    const kot::SolveResult r = kot::solve(p, c, (kot::IterCallback)cb, user, gamma_out, x_out,
+                                          reinterpret_cast<kot::IterRecord*>(trace), trace_cap, false);
+    out->converged = r.converged;
+    out->iterations = r.iterations;
+    out->residual_norm = r.residual_norm;
+    out->ot_estimate = r.ot_estimate;
+    out->total_ms = r.total_ms;
+    if (r.status != kot::KOT_OK) throw kot::KotError(r.status, "non-finite residual in solver iterate");
+  });
+  return status;
+}
+
+int kot_solve_pure_eg(kot_problem* h, const kot_solver_cfg* cfg, double* gamma_out, double* x_out,
+                      kot_iter_record* trace, int trace_cap, kot_report* out) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    const kot::SolverCfg c = to_cfg(cfg);
+    const kot::SolveResult r = kot::solve(p, c, nullptr, nullptr, gamma_out, x_out,
+                                          reinterpret_cast<kot::IterRecord*>(trace), trace_cap, true);
+    out->converged = r.converged;
+    out->iterations = r.iterations;
+    out->residual_norm = r.residual_norm;
+    out->ot_estimate = r.ot_estimate;
+    out->total_ms = r.total_ms;
+    if (r.status != kot::KOT_OK) throw kot::KotError(r.status, "non-finite residual in solver iterate");
+  });
+}
+
+int kot_iterate(kot_problem* h, const kot_solver_cfg* cfg, const double* w_gamma, const double* w_x,
+                const double* v_gamma, const double* v_x, double theta, int k, double* w_gamma_out, double* w_x_out,
+                double* v_gamma_out, double* v_x_out, double* theta_out, kot_iter_record* rec) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    const kot::SolverCfg c = to_cfg(cfg);
+    check_cfg(c);
+    kot::ReplayIn in{w_gamma, w_x, v_gamma, v_x, theta, k};
+    kot::ReplayOut o{w_gamma_out, w_x_out, v_gamma_out, v_x_out, 0.0};
+    const kot::IterRecord r = kot::iterate_once(p, c, in, o);
+    *theta_out = o.theta;
+    if (rec) std::memcpy(rec, &r, sizeof(r));
+  });
+}
+
+// ------------------------------------------------------------ operators
+
+namespace {
+struct DevBuf {
+  double* p = nullptr;
+  explicit DevBuf(long count) { KOT_CUDA(cudaMalloc(&p, std::max(count, 1L) * sizeof(double))); }
+  ~DevBuf() { cudaFree(p); }
+};
+}  // namespace
+
+static void up(kot::Problem& p, double* d, const double* h, long count) {
+  KOT_CUDA(cudaMemcpyAsync(d, h, count * 8, cudaMemcpyHostToDevice, p.st));
+}
+static void down(kot::Problem& p, double* h, const double* d, long count) {
+  KOT_CUDA(cudaMemcpyAsync(h, d, count * 8, cudaMemcpyDeviceToHost, p.st));
+}
+
+// A scratch problem for the matrix-only entry points (no instance data needed).
+static std::unique_ptr<kot::Problem> scratch_problem(int n, int device) {
+  std::vector<double> zeros(1, 0.0);
+  std::vector<double> q((long)n * n, 0.0), r((long)n * n, 0.0), z(n, 0.0);
+  for (int i = 0; i < n; ++i) q[(long)i * n + i] = r[(long)i * n + i] = 1.0;
+  return kot::problem_from_host(q.data(), z.data(), 0.0, r.data(), nullptr, n, 1.0, 1.0, 0.0, device);
+}
+
+int kot_gram(const double* pts, int n, int d, double bandwidth_sq, int device, double* out) {
+  return guarded([&] {
+    kot::kot_require(bandwidth_sq > 0.0, kot::KOT_EINVAL, "bandwidth_sq must be positive");
+    KOT_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    KOT_CUDA(cudaStreamCreate(&st));
+    DevBuf dp((long)n * d), dout((long)n * n);
+    KOT_CUDA(cudaMemcpyAsync(dp.p, pts, (long)n * d * 8, cudaMemcpyHostToDevice, st));
+    kot::gram_square(dp.p, dp.p, n, d, bandwidth_sq, bandwidth_sq, 1, false, dout.p, st);
+    KOT_CUDA(cudaMemcpyAsync(out, dout.p, (long)n * n * 8, cudaMemcpyDeviceToHost, st));
+    KOT_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+  });
+}
+
+int kot_cholesky_psd(const double* k, int n, int device, double* r_upper, double* jitter) {
+  return guarded([&] {
+    kot::kot_require(n >= 1, kot::KOT_EINVAL, "order must be >= 1");
+    KOT_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    KOT_CUDA(cudaStreamCreate(&st));
+    DevBuf dk((long)n * n), dr((long)n * n), work((long)n * n + 8);
+    int* flag;
+    KOT_CUDA(cudaMalloc(&flag, sizeof(int)));
+    KOT_CUDA(cudaMemcpyAsync(dk.p, k, (long)n * n * 8, cudaMemcpyHostToDevice, st));
+    try {
+      *jitter = kot::cholesky_psd_device(dk.p, n, dr.p, work.p, work.p + (long)n * n, flag, st);
+    } catch (...) {
+      cudaFree(flag);
+      cudaStreamDestroy(st);
+      throw;
+    }
+    KOT_CUDA(cudaMemcpyAsync(r_upper, dr.p, (long)n * n * 8, cudaMemcpyDeviceToHost, st));
+    KOT_CUDA(cudaStreamSynchronize(st));
+    cudaFree(flag);
+    cudaStreamDestroy(st);
+  });
+}
+
+int kot_sym_eig(const double* z, int n, int device, double* vecs, double* vals, int* n_pos) {
+  return guarded([&] {
+    auto p = scratch_problem(n, device);
+    const long nn = (long)n * n;
+    up(*p, p->M1, z, nn);
+    kot::symmetrize(*p, p->M1, p->M2);  // sym(z), linalg.py:66
+    kot::Decomp dc{p->M3, p->M4, 0};
+    kot::eigh(*p, p->M2, dc);
+    down(*p, vecs, dc.P, nn);
+    down(*p, vals, dc.vals, n);
+    KOT_CUDA(cudaStreamSynchronize(p->st));
+    *n_pos = dc.k;
+  });
+}
+
+int kot_proj_psd(const double* z, int n, int device, double* out) {
+  return guarded([&] {
+    auto p = scratch_problem(n, device);
+    const long nn = (long)n * n;
+    up(*p, p->M1, z, nn);
+    kot::symmetrize(*p, p->M1, p->M2);
+    kot::Decomp dc{p->M3, p->M4, 0};
+    kot::eigh(*p, p->M2, dc);
+    kot::proj(*p, dc, nullptr, p->M5);
+    down(*p, out, p->M5, nn);
+    KOT_CUDA(cudaStreamSynchronize(p->st));
+  });
+}
+
+int kot_spectral_apply(const double* z, int n, int device, int mode, double mu, int path, const double* s,
+                       double* out) {
+  return guarded([&] {
+    if (mode == 0) kot::kot_require(mu > 0.0, kot::KOT_EINVAL, "regularization mu must be positive");
+    auto p = scratch_problem(n, device);
+    kot::Bufs& b = p->bufs();
+    const long nn = (long)n * n;
+    up(*p, p->M1, z, nn);
+    kot::symmetrize(*p, p->M1, p->M2);
+    kot::Decomp dc{b.Pw, b.valw, 0};
+    kot::eigh(*p, p->M2, dc);
+    up(*p, b.Xw, s, nn);
+    kot::spectral_filter(*p, dc, b.Xw, b.Xv, mu, mode, path);
+    down(*p, out, b.Xv, nn);
+    KOT_CUDA(cudaStreamSynchronize(p->st));
+  });
+}
+
+int kot_phi_forward(kot_problem* h, const double* x, double* out) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    kot::Bufs& b = p.bufs();
+    const long nn = (long)p.n * p.n;
+    up(p, b.Xh, x, nn);
+    kot::phi_forward(p, b.Xh, b.e1);
+    down(p, out, b.e1, p.n);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+  });
+}
+
+int kot_phi_adjoint(kot_problem* h, const double* gamma, double* out) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    kot::Bufs& b = p.bufs();
+    const long nn = (long)p.n * p.n;
+    up(p, b.e1, gamma, p.n);
+    kot::phi_adjoint(p, b.e1, b.Xh);
+    down(p, out, b.Xh, nn);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+  });
+}
+
+int kot_residual_parts(kot_problem* h, const double* gamma, const double* x, double* r1, double* r2, double* eigvals,
+                       int* n_pos, double* res_norm) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    kot::Bufs& b = p.bufs();
+    const long nn = (long)p.n * p.n;
+    up(p, b.gw, gamma, p.n);
+    up(p, b.Xw, x, nn);
+    kot::Decomp dc{b.Pw, b.valw, 0};
+    const double res = kot::residual_parts(p, b.gw, b.Xw, b.r1w, b.r2w, dc);
+    if (r1) down(p, r1, b.r1w, p.n);
+    if (r2) down(p, r2, b.r2w, nn);
+    if (eigvals) down(p, eigvals, dc.vals, p.n);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+    if (n_pos) *n_pos = dc.k;
+    if (res_norm) *res_norm = res;
+  });
+}
+
+int kot_middle_operator(kot_problem* h, const double* gamma, const double* x, double theta, const double* v,
+                        double* out, double* mu_out) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    kot::Bufs& b = p.bufs();
+    const long nn = (long)p.n * p.n;
+    up(p, b.gw, gamma, p.n);
+    up(p, b.Xw, x, nn);
+    kot::Decomp dc{b.Pw, b.valw, 0};
+    const double res = kot::residual_parts(p, b.gw, b.Xw, b.r1w, b.r2w, dc);
+    kot::kot_require(res > 0.0, kot::KOT_EINVAL, "context requires a nonzero residual");
+    const double mu = theta * res;
+    up(p, b.e2, v, p.n);
+    kot::middle_operator(p, dc, mu, b.e2, b.e1);
+    down(p, out, b.e1, p.n);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+    if (mu_out) *mu_out = mu;
+  });
+}
+
+int kot_newton_direction(kot_problem* h, const kot_solver_cfg* cfg, const double* gamma, const double* x,
+                         double theta, double* dgamma, double* dx, int* cg_iters, int* criterion_met,
+                         double* crit_lhs, double* crit_rhs) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    const kot::SolverCfg c = to_cfg(cfg);
+    check_cfg(c);
+    kot::Bufs& b = p.bufs();
+    const long nn = (long)p.n * p.n;
+    up(p, b.gw, gamma, p.n);
+    up(p, b.Xw, x, nn);
+    kot::Decomp dc{b.Pw, b.valw, 0};
+    const double res = kot::residual_parts(p, b.gw, b.Xw, b.r1w, b.r2w, dc);
+    kot::kot_require(res > 0.0, kot::KOT_EINVAL, "context requires a nonzero residual");
+    const kot::NewtonOut o = kot::newton_direction(p, b.r1w, b.r2w, res, dc, theta * res, c, b.dg, b.dX);
+    down(p, dgamma, b.dg, p.n);
+    down(p, dx, b.dX, nn);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+    *cg_iters = o.cg_iters;
+    *criterion_met = o.met;
+    *crit_lhs = o.lhs;
+    *crit_rhs = o.rhs;
+  });
+}
+
+int kot_eg_step(kot_problem* h, const double* gamma, const double* x, double stepsize, double* gamma_out,
+                double* x_out) {
+  return guarded([&] {
+    kot::kot_require(stepsize > 0.0, kot::KOT_EINVAL, "stepsize must be positive");
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    kot::Bufs& b = p.bufs();
+    const long nn = (long)p.n * p.n;
+    up(p, b.gv, gamma, p.n);
+    up(p, b.Xv, x, nn);
+    kot::eg_step(p, b.gv, b.Xv, stepsize, b.gt, b.Xt);
+    down(p, gamma_out, b.gt, p.n);
+    down(p, x_out, b.Xt, nn);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+  });
+}
+
+int kot_objective(kot_problem* h, const double* gamma, double* out) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    kot::Bufs& b = p.bufs();
+    up(p, b.e1, gamma, p.n);
+    kot::finalize(p, kot::FIN_QV, b.e1, false, nullptr, 0.0, b.e2);  // Qγ
+    const double quad = kot::dev_dot(p, b.e1, b.e2, p.n) / (4.0 * p.l2);
+    const double lin = kot::dev_dot(p, b.e1, p.z, p.n) / (2.0 * p.l2);
+    *out = quad - lin + p.q_sq / (4.0 * p.l2);
+  });
+}
+
+int kot_ot_estimate(kot_problem* h, const double* gamma, double* out) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    kot::kot_require(p.has_embed, kot::KOT_EINVAL, "instance carries no embedding sums; assemble() provides them");
+    kot::Bufs& b = p.bufs();
+    up(p, b.e1, gamma, p.n);
+    *out = (p.q_sq - kot::dev_dot(p, b.e1, p.embed, p.n)) / (2.0 * p.l2);
+  });
+}
+
+}  // extern "C"

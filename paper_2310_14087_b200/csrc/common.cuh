@@ -1,0 +1,82 @@
+// Shared helpers for libkotgpu (sm_100a, FP64).
+#pragma once
+#include <cuda_runtime.h>
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace kot {
+
+// Status codes of the C ABI (include/kotgpu.h); map 1:1 onto the reference's
+// exception classes.
+enum Status : int {
+  KOT_OK = 0,
+  KOT_EINVAL = 1,        // ValueError
+  KOT_EINDEFINITE = 2,   // IndefiniteKernelError (linalg.py:114)
+  KOT_EEIG = 3,          // EigenSolveError (linalg.py:70)
+  KOT_ENUMERICS = 4,     // SolverNumericsError (solver.py:28-33)
+  KOT_ECG = 5,           // FloatingPointError in CG (linalg.py:146,156)
+  KOT_ECUDA = 6,
+  KOT_EASSERT = 7,       // AssertionError (psdcone.py:77)
+};
+
+struct KotError : public std::runtime_error {
+  int code;
+  KotError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define KOT_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      (void)cudaGetLastError(); /* clear non-sticky errors so later calls are clean */   \
+      throw ::kot::KotError(::kot::KOT_ECUDA, std::string(#call) + ": " +              \
+                                                  cudaGetErrorString(e_));               \
+    }                                                                                    \
+  } while (0)
+
+// Every kernel launch of the library goes through KOT_LAUNCH_CHECK (counted:
+// kot_launch_count() backs bench.py's "gpu_launches").
+extern std::atomic<long long> g_kot_launches;
+#define KOT_LAUNCH_CHECK()                     \
+  do {                                         \
+    ::kot::g_kot_launches.fetch_add(1);        \
+    KOT_CUDA(cudaGetLastError());              \
+  } while (0)
+
+inline void kot_require(bool ok, int code, const std::string& msg) {
+  if (!ok) throw KotError(code, msg);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Deterministic block sum (fixed tree); every thread gets the result.
+// `sh` must hold >= 32 doubles.  blockDim.x must be a multiple of 32.
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = (lane < nw) ? sh[lane] : 0.0;
+  t = warp_sum(t);
+  return t;
+}
+
+inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
+
+constexpr int kNumSMs = 148;
+
+}  // namespace kot

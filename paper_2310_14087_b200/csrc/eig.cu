@@ -1,0 +1,963 @@
+// Hand-written FP64 symmetric eigensolver for the PSD-cone projection
+// (north-star item 4; replaces np.linalg.eigh / LAPACK dsyevd called from
+// reference linalg.py:60-83, four times per SSN iteration).
+//
+//   1. sytrd  — blocked Householder tridiagonalisation (LAPACK dlatrd
+//      structure, lower).  Each NB=32 panel runs as ONE cooperative
+//      persistent kernel (2 grid barriers per column: column update |
+//      Householder + symv), followed by the DMMA core for the trailing
+//      symmetric rank-2NB update (one triangle + mirror).
+//   2. stedc  — tridiagonal divide & conquer: leaves (≤32) by implicit QL
+//      in one warp each; merges by deflation (dlaed2 rules), a warp-per-root
+//      secular-equation solver (middle-way rational steps inside a bisection
+//      bracket, roots stored as pole-origin + offset so d_i − λ_j is exact),
+//      Gu–Eisenstat recomputation of z for orthogonal eigenvectors, and the
+//      eigenvector update as a DMMA GEMM with a column-scatter epilogue.
+//   3. ormtr  — back-transform P = Q_H·Q_T with compact-WY blocks
+//      (I − V T Vᵀ), three DMMA GEMMs per panel.
+//   4. descending order + k = #(σ > 0)  (strict, zero → ᾱ, linalg.py:74-83).
+// Consumers (proj, 𝒯, M) are basis-invariant, so eigenvector signs and the
+// basis inside clusters may differ from LAPACK.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <vector>
+
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace kot {
+
+constexpr int TRD_NB = 32;
+constexpr int TRD_THREADS = 256;
+constexpr int TRD_WARPS = TRD_THREADS / 32;
+constexpr int TRD_PSTRIDE = 2 * TRD_NB + 2;
+constexpr int DC_LEAF = 32;
+constexpr double DEPS = DBL_EPSILON * 0.5;  // LAPACK dlamch('E')
+
+// ============================================================== workspace
+
+EigWork::EigWork(int n_) : n(n_) {
+  const long nn = (long)n * n;
+  auto alloc = [&](double** p, long cnt) { KOT_CUDA(cudaMalloc(p, std::max(cnt, 1L) * sizeof(double))); };
+  alloc(&A, nn);
+  alloc(&Vall, nn);
+  alloc(&X, (long)n * 3 * TRD_NB);
+  alloc(&d, n);
+  alloc(&e, n);
+  alloc(&tau, n);
+  alloc(&xv, n);
+  alloc(&yv, n);
+  alloc(&part, (long)kNumSMs * TRD_PSTRIDE);
+  alloc(&partn, kNumSMs);
+  alloc(&Tf, TRD_NB * TRD_NB * 2);
+  alloc(&W1, (long)TRD_NB * n * 2);
+  alloc(&Q, nn);
+  alloc(&Qw, nn);
+  alloc(&Qnd, nn);
+  alloc(&Dl, nn);
+  alloc(&zs, n);
+  alloc(&ds, n);
+  alloc(&dlam, n);
+  alloc(&wv, n);
+  alloc(&what, n);
+  alloc(&lam, n);
+  alloc(&dfv, n);
+  alloc(&rotcs, 2L * n);
+  alloc(&rho, n);
+  KOT_CUDA(cudaMalloc(&ibuf, sizeof(int) * (8L * n + 64)));
+  KOT_CUDA(cudaMalloc(&dbuf, 16L * n + 4096 + 64L * n));
+  KOT_CUDA(cudaMallocHost(&hbuf, sizeof(int) * (12L * n + 512)));
+}
+
+EigWork::~EigWork() {
+  for (double* p : {A, Vall, X, d, e, tau, xv, yv, part, partn, Tf, W1, Q, Qw, Qnd, Dl, zs, ds, dlam, wv, what, lam,
+                    dfv, rotcs, rho})
+    cudaFree(p);
+  cudaFree(ibuf);
+  cudaFree(dbuf);
+  cudaFreeHost(hbuf);
+}
+
+// ================================================================= sytrd
+
+struct TrdArgs {
+  double* A;
+  int n, p0, nb;
+  double* X;  // n × 3NB : [V | W | V]
+  double* Vall;
+  double* d;
+  double* e;
+  double* tau;
+  double* xv;
+  double* yv;
+  double* part;   // [G][TRD_PSTRIDE]: t1[NB], t2[NB], yvv
+  double* partn;  // [G]: Σ x_r², r >= c+2
+};
+
+__global__ void __launch_bounds__(TRD_THREADS) sytrd_panel_kernel(TrdArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double vsh[];  // Householder vector staged per CTA (length n)
+  __shared__ double sred[TRD_WARPS][TRD_PSTRIDE];
+  __shared__ double tred[TRD_PSTRIDE];
+  __shared__ double wrow[TRD_NB], vrow[TRD_NB];
+  __shared__ double nrm_sh[TRD_WARPS];
+
+  const int n = a.n, p0 = a.p0, nb = a.nb;
+  const int G = gridDim.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gw = blockIdx.x * TRD_WARPS + wid;
+  const int NW = G * TRD_WARPS;
+  constexpr int LDX = 3 * TRD_NB;
+  double* V = a.X;
+  double* Wm = a.X + TRD_NB;
+  double* V2 = a.X + 2 * TRD_NB;
+
+  double tau_prev = 0.0;
+
+  for (int jj = 0; jj <= nb; ++jj) {
+    const int c = p0 + jj;
+    // ------------------------------------------------------------ phase Q
+    if (jj > 0) {
+      const int m = jj - 1;  // t-range of the previous column's corrections
+      for (int q = threadIdx.x; q < TRD_PSTRIDE; q += blockDim.x) {
+        double s = 0.0;
+        if (q < m || (q >= TRD_NB && q < TRD_NB + m) || q == 2 * TRD_NB)
+          for (int g = 0; g < G; ++g) s += a.part[(long)g * TRD_PSTRIDE + q];
+        tred[q] = s;
+      }
+      __syncthreads();
+      // α = −½ τ (wᵀv),  wᵀv = τ (yᵀv − 2 t1·t2)
+      double t12 = 0.0;
+      for (int t = 0; t < m; ++t) t12 += tred[t] * tred[TRD_NB + t];
+      const double alpha_prev = -0.5 * tau_prev * (tau_prev * (tred[2 * TRD_NB] - 2.0 * t12));
+      // finish W[:, jj-1] for rows r >= c: w_r = τ (y_r − V_r·t1 − W_r·t2) + α v_r
+      auto finish_row = [&](int r) -> double {
+        double s = 0.0;
+        if (lane < m) s = V[(long)r * LDX + lane] * tred[lane] + Wm[(long)r * LDX + lane] * tred[TRD_NB + lane];
+        s = warp_sum(s);
+        return tau_prev * (a.yv[r] - s) + alpha_prev * V[(long)r * LDX + jj - 1];
+      };
+      for (int r = c + ((gw - c) % NW + NW) % NW; r < n; r += NW) {
+        const double w = finish_row(r);
+        if (lane == 0) Wm[(long)r * LDX + jj - 1] = w;
+      }
+      if (jj < nb && wid == 0) {
+        const double wc = finish_row(c);  // identical arithmetic to the owner's
+        if (lane == 0) wrow[jj - 1] = wc;
+      }
+    }
+    if (jj == nb) break;
+    // rows c of V and W (t < jj) for the column update
+    if (threadIdx.x < jj) {
+      if (threadIdx.x < jj - 1 || jj == 0) wrow[threadIdx.x] = Wm[(long)c * LDX + threadIdx.x];
+      vrow[threadIdx.x] = V[(long)c * LDX + threadIdx.x];
+    }
+    __syncthreads();
+    double nrm = 0.0;
+    for (int r = c + ((gw - c) % NW + NW) % NW; r < n; r += NW) {
+      double s = 0.0;
+      if (lane < jj) s = V[(long)r * LDX + lane] * wrow[lane] + Wm[(long)r * LDX + lane] * vrow[lane];
+      s = warp_sum(s);
+      const double x = a.A[(long)r * n + c] - s;
+      if (lane == 0) {
+        a.xv[r] = x;
+        if (r == c) a.d[c] = x;
+        if (r >= c + 2) nrm += x * x;
+      }
+    }
+    if (lane == 0) nrm_sh[wid] = nrm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < TRD_WARPS; ++w) s += nrm_sh[w];
+      a.partn[blockIdx.x] = s;
+    }
+    grid.sync();
+    // ------------------------------------------------------------ phase S
+    double xn2 = 0.0;
+    for (int g = 0; g < G; ++g) xn2 += a.partn[g];
+    const double alpha = a.xv[c + 1];
+    double beta, tau, scale;
+    if (xn2 == 0.0) {  // dlarfg: H = I
+      tau = 0.0;
+      beta = alpha;
+      scale = 1.0;
+    } else {
+      beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    tau_prev = tau;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.e[c] = beta;
+      a.tau[c] = tau;
+    }
+    const int m = n - c - 1;
+    for (int s = threadIdx.x; s < m; s += blockDim.x) vsh[s] = (s == 0) ? 1.0 : a.xv[c + 1 + s] * scale;
+    __syncthreads();
+    double pt1 = 0.0, pt2 = 0.0, pyv = 0.0;  // lane t accumulates t1_t, t2_t
+    for (int r = (c + 1) + ((gw - c - 1) % NW + NW) % NW; r < n; r += NW) {
+      const double vr = vsh[r - c - 1];
+      const double* Ar = a.A + (long)r * n + c + 1;
+      double y = 0.0;
+      for (int s = lane; s < m; s += 32) y += Ar[s] * vsh[s];
+      y = warp_sum(y);
+      if (lane == 0) {
+        a.yv[r] = y;
+        V[(long)r * LDX + jj] = vr;
+        V2[(long)r * LDX + jj] = vr;
+        a.Vall[(long)r * n + c] = vr;
+        pyv += y * vr;
+      }
+      if (lane < jj) {
+        pt1 += Wm[(long)r * LDX + lane] * vr;
+        pt2 += V[(long)r * LDX + lane] * vr;
+      }
+    }
+    sred[wid][lane] = pt1;
+    sred[wid][TRD_NB + lane] = pt2;
+    if (lane == 0) sred[wid][2 * TRD_NB] = pyv;
+    __syncthreads();
+    for (int q = threadIdx.x; q <= 2 * TRD_NB; q += blockDim.x) {
+      double s = 0.0;
+      for (int w = 0; w < TRD_WARPS; ++w) s += sred[w][q];
+      a.part[(long)blockIdx.x * TRD_PSTRIDE + q] = s;
+    }
+    grid.sync();
+  }
+}
+
+__global__ void set_last_diag_kernel(const double* A, int n, double* d) { d[n - 1] = A[(long)(n - 1) * n + n - 1]; }
+
+static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st) {
+  KOT_CUDA(cudaMemcpyAsync(w.A, Z, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
+  KOT_CUDA(cudaMemsetAsync(w.Vall, 0, sizeof(double) * n * n, st));
+  static int smem_set_for = 0;
+  for (int p0 = 0; p0 < n - 1; p0 += TRD_NB) {
+    const int nb = std::min(TRD_NB, n - 1 - p0);
+    KOT_CUDA(cudaMemsetAsync(w.X, 0, sizeof(double) * n * 3 * TRD_NB, st));
+    const int rows = n - p0;
+    const int G = std::max(1, std::min(kNumSMs, ceil_div(rows, 16)));
+    TrdArgs args{w.A, n, p0, nb, w.X, w.Vall, w.d, w.e, w.tau, w.xv, w.yv, w.part, w.partn};
+    void* kargs[] = {&args};
+    const size_t smem = sizeof(double) * std::max(rows, 1);
+    if (smem > 48 * 1024 && smem_set_for < (int)smem) {
+      KOT_CUDA(cudaFuncSetAttribute(sytrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      smem_set_for = (int)smem;
+    }
+    KOT_CUDA(cudaLaunchCooperativeKernel((void*)sytrd_panel_kernel, G, TRD_THREADS, kargs, smem, st));
+    KOT_LAUNCH_CHECK();
+    // trailing update A22 -= V Wᵀ + W Vᵀ on rows/cols >= p0+nb
+    const int t0 = p0 + nb;
+    const int m2 = n - t0;
+    if (m2 > 0) {
+      constexpr int LDX = 3 * TRD_NB;
+      GemmShape s = make_shape(m2, m2, 2 * TRD_NB, w.X + (long)t0 * LDX, LDX, w.X + (long)t0 * LDX + TRD_NB, LDX);
+      s.sym_tiles = 1;
+      double* C = w.A + (long)t0 * n + t0;
+      EpiSymMirror epi{C, n, -1.0, C, 1.0, 0.0};
+      gemm_launch<false, true>(s, epi, st);
+    }
+  }
+  set_last_diag_kernel<<<1, 1, 0, st>>>(w.A, n, w.d);
+  KOT_LAUNCH_CHECK();
+}
+
+// ======================================================== tridiagonal D&C
+
+// Subtract the rank-one couplings at every split point (dlaed0): d[s], d[s+1] -= |e[s]|.
+__global__ void dc_split_kernel(double* d, const double* e, const int* splits, int ns) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int i = 0; i < ns; ++i) {
+    const int s = splits[i];
+    const double r = fabs(e[s]);
+    d[s] -= r;
+    d[s + 1] -= r;
+  }
+}
+
+// Leaves: implicit QL (tqli) on a ≤32 tridiagonal, one warp per leaf.  Every
+// lane runs the scalar recurrence redundantly; lane k owns row k of Z.
+__global__ void dc_leaf_kernel(double* d, const double* e, const int* leaf_off, const int* leaf_len, int nleaves,
+                               double* Q, int ldq, int* err) {
+  const int leaf = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (leaf >= nleaves) return;
+  const int lane = threadIdx.x & 31;
+  const int o = leaf_off[leaf], m = leaf_len[leaf];
+  double dd[DC_LEAF], ee[DC_LEAF], z[DC_LEAF];
+  for (int i = 0; i < m; ++i) {
+    dd[i] = d[o + i];
+    ee[i] = (i < m - 1) ? e[o + i] : 0.0;
+    z[i] = (i == lane) ? 1.0 : 0.0;
+  }
+  for (int l = 0; l < m; ++l) {
+    int iter = 0, mm;
+    do {
+      for (mm = l; mm < m - 1; ++mm) {
+        const double sd = fabs(dd[mm]) + fabs(dd[mm + 1]);
+        if (fabs(ee[mm]) + sd == sd) break;
+      }
+      if (mm != l) {
+        if (iter++ == 60) {
+          if (lane == 0) atomicExch(err, 1);
+          break;
+        }
+        double g = (dd[l + 1] - dd[l]) / (2.0 * ee[l]);
+        double r = hypot(g, 1.0);
+        g = dd[mm] - dd[l] + ee[l] / (g + copysign(r, g));
+        double s = 1.0, c = 1.0, p = 0.0;
+        int i;
+        for (i = mm - 1; i >= l; --i) {
+          double f = s * ee[i];
+          const double b = c * ee[i];
+          r = hypot(f, g);
+          ee[i + 1] = r;
+          if (r == 0.0) {
+            dd[i + 1] -= p;
+            ee[mm] = 0.0;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = dd[i + 1] - p;
+          r = (dd[i] - g) * s + 2.0 * c * b;
+          p = s * r;
+          dd[i + 1] = g + p;
+          g = c * r - b;
+          f = z[i + 1];
+          z[i + 1] = s * z[i] + c * f;
+          z[i] = c * z[i] - s * f;
+        }
+        if (r == 0.0 && i >= l) continue;
+        dd[l] -= p;
+        ee[l] = g;
+        ee[mm] = 0.0;
+      }
+    } while (mm != l);
+  }
+  // ascending selection sort (lane-redundant on dd, each lane permutes its row)
+  for (int i = 0; i < m - 1; ++i) {
+    int kmin = i;
+    for (int j = i + 1; j < m; ++j)
+      if (dd[j] < dd[kmin]) kmin = j;
+    if (kmin != i) {
+      const double t = dd[i];
+      dd[i] = dd[kmin];
+      dd[kmin] = t;
+      const double tz = z[i];
+      z[i] = z[kmin];
+      z[kmin] = tz;
+    }
+  }
+  if (lane < m)
+    for (int i = 0; i < m; ++i) Q[(long)(o + lane) * ldq + o + i] = z[i];
+  if (lane == 0)
+    for (int i = 0; i < m; ++i) d[o + i] = dd[i];
+}
+
+struct MergeDesc {
+  int o, n1, n2;
+  long off;  // offset of this merge's K×K / n×K scratch (prefix of n_m²)
+};
+
+// Per-merge bookkeeping (one CTA per merge; sequential parts on thread 0):
+// z extraction, sort, dlaed2 deflation.  Integer outputs in ibuf regions:
+//   perm[o..o+n)   : sorted position → local column of the block
+//   ndcol[o..)     : sorted positions of the K non-deflated columns
+//   dcol[o..)      : sorted positions of the deflated columns (sorted by value)
+//   rot[o..)       : (pj, nj) index pairs of the deflation rotations
+//   meta[4*mi..]   : K, ndefl, nrot
+__global__ void dc_merge_prep_kernel(const MergeDesc* md, const double* Q, int ldq, const double* d, const double* e,
+                                     double* zs, double* ds, double* dlam, double* wv, double* dfv, double* rotcs,
+                                     double* rho_out, int* perm, int* ndcol, int* dcol, int* rot, int* meta) {
+  const MergeDesc m = md[blockIdx.x];
+  const int o = m.o, n1 = m.n1, n = m.n1 + m.n2;
+  const int sidx = o + n1 - 1;
+  const double esplit = e[sidx];
+  const double sgn = (esplit < 0.0) ? -1.0 : 1.0;
+  const double rs2 = 1.0 / sqrt(2.0);  // dlaed2: z ← z/√2, ρ ← |2ρ|
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double zz = (i < n1) ? Q[(long)(o + n1 - 1) * ldq + o + i] : sgn * Q[(long)(o + n1) * ldq + o + i];
+    zs[o + i] = zz * rs2;  // unsorted for now
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const double rho = fabs(2.0 * esplit);
+  rho_out[blockIdx.x] = rho;
+  // merge the two ascending halves
+  int* P = perm + o;
+  {
+    int i = 0, j = n1, k = 0;
+    while (i < n1 && j < n) P[k++] = (d[o + j] < d[o + i]) ? j++ : i++;
+    while (i < n1) P[k++] = i++;
+    while (j < n) P[k++] = j++;
+  }
+  double* D = ds + o;
+  double* Z = dlam + o;  // temp: sorted z (dlam reused after)
+  double zmax = 0.0, dmax = 0.0;
+  for (int k = 0; k < n; ++k) {
+    D[k] = d[o + P[k]];
+    Z[k] = zs[o + P[k]];
+    zmax = fmax(zmax, fabs(Z[k]));
+    dmax = fmax(dmax, fabs(D[k]));
+  }
+  const double tol = 8.0 * DEPS * fmax(dmax, zmax);
+  int K = 0, nd = 0, nr = 0;
+  int* NDC = ndcol + o;
+  int* DC = dcol + o;
+  int* RT = rot + 2 * o;
+  double* DFV = dfv + o;
+  double* RCS = rotcs + 2 * o;
+  double* WV = wv + o;
+  // dlamda written after the scan (Z aliases dlam)
+  double* tmpd = zs + o;  // reuse zs for nondeflated d values
+  if (rho * zmax <= tol) {
+    for (int k = 0; k < n; ++k) {
+      DC[nd] = k;
+      DFV[nd] = D[k];
+      ++nd;
+    }
+  } else {
+    int pj = -1;
+    for (int j = 0; j < n; ++j) {
+      if (rho * fabs(Z[j]) <= tol) {
+        DC[nd] = j;
+        DFV[nd] = D[j];
+        ++nd;
+        continue;
+      }
+      if (pj < 0) {
+        pj = j;
+        continue;
+      }
+      double s = Z[pj], c = Z[j];
+      const double tau = hypot(c, s);
+      double t = D[j] - D[pj];
+      c /= tau;
+      s = -s / tau;
+      if (fabs(t * c * s) <= tol) {
+        Z[j] = tau;
+        Z[pj] = 0.0;
+        RT[2 * nr] = pj;
+        RT[2 * nr + 1] = j;
+        RCS[2 * nr] = c;
+        RCS[2 * nr + 1] = s;
+        ++nr;
+        t = D[pj] * c * c + D[j] * s * s;
+        D[j] = D[pj] * s * s + D[j] * c * c;
+        D[pj] = t;
+        DC[nd] = pj;
+        DFV[nd] = D[pj];
+        ++nd;
+        pj = j;
+      } else {
+        NDC[K] = pj;
+        tmpd[K] = D[pj];
+        WV[K] = Z[pj];
+        ++K;
+        pj = j;
+      }
+    }
+    if (pj >= 0) {
+      NDC[K] = pj;
+      tmpd[K] = D[pj];
+      WV[K] = Z[pj];
+      ++K;
+    }
+  }
+  for (int k = 0; k < K; ++k) dlam[o + k] = tmpd[k];
+  // insertion-sort the deflated list by value (nearly sorted already)
+  for (int i = 1; i < nd; ++i) {
+    const double v = DFV[i];
+    const int cidx = DC[i];
+    int j = i - 1;
+    while (j >= 0 && DFV[j] > v) {
+      DFV[j + 1] = DFV[j];
+      DC[j + 1] = DC[j];
+      --j;
+    }
+    DFV[j + 1] = v;
+    DC[j + 1] = cidx;
+  }
+  meta[4 * blockIdx.x + 0] = K;
+  meta[4 * blockIdx.x + 1] = nd;
+  meta[4 * blockIdx.x + 2] = nr;
+}
+
+// Gather the block columns into sorted order, apply the deflation rotations
+// (thread per row, rotations in order), then split into the contiguous
+// non-deflated matrix Qnd (n × K) and the deflated columns (kept in Qw).
+__global__ void dc_merge_vec_kernel(const MergeDesc* md, const double* Q, double* Qw, double* Qnd, int ldq,
+                                    const int* perm, const int* ndcol, const int* rot, const double* rotcs,
+                                    const int* meta) {
+  const MergeDesc m = md[blockIdx.y];
+  const int o = m.o, n = m.n1 + m.n2;
+  const int K = meta[4 * blockIdx.y], nr = meta[4 * blockIdx.y + 2];
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const double* qrow = Q + (long)(o + r) * ldq + o;
+  double* wrow = Qw + (long)(o + r) * ldq + o;
+  const int* P = perm + o;
+  for (int j = 0; j < n; ++j) wrow[j] = qrow[P[j]];
+  const int* RT = rot + 2 * o;
+  const double* RCS = rotcs + 2 * o;
+  for (int q = 0; q < nr; ++q) {
+    const int pj = RT[2 * q], nj = RT[2 * q + 1];
+    const double c = RCS[2 * q], s = RCS[2 * q + 1];
+    const double x = wrow[pj], y = wrow[nj];
+    wrow[pj] = c * x + s * y;
+    wrow[nj] = c * y - s * x;
+  }
+  double* nd = Qnd + m.off + (long)r * K;
+  for (int k = 0; k < K; ++k) nd[k] = wrow[ndcol[o + k]];
+}
+
+struct RootRef {
+  int merge, j;
+};
+
+// Secular equation 1 + ρ Σ w_i²/(d_i − λ) = 0, one warp per root.
+// Stores λ_j and column j of Δ (Δ_ij = d_i − λ_j, computed from the origin pole).
+__global__ void dc_secular_kernel(const MergeDesc* md, const RootRef* roots, int nroots, const int* meta,
+                                  const double* dlam, const double* wv, const double* rho_arr, double* lam,
+                                  double* Dl, int* err) {
+  const int rid = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (rid >= nroots) return;
+  const int lane = threadIdx.x & 31;
+  const RootRef rr = roots[rid];
+  const MergeDesc m = md[rr.merge];
+  const int K = meta[4 * rr.merge];
+  const int j = rr.j;
+  const double* dl = dlam + m.o;
+  const double* w = wv + m.o;
+  const double rho = rho_arr[rr.merge];
+  double* delta = Dl + m.off + (long)j * K;
+  if (K == 1) {
+    if (lane == 0) {
+      const double t = rho * w[0] * w[0];
+      lam[m.o] = dl[0] + t;
+      delta[0] = -t;
+    }
+    return;
+  }
+  int o;
+  double lo, hi;
+  if (j < K - 1) {
+    const double gap = dl[j + 1] - dl[j];
+    const double mid = 0.5 * gap;
+    double f = 0.0;
+    for (int i = lane; i < K; i += 32) f += w[i] * w[i] / ((dl[i] - dl[j]) - mid);
+    f = 1.0 + rho * warp_sum(f);
+    if (f >= 0.0) {
+      o = j;
+      lo = 0.0;
+      hi = mid;
+    } else {
+      o = j + 1;
+      lo = -(gap - mid);
+      hi = 0.0;
+    }
+  } else {
+    double s = 0.0;
+    for (int i = lane; i < K; i += 32) s += w[i] * w[i];
+    o = K - 1;
+    lo = 0.0;
+    hi = rho * warp_sum(s);
+  }
+  const double dor = dl[o];
+  double tau = 0.5 * (lo + hi);
+  bool ok = false;
+  for (int it = 0; it < 200; ++it) {
+    double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
+    for (int i = lane; i < K; i += 32) {
+      const double del = (dl[i] - dor) - tau;
+      const double t = w[i] / del;
+      if (i <= j) {
+        psi += w[i] * t;
+        dpsi += t * t;
+      } else {
+        phi += w[i] * t;
+        dphi += t * t;
+      }
+    }
+    psi = rho * warp_sum(psi);
+    dpsi = rho * warp_sum(dpsi);
+    phi = rho * warp_sum(phi);
+    dphi = rho * warp_sum(dphi);
+    const double f = 1.0 + psi + phi;
+    const double ftol = 16.0 * DEPS * (1.0 + fabs(psi) + fabs(phi) + fabs(tau) * (dpsi + dphi));
+    if (fabs(f) <= ftol) {
+      ok = true;
+      break;
+    }
+    if (f < 0.0)
+      lo = tau;
+    else
+      hi = tau;
+    if (hi - lo <= 4.0 * DEPS * fmax(fabs(lo), fabs(hi))) {
+      ok = true;
+      break;
+    }
+    // middle-way rational step (match ψ, ψ' and φ, φ' with the two nearest poles)
+    const double dL = (dl[j] - dor) - tau;
+    double eta = NAN;
+    if (j < K - 1) {
+      const double dR = (dl[j + 1] - dor) - tau;
+      const double c = f - dL * dpsi - dR * dphi;
+      const double s1 = dL * dL * dpsi, s2 = dR * dR * dphi;
+      const double A = c, B = -(c * (dL + dR) + s1 + s2), C = c * dL * dR + s1 * dR + s2 * dL;
+      if (A == 0.0) {
+        eta = -C / B;
+      } else {
+        double disc = B * B - 4.0 * A * C;
+        disc = disc > 0.0 ? sqrt(disc) : 0.0;
+        const double q = -0.5 * (B + copysign(disc, B));
+        const double r1 = q / A, r2 = (q != 0.0) ? C / q : NAN;
+        if (r1 > dL && r1 < dR)
+          eta = r1;
+        else if (r2 > dL && r2 < dR)
+          eta = r2;
+      }
+    } else {
+      const double c = f - dL * dpsi;
+      if (c > 0.0) eta = dL + dL * dL * dpsi / c;
+    }
+    double tn = tau + eta;
+    if (!(tn > lo && tn < hi)) tn = 0.5 * (lo + hi);
+    if (tn == tau) {
+      ok = true;
+      break;
+    }
+    tau = tn;
+  }
+  if (!ok && lane == 0) atomicExch(err, 2);
+  for (int i = lane; i < K; i += 32) delta[i] = (dl[i] - dor) - tau;
+  if (lane == 0) lam[m.o + j] = dor + tau;
+}
+
+// Gu–Eisenstat: ŵ_i = sign(w_i) sqrt(−Δ_ii Π_{j≠i} Δ_ij/(d_i − d_j)); warp per i.
+__global__ void dc_what_kernel(const MergeDesc* md, const RootRef* rows, int nrows, const int* meta,
+                               const double* dlam, const double* wv, const double* Dl, double* what) {
+  const int rid = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (rid >= nrows) return;
+  const int lane = threadIdx.x & 31;
+  const RootRef rr = rows[rid];
+  const MergeDesc m = md[rr.merge];
+  const int K = meta[4 * rr.merge];
+  const int i = rr.j;
+  const double* dl = dlam + m.o;
+  const double* D = Dl + m.off;
+  double p = 1.0;
+  for (int j = lane; j < K; j += 32) {
+    const double dij = D[(long)j * K + i];
+    p *= (j == i) ? dij : dij / (dl[i] - dl[j]);
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) p *= __shfl_xor_sync(0xffffffffu, p, s);
+  if (lane == 0) what[m.o + i] = copysign(sqrt(fmax(-p, 0.0)), wv[m.o + i]);
+}
+
+// Column j of U: u_i = ŵ_i/Δ_ij normalised (in place over Δ); warp per column.
+__global__ void dc_vec_kernel(const MergeDesc* md, const RootRef* roots, int nroots, const int* meta,
+                              const double* what, double* Dl) {
+  const int rid = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (rid >= nroots) return;
+  const int lane = threadIdx.x & 31;
+  const RootRef rr = roots[rid];
+  const MergeDesc m = md[rr.merge];
+  const int K = meta[4 * rr.merge];
+  double* col = Dl + m.off + (long)rr.j * K;
+  const double* wh = what + m.o;
+  double s = 0.0;
+  for (int i = lane; i < K; i += 32) {
+    const double u = wh[i] / col[i];
+    col[i] = u;
+    s += u * u;
+  }
+  s = warp_sum(s);
+  const double inv = 1.0 / sqrt(s);
+  for (int i = lane; i < K; i += 32) col[i] *= inv;
+}
+
+// Merge the ascending roots with the ascending deflated values: write the
+// merged eigenvalues into d[o..o+n) and the destination column of every
+// eigenvector (non-deflated: colmap[o+k]; deflated: colmap[o+K+t]).
+__global__ void dc_order_kernel(const MergeDesc* md, const int* meta, const double* lam, const double* dfv, double* d,
+                                int* colmap) {
+  if (threadIdx.x != 0) return;
+  const MergeDesc m = md[blockIdx.x];
+  const int o = m.o;
+  const int K = meta[4 * blockIdx.x], nd = meta[4 * blockIdx.x + 1];
+  int a = 0, b = 0, pos = 0;
+  while (a < K || b < nd) {
+    const bool take_root = (b >= nd) || (a < K && lam[o + a] <= dfv[o + b]);
+    if (take_root) {
+      d[o + pos] = lam[o + a];
+      colmap[o + a] = pos;
+      ++a;
+    } else {
+      d[o + pos] = dfv[o + b];
+      colmap[o + K + b] = pos;
+      ++b;
+    }
+    ++pos;
+  }
+}
+
+__global__ void dc_copy_deflated_kernel(const MergeDesc* md, const int* meta, const double* Qw, double* Q, int ldq,
+                                        const int* dcol, const int* colmap) {
+  const MergeDesc m = md[blockIdx.y];
+  const int o = m.o, n = m.n1 + m.n2;
+  const int K = meta[4 * blockIdx.y], nd = meta[4 * blockIdx.y + 1];
+  const long total = (long)n * nd;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / nd), t = (int)(e % nd);
+    Q[(long)(o + r) * ldq + o + colmap[o + K + t]] = Qw[(long)(o + r) * ldq + o + dcol[o + t]];
+  }
+}
+
+struct EpiColMap {
+  static constexpr bool kRowDot = false;
+  double* Q;
+  long ldq;
+  int o;
+  const int* colmap;  // colmap[o + c]
+  __device__ void store(int r, int c, double v) const { Q[(long)(o + r) * ldq + o + colmap[o + c]] = v; }
+  __device__ double rowdot_weight(int, int) const { return 0; }
+  __device__ void rowdot_store(int, int, double) const {}
+};
+
+struct DcNode {
+  int o, n, depth;
+  bool leaf;
+};
+
+static void dc_build(int o, int n, int depth, std::vector<DcNode>& out) {
+  if (n <= DC_LEAF) {
+    out.push_back({o, n, depth, true});
+    return;
+  }
+  const int n1 = n / 2;
+  out.push_back({o, n, depth, false});
+  dc_build(o, n1, depth + 1, out);
+  dc_build(o + n1, n - n1, depth + 1, out);
+}
+
+// Eigen-decomposition of the symmetric tridiagonal (w.d, w.e): ascending
+// eigenvalues in w.d, eigenvectors in w.Q (row-major, columns).
+static void stedc(int n, EigWork& w, cudaStream_t st) {
+  std::vector<DcNode> nodes;
+  dc_build(0, n, 0, nodes);
+  int* ib = w.ibuf;
+  int* perm = ib;
+  int* ndcol = ib + n;
+  int* dcol = ib + 2L * n;
+  int* rot = ib + 3L * n;     // 2n
+  int* colmap = ib + 5L * n;  // n
+  int* err = ib + 6L * n;     // 1
+  KOT_CUDA(cudaMemsetAsync(w.Q, 0, sizeof(double) * n * n, st));
+  KOT_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  // host-pinned staging regions (distinct per purpose: copies are asynchronous)
+  int* h_packed = w.hbuf;                                           // <= 2n + 8 ints
+  char* h_desc = reinterpret_cast<char*>(w.hbuf + 2L * n + 64);      // <= n/16 descs
+  char* h_roots = reinterpret_cast<char*>(w.hbuf + 8L * n + 128);    // <= n RootRef
+  char* d_desc_base = reinterpret_cast<char*>(w.dbuf);
+  std::vector<int> splits, loff, llen;
+  int maxdepth = 0;
+  for (auto& nd : nodes) {
+    maxdepth = std::max(maxdepth, nd.depth);
+    if (nd.leaf) {
+      loff.push_back(nd.o);
+      llen.push_back(nd.n);
+    } else {
+      splits.push_back(nd.o + nd.n / 2 - 1);
+    }
+  }
+  std::vector<int> packed;
+  packed.insert(packed.end(), splits.begin(), splits.end());
+  packed.insert(packed.end(), loff.begin(), loff.end());
+  packed.insert(packed.end(), llen.begin(), llen.end());
+  std::copy(packed.begin(), packed.end(), h_packed);
+  int* d_packed = reinterpret_cast<int*>(d_desc_base);
+  KOT_CUDA(cudaMemcpyAsync(d_packed, h_packed, sizeof(int) * packed.size(), cudaMemcpyHostToDevice, st));
+  const int* dsplit = d_packed;
+  const int* dloff = d_packed + splits.size();
+  const int* dllen = dloff + loff.size();
+  if (!splits.empty()) {
+    dc_split_kernel<<<1, 1, 0, st>>>(w.d, w.e, dsplit, (int)splits.size());
+    KOT_LAUNCH_CHECK();
+  }
+  const int nleaves = (int)loff.size();
+  dc_leaf_kernel<<<ceil_div(nleaves, 4), 128, 0, st>>>(w.d, w.e, dloff, dllen, nleaves, w.Q, n, err);
+  KOT_LAUNCH_CHECK();
+  // per-level device descriptors after the packed ints (8-byte aligned)
+  const size_t packed_bytes = ((sizeof(int) * packed.size() + 63) / 64) * 64;
+  MergeDesc* dms = reinterpret_cast<MergeDesc*>(d_desc_base + packed_bytes);
+
+  for (int depth = maxdepth; depth >= 0; --depth) {
+    std::vector<MergeDesc> ms;
+    long off = 0;
+    for (auto& nd : nodes)
+      if (!nd.leaf && nd.depth == depth) {
+        ms.push_back({nd.o, nd.n / 2, nd.n - nd.n / 2, off});
+        off += (long)nd.n * nd.n;
+      }
+    if (ms.empty()) continue;
+    const int nm = (int)ms.size();
+    int* dmeta = reinterpret_cast<int*>(dms + nm);
+    RootRef* droots = reinterpret_cast<RootRef*>(dmeta + 4 * nm);
+    memcpy(h_desc, ms.data(), sizeof(MergeDesc) * nm);
+    KOT_CUDA(cudaMemcpyAsync(dms, h_desc, sizeof(MergeDesc) * nm, cudaMemcpyHostToDevice, st));
+    dc_merge_prep_kernel<<<nm, 128, 0, st>>>(dms, w.Q, n, w.d, w.e, w.zs, w.ds, w.dlam, w.wv, w.dfv, w.rotcs,
+                                             w.rho, perm, ndcol, dcol, rot, dmeta);
+    KOT_LAUNCH_CHECK();
+    std::vector<int> meta(4 * nm);
+    KOT_CUDA(cudaMemcpyAsync(meta.data(), dmeta, sizeof(int) * 4 * nm, cudaMemcpyDeviceToHost, st));
+    KOT_CUDA(cudaStreamSynchronize(st));
+    int maxn = 0;
+    std::vector<RootRef> roots;
+    for (int i = 0; i < nm; ++i) {
+      maxn = std::max(maxn, ms[i].n1 + ms[i].n2);
+      for (int j = 0; j < meta[4 * i]; ++j) roots.push_back({i, j});
+    }
+    dc_merge_vec_kernel<<<dim3(ceil_div(maxn, 128), nm), 128, 0, st>>>(dms, w.Q, w.Qw, w.Qnd, n, perm, ndcol, rot,
+                                                                       w.rotcs, dmeta);
+    KOT_LAUNCH_CHECK();
+    const int nr = (int)roots.size();
+    if (nr > 0) {
+      memcpy(h_roots, roots.data(), sizeof(RootRef) * nr);
+      KOT_CUDA(cudaMemcpyAsync(droots, h_roots, sizeof(RootRef) * nr, cudaMemcpyHostToDevice, st));
+      dc_secular_kernel<<<ceil_div(nr, 8), 256, 0, st>>>(dms, droots, nr, dmeta, w.dlam, w.wv, w.rho, w.lam, w.Dl,
+                                                          err);
+      KOT_LAUNCH_CHECK();
+      dc_what_kernel<<<ceil_div(nr, 8), 256, 0, st>>>(dms, droots, nr, dmeta, w.dlam, w.wv, w.Dl, w.what);
+      KOT_LAUNCH_CHECK();
+      dc_vec_kernel<<<ceil_div(nr, 8), 256, 0, st>>>(dms, droots, nr, dmeta, w.what, w.Dl);
+      KOT_LAUNCH_CHECK();
+    }
+    dc_order_kernel<<<nm, 32, 0, st>>>(dms, dmeta, w.lam, w.dfv, w.d, colmap);
+    KOT_LAUNCH_CHECK();
+    dc_copy_deflated_kernel<<<dim3(64, nm), 256, 0, st>>>(dms, dmeta, w.Qw, w.Q, n, dcol, colmap);
+    KOT_LAUNCH_CHECK();
+    for (int i = 0; i < nm; ++i) {
+      const int K = meta[4 * i];
+      if (K == 0) continue;
+      const int nn = ms[i].n1 + ms[i].n2;
+      GemmShape s = make_shape(nn, K, K, w.Qnd + ms[i].off, K, w.Dl + ms[i].off, K);
+      EpiColMap epi{w.Q, n, ms[i].o, colmap};
+      gemm_launch<false, true>(s, epi, st);
+    }
+  }
+  int herr = 0;
+  KOT_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  KOT_CUDA(cudaStreamSynchronize(st));
+  if (herr)
+    throw KotError(KOT_EEIG, herr == 1 ? "tridiagonal QL failed to converge"
+                                       : "secular equation solver failed to converge");
+}
+
+// ====================================================== back-transform
+
+// T factor of the forward block reflector (dlarft 'F','C') from S = VᵀV.
+__global__ void larft_kernel(const double* S, const double* tau, int nb, double* T) {
+  __shared__ double Ts[TRD_NB][TRD_NB + 1];
+  const int lane = threadIdx.x;
+  for (int i = 0; i < nb; ++i) {
+    double tmp = 0.0;
+    if (lane < i)
+      for (int k = lane; k < i; ++k) tmp += Ts[lane][k] * S[k * nb + i];
+    __syncwarp();
+    if (lane < i) Ts[lane][i] = -tau[i] * tmp;
+    if (lane == i) Ts[i][i] = tau[i];
+    if (lane > i && lane < nb) Ts[lane][i] = 0.0;
+    __syncwarp();
+  }
+  for (int e = lane; e < nb * nb; e += 32) T[e] = Ts[e / nb][e % nb];
+}
+
+__global__ void reverse_cols_kernel(const double* Q, const double* dasc, double* P, double* vals, int n) {
+  const long total = (long)n * n;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / n), c = (int)(e % n);
+    P[e] = Q[(long)r * n + (n - 1 - c)];
+  }
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) vals[i] = dasc[n - 1 - i];
+}
+
+__global__ void count_pos_kernel(const double* vals, int n, int* k) {
+  __shared__ int cnt[32];
+  int c = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) c += (vals[i] > 0.0) ? 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) cnt[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += cnt[w];
+    *k = s;
+  }
+}
+
+static void ormtr(int n, EigWork& w, double* P, cudaStream_t st) {
+  const int npan = (n - 1 + TRD_NB - 1) / TRD_NB;
+  for (int pi = npan - 1; pi >= 0; --pi) {
+    const int p0 = pi * TRD_NB;
+    const int nb = std::min(TRD_NB, n - 1 - p0);
+    const int r0 = p0 + 1;
+    const int mrows = n - r0;
+    const double* Vp = w.Vall + (long)r0 * n + p0;  // mrows × nb (ld n)
+    // S = Vᵀ V
+    {
+      GemmShape s = make_shape(nb, nb, mrows, Vp, n, Vp, n);
+      EpiAxpby epi{w.Tf + TRD_NB * TRD_NB, nb, 1.0, 0.0};
+      gemm_launch<true, false>(s, epi, st);
+    }
+    larft_kernel<<<1, 32, 0, st>>>(w.Tf + TRD_NB * TRD_NB, w.tau + p0, nb, w.Tf);
+    KOT_LAUNCH_CHECK();
+    // W1 = Vᵀ P[r0:, :]
+    {
+      GemmShape s = make_shape(nb, n, mrows, Vp, n, P + (long)r0 * n, n);
+      EpiAxpby epi{w.W1, n, 1.0, 0.0};
+      gemm_launch<true, false>(s, epi, st);
+    }
+    // W2 = T W1
+    {
+      GemmShape s = make_shape(nb, n, nb, w.Tf, nb, w.W1, n);
+      EpiAxpby epi{w.W1 + (long)TRD_NB * n, n, 1.0, 0.0};
+      gemm_launch<false, false>(s, epi, st);
+    }
+    // P[r0:, :] -= V W2
+    {
+      GemmShape s = make_shape(mrows, n, nb, Vp, n, w.W1 + (long)TRD_NB * n, n);
+      EpiAxpby epi{P + (long)r0 * n, n, -1.0, 1.0};
+      gemm_launch<false, false>(s, epi, st);
+    }
+  }
+}
+
+__global__ void eig1_kernel(const double* Z, double* P, double* vals) {
+  vals[0] = Z[0];
+  P[0] = 1.0;
+}
+
+void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigWork& w, cudaStream_t st) {
+  if (n == 1) {
+    eig1_kernel<<<1, 1, 0, st>>>(Z, P, vals);
+    KOT_LAUNCH_CHECK();
+  } else {
+    sytrd(Z, n, w, st);
+    stedc(n, w, st);
+    reverse_cols_kernel<<<std::min(ceil_div((long)n * n, 256), 2048), 256, 0, st>>>(w.Q, w.d, P, vals, n);
+    KOT_LAUNCH_CHECK();
+    ormtr(n, w, P, st);
+  }
+  count_pos_kernel<<<1, 256, 0, st>>>(vals, n, dk);
+  KOT_LAUNCH_CHECK();
+}
+
+}  // namespace kot

@@ -1,0 +1,332 @@
+// FP64 tensor-core GEMM core for sm_100a.
+//
+// tcgen05 has no FP64 kind (ptxas rejects .kind::f64), so the
+// FP64 tensor path on B200 is the warp-level DMMA (`mma.sync.m8n8k4.f64`,
+// SASS DMMA.8x8x4).  This core stages op(A)/op(B) tiles global→shared with a
+// 3-stage cp.async (LDGSTS) pipeline into bank-conflict-free padded layouts,
+// each warp owns a 32×32 C sub-tile (16 DMMA per k4 step), and a pluggable
+// epilogue consumes the accumulators:
+//   * plain / axpby stores,
+//   * symmetric "compute one triangle and mirror" stores (keeps symmetric
+//     iterates bitwise symmetric),
+//   * fused row-dot partials  out[r] = Σ_c acc(r,c)·E(r,c)  (Φ and the
+//     structure-reduced CG matvec), reduced deterministically afterwards.
+// Structural zeros of triangular operands (R is upper triangular) are skipped
+// by restricting the K range per output tile.
+#pragma once
+#include "common.cuh"
+
+namespace kot {
+
+constexpr int GB_M = 64, GB_N = 64, GB_K = 16, G_STAGES = 3, G_THREADS = 128;
+constexpr int G_PADK = GB_K + 4;  // stride ≡ 4 (mod 16) doubles → conflict-free fragment loads
+constexpr int G_PADM = GB_M + 4;
+constexpr int G_PADN = GB_N + 4;
+constexpr int G_ATILE = (GB_M * G_PADK > GB_K * G_PADM) ? GB_M * G_PADK : GB_K * G_PADM;
+constexpr int G_BTILE = (GB_N * G_PADK > GB_K * G_PADN) ? GB_N * G_PADK : GB_K * G_PADN;
+constexpr int G_SMEM_BYTES = G_STAGES * (G_ATILE + G_BTILE + GB_K) * 8;
+
+// C(M×N) = op(A)(M×K) · diag(kscale) · op(B)(K×N), all row-major.
+//   op(A)[m][k] = TA ? A[k*lda+m] : A[m*lda+k]
+//   op(B)[k][n] = TB ? B[n*ldb+k] : B[k*ldb+n]
+struct GemmShape {
+  int M, N, K;
+  const double* A;
+  long lda;
+  const double* B;
+  long ldb;
+  const double* kscale;  // nullable
+  // K-range restriction per output tile (structural zeros of triangular R):
+  //   k_begin = max(kb_m ? m0 : 0, kb_n ? n0 : 0)
+  //   k_end   = min(K, ke_m ? m0+BM : K, ke_n ? n0+BN : K)
+  int kb_m, kb_n, ke_m, ke_n;
+  int sym_tiles;  // enumerate only tiles with tm <= tn (symmetric outputs)
+  int batch_stride_unused;
+};
+
+__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_8(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Load a (rows × cols) tile whose global rows are contiguous (row-major, ld),
+// into smem with padded stride `pad`.  Rows [r0, r0+ROWS), cols [c0, c0+COLS);
+// elements outside [0,rmax)×[0,cmax) are zero-filled.
+template <int ROWS, int COLS, int VEC>
+__device__ __forceinline__ void load_tile(double* sm, int pad, const double* g, long ld, int r0, int c0,
+                                          int rmax, int cmax) {
+  constexpr int CPR = COLS / VEC;  // chunks per row
+  constexpr int TOTAL = ROWS * CPR;
+#pragma unroll
+  for (int i = threadIdx.x; i < TOTAL; i += G_THREADS) {
+    const int r = i / CPR, c = (i % CPR) * VEC;
+    const int gr = r0 + r, gc = c0 + c;
+    int valid = 0;
+    if (gr < rmax) valid = min(max(cmax - gc, 0), VEC);
+    const double* src = valid ? (g + (long)gr * ld + gc) : g;
+    double* dst = sm + r * pad + c;
+    if (VEC == 2)
+      cp_async_16(dst, src, valid * 8);
+    else
+      cp_async_8(dst, src, valid * 8);
+  }
+}
+
+// Epilogue interface:
+//   static constexpr bool kRowDot;            // use the fused row-dot path
+//   __device__ void store(int r, int c, double v) const;          (kRowDot == false)
+//   __device__ double rowdot_weight(int r, int c) const;          (kRowDot == true)
+//   __device__ void rowdot_store(int tn, int r, double partial) const;
+template <bool TA, bool TB, int VEC, class Epi>
+__global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi epi) {
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;
+  double* Bs = gsm + G_STAGES * G_ATILE;
+  double* Ks = gsm + G_STAGES * (G_ATILE + G_BTILE);
+
+  const int tiles_m = (s.M + GB_M - 1) / GB_M;
+  const int tiles_n = (s.N + GB_N - 1) / GB_N;
+  int tm, tn;
+  if (s.sym_tiles) {
+    int t = blockIdx.x;
+    tm = 0;
+    while (t >= tiles_n - tm) {
+      t -= tiles_n - tm;
+      ++tm;
+    }
+    tn = tm + t;
+  } else {
+    tm = blockIdx.x % tiles_m;
+    tn = blockIdx.x / tiles_m;
+  }
+  if (tm >= tiles_m || tn >= tiles_n) return;
+  const int m0 = tm * GB_M, n0 = tn * GB_N;
+
+  int kbeg = 0, kend = s.K;
+  if (s.kb_m) kbeg = max(kbeg, m0);
+  if (s.kb_n) kbeg = max(kbeg, n0);
+  if (s.ke_m) kend = min(kend, m0 + GB_M);
+  if (s.ke_n) kend = min(kend, n0 + GB_N);
+  kbeg = (kbeg / GB_K) * GB_K;
+  const int nkt = kend > kbeg ? (kend - kbeg + GB_K - 1) / GB_K : 0;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto issue = [&](int kt, int stage) {
+    const int k0 = kbeg + kt * GB_K;
+    double* as = As + stage * G_ATILE;
+    double* bs = Bs + stage * G_BTILE;
+    if (TA)  // A stored K×M: tile rows k, cols m
+      load_tile<GB_K, GB_M, VEC>(as, G_PADM, s.A, s.lda, k0, m0, s.K, s.M);
+    else
+      load_tile<GB_M, GB_K, VEC>(as, G_PADK, s.A, s.lda, m0, k0, s.M, s.K);
+    if (TB)  // B stored N×K
+      load_tile<GB_N, GB_K, VEC>(bs, G_PADK, s.B, s.ldb, n0, k0, s.N, s.K);
+    else
+      load_tile<GB_K, GB_N, VEC>(bs, G_PADN, s.B, s.ldb, k0, n0, s.K, s.N);
+    if (s.kscale != nullptr && threadIdx.x < GB_K) {
+      const int k = k0 + threadIdx.x;
+      cp_async_8(Ks + stage * GB_K + threadIdx.x, k < s.K ? s.kscale + k : s.kscale, k < s.K ? 8 : 0);
+    }
+  };
+
+#pragma unroll
+  for (int st = 0; st < G_STAGES - 1; ++st) {
+    if (st < nkt) issue(st, st);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < nkt; ++kt) {
+    cp_async_wait<G_STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + G_STAGES - 1;
+      if (nk < nkt) issue(nk, nk % G_STAGES);
+      cp_async_commit();
+    }
+    const int stage = kt % G_STAGES;
+    const double* as = As + stage * G_ATILE;
+    const double* bs = Bs + stage * G_BTILE;
+    const double* ks = Ks + stage * GB_K;
+#pragma unroll
+    for (int kk = 0; kk < GB_K; kk += 4) {
+      double a[4], b[4];
+      const double kscl = (s.kscale != nullptr) ? ks[kk + t] : 1.0;
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const int m = wm + i * 8 + g;
+        a[i] = (TA ? as[(kk + t) * G_PADM + m] : as[m * G_PADK + kk + t]) * kscl;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int n = wn + j * 8 + g;
+        b[j] = TB ? bs[n * G_PADK + kk + t] : bs[(kk + t) * G_PADN + n];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  if constexpr (Epi::kRowDot) {
+    // partial[r] = Σ_{c in this tile} acc(r,c)·E(r,c): 4-lane shuffle + 2-warp smem combine.
+    __syncthreads();
+    double* red = gsm;  // reuse: [2][GB_M]
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const int r = m0 + wm + i * 8 + g;
+      double p = 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int c = n0 + wn + j * 8 + 2 * t + h;
+          if (r < s.M && c < s.N) p += acc[i][j][h] * epi.rowdot_weight(r, c);
+        }
+      p += __shfl_xor_sync(0xffffffffu, p, 1);
+      p += __shfl_xor_sync(0xffffffffu, p, 2);
+      if (t == 0) red[(warp & 1) * GB_M + wm + i * 8 + g] = p;
+    }
+    __syncthreads();
+    if (threadIdx.x < GB_M) {
+      const int r = m0 + threadIdx.x;
+      if (r < s.M) epi.rowdot_store(tn, r, red[threadIdx.x] + red[GB_M + threadIdx.x]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const int r = m0 + wm + i * 8 + g;
+      if (r >= s.M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int c = n0 + wn + j * 8 + 2 * t + h;
+          if (c < s.N) epi.store(r, c, acc[i][j][h]);
+        }
+    }
+  }
+}
+
+inline int gemm_grid(const GemmShape& s) {
+  const int tm = (s.M + GB_M - 1) / GB_M, tn = (s.N + GB_N - 1) / GB_N;
+  if (s.sym_tiles) return tm * (tm + 1) / 2;
+  return tm * tn;
+}
+
+inline bool gemm_vec2_ok(const GemmShape& s) {
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return al(s.A) && al(s.B) && (s.lda % 2 == 0) && (s.ldb % 2 == 0);
+}
+
+template <bool TA, bool TB, class Epi>
+void gemm_launch(const GemmShape& s, const Epi& epi, cudaStream_t st) {
+  if (s.M <= 0 || s.N <= 0) return;
+  const int grid = gemm_grid(s);
+  if (gemm_vec2_ok(s)) {
+    auto k = gemm_dmma_kernel<TA, TB, 2, Epi>;
+    static bool attr = false;
+    if (!attr) {
+      KOT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES));
+      attr = true;
+    }
+    k<<<grid, G_THREADS, G_SMEM_BYTES, st>>>(s, epi);
+  } else {
+    auto k = gemm_dmma_kernel<TA, TB, 1, Epi>;
+    static bool attr = false;
+    if (!attr) {
+      KOT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES));
+      attr = true;
+    }
+    k<<<grid, G_THREADS, G_SMEM_BYTES, st>>>(s, epi);
+  }
+  KOT_LAUNCH_CHECK();
+}
+
+inline GemmShape make_shape(int M, int N, int K, const double* A, long lda, const double* B, long ldb) {
+  GemmShape s{};
+  s.M = M;
+  s.N = N;
+  s.K = K;
+  s.A = A;
+  s.lda = lda;
+  s.B = B;
+  s.ldb = ldb;
+  return s;
+}
+
+// ------------------------------------------------------------------ epilogues
+
+// C = alpha*acc + beta*C
+struct EpiAxpby {
+  static constexpr bool kRowDot = false;
+  double* C;
+  long ldc;
+  double alpha, beta;
+  __device__ void store(int r, int c, double v) const {
+    double* p = C + (long)r * ldc + c;
+    *p = (beta == 0.0) ? alpha * v : alpha * v + beta * (*p);
+  }
+  __device__ double rowdot_weight(int, int) const { return 0; }
+  __device__ void rowdot_store(int, int, double) const {}
+};
+
+// Symmetric output: only tiles tm<=tn are computed; value written to (r,c) and (c,r).
+// out = beta*X(r,c) + alpha*(acc + diag*δ_rc)   (X must itself be symmetric; beta ignored if X null)
+struct EpiSymMirror {
+  static constexpr bool kRowDot = false;
+  double* C;
+  long ldc;
+  double alpha;
+  const double* X;  // nullable
+  double beta;
+  double diag;
+  __device__ void store(int r, int c, double v) const {
+    if (r > c) return;  // the diagonal tile computes both halves; keep one
+    double o = v;
+    if (r == c) o = __dadd_rn(o, diag);
+    o = __dmul_rn(alpha, o);
+    if (X != nullptr) o = __dadd_rn(__dmul_rn(beta, X[(long)r * ldc + c]), o);
+    C[(long)r * ldc + c] = o;
+    C[(long)c * ldc + r] = o;
+  }
+  __device__ double rowdot_weight(int, int) const { return 0; }
+  __device__ void rowdot_store(int, int, double) const {}
+};
+
+// partial[tn][r] = Σ_c acc(r,c)·E[r][c]
+struct EpiRowDot {
+  static constexpr bool kRowDot = true;
+  const double* E;
+  long lde;
+  double* partial;  // [tiles_n][ldp]
+  long ldp;
+  __device__ void store(int, int, double) const {}
+  __device__ double rowdot_weight(int r, int c) const { return E[(long)r * lde + c]; }
+  __device__ void rowdot_store(int tn, int r, double p) const { partial[(long)tn * ldp + r] = p; }
+};
+
+}  // namespace kot

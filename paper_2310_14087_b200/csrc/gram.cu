@@ -1,0 +1,209 @@
+// Gaussian Gram assembly (north-star item 1; reference kernels.py:61-94,
+// problem.py:135-169).
+//
+// * Square Grams are computed one triangle at a time and mirrored, so Q and
+//   K are bitwise symmetric with a unit diagonal per kernel, exactly as the
+//   reference's sym(g)+fill_diagonal(1) produces (kernels.py:70-72).
+// * Squared distances are accumulated dimension by dimension without FMA
+//   contraction, the same order scipy's cdist('sqeuclidean') uses.
+// * The mean embeddings (column means of the n×ℓ sample/filling Gram) and the
+//   embedding norms (mean of the n×n sample Gram) are fused reductions: the
+//   rectangular Grams are never materialised in HBM.
+// Point tiles are staged in shared memory; each CTA owns a 32×32 output tile.
+#include "kernels.cuh"
+
+namespace kot {
+
+constexpr int GT = 32;      // output tile
+constexpr int GMAXD = 128;  // max point dimension staged (pair kernel: 2d)
+
+__device__ __forceinline__ double sqdist_seq(const double* a, const double* b, int d) {
+  double s = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double t = __dsub_rn(a[k], b[k]);
+    s = __dadd_rn(s, __dmul_rn(t, t));
+  }
+  return s;
+}
+
+// out[i][j] = Σ_s exp(-||P_s[i]-P_s[j]||² / (2 bw_s)), s over 1 or 2 point sets
+// with (d_s) dims each, upper tiles only, mirrored; diagonal = nsets.
+// If `pair` (K on [x y] ∈ R^{2d}), the two sets are concatenated instead.
+__global__ void gram_square_kernel(const double* __restrict__ P0, const double* __restrict__ P1, int n,
+                                   int d, double twobw0, double twobw1, int nsets, int pair,
+                                   double* __restrict__ out) {
+  extern __shared__ double gsh[];
+  const int tiles = (n + GT - 1) / GT;
+  int t = blockIdx.x, ti = 0;
+  while (t >= tiles - ti) {
+    t -= tiles - ti;
+    ++ti;
+  }
+  const int tj = ti + t;
+  const int i0 = ti * GT, j0 = tj * GT;
+  const int D = pair ? 2 * d : d;
+  const int LD = D + 1;
+  double* si = gsh;
+  double* sj = gsh + GT * LD;
+  const int sets = pair ? 1 : nsets;
+  // thread layout: 256 threads, each computes 4 entries (rows ty*4.., col tx)
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 4
+  double res[4] = {0, 0, 0, 0};
+  for (int s = 0; s < sets; ++s) {
+    const double* P = (s == 0) ? P0 : P1;
+    const double twobw = (s == 0) ? twobw0 : twobw1;
+    __syncthreads();
+    for (int e = threadIdx.x; e < GT * D; e += blockDim.x) {
+      const int r = e / D, k = e % D;
+      double vi = 0.0, vj = 0.0;
+      if (pair) {
+        const double* src = (k < d) ? P0 : P1;
+        const int kk = (k < d) ? k : k - d;
+        if (i0 + r < n) vi = src[(long)(i0 + r) * d + kk];
+        if (j0 + r < n) vj = src[(long)(j0 + r) * d + kk];
+      } else {
+        if (i0 + r < n) vi = P[(long)(i0 + r) * d + k];
+        if (j0 + r < n) vj = P[(long)(j0 + r) * d + k];
+      }
+      si[r * LD + k] = vi;
+      sj[r * LD + k] = vj;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = ty * 4 + q;
+      const double dd = sqdist_seq(si + r * LD, sj + tx * LD, D);
+      res[q] = __dadd_rn(res[q], exp(-dd / twobw));
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = i0 + ty * 4 + q, j = j0 + tx;
+    if (i >= n || j >= n || i > j) continue;
+    const double v = (i == j) ? (double)sets : res[q];
+    out[(long)i * n + j] = v;
+    out[(long)j * n + i] = v;
+  }
+}
+
+// embed[j] = mean_i exp(-||S_i - F_j||²/(2bw)) summed over the (S,F) pairs
+// (mu: xs/xt, nu: ys/yt).  Column mean accumulated row by row, as numpy's
+// .mean(axis=0) on a C-contiguous array does.
+__global__ void embed_kernel(const double* __restrict__ xs, int nx, const double* __restrict__ ys, int ny,
+                             const double* __restrict__ xt, const double* __restrict__ yt, int l, int d,
+                             double twobw, double lambda2, double* __restrict__ embed,
+                             double* __restrict__ z) {
+  extern __shared__ double sh[];  // staged sample chunk: [CH][d]
+  const int CH = 64;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  double fj[GMAXD];
+  double tot = 0.0;
+  for (int set = 0; set < 2; ++set) {
+    const double* S = set ? ys : xs;
+    const double* F = set ? yt : xt;
+    const int ns = set ? ny : nx;
+    if (j < l)
+      for (int k = 0; k < d; ++k) fj[k] = F[(long)j * d + k];
+    double acc = 0.0;
+    for (int c0 = 0; c0 < ns; c0 += CH) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < CH * d; e += blockDim.x) {
+        const int r = e / d, k = e % d;
+        sh[e] = (c0 + r < ns) ? S[(long)(c0 + r) * d + k] : 0.0;
+      }
+      __syncthreads();
+      if (j < l) {
+        const int cn = min(CH, ns - c0);
+        for (int r = 0; r < cn; ++r) {
+          double s = 0.0;
+          for (int k = 0; k < d; ++k) {
+            const double t = __dsub_rn(sh[r * d + k], fj[k]);
+            s = __dadd_rn(s, __dmul_rn(t, t));
+          }
+          acc = __dadd_rn(acc, exp(-s / twobw));
+        }
+      }
+    }
+    tot = (set == 0) ? acc / ns : tot + acc / ns;
+  }
+  if (j < l) {
+    double cost = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double t = __dsub_rn(xt[(long)j * d + k], yt[(long)j * d + k]);
+      cost = __dadd_rn(cost, __dmul_rn(t, t));
+    }
+    embed[j] = tot;
+    z[j] = tot - lambda2 * cost;
+  }
+}
+
+// Partial sums of the square sample Gram (unit diagonal) per row block,
+// deterministic: part[blockIdx.x] = Σ_{i in block rows} Σ_j g_ij.
+__global__ void gram_sum_kernel(const double* __restrict__ S, int n, int d, double twobw,
+                                double* __restrict__ part) {
+  __shared__ double red[32];
+  const int i = blockIdx.x;  // one row per block
+  double acc = 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double v;
+    if (j == i) {
+      v = 1.0;
+    } else {
+      double s = 0.0;
+      for (int k = 0; k < d; ++k) {
+        const double t = __dsub_rn(S[(long)i * d + k], S[(long)j * d + k]);
+        s = __dadd_rn(s, __dmul_rn(t, t));
+      }
+      v = exp(-s / twobw);
+    }
+    acc += v;
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) part[i] = acc;
+}
+
+__global__ void sum_parts_kernel(const double* __restrict__ p0, int n0, const double* __restrict__ p1, int n1,
+                                 double* __restrict__ out) {
+  __shared__ double red[32];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < n0; i += blockDim.x) a += p0[i];
+  for (int i = threadIdx.x; i < n1; i += blockDim.x) b += p1[i];
+  a = block_sum(a, red);
+  b = block_sum(b, red);
+  if (threadIdx.x == 0) out[0] = a / ((double)n0 * n0) + b / ((double)n1 * n1);
+}
+
+void gram_square(const double* P0, const double* P1, int n, int d, double bw0, double bw1, int nsets,
+                 bool pair, double* out, cudaStream_t st) {
+  kot_require((pair ? 2 * d : d) <= GMAXD, KOT_EINVAL, "point dimension too large for the Gram kernel");
+  const int tiles = (n + GT - 1) / GT;
+  const int D = pair ? 2 * d : d;
+  const size_t smem = 2 * GT * (D + 1) * sizeof(double);
+  if (smem > 48 * 1024)
+    KOT_CUDA(cudaFuncSetAttribute(gram_square_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  gram_square_kernel<<<tiles * (tiles + 1) / 2, 256, smem, st>>>(P0, P1, n, d, 2.0 * bw0,
+                                                               2.0 * bw1, nsets, pair ? 1 : 0, out);
+  KOT_LAUNCH_CHECK();
+}
+
+void assemble_device(const double* xs, int nx, const double* ys, int ny, const double* xt, const double* yt,
+                     int l, int d, double bw, double lambda2, double* Q, double* Kmat, double* embed,
+                     double* z, double* q_sq, double* scratch, cudaStream_t st) {
+  kot_require(d <= GMAXD / 2 && d >= 1, KOT_EINVAL, "point dimension must be in [1, 64]");
+  // Q = G(xt) + G(yt): unit diagonals sum to 2.
+  gram_square(xt, yt, l, d, bw, bw, 2, false, Q, st);
+  // K on [xt yt] ∈ R^{2d}
+  gram_square(xt, yt, l, d, bw, bw, 1, true, Kmat, st);
+  const int thr = 128;
+  embed_kernel<<<ceil_div(l, thr), thr, 64 * d * sizeof(double), st>>>(xs, nx, ys, ny, xt, yt, l, d,
+                                                                       2.0 * bw, lambda2, embed, z);
+  KOT_LAUNCH_CHECK();
+  gram_sum_kernel<<<nx, 256, 0, st>>>(xs, nx, d, 2.0 * bw, scratch);
+  KOT_LAUNCH_CHECK();
+  gram_sum_kernel<<<ny, 256, 0, st>>>(ys, ny, d, 2.0 * bw, scratch + nx);
+  KOT_LAUNCH_CHECK();
+  sum_parts_kernel<<<1, 256, 0, st>>>(scratch, nx, scratch + nx, ny, q_sq);
+  KOT_LAUNCH_CHECK();
+}
+
+}  // namespace kot

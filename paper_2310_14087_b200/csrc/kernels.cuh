@@ -1,0 +1,39 @@
+// Internal (C++) interface of libkotgpu: device-level building blocks.
+#pragma once
+#include "common.cuh"
+
+namespace kot {
+
+// ---------------------------------------------------------------- gram.cu
+void gram_square(const double* P0, const double* P1, int n, int d, double bw0, double bw1, int nsets, bool pair,
+                 double* out, cudaStream_t st);
+void assemble_device(const double* xs, int nx, const double* ys, int ny, const double* xt, const double* yt, int l,
+                     int d, double bw, double lambda2, double* Q, double* Kmat, double* embed, double* z,
+                     double* q_sq, double* scratch, cudaStream_t st);
+
+// ---------------------------------------------------------------- chol.cu
+// Upper R with RᵀR = sym(K) + jitter·I (row-major).  work: n*n doubles; dscal: 1 device double.
+double cholesky_psd_device(const double* K, int n, double* R, double* work, double* dscal, int* dflag,
+                           cudaStream_t st);
+
+// ----------------------------------------------------------------- eig.cu
+struct EigWork {
+  int n;
+  double *A = nullptr, *Vall = nullptr, *X = nullptr, *d = nullptr, *e = nullptr, *tau = nullptr;
+  double *xv = nullptr, *yv = nullptr, *part = nullptr, *partn = nullptr, *Tf = nullptr, *W1 = nullptr;
+  double *Q = nullptr, *Qw = nullptr, *Qnd = nullptr, *Dl = nullptr;
+  double *zs = nullptr, *ds = nullptr, *dlam = nullptr, *wv = nullptr, *what = nullptr, *lam = nullptr;
+  double *dfv = nullptr, *rotcs = nullptr, *rho = nullptr;
+  int* ibuf = nullptr;
+  void* dbuf = nullptr;
+  int* hbuf = nullptr;
+  explicit EigWork(int n);
+  ~EigWork();
+  EigWork(const EigWork&) = delete;
+  EigWork& operator=(const EigWork&) = delete;
+};
+// Z symmetric (n×n, row-major, device).  Outputs: P (columns = eigenvectors,
+// descending eigenvalues), vals (descending), *dk = #(vals > 0).
+void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigWork& w, cudaStream_t st);
+
+}  // namespace kot

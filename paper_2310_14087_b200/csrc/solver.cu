@@ -1,0 +1,415 @@
+// Algorithm 1 (inexact regularized Newton direction with CG) and Algorithm 2
+// (EG-safeguarded SSN loop) on device-resident state.
+//
+// Reference: newton.py:144-211 (newton_direction, theta_update),
+// linalg.py:117-162 (cg_solve), solver.py:114-289 (solve, solve_pure_eg).
+// Control flow, tie-breaking and error conditions follow the reference line
+// by line; all vectors/matrices stay in HBM and only the scalars that steer
+// the control flow (norms, pAp, flags) cross to the host.
+#include <chrono>
+#include <cmath>
+#include <utility>
+#include <vector>
+
+#include "gemm.cuh"
+#include "ssn.cuh"
+
+namespace kot {
+
+using clk = std::chrono::steady_clock;
+static double ms_since(clk::time_point t0) {
+  return std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+}
+
+// ------------------------------------------------------------------- CG
+
+constexpr int CG_THREADS = 1024;
+// scalar slots in p.dsc used by CG
+constexpr int SC_RR = 8, SC_BN = 9, SC_PAP = 10, SC_RES = 11, SC_FLAG = 12;
+
+__global__ void __launch_bounds__(CG_THREADS) cg_init_kernel(int n, const double* __restrict__ b, double* x,
+                                                             double* r, double* pv, double* sc) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double bi = b[i];
+    x[i] = 0.0;
+    r[i] = bi;
+    pv[i] = bi;
+    s += bi * bi;
+  }
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) {
+    sc[SC_RR] = s;
+    sc[SC_BN] = sqrt(s);
+  }
+}
+
+// one CG update after ap = A p (linalg.py:142-161)
+__global__ void __launch_bounds__(CG_THREADS) cg_step_kernel(int n, double* x, double* r, double* pv,
+                                                             const double* __restrict__ ap, double* sc) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += pv[i] * ap[i];
+  const double pap = block_sum(s, sh);
+  const double rr = sc[SC_RR];
+  __syncthreads();
+  if (threadIdx.x == 0) sc[SC_PAP] = pap;
+  if (!isfinite(pap)) {
+    if (threadIdx.x == 0) sc[SC_FLAG] = 1.0;
+    return;
+  }
+  if (pap <= 0.0) {
+    if (threadIdx.x == 0) sc[SC_FLAG] = 2.0;
+    return;
+  }
+  const double alpha = rr / pap;
+  double s2 = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pv[i]));
+    const double ri = __dsub_rn(r[i], __dmul_rn(alpha, ap[i]));
+    r[i] = ri;
+    s2 += ri * ri;
+  }
+  const double rrn = block_sum(s2, sh);
+  const double res = sqrt(rrn);
+  const double beta = rrn / rr;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) pv[i] = __dadd_rn(r[i], __dmul_rn(beta, pv[i]));
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sc[SC_RES] = res;
+    sc[SC_RR] = rrn;
+    sc[SC_FLAG] = isfinite(res) ? 0.0 : 3.0;
+  }
+}
+
+struct CgOut {
+  int iters;
+  double res;
+};
+
+// x (= b.cx) solves A x = rhs to tol·‖rhs‖ with A = middle operator.
+static CgOut cg_solve(Problem& p, const Decomp& dc, double mu, const double* rhs, double tol, int max_iter) {
+  Bufs& b = p.bufs();
+  const int n = p.n;
+  kot_require(max_iter >= 1, KOT_EINVAL, "max_iter must be >= 1");
+  cg_init_kernel<<<1, CG_THREADS, 0, p.st>>>(n, rhs, b.cx, b.cr, b.cp, p.dsc);
+  KOT_LAUNCH_CHECK();
+  fetch(p, 16);
+  const double target = tol * p.hsc[SC_BN];
+  double res = p.hsc[SC_BN];
+  if (res <= target) return {0, res};
+  int it = 0;
+  for (it = 1; it <= max_iter; ++it) {
+    middle_operator(p, dc, mu, b.cp, b.cap);
+    cg_step_kernel<<<1, CG_THREADS, 0, p.st>>>(n, b.cx, b.cr, b.cp, b.cap, p.dsc);
+    KOT_LAUNCH_CHECK();
+    fetch(p, 16);
+    const int flag = (int)p.hsc[SC_FLAG];
+    if (flag == 1) throw KotError(KOT_ECG, "non-finite curvature in conjugate gradient");
+    if (flag == 2) {  // p collapsed to numerical zero on an SPD operator
+      it -= 1;
+      break;
+    }
+    res = p.hsc[SC_RES];
+    if (flag == 3) throw KotError(KOT_ECG, "non-finite residual in conjugate gradient");
+    if (res <= target) return {it, res};
+  }
+  if (it > max_iter) it = max_iter;
+  return {it, res};
+}
+
+// --------------------------------------------------------------- Newton
+
+NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, double rn, const Decomp& dc, double mu,
+                           const SolverCfg& cfg, double* dg, double* dX) {
+  Bufs& b = p.bufs();
+  const int n = p.n;
+  const long nn = (long)n * n;
+  kot_require(rn > 0.0, KOT_EINVAL, "direction requires a nonzero residual");
+  // filt = r2 + 𝒯[r2];  a1 = −r1 − Φ(filt)/(μ+1);  ã2 = −filt/(μ+1)   (newton.py:161-163)
+  spectral_filter(p, dc, r2, p.M2, mu, 0);
+  axpby(p, nn, 1.0, r2, 1.0, p.M2, b.filt);
+  phi_partials(p, b.filt);
+  finalize(p, FIN_A1, nullptr, true, r1, mu, b.a1);
+  neg_div(p, nn, b.filt, mu + 1.0, b.a2t);
+  double rel = cfg.has_cg_tol ? cfg.cg_tol : cfg.tau * std::min(1.0, cfg.kappa * rn);
+  const double a1n = dev_norm(p, b.a1, n);
+  KOT_CUDA(cudaMemsetAsync(b.sol, 0, sizeof(double) * n, p.st));
+  NewtonOut out{0, 0, 0, INFINITY, 0.0, 0.0};
+  const auto t0 = clk::now();
+  for (int att = 0; att <= cfg.cg_restarts; ++att) {
+    out.attempts = att + 1;
+    const double* rhs = b.a1;
+    if (att) {
+      middle_operator(p, dc, mu, b.sol, b.e3);
+      axpby(p, n, 1.0, b.a1, -1.0, b.e3, b.rhs);
+      rhs = b.rhs;
+    }
+    const double bn = dev_norm(p, rhs, n);
+    if (bn > 0.0 && a1n > 0.0) {
+      const CgOut c = cg_solve(p, dc, mu, rhs, rel * a1n / bn, cfg.cg_max);
+      axpby(p, n, 1.0, b.sol, 1.0, b.cx, b.sol);
+      out.cg_iters += c.iters;
+    }
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+    out.cg_ms = ms_since(t0);
+    // dw = (sol, ã2 − 𝒯[Φ*(sol)])
+    KOT_CUDA(cudaMemcpyAsync(dg, b.sol, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
+    phi_adjoint(p, b.sol, p.M1);
+    spectral_filter(p, dc, p.M1, p.M2, mu, 0);
+    axpby(p, nn, 1.0, b.a2t, -1.0, p.M2, dX);
+    // criterion ‖(J+μI)dw + r‖ ≤ τ min(1, κ‖r‖‖dw‖)   (newton.py:131-141, problem.py:222-236)
+    phi_partials(p, dX);
+    finalize(p, FIN_JTOP, dg, true, r1, mu, b.e1);
+    phi_adjoint_ex(p, dg, p.M1, 1.0, dX, -1.0, 0.0);  // Φ*(dγ) − dX
+    spectral_filter(p, dc, p.M1, p.M2, mu, 1);         // M[·]
+    jac_bottom(p, nn, p.M2, dX, mu, r2, p.M1);
+    dev_reduce(p, b.e1, nullptr, n, 0, true);
+    dev_reduce(p, p.M1, nullptr, nn, 1, true);
+    dev_reduce(p, dg, nullptr, n, 2, true);
+    dev_reduce(p, dX, nullptr, nn, 3, true);
+    fetch(p, 4);
+    out.lhs = p.hsc[0] + p.hsc[1];
+    const double dwn = p.hsc[2] + p.hsc[3];
+    out.rhs = cfg.tau * std::min(1.0, cfg.kappa * rn * dwn);
+    out.met = out.lhs <= out.rhs;
+    if (out.met) break;
+    rel /= 10.0;
+  }
+  return out;
+}
+
+static double theta_update(double theta, double rho, double dw_sq, const SolverCfg& c) {
+  double t;
+  if (rho >= c.alpha2 * dw_sq)
+    t = std::max(c.theta_min, c.beta0 * theta);
+  else if (rho >= c.alpha1 * dw_sq)
+    t = c.beta1 * theta;
+  else
+    t = std::min(c.theta_max, c.beta2 * theta);
+  return std::min(std::max(t, c.theta_min), c.theta_max);
+}
+
+// ----------------------------------------------------------------- solve
+
+struct HostProbe {
+  std::vector<double> wg, wx, rg, rx, dg, dx;
+};
+
+static void copy_state(Problem& p, Bufs& b, Decomp& dw, const Decomp& dv) {
+  const int n = p.n;
+  const long nn = (long)n * n;
+  KOT_CUDA(cudaMemcpyAsync(b.gw, b.gv, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
+  KOT_CUDA(cudaMemcpyAsync(b.Xw, b.Xv, sizeof(double) * nn, cudaMemcpyDeviceToDevice, p.st));
+  KOT_CUDA(cudaMemcpyAsync(b.r1w, b.r1v, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
+  KOT_CUDA(cudaMemcpyAsync(b.r2w, b.r2v, sizeof(double) * nn, cudaMemcpyDeviceToDevice, p.st));
+  KOT_CUDA(cudaMemcpyAsync(dw.P, dv.P, sizeof(double) * nn, cudaMemcpyDeviceToDevice, p.st));
+  KOT_CUDA(cudaMemcpyAsync(dw.vals, dv.vals, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
+  dw.k = dv.k;
+}
+
+// One pass of the solver.py:142-222 loop body on the current buffers.
+// Returns false if a non-finite residual was met (SolverNumericsError).
+struct LoopState {
+  double res_w, res_v, theta;
+  Decomp dw, dv, dt;
+};
+
+static bool loop_body(Problem& p, const SolverCfg& cfg, LoopState& s, int k, IterRecord& rec, IterCallback cb,
+                      void* user, HostProbe* hp) {
+  Bufs& b = p.bufs();
+  const int n = p.n;
+  const long nn = (long)n * n;
+  const auto t_it = clk::now();
+  double eg_ms = 0.0, resid_ms = 0.0;
+  if (k % cfg.safeguard_every == 0) {
+    auto t0 = clk::now();
+    eg_step(p, b.gv, b.Xv, cfg.eg_stepsize, b.gv, b.Xv);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+    eg_ms = ms_since(t0);
+    t0 = clk::now();
+    s.res_v = residual_parts(p, b.gv, b.Xv, b.r1v, b.r2v, s.dv);
+    resid_ms += ms_since(t0);
+    if (!std::isfinite(s.res_v)) return false;
+  }
+  auto t0 = clk::now();
+  kot_require(s.res_w > 0.0, KOT_EINVAL, "context requires a nonzero residual");
+  const double mu = s.theta * s.res_w;
+  kot_require(mu > 0.0, KOT_EINVAL, "regularization mu must be positive");
+  const NewtonOut st = newton_direction(p, b.r1w, b.r2w, s.res_w, s.dw, mu, cfg, b.dg, b.dX);
+  KOT_CUDA(cudaStreamSynchronize(p.st));
+  const double newton_ms = ms_since(t0);
+  axpby(p, n, 1.0, b.gw, 1.0, b.dg, b.gt);
+  axpby(p, nn, 1.0, b.Xw, 1.0, b.dX, b.Xt);
+  t0 = clk::now();
+  const double res_t = residual_parts(p, b.gt, b.Xt, b.r1t, b.r2t, s.dt);
+  resid_ms += ms_since(t0);
+  if (!std::isfinite(res_t)) return false;
+  if (cb) {
+    hp->wg.resize(n);
+    hp->wx.resize(nn);
+    hp->rg.resize(n);
+    hp->rx.resize(nn);
+    hp->dg.resize(n);
+    hp->dx.resize(nn);
+    KOT_CUDA(cudaMemcpyAsync(hp->wg.data(), b.gw, sizeof(double) * n, cudaMemcpyDeviceToHost, p.st));
+    KOT_CUDA(cudaMemcpyAsync(hp->wx.data(), b.Xw, sizeof(double) * nn, cudaMemcpyDeviceToHost, p.st));
+    KOT_CUDA(cudaMemcpyAsync(hp->rg.data(), b.r1w, sizeof(double) * n, cudaMemcpyDeviceToHost, p.st));
+    KOT_CUDA(cudaMemcpyAsync(hp->rx.data(), b.r2w, sizeof(double) * nn, cudaMemcpyDeviceToHost, p.st));
+    KOT_CUDA(cudaMemcpyAsync(hp->dg.data(), b.dg, sizeof(double) * n, cudaMemcpyDeviceToHost, p.st));
+    KOT_CUDA(cudaMemcpyAsync(hp->dx.data(), b.dX, sizeof(double) * nn, cudaMemcpyDeviceToHost, p.st));
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+    cb(user, k, hp->wg.data(), hp->wx.data(), hp->rg.data(), hp->rx.data(), mu, s.theta, hp->dg.data(),
+       hp->dx.data(), st.met);
+  }
+  // damping update from the trial point, whether or not it is kept (solver.py:224-226)
+  dev_reduce(p, b.r1t, b.dg, n, 0, false);
+  dev_reduce(p, b.r2t, b.dX, nn, 1, false);
+  dev_reduce(p, b.dg, nullptr, n, 2, true);
+  dev_reduce(p, b.dX, nullptr, nn, 3, true);
+  fetch(p, 4);
+  const double rho = -(p.hsc[0] + p.hsc[1]);
+  const double dwn = p.hsc[2] + p.hsc[3];
+  const double theta_next = theta_update(s.theta, rho, dwn * dwn, cfg);
+  int acc_ssn;
+  if (res_t <= s.res_v) {
+    acc_ssn = 1;
+    std::swap(b.gw, b.gt);
+    std::swap(b.Xw, b.Xt);
+    std::swap(b.r1w, b.r1t);
+    std::swap(b.r2w, b.r2t);
+    std::swap(s.dw, s.dt);
+    s.res_w = res_t;
+  } else {
+    acc_ssn = 0;
+    copy_state(p, b, s.dw, s.dv);
+    s.res_w = s.res_v;
+  }
+  rec.iteration = k;
+  rec.res_accepted = s.res_w;
+  rec.res_ssn = res_t;
+  rec.res_eg = s.res_v;
+  rec.accepted_ssn = acc_ssn;
+  rec.theta = s.theta;
+  rec.mu = mu;
+  rec.cg_iters = st.cg_iters;
+  rec.criterion_met = st.met;
+  rec.crit_lhs = st.lhs;
+  rec.crit_rhs = st.rhs;
+  rec.eg_ms = eg_ms;
+  rec.newton_ms = newton_ms;
+  rec.cg_ms = st.cg_ms;
+  rec.resid_ms = resid_ms;
+  KOT_CUDA(cudaStreamSynchronize(p.st));
+  rec.step_ms = ms_since(t_it);
+  rec.n_pos = s.dw.k;
+  rec.attempts = st.attempts;
+  s.theta = theta_next;
+  return true;
+}
+
+static void init_state(Problem& p, LoopState& s) {
+  Bufs& b = p.bufs();
+  const int n = p.n;
+  const long nn = (long)n * n;
+  s.dw = Decomp{b.Pw, b.valw, 0};
+  s.dv = Decomp{b.Pv, b.valv, 0};
+  s.dt = Decomp{b.Pt, b.valt, 0};
+  for (double* v : {b.gw, b.gv}) KOT_CUDA(cudaMemsetAsync(v, 0, sizeof(double) * n, p.st));
+  for (double* m : {b.Xw, b.Xv}) KOT_CUDA(cudaMemsetAsync(m, 0, sizeof(double) * nn, p.st));
+}
+
+SolveResult solve(Problem& p, const SolverCfg& cfg, IterCallback cb, void* user, double* gamma_out, double* x_out,
+                  IterRecord* trace, int trace_cap, bool pure_eg) {
+  kot_require(cfg.residual_tol > 0.0, KOT_EINVAL, "residual_tol must be positive");
+  kot_require(cfg.max_iter >= 1, KOT_EINVAL, "max_iter must be >= 1");
+  kot_require(cfg.safeguard_every >= 1, KOT_EINVAL, "safeguard_every must be >= 1");
+  kot_require(cfg.eg_stepsize > 0.0, KOT_EINVAL, "stepsize must be positive");
+  const auto t_start = clk::now();
+  Bufs& b = p.bufs();
+  const int n = p.n;
+  const long nn = (long)n * n;
+  LoopState s;
+  init_state(p, s);
+  SolveResult out{KOT_OK, 0, 0, 0.0, NAN, 0.0};
+  HostProbe hp;
+  // initial residual at the zero pair (solver.py:129-139)
+  double res0 = pure_eg ? residual_parts(p, b.gv, b.Xv, b.r1v, b.r2v, s.dv)
+                        : residual_parts(p, b.gw, b.Xw, b.r1w, b.r2w, s.dw);
+  s.res_w = s.res_v = res0;
+  s.theta = cfg.theta0;
+  int k = 0;
+  bool conv = res0 <= cfg.residual_tol;
+  bool finite = std::isfinite(res0);
+  while (finite && !conv && k < cfg.max_iter) {
+    IterRecord rec{};
+    if (pure_eg) {
+      const auto t_it = clk::now();
+      auto t0 = clk::now();
+      eg_step(p, b.gv, b.Xv, cfg.eg_stepsize, b.gv, b.Xv);
+      KOT_CUDA(cudaStreamSynchronize(p.st));
+      const double eg_ms = ms_since(t0);
+      t0 = clk::now();
+      s.res_v = residual_parts(p, b.gv, b.Xv, b.r1v, b.r2v, s.dv);
+      const double resid_ms = ms_since(t0);
+      if (!std::isfinite(s.res_v)) {
+        finite = false;
+        break;
+      }
+      rec = IterRecord{k, s.res_v, NAN, s.res_v, 0, NAN, NAN, 0, 0, NAN, NAN, eg_ms, 0.0, 0.0, resid_ms,
+                       ms_since(t_it), s.dv.k, 0};
+      s.res_w = s.res_v;
+    } else if (!loop_body(p, cfg, s, k, rec, cb, user, &hp)) {
+      finite = false;
+      break;
+    }
+    if (trace && k < trace_cap) trace[k] = rec;
+    ++k;
+    conv = s.res_w <= cfg.residual_tol;
+  }
+  out.iterations = k;
+  out.converged = conv ? 1 : 0;
+  out.residual_norm = s.res_w;
+  if (!finite) {
+    out.status = KOT_ENUMERICS;
+    return out;
+  }
+  const double* gfin = pure_eg ? b.gv : b.gw;
+  const double* xfin = pure_eg ? b.Xv : b.Xw;
+  if (p.has_embed) out.ot_estimate = (p.q_sq - dev_dot(p, gfin, p.embed, n)) / (2.0 * p.l2);
+  if (gamma_out) KOT_CUDA(cudaMemcpyAsync(gamma_out, gfin, sizeof(double) * n, cudaMemcpyDeviceToHost, p.st));
+  if (x_out) KOT_CUDA(cudaMemcpyAsync(x_out, xfin, sizeof(double) * nn, cudaMemcpyDeviceToHost, p.st));
+  KOT_CUDA(cudaStreamSynchronize(p.st));
+  out.total_ms = ms_since(t_start);
+  return out;
+}
+
+IterRecord iterate_once(Problem& p, const SolverCfg& cfg, const ReplayIn& in, ReplayOut& out) {
+  Bufs& b = p.bufs();
+  const int n = p.n;
+  const long nn = (long)n * n;
+  LoopState s;
+  init_state(p, s);
+  KOT_CUDA(cudaMemcpyAsync(b.gw, in.wg, sizeof(double) * n, cudaMemcpyHostToDevice, p.st));
+  KOT_CUDA(cudaMemcpyAsync(b.Xw, in.wx, sizeof(double) * nn, cudaMemcpyHostToDevice, p.st));
+  KOT_CUDA(cudaMemcpyAsync(b.gv, in.vg, sizeof(double) * n, cudaMemcpyHostToDevice, p.st));
+  KOT_CUDA(cudaMemcpyAsync(b.Xv, in.vx, sizeof(double) * nn, cudaMemcpyHostToDevice, p.st));
+  s.res_w = residual_parts(p, b.gw, b.Xw, b.r1w, b.r2w, s.dw);
+  s.res_v = s.res_w;
+  if (in.k % cfg.safeguard_every != 0) s.res_v = residual_parts(p, b.gv, b.Xv, b.r1v, b.r2v, s.dv);
+  s.theta = in.theta;
+  IterRecord rec{};
+  HostProbe hp;
+  if (!loop_body(p, cfg, s, in.k, rec, nullptr, nullptr, &hp))
+    throw KotError(KOT_ENUMERICS, "non-finite residual in solver iterate");
+  KOT_CUDA(cudaMemcpyAsync(out.wg, b.gw, sizeof(double) * n, cudaMemcpyDeviceToHost, p.st));
+  KOT_CUDA(cudaMemcpyAsync(out.wx, b.Xw, sizeof(double) * nn, cudaMemcpyDeviceToHost, p.st));
+  KOT_CUDA(cudaMemcpyAsync(out.vg, b.gv, sizeof(double) * n, cudaMemcpyDeviceToHost, p.st));
+  KOT_CUDA(cudaMemcpyAsync(out.vx, b.Xv, sizeof(double) * nn, cudaMemcpyDeviceToHost, p.st));
+  KOT_CUDA(cudaStreamSynchronize(p.st));
+  out.theta = s.theta;
+  return rec;
+}
+
+}  // namespace kot

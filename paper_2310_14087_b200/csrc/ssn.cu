@@ -1,0 +1,478 @@
+// SSN operators on device (north-star items 3, 5, 6).
+//
+// Reference map (pkg/src/kot/...):
+//   phi_forward  problem.py:172-177  → DMMA GEMM R·X (triangular K-skip) with a
+//                                       fused row-dot epilogue against R
+//   phi_adjoint  problem.py:180-185  → DMMA Rᵀdiag(γ)R, one triangle + mirror,
+//                                       with the Z / EG argument fused in
+//   proj         psdcone.py:52-59    → DMMA P_α diag(σ_α) P_αᵀ + mirror, X − Π fused
+//   𝒯 / M        psdcone.py:94-151   → low-rank 4-GEMM chain, ξ/η computed from σ
+//                                       in the epilogue (no k×(ℓ−k) coefficient matrix)
+//   residual     problem.py:204-214,  eg_step eg.py:34-41
+//   CG           linalg.py:117-162   → fused single-CTA update kernel
+//   newton       newton.py:116-195
+#include <chrono>
+#include <cmath>
+
+#include "gemm.cuh"
+#include "ssn.cuh"
+
+namespace kot {
+
+// ---------------------------------------------------------------- Problem
+
+double* Problem::alloc(long count) {
+  double* p = nullptr;
+  KOT_CUDA(cudaMalloc(&p, std::max(count, 1L) * sizeof(double)));
+  owned.push_back(p);
+  return p;
+}
+
+void Problem::init_scratch() {
+  const long nn = (long)n * n;
+  const int tiles = ceil_div(n, GB_N);
+  partial = alloc((long)tiles * n);
+  M1 = alloc(nn);
+  M2 = alloc(nn);
+  M3 = alloc(nn);
+  M4 = alloc(nn);
+  M5 = alloc(nn);
+  red = alloc(512 * 16);
+  dsc = alloc(64);
+  KOT_CUDA(cudaMallocHost(&hsc, 64 * sizeof(double)));
+  KOT_CUDA(cudaMalloc(&dk, 16 * sizeof(int)));
+  dflag = dk + 8;
+  KOT_CUDA(cudaMallocHost(&hk, 16 * sizeof(int)));
+  eig.reset(new EigWork(n));
+}
+
+Problem::~Problem() {
+  if (st) cudaStreamSynchronize(st);
+  eig.reset();
+  for (double* p : owned) cudaFree(p);
+  if (hsc) cudaFreeHost(hsc);
+  if (dk) cudaFree(dk);
+  if (hk) cudaFreeHost(hk);
+  if (st) cudaStreamDestroy(st);
+}
+
+static std::unique_ptr<Problem> make_problem(int n, int device) {
+  kot_require(n >= 1, KOT_EINVAL, "problem order must be >= 1");
+  KOT_CUDA(cudaSetDevice(device));
+  std::unique_ptr<Problem> p(new Problem());
+  p->n = n;
+  p->device = device;
+  KOT_CUDA(cudaStreamCreateWithFlags(&p->st, cudaStreamNonBlocking));
+  const long nn = (long)n * n;
+  p->Q = p->alloc(nn);
+  p->z = p->alloc(n);
+  p->R = p->alloc(nn);
+  p->embed = p->alloc(n);
+  p->init_scratch();
+  return p;
+}
+
+__global__ void sym_copy_kernel(const double* __restrict__ a, double* __restrict__ out, int n) {
+  const long total = (long)n * n;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / n), c = (int)(i % n);
+    out[i] = 0.5 * (a[i] + a[(long)c * n + r]);  // problem.py:112 q_mat = symmetrize(q)
+  }
+}
+
+int ew_grid(long count) { return (int)std::min<long>(ceil_div(count, 256), 4L * kNumSMs * 8); }
+
+std::unique_ptr<Problem> problem_from_host(const double* q, const double* z, double q_sq, const double* r,
+                                           const double* embed, int n, double l1, double l2, double jitter,
+                                           int device) {
+  kot_require(l1 > 0.0 && l2 > 0.0, KOT_EINVAL, "regularization parameters must be positive");
+  auto p = make_problem(n, device);
+  const long nn = (long)n * n;
+  p->l1 = l1;
+  p->l2 = l2;
+  p->q_sq = q_sq;
+  p->jitter = jitter;
+  KOT_CUDA(cudaMemcpyAsync(p->M1, q, nn * sizeof(double), cudaMemcpyHostToDevice, p->st));
+  sym_copy_kernel<<<ew_grid(nn), 256, 0, p->st>>>(p->M1, p->Q, n);
+  KOT_LAUNCH_CHECK();
+  KOT_CUDA(cudaMemcpyAsync(p->z, z, n * sizeof(double), cudaMemcpyHostToDevice, p->st));
+  KOT_CUDA(cudaMemcpyAsync(p->R, r, nn * sizeof(double), cudaMemcpyHostToDevice, p->st));
+  if (embed) {
+    KOT_CUDA(cudaMemcpyAsync(p->embed, embed, n * sizeof(double), cudaMemcpyHostToDevice, p->st));
+    p->has_embed = true;
+  }
+  KOT_CUDA(cudaStreamSynchronize(p->st));
+  return p;
+}
+
+std::unique_ptr<Problem> problem_assemble(const double* xs, int nx, const double* ys, int ny, const double* xt,
+                                          const double* yt, int l, int d, double bw, double l1, double l2,
+                                          int device) {
+  kot_require(l1 > 0.0 && l2 > 0.0, KOT_EINVAL, "lambda1 and lambda2 must be positive");
+  kot_require(bw > 0.0, KOT_EINVAL, "bandwidth_sq must be positive");
+  kot_require(nx >= 1 && ny >= 1, KOT_EINVAL, "sample set is empty");
+  auto p = make_problem(l, device);
+  p->l1 = l1;
+  p->l2 = l2;
+  const long nn = (long)l * l;
+  // host → device staging of the raw points (in M3; freed scratch)
+  double* dxs = p->alloc((long)nx * d);
+  double* dys = p->alloc((long)ny * d);
+  double* dxt = p->alloc((long)l * d);
+  double* dyt = p->alloc((long)l * d);
+  KOT_CUDA(cudaMemcpyAsync(dxs, xs, sizeof(double) * nx * d, cudaMemcpyHostToDevice, p->st));
+  KOT_CUDA(cudaMemcpyAsync(dys, ys, sizeof(double) * ny * d, cudaMemcpyHostToDevice, p->st));
+  KOT_CUDA(cudaMemcpyAsync(dxt, xt, sizeof(double) * l * d, cudaMemcpyHostToDevice, p->st));
+  KOT_CUDA(cudaMemcpyAsync(dyt, yt, sizeof(double) * l * d, cudaMemcpyHostToDevice, p->st));
+  p->Kmat = p->alloc(nn);
+  double* scratch = p->alloc(nx + ny + 8);
+  assemble_device(dxs, nx, dys, ny, dxt, dyt, l, d, bw, l2, p->Q, p->Kmat, p->embed, p->z, p->dsc, scratch, p->st);
+  KOT_CUDA(cudaMemcpyAsync(p->hsc, p->dsc, sizeof(double), cudaMemcpyDeviceToHost, p->st));
+  KOT_CUDA(cudaStreamSynchronize(p->st));
+  p->q_sq = p->hsc[0];
+  p->has_embed = true;
+  p->jitter = cholesky_psd_device(p->Kmat, l, p->R, p->M1, p->dsc + 32, p->dflag, p->st);
+  KOT_CUDA(cudaStreamSynchronize(p->st));
+  return p;
+}
+
+void symmetrize(Problem& p, const double* a, double* out) {
+  sym_copy_kernel<<<ew_grid((long)p.n * p.n), 256, 0, p.st>>>(a, out, p.n);
+  KOT_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------- reductions
+
+__global__ void dot_partial_kernel(const double* __restrict__ a, const double* __restrict__ b, long count,
+                                   double* __restrict__ part) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x)
+    s += b ? a[i] * b[i] : a[i] * a[i];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void sum_partials_kernel(const double* __restrict__ part, int np, double* __restrict__ out, int do_sqrt) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) out[0] = do_sqrt ? sqrt(s) : s;
+}
+
+static int red_grid(long count) { return (int)std::min<long>(std::max<long>(ceil_div(count, 4096), 1), 512); }
+
+// writes into p.dsc[slot] asynchronously
+void dev_reduce(Problem& p, const double* a, const double* b, long count, int slot, bool sq) {
+  const int G = red_grid(count);
+  dot_partial_kernel<<<G, 256, 0, p.st>>>(a, b, count, p.red + 512 * slot);
+  KOT_LAUNCH_CHECK();
+  sum_partials_kernel<<<1, 256, 0, p.st>>>(p.red + 512 * slot, G, p.dsc + slot, sq ? 1 : 0);
+  KOT_LAUNCH_CHECK();
+}
+
+void fetch(Problem& p, int count) {
+  KOT_CUDA(cudaMemcpyAsync(p.hsc, p.dsc, sizeof(double) * count, cudaMemcpyDeviceToHost, p.st));
+  KOT_CUDA(cudaStreamSynchronize(p.st));
+}
+
+double dev_norm(Problem& p, const double* x, long count) {
+  dev_reduce(p, x, nullptr, count, 0, true);
+  fetch(p, 1);
+  return p.hsc[0];
+}
+
+double dev_dot(Problem& p, const double* x, const double* y, long count) {
+  dev_reduce(p, x, y, count, 0, false);
+  fetch(p, 1);
+  return p.hsc[0];
+}
+
+// ------------------------------------------------------------ elementwise
+
+__global__ void axpby_kernel(long count, double a, const double* __restrict__ x, double b,
+                             const double* __restrict__ y, double* __restrict__ out) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x) {
+    const double xv = (a == 1.0) ? x[i] : __dmul_rn(a, x[i]);
+    const double yv = y ? ((b == 1.0) ? y[i] : __dmul_rn(b, y[i])) : 0.0;
+    out[i] = __dadd_rn(xv, yv);
+  }
+}
+void axpby(Problem& p, long count, double a, const double* x, double b, const double* y, double* out) {
+  axpby_kernel<<<ew_grid(count), 256, 0, p.st>>>(count, a, x, b, y, out);
+  KOT_LAUNCH_CHECK();
+}
+
+// out = -(x / c)
+__global__ void neg_div_kernel(long count, const double* __restrict__ x, double c, double* __restrict__ out) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x)
+    out[i] = -(x[i] / c);
+}
+
+// POS:   out = G + Gᵀ
+// NONPOS: out = S/μ − (G + Gᵀ)   (mode 0, eliminator)   |  S − (G + Gᵀ)  (mode 1, Jacobian)
+__global__ void symadd_kernel(int n, const double* __restrict__ G, const double* S, int nonpos, int mode, double mu,
+                              double* out) {
+  const long total = (long)n * n;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / n), c = (int)(i % n);
+    const double g = __dadd_rn(G[i], G[(long)c * n + r]);
+    if (!nonpos)
+      out[i] = g;
+    else
+      out[i] = __dsub_rn(mode == 0 ? S[i] / mu : S[i], g);
+  }
+}
+
+// out = (a + (1+μ)·b) + c    (Jacobian bottom block + r2)
+__global__ void jac_bottom_kernel(long count, const double* __restrict__ a, const double* __restrict__ b, double mu,
+                                  const double* __restrict__ c, double* __restrict__ out) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x)
+    out[i] = __dadd_rn(__dadd_rn(a[i], __dmul_rn(1.0 + mu, b[i])), c[i]);
+}
+
+void neg_div(Problem& p, long count, const double* x, double c, double* out) {
+  neg_div_kernel<<<ew_grid(count), 256, 0, p.st>>>(count, x, c, out);
+  KOT_LAUNCH_CHECK();
+}
+
+void jac_bottom(Problem& p, long count, const double* a, const double* b, double mu, const double* c, double* out) {
+  jac_bottom_kernel<<<ew_grid(count), 256, 0, p.st>>>(count, a, b, mu, c, out);
+  KOT_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------- Φ finalize
+
+
+struct FinArgs {
+  int n, mode, tiles;
+  const double* Q;
+  const double* u;
+  const double* partial;
+  const double* z;
+  const double* r1;
+  double l2, mu;
+  double* out;
+};
+
+// warp per row: GEMV row of Q (coalesced) + fixed-order sum of the Φ partials.
+__global__ void finalize_kernel(FinArgs f) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < f.n; r += gridDim.x * warps) {
+    double qv = 0.0, ph = 0.0;
+    if (f.Q) {
+      const double* qr = f.Q + (long)r * f.n;
+      for (int c = lane; c < f.n; c += 32) qv += qr[c] * f.u[c];
+      qv = warp_sum(qv);
+    }
+    if (f.partial) {
+      for (int tn = r / GB_N + lane; tn < f.tiles; tn += 32) ph += f.partial[(long)tn * f.n + r];
+      ph = warp_sum(ph);
+    }
+    if (lane) continue;
+    const double two_l2 = 2.0 * f.l2;
+    double o;
+    switch (f.mode) {
+      case FIN_RES: o = __dsub_rn(__dsub_rn(qv, f.z[r]) / two_l2, ph); break;
+      case FIN_MATVEC: o = __dadd_rn(__dadd_rn(qv / two_l2, __dmul_rn(f.mu, f.u[r])), ph); break;
+      case FIN_A1: o = __dsub_rn(-f.r1[r], ph / (f.mu + 1.0)); break;
+      case FIN_JTOP:
+        o = __dadd_rn(__dsub_rn(__dadd_rn(qv / two_l2, __dmul_rn(f.mu, f.u[r])), ph), f.r1[r]);
+        break;
+      case FIN_PHI: o = ph; break;
+      case FIN_GRAD: o = __dsub_rn(qv, f.z[r]) / two_l2; break;
+      default: o = qv; break;
+    }
+    f.out[r] = o;
+  }
+}
+
+void finalize(Problem& p, int mode, const double* u, bool with_phi, const double* r1, double mu,
+                     double* out) {
+  FinArgs f;
+  f.n = p.n;
+  f.mode = mode;
+  f.tiles = ceil_div(p.n, GB_N);
+  const bool need_q = (mode == FIN_RES || mode == FIN_MATVEC || mode == FIN_JTOP || mode == FIN_GRAD || mode == FIN_QV);
+  f.Q = need_q ? p.Q : nullptr;
+  f.u = u;
+  f.partial = with_phi ? p.partial : nullptr;
+  f.z = p.z;
+  f.r1 = r1;
+  f.l2 = p.l2;
+  f.mu = mu;
+  f.out = out;
+  finalize_kernel<<<std::min(ceil_div(p.n, 8), 8 * kNumSMs), 256, 0, p.st>>>(f);
+  KOT_LAUNCH_CHECK();
+}
+
+// Φ(X) row-dot partials: tile (tm, tn>=tm) of R·X contracted against R.
+void phi_partials(Problem& p, const double* X) {
+  const int n = p.n;
+  GemmShape s = make_shape(n, n, n, p.R, n, X, n);
+  s.kb_m = 1;       // R[m][k] = 0 for k < m
+  s.sym_tiles = 1;  // R[r][c] = 0 for c < r ⇒ tiles tn < tm contribute nothing
+  EpiRowDot epi{p.R, n, p.partial, n};
+  gemm_launch<false, false>(s, epi, p.st);
+}
+
+void phi_forward(Problem& p, const double* X, double* out) {
+  phi_partials(p, X);
+  finalize(p, FIN_PHI, nullptr, true, nullptr, 0.0, out);
+}
+
+// out = beta·X + alpha·(Rᵀdiag(γ)R + diag·I), one triangle + mirror.
+void phi_adjoint_ex(Problem& p, const double* g, double* out, double alpha, const double* X, double beta,
+                           double diag) {
+  const int n = p.n;
+  GemmShape s = make_shape(n, n, n, p.R, n, p.R, n);
+  s.kscale = g;
+  s.ke_m = 1;
+  s.ke_n = 1;
+  s.sym_tiles = 1;
+  EpiSymMirror epi{out, n, alpha, X, beta, diag};
+  gemm_launch<true, false>(s, epi, p.st);
+}
+
+void phi_adjoint(Problem& p, const double* g, double* out) { phi_adjoint_ex(p, g, out, 1.0, nullptr, 0.0, 0.0); }
+
+void eigh(Problem& p, const double* Z, Decomp& dc) {
+  syevd_device(Z, p.n, dc.P, dc.vals, p.dk, *p.eig, p.st);
+  KOT_CUDA(cudaMemcpyAsync(p.hk, p.dk, sizeof(int), cudaMemcpyDeviceToHost, p.st));
+  KOT_CUDA(cudaStreamSynchronize(p.st));
+  dc.k = p.hk[0];
+}
+
+void proj(Problem& p, const Decomp& dc, const double* X, double* out) {
+  const int n = p.n;
+  GemmShape s = make_shape(n, n, dc.k, dc.P, n, dc.P, n);
+  s.kscale = dc.vals;
+  s.sym_tiles = 1;
+  EpiSymMirror epi = X ? EpiSymMirror{out, n, -1.0, X, 1.0, 0.0} : EpiSymMirror{out, n, 1.0, nullptr, 0.0, 0.0};
+  gemm_launch<false, true>(s, epi, p.st);
+}
+
+// Ĉ = W∘C on the α (pos) or ᾱ rows; ξ/η computed from σ (psdcone.py:67-80,103-110).
+struct EpiSpectral {
+  static constexpr bool kRowDot = false;
+  double* C;
+  long ldc;
+  const double* vals;
+  int k, pos, mode;
+  double mu;
+  __device__ void store(int r, int c, double v) const {
+    double o;
+    if (pos) {
+      if (c < k) {
+        o = (mode == 0) ? v / (2.0 * mu) : v * 0.5;
+      } else {
+        const double sa = vals[r], sb = vals[c];
+        const double eta = sa / (sa - sb);
+        o = (mode == 0) ? (eta / (mu + 1.0 - eta)) * v : eta * v;
+      }
+    } else {
+      if (c >= k) {
+        o = (mode == 0) ? v / (2.0 * mu) : v * 0.5;
+      } else {
+        const double sa = vals[c], sb = vals[k + r];
+        const double eta = sa / (sa - sb);
+        o = (mode == 0) ? (1.0 / mu - eta / (mu + 1.0 - eta)) * v : (1.0 - eta) * v;
+      }
+    }
+    C[(long)r * ldc + c] = o;
+  }
+  __device__ double rowdot_weight(int, int) const { return 0; }
+  __device__ void rowdot_store(int, int, double) const {}
+};
+
+void spectral_filter(Problem& p, const Decomp& dc, const double* S, double* out, double mu, int mode,
+                     int force_path) {
+  const int n = p.n, k = dc.k;
+  const bool pos = (force_path < 0) ? (k <= n - k) : (force_path == 0);
+  const int ks = pos ? k : n - k;
+  const double* Psub = pos ? dc.P : dc.P + k;
+  double* U = p.M3;
+  double* C = p.M4;
+  double* H = p.M3;
+  double* G = p.M5;
+  if (ks > 0) {
+    {  // U = P_subᵀ S
+      GemmShape s = make_shape(ks, n, n, Psub, n, S, n);
+      gemm_launch<true, false>(s, EpiAxpby{U, n, 1.0, 0.0}, p.st);
+    }
+    {  // Ĉ = W ∘ (U P)
+      GemmShape s = make_shape(ks, n, n, U, n, dc.P, n);
+      gemm_launch<false, false>(s, EpiSpectral{C, n, dc.vals, k, pos ? 1 : 0, mode, mu}, p.st);
+    }
+    {  // H = Ĉ Pᵀ
+      GemmShape s = make_shape(ks, n, n, C, n, dc.P, n);
+      gemm_launch<false, true>(s, EpiAxpby{H, n, 1.0, 0.0}, p.st);
+    }
+  }
+  {  // G = P_sub H   (zeros when ks == 0)
+    GemmShape s = make_shape(n, n, ks, Psub, n, H, n);
+    gemm_launch<false, false>(s, EpiAxpby{G, n, 1.0, 0.0}, p.st);
+  }
+  symadd_kernel<<<ew_grid((long)n * n), 256, 0, p.st>>>(n, G, S, pos ? 0 : 1, mode, mu, out);
+  KOT_LAUNCH_CHECK();
+}
+
+double residual_parts(Problem& p, const double* g, const double* X, double* r1, double* r2, Decomp& dc) {
+  const int n = p.n;
+  const long nn = (long)n * n;
+  phi_partials(p, X);
+  finalize(p, FIN_RES, g, true, nullptr, 0.0, r1);
+  // Z = X − (Φ*(γ) + λ₁ I)
+  phi_adjoint_ex(p, g, p.M1, -1.0, X, 1.0, p.l1);
+  eigh(p, p.M1, dc);
+  proj(p, dc, X, r2);
+  dev_reduce(p, r1, nullptr, n, 0, true);
+  dev_reduce(p, r2, nullptr, nn, 1, true);
+  fetch(p, 2);
+  return p.hsc[0] + p.hsc[1];
+}
+
+void middle_operator(Problem& p, const Decomp& dc, double mu, const double* v, double* out) {
+  phi_adjoint(p, v, p.M1);
+  spectral_filter(p, dc, p.M1, p.M2, mu, 0);
+  phi_partials(p, p.M2);
+  finalize(p, FIN_MATVEC, v, true, nullptr, mu, out);
+}
+
+void eg_step(Problem& p, const double* g, const double* X, double s, double* g_out, double* X_out) {
+  Bufs& b = p.bufs();
+  const int n = p.n;
+  Decomp dc{b.Pe, b.vale, 0};
+  // field at v: g_vec = ∇f(γ) − Φ(X); g_mat = Φ*(γ) + λ₁I   (eg.py:27-31)
+  phi_partials(p, X);
+  finalize(p, FIN_RES, g, true, nullptr, 0.0, b.e1);
+  axpby(p, n, 1.0, g, -s, b.e1, b.e2);            // γ½ = γ − s g_vec
+  phi_adjoint_ex(p, g, p.M1, -s, X, 1.0, p.l1);     // X − s (Φ*(γ) + λ₁I)
+  eigh(p, p.M1, dc);
+  proj(p, dc, nullptr, b.Xh);                       // X½ = Π(·)
+  phi_partials(p, b.Xh);
+  finalize(p, FIN_RES, b.e2, true, nullptr, 0.0, b.e1);
+  phi_adjoint_ex(p, b.e2, p.M1, -s, X, 1.0, p.l1);  // X − s (Φ*(γ½) + λ₁I)
+  axpby(p, n, 1.0, g, -s, b.e1, g_out);             // γ − s g_vec(½)
+  eigh(p, p.M1, dc);
+  proj(p, dc, nullptr, X_out);
+}
+
+Bufs& Problem::bufs() {
+  if (!bufs_) {
+    bufs_.reset(new Bufs());
+    Bufs& b = *bufs_;
+    const long nn = (long)n * n;
+    for (double** m : {&b.Xw, &b.Xv, &b.Xt, &b.r2w, &b.r2v, &b.r2t, &b.Pw, &b.Pv, &b.Pt, &b.Pe, &b.Xh, &b.dX,
+                       &b.filt, &b.a2t})
+      *m = alloc(nn);
+    for (double** v : {&b.gw, &b.gv, &b.gt, &b.r1w, &b.r1v, &b.r1t, &b.valw, &b.valv, &b.valt, &b.vale, &b.dg,
+                       &b.a1, &b.rhs, &b.sol, &b.corr, &b.cx, &b.cr, &b.cp, &b.cap, &b.e1, &b.e2, &b.e3})
+      *v = alloc(n);
+  }
+  return *bufs_;
+}
+
+}  // namespace kot

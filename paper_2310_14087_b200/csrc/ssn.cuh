@@ -1,0 +1,138 @@
+// Device-resident SSN problem and operators (reference problem.py, psdcone.py,
+// newton.py, eg.py, solver.py).
+#pragma once
+#include <memory>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace kot {
+
+struct Decomp {
+  double* P = nullptr;     // n×n, columns = eigenvectors (descending)
+  double* vals = nullptr;  // n
+  int k = 0;               // #(σ > 0)
+};
+
+struct SolverCfg {
+  double tau, kappa, alpha1, alpha2, beta0, beta1, beta2, theta_min, theta_max, theta0;
+  int cg_max, cg_restarts;
+  double cg_tol;
+  int has_cg_tol;
+  double eg_stepsize, residual_tol;
+  int max_iter, safeguard_every;
+};
+
+struct IterRecord {
+  int iteration;
+  double res_accepted, res_ssn, res_eg;
+  int accepted_ssn;
+  double theta, mu;
+  int cg_iters, criterion_met;
+  double crit_lhs, crit_rhs, eg_ms, newton_ms, cg_ms, resid_ms, step_ms;
+  int n_pos, attempts;
+};
+
+// Solver-owned device buffers (allocated on first use).
+struct Bufs {
+  double *Xw, *Xv, *Xt, *r2w, *r2v, *r2t, *Pw, *Pv, *Pt, *Pe, *Xh, *dX, *filt, *a2t;  // n×n
+  double *gw, *gv, *gt, *r1w, *r1v, *r1t, *valw, *valv, *valt, *vale, *dg, *a1, *rhs, *sol, *corr;  // n
+  double *cx, *cr, *cp, *cap, *e1, *e2, *e3;  // n
+};
+
+struct Problem {
+  int n = 0;
+  int device = 0;
+  double l1 = 0, l2 = 0, q_sq = 0, jitter = 0;
+  bool has_embed = false;
+  cudaStream_t st = nullptr;
+  // instance data (device)
+  double *Q = nullptr, *z = nullptr, *R = nullptr, *embed = nullptr, *Kmat = nullptr;
+  // scratch
+  std::unique_ptr<EigWork> eig;
+  std::vector<double*> owned;
+  double* partial = nullptr;  // rowdot partials [tiles][n]
+  double *M1 = nullptr, *M2 = nullptr, *M3 = nullptr, *M4 = nullptr, *M5 = nullptr;  // n×n temps
+  double* red = nullptr;   // reduction partials
+  double* dsc = nullptr;   // device scalars
+  double* hsc = nullptr;   // pinned host scalars
+  int* dk = nullptr;
+  int* dflag = nullptr;
+  int* hk = nullptr;       // pinned
+
+  std::unique_ptr<Bufs> bufs_;
+  Bufs& bufs();
+  double* alloc(long count);
+  void init_scratch();
+  ~Problem();
+};
+
+std::unique_ptr<Problem> problem_from_host(const double* q, const double* z, double q_sq, const double* r,
+                                           const double* embed, int n, double l1, double l2, double jitter, int device);
+std::unique_ptr<Problem> problem_assemble(const double* xs, int nx, const double* ys, int ny, const double* xt,
+                                          const double* yt, int l, int d, double bw, double l1, double l2, int device);
+
+// ---- operators (device pointers in/out, all on p.st)
+void phi_forward(Problem& p, const double* X, double* out);
+void phi_adjoint(Problem& p, const double* g, double* out);
+void eigh(Problem& p, const double* Z, Decomp& dc);
+void proj(Problem& p, const Decomp& dc, const double* X, double* out);  // out = X − Π (X!=null) or Π
+// mode 0: eliminator 𝒯 with μ; mode 1: projection Jacobian M. force_path: -1 auto, 0 POS, 1 NONPOS.
+void spectral_filter(Problem& p, const Decomp& dc, const double* S, double* out, double mu, int mode,
+                     int force_path = -1);
+double residual_parts(Problem& p, const double* g, const double* X, double* r1, double* r2, Decomp& dc);
+void middle_operator(Problem& p, const Decomp& dc, double mu, const double* v, double* out);
+void eg_step(Problem& p, const double* g, const double* X, double s, double* g_out, double* X_out);
+
+struct NewtonOut {
+  int cg_iters, met, attempts;
+  double lhs, rhs, cg_ms;
+};
+NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, double res_norm, const Decomp& dc,
+                           double mu, const SolverCfg& cfg, double* dg, double* dX);
+
+// internal helpers shared with solver.cu
+enum FinMode { FIN_RES = 0, FIN_MATVEC = 1, FIN_A1 = 2, FIN_JTOP = 3, FIN_PHI = 4, FIN_GRAD = 5, FIN_QV = 6 };
+void dev_reduce(Problem& p, const double* a, const double* b, long count, int slot, bool sq);
+void fetch(Problem& p, int count);
+void axpby(Problem& p, long count, double a, const double* x, double b, const double* y, double* out);
+void finalize(Problem& p, int mode, const double* u, bool with_phi, const double* r1, double mu, double* out);
+void phi_partials(Problem& p, const double* X);
+void phi_adjoint_ex(Problem& p, const double* g, double* out, double alpha, const double* X, double beta, double diag);
+int ew_grid(long count);
+void symmetrize(Problem& p, const double* a, double* out);  // 0.5 (a + aᵀ)
+void neg_div(Problem& p, long count, const double* x, double c, double* out);               // out = −(x/c)
+void jac_bottom(Problem& p, long count, const double* a, const double* b, double mu, const double* c,
+                double* out);                                                                 // (a + (1+μ)b) + c
+
+// host-side reductions (synchronising)
+double dev_norm(Problem& p, const double* x, long count);
+double dev_dot(Problem& p, const double* x, const double* y, long count);
+
+// ---- solver
+typedef void (*IterCallback)(void* user, int iteration, const double* w_gamma, const double* w_x,
+                             const double* r_gamma, const double* r_x, double mu, double theta,
+                             const double* dw_gamma, const double* dw_x, int criterion_met);
+struct SolveResult {
+  int status;  // KOT_OK or KOT_ENUMERICS
+  int converged;
+  int iterations;
+  double residual_norm;
+  double ot_estimate;
+  double total_ms;
+};
+SolveResult solve(Problem& p, const SolverCfg& cfg, IterCallback cb, void* user, double* gamma_out, double* x_out,
+                  IterRecord* trace, int trace_cap, bool pure_eg);
+
+struct ReplayIn {
+  const double *wg, *wx, *vg, *vx;
+  double theta;
+  int k;
+};
+struct ReplayOut {
+  double *wg, *wx, *vg, *vx;
+  double theta;
+};
+IterRecord iterate_once(Problem& p, const SolverCfg& cfg, const ReplayIn& in, ReplayOut& out);
+
+}  // namespace kot

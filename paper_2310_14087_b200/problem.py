@@ -1,0 +1,248 @@
+"""Dual instance, residual map and Jacobian (mirror of reference ``kot.problem``).
+
+Reference: ``pkg/src/kot/problem.py``.  ``ProblemData`` keeps the
+reference's host fields (NumPy arrays) and, lazily, a device-resident copy
+(``kot_problem`` handle) that every operator and ``solve`` run against;
+``assemble`` builds the instance on the GPU and keeps that handle.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from paper_2310_14087_b200 import _lib
+from paper_2310_14087_b200.kernels import KernelSpec, SampleSet
+from paper_2310_14087_b200.linalg import SpectralDecomp, symmetrize
+
+
+@dataclass(frozen=True)
+class FillingPoints:
+    """Paired grid points at which the transport equality is sampled (problem.py:25-42)."""
+
+    x_tilde: np.ndarray
+    y_tilde: np.ndarray
+
+    def __post_init__(self) -> None:
+        x = np.atleast_2d(np.asarray(self.x_tilde, dtype=float))
+        y = np.atleast_2d(np.asarray(self.y_tilde, dtype=float))
+        if x.shape != y.shape or x.shape[0] < 1:
+            raise ValueError("x_tilde and y_tilde must have equal shape (n, d), n >= 1")
+        object.__setattr__(self, "x_tilde", x)
+        object.__setattr__(self, "y_tilde", y)
+
+    @property
+    def count(self) -> int:
+        return self.x_tilde.shape[0]
+
+
+@dataclass
+class IteratePair:
+    """Solver state w = (gamma, X); pair norm ||γ||₂ + ||X||_F (problem.py:45-83)."""
+
+    gamma: np.ndarray
+    x_mat: np.ndarray
+
+    def norm(self) -> float:
+        return float(np.linalg.norm(self.gamma) + np.linalg.norm(self.x_mat))
+
+    def dot(self, other: "IteratePair") -> float:
+        return float(self.gamma @ other.gamma + np.sum(self.x_mat * other.x_mat))
+
+    def copy(self) -> "IteratePair":
+        return IteratePair(self.gamma.copy(), self.x_mat.copy())
+
+    def __add__(self, other: "IteratePair") -> "IteratePair":
+        return IteratePair(self.gamma + other.gamma, self.x_mat + other.x_mat)
+
+    def __sub__(self, other: "IteratePair") -> "IteratePair":
+        return IteratePair(self.gamma - other.gamma, self.x_mat - other.x_mat)
+
+    def __mul__(self, c: float) -> "IteratePair":
+        return IteratePair(c * self.gamma, c * self.x_mat)
+
+    __rmul__ = __mul__
+
+    def is_finite(self) -> bool:
+        return bool(np.all(np.isfinite(self.gamma)) and np.all(np.isfinite(self.x_mat)))
+
+
+def zero_pair(n: int) -> IteratePair:
+    return IteratePair(np.zeros(n), np.zeros((n, n)))
+
+
+class DeviceProblem:
+    """Owns a ``kot_problem*`` (device-resident Q, z, R, embed + solver workspace)."""
+
+    def __init__(self, handle: int, device: int):
+        self.handle = C.c_void_p(handle)
+        self.device = device
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.lib().kot_problem_destroy(self.handle)
+                self.handle = C.c_void_p(0)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+@dataclass(eq=False)
+class ProblemData:
+    """Assembled dual instance (problem.py:86-123); R.T R = K + jitter I, rows of R are features."""
+
+    q_mat: np.ndarray
+    z: np.ndarray
+    q_sq: float
+    chol_upper: np.ndarray
+    lambda1: float
+    lambda2: float
+    embed_sum: np.ndarray | None = None
+    filling: FillingPoints | None = None
+    spec_x: KernelSpec | None = None
+    spec_y: KernelSpec | None = None
+    spec_xy: KernelSpec | None = None
+    jitter: float = 0.0
+    _dev: DeviceProblem | None = field(default=None, repr=False)
+    _kmat: np.ndarray | None = field(default=None, repr=False)
+
+    def __post_init__(self) -> None:
+        self.q_mat = symmetrize(np.asarray(self.q_mat, dtype=float))
+        self.z = np.asarray(self.z, dtype=float)
+        self.chol_upper = np.asarray(self.chol_upper, dtype=float)
+        n = self.q_mat.shape[0]
+        if self.z.shape != (n,) or self.chol_upper.shape != (n, n):
+            raise ValueError("inconsistent instance dimensions")
+        if self.lambda1 <= 0.0 or self.lambda2 <= 0.0:
+            raise ValueError("regularization parameters must be positive")
+
+    @property
+    def n(self) -> int:
+        return self.z.shape[0]
+
+    def device_problem(self, device: int | None = None) -> DeviceProblem:
+        """Upload (once) and return the device-resident copy of this instance."""
+        dev = _lib.default_device() if device is None else device
+        if self._dev is None or self._dev.device != dev:
+            h = C.c_void_p(0)
+            emb = None if self.embed_sum is None else _lib.f64(self.embed_sum)
+            q, z, r = _lib.f64(self.q_mat), _lib.f64(self.z), _lib.f64(self.chol_upper)
+            _lib.check(_lib.lib().kot_problem_create(
+                _lib.ptr(q), _lib.ptr(z), float(self.q_sq), _lib.ptr(r), _lib.ptr(emb), self.n,
+                float(self.lambda1), float(self.lambda2), float(self.jitter), dev, C.byref(h)))
+            self._dev = DeviceProblem(h.value, dev)
+        return self._dev
+
+    def pair_gram(self) -> np.ndarray | None:
+        """The pair-kernel Gram K (only for instances built by ``assemble``)."""
+        return self._kmat
+
+
+def build_kernel_specs(dim: int, bandwidth_sq: float) -> tuple[KernelSpec, KernelSpec, KernelSpec]:
+    """One bandwidth, three kernels: marginals on R^d, pairs on R^{2d} (problem.py:126-132)."""
+    return (KernelSpec(bandwidth_sq, dim), KernelSpec(bandwidth_sq, dim), KernelSpec(bandwidth_sq, 2 * dim))
+
+
+def assemble(samples_mu: SampleSet, samples_nu: SampleSet, filling: FillingPoints, lambda1: float,
+             lambda2: float, spec_x: KernelSpec, spec_y: KernelSpec, spec_xy: KernelSpec,
+             device: int | None = None) -> ProblemData:
+    """Build the dual instance on the GPU (problem.py:135-169)."""
+    if lambda1 <= 0.0 or lambda2 <= 0.0:
+        raise ValueError("lambda1 and lambda2 must be positive")
+    if len(samples_mu) == 0 or len(samples_nu) == 0:
+        raise ValueError("sample set is empty")
+    xt, yt = _lib.f64(filling.x_tilde), _lib.f64(filling.y_tilde)
+    l, d = xt.shape
+    for spec, dim in ((spec_x, d), (spec_y, d), (spec_xy, 2 * d)):
+        if spec.input_dim != dim:
+            raise ValueError(f"kernel expects dimension {spec.input_dim}, got {dim}")
+    if not (spec_x.bandwidth_sq == spec_y.bandwidth_sq == spec_xy.bandwidth_sq):
+        raise NotImplementedError("the device assembly uses one bandwidth (build_kernel_specs)")
+    xs, ys = _lib.f64(samples_mu.points), _lib.f64(samples_nu.points)
+    if xs.shape[1] != d or ys.shape[1] != d:
+        raise ValueError("sample dimension mismatch")
+    dev = _lib.default_device() if device is None else device
+    h = C.c_void_p(0)
+    _lib.check(_lib.lib().kot_assemble(_lib.ptr(xs), xs.shape[0], _lib.ptr(ys), ys.shape[0], _lib.ptr(xt),
+                                       _lib.ptr(yt), l, d, float(spec_x.bandwidth_sq), float(lambda1),
+                                       float(lambda2), dev, C.byref(h)))
+    dp = DeviceProblem(h.value, dev)
+    q, z, r, emb, kmat = np.empty((l, l)), np.empty(l), np.empty((l, l)), np.empty(l), np.empty((l, l))
+    _lib.check(_lib.lib().kot_problem_download(dp.handle, _lib.ptr(q), _lib.ptr(z), _lib.ptr(r), _lib.ptr(emb),
+                                               _lib.ptr(kmat)))
+    qsq, jit = C.c_double(), C.c_double()
+    _lib.check(_lib.lib().kot_problem_info(dp.handle, None, C.byref(qsq), C.byref(jit), None, None, None))
+    pd = ProblemData(q_mat=q, z=z, q_sq=float(qsq.value), chol_upper=r, lambda1=lambda1, lambda2=lambda2,
+                     embed_sum=emb, filling=filling, spec_x=spec_x, spec_y=spec_y, spec_xy=spec_xy,
+                     jitter=float(jit.value))
+    pd._dev = dp
+    pd._kmat = kmat
+    return pd
+
+
+def phi_forward(pd: ProblemData, x_mat) -> np.ndarray:
+    """Φ(X)_i = r_i X r_iᵀ, r_i = row i of R (problem.py:172-177)."""
+    x = _lib.f64(x_mat)
+    if x.shape != (pd.n, pd.n):
+        raise ValueError("matrix order mismatch")
+    out = np.empty(pd.n)
+    _lib.check(_lib.lib().kot_phi_forward(pd.device_problem().handle, _lib.ptr(x), _lib.ptr(out)))
+    return out
+
+
+def phi_adjoint(pd: ProblemData, gamma) -> np.ndarray:
+    """Φ*(γ) = Rᵀ diag(γ) R, exactly symmetric (problem.py:180-185)."""
+    g = _lib.f64(gamma)
+    if g.shape != (pd.n,):
+        raise ValueError("vector length mismatch")
+    out = np.empty((pd.n, pd.n))
+    _lib.check(_lib.lib().kot_phi_adjoint(pd.device_problem().handle, _lib.ptr(g), _lib.ptr(out)))
+    return out
+
+
+def objective(pd: ProblemData, gamma) -> float:
+    """Dual quadratic objective value at γ (problem.py:192-196)."""
+    g = _lib.f64(gamma, (pd.n,))
+    out = C.c_double()
+    _lib.check(_lib.lib().kot_objective(pd.device_problem().handle, _lib.ptr(g), C.byref(out)))
+    return float(out.value)
+
+
+def ot_estimate(pd: ProblemData, gamma_hat) -> float:
+    """(q² − γ̂·embed)/(2λ₂) (problem.py:244-251)."""
+    if pd.embed_sum is None:
+        raise ValueError("instance carries no embedding sums; assemble() provides them")
+    g = _lib.f64(gamma_hat, (pd.n,))
+    out = C.c_double()
+    _lib.check(_lib.lib().kot_ot_estimate(pd.device_problem().handle, _lib.ptr(g), C.byref(out)))
+    return float(out.value)
+
+
+@dataclass(frozen=True)
+class ResidualInfo:
+    """Spectral summary of the decomposition computed inside residual_parts (device-resident)."""
+
+    eigvals: np.ndarray
+    n_pos: int
+
+
+def residual_parts(pd: ProblemData, w: IteratePair) -> tuple[IteratePair, ResidualInfo]:
+    """(r1, r2) and the spectrum of Z = sym(X) − (Φ*(γ)+λ₁I) (problem.py:204-214)."""
+    g, x = _lib.f64(w.gamma, (pd.n,)), _lib.f64(w.x_mat, (pd.n, pd.n))
+    r1, r2, ev = np.empty(pd.n), np.empty((pd.n, pd.n)), np.empty(pd.n)
+    k, res = C.c_int(), C.c_double()
+    _lib.check(_lib.lib().kot_residual_parts(pd.device_problem().handle, _lib.ptr(g), _lib.ptr(x), _lib.ptr(r1),
+                                             _lib.ptr(r2), _lib.ptr(ev), C.byref(k), C.byref(res)))
+    return IteratePair(r1, r2), ResidualInfo(ev, int(k.value))
+
+
+def residual(pd: ProblemData, w: IteratePair) -> IteratePair:
+    """Nonsmooth KKT residual (problem.py:217-219)."""
+    return residual_parts(pd, w)[0]
+
+
+__all__ = ["FillingPoints", "IteratePair", "ProblemData", "DeviceProblem", "SpectralDecomp", "zero_pair",
+           "build_kernel_specs", "assemble", "phi_forward", "phi_adjoint", "objective", "ot_estimate",
+           "residual_parts", "residual", "ResidualInfo"]

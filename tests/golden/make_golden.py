@@ -59,6 +59,8 @@ def _trace_arrays(trace, prefix):
         prefix + "mu": np.array([t.mu for t in trace]),
         prefix + "cg_iters": np.array([t.cg_iters for t in trace]),
         prefix + "criterion_met": np.array([t.criterion_met for t in trace]),
+        prefix + "crit_lhs": np.array([t.crit_lhs for t in trace]),
+        prefix + "crit_rhs": np.array([t.crit_rhs for t in trace]),
     }
 
 

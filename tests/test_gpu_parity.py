@@ -1,0 +1,363 @@
+"""GPU parity: libkotgpu (through the C ABI) vs the CPU oracle and reference golden vectors.
+
+Tolerances follow SURVEY.md §8(c) P1/P2/P3: ~1e-13 relative for Gram/Φ/Φ*,
+≤1e-11 for eigen-derived operators, ≤1e-9 for one lock-step replay
+iteration, objective ≤1e-8 / potentials ≤1e-6 at tol 1e-10.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import random_problem_arrays, random_symmetric, symmetric_with_signs
+from oracle import kot_port as O
+
+pytestmark = pytest.mark.gpu
+
+K = pytest.importorskip("paper_2310_14087_b200")
+from paper_2310_14087_b200 import linalg as GL  # noqa: E402
+from paper_2310_14087_b200 import newton as GN  # noqa: E402
+from paper_2310_14087_b200 import problem as GP  # noqa: E402
+from paper_2310_14087_b200 import psdcone as GC  # noqa: E402
+from paper_2310_14087_b200 import solver as GS  # noqa: E402
+from paper_2310_14087_b200.eg import EgConfig, eg_step  # noqa: E402
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def gpu_pd(d, p=""):
+    return GP.ProblemData(q_mat=d[p + "q"], z=d[p + "z"], q_sq=float(d[p + "q_sq"]), chol_upper=d[p + "r"],
+                          lambda1=float(d[p + "l1"]), lambda2=float(d[p + "l2"]), embed_sum=d.get(p + "embed"))
+
+
+def oracle_pd(d, p=""):
+    return O.Problem(q=d[p + "q"], z=d[p + "z"], q_sq=float(d[p + "q_sq"]), r=d[p + "r"], l1=float(d[p + "l1"]),
+                     l2=float(d[p + "l2"]), embed=d.get(p + "embed"))
+
+
+# ------------------------------------------------------------------ eigen
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 17, 31, 32, 33, 64, 65, 100, 129, 257, 500])
+def test_sym_eig_random(n):
+    rng = np.random.default_rng(n)
+    z = random_symmetric(rng, n)
+    dc = GL.sym_eig(z)
+    ref = np.sort(np.linalg.eigvalsh(z))[::-1]
+    nz = np.linalg.norm(z)
+    assert np.max(np.abs(dc.eigvals - ref)) <= 1e-13 * max(nz, 1.0)
+    p = dc.eigvecs
+    assert np.linalg.norm(p.T @ p - np.eye(n)) <= 1e-13 * n
+    assert np.linalg.norm((p * dc.eigvals) @ p.T - z) <= 1e-13 * max(nz, 1.0) * np.sqrt(n)
+    assert dc.n_pos == int(np.count_nonzero(ref > 0))
+
+
+@pytest.mark.parametrize("n,kind", [(40, "clustered"), (200, "clustered"), (300, "lowrank"), (128, "diag"),
+                                    (96, "scaled"), (1000, "signs")])
+def test_sym_eig_structured(n, kind):
+    rng = np.random.default_rng(7)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    if kind == "clustered":
+        vals = np.repeat([3.0, 1e-3, -1e-3, -2.0], n // 4)
+        vals = np.concatenate([vals, np.zeros(n - vals.size)])
+    elif kind == "lowrank":
+        vals = np.zeros(n)
+        vals[:5] = [5, 4, 3, 2, 1]
+        vals[-3:] = -1e-4
+    elif kind == "diag":
+        z = np.diag(np.linspace(-1, 1, n))
+        vals = None
+    elif kind == "scaled":
+        vals = np.logspace(-8, 8, n) * np.where(np.arange(n) % 2, 1, -1)
+    else:
+        z = symmetric_with_signs(rng, n, n // 3)
+        vals = None
+    if vals is not None:
+        z = (q * vals) @ q.T
+        z = 0.5 * (z + z.T)
+    dc = GL.sym_eig(z)
+    ref = np.sort(np.linalg.eigvalsh(z))[::-1]
+    nz = np.linalg.norm(z, 2)
+    assert np.max(np.abs(dc.eigvals - ref)) <= 1e-12 * nz
+    p = dc.eigvecs
+    assert np.linalg.norm(p.T @ p - np.eye(n)) <= 1e-12 * n
+    assert np.linalg.norm((p * dc.eigvals) @ p.T - z) <= 1e-12 * nz * n
+
+
+def test_sym_eig_kats():
+    # test_linalg.py:13-44
+    d = GL.sym_eig(np.diag([2.0, -1.0]))
+    assert np.allclose(np.abs(d.eigvecs), np.eye(2)) and np.allclose(d.eigvals, [2.0, -1.0])
+    assert d.pos_idx.tolist() == [0] and d.nonpos_idx.tolist() == [1]
+    d = GL.sym_eig(np.eye(3))
+    assert np.allclose(d.eigvals, 1.0) and d.pos_idx.tolist() == [0, 1, 2] and d.nonpos_idx.size == 0
+    d = GL.sym_eig(np.diag([0.0, 1.0, -2.0]))
+    assert d.eigvals.tolist() == [1.0, 0.0, -2.0]
+    assert d.pos_idx.tolist() == [0] and d.nonpos_idx.tolist() == [1, 2]
+
+
+# ---------------------------------------------------------------- Cholesky
+
+def test_cholesky_kats(small, cfg1):
+    f = GL.cholesky_psd(np.eye(2))
+    assert np.allclose(f.upper, np.eye(2)) and f.jitter_applied == 0.0
+    f = GL.cholesky_psd(np.array([[4.0, 2.0], [2.0, 2.0]]))
+    assert np.allclose(f.upper, [[2.0, 1.0], [0.0, 1.0]])
+    f = GL.cholesky_psd(small["chol_rankdef_in"])
+    assert f.jitter_applied == float(small["chol_rankdef_jitter"]) > 0
+    tgt = small["chol_rankdef_in"] + f.jitter_applied * np.eye(3)
+    assert np.linalg.norm(f.upper.T @ f.upper - tgt) <= 1e-8 * np.linalg.norm(tgt)
+    with pytest.raises(GL.IndefiniteKernelError):
+        GL.cholesky_psd(np.diag([1.0, -1.0]))
+    f = GL.cholesky_psd(cfg1["kmat"])
+    assert f.jitter_applied == 0.0
+    assert rel(f.upper, cfg1["r"]) <= 1e-13
+    assert np.all(np.tril(f.upper, -1) == 0.0)
+
+
+@pytest.mark.parametrize("n", [130, 700])
+def test_cholesky_large(n):
+    rng = np.random.default_rng(n)
+    pts = rng.uniform(-1, 1, (n, 6))
+    k = O.gaussian_gram(1.0, pts)
+    up, jit = O.cholesky_psd(k)
+    f = GL.cholesky_psd(k)
+    assert f.jitter_applied == jit
+    assert rel(f.upper, up) <= 1e-11
+
+
+# -------------------------------------------------------------- assembly
+
+def test_gram_matches_oracle():
+    rng = np.random.default_rng(3)
+    pts = rng.uniform(-1, 1, (77, 5))
+    g = K.kernels.gram_matrix(K.KernelSpec(0.7, 5), pts)
+    assert np.array_equal(g, g.T) and np.all(np.diag(g) == 1.0)
+    assert rel(g, O.gaussian_gram(0.7, pts)) <= 1e-15
+
+
+def test_assemble_cfg1(cfg1):
+    sx, sy, sxy = K.build_kernel_specs(2, float(cfg1["bw_sq"]))
+    pd = K.assemble(K.SampleSet(cfg1["xs"]), K.SampleSet(cfg1["ys"]), K.FillingPoints(cfg1["xt"], cfg1["yt"]),
+                    float(cfg1["l1"]), float(cfg1["l2"]), sx, sy, sxy)
+    assert rel(pd.q_mat, cfg1["q"]) <= 1e-15
+    assert rel(pd.z, cfg1["z"]) <= 1e-14
+    assert rel(pd.embed_sum, cfg1["embed"]) <= 1e-14
+    assert pd.q_sq == pytest.approx(float(cfg1["q_sq"]), rel=1e-14)
+    assert pd.jitter == 0.0
+    assert rel(pd.chol_upper, cfg1["r"]) <= 1e-13
+    assert rel(pd.pair_gram(), cfg1["kmat"]) <= 1e-15
+
+
+# ------------------------------------------------------------ operators
+
+def test_phi_and_adjoint(cfg1):
+    pd = gpu_pd(cfg1)
+    g, x = cfg1["op_g"], cfg1["op_x"]
+    assert rel(GP.phi_forward(pd, x), cfg1["op_phi"]) <= 1e-13
+    pa = GP.phi_adjoint(pd, g)
+    assert np.array_equal(pa, pa.T)
+    assert rel(pa, cfg1["op_phi_adj"]) <= 1e-13
+    # adjointness <Φ(X), γ> = <X, Φ*(γ)>
+    rng = np.random.default_rng(0)
+    xr = random_symmetric(rng, pd.n)
+    gr = rng.standard_normal(pd.n)
+    lhs = GP.phi_forward(pd, xr) @ gr
+    rhs = np.sum(xr * GP.phi_adjoint(pd, gr))
+    assert abs(lhs - rhs) <= 1e-13 * abs(rhs)
+
+
+def test_residual_parts(cfg1):
+    pd = gpu_pd(cfg1)
+    r, info = GP.residual_parts(pd, GP.IteratePair(cfg1["op_g"], cfg1["op_x"]))
+    assert rel(r.gamma, cfg1["op_r1"]) <= 1e-12
+    assert rel(r.x_mat, cfg1["op_r2"]) <= 1e-11
+    assert np.array_equal(r.x_mat, r.x_mat.T)
+    assert np.max(np.abs(info.eigvals - cfg1["op_eigvals"])) <= 1e-12 * np.abs(cfg1["op_eigvals"]).max()
+    assert info.n_pos == int(cfg1["op_npos"])
+
+
+@pytest.mark.parametrize("n_pos", [0, 1, 3, 5, 6])
+def test_spectral_operators_sign_fixtures(small, n_pos):
+    p = f"sign{n_pos}_"
+    z, s = small[p + "z"], small[p + "s"]
+    assert np.max(np.abs(GC.proj_psd(z) - small[p + "proj"])) <= 1e-13
+    assert np.max(np.abs(GC.apply_proj_jacobian_at(z, s) - small[p + "mz"])) <= 1e-13
+    for mu in (0.03, 1.0, 17.0):
+        ref = small[f"{p}elim_{mu}"]
+        for path in (None, GC.POS_BLOCK, GC.NONPOS_COMPLEMENT):
+            out = GC.apply_eliminator_at(z, s, mu, path)
+            assert np.linalg.norm(out - ref) <= 1e-12 * max(np.linalg.norm(ref), 1.0)
+
+
+def test_eliminator_and_jacobian_cfg1(cfg1):
+    pd_o = oracle_pd(cfg1)
+    zarg = O.sym(cfg1["op_x"]) - O.constraint_matrix(pd_o, cfg1["op_g"])
+    s, mu = cfg1["op_s"], float(cfg1["op_mu"])
+    el = GC.apply_eliminator_at(zarg, s, mu)
+    assert rel(el, cfg1["op_elim"]) <= 1e-11
+    mz = GC.apply_proj_jacobian_at(zarg, s)
+    assert rel(mz, cfg1["op_mz"]) <= 1e-11
+
+
+def test_middle_operator(cfg1):
+    pd = gpu_pd(cfg1)
+    out, mu = GN.middle_operator_at(pd, GP.IteratePair(cfg1["op_g"], cfg1["op_x"]), float(cfg1["op_theta"]),
+                                    cfg1["op_v"])
+    assert mu == pytest.approx(float(cfg1["op_mu"]), rel=1e-12)
+    assert rel(out, cfg1["op_middle"]) <= 1e-11
+
+
+def _perturbed_oracle_pd(d, seed, p=""):
+    """Oracle problem with R perturbed by ±1 ulp (the oracle's own rounding spread)."""
+    rng = np.random.default_rng(seed)
+    r = d[p + "r"] * (1.0 + rng.choice([-1.0, 1.0], d[p + "r"].shape) * 2.2e-16)
+    return O.Problem(q=d[p + "q"], z=d[p + "z"], q_sq=float(d[p + "q_sq"]), r=r, l1=float(d[p + "l1"]),
+                     l2=float(d[p + "l2"]), embed=d.get(p + "embed"))
+
+
+def test_newton_direction(cfg1):
+    """Default profile: CG stops at the 20×(1+2) cap, so the direction is only determined up to the
+    oracle's own ulp sensitivity (measured: ≈2.3e-5 relative); the tolerance is 10× that spread."""
+    pd = gpu_pd(cfg1)
+    w = GP.IteratePair(cfg1["op_g"], cfg1["op_x"])
+    st = GN.newton_direction_at(pd, w, float(cfg1["op_theta"]), GN.NewtonConfig())
+    spread = 0.0
+    for seed in (1, 2):
+        po = _perturbed_oracle_pd(cfg1, seed)
+        r, dc = O.residual_parts(po, O.Pair(cfg1["op_g"], cfg1["op_x"]))
+        so = O.newton_direction(po, r, O.newton_context(dc, r.norm(), float(cfg1["op_theta"])), O.NewtonCfg())
+        spread = max(spread, rel(so.dw.g, cfg1["op_dir_dg"]))
+    assert st.cg_iters == int(cfg1["op_dir_cg"])
+    assert st.criterion_met == bool(cfg1["op_dir_met"])
+    assert rel(st.dw.gamma, cfg1["op_dir_dg"]) <= max(1e-9, 10 * spread)
+    assert rel(st.dw.x_mat, cfg1["op_dir_dx"]) <= max(1e-9, 10 * spread)
+    assert np.array_equal(st.dw.x_mat, st.dw.x_mat.T)
+
+
+def test_newton_direction_converged_cg(cfg1):
+    """With CG driven to 1e-13 the direction is well determined: GPU vs oracle ≤ 1e-9 (Lemma-1 regime)."""
+    pd = gpu_pd(cfg1)
+    po = oracle_pd(cfg1)
+    cfg = GN.NewtonConfig(cg_tol=1e-13, cg_max=3000, cg_restarts=0)
+    w = GP.IteratePair(cfg1["op_g"], cfg1["op_x"])
+    st = GN.newton_direction_at(pd, w, float(cfg1["op_theta"]), cfg)
+    r, dc = O.residual_parts(po, O.Pair(cfg1["op_g"], cfg1["op_x"]))
+    so = O.newton_direction(po, r, O.newton_context(dc, r.norm(), float(cfg1["op_theta"])),
+                            O.NewtonCfg(cg_tol=1e-13, cg_max=3000, cg_restarts=0))
+    assert rel(st.dw.gamma, so.dw.g) <= 1e-8
+    assert rel(st.dw.x_mat, so.dw.x) <= 1e-8
+
+
+def test_eg_step(cfg1):
+    pd = gpu_pd(cfg1)
+    v = eg_step(pd, GP.IteratePair(cfg1["op_g"], cfg1["op_eg_in_x"]), EgConfig(float(cfg1["eg_stepsize"])))
+    assert rel(v.gamma, cfg1["op_eg_g"]) <= 1e-12
+    assert rel(v.x_mat, cfg1["op_eg_x"]) <= 1e-11
+    assert np.array_equal(v.x_mat, v.x_mat.T)
+
+
+def test_objective_and_ot(cfg1):
+    pd = gpu_pd(cfg1)
+    assert GP.objective(pd, cfg1["op_g"]) == pytest.approx(float(cfg1["op_objective"]), rel=1e-13)
+    assert GP.ot_estimate(pd, cfg1["tight_gamma"]) == pytest.approx(float(cfg1["tight_ot"]), rel=1e-12)
+
+
+# ------------------------------------------------------------------ solve
+
+@pytest.mark.parametrize("name", ["interior", "active"])
+def test_scalar_kkt_fixtures(small, name):
+    z = 1.0 if name == "interior" else -4.0
+    pd = GP.ProblemData(q_mat=[[2.0]], z=[z], q_sq=0.0, chol_upper=[[1.0]], lambda1=1.0, lambda2=0.5)
+    rep = K.solve(pd, K.SolverConfig(residual_tol=1e-12, max_iter=100))
+    assert rep.termination == "converged"
+    assert rep.iterations == int(small[f"scalar_{name}_iters"])
+    eg, ex = (0.5, 0.0) if name == "interior" else (-1.0, 2.0)
+    assert rep.gamma_hat[0] == pytest.approx(eg, abs=1e-10)
+    assert rep.x_hat[0, 0] == pytest.approx(ex, abs=1e-10)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_random_problem_solves(small, seed):
+    p = f"rand{seed}_"
+    pd = gpu_pd(small, p)
+    rep = K.solve(pd, K.SolverConfig(residual_tol=1e-10, max_iter=200))
+    ref_iters = int(small[p + "iters"])
+    if ref_iters < 200:  # the reference converges: same end point
+        assert rep.termination == "converged"
+        assert abs(rep.iterations - ref_iters) <= 2
+        assert rel(rep.gamma_hat, small[p + "gamma"]) <= 1e-8
+    else:  # the reference stalls at max_iter (seed 2: ‖R‖≈9.4e-3); so must we, at the same level
+        assert rep.termination == "max_iter"
+        assert rep.residual_norm == pytest.approx(float(small[p + "res"]), rel=0.05)
+
+
+def test_lockstep_replay_cfg1(cfg1):
+    """one GPU iteration from each saved oracle state.
+
+    The oracle is run from the same state on ±1-ulp perturbations of R (4 seeds).  The GPU's CG
+    count must be one the oracle ensemble produces (Eq.(9) knife edges flip the restart count:
+    measured at state 5, where 2 of 4 perturbed oracle runs take 60 CG steps instead of 40);
+    when it matches the reference, the next state must agree to max(1e-9, 20× ensemble spread)."""
+    pd = gpu_pd(cfg1)
+    cfg = K.SolverConfig(eg=EgConfig(float(cfg1["eg_stepsize"])), residual_tol=1e-12, max_iter=40)
+    ocfg = O.SolverCfg(eg_stepsize=float(cfg1["eg_stepsize"]), residual_tol=1e-12, max_iter=40)
+    matched = 0
+    for i in cfg1["replay_iters"]:
+        if f"rp{i}_next_wg" not in cfg1:
+            continue
+        w = GP.IteratePair(cfg1[f"rp{i}_wg"], cfg1[f"rp{i}_wx"])
+        v = GP.IteratePair(cfg1[f"rp{i}_vg"], cfg1[f"rp{i}_vx"])
+        spread, cg_set = 0.0, {int(cfg1["paper_cg_iters"][i])}
+        for seed in (11, 12, 13, 14):
+            po = _perturbed_oracle_pd(cfg1, seed)
+            ow = O.Pair(w.gamma.copy(), w.x_mat.copy())
+            r_w, dc_w = O.residual_parts(po, ow)
+            st0 = O.State(ow, O.Pair(v.gamma.copy(), v.x_mat.copy()), r_w, dc_w, r_w.norm(), None, None,
+                          r_w.norm(), float(cfg1[f"rp{i}_theta"]))
+            ost, orec, _ = O.iterate_once(po, st0, int(i), ocfg)
+            cg_set.add(orec.cg_iters)
+            if orec.cg_iters == int(cfg1["paper_cg_iters"][i]):
+                spread = max(spread, rel(ost.w.g, cfg1[f"rp{i}_next_wg"]), rel(ost.w.x, cfg1[f"rp{i}_next_wx"]))
+        w2, v2, th2, rec = GS.iterate(pd, cfg, w, v, float(cfg1[f"rp{i}_theta"]), int(i))
+        assert rec.cg_iters in cg_set, (i, rec.cg_iters, cg_set)
+        # the EG step has no CG: v is determined to eigensolver accuracy
+        assert rel(v2.gamma, cfg1[f"rp{i}_next_vg"]) <= 1e-9, i
+        assert rel(v2.x_mat, cfg1[f"rp{i}_next_vx"]) <= 1e-9, i
+        if rec.cg_iters != int(cfg1["paper_cg_iters"][i]):
+            continue
+        tol = max(1e-9, 20 * spread)
+        assert rec.accepted == ("ssn" if cfg1["paper_accepted_ssn"][i] else "eg"), i
+        assert th2 == pytest.approx(float(cfg1[f"rp{i}_next_theta"]), rel=1e-12), i
+        assert rel(w2.gamma, cfg1[f"rp{i}_next_wg"]) <= tol, (i, tol)
+        assert rel(w2.x_mat, cfg1[f"rp{i}_next_wx"]) <= tol, (i, tol)
+        matched += 1
+    assert matched >= 4
+
+
+def test_paper_profile_first_iterations(cfg1):
+    pd = gpu_pd(cfg1)
+    cfg = K.SolverConfig(eg=EgConfig(float(cfg1["eg_stepsize"])), residual_tol=1e-12, max_iter=40)
+    rep = K.solve(pd, cfg)
+    res = np.array([t.res_accepted for t in rep.trace])
+    ref = cfg1["paper_res_accepted"]
+    # chaotic at ulp level: tight agreement only on the first iterations
+    assert np.allclose(res[:2], ref[:2], rtol=1e-8)
+    # beyond that only the envelope is reproducible (oracle vs itself under ±2 ulp: >1e-2 by iter 4-88)
+    assert np.all(np.abs(np.log(res / ref)) <= np.log(3.0))
+    assert rep.iterations == 40
+
+
+def test_tight_profile_end_state(cfg1):
+    """tol 1e-10 end state vs the reference."""
+    pd = gpu_pd(cfg1)
+    cfg = K.SolverConfig(newton=K.NewtonConfig(alpha1=1e-8, alpha2=1e-4, cg_max=500),
+                         eg=EgConfig(float(cfg1["eg_stepsize"])), residual_tol=1e-10, max_iter=1000)
+    rep = K.solve(pd, cfg)
+    assert rep.termination == "converged"
+    ref_iters = int(cfg1["tight_iters"])
+    assert abs(rep.iterations - ref_iters) <= 30  # oracle's own ulp spread is −24…+10
+    obj = O.objective(oracle_pd(cfg1), rep.gamma_hat)
+    assert obj == pytest.approx(float(cfg1["tight_objective"]), rel=1e-8)
+    assert rel(rep.gamma_hat, cfg1["tight_gamma"]) <= 1e-6
+    assert rep.ot_estimate == pytest.approx(float(cfg1["tight_ot"]), rel=1e-8)
