@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark: SSN iterations/s of the B200 kernel-OT solver on the BASELINE configs.
+
+Contract (see README/DESIGN): ``python bench.py --gpus N --steps K --warmup W``
+prints ONE JSON line on rank 0.  A *step* is one outer SSN iteration
+(Algorithm 2: EG safeguard + Newton direction with CG + trial residual) of a
+continuous solve trajectory on the headline workload (BASELINE.json
+configs[2]: d=10, n=ℓ=2000, σ=1.5, λ1=1e-4, λ2=1/ℓ, FP64), paper profile
+(``NewtonConfig()`` defaults), EG stepsize 0.5/(‖Q‖_F/(2λ2)+‖K‖_F)
+(SURVEY.md §8(d)).  Synthetic seeded data (the reference ships none).
+
+* ``value``: iterations/s over the K timed iterations, inputs resident in HBM,
+  timed with CUDA events on the library's stream, barrier + synchronize on both
+  sides, max over ranks; N>1 runs N independent replicas (single problems do not
+  shard: SURVEY.md §8(e) "configs 1-3: replicas only") → ``scaling: weak``.
+* ``e2e``: the same metric through the public API ``solve(ProblemData)`` from
+  host arrays — H2D of the instance and D2H of (γ̂, X̂) inside the timed region.
+* ``roofline``: the dominant kernel (live CUDA-event timing inside libkotgpu's
+  phase profiler), against MEASURED_PEAKS.json / the measured DMMA peak.
+* ``cpu_baseline``: the NumPy oracle (oracle/, a restatement of the reference)
+  on this box's host cores for a bounded sample (1 SSN iteration).
+* ``--impl reference``: the reference's CPU algorithm (the oracle port; the
+  reference is pure Python and cannot be installed on the box) on the same config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DMMA_PEAK_TFLOPS = 37.12  # measured, profiles/r01/fp64_peak_microbench.txt (mma.sync m8n8k4 f64)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m.get("hbm_gbs", 6553.6)), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def workload(name: str):
+    from paper_2310_14087_b200 import configs
+    if name == "cfg1":
+        return configs.config1()
+    if name == "cfg2":
+        return configs.config2()
+    if name.startswith("cfg3"):
+        n = int(name.split(":")[1]) if ":" in name else 2000
+        return configs.config3(n=n)
+    if name.startswith("cfg5"):
+        seed = int(name.split(":")[1]) if ":" in name else 0
+        return configs.config5_member(seed)
+    raise SystemExit(f"unknown config {name}")
+
+
+def describe(wl, profile: str) -> dict:
+    return {"workload": f"{wl.name}: d={wl.d}, n=l={wl.l}, bandwidth_sq={wl.bandwidth_sq}, "
+                        f"lambda1={wl.lambda1}, lambda2=1/{wl.l}; {profile} profile; "
+                        "EG stepsize 0.5/(||Q||_F/(2 lambda2)+||K||_F); one step = one SSN outer iteration",
+            "l": wl.l, "n_samples": wl.xs.shape[0], "d": wl.d, "profile": profile,
+            "l2_flush": f"none needed: per-iteration working set ~{25 * 8 * wl.l * wl.l / 1e9:.2f} GB > 126 MB L2",
+            "data": "seeded synthetic (SURVEY.md §8(d))"}
+
+
+def newton_cfg(profile: str):
+    import paper_2310_14087_b200 as K
+    from paper_2310_14087_b200 import configs
+    return K.NewtonConfig(**configs.PROFILES[profile])
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(world, x: float, local: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(world, x: float, local: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# --------------------------------------------------------------------- CPU legs
+
+def oracle_problem(wl):
+    from oracle import kot_port as O
+    pd, kmat = O.assemble(wl.xs, wl.ys, wl.xt, wl.yt, wl.lambda1, wl.lambda2, wl.bandwidth_sq)
+    return pd, kmat
+
+
+def oracle_iters_per_s(wl, profile: str, warmup: int, steps: int) -> tuple[float, float, dict]:
+    """Time `steps` SSN iterations of the oracle (after `warmup`) on the host cores."""
+    from oracle import kot_port as O
+    from paper_2310_14087_b200 import configs
+    pd, kmat = oracle_problem(wl)
+    step = configs.eg_stepsize(pd.q, kmat, pd.l2)
+    cfg = O.SolverCfg(newton=O.NewtonCfg(**configs.PROFILES[profile]), eg_stepsize=step, residual_tol=1e-300,
+                      max_iter=10 ** 9)
+    st = O.initial_state(pd, cfg)
+    k = 0
+    for _ in range(warmup):
+        st, _, _ = O.iterate_once(pd, st, k, cfg)
+        k += 1
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st, _, _ = O.iterate_once(pd, st, k, cfg)
+        k += 1
+    dt = time.perf_counter() - t0
+    return steps / dt, dt, {"first_iteration": k - steps}
+
+
+def cpu_info() -> dict:
+    cores = len(os.sched_getaffinity(0))
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"cores": cores, "cpu": model, "blas_threads": os.environ.get("OPENBLAS_NUM_THREADS", "all")}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    wl = workload(args.config)
+    v, dt, extra = oracle_iters_per_s(wl, args.profile, args.warmup, args.steps)
+    ci = cpu_info()
+    line = {
+        "impl": "reference", "metric": f"SSN iters/s at n=l={wl.l} FP64 ({args.profile} profile)",
+        "value": v, "unit": "iter/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": describe(wl, args.profile),
+        "cpu_baseline": {"value": v, "unit": "iter/s", "cores": ci["cores"], "kind": "port",
+                         "sample": f"{args.steps} SSN iterations of {wl.name} after {args.warmup} warm-up "
+                                   "iterations from the zero pair, NumPy/OpenBLAS oracle (oracle/kot_port.py)",
+                         "cpu": ci["cpu"]},
+        "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- GPU leg
+
+def run_gpu(args):
+    world, rank, local = dist_setup(args.gpus)
+    os.environ["KOT_DEVICE"] = str(local)
+    import torch
+
+    import paper_2310_14087_b200 as K
+    from paper_2310_14087_b200 import _lib, configs, solver
+
+    torch.cuda.set_device(local)
+    wl = workload(args.config)
+    sx, sy, sxy = K.build_kernel_specs(wl.d, wl.bandwidth_sq)
+    pd = K.assemble(K.SampleSet(wl.xs), K.SampleSet(wl.ys), K.FillingPoints(wl.xt, wl.yt), wl.lambda1,
+                    wl.lambda2, sx, sy, sxy, device=local)
+    stepsize = configs.eg_stepsize(pd.q_mat, pd.pair_gram(), pd.lambda2)
+    cfg = K.SolverConfig(newton=newton_cfg(args.profile), eg=K.EgConfig(stepsize), residual_tol=1e-300,
+                         max_iter=10 ** 6)
+
+    # ---------------- device-resident timed region (value)
+    se = solver.Session(pd, cfg)
+    stream = torch.cuda.ExternalStream(se.stream, device=f"cuda:{local}")
+    for _ in range(args.warmup):
+        se.step(1)
+    torch.cuda.synchronize()
+    barrier(world)
+    l0 = _lib.launch_count()
+    _lib.profile_enable(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        barrier(world)
+        ev0.record(stream)
+        done = 0
+        for _ in range(args.steps):
+            done += se.step(1)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    ms = ev0.elapsed_time(ev1)
+    prof = _lib.profile_read()
+    _lib.profile_enable(False)
+    launches = _lib.launch_count() - l0
+    recs = se.records[args.warmup:]
+    se.close()
+    ms_max = max_over_ranks(world, ms, local)
+    total_iters = sum_over_ranks(world, float(done), local)
+    value = total_iters / (ms_max / 1e3)
+
+    # ---------------- end to end through the public API from host buffers (e2e)
+    pd_host = K.ProblemData(q_mat=pd.q_mat.copy(), z=pd.z.copy(), q_sq=pd.q_sq, chol_upper=pd.chol_upper.copy(),
+                            lambda1=pd.lambda1, lambda2=pd.lambda2, embed_sum=pd.embed_sum.copy())
+    cfg_e = K.SolverConfig(newton=newton_cfg(args.profile), eg=K.EgConfig(stepsize), residual_tol=1e-300,
+                           max_iter=args.steps)
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    rep = K.solve(pd_host, cfg_e)
+    torch.cuda.synchronize()
+    t_e2e = time.perf_counter() - t0
+    barrier(world)
+    t_e2e = max_over_ranks(world, t_e2e, local)
+    n = pd.n
+    e2e_iters = sum_over_ranks(world, float(rep.iterations), local)
+    h2d = (2 * n * n + 2 * n) * 8 / max(rep.iterations, 1)
+    d2h = ((n * n + n) * 8 + rep.iterations * 8 * 16) / max(rep.iterations, 1)
+
+    if rank != 0:
+        return 0
+
+    # ---------------- roofline of the dominant kernel
+    hbm, peak_kind = peaks()
+    kern = {k: v for k, v in prof.items() if k in ("sytrd_panel", "gemm_dmma")}
+    dom = max(kern, key=lambda k: kern[k]["ms"]) if kern else None
+    roof = None
+    if dom == "sytrd_panel":
+        e = kern[dom]
+        ach = e["bytes"] / e["calls"] / (e["ms"] / e["calls"] * 1e-3) / 1e9
+        roof = {"kernel": "sytrd_panel_kernel (cooperative Householder panel: column update + symv)",
+                "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "algorithmic": "per launch: sum over its 32 columns of one lower-triangle read of the "
+                               "trailing matrix, 8*m(m+1)/2 B",
+                "share_of_step": e["ms"] / ms, "avg_launch_ms": e["ms"] / e["calls"]}
+    elif dom == "gemm_dmma":
+        e = kern[dom]
+        ach = e["flops"] / (e["ms"] * 1e-3) / 1e12
+        roof = {"kernel": "gemm_dmma_kernel (mma.sync m8n8k4 f64, all shapes)", "bound": "tensor",
+                "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
+                "traffic": None, "peak_source": "measured DMMA microbenchmark (MEASURED_PEAKS.json has no FP64)",
+                "share_of_step": e["ms"] / ms, "avg_launch_ms": e["ms"] / e["calls"]}
+    phases = {k: {"ms_per_step": v["ms"] / max(done, 1), "calls_per_step": v["calls"] / max(done, 1),
+                  **({"tflops": v["flops"] / (v["ms"] * 1e-3) / 1e12} if v["flops"] and v["ms"] else {})}
+              for k, v in prof.items()}
+
+    # ---------------- CPU baseline (oracle port, bounded sample)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, dt, extra = oracle_iters_per_s(wl, args.profile, 0, 3)
+        ci = cpu_info()
+        cpu = {"value": v, "unit": "iter/s", "cores": ci["cores"], "kind": "port",
+               "sample": f"the first 3 SSN iterations (from the zero pair) of {wl.name}, NumPy/OpenBLAS oracle "
+                         f"with {ci['blas_threads']} BLAS threads; {dt:.1f} s", "cpu": ci["cpu"]}
+
+    line = {
+        "metric": f"SSN iters/s at n=l={wl.l} FP64 ({args.profile} profile)",
+        "value": value, "unit": "iter/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / max(done, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": {**describe(wl, args.profile), "parallelism": f"replicas{world}"},
+        "e2e": {"value": e2e_iters / t_e2e, "unit": "iter/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "api": "paper_2310_14087_b200.solve(ProblemData from host arrays)",
+                "iterations": rep.iterations},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+        "phases": phases,
+        "trace": {"res": [r.res_accepted for r in recs][:64], "cg_iters": [r.cg_iters for r in recs][:64],
+                  "n_pos": [r.n_pos for r in recs][:64]},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--profile", default="paper", choices=["paper", "tight"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -109,6 +109,29 @@ int kot_iterate(kot_problem* p, const kot_solver_cfg* cfg, const double* w_gamma
                 double* w_x_out, double* v_gamma_out, double* v_x_out, double* theta_out,
                 kot_iter_record* rec);
 
+/* ---- sessions: a solve driven in chunks (bench.py: warm-up + timed
+ * iterations of one continuous trajectory, timed with CUDA events on the
+ * problem's stream) ---------------------------------------------------- */
+typedef struct kot_session kot_session;
+int kot_session_begin(kot_problem* p, const kot_solver_cfg* cfg, kot_session** out);
+/* run up to `iters` loop bodies; *done = how many ran (stops at convergence/max_iter) */
+int kot_session_step(kot_session* s, int iters, kot_iter_record* recs /* nullable */, int* done);
+int kot_session_result(kot_session* s, double* gamma_out, double* x_out, kot_report* out);
+void kot_session_end(kot_session* s);
+/* the cudaStream_t (as void*) every kernel of this problem is launched on */
+void* kot_problem_stream(kot_problem* p);
+
+/* ---- phase profiler (CUDA events around library phases; off by default) --- */
+typedef struct {
+  char name[32];
+  long long calls;
+  double ms;      /* summed event time */
+  double flops;   /* algorithmic FLOPs (0 where not applicable) */
+  double bytes;   /* algorithmic HBM/L2 bytes (0 where not applicable) */
+} kot_prof_entry;
+int kot_profile_enable(int on);      /* resets the counters */
+int kot_profile_read(kot_prof_entry* out, int cap);  /* returns #entries */
+
 /* ---- operators (host buffers in/out; per-kernel parity) ----------------- */
 
 /* gram_matrix (kernels.py:61-73), square form: out = exp(-|a_i-a_j|^2/(2 bw)), unit diag. */

@@ -42,6 +42,11 @@ class ReportC(C.Structure):
                 ("ot_estimate", C.c_double), ("total_ms", C.c_double)]
 
 
+class ProfEntryC(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("calls", C.c_longlong), ("ms", C.c_double), ("flops", C.c_double),
+                ("bytes", C.c_double)]
+
+
 IterCB = C.CFUNCTYPE(None, C.c_void_p, C.c_int, dptr, dptr, dptr, dptr, C.c_double, C.c_double, dptr, dptr,
                      C.c_int)
 
@@ -62,6 +67,13 @@ _SIGS = {
                                     C.c_int, C.POINTER(ReportC)]),
     "kot_iterate": (C.c_int, [C.c_void_p, C.POINTER(SolverCfgC), dptr, dptr, dptr, dptr, C.c_double, C.c_int,
                               dptr, dptr, dptr, dptr, dptr, C.POINTER(IterRecordC)]),
+    "kot_session_begin": (C.c_int, [C.c_void_p, C.POINTER(SolverCfgC), C.POINTER(C.c_void_p)]),
+    "kot_session_step": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(IterRecordC), iptr]),
+    "kot_session_result": (C.c_int, [C.c_void_p, dptr, dptr, C.POINTER(ReportC)]),
+    "kot_session_end": (None, [C.c_void_p]),
+    "kot_problem_stream": (C.c_void_p, [C.c_void_p]),
+    "kot_profile_enable": (C.c_int, [C.c_int]),
+    "kot_profile_read": (C.c_int, [C.POINTER(ProfEntryC), C.c_int]),
     "kot_gram": (C.c_int, [dptr, C.c_int, C.c_int, C.c_double, C.c_int, dptr]),
     "kot_cholesky_psd": (C.c_int, [dptr, C.c_int, C.c_int, dptr, dptr]),
     "kot_sym_eig": (C.c_int, [dptr, C.c_int, C.c_int, dptr, dptr, iptr]),
@@ -169,3 +181,15 @@ def default_device() -> int:
 
 def launch_count() -> int:
     return int(lib().kot_launch_count())
+
+
+def profile_enable(on: bool = True) -> None:
+    lib().kot_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    buf = (ProfEntryC * 64)()
+    n = lib().kot_profile_read(buf, 64)
+    return {buf[i].name.decode(): dict(calls=int(buf[i].calls), ms=float(buf[i].ms), flops=float(buf[i].flops),
+                                        bytes=float(buf[i].bytes))
+            for i in range(n)}

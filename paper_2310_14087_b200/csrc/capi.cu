@@ -172,6 +172,49 @@ int kot_iterate(kot_problem* h, const kot_solver_cfg* cfg, const double* w_gamma
   });
 }
 
+struct kot_session {
+  kot::Session* s;
+  kot_problem* h;
+};
+
+int kot_session_begin(kot_problem* h, const kot_solver_cfg* cfg, kot_session** out) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    const kot::SolverCfg c = to_cfg(cfg);
+    check_cfg(c);
+    *out = new kot_session{kot::session_begin(p, c), h};
+  });
+}
+
+int kot_session_step(kot_session* s, int iters, kot_iter_record* recs, int* done) {
+  return guarded([&] {
+    KOT_CUDA(cudaSetDevice(s->h->p->device));
+    *done = kot::session_step(*s->s, iters, reinterpret_cast<kot::IterRecord*>(recs));
+  });
+}
+
+int kot_session_result(kot_session* s, double* gamma_out, double* x_out, kot_report* out) {
+  return guarded([&] {
+    KOT_CUDA(cudaSetDevice(s->h->p->device));
+    kot::SolveResult r{};
+    kot::session_result(*s->s, gamma_out, x_out, r);
+    out->converged = r.converged;
+    out->iterations = r.iterations;
+    out->residual_norm = r.residual_norm;
+    out->ot_estimate = r.ot_estimate;
+    out->total_ms = r.total_ms;
+  });
+}
+
+void kot_session_end(kot_session* s) {
+  if (!s) return;
+  kot::session_end(s->s);
+  delete s;
+}
+
+void* kot_problem_stream(kot_problem* h) { return (void*)h->p->st; }
+
 // ------------------------------------------------------------ operators
 
 namespace {

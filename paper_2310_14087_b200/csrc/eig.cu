@@ -244,13 +244,19 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st) {
     const int G = std::max(1, std::min(kNumSMs, ceil_div(rows, 16)));
     TrdArgs args{w.A, n, p0, nb, w.X, w.Vall, w.d, w.e, w.tau, w.xv, w.yv, w.part, w.partn};
     void* kargs[] = {&args};
+    // algorithmic bytes: one read of the lower triangle of every trailing matrix this panel reflects
+    double bytes = 0.0;
+    for (int c = p0; c < p0 + nb; ++c) bytes += 8.0 * 0.5 * (double)(n - c - 1) * (n - c);
     const size_t smem = sizeof(double) * std::max(rows, 1);
     if (smem > 48 * 1024 && smem_set_for < (int)smem) {
       KOT_CUDA(cudaFuncSetAttribute(sytrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       smem_set_for = (int)smem;
     }
-    KOT_CUDA(cudaLaunchCooperativeKernel((void*)sytrd_panel_kernel, G, TRD_THREADS, kargs, smem, st));
-    KOT_LAUNCH_CHECK();
+    {
+      ProfScope pscope("sytrd_panel", st, 0.0, bytes);
+      KOT_CUDA(cudaLaunchCooperativeKernel((void*)sytrd_panel_kernel, G, TRD_THREADS, kargs, smem, st));
+      KOT_LAUNCH_CHECK();
+    }
     // trailing update A22 -= V Wᵀ + W Vᵀ on rows/cols >= p0+nb
     const int t0 = p0 + nb;
     const int m2 = n - t0;
@@ -950,8 +956,15 @@ void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigW
     eig1_kernel<<<1, 1, 0, st>>>(Z, P, vals);
     KOT_LAUNCH_CHECK();
   } else {
-    sytrd(Z, n, w, st);
-    stedc(n, w, st);
+    {
+      ProfScope ps("eig.sytrd", st, 4.0 / 3.0 * n * (double)n * n);
+      sytrd(Z, n, w, st);
+    }
+    {
+      ProfScope ps("eig.stedc", st);
+      stedc(n, w, st);
+    }
+    ProfScope ps("eig.ormtr", st, 2.0 * n * (double)n * n);
     reverse_cols_kernel<<<std::min(ceil_div((long)n * n, 256), 2048), 256, 0, st>>>(w.Q, w.d, P, vals, n);
     KOT_LAUNCH_CHECK();
     ormtr(n, w, P, st);

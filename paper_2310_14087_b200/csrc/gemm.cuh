@@ -14,7 +14,9 @@
 // Structural zeros of triangular operands (R is upper triangular) are skipped
 // by restricting the K range per output tile.
 #pragma once
+#include <algorithm>
 #include "common.cuh"
+#include "prof.cuh"
 
 namespace kot {
 
@@ -242,9 +244,28 @@ inline bool gemm_vec2_ok(const GemmShape& s) {
   return al(s.A) && al(s.B) && (s.lda % 2 == 0) && (s.ldb % 2 == 0);
 }
 
+// Algorithmic FLOPs of one launch: per computed tile, 2·rows·cols·(true K range),
+// excluding zero padding and the structurally-zero tiles that are skipped.
+inline double gemm_alg_flops(const GemmShape& s) {
+  const int tm_n = (s.M + GB_M - 1) / GB_M, tn_n = (s.N + GB_N - 1) / GB_N;
+  double f = 0.0;
+  for (int tm = 0; tm < tm_n; ++tm)
+    for (int tn = s.sym_tiles ? tm : 0; tn < tn_n; ++tn) {
+      const int m0 = tm * GB_M, n0 = tn * GB_N;
+      int kb = 0, ke = s.K;
+      if (s.kb_m) kb = std::max(kb, m0);
+      if (s.kb_n) kb = std::max(kb, n0);
+      if (s.ke_m) ke = std::min(ke, m0 + GB_M);
+      if (s.ke_n) ke = std::min(ke, n0 + GB_N);
+      if (ke > kb) f += 2.0 * std::min(GB_M, s.M - m0) * std::min(GB_N, s.N - n0) * (double)(ke - kb);
+    }
+  return f;
+}
+
 template <bool TA, bool TB, class Epi>
 void gemm_launch(const GemmShape& s, const Epi& epi, cudaStream_t st) {
   if (s.M <= 0 || s.N <= 0) return;
+  ProfScope prof("gemm_dmma", st, prof_enabled() ? gemm_alg_flops(s) : 0.0);
   const int grid = gemm_grid(s);
   if (gemm_vec2_ok(s)) {
     auto k = gemm_dmma_kernel<TA, TB, 2, Epi>;

@@ -127,6 +127,7 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
   const int n = p.n;
   const long nn = (long)n * n;
   kot_require(rn > 0.0, KOT_EINVAL, "direction requires a nonzero residual");
+  ProfScope ps("newton", p.st);
   // filt = r2 + 𝒯[r2];  a1 = −r1 − Φ(filt)/(μ+1);  ã2 = −filt/(μ+1)   (newton.py:161-163)
   spectral_filter(p, dc, r2, p.M2, mu, 0);
   axpby(p, nn, 1.0, r2, 1.0, p.M2, b.filt);
@@ -222,6 +223,7 @@ static bool loop_body(Problem& p, const SolverCfg& cfg, LoopState& s, int k, Ite
   const int n = p.n;
   const long nn = (long)n * n;
   const auto t_it = clk::now();
+  ProfScope ps("ssn_iteration", p.st);
   double eg_ms = 0.0, resid_ms = 0.0;
   if (k % cfg.safeguard_every == 0) {
     auto t0 = clk::now();
@@ -384,6 +386,67 @@ SolveResult solve(Problem& p, const SolverCfg& cfg, IterCallback cb, void* user,
   out.total_ms = ms_since(t_start);
   return out;
 }
+
+// ---------------------------------------------------------------- sessions
+// A solve whose iterations are driven in chunks by the caller (bench.py times
+// W warm-up + K measured iterations of one continuous trajectory).
+struct Session {
+  Problem* p;
+  SolverCfg cfg;
+  LoopState s;
+  HostProbe hp;
+  int k = 0;
+  bool conv = false;
+};
+
+Session* session_begin(Problem& p, const SolverCfg& cfg) {
+  kot_require(cfg.residual_tol > 0.0 && cfg.max_iter >= 1 && cfg.safeguard_every >= 1 && cfg.eg_stepsize > 0.0,
+              KOT_EINVAL, "invalid solver configuration");
+  Bufs& b = p.bufs();
+  auto* se = new Session();
+  se->p = &p;
+  se->cfg = cfg;
+  init_state(p, se->s);
+  const double res0 = residual_parts(p, b.gw, b.Xw, b.r1w, b.r2w, se->s.dw);
+  se->s.res_w = se->s.res_v = res0;
+  se->s.theta = cfg.theta0;
+  se->conv = res0 <= cfg.residual_tol;
+  if (!std::isfinite(res0)) {
+    delete se;
+    throw KotError(KOT_ENUMERICS, "non-finite residual in solver iterate");
+  }
+  return se;
+}
+
+int session_step(Session& se, int iters, IterRecord* recs) {
+  int done = 0;
+  for (int i = 0; i < iters && !se.conv && se.k < se.cfg.max_iter; ++i) {
+    IterRecord rec{};
+    if (!loop_body(*se.p, se.cfg, se.s, se.k, rec, nullptr, nullptr, &se.hp))
+      throw KotError(KOT_ENUMERICS, "non-finite residual in solver iterate");
+    if (recs) recs[done] = rec;
+    ++done;
+    ++se.k;
+    se.conv = se.s.res_w <= se.cfg.residual_tol;
+  }
+  return done;
+}
+
+void session_result(Session& se, double* gamma, double* x, SolveResult& out) {
+  Problem& p = *se.p;
+  Bufs& b = p.bufs();
+  out.status = KOT_OK;
+  out.converged = se.conv ? 1 : 0;
+  out.iterations = se.k;
+  out.residual_norm = se.s.res_w;
+  out.ot_estimate = p.has_embed ? (p.q_sq - dev_dot(p, b.gw, p.embed, p.n)) / (2.0 * p.l2) : NAN;
+  if (gamma) KOT_CUDA(cudaMemcpyAsync(gamma, b.gw, sizeof(double) * p.n, cudaMemcpyDeviceToHost, p.st));
+  if (x) KOT_CUDA(cudaMemcpyAsync(x, b.Xw, sizeof(double) * (long)p.n * p.n, cudaMemcpyDeviceToHost, p.st));
+  KOT_CUDA(cudaStreamSynchronize(p.st));
+  out.total_ms = 0.0;
+}
+
+void session_end(Session* se) { delete se; }
 
 IterRecord iterate_once(Problem& p, const SolverCfg& cfg, const ReplayIn& in, ReplayOut& out) {
   Bufs& b = p.bufs();

@@ -339,6 +339,7 @@ void phi_adjoint_ex(Problem& p, const double* g, double* out, double alpha, cons
 void phi_adjoint(Problem& p, const double* g, double* out) { phi_adjoint_ex(p, g, out, 1.0, nullptr, 0.0, 0.0); }
 
 void eigh(Problem& p, const double* Z, Decomp& dc) {
+  ProfScope ps("eigh", p.st, 14.0 / 3.0 * p.n * (double)p.n * p.n);
   syevd_device(Z, p.n, dc.P, dc.vals, p.dk, *p.eig, p.st);
   KOT_CUDA(cudaMemcpyAsync(p.hk, p.dk, sizeof(int), cudaMemcpyDeviceToHost, p.st));
   KOT_CUDA(cudaStreamSynchronize(p.st));
@@ -420,6 +421,7 @@ void spectral_filter(Problem& p, const Decomp& dc, const double* S, double* out,
 }
 
 double residual_parts(Problem& p, const double* g, const double* X, double* r1, double* r2, Decomp& dc) {
+  ProfScope ps("residual", p.st);
   const int n = p.n;
   const long nn = (long)n * n;
   phi_partials(p, X);
@@ -435,6 +437,9 @@ double residual_parts(Problem& p, const double* g, const double* X, double* r1, 
 }
 
 void middle_operator(Problem& p, const Decomp& dc, double mu, const double* v, double* out) {
+  // F_mv = ℓ³ + 8kℓ² + 2ℓ², k = min(|α|, |ᾱ|)
+  const double n = p.n, kk = std::min(dc.k, p.n - dc.k);
+  ProfScope ps("matvec", p.st, n * n * n + 8.0 * kk * n * n + 2.0 * n * n);
   phi_adjoint(p, v, p.M1);
   spectral_filter(p, dc, p.M1, p.M2, mu, 0);
   phi_partials(p, p.M2);
@@ -442,6 +447,7 @@ void middle_operator(Problem& p, const Decomp& dc, double mu, const double* v, d
 }
 
 void eg_step(Problem& p, const double* g, const double* X, double s, double* g_out, double* X_out) {
+  ProfScope ps("eg_step", p.st);
   Bufs& b = p.bufs();
   const int n = p.n;
   Decomp dc{b.Pe, b.vale, 0};

@@ -135,4 +135,10 @@ struct ReplayOut {
 };
 IterRecord iterate_once(Problem& p, const SolverCfg& cfg, const ReplayIn& in, ReplayOut& out);
 
+struct Session;
+Session* session_begin(Problem& p, const SolverCfg& cfg);
+int session_step(Session& se, int iters, IterRecord* recs);
+void session_result(Session& se, double* gamma, double* x, SolveResult& out);
+void session_end(Session* se);
+
 }  // namespace kot

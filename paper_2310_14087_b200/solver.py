@@ -168,3 +168,53 @@ def iterate(pd: ProblemData, cfg: SolverConfig, w: IteratePair, v: IteratePair, 
                                       _lib.ptr(_lib.f64(v.x_mat)), float(theta), int(k), _lib.ptr(wg),
                                       _lib.ptr(wx), _lib.ptr(vg), _lib.ptr(vx), C.byref(th), C.byref(rec)))
     return IteratePair(wg, wx), IteratePair(vg, vx), float(th.value), _record(rec)
+
+
+class Session:
+    """A solve driven in chunks on device-resident state (used by bench.py).
+
+    ``step(k)`` runs k loop bodies of Algorithm 2 continuing the same trajectory;
+    ``stream`` is the CUDA stream every kernel of this problem is launched on.
+    """
+
+    def __init__(self, pd: ProblemData, cfg: SolverConfig):
+        self.pd = pd
+        self.cfg = cfg
+        self._dp = pd.device_problem()
+        self._c = cfg.to_c()
+        h = C.c_void_p(0)
+        _lib.check(_lib.lib().kot_session_begin(self._dp.handle, C.byref(self._c), C.byref(h)))
+        self._h = h
+        self.records: list[IterationRecord] = []
+
+    @property
+    def stream(self) -> int:
+        return int(_lib.lib().kot_problem_stream(self._dp.handle) or 0)
+
+    def step(self, iters: int) -> int:
+        recs = (_lib.IterRecordC * max(iters, 1))()
+        done = C.c_int(0)
+        _lib.check(_lib.lib().kot_session_step(self._h, int(iters), recs, C.byref(done)))
+        self.records.extend(_record(recs[i]) for i in range(done.value))
+        return int(done.value)
+
+    def result(self, want_x: bool = False) -> SolverReport:
+        n = self.pd.n
+        gamma = np.empty(n)
+        x = np.empty((n, n)) if want_x else None
+        rep = _lib.ReportC()
+        _lib.check(_lib.lib().kot_session_result(self._h, _lib.ptr(gamma), _lib.ptr(x), C.byref(rep)))
+        ot = float(rep.ot_estimate) if self.pd.embed_sum is not None else None
+        return SolverReport(gamma, x, ot, float(rep.residual_norm), CONVERGED if rep.converged else MAX_ITER,
+                            list(self.records), float("nan"))
+
+    def close(self):
+        if self._h:
+            _lib.lib().kot_session_end(self._h)
+            self._h = C.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
