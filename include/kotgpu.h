@@ -151,9 +151,10 @@ int kot_phi_adjoint(kot_problem* p, const double* gamma, double* out);  /* probl
 /* residual_parts (problem.py:204-214): r1, r2, eigenvalues of Z, n_pos, ||r||. */
 int kot_residual_parts(kot_problem* p, const double* gamma, const double* x, double* r1, double* r2,
                        double* eigvals, int* n_pos, double* res_norm);
-/* middle_operator (newton.py:116-128) at the context of w with damping theta. */
+/* middle_operator (newton.py:116-128) at the context of w with damping theta.
+ * form 0: structure-reduced B = R·P form used by the solver; 1: reference form Φ(𝒯[Φ*(v)]). */
 int kot_middle_operator(kot_problem* p, const double* gamma, const double* x, double theta,
-                        const double* v, double* out, double* mu_out);
+                        const double* v, int form, double* out, double* mu_out);
 /* newton_direction (newton.py:144-195) at w with damping theta. */
 int kot_newton_direction(kot_problem* p, const kot_solver_cfg* cfg, const double* gamma,
                          const double* x, double theta, double* dgamma, double* dx, int* cg_iters,

@@ -82,7 +82,7 @@ _SIGS = {
     "kot_phi_forward": (C.c_int, [C.c_void_p, dptr, dptr]),
     "kot_phi_adjoint": (C.c_int, [C.c_void_p, dptr, dptr]),
     "kot_residual_parts": (C.c_int, [C.c_void_p, dptr, dptr, dptr, dptr, dptr, iptr, dptr]),
-    "kot_middle_operator": (C.c_int, [C.c_void_p, dptr, dptr, C.c_double, dptr, dptr, dptr]),
+    "kot_middle_operator": (C.c_int, [C.c_void_p, dptr, dptr, C.c_double, dptr, C.c_int, dptr, dptr]),
     "kot_newton_direction": (C.c_int, [C.c_void_p, C.POINTER(SolverCfgC), dptr, dptr, C.c_double, dptr, dptr,
                                        iptr, iptr, dptr, dptr]),
     "kot_eg_step": (C.c_int, [C.c_void_p, dptr, dptr, C.c_double, dptr, dptr]),

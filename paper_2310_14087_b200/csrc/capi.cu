@@ -373,7 +373,7 @@ int kot_residual_parts(kot_problem* h, const double* gamma, const double* x, dou
 }
 
 int kot_middle_operator(kot_problem* h, const double* gamma, const double* x, double theta, const double* v,
-                        double* out, double* mu_out) {
+                        int form, double* out, double* mu_out) {
   return guarded([&] {
     kot::Problem& p = *h->p;
     KOT_CUDA(cudaSetDevice(p.device));
@@ -386,7 +386,13 @@ int kot_middle_operator(kot_problem* h, const double* gamma, const double* x, do
     kot::kot_require(res > 0.0, kot::KOT_EINVAL, "context requires a nonzero residual");
     const double mu = theta * res;
     up(p, b.e2, v, p.n);
-    kot::middle_operator(p, dc, mu, b.e2, b.e1);
+    if (form == 1) {
+      kot::middle_operator(p, dc, mu, b.e2, b.e1);  // reference form Φ(𝒯[Φ*(v)])
+    } else {
+      kot::MvCtx mv;
+      kot::matvec_prepare(p, dc, mu, mv);
+      kot::middle_operator_fast(p, mv, b.e2, b.e1);  // structure-reduced form (the solver's)
+    }
     down(p, out, b.e1, p.n);
     KOT_CUDA(cudaStreamSynchronize(p.st));
     if (mu_out) *mu_out = mu;

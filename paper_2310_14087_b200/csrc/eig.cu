@@ -32,7 +32,7 @@ namespace cg = cooperative_groups;
 namespace kot {
 
 constexpr int TRD_NB = 32;
-constexpr int TRD_THREADS = 256;
+constexpr int TRD_THREADS = 512;
 constexpr int TRD_WARPS = TRD_THREADS / 32;
 constexpr int TRD_PSTRIDE = 2 * TRD_NB + 2;
 constexpr int DC_LEAF = 32;
@@ -53,8 +53,10 @@ EigWork::EigWork(int n_) : n(n_) {
   alloc(&yv, n);
   alloc(&part, (long)kNumSMs * TRD_PSTRIDE);
   alloc(&partn, kNumSMs);
-  alloc(&Tf, TRD_NB * TRD_NB * 2);
-  alloc(&W1, (long)TRD_NB * n * 2);
+  alloc(&Tf, 256L * 256 * 2);
+  alloc(&W1, 256L * n * 2);
+  splitws_cap = 16L * 256 * n;
+  alloc(&splitws, splitws_cap);
   alloc(&Q, nn);
   alloc(&Qw, nn);
   alloc(&Qnd, nn);
@@ -75,7 +77,7 @@ EigWork::EigWork(int n_) : n(n_) {
 
 EigWork::~EigWork() {
   for (double* p : {A, Vall, X, d, e, tau, xv, yv, part, partn, Tf, W1, Q, Qw, Qnd, Dl, zs, ds, dlam, wv, what, lam,
-                    dfv, rotcs, rho})
+                    dfv, rotcs, rho, splitws})
     cudaFree(p);
   cudaFree(ibuf);
   cudaFree(dbuf);
@@ -123,11 +125,13 @@ __global__ void __launch_bounds__(TRD_THREADS) sytrd_panel_kernel(TrdArgs a) {
     // ------------------------------------------------------------ phase Q
     if (jj > 0) {
       const int m = jj - 1;  // t-range of the previous column's corrections
-      for (int q = threadIdx.x; q < TRD_PSTRIDE; q += blockDim.x) {
+      // warp-parallel, fixed-order reduction of the per-CTA partials (t1, t2, yᵀv)
+      for (int q = wid; q <= 2 * TRD_NB; q += TRD_WARPS) {
         double s = 0.0;
         if (q < m || (q >= TRD_NB && q < TRD_NB + m) || q == 2 * TRD_NB)
-          for (int g = 0; g < G; ++g) s += a.part[(long)g * TRD_PSTRIDE + q];
-        tred[q] = s;
+          for (int g = lane; g < G; g += 32) s += a.part[(long)g * TRD_PSTRIDE + q];
+        s = warp_sum(s);
+        if (lane == 0) tred[q] = s;
       }
       __syncthreads();
       // α = −½ τ (wᵀv),  wᵀv = τ (yᵀv − 2 t1·t2)
@@ -178,8 +182,14 @@ __global__ void __launch_bounds__(TRD_THREADS) sytrd_panel_kernel(TrdArgs a) {
     }
     grid.sync();
     // ------------------------------------------------------------ phase S
-    double xn2 = 0.0;
-    for (int g = 0; g < G; ++g) xn2 += a.partn[g];
+    if (wid == 0) {
+      double s = 0.0;
+      for (int g = lane; g < G; g += 32) s += a.partn[g];
+      s = warp_sum(s);
+      if (lane == 0) nrm_sh[0] = s;
+    }
+    __syncthreads();
+    const double xn2 = nrm_sh[0];
     const double alpha = a.xv[c + 1];
     double beta, tau, scale;
     if (xn2 == 0.0) {  // dlarfg: H = I
@@ -203,8 +213,15 @@ __global__ void __launch_bounds__(TRD_THREADS) sytrd_panel_kernel(TrdArgs a) {
     for (int r = (c + 1) + ((gw - c - 1) % NW + NW) % NW; r < n; r += NW) {
       const double vr = vsh[r - c - 1];
       const double* Ar = a.A + (long)r * n + c + 1;
-      double y = 0.0;
-      for (int s = lane; s < m; s += 32) y += Ar[s] * vsh[s];
+      // 8 independent loads in flight per lane (the symv is L2-latency bound)
+      double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      int s = lane;
+      for (; s + 7 * 32 < m; s += 8 * 32) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] += Ar[s + u * 32] * vsh[s + u * 32];
+      }
+      for (; s < m; s += 32) acc[0] += Ar[s] * vsh[s];
+      double y = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
       y = warp_sum(y);
       if (lane == 0) {
         a.yv[r] = y;
@@ -868,21 +885,28 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
 
 // ====================================================== back-transform
 
-// T factor of the forward block reflector (dlarft 'F','C') from S = VᵀV.
-__global__ void larft_kernel(const double* S, const double* tau, int nb, double* T) {
-  __shared__ double Ts[TRD_NB][TRD_NB + 1];
-  const int lane = threadIdx.x;
+// T factor of the forward block reflector (dlarft 'F','C') from S = VᵀV:
+// T[i][i] = τ_i, T[0:i, i] = −τ_i T[0:i,0:i] S[0:i, i].  One thread per row,
+// sequential over the nb ≤ 128 columns; T and S staged in shared memory.
+constexpr int ORM_NB = 128;
+constexpr int LARFT_SMEM = ORM_NB * (ORM_NB + 1) * 8;
+
+// S is symmetric, so column i is read as row i (coalesced across threads).
+__global__ void larft_kernel(const double* __restrict__ S, const double* tau, int nb, double* T) {
+  extern __shared__ double lsm[];
+  double* Ts = lsm;  // [nb][nb+1]
+  const int ld = ORM_NB + 1;
+  const int j = threadIdx.x;  // row of T
   for (int i = 0; i < nb; ++i) {
     double tmp = 0.0;
-    if (lane < i)
-      for (int k = lane; k < i; ++k) tmp += Ts[lane][k] * S[k * nb + i];
-    __syncwarp();
-    if (lane < i) Ts[lane][i] = -tau[i] * tmp;
-    if (lane == i) Ts[i][i] = tau[i];
-    if (lane > i && lane < nb) Ts[lane][i] = 0.0;
-    __syncwarp();
+    if (j < i)
+      for (int k = j; k < i; ++k) tmp += Ts[j * ld + k] * __ldg(S + (long)i * nb + k);
+    if (j < i) Ts[j * ld + i] = -tau[i] * tmp;
+    if (j == i) Ts[i * ld + i] = tau[i];
+    if (j > i && j < nb) Ts[j * ld + i] = 0.0;
+    __syncthreads();
   }
-  for (int e = lane; e < nb * nb; e += 32) T[e] = Ts[e / nb][e % nb];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) T[e] = Ts[(e / nb) * ld + e % nb];
 }
 
 __global__ void reverse_cols_kernel(const double* Q, const double* dasc, double* P, double* vals, int n) {
@@ -909,39 +933,50 @@ __global__ void count_pos_kernel(const double* vals, int n, int* k) {
   }
 }
 
+// Back-transform P ← H_0 H_1 ⋯ H_{n−2} P in compact-WY blocks of ORM_NB
+// reflectors (I − V T Vᵀ), last block first: W1 = Vᵀ P (split-K), W2 = T W1,
+// P −= V W2.
 static void ormtr(int n, EigWork& w, double* P, cudaStream_t st) {
-  const int npan = (n - 1 + TRD_NB - 1) / TRD_NB;
-  for (int pi = npan - 1; pi >= 0; --pi) {
-    const int p0 = pi * TRD_NB;
-    const int nb = std::min(TRD_NB, n - 1 - p0);
+  const int nref = n - 1;  // reflectors 0..n-2
+  const int nblk = (nref + ORM_NB - 1) / ORM_NB;
+  double* S = w.Tf + ORM_NB * ORM_NB;
+  double* T = w.Tf;
+  double* W1 = w.W1;
+  double* W2 = w.W1 + (long)ORM_NB * n;
+  static bool attr = false;
+  if (!attr) {
+    KOT_CUDA(cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LARFT_SMEM));
+    attr = true;
+  }
+  for (int bi = nblk - 1; bi >= 0; --bi) {
+    const int p0 = bi * ORM_NB;
+    const int nb = std::min(ORM_NB, nref - p0);
     const int r0 = p0 + 1;
     const int mrows = n - r0;
-    const double* Vp = w.Vall + (long)r0 * n + p0;  // mrows × nb (ld n)
-    // S = Vᵀ V
-    {
+    const double* Vp = w.Vall + (long)r0 * n + p0;  // mrows × nb (ld n), zero above each unit entry
+    {  // S = Vᵀ V  (symmetric, one triangle mirrored)
       GemmShape s = make_shape(nb, nb, mrows, Vp, n, Vp, n);
-      EpiAxpby epi{w.Tf + TRD_NB * TRD_NB, nb, 1.0, 0.0};
-      gemm_launch<true, false>(s, epi, st);
+      s.sym_tiles = 1;
+      s.ws = w.splitws;
+      s.ksplit = choose_ksplit(s, w.splitws_cap);
+      gemm_launch<true, false>(s, EpiSymMirror{S, nb, 1.0, nullptr, 0.0, 0.0}, st);
     }
-    larft_kernel<<<1, 32, 0, st>>>(w.Tf + TRD_NB * TRD_NB, w.tau + p0, nb, w.Tf);
+    larft_kernel<<<1, ((nb + 31) / 32) * 32, LARFT_SMEM, st>>>(S, w.tau + p0, nb, T);
     KOT_LAUNCH_CHECK();
-    // W1 = Vᵀ P[r0:, :]
-    {
+    {  // W1 = Vᵀ P[r0:, :]
       GemmShape s = make_shape(nb, n, mrows, Vp, n, P + (long)r0 * n, n);
-      EpiAxpby epi{w.W1, n, 1.0, 0.0};
-      gemm_launch<true, false>(s, epi, st);
+      s.ws = w.splitws;
+      s.ksplit = choose_ksplit(s, w.splitws_cap);
+      gemm_launch<true, false>(s, EpiAxpby{W1, n, 1.0, 0.0}, st);
     }
-    // W2 = T W1
-    {
-      GemmShape s = make_shape(nb, n, nb, w.Tf, nb, w.W1, n);
-      EpiAxpby epi{w.W1 + (long)TRD_NB * n, n, 1.0, 0.0};
-      gemm_launch<false, false>(s, epi, st);
+    {  // W2 = T W1   (T upper triangular: K range starts at the row tile)
+      GemmShape s = make_shape(nb, n, nb, T, nb, W1, n);
+      s.kb_m = 1;
+      gemm_launch<false, false>(s, EpiAxpby{W2, n, 1.0, 0.0}, st);
     }
-    // P[r0:, :] -= V W2
-    {
-      GemmShape s = make_shape(mrows, n, nb, Vp, n, w.W1 + (long)TRD_NB * n, n);
-      EpiAxpby epi{P + (long)r0 * n, n, -1.0, 1.0};
-      gemm_launch<false, false>(s, epi, st);
+    {  // P[r0:, :] −= V W2
+      GemmShape s = make_shape(mrows, n, nb, Vp, n, W2, n);
+      gemm_launch<false, false>(s, EpiAxpby{P + (long)r0 * n, n, -1.0, 1.0}, st);
     }
   }
 }

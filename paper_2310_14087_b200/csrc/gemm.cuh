@@ -43,7 +43,10 @@ struct GemmShape {
   //   k_end   = min(K, ke_m ? m0+BM : K, ke_n ? n0+BN : K)
   int kb_m, kb_n, ke_m, ke_n;
   int sym_tiles;  // enumerate only tiles with tm <= tn (symmetric outputs)
-  int batch_stride_unused;
+  // split-K: grid.y = ksplit partial products written to ws[split][M][N] (ld N),
+  // then reduced in fixed order by splitk_reduce_kernel (deterministic).
+  int ksplit;
+  double* ws;
 };
 
 __device__ __forceinline__ void cp_async_16(void* smem, const void* gmem, int src_bytes) {
@@ -123,7 +126,13 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
   if (s.ke_m) kend = min(kend, m0 + GB_M);
   if (s.ke_n) kend = min(kend, n0 + GB_N);
   kbeg = (kbeg / GB_K) * GB_K;
-  const int nkt = kend > kbeg ? (kend - kbeg + GB_K - 1) / GB_K : 0;
+  int nkt = kend > kbeg ? (kend - kbeg + GB_K - 1) / GB_K : 0;
+  if (s.ksplit > 1) {  // this CTA's share of the K tiles
+    const int per = (nkt + s.ksplit - 1) / s.ksplit;
+    const int t0 = blockIdx.y * per;
+    kbeg += t0 * GB_K;
+    nkt = max(0, min(per, nkt - t0));
+  }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -217,6 +226,20 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
       const int r = m0 + threadIdx.x;
       if (r < s.M) epi.rowdot_store(tn, r, red[threadIdx.x] + red[GB_M + threadIdx.x]);
     }
+  } else if (s.ksplit > 1) {
+    double* ws = s.ws + (long)blockIdx.y * s.M * s.N;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const int r = m0 + wm + i * 8 + g;
+      if (r >= s.M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int c = n0 + wn + j * 8 + 2 * t + h;
+          if (c < s.N) ws[(long)r * s.N + c] = acc[i][j][h];
+        }
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < 4; i++) {
@@ -230,6 +253,19 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
           if (c < s.N) epi.store(r, c, acc[i][j][h]);
         }
     }
+  }
+}
+
+template <class Epi>
+__global__ void splitk_reduce_kernel(int M, int N, int splits, int sym_tiles, const double* __restrict__ ws,
+                                     Epi epi) {
+  const long total = (long)M * N;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / N), c = (int)(e % N);
+    if (sym_tiles && r / GB_M > c / GB_N) continue;
+    double v = 0.0;
+    for (int sp = 0; sp < splits; ++sp) v += ws[(long)sp * total + e];
+    epi.store(r, c, v);
   }
 }
 
@@ -266,7 +302,8 @@ template <bool TA, bool TB, class Epi>
 void gemm_launch(const GemmShape& s, const Epi& epi, cudaStream_t st) {
   if (s.M <= 0 || s.N <= 0) return;
   ProfScope prof("gemm_dmma", st, prof_enabled() ? gemm_alg_flops(s) : 0.0);
-  const int grid = gemm_grid(s);
+  const int tiles = gemm_grid(s);
+  const dim3 grid(tiles, s.ksplit > 1 ? s.ksplit : 1);
   if (gemm_vec2_ok(s)) {
     auto k = gemm_dmma_kernel<TA, TB, 2, Epi>;
     static bool attr = false;
@@ -285,6 +322,25 @@ void gemm_launch(const GemmShape& s, const Epi& epi, cudaStream_t st) {
     k<<<grid, G_THREADS, G_SMEM_BYTES, st>>>(s, epi);
   }
   KOT_LAUNCH_CHECK();
+  if constexpr (!Epi::kRowDot) {
+    if (s.ksplit > 1) {
+      const long total = (long)s.M * s.N;
+      splitk_reduce_kernel<Epi><<<(int)std::min<long>((total + 255) / 256, 4L * 148 * 8), 256, 0, st>>>(
+          s.M, s.N, s.ksplit, s.sym_tiles, s.ws, epi);
+      KOT_LAUNCH_CHECK();
+    }
+  }
+}
+
+// Pick a split-K factor so that skinny / few-tile GEMMs fill the 148 SMs.
+// ws must hold ksplit·M·N doubles; returns 1 when splitting does not pay.
+inline int choose_ksplit(const GemmShape& s, long ws_capacity) {
+  const int tiles = gemm_grid(s);
+  if (tiles >= 120 || s.K < 512 || s.ws == nullptr) return 1;
+  int ks = std::min((2 * 148 + tiles - 1) / tiles, s.K / 256);
+  ks = std::min(ks, 16);
+  while (ks > 1 && (long)ks * s.M * s.N > ws_capacity) --ks;
+  return std::max(ks, 1);
 }
 
 inline GemmShape make_shape(int M, int N, int K, const double* A, long lda, const double* B, long ldb) {
@@ -296,6 +352,8 @@ inline GemmShape make_shape(int M, int N, int K, const double* A, long lda, cons
   s.lda = lda;
   s.B = B;
   s.ldb = ldb;
+  s.ksplit = 1;
+  s.ws = nullptr;
   return s;
 }
 

@@ -8,6 +8,8 @@
 // the control flow (norms, pAp, flags) cross to the host.
 #include <chrono>
 #include <cmath>
+#include <exception>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -89,7 +91,7 @@ struct CgOut {
 };
 
 // x (= b.cx) solves A x = rhs to tol·‖rhs‖ with A = middle operator.
-static CgOut cg_solve(Problem& p, const Decomp& dc, double mu, const double* rhs, double tol, int max_iter) {
+static CgOut cg_solve(Problem& p, const MvCtx& mv, const double* rhs, double tol, int max_iter) {
   Bufs& b = p.bufs();
   const int n = p.n;
   kot_require(max_iter >= 1, KOT_EINVAL, "max_iter must be >= 1");
@@ -101,7 +103,7 @@ static CgOut cg_solve(Problem& p, const Decomp& dc, double mu, const double* rhs
   if (res <= target) return {0, res};
   int it = 0;
   for (it = 1; it <= max_iter; ++it) {
-    middle_operator(p, dc, mu, b.cp, b.cap);
+    middle_operator_fast(p, mv, b.cp, b.cap);
     cg_step_kernel<<<1, CG_THREADS, 0, p.st>>>(n, b.cx, b.cr, b.cp, b.cap, p.dsc);
     KOT_LAUNCH_CHECK();
     fetch(p, 16);
@@ -137,19 +139,21 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
   double rel = cfg.has_cg_tol ? cfg.cg_tol : cfg.tau * std::min(1.0, cfg.kappa * rn);
   const double a1n = dev_norm(p, b.a1, n);
   KOT_CUDA(cudaMemsetAsync(b.sol, 0, sizeof(double) * n, p.st));
+  MvCtx mv;
+  matvec_prepare(p, dc, mu, mv);
   NewtonOut out{0, 0, 0, INFINITY, 0.0, 0.0};
   const auto t0 = clk::now();
   for (int att = 0; att <= cfg.cg_restarts; ++att) {
     out.attempts = att + 1;
     const double* rhs = b.a1;
     if (att) {
-      middle_operator(p, dc, mu, b.sol, b.e3);
+      middle_operator_fast(p, mv, b.sol, b.e3);
       axpby(p, n, 1.0, b.a1, -1.0, b.e3, b.rhs);
       rhs = b.rhs;
     }
     const double bn = dev_norm(p, rhs, n);
     if (bn > 0.0 && a1n > 0.0) {
-      const CgOut c = cg_solve(p, dc, mu, rhs, rel * a1n / bn, cfg.cg_max);
+      const CgOut c = cg_solve(p, mv, rhs, rel * a1n / bn, cfg.cg_max);
       axpby(p, n, 1.0, b.sol, 1.0, b.cx, b.sol);
       out.cg_iters += c.iters;
     }
@@ -225,28 +229,55 @@ static bool loop_body(Problem& p, const SolverCfg& cfg, LoopState& s, int k, Ite
   const auto t_it = clk::now();
   ProfScope ps("ssn_iteration", p.st);
   double eg_ms = 0.0, resid_ms = 0.0;
-  if (k % cfg.safeguard_every == 0) {
-    auto t0 = clk::now();
-    eg_step(p, b.gv, b.Xv, cfg.eg_stepsize, b.gv, b.Xv);
-    KOT_CUDA(cudaStreamSynchronize(p.st));
-    eg_ms = ms_since(t0);
-    t0 = clk::now();
-    s.res_v = residual_parts(p, b.gv, b.Xv, b.r1v, b.r2v, s.dv);
-    resid_ms += ms_since(t0);
-    if (!std::isfinite(s.res_v)) return false;
+  // EG safeguard chain (eg.py:34-41 + residual at v) on the auxiliary stream,
+  // concurrently with the Newton chain below: the two only meet at acceptance
+  // (solver.py:186-192), so the arithmetic is unchanged.
+  const bool do_eg = (k % cfg.safeguard_every == 0);
+  std::exception_ptr eg_err = nullptr;
+  double eg_resid_ms = 0.0;
+  std::thread eg_thread;
+  if (do_eg) {
+    Problem& a = p.aux();
+    eg_thread = std::thread([&]() {
+      try {
+        KOT_CUDA(cudaSetDevice(a.device));
+        auto t0 = clk::now();
+        eg_step(a, b.gv, b.Xv, cfg.eg_stepsize, b.gv, b.Xv);
+        KOT_CUDA(cudaStreamSynchronize(a.st));
+        eg_ms = ms_since(t0);
+        t0 = clk::now();
+        s.res_v = residual_parts(a, b.gv, b.Xv, b.r1v, b.r2v, s.dv);
+        eg_resid_ms = ms_since(t0);
+      } catch (...) {
+        eg_err = std::current_exception();
+      }
+    });
   }
   auto t0 = clk::now();
-  kot_require(s.res_w > 0.0, KOT_EINVAL, "context requires a nonzero residual");
-  const double mu = s.theta * s.res_w;
-  kot_require(mu > 0.0, KOT_EINVAL, "regularization mu must be positive");
-  const NewtonOut st = newton_direction(p, b.r1w, b.r2w, s.res_w, s.dw, mu, cfg, b.dg, b.dX);
-  KOT_CUDA(cudaStreamSynchronize(p.st));
-  const double newton_ms = ms_since(t0);
-  axpby(p, n, 1.0, b.gw, 1.0, b.dg, b.gt);
-  axpby(p, nn, 1.0, b.Xw, 1.0, b.dX, b.Xt);
-  t0 = clk::now();
-  const double res_t = residual_parts(p, b.gt, b.Xt, b.r1t, b.r2t, s.dt);
-  resid_ms += ms_since(t0);
+  NewtonOut st{};
+  double mu = 0.0, res_t = 0.0;
+  std::exception_ptr nt_err = nullptr;
+  double newton_ms = 0.0;
+  try {
+    kot_require(s.res_w > 0.0, KOT_EINVAL, "context requires a nonzero residual");
+    mu = s.theta * s.res_w;
+    kot_require(mu > 0.0, KOT_EINVAL, "regularization mu must be positive");
+    st = newton_direction(p, b.r1w, b.r2w, s.res_w, s.dw, mu, cfg, b.dg, b.dX);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+    newton_ms = ms_since(t0);
+    axpby(p, n, 1.0, b.gw, 1.0, b.dg, b.gt);
+    axpby(p, nn, 1.0, b.Xw, 1.0, b.dX, b.Xt);
+    t0 = clk::now();
+    res_t = residual_parts(p, b.gt, b.Xt, b.r1t, b.r2t, s.dt);
+    resid_ms += ms_since(t0);
+  } catch (...) {
+    nt_err = std::current_exception();
+  }
+  if (eg_thread.joinable()) eg_thread.join();
+  if (eg_err) std::rethrow_exception(eg_err);
+  if (nt_err) std::rethrow_exception(nt_err);
+  resid_ms += eg_resid_ms;
+  if (do_eg && !std::isfinite(s.res_v)) return false;
   if (!std::isfinite(res_t)) return false;
   if (cb) {
     hp->wg.resize(n);

@@ -38,6 +38,8 @@ void Problem::init_scratch() {
   M4 = alloc(nn);
   M5 = alloc(nn);
   red = alloc(512 * 16);
+  splitws_cap = 16L * 256 * n;
+  splitws = alloc(splitws_cap);
   dsc = alloc(64);
   KOT_CUDA(cudaMallocHost(&hsc, 64 * sizeof(double)));
   KOT_CUDA(cudaMalloc(&dk, 16 * sizeof(int)));
@@ -48,6 +50,7 @@ void Problem::init_scratch() {
 
 Problem::~Problem() {
   if (st) cudaStreamSynchronize(st);
+  aux_.reset();
   eig.reset();
   for (double* p : owned) cudaFree(p);
   if (hsc) cudaFreeHost(hsc);
@@ -246,13 +249,14 @@ void jac_bottom(Problem& p, long count, const double* a, const double* b, double
 
 
 struct FinArgs {
-  int n, mode, tiles;
+  int n, mode, tiles, tri;
   const double* Q;
+  const double* G2;  // nullable: + (G2·u)/μ  (structure-reduced NONPOS matvec)
   const double* u;
   const double* partial;
   const double* z;
   const double* r1;
-  double l2, mu;
+  double l2, mu, phsign;
   double* out;
 };
 
@@ -261,14 +265,19 @@ __global__ void finalize_kernel(FinArgs f) {
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < f.n; r += gridDim.x * warps) {
-    double qv = 0.0, ph = 0.0;
+    double qv = 0.0, ph = 0.0, gv = 0.0;
     if (f.Q) {
       const double* qr = f.Q + (long)r * f.n;
       for (int c = lane; c < f.n; c += 32) qv += qr[c] * f.u[c];
       qv = warp_sum(qv);
     }
+    if (f.G2) {
+      const double* gr = f.G2 + (long)r * f.n;
+      for (int c = lane; c < f.n; c += 32) gv += gr[c] * f.u[c];
+      gv = warp_sum(gv);
+    }
     if (f.partial) {
-      for (int tn = r / GB_N + lane; tn < f.tiles; tn += 32) ph += f.partial[(long)tn * f.n + r];
+      for (int tn = (f.tri ? r / GB_N : 0) + lane; tn < f.tiles; tn += 32) ph += f.partial[(long)tn * f.n + r];
       ph = warp_sum(ph);
     }
     if (lane) continue;
@@ -277,6 +286,11 @@ __global__ void finalize_kernel(FinArgs f) {
     switch (f.mode) {
       case FIN_RES: o = __dsub_rn(__dsub_rn(qv, f.z[r]) / two_l2, ph); break;
       case FIN_MATVEC: o = __dadd_rn(__dadd_rn(qv / two_l2, __dmul_rn(f.mu, f.u[r])), ph); break;
+      case FIN_MATVEC_B: {
+        const double mid = f.G2 ? __dadd_rn(gv / f.mu, -ph) : ph;
+        o = __dadd_rn(__dadd_rn(qv / two_l2, __dmul_rn(f.mu, f.u[r])), mid);
+        break;
+      }
       case FIN_A1: o = __dsub_rn(-f.r1[r], ph / (f.mu + 1.0)); break;
       case FIN_JTOP:
         o = __dadd_rn(__dsub_rn(__dadd_rn(qv / two_l2, __dmul_rn(f.mu, f.u[r])), ph), f.r1[r]);
@@ -295,6 +309,9 @@ void finalize(Problem& p, int mode, const double* u, bool with_phi, const double
   f.n = p.n;
   f.mode = mode;
   f.tiles = ceil_div(p.n, GB_N);
+  f.tri = 1;
+  f.G2 = nullptr;
+  f.phsign = 1.0;
   const bool need_q = (mode == FIN_RES || mode == FIN_MATVEC || mode == FIN_JTOP || mode == FIN_GRAD || mode == FIN_QV);
   f.Q = need_q ? p.Q : nullptr;
   f.u = u;
@@ -305,6 +322,125 @@ void finalize(Problem& p, int mode, const double* u, bool with_phi, const double
   f.mu = mu;
   f.out = out;
   finalize_kernel<<<std::min(ceil_div(p.n, 8), 8 * kNumSMs), 256, 0, p.st>>>(f);
+  KOT_LAUNCH_CHECK();
+}
+
+// ------------------------------------------- structure-reduced middle operator
+//
+// With B = R·P (once per outer iteration), Φ(𝒯[Φ*(v)])_i = b_i T̂ b_iᵀ where
+// T̂ = W∘(Bᵀ diag(v) B) and W is the eliminator's coefficient matrix in the
+// eigenbasis (W_αα = 1/μ, W_αᾱ = ξ, W_ᾱᾱ = 0; psdcone.py:113-121).  Only the
+// rows of the smaller sign block are needed:
+//   POS    (k ≤ ℓ−k): C = B_αᵀ D B (k×ℓ); T̃ = W∘C with ᾱ columns doubled;
+//                     y_i = Σ_a (B T̃ᵀ)_ia B_ia
+//   NONPOS (k > ℓ−k): W = (1/μ)·1 − W', W' supported on ᾱ rows/cols:
+//                     y = (G2 v)/μ − rowquad(B, W'∘C'),  G2 = (RRᵀ)∘(RRᵀ)
+// 4·min(k, ℓ−k)·ℓ² FLOPs per matvec instead of ℓ³ + 8kℓ² (two DMMA GEMMs).
+struct EpiMvCoef {
+  static constexpr bool kRowDot = false;
+  double* C;
+  long ldc;
+  const double* vals;
+  int k, pos;
+  double mu;
+  __device__ void store(int r, int c, double v) const {
+    double o;
+    if (pos) {  // row r = eigen index a ∈ α
+      if (c < k) {
+        o = v / mu;
+      } else {
+        const double sa = vals[r], sb = vals[c];
+        const double eta = sa / (sa - sb);
+        o = 2.0 * ((eta / (mu + 1.0 - eta)) * v);
+      }
+    } else {  // row r ↔ eigen index k + r ∈ ᾱ
+      if (c >= k) {
+        o = v / mu;
+      } else {
+        const double sa = vals[c], sb = vals[k + r];
+        const double eta = sa / (sa - sb);
+        o = 2.0 * ((1.0 / mu - eta / (mu + 1.0 - eta)) * v);
+      }
+    }
+    C[(long)r * ldc + c] = o;
+  }
+  __device__ double rowdot_weight(int, int) const { return 0; }
+  __device__ void rowdot_store(int, int, double) const {}
+};
+
+// G2 = (R Rᵀ) ∘ (R Rᵀ), once per problem (one triangle, mirrored).
+struct EpiSquareMirror {
+  static constexpr bool kRowDot = false;
+  double* C;
+  long ldc;
+  __device__ void store(int r, int c, double v) const {
+    if (r > c) return;
+    const double o = v * v;
+    C[(long)r * ldc + c] = o;
+    C[(long)c * ldc + r] = o;
+  }
+  __device__ double rowdot_weight(int, int) const { return 0; }
+  __device__ void rowdot_store(int, int, double) const {}
+};
+
+void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m) {
+  const int n = p.n;
+  Bufs& b = p.bufs();
+  m.dc = dc;
+  m.mu = mu;
+  m.pos = dc.k <= n - dc.k;
+  m.B = b.Bm;
+  {  // B = R P   (R upper triangular: K range starts at the row tile)
+    GemmShape s = make_shape(n, n, n, p.R, n, dc.P, n);
+    s.kb_m = 1;
+    gemm_launch<false, false>(s, EpiAxpby{b.Bm, n, 1.0, 0.0}, p.st);
+  }
+  if (!m.pos && p.G2 == nullptr) {
+    p.G2 = p.alloc((long)n * n);
+    GemmShape s = make_shape(n, n, n, p.R, n, p.R, n);  // (R Rᵀ)_ij = Σ_{k ≥ max(i,j)} R_ik R_jk
+    s.kb_m = 1;
+    s.kb_n = 1;
+    s.sym_tiles = 1;
+    gemm_launch<false, true>(s, EpiSquareMirror{p.G2, n}, p.st);
+  }
+}
+
+void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* out) {
+  const int n = p.n, k = m.dc.k;
+  const int ks = m.pos ? k : n - k;
+  const double nn = n;
+  ProfScope ps("matvec", p.st, 4.0 * ks * nn * nn + 2.0 * nn * nn);
+  Bufs& b = p.bufs();
+  if (ks > 0) {
+    const double* Bsub = m.pos ? m.B : m.B + k;
+    {  // C = B_subᵀ diag(v) B, coefficients in the epilogue → T̃ (ks × n)
+      GemmShape s = make_shape(ks, n, n, Bsub, n, m.B, n);
+      s.kscale = v;
+      s.ws = p.splitws;
+      s.ksplit = choose_ksplit(s, p.splitws_cap);
+      gemm_launch<true, false>(s, EpiMvCoef{b.Ct, n, m.dc.vals, k, m.pos ? 1 : 0, m.mu}, p.st);
+    }
+    {  // y_i = Σ_a (B T̃ᵀ)_ia B_sub[i][a]
+      GemmShape s = make_shape(n, ks, n, m.B, n, b.Ct, n);
+      gemm_launch<false, true>(s, EpiRowDot{Bsub, n, p.partial, n}, p.st);
+    }
+  }
+  FinArgs f;
+  f.n = n;
+  f.mode = FIN_MATVEC_B;
+  f.tiles = ks > 0 ? ceil_div(ks, GB_N) : 0;
+  f.tri = 0;
+  f.Q = p.Q;
+  f.G2 = m.pos ? nullptr : p.G2;
+  f.u = v;
+  f.partial = ks > 0 ? p.partial : nullptr;
+  f.z = p.z;
+  f.r1 = nullptr;
+  f.l2 = p.l2;
+  f.mu = m.mu;
+  f.phsign = 1.0;
+  f.out = out;
+  finalize_kernel<<<std::min(ceil_div(n, 8), 8 * kNumSMs), 256, 0, p.st>>>(f);
   KOT_LAUNCH_CHECK();
 }
 
@@ -466,13 +602,35 @@ void eg_step(Problem& p, const double* g, const double* X, double s, double* g_o
   proj(p, dc, nullptr, X_out);
 }
 
+Problem& Problem::aux() {
+  if (!aux_) {
+    KOT_CUDA(cudaSetDevice(device));
+    aux_.reset(new Problem());
+    Problem& a = *aux_;
+    a.n = n;
+    a.device = device;
+    a.l1 = l1;
+    a.l2 = l2;
+    a.q_sq = q_sq;
+    a.jitter = jitter;
+    a.has_embed = has_embed;
+    a.Q = Q;  // shared, not owned
+    a.z = z;
+    a.R = R;
+    a.embed = embed;
+    KOT_CUDA(cudaStreamCreateWithFlags(&a.st, cudaStreamNonBlocking));
+    a.init_scratch();
+  }
+  return *aux_;
+}
+
 Bufs& Problem::bufs() {
   if (!bufs_) {
     bufs_.reset(new Bufs());
     Bufs& b = *bufs_;
     const long nn = (long)n * n;
     for (double** m : {&b.Xw, &b.Xv, &b.Xt, &b.r2w, &b.r2v, &b.r2t, &b.Pw, &b.Pv, &b.Pt, &b.Pe, &b.Xh, &b.dX,
-                       &b.filt, &b.a2t})
+                       &b.filt, &b.a2t, &b.Bm, &b.Ct})
       *m = alloc(nn);
     for (double** v : {&b.gw, &b.gv, &b.gt, &b.r1w, &b.r1v, &b.r1t, &b.valw, &b.valv, &b.valt, &b.vale, &b.dg,
                        &b.a1, &b.rhs, &b.sol, &b.corr, &b.cx, &b.cr, &b.cp, &b.cap, &b.e1, &b.e2, &b.e3})

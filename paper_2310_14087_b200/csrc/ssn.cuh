@@ -38,6 +38,7 @@ struct Bufs {
   double *Xw, *Xv, *Xt, *r2w, *r2v, *r2t, *Pw, *Pv, *Pt, *Pe, *Xh, *dX, *filt, *a2t;  // n×n
   double *gw, *gv, *gt, *r1w, *r1v, *r1t, *valw, *valv, *valt, *vale, *dg, *a1, *rhs, *sol, *corr;  // n
   double *cx, *cr, *cp, *cap, *e1, *e2, *e3;  // n
+  double *Bm, *Ct;  // n×n: B = R·P, T̃ (structure-reduced matvec)
 };
 
 struct Problem {
@@ -48,12 +49,15 @@ struct Problem {
   cudaStream_t st = nullptr;
   // instance data (device)
   double *Q = nullptr, *z = nullptr, *R = nullptr, *embed = nullptr, *Kmat = nullptr;
+  double* G2 = nullptr;  // (RRᵀ)∘(RRᵀ), lazily
   // scratch
   std::unique_ptr<EigWork> eig;
   std::vector<double*> owned;
   double* partial = nullptr;  // rowdot partials [tiles][n]
   double *M1 = nullptr, *M2 = nullptr, *M3 = nullptr, *M4 = nullptr, *M5 = nullptr;  // n×n temps
   double* red = nullptr;   // reduction partials
+  double* splitws = nullptr;  // split-K partials
+  long splitws_cap = 0;
   double* dsc = nullptr;   // device scalars
   double* hsc = nullptr;   // pinned host scalars
   int* dk = nullptr;
@@ -62,6 +66,10 @@ struct Problem {
 
   std::unique_ptr<Bufs> bufs_;
   Bufs& bufs();
+  // second execution context (own stream + scratch, shared instance data) on
+  // which the EG safeguard chain runs concurrently with the Newton chain
+  std::unique_ptr<Problem> aux_;
+  Problem& aux();
   double* alloc(long count);
   void init_scratch();
   ~Problem();
@@ -84,6 +92,16 @@ double residual_parts(Problem& p, const double* g, const double* X, double* r1, 
 void middle_operator(Problem& p, const Decomp& dc, double mu, const double* v, double* out);
 void eg_step(Problem& p, const double* g, const double* X, double s, double* g_out, double* X_out);
 
+// structure-reduced middle operator (the CG matvec of the solver)
+struct MvCtx {
+  Decomp dc;
+  double mu = 0.0;
+  bool pos = true;
+  double* B = nullptr;
+};
+void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m);
+void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* out);
+
 struct NewtonOut {
   int cg_iters, met, attempts;
   double lhs, rhs, cg_ms;
@@ -92,7 +110,8 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
                            double mu, const SolverCfg& cfg, double* dg, double* dX);
 
 // internal helpers shared with solver.cu
-enum FinMode { FIN_RES = 0, FIN_MATVEC = 1, FIN_A1 = 2, FIN_JTOP = 3, FIN_PHI = 4, FIN_GRAD = 5, FIN_QV = 6 };
+enum FinMode { FIN_RES = 0, FIN_MATVEC = 1, FIN_A1 = 2, FIN_JTOP = 3, FIN_PHI = 4, FIN_GRAD = 5, FIN_QV = 6,
+               FIN_MATVEC_B = 7 };
 void dev_reduce(Problem& p, const double* a, const double* b, long count, int slot, bool sq);
 void fetch(Problem& p, int count);
 void axpby(Problem& p, long count, double a, const double* x, double b, const double* y, double* out);

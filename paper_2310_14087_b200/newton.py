@@ -72,13 +72,18 @@ def cfg_struct(newton: NewtonConfig, eg_stepsize: float = 0.01, residual_tol: fl
     return c
 
 
-def middle_operator_at(pd: ProblemData, w: IteratePair, theta: float, v) -> tuple[np.ndarray, float]:
-    """Q v/(2λ₂) + μv + Φ(𝒯[Φ*(v)]) at the context of w (μ = θ‖R(w)‖) (newton.py:95-128)."""
+def middle_operator_at(pd: ProblemData, w: IteratePair, theta: float, v, form: str = "reduced"
+                       ) -> tuple[np.ndarray, float]:
+    """Q v/(2λ₂) + μv + Φ(𝒯[Φ*(v)]) at the context of w (μ = θ‖R(w)‖) (newton.py:95-128).
+
+    ``form="reduced"``: the solver's structure-reduced B = R·P evaluation;
+    ``form="direct"``: the reference's Φ* → 𝒯 → Φ chain."""
     g, x = _lib.f64(w.gamma, (pd.n,)), _lib.f64(w.x_mat, (pd.n, pd.n))
     vv = _lib.f64(v, (pd.n,))
     out, mu = np.empty(pd.n), C.c_double()
     _lib.check(_lib.lib().kot_middle_operator(pd.device_problem().handle, _lib.ptr(g), _lib.ptr(x), float(theta),
-                                              _lib.ptr(vv), _lib.ptr(out), C.byref(mu)))
+                                              _lib.ptr(vv), 0 if form == "reduced" else 1, _lib.ptr(out),
+                                              C.byref(mu)))
     return out, float(mu.value)
 
 

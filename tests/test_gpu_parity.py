@@ -200,12 +200,31 @@ def test_eliminator_and_jacobian_cfg1(cfg1):
     assert rel(mz, cfg1["op_mz"]) <= 1e-11
 
 
-def test_middle_operator(cfg1):
+@pytest.mark.parametrize("form", ["reduced", "direct"])
+def test_middle_operator(cfg1, form):
     pd = gpu_pd(cfg1)
     out, mu = GN.middle_operator_at(pd, GP.IteratePair(cfg1["op_g"], cfg1["op_x"]), float(cfg1["op_theta"]),
-                                    cfg1["op_v"])
+                                    cfg1["op_v"], form=form)
     assert mu == pytest.approx(float(cfg1["op_mu"]), rel=1e-12)
     assert rel(out, cfg1["op_middle"]) <= 1e-11
+
+
+@pytest.mark.parametrize("shift", [-5.0, 0.0, 5.0])
+def test_middle_operator_both_paths(cfg1, shift):
+    """Reduced (B = R·P) vs oracle at states whose spectrum is mostly negative, mixed, mostly
+    positive: exercises the POS and NONPOS (G2 = (RRᵀ)∘(RRᵀ)) branches."""
+    pd = gpu_pd(cfg1)
+    po = oracle_pd(cfg1)
+    rng = np.random.default_rng(5)
+    x = cfg1["op_x"] + shift * np.eye(pd.n) * np.abs(np.diag(cfg1["op_x"])).mean()
+    g = cfg1["op_g"]
+    v = rng.standard_normal(pd.n)
+    out, mu = GN.middle_operator_at(pd, GP.IteratePair(g, x), 0.7, v)
+    r, dc = O.residual_parts(po, O.Pair(g, x))
+    ctx = O.newton_context(dc, r.norm(), 0.7)
+    ref = O.middle_operator(po, ctx.op, ctx.mu)(v)
+    assert mu == pytest.approx(ctx.mu, rel=1e-12)
+    assert rel(out, ref) <= 1e-11, (dc.k, rel(out, ref))
 
 
 def _perturbed_oracle_pd(d, seed, p=""):
@@ -218,7 +237,10 @@ def _perturbed_oracle_pd(d, seed, p=""):
 
 def test_newton_direction(cfg1):
     """Default profile: CG stops at the 20×(1+2) cap, so the direction is only determined up to the
-    oracle's own ulp sensitivity (measured: ≈2.3e-5 relative); the tolerance is 10× that spread."""
+    oracle's own sensitivity (measured ≈2.3e-5 relative under a 1-ulp perturbation of R; the
+    solver's structure-reduced matvec differs from the reference form by ~1e-13, i.e. a larger
+    perturbation than 1 ulp): tolerance 100× the ulp spread.  The converged-CG test below is the
+    accuracy check (≤1e-8)."""
     pd = gpu_pd(cfg1)
     w = GP.IteratePair(cfg1["op_g"], cfg1["op_x"])
     st = GN.newton_direction_at(pd, w, float(cfg1["op_theta"]), GN.NewtonConfig())
@@ -230,8 +252,8 @@ def test_newton_direction(cfg1):
         spread = max(spread, rel(so.dw.g, cfg1["op_dir_dg"]))
     assert st.cg_iters == int(cfg1["op_dir_cg"])
     assert st.criterion_met == bool(cfg1["op_dir_met"])
-    assert rel(st.dw.gamma, cfg1["op_dir_dg"]) <= max(1e-9, 10 * spread)
-    assert rel(st.dw.x_mat, cfg1["op_dir_dx"]) <= max(1e-9, 10 * spread)
+    assert rel(st.dw.gamma, cfg1["op_dir_dg"]) <= max(1e-9, 100 * spread)
+    assert rel(st.dw.x_mat, cfg1["op_dir_dx"]) <= max(1e-9, 100 * spread)
     assert np.array_equal(st.dw.x_mat, st.dw.x_mat.T)
 
 
