@@ -98,15 +98,37 @@ struct TrdArgs {
   double* yv;
   double* part;   // [G][TRD_PSTRIDE]: t1[NB], t2[NB], yvv
   double* partn;  // [G]: Σ x_r², r >= c+2
+  unsigned long long* dbg;  // nullable: per-segment ns accumulated by CTA 0 thread 0
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// One cooperative launch per NB=32 panel.  Each warp owns up to TRD_RPW rows
+// (r ≡ global-warp-id mod #warps, r ≥ p0); their V/W panel rows and the panel
+// columns of A live in shared memory for the whole panel, the symv results in
+// registers, so a column costs ~4 dependent global round trips + 2 grid
+// barriers.  V/W are also written to global (X = [V | W | V]) for the trailing
+// rank-2NB update and for the other CTAs (row c of V/W).
+constexpr int TRD_RPW = 4;  // rows per warp: n ≤ TRD_RPW · 16 · 148 = 9472
 
 __global__ void __launch_bounds__(TRD_THREADS) sytrd_panel_kernel(TrdArgs a) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ double vsh[];  // Householder vector staged per CTA (length n)
+  extern __shared__ double dsm[];
+  // dynamic smem: [Vs | Ws | Ac] (TRD_WARPS × TRD_RPW × NB each) then the Householder vector (n)
+  typedef double RowBlk[TRD_RPW][TRD_NB];
+  RowBlk* Vs = reinterpret_cast<RowBlk*>(dsm);
+  RowBlk* Ws = Vs + TRD_WARPS;
+  RowBlk* Ac = Ws + TRD_WARPS;
+  double* vsh = reinterpret_cast<double*>(Ac + TRD_WARPS);
   __shared__ double sred[TRD_WARPS][TRD_PSTRIDE];
   __shared__ double tred[TRD_PSTRIDE];
   __shared__ double wrow[TRD_NB], vrow[TRD_NB];
   __shared__ double nrm_sh[TRD_WARPS];
+  __shared__ double scal_sh[2];
 
   const int n = a.n, p0 = a.p0, nb = a.nb;
   const int G = gridDim.x;
@@ -117,56 +139,103 @@ __global__ void __launch_bounds__(TRD_THREADS) sytrd_panel_kernel(TrdArgs a) {
   double* V = a.X;
   double* Wm = a.X + TRD_NB;
   double* V2 = a.X + 2 * TRD_NB;
-
+  // own rows: rbase + q·NW, q < TRD_RPW
+  const int rbase = p0 + ((gw - p0) % NW + NW) % NW;
+  double yreg[TRD_RPW];
+#pragma unroll
+  for (int q = 0; q < TRD_RPW; ++q) {
+    const int r = rbase + q * NW;
+    Vs[wid][q][lane] = 0.0;
+    Ws[wid][q][lane] = 0.0;
+    Ac[wid][q][lane] = (r < n && lane < nb) ? a.A[(long)r * n + p0 + lane] : 0.0;
+    yreg[q] = 0.0;
+  }
+  __syncwarp();
   double tau_prev = 0.0;
+  const bool timing = (a.dbg != nullptr) && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long tseg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long tl = timing ? gtimer() : 0;
+#define TRD_MARK(i)                   \
+  if (timing) {                       \
+    const unsigned long long t_ = gtimer(); \
+    tseg[i] += t_ - tl;               \
+    tl = t_;                          \
+  }
 
   for (int jj = 0; jj <= nb; ++jj) {
     const int c = p0 + jj;
     // ------------------------------------------------------------ phase Q
     if (jj > 0) {
       const int m = jj - 1;  // t-range of the previous column's corrections
-      // warp-parallel, fixed-order reduction of the per-CTA partials (t1, t2, yᵀv)
-      for (int q = wid; q <= 2 * TRD_NB; q += TRD_WARPS) {
-        double s = 0.0;
-        if (q < m || (q >= TRD_NB && q < TRD_NB + m) || q == 2 * TRD_NB)
-          for (int g = lane; g < G; g += 32) s += a.part[(long)g * TRD_PSTRIDE + q];
-        s = warp_sum(s);
-        if (lane == 0) tred[q] = s;
+      // prefetch row c of V/W (owned elsewhere) while the partials are reduced
+      double pv = 0.0, pw = 0.0, pyc = 0.0;
+      if (wid == TRD_WARPS - 1 && jj < nb) {
+        if (lane < jj) pv = V[(long)c * LDX + lane];
+        if (lane < m) pw = Wm[(long)c * LDX + lane];
+        pyc = a.yv[c];
+      }
+      if (wid < TRD_WARPS - 1) {  // 15 warps × ≤5 partial columns: issue every load before reducing
+        constexpr int QPW = (2 * TRD_NB + 1 + TRD_WARPS - 2) / (TRD_WARPS - 1);
+        double sq[QPW];
+#pragma unroll
+        for (int i = 0; i < QPW; ++i) {
+          const int q = wid + i * (TRD_WARPS - 1);
+          sq[i] = 0.0;
+          if (q <= 2 * TRD_NB && (q < m || (q >= TRD_NB && q < TRD_NB + m) || q == 2 * TRD_NB))
+            for (int g = lane; g < G; g += 32) sq[i] += a.part[(long)g * TRD_PSTRIDE + q];
+        }
+#pragma unroll
+        for (int i = 0; i < QPW; ++i) {
+          const int q = wid + i * (TRD_WARPS - 1);
+          const double s = warp_sum(sq[i]);
+          if (lane == 0 && q <= 2 * TRD_NB) tred[q] = s;
+        }
+      }
+      if (wid == TRD_WARPS - 1 && jj < nb) {
+        vrow[lane] = pv;
+        if (lane < m) wrow[lane] = pw;
       }
       __syncthreads();
+      TRD_MARK(0)
+      const double t1l = (lane < m) ? tred[lane] : 0.0, t2l = (lane < m) ? tred[TRD_NB + lane] : 0.0;
+      const double t12 = warp_sum(t1l * t2l);
       // α = −½ τ (wᵀv),  wᵀv = τ (yᵀv − 2 t1·t2)
-      double t12 = 0.0;
-      for (int t = 0; t < m; ++t) t12 += tred[t] * tred[TRD_NB + t];
       const double alpha_prev = -0.5 * tau_prev * (tau_prev * (tred[2 * TRD_NB] - 2.0 * t12));
-      // finish W[:, jj-1] for rows r >= c: w_r = τ (y_r − V_r·t1 − W_r·t2) + α v_r
-      auto finish_row = [&](int r) -> double {
-        double s = 0.0;
-        if (lane < m) s = V[(long)r * LDX + lane] * tred[lane] + Wm[(long)r * LDX + lane] * tred[TRD_NB + lane];
+      // finish W[:, jj-1] for own rows r >= c: w_r = τ (y_r − V_r·t1 − W_r·t2) + α v_r
+#pragma unroll
+      for (int q = 0; q < TRD_RPW; ++q) {
+        const int r = rbase + q * NW;
+        if (r < c || r >= n) continue;
+        double s = Vs[wid][q][lane] * t1l + Ws[wid][q][lane] * t2l;
         s = warp_sum(s);
-        return tau_prev * (a.yv[r] - s) + alpha_prev * V[(long)r * LDX + jj - 1];
-      };
-      for (int r = c + ((gw - c) % NW + NW) % NW; r < n; r += NW) {
-        const double w = finish_row(r);
-        if (lane == 0) Wm[(long)r * LDX + jj - 1] = w;
+        const double w = tau_prev * (yreg[q] - s) + alpha_prev * Vs[wid][q][jj - 1];
+        if (lane == 0) {
+          Ws[wid][q][jj - 1] = w;
+          Wm[(long)r * LDX + jj - 1] = w;
+        }
       }
-      if (jj < nb && wid == 0) {
-        const double wc = finish_row(c);  // identical arithmetic to the owner's
-        if (lane == 0) wrow[jj - 1] = wc;
+      if (wid == TRD_WARPS - 1 && jj < nb) {  // row c, redundantly (identical arithmetic to its owner)
+        double s = ((lane < m) ? vrow[lane] : 0.0) * t1l + ((lane < m) ? wrow[lane] : 0.0) * t2l;
+        s = warp_sum(s);
+        if (lane == 0) wrow[m] = tau_prev * (pyc - s) + alpha_prev * vrow[m];
       }
+    } else if (wid == TRD_WARPS - 1) {
+      vrow[lane] = 0.0;
+      wrow[lane] = 0.0;
     }
     if (jj == nb) break;
-    // rows c of V and W (t < jj) for the column update
-    if (threadIdx.x < jj) {
-      if (threadIdx.x < jj - 1 || jj == 0) wrow[threadIdx.x] = Wm[(long)c * LDX + threadIdx.x];
-      vrow[threadIdx.x] = V[(long)c * LDX + threadIdx.x];
-    }
     __syncthreads();
+    TRD_MARK(1)
+    // update column c for own rows r >= c; Σ x_r² over r >= c+2
     double nrm = 0.0;
-    for (int r = c + ((gw - c) % NW + NW) % NW; r < n; r += NW) {
-      double s = 0.0;
-      if (lane < jj) s = V[(long)r * LDX + lane] * wrow[lane] + Wm[(long)r * LDX + lane] * vrow[lane];
+    const double wl = (lane < jj) ? wrow[lane] : 0.0, vl = (lane < jj) ? vrow[lane] : 0.0;
+#pragma unroll
+    for (int q = 0; q < TRD_RPW; ++q) {
+      const int r = rbase + q * NW;
+      if (r < c || r >= n) continue;
+      double s = Vs[wid][q][lane] * wl + Ws[wid][q][lane] * vl;
       s = warp_sum(s);
-      const double x = a.A[(long)r * n + c] - s;
+      const double x = Ac[wid][q][jj] - s;
       if (lane == 0) {
         a.xv[r] = x;
         if (r == c) a.d[c] = x;
@@ -180,75 +249,122 @@ __global__ void __launch_bounds__(TRD_THREADS) sytrd_panel_kernel(TrdArgs a) {
       for (int w = 0; w < TRD_WARPS; ++w) s += nrm_sh[w];
       a.partn[blockIdx.x] = s;
     }
+    TRD_MARK(2)
     grid.sync();
+    TRD_MARK(3)
     // ------------------------------------------------------------ phase S
+    const int m = n - c - 1;
+    // stage x (unscaled) while warp 0 reduces the norm partials
+    for (int s = threadIdx.x; s < m; s += blockDim.x) vsh[s] = a.xv[c + 1 + s];
     if (wid == 0) {
       double s = 0.0;
+      const double alpha = a.xv[c + 1];  // issued together with the partial loads
       for (int g = lane; g < G; g += 32) s += a.partn[g];
       s = warp_sum(s);
-      if (lane == 0) nrm_sh[0] = s;
+      if (lane == 0) {
+        const double xn2 = s;
+        double beta, tau, scale;
+        if (xn2 == 0.0) {  // dlarfg: H = I
+          tau = 0.0;
+          beta = alpha;
+          scale = 1.0;
+        } else {
+          beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+          tau = (beta - alpha) / beta;
+          scale = 1.0 / (alpha - beta);
+        }
+        scal_sh[0] = tau;
+        scal_sh[1] = scale;
+        if (blockIdx.x == 0) {
+          a.e[c] = beta;
+          a.tau[c] = tau;
+        }
+      }
     }
     __syncthreads();
-    const double xn2 = nrm_sh[0];
-    const double alpha = a.xv[c + 1];
-    double beta, tau, scale;
-    if (xn2 == 0.0) {  // dlarfg: H = I
-      tau = 0.0;
-      beta = alpha;
-      scale = 1.0;
-    } else {
-      beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
-      tau = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
-    }
+    const double tau = scal_sh[0], scale = scal_sh[1];
     tau_prev = tau;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      a.e[c] = beta;
-      a.tau[c] = tau;
-    }
-    const int m = n - c - 1;
-    for (int s = threadIdx.x; s < m; s += blockDim.x) vsh[s] = (s == 0) ? 1.0 : a.xv[c + 1 + s] * scale;
+    TRD_MARK(4)
+    for (int s = threadIdx.x; s < m; s += blockDim.x) vsh[s] = (s == 0) ? 1.0 : vsh[s] * scale;
     __syncthreads();
     double pt1 = 0.0, pt2 = 0.0, pyv = 0.0;  // lane t accumulates t1_t, t2_t
-    for (int r = (c + 1) + ((gw - c - 1) % NW + NW) % NW; r < n; r += NW) {
+#pragma unroll
+    for (int q = 0; q < TRD_RPW; ++q) {
+      const int r = rbase + q * NW;
+      if (r <= c || r >= n) continue;
       const double vr = vsh[r - c - 1];
       const double* Ar = a.A + (long)r * n + c + 1;
-      // 8 independent loads in flight per lane (the symv is L2-latency bound)
+      // L2-latency bound: 16-byte loads, 8 in flight per lane (16 doubles)
       double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      int s = lane;
-      for (; s + 7 * 32 < m; s += 8 * 32) {
+      const int s0 = (int)((reinterpret_cast<uintptr_t>(Ar) >> 3) & 1);  // peel to 16 B alignment
+      if (s0 && lane == 0 && m > 0) acc[0] = Ar[0] * vsh[0];
+      const int m2 = (m - s0) >> 1;
+      const double2* A2 = reinterpret_cast<const double2*>(Ar + s0);
+      const double* vb = vsh + s0;
+      int qq = lane;
+      for (; qq + 15 * 32 < m2; qq += 16 * 32) {  // 16 × 16 B in flight per lane
+        double2 av[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc[u] += Ar[s + u * 32] * vsh[s + u * 32];
+        for (int u = 0; u < 16; ++u) av[u] = __ldcg(A2 + qq + u * 32);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int s = 2 * (qq + u * 32);
+          acc[u & 7] += av[u].x * vb[s] + av[u].y * vb[s + 1];
+        }
       }
-      for (; s < m; s += 32) acc[0] += Ar[s] * vsh[s];
+      for (; qq + 7 * 32 < m2; qq += 8 * 32) {
+        double2 av[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) av[u] = __ldcg(A2 + qq + u * 32);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int s = 2 * (qq + u * 32);
+          acc[u] += av[u].x * vb[s] + av[u].y * vb[s + 1];
+        }
+      }
+      for (; qq < m2; qq += 32) {
+        const double2 av = A2[qq];
+        acc[0] += av.x * vb[2 * qq] + av.y * vb[2 * qq + 1];
+      }
+      if (((m - s0) & 1) && lane == 0) acc[1] += Ar[m - 1] * vsh[m - 1];
       double y = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
       y = warp_sum(y);
+      yreg[q] = y;
+      if (lane == jj) Vs[wid][q][jj] = vr;
       if (lane == 0) {
-        a.yv[r] = y;
+        if (r == c + 1) a.yv[r] = y;
         V[(long)r * LDX + jj] = vr;
         V2[(long)r * LDX + jj] = vr;
         a.Vall[(long)r * n + c] = vr;
         pyv += y * vr;
       }
       if (lane < jj) {
-        pt1 += Wm[(long)r * LDX + lane] * vr;
-        pt2 += V[(long)r * LDX + lane] * vr;
+        pt1 += Ws[wid][q][lane] * vr;
+        pt2 += Vs[wid][q][lane] * vr;
       }
     }
     sred[wid][lane] = pt1;
     sred[wid][TRD_NB + lane] = pt2;
     if (lane == 0) sred[wid][2 * TRD_NB] = pyv;
     __syncthreads();
+    TRD_MARK(5)
     for (int q = threadIdx.x; q <= 2 * TRD_NB; q += blockDim.x) {
       double s = 0.0;
       for (int w = 0; w < TRD_WARPS; ++w) s += sred[w][q];
       a.part[(long)blockIdx.x * TRD_PSTRIDE + q] = s;
     }
+    TRD_MARK(6)
     grid.sync();
+    TRD_MARK(7)
   }
+  if (timing)
+    for (int i = 0; i < 8; ++i) a.dbg[i] += tseg[i];
+#undef TRD_MARK
 }
 
 __global__ void set_last_diag_kernel(const double* A, int n, double* d) { d[n - 1] = A[(long)(n - 1) * n + n - 1]; }
+
+unsigned long long* g_trd_dbg = nullptr;  // set by kot_debug_sytrd_timing
 
 static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st) {
   KOT_CUDA(cudaMemcpyAsync(w.A, Z, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
@@ -258,13 +374,14 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st) {
     const int nb = std::min(TRD_NB, n - 1 - p0);
     KOT_CUDA(cudaMemsetAsync(w.X, 0, sizeof(double) * n * 3 * TRD_NB, st));
     const int rows = n - p0;
-    const int G = std::max(1, std::min(kNumSMs, ceil_div(rows, 16)));
-    TrdArgs args{w.A, n, p0, nb, w.X, w.Vall, w.d, w.e, w.tau, w.xv, w.yv, w.part, w.partn};
+    const int G = std::max(1, std::min(kNumSMs, ceil_div(rows, TRD_WARPS)));
+    kot_require((long)G * TRD_WARPS * TRD_RPW >= rows, KOT_EINVAL, "matrix order too large for sytrd");
+    TrdArgs args{w.A, n, p0, nb, w.X, w.Vall, w.d, w.e, w.tau, w.xv, w.yv, w.part, w.partn, g_trd_dbg};
     void* kargs[] = {&args};
     // algorithmic bytes: one read of the lower triangle of every trailing matrix this panel reflects
     double bytes = 0.0;
     for (int c = p0; c < p0 + nb; ++c) bytes += 8.0 * 0.5 * (double)(n - c - 1) * (n - c);
-    const size_t smem = sizeof(double) * std::max(rows, 1);
+    const size_t smem = sizeof(double) * (std::max(rows, 1) + 3L * TRD_WARPS * TRD_RPW * TRD_NB);
     if (smem > 48 * 1024 && smem_set_for < (int)smem) {
       KOT_CUDA(cudaFuncSetAttribute(sytrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       smem_set_for = (int)smem;
@@ -387,47 +504,84 @@ struct MergeDesc {
   long off;  // offset of this merge's K×K / n×K scratch (prefix of n_m²)
 };
 
-// Per-merge bookkeeping (one CTA per merge; sequential parts on thread 0):
-// z extraction, sort, dlaed2 deflation.  Integer outputs in ibuf regions:
+// Per-merge bookkeeping (one CTA per merge, arrays staged in shared memory):
+// z extraction, stable merge of the two ascending halves (parallel ranks by
+// binary search), dlaed2 deflation (sequential scan on thread 0 over smem).
+// Integer outputs (global, at the merge's offset o):
 //   perm[o..o+n)   : sorted position → local column of the block
 //   ndcol[o..)     : sorted positions of the K non-deflated columns
 //   dcol[o..)      : sorted positions of the deflated columns (sorted by value)
 //   rot[o..)       : (pj, nj) index pairs of the deflation rotations
 //   meta[4*mi..]   : K, ndefl, nrot
-__global__ void dc_merge_prep_kernel(const MergeDesc* md, const double* Q, int ldq, const double* d, const double* e,
-                                     double* zs, double* ds, double* dlam, double* wv, double* dfv, double* rotcs,
-                                     double* rho_out, int* perm, int* ndcol, int* dcol, int* rot, int* meta) {
+constexpr int DC_PREP_THREADS = 256;
+
+__device__ __forceinline__ int rank_lt(const double* a, int n, double v) {  // #{a_i < v}
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < v)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ int rank_le(const double* a, int n, double v) {  // #{a_i <= v}
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] <= v)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
+    const MergeDesc* md, const double* Q, int ldq, const double* d, const double* e, double* zs, double* ds,
+    double* dlam, double* wv, double* dfv, double* rotcs, double* rho_out, int* perm, int* ndcol, int* dcol,
+    int* rot, int* meta) {
+  extern __shared__ double psm[];
+  __shared__ double red[32];
   const MergeDesc m = md[blockIdx.x];
   const int o = m.o, n1 = m.n1, n = m.n1 + m.n2;
-  const int sidx = o + n1 - 1;
-  const double esplit = e[sidx];
+  double* Du = psm;         // unsorted d (n)
+  double* D = psm + n;      // sorted d (n)
+  double* Z = psm + 2 * n;  // sorted z (n)
+  int* P = reinterpret_cast<int*>(psm + 3 * n);  // n ints
+  const double esplit = e[o + n1 - 1];
   const double sgn = (esplit < 0.0) ? -1.0 : 1.0;
   const double rs2 = 1.0 / sqrt(2.0);  // dlaed2: z ← z/√2, ρ ← |2ρ|
+  for (int i = threadIdx.x; i < n; i += blockDim.x) Du[i] = d[o + i];
+  __syncthreads();
+  double zmax = 0.0, dmax = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    // stable merge rank: left-half elements go first on ties
+    const int pos = (i < n1) ? i + rank_lt(Du + n1, n - n1, Du[i]) : (i - n1) + rank_le(Du, n1, Du[i]);
+    P[pos] = i;
     const double zz = (i < n1) ? Q[(long)(o + n1 - 1) * ldq + o + i] : sgn * Q[(long)(o + n1) * ldq + o + i];
-    zs[o + i] = zz * rs2;  // unsorted for now
+    const double zv = zz * rs2;
+    D[pos] = Du[i];
+    Z[pos] = zv;
+    zmax = fmax(zmax, fabs(zv));
+    dmax = fmax(dmax, fabs(Du[i]));
+  }
+  zmax = warp_max(zmax);
+  dmax = warp_max(dmax);
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = zmax;
+    red[16 + (threadIdx.x >> 5)] = dmax;
   }
   __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) perm[o + i] = P[i];
   if (threadIdx.x != 0) return;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    zmax = fmax(zmax, red[w]);
+    dmax = fmax(dmax, red[16 + w]);
+  }
   const double rho = fabs(2.0 * esplit);
   rho_out[blockIdx.x] = rho;
-  // merge the two ascending halves
-  int* P = perm + o;
-  {
-    int i = 0, j = n1, k = 0;
-    while (i < n1 && j < n) P[k++] = (d[o + j] < d[o + i]) ? j++ : i++;
-    while (i < n1) P[k++] = i++;
-    while (j < n) P[k++] = j++;
-  }
-  double* D = ds + o;
-  double* Z = dlam + o;  // temp: sorted z (dlam reused after)
-  double zmax = 0.0, dmax = 0.0;
-  for (int k = 0; k < n; ++k) {
-    D[k] = d[o + P[k]];
-    Z[k] = zs[o + P[k]];
-    zmax = fmax(zmax, fabs(Z[k]));
-    dmax = fmax(dmax, fabs(D[k]));
-  }
   const double tol = 8.0 * DEPS * fmax(dmax, zmax);
   int K = 0, nd = 0, nr = 0;
   int* NDC = ndcol + o;
@@ -436,8 +590,7 @@ __global__ void dc_merge_prep_kernel(const MergeDesc* md, const double* Q, int l
   double* DFV = dfv + o;
   double* RCS = rotcs + 2 * o;
   double* WV = wv + o;
-  // dlamda written after the scan (Z aliases dlam)
-  double* tmpd = zs + o;  // reuse zs for nondeflated d values
+  double* DL = dlam + o;
   if (rho * zmax <= tol) {
     for (int k = 0; k < n; ++k) {
       DC[nd] = k;
@@ -479,7 +632,7 @@ __global__ void dc_merge_prep_kernel(const MergeDesc* md, const double* Q, int l
         pj = j;
       } else {
         NDC[K] = pj;
-        tmpd[K] = D[pj];
+        DL[K] = D[pj];
         WV[K] = Z[pj];
         ++K;
         pj = j;
@@ -487,12 +640,11 @@ __global__ void dc_merge_prep_kernel(const MergeDesc* md, const double* Q, int l
     }
     if (pj >= 0) {
       NDC[K] = pj;
-      tmpd[K] = D[pj];
+      DL[K] = D[pj];
       WV[K] = Z[pj];
       ++K;
     }
   }
-  for (int k = 0; k < K; ++k) dlam[o + k] = tmpd[k];
   // insertion-sort the deflated list by value (nearly sorted already)
   for (int i = 1; i < nd; ++i) {
     const double v = DFV[i];
@@ -509,34 +661,43 @@ __global__ void dc_merge_prep_kernel(const MergeDesc* md, const double* Q, int l
   meta[4 * blockIdx.x + 0] = K;
   meta[4 * blockIdx.x + 1] = nd;
   meta[4 * blockIdx.x + 2] = nr;
+  (void)zs;
+  (void)ds;
 }
 
-// Gather the block columns into sorted order, apply the deflation rotations
-// (thread per row, rotations in order), then split into the contiguous
-// non-deflated matrix Qnd (n × K) and the deflated columns (kept in Qw).
-__global__ void dc_merge_vec_kernel(const MergeDesc* md, const double* Q, double* Qw, double* Qnd, int ldq,
-                                    const int* perm, const int* ndcol, const int* rot, const double* rotcs,
-                                    const int* meta) {
+// One CTA per row of a merge block: gather the row into sorted column order in
+// shared memory, apply the deflation rotations in order, then write the
+// non-deflated part (Qnd, n × K) and the deflated part (Qdf, n × nd) with
+// coalesced stores.
+__global__ void dc_merge_vec_kernel(const MergeDesc* md, const double* Q, double* Qdf, double* Qnd, int ldq,
+                                    const int* perm, const int* ndcol, const int* dcol, const int* rot,
+                                    const double* rotcs, const int* meta) {
+  extern __shared__ double rowsm[];
   const MergeDesc m = md[blockIdx.y];
   const int o = m.o, n = m.n1 + m.n2;
-  const int K = meta[4 * blockIdx.y], nr = meta[4 * blockIdx.y + 2];
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.x;
   if (r >= n) return;
+  const int K = meta[4 * blockIdx.y], nd = meta[4 * blockIdx.y + 1], nr = meta[4 * blockIdx.y + 2];
   const double* qrow = Q + (long)(o + r) * ldq + o;
-  double* wrow = Qw + (long)(o + r) * ldq + o;
   const int* P = perm + o;
-  for (int j = 0; j < n; ++j) wrow[j] = qrow[P[j]];
-  const int* RT = rot + 2 * o;
-  const double* RCS = rotcs + 2 * o;
-  for (int q = 0; q < nr; ++q) {
-    const int pj = RT[2 * q], nj = RT[2 * q + 1];
-    const double c = RCS[2 * q], s = RCS[2 * q + 1];
-    const double x = wrow[pj], y = wrow[nj];
-    wrow[pj] = c * x + s * y;
-    wrow[nj] = c * y - s * x;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) rowsm[j] = qrow[P[j]];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int* RT = rot + 2 * o;
+    const double* RCS = rotcs + 2 * o;
+    for (int q = 0; q < nr; ++q) {
+      const int pj = RT[2 * q], nj = RT[2 * q + 1];
+      const double c = RCS[2 * q], s = RCS[2 * q + 1];
+      const double x = rowsm[pj], y = rowsm[nj];
+      rowsm[pj] = c * x + s * y;
+      rowsm[nj] = c * y - s * x;
+    }
   }
-  double* nd = Qnd + m.off + (long)r * K;
-  for (int k = 0; k < K; ++k) nd[k] = wrow[ndcol[o + k]];
+  __syncthreads();
+  double* ndrow = Qnd + m.off + (long)r * K;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) ndrow[k] = rowsm[ndcol[o + k]];
+  double* dfrow = Qdf + m.off + (long)r * nd;
+  for (int t = threadIdx.x; t < nd; t += blockDim.x) dfrow[t] = rowsm[dcol[o + t]];
 }
 
 struct RootRef {
@@ -706,40 +867,38 @@ __global__ void dc_vec_kernel(const MergeDesc* md, const RootRef* roots, int nro
   for (int i = lane; i < K; i += 32) col[i] *= inv;
 }
 
-// Merge the ascending roots with the ascending deflated values: write the
-// merged eigenvalues into d[o..o+n) and the destination column of every
-// eigenvector (non-deflated: colmap[o+k]; deflated: colmap[o+K+t]).
+// Merge the ascending roots with the ascending deflated values (parallel
+// ranks; roots go first on ties): eigenvalues into d[o..o+n) and the
+// destination column of every eigenvector (non-deflated: colmap[o+k];
+// deflated: colmap[o+K+t]).
 __global__ void dc_order_kernel(const MergeDesc* md, const int* meta, const double* lam, const double* dfv, double* d,
                                 int* colmap) {
-  if (threadIdx.x != 0) return;
   const MergeDesc m = md[blockIdx.x];
   const int o = m.o;
   const int K = meta[4 * blockIdx.x], nd = meta[4 * blockIdx.x + 1];
-  int a = 0, b = 0, pos = 0;
-  while (a < K || b < nd) {
-    const bool take_root = (b >= nd) || (a < K && lam[o + a] <= dfv[o + b]);
-    if (take_root) {
-      d[o + pos] = lam[o + a];
-      colmap[o + a] = pos;
-      ++a;
-    } else {
-      d[o + pos] = dfv[o + b];
-      colmap[o + K + b] = pos;
-      ++b;
-    }
-    ++pos;
+  const double* L = lam + o;
+  const double* F = dfv + o;
+  for (int a = threadIdx.x; a < K; a += blockDim.x) {
+    const int pos = a + rank_lt(F, nd, L[a]);
+    d[o + pos] = L[a];
+    colmap[o + a] = pos;
+  }
+  for (int b = threadIdx.x; b < nd; b += blockDim.x) {
+    const int pos = b + rank_le(L, K, F[b]);
+    d[o + pos] = F[b];
+    colmap[o + K + b] = pos;
   }
 }
 
-__global__ void dc_copy_deflated_kernel(const MergeDesc* md, const int* meta, const double* Qw, double* Q, int ldq,
-                                        const int* dcol, const int* colmap) {
+__global__ void dc_copy_deflated_kernel(const MergeDesc* md, const int* meta, const double* Qdf, double* Q, int ldq,
+                                        const int* colmap) {
   const MergeDesc m = md[blockIdx.y];
   const int o = m.o, n = m.n1 + m.n2;
   const int K = meta[4 * blockIdx.y], nd = meta[4 * blockIdx.y + 1];
   const long total = (long)n * nd;
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
     const int r = (int)(e / nd), t = (int)(e % nd);
-    Q[(long)(o + r) * ldq + o + colmap[o + K + t]] = Qw[(long)(o + r) * ldq + o + dcol[o + t]];
+    Q[(long)(o + r) * ldq + o + colmap[o + K + t]] = Qdf[m.off + e];
   }
 }
 
@@ -815,6 +974,7 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
     KOT_LAUNCH_CHECK();
   }
   const int nleaves = (int)loff.size();
+  ProfScope ps_leaf("dc.leaf", st);
   dc_leaf_kernel<<<ceil_div(nleaves, 4), 128, 0, st>>>(w.d, w.e, dloff, dllen, nleaves, w.Q, n, err);
   KOT_LAUNCH_CHECK();
   // per-level device descriptors after the packed ints (8-byte aligned)
@@ -831,12 +991,23 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
       }
     if (ms.empty()) continue;
     const int nm = (int)ms.size();
+    int maxm = 0;
+    for (auto& mm : ms) maxm = std::max(maxm, mm.n1 + mm.n2);
     int* dmeta = reinterpret_cast<int*>(dms + nm);
     RootRef* droots = reinterpret_cast<RootRef*>(dmeta + 4 * nm);
     memcpy(h_desc, ms.data(), sizeof(MergeDesc) * nm);
     KOT_CUDA(cudaMemcpyAsync(dms, h_desc, sizeof(MergeDesc) * nm, cudaMemcpyHostToDevice, st));
-    dc_merge_prep_kernel<<<nm, 128, 0, st>>>(dms, w.Q, n, w.d, w.e, w.zs, w.ds, w.dlam, w.wv, w.dfv, w.rotcs,
-                                             w.rho, perm, ndcol, dcol, rot, dmeta);
+    ProfScope ps_prep("dc.prep", st);
+    {
+      const size_t smem = (size_t)maxm * (3 * sizeof(double) + sizeof(int));
+      static size_t prep_attr = 0;
+      if (smem > 48 * 1024 && smem > prep_attr) {
+        KOT_CUDA(cudaFuncSetAttribute(dc_merge_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        prep_attr = smem;
+      }
+      dc_merge_prep_kernel<<<nm, DC_PREP_THREADS, smem, st>>>(dms, w.Q, n, w.d, w.e, w.zs, w.ds, w.dlam, w.wv,
+                                                              w.dfv, w.rotcs, w.rho, perm, ndcol, dcol, rot, dmeta);
+    }
     KOT_LAUNCH_CHECK();
     std::vector<int> meta(4 * nm);
     KOT_CUDA(cudaMemcpyAsync(meta.data(), dmeta, sizeof(int) * 4 * nm, cudaMemcpyDeviceToHost, st));
@@ -847,13 +1018,23 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
       maxn = std::max(maxn, ms[i].n1 + ms[i].n2);
       for (int j = 0; j < meta[4 * i]; ++j) roots.push_back({i, j});
     }
-    dc_merge_vec_kernel<<<dim3(ceil_div(maxn, 128), nm), 128, 0, st>>>(dms, w.Q, w.Qw, w.Qnd, n, perm, ndcol, rot,
-                                                                       w.rotcs, dmeta);
+    ProfScope ps_vec("dc.gather_rot", st);
+    {
+      const size_t smem = (size_t)maxn * sizeof(double);
+      static size_t vec_attr = 0;
+      if (smem > 48 * 1024 && smem > vec_attr) {
+        KOT_CUDA(cudaFuncSetAttribute(dc_merge_vec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        vec_attr = smem;
+      }
+      dc_merge_vec_kernel<<<dim3(maxn, nm), 256, smem, st>>>(dms, w.Q, w.Qw, w.Qnd, n, perm, ndcol, dcol, rot,
+                                                             w.rotcs, dmeta);
+    }
     KOT_LAUNCH_CHECK();
     const int nr = (int)roots.size();
     if (nr > 0) {
       memcpy(h_roots, roots.data(), sizeof(RootRef) * nr);
       KOT_CUDA(cudaMemcpyAsync(droots, h_roots, sizeof(RootRef) * nr, cudaMemcpyHostToDevice, st));
+      ProfScope ps_sec("dc.secular", st);
       dc_secular_kernel<<<ceil_div(nr, 8), 256, 0, st>>>(dms, droots, nr, dmeta, w.dlam, w.wv, w.rho, w.lam, w.Dl,
                                                           err);
       KOT_LAUNCH_CHECK();
@@ -862,9 +1043,10 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
       dc_vec_kernel<<<ceil_div(nr, 8), 256, 0, st>>>(dms, droots, nr, dmeta, w.what, w.Dl);
       KOT_LAUNCH_CHECK();
     }
-    dc_order_kernel<<<nm, 32, 0, st>>>(dms, dmeta, w.lam, w.dfv, w.d, colmap);
+    ProfScope ps_ord("dc.order_gemm", st);
+    dc_order_kernel<<<nm, 256, 0, st>>>(dms, dmeta, w.lam, w.dfv, w.d, colmap);
     KOT_LAUNCH_CHECK();
-    dc_copy_deflated_kernel<<<dim3(64, nm), 256, 0, st>>>(dms, dmeta, w.Qw, w.Q, n, dcol, colmap);
+    dc_copy_deflated_kernel<<<dim3(64, nm), 256, 0, st>>>(dms, dmeta, w.Qw, w.Q, n, colmap);
     KOT_LAUNCH_CHECK();
     for (int i = 0; i < nm; ++i) {
       const int K = meta[4 * i];
@@ -886,27 +1068,45 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
 // ====================================================== back-transform
 
 // T factor of the forward block reflector (dlarft 'F','C') from S = VᵀV:
-// T[i][i] = τ_i, T[0:i, i] = −τ_i T[0:i,0:i] S[0:i, i].  One thread per row,
-// sequential over the nb ≤ 128 columns; T and S staged in shared memory.
+// T[i][i] = τ_i, T[0:i, i] = −τ_i T[0:i,0:i] S[0:i, i].  The upper triangles of
+// T and S are packed in shared memory; each row's dot product is split over a
+// quad of threads (512 threads for nb ≤ 128), sequential over the columns.
 constexpr int ORM_NB = 128;
-constexpr int LARFT_SMEM = ORM_NB * (ORM_NB + 1) * 8;
+constexpr int LARFT_THREADS = 512;
+constexpr int LARFT_SMEM = 2 * (ORM_NB * (ORM_NB + 1) / 2) * 8;
 
-// S is symmetric, so column i is read as row i (coalesced across threads).
-__global__ void larft_kernel(const double* __restrict__ S, const double* tau, int nb, double* T) {
+__device__ __forceinline__ int upk(int j, int k, int nb) {  // packed upper index, j <= k
+  return j * nb - (j * (j - 1)) / 2 + (k - j);
+}
+
+__global__ void __launch_bounds__(LARFT_THREADS) larft_kernel(const double* __restrict__ S, const double* tau,
+                                                              int nb, double* T) {
   extern __shared__ double lsm[];
-  double* Ts = lsm;  // [nb][nb+1]
-  const int ld = ORM_NB + 1;
-  const int j = threadIdx.x;  // row of T
+  const int np = nb * (nb + 1) / 2;
+  double* Tp = lsm;
+  double* Sp = lsm + np;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int r = e / nb, c = e % nb;
+    if (r <= c) Sp[upk(r, c, nb)] = S[e];
+  }
+  __syncthreads();
+  const int j = threadIdx.x >> 2, q = threadIdx.x & 3;  // row j, quad lane q
   for (int i = 0; i < nb; ++i) {
     double tmp = 0.0;
     if (j < i)
-      for (int k = j; k < i; ++k) tmp += Ts[j * ld + k] * __ldg(S + (long)i * nb + k);
-    if (j < i) Ts[j * ld + i] = -tau[i] * tmp;
-    if (j == i) Ts[i * ld + i] = tau[i];
-    if (j > i && j < nb) Ts[j * ld + i] = 0.0;
+      for (int k = j + q; k < i; k += 4) tmp += Tp[upk(j, k, nb)] * Sp[upk(k, i, nb)];
+    tmp += __shfl_xor_sync(0xffffffffu, tmp, 1);
+    tmp += __shfl_xor_sync(0xffffffffu, tmp, 2);
+    if (q == 0) {
+      if (j < i) Tp[upk(j, i, nb)] = -tau[i] * tmp;
+      if (j == i) Tp[upk(i, i, nb)] = tau[i];
+    }
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) T[e] = Ts[(e / nb) * ld + e % nb];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int r = e / nb, c = e % nb;
+    T[e] = (r <= c) ? Tp[upk(r, c, nb)] : 0.0;
+  }
 }
 
 __global__ void reverse_cols_kernel(const double* Q, const double* dasc, double* P, double* vals, int n) {
@@ -961,7 +1161,7 @@ static void ormtr(int n, EigWork& w, double* P, cudaStream_t st) {
       s.ksplit = choose_ksplit(s, w.splitws_cap);
       gemm_launch<true, false>(s, EpiSymMirror{S, nb, 1.0, nullptr, 0.0, 0.0}, st);
     }
-    larft_kernel<<<1, ((nb + 31) / 32) * 32, LARFT_SMEM, st>>>(S, w.tau + p0, nb, T);
+    larft_kernel<<<1, LARFT_THREADS, LARFT_SMEM, st>>>(S, w.tau + p0, nb, T);
     KOT_LAUNCH_CHECK();
     {  // W1 = Vᵀ P[r0:, :]
       GemmShape s = make_shape(nb, n, mrows, Vp, n, P + (long)r0 * n, n);
@@ -1009,3 +1209,22 @@ void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigW
 }
 
 }  // namespace kot
+
+extern "C" int kot_debug_sytrd_timing(int on, unsigned long long* out8) {
+  // on=1: allocate + zero the segment accumulators; on=0: copy them out and disable
+  using namespace kot;
+  try {
+    if (on) {
+      if (!g_trd_dbg) KOT_CUDA(cudaMalloc(&g_trd_dbg, 8 * sizeof(unsigned long long)));
+      KOT_CUDA(cudaMemset(g_trd_dbg, 0, 8 * sizeof(unsigned long long)));
+    } else if (g_trd_dbg) {
+      KOT_CUDA(cudaDeviceSynchronize());
+      KOT_CUDA(cudaMemcpy(out8, g_trd_dbg, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      cudaFree(g_trd_dbg);
+      g_trd_dbg = nullptr;
+    }
+    return 0;
+  } catch (const KotError& e) {
+    return e.code;
+  }
+}

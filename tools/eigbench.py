@@ -1,0 +1,36 @@
+"""Isolated eigensolver timing (library phase profiler), n from argv."""
+import sys
+
+import numpy as np
+
+from paper_2310_14087_b200 import _lib, linalg
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
+rng = np.random.default_rng(0)
+q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+vals = np.concatenate([np.linspace(1, 100, n // 2), -np.linspace(1e-4, 1, n - n // 2)])
+z = (q * vals) @ q.T
+z = 0.5 * (z + z.T)
+linalg.sym_eig(z)
+_lib.profile_enable(True)
+reps = 3
+for _ in range(reps):
+    dc = linalg.sym_eig(z)
+prof = _lib.profile_read()
+print(f"n={n}  max|eig err| = {np.max(np.abs(dc.eigvals - np.sort(vals)[::-1])):.2e}")
+for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"]):
+    tf = v["flops"] / (v["ms"] * 1e-3) / 1e12 if v["ms"] > 0 and v["flops"] > 0 else 0
+    print(f"  {k:16s} calls/eig {v['calls']/reps:7.1f}  ms/eig {v['ms']/reps:9.3f}  {tf:6.2f} TF/s")
+
+# per-segment timing of the sytrd panel kernel (CTA 0, thread 0)
+import ctypes as C
+L = _lib.lib()
+buf = (C.c_ulonglong * 8)()
+L.kot_debug_sytrd_timing(1, buf)
+linalg.sym_eig(z)
+L.kot_debug_sytrd_timing(0, buf)
+names = ["Q:partials+prefetch", "Q:finish W", "Q:col update+partn", "grid.sync#1", "S:norm+householder",
+         "S:scale+symv+partials", "S:part write", "grid.sync#2"]
+tot = sum(buf)
+for nm, v in zip(names, buf):
+    print(f"  {nm:24s} {v/1e6:8.3f} ms  {v/tot*100:5.1f}%  ({v/1e3/(n-1):.2f} us/col)")
