@@ -22,6 +22,8 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <condition_variable>
+#include <mutex>
 #include <vector>
 
 #include "gemm.cuh"
@@ -1186,6 +1188,39 @@ __global__ void eig1_kernel(const double* Z, double* P, double* vals) {
   P[0] = 1.0;
 }
 
+// Cooperative sytrd grids from different streams/host threads must never need
+// more co-resident CTAs than the SMs can hold at once (their blocks spin on a
+// grid barrier).  This process-wide gate admits at most `cap` concurrent
+// sytrd calls, cap = co-resident panel CTAs per SM for this n.
+namespace {
+std::mutex g_coop_mu;
+std::condition_variable g_coop_cv;
+int g_coop_active = 0;
+struct CoopGate {
+  explicit CoopGate(int cap) {
+    std::unique_lock<std::mutex> lk(g_coop_mu);
+    g_coop_cv.wait(lk, [&] { return g_coop_active < cap; });
+    ++g_coop_active;
+  }
+  ~CoopGate() {
+    {
+      std::lock_guard<std::mutex> lk(g_coop_mu);
+      --g_coop_active;
+    }
+    g_coop_cv.notify_all();
+  }
+};
+}  // namespace
+
+static int sytrd_coresident_cap(int n) {
+  const size_t smem = sizeof(double) * (std::max(n, 1) + 3L * TRD_WARPS * TRD_RPW * TRD_NB);
+  if (smem > 48 * 1024)
+    KOT_CUDA(cudaFuncSetAttribute(sytrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  KOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sytrd_panel_kernel, TRD_THREADS, smem));
+  return std::max(1, per_sm);
+}
+
 void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigWork& w, cudaStream_t st) {
   if (n == 1) {
     eig1_kernel<<<1, 1, 0, st>>>(Z, P, vals);
@@ -1193,7 +1228,9 @@ void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigW
   } else {
     {
       ProfScope ps("eig.sytrd", st, 4.0 / 3.0 * n * (double)n * n);
+      CoopGate gate(sytrd_coresident_cap(n));
       sytrd(Z, n, w, st);
+      KOT_CUDA(cudaStreamSynchronize(st));  // the gate is held until the grids have retired
     }
     {
       ProfScope ps("eig.stedc", st);

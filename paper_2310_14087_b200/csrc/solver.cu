@@ -103,7 +103,10 @@ static CgOut cg_solve(Problem& p, const MvCtx& mv, const double* rhs, double tol
   if (res <= target) return {0, res};
   int it = 0;
   for (it = 1; it <= max_iter; ++it) {
-    middle_operator_fast(p, mv, b.cp, b.cap);
+    if (mv.direct)
+      middle_operator(p, mv.dc, mv.mu, b.cp, b.cap);
+    else
+      middle_operator_fast(p, mv, b.cp, b.cap);
     cg_step_kernel<<<1, CG_THREADS, 0, p.st>>>(n, b.cx, b.cr, b.cp, b.cap, p.dsc);
     KOT_LAUNCH_CHECK();
     fetch(p, 16);
@@ -147,7 +150,10 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
     out.attempts = att + 1;
     const double* rhs = b.a1;
     if (att) {
-      middle_operator_fast(p, mv, b.sol, b.e3);
+      if (mv.direct)
+        middle_operator(p, dc, mu, b.sol, b.e3);
+      else
+        middle_operator_fast(p, mv, b.sol, b.e3);
       axpby(p, n, 1.0, b.a1, -1.0, b.e3, b.rhs);
       rhs = b.rhs;
     }

@@ -13,6 +13,8 @@
 //   newton       newton.py:116-195
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "gemm.cuh"
 #include "ssn.cuh"
@@ -388,6 +390,12 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m) {
   Bufs& b = p.bufs();
   m.dc = dc;
   m.mu = mu;
+  static const bool direct = [] {
+    const char* e = std::getenv("KOT_MATVEC");
+    return e != nullptr && std::string(e) == "direct";
+  }();
+  m.direct = direct;
+  if (direct) return;
   m.pos = dc.k <= n - dc.k;
   m.B = b.Bm;
   {  // B = R P   (R upper triangular: K range starts at the row tile)

@@ -97,6 +97,7 @@ struct MvCtx {
   Decomp dc;
   double mu = 0.0;
   bool pos = true;
+  bool direct = false;  // diagnostic: KOT_MATVEC=direct uses the reference Φ*→𝒯→Φ chain
   double* B = nullptr;
 };
 void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m);

@@ -1,0 +1,243 @@
+"""CPU-only tests: the C-ABI library loads and exports the header's symbols, host-side logic
+(configs, validation, damping rule, batch sharding/packing) and the multi-process gather
+path (gloo, world_size 2).  No CUDA compute runs here."""
+
+import os
+import re
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import kot_port as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+# ---------------------------------------------------------------- ABI
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "kotgpu.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = set(re.findall(r"\b(kot_[a-z0-9_]+)\s*\(", src))
+    names -= {"kot_iter_cb"}
+    return sorted(names)
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2310_14087_b200 import _lib
+    lib = _lib.lib()
+    declared = header_functions()
+    assert len(declared) >= 25
+    for name in declared:
+        assert hasattr(lib, name), name
+    # every declared entry point is bound with a signature by the Python layer (debug hooks excepted)
+    bound = set(_lib.exported_symbols())
+    missing = [n for n in declared if n not in bound]
+    assert not missing, missing
+
+
+def test_debug_hook_exported():
+    from paper_2310_14087_b200 import _lib
+    assert hasattr(_lib.lib(), "kot_debug_sytrd_timing")
+
+
+def test_ctypes_struct_layouts_match_c(tmp_path):
+    """Compile a probe against include/kotgpu.h with gcc and compare sizes/offsets with ctypes."""
+    import ctypes as C
+    import shutil
+    import subprocess
+    from paper_2310_14087_b200 import _lib
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "probe.c"
+    src.write_text(
+        f'#include "{ROOT}/include/kotgpu.h"\n#include <stdio.h>\n#include <stddef.h>\n'
+        'int main(){printf("%zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(kot_solver_cfg),'
+        ' offsetof(kot_solver_cfg, cg_tol), offsetof(kot_solver_cfg, eg_stepsize),'
+        ' offsetof(kot_solver_cfg, safeguard_every), sizeof(kot_iter_record),'
+        ' offsetof(kot_iter_record, step_ms), sizeof(kot_report), sizeof(kot_prof_entry));return 0;}\n')
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    want = [C.sizeof(_lib.SolverCfgC), _lib.SolverCfgC.cg_tol.offset, _lib.SolverCfgC.eg_stepsize.offset,
+            _lib.SolverCfgC.safeguard_every.offset, C.sizeof(_lib.IterRecordC), _lib.IterRecordC.step_ms.offset,
+            C.sizeof(_lib.ReportC), C.sizeof(_lib.ProfEntryC)]
+    assert got == want
+
+
+def test_no_cpu_fallback_without_gpu():
+    """The product path fails loudly when no GPU is present (no silent NumPy fallback)."""
+    import paper_2310_14087_b200 as K
+    from paper_2310_14087_b200 import _lib
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present")
+    except ImportError:
+        pass
+    with pytest.raises(_lib.CudaError):
+        K.linalg.sym_eig(np.eye(3))
+    pd = K.ProblemData(q_mat=[[2.0]], z=[1.0], q_sq=0.0, chol_upper=[[1.0]], lambda1=1.0, lambda2=0.5)
+    with pytest.raises(_lib.CudaError):
+        K.solve(pd)
+
+
+# ------------------------------------------------------- host-side API
+
+def test_dataclass_validation_mirrors_reference():
+    import paper_2310_14087_b200 as K
+    with pytest.raises(ValueError):
+        K.KernelSpec(0.0, 2)
+    with pytest.raises(ValueError):
+        K.KernelSpec(1.0, 2, family="laplace")
+    with pytest.raises(ValueError):
+        K.SampleSet(np.ones(3))
+    with pytest.raises(ValueError):
+        K.SampleSet(np.array([[np.nan, 1.0]]))
+    with pytest.raises(ValueError):
+        K.FillingPoints(np.ones((3, 2)), np.ones((2, 2)))
+    with pytest.raises(ValueError):
+        K.ProblemData(q_mat=np.eye(2), z=np.zeros(3), q_sq=0.0, chol_upper=np.eye(2), lambda1=1.0, lambda2=1.0)
+    with pytest.raises(ValueError):
+        K.ProblemData(q_mat=np.eye(2), z=np.zeros(2), q_sq=0.0, chol_upper=np.eye(2), lambda1=0.0, lambda2=1.0)
+    for bad in (dict(tau=1.0), dict(alpha1=2.0, alpha2=1.0), dict(beta0=1.5), dict(theta_min=0.0), dict(cg_max=0)):
+        with pytest.raises(ValueError):
+            K.NewtonConfig(**bad)
+    with pytest.raises(ValueError):
+        K.EgConfig(stepsize=0.0)
+    for bad in (dict(residual_tol=0.0), dict(max_iter=0), dict(safeguard_every=0)):
+        with pytest.raises(ValueError):
+            K.SolverConfig(**bad)
+    # q_mat is symmetrised on construction (problem.py:112)
+    pd = K.ProblemData(q_mat=[[1.0, 2.0], [0.0, 1.0]], z=[0.0, 0.0], q_sq=0.0, chol_upper=np.eye(2),
+                       lambda1=1.0, lambda2=1.0)
+    assert np.array_equal(pd.q_mat, [[1.0, 1.0], [1.0, 1.0]])
+
+
+def test_iterate_pair_algebra():
+    from paper_2310_14087_b200.problem import IteratePair, zero_pair
+    a = IteratePair(np.array([3.0, 4.0]), np.array([[0.0, 0.0], [0.0, 12.0]]))
+    assert a.norm() == pytest.approx(5.0 + 12.0)  # problem.py:56-57: a sum of norms
+    assert a.dot(a) == pytest.approx(25.0 + 144.0)
+    b = zero_pair(2)
+    assert (a + b).norm() == a.norm() and (2 * a).norm() == 2 * a.norm()
+    assert a.is_finite() and not IteratePair(np.array([np.inf]), np.zeros((1, 1))).is_finite()
+
+
+def test_theta_update_matches_oracle():
+    from paper_2310_14087_b200 import newton
+    rng = np.random.default_rng(0)
+    cfg_g = newton.NewtonConfig()
+    cfg_o = O.NewtonCfg()
+    for _ in range(500):
+        theta = float(np.exp(rng.uniform(-12, 12)))
+        rho = float(rng.normal() * 10 ** rng.uniform(-8, 2))
+        dw2 = float(10 ** rng.uniform(-6, 4))
+        assert newton.theta_update(theta, rho, dw2, cfg_g) == O.theta_update(theta, rho, dw2, cfg_o)
+
+
+def test_solver_cfg_struct_roundtrip():
+    import paper_2310_14087_b200 as K
+    c = K.SolverConfig(newton=K.NewtonConfig(alpha1=1e-8, cg_tol=1e-9), eg=K.EgConfig(0.25), residual_tol=1e-7,
+                       max_iter=77, safeguard_every=3).to_c()
+    assert (c.alpha1, c.cg_tol, c.has_cg_tol, c.eg_stepsize, c.residual_tol, c.max_iter, c.safeguard_every) == (
+        1e-8, 1e-9, 1, 0.25, 1e-7, 77, 3)
+    assert K.SolverConfig().to_c().has_cg_tol == 0
+
+
+def test_configs_are_seeded_and_shaped():
+    from paper_2310_14087_b200 import configs
+    a, b = configs.config2(), configs.config2()
+    assert np.array_equal(a.xs, b.xs) and a.xs.shape == (500, 5) and a.xt.shape == (500, 5)
+    assert np.all(np.abs(a.xs) <= 1.0) and np.all(np.abs(a.ys) <= 1.0)
+    c3 = configs.config3(n=300)
+    assert c3.xs.shape == (300, 10) and np.all(np.linalg.norm(c3.xs, axis=1) <= 1.0 + 1e-15)
+    assert c3.bandwidth_sq == 2.25 and c3.lambda2 == 1.0 / 300
+    m = configs.config5_member(6)
+    assert m.bandwidth_sq == pytest.approx(1.5 ** 2) and m.xs.shape == (1000, 10)
+    c4 = configs.config4(n=64)
+    assert c4.xs.shape == (64, 64) and np.allclose(np.linalg.norm(c4.xs, axis=1), 1.0)
+
+
+def test_eg_stepsize_rule():
+    from paper_2310_14087_b200 import configs
+    q = np.array([[2.0, 0.0], [0.0, 2.0]])
+    k = np.eye(2)
+    s = configs.eg_stepsize(q, k, 0.5)
+    assert s == pytest.approx(0.5 / (np.sqrt(8.0) / 1.0 + np.sqrt(2.0)))
+
+
+# ------------------------------------------------------------- batches
+
+def fake_result(seed, l=6):  # noqa: E741
+    from paper_2310_14087_b200.batch import BatchResult
+    return BatchResult(seed, seed % 7 + 1, seed % 2 == 0, 1e-7 * (seed + 1), float(seed), -float(seed), 1.0,
+                       np.arange(l, dtype=float) + seed)
+
+
+def test_shard_spreads_sigma_groups():
+    from paper_2310_14087_b200.batch import shard
+    seeds = list(range(512))
+    for world in (1, 2, 4, 8):
+        parts = [shard(seeds, world, r) for r in range(world)]
+        assert sorted(sum(parts, [])) == seeds
+        for p in parts:
+            counts = np.bincount(np.array(p) % 4, minlength=4)
+            assert counts.max() - counts.min() <= 1
+
+
+def test_pack_unpack_and_local_runner():
+    from paper_2310_14087_b200.batch import pack, run_local, unpack
+    r = fake_result(5)
+    u = unpack(pack(r, 6))
+    assert u.seed == 5 and u.iterations == r.iterations and np.array_equal(u.gamma_hat, r.gamma_hat)
+    out = run_local(list(range(10)), fake_result, concurrency=3)
+    assert [o.seed for o in out] == list(range(10))
+
+    def boom(s):
+        raise RuntimeError("x")
+    with pytest.raises(RuntimeError):
+        run_local([1, 2], boom, concurrency=2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _gather_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2310_14087_b200.batch import gather_to_root, run_local, shard
+    seeds = list(range(11))
+    mine = shard(seeds, world, rank)
+    res = run_local(mine, fake_result, concurrency=2)
+    allr = gather_to_root(res, 6, world, rank)
+    if rank == 0:
+        q.put([(r.seed, r.iterations, r.gamma_hat.tolist()) for r in allr])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_multiprocess_gather_gloo():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [g[0] for g in got] == list(range(11))
+    for seed, it, gam in got:
+        ref = fake_result(seed)
+        assert it == ref.iterations and np.array_equal(gam, ref.gamma_hat)
