@@ -34,7 +34,7 @@ namespace cg = cooperative_groups;
 namespace kot {
 
 constexpr int TRD_NB = 32;
-constexpr int TRD_THREADS = 512;
+constexpr int TRD_THREADS = 256;
 constexpr int TRD_WARPS = TRD_THREADS / 32;
 constexpr int TRD_PSTRIDE = 2 * TRD_NB + 2;
 constexpr int DC_LEAF = 32;
@@ -98,7 +98,7 @@ struct TrdArgs {
   double* tau;
   double* xv;
   double* yv;
-  double* part;   // [G][TRD_PSTRIDE]: t1[NB], t2[NB], yvv
+  double* part;   // [TRD_PSTRIDE][kNumSMs]: t1[NB], t2[NB], yvv per CTA (transposed: coalesced reduction)
   double* partn;  // [G]: Σ x_r², r >= c+2
   unsigned long long* dbg;  // nullable: per-segment ns accumulated by CTA 0 thread 0
 };
@@ -115,9 +115,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // registers, so a column costs ~4 dependent global round trips + 2 grid
 // barriers.  V/W are also written to global (X = [V | W | V]) for the trailing
 // rank-2NB update and for the other CTAs (row c of V/W).
-constexpr int TRD_RPW = 4;  // rows per warp: n ≤ TRD_RPW · 16 · 148 = 9472
+constexpr int TRD_RPW = 8;  // rows per warp: n ≤ TRD_RPW · 8 · 148 = 9472
 
-__global__ void __launch_bounds__(TRD_THREADS) sytrd_panel_kernel(TrdArgs a) {
+__global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double dsm[];
   // dynamic smem: [Vs | Ws | Ac] (TRD_WARPS × TRD_RPW × NB each) then the Householder vector (n)
@@ -176,15 +176,24 @@ __global__ void __launch_bounds__(TRD_THREADS) sytrd_panel_kernel(TrdArgs a) {
         if (lane < m) pw = Wm[(long)c * LDX + lane];
         pyc = a.yv[c];
       }
-      if (wid < TRD_WARPS - 1) {  // 15 warps × ≤5 partial columns: issue every load before reducing
+      if (wid < TRD_WARPS - 1) {  // TRD_WARPS−1 warps share the partial columns; every load issued up front
         constexpr int QPW = (2 * TRD_NB + 1 + TRD_WARPS - 2) / (TRD_WARPS - 1);
+        constexpr int GPL = (kNumSMs + 31) / 32;  // partials per lane (G ≤ 148)
         double sq[QPW];
 #pragma unroll
         for (int i = 0; i < QPW; ++i) {
           const int q = wid + i * (TRD_WARPS - 1);
-          sq[i] = 0.0;
-          if (q <= 2 * TRD_NB && (q < m || (q >= TRD_NB && q < TRD_NB + m) || q == 2 * TRD_NB))
-            for (int g = lane; g < G; g += 32) sq[i] += a.part[(long)g * TRD_PSTRIDE + q];
+          const bool need = q <= 2 * TRD_NB && (q < m || (q >= TRD_NB && q < TRD_NB + m) || q == 2 * TRD_NB);
+          double v[GPL];
+#pragma unroll
+          for (int u = 0; u < GPL; ++u) {
+            const int g = lane + 32 * u;
+            v[u] = (need && g < G) ? __ldcg(a.part + (long)q * kNumSMs + g) : 0.0;
+          }
+          double s = 0.0;
+#pragma unroll
+          for (int u = 0; u < GPL; ++u) s += v[u];
+          sq[i] = s;
         }
 #pragma unroll
         for (int i = 0; i < QPW; ++i) {
@@ -259,9 +268,14 @@ __global__ void __launch_bounds__(TRD_THREADS) sytrd_panel_kernel(TrdArgs a) {
     // stage x (unscaled) while warp 0 reduces the norm partials
     for (int s = threadIdx.x; s < m; s += blockDim.x) vsh[s] = a.xv[c + 1 + s];
     if (wid == 0) {
-      double s = 0.0;
       const double alpha = a.xv[c + 1];  // issued together with the partial loads
-      for (int g = lane; g < G; g += 32) s += a.partn[g];
+      constexpr int GPL = (kNumSMs + 31) / 32;
+      double v[GPL];
+#pragma unroll
+      for (int u = 0; u < GPL; ++u) v[u] = (lane + 32 * u < G) ? __ldcg(a.partn + lane + 32 * u) : 0.0;
+      double s = 0.0;
+#pragma unroll
+      for (int u = 0; u < GPL; ++u) s += v[u];
       s = warp_sum(s);
       if (lane == 0) {
         const double xn2 = s;
@@ -353,7 +367,7 @@ __global__ void __launch_bounds__(TRD_THREADS) sytrd_panel_kernel(TrdArgs a) {
     for (int q = threadIdx.x; q <= 2 * TRD_NB; q += blockDim.x) {
       double s = 0.0;
       for (int w = 0; w < TRD_WARPS; ++w) s += sred[w][q];
-      a.part[(long)blockIdx.x * TRD_PSTRIDE + q] = s;
+      a.part[(long)q * kNumSMs + blockIdx.x] = s;
     }
     TRD_MARK(6)
     grid.sync();
