@@ -162,6 +162,10 @@ int kot_newton_direction(kot_problem* p, const kot_solver_cfg* cfg, const double
 /* eg_step (eg.py:34-41). */
 int kot_eg_step(kot_problem* p, const double* gamma, const double* x, double stepsize,
                 double* gamma_out, double* x_out);
+/* evaluate_map (problem.py:254-284): potential u(q_j) and Monge map T(q_j) = q_j − ∇u(q_j). */
+int kot_evaluate_map(const double* xs, int n, const double* x_tilde, const double* gamma_hat, int l,
+                     const double* queries, int m, int d, double bandwidth_sq, double lambda2, int device,
+                     double* u_out, double* t_out);
 /* objective (problem.py:192-196) and ot_estimate (problem.py:244-251). */
 int kot_objective(kot_problem* p, const double* gamma, double* out);
 int kot_ot_estimate(kot_problem* p, const double* gamma, double* out);

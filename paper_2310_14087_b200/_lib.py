@@ -87,6 +87,8 @@ _SIGS = {
                                        iptr, iptr, dptr, dptr]),
     "kot_eg_step": (C.c_int, [C.c_void_p, dptr, dptr, C.c_double, dptr, dptr]),
     "kot_objective": (C.c_int, [C.c_void_p, dptr, dptr]),
+    "kot_evaluate_map": (C.c_int, [dptr, C.c_int, dptr, dptr, C.c_int, dptr, C.c_int, C.c_int, C.c_double,
+                                   C.c_double, C.c_int, dptr, dptr]),
     "kot_ot_estimate": (C.c_int, [C.c_void_p, dptr, dptr]),
 }
 

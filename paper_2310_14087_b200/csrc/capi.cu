@@ -255,6 +255,28 @@ int kot_gram(const double* pts, int n, int d, double bandwidth_sq, int device, d
   });
 }
 
+int kot_evaluate_map(const double* xs, int n, const double* xt, const double* gamma, int l, const double* queries,
+                     int m, int d, double bandwidth_sq, double lambda2, int device, double* u_out, double* t_out) {
+  return guarded([&] {
+    kot::kot_require(bandwidth_sq > 0.0 && lambda2 > 0.0, kot::KOT_EINVAL, "bandwidth_sq and lambda2 must be positive");
+    kot::kot_require(n >= 1 && l >= 1 && m >= 0, kot::KOT_EINVAL, "empty sample or filling set");
+    KOT_CUDA(cudaSetDevice(device));
+    if (m == 0) return;
+    cudaStream_t st;
+    KOT_CUDA(cudaStreamCreate(&st));
+    DevBuf dxs((long)n * d), dxt((long)l * d), dg(l), dq((long)m * d), du(m), dt((long)m * d);
+    KOT_CUDA(cudaMemcpyAsync(dxs.p, xs, (long)n * d * 8, cudaMemcpyHostToDevice, st));
+    KOT_CUDA(cudaMemcpyAsync(dxt.p, xt, (long)l * d * 8, cudaMemcpyHostToDevice, st));
+    KOT_CUDA(cudaMemcpyAsync(dg.p, gamma, (long)l * 8, cudaMemcpyHostToDevice, st));
+    KOT_CUDA(cudaMemcpyAsync(dq.p, queries, (long)m * d * 8, cudaMemcpyHostToDevice, st));
+    kot::evaluate_map_device(dxs.p, n, dxt.p, dg.p, l, dq.p, m, d, bandwidth_sq, lambda2, du.p, dt.p, st);
+    KOT_CUDA(cudaMemcpyAsync(u_out, du.p, (long)m * 8, cudaMemcpyDeviceToHost, st));
+    KOT_CUDA(cudaMemcpyAsync(t_out, dt.p, (long)m * d * 8, cudaMemcpyDeviceToHost, st));
+    KOT_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+  });
+}
+
 int kot_cholesky_psd(const double* k, int n, int device, double* r_upper, double* jitter) {
   return guarded([&] {
     kot::kot_require(n >= 1, kot::KOT_EINVAL, "order must be >= 1");

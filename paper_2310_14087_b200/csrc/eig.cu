@@ -1209,17 +1209,25 @@ __global__ void eig1_kernel(const double* Z, double* P, double* vals) {
 namespace {
 std::mutex g_coop_mu;
 std::condition_variable g_coop_cv;
-int g_coop_active = 0;
+int g_coop_active = 0, g_coop_bg = 0;
+// Background (lane 1) callers may hold at most cap−1 slots, so a lane-0
+// (Newton-chain) eigensolve never queues behind the EG pipeline.
 struct CoopGate {
-  explicit CoopGate(int cap) {
+  int lane;
+  CoopGate(int cap, int lane_) : lane(lane_) {
     std::unique_lock<std::mutex> lk(g_coop_mu);
-    g_coop_cv.wait(lk, [&] { return g_coop_active < cap; });
+    if (lane == 0 || cap < 2)
+      g_coop_cv.wait(lk, [&] { return g_coop_active < cap; });
+    else
+      g_coop_cv.wait(lk, [&] { return g_coop_active < cap && g_coop_bg < cap - 1; });
     ++g_coop_active;
+    if (lane != 0) ++g_coop_bg;
   }
   ~CoopGate() {
     {
       std::lock_guard<std::mutex> lk(g_coop_mu);
       --g_coop_active;
+      if (lane != 0) --g_coop_bg;
     }
     g_coop_cv.notify_all();
   }
@@ -1235,14 +1243,15 @@ static int sytrd_coresident_cap(int n) {
   return std::max(1, per_sm);
 }
 
-void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigWork& w, cudaStream_t st) {
+void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigWork& w, cudaStream_t st,
+                  int lane) {
   if (n == 1) {
     eig1_kernel<<<1, 1, 0, st>>>(Z, P, vals);
     KOT_LAUNCH_CHECK();
   } else {
     {
       ProfScope ps("eig.sytrd", st, 4.0 / 3.0 * n * (double)n * n);
-      CoopGate gate(sytrd_coresident_cap(n));
+      CoopGate gate(sytrd_coresident_cap(n), lane);
       sytrd(Z, n, w, st);
       KOT_CUDA(cudaStreamSynchronize(st));  // the gate is held until the grids have retired
     }

@@ -207,3 +207,68 @@ void assemble_device(const double* xs, int nx, const double* ys, int ny, const d
 }
 
 }  // namespace kot
+
+namespace kot {
+
+// evaluate_map (reference problem.py:254-284): for each query q_j, fused over
+// the samples and the filling points (no n×m Gram in HBM):
+//   emb_j = mean_i k(x_i, q_j),            S_j = mean_i k(x_i, q_j) x_i
+//   wgt_j = Σ_i γ_i k(x̃_i, q_j),           F_j = Σ_i γ_i k(x̃_i, q_j) x̃_i
+//   u_j = (emb_j − wgt_j)/(2λ₂),  ∇u_j = ((S_j − emb_j q_j) − (F_j − wgt_j q_j)) / (2λ₂σ²),  T_j = q_j − ∇u_j
+// One warp per query; lanes stride the points; fixed-order warp reductions.
+constexpr int MAP_MAXD = 64;
+
+__global__ void evaluate_map_kernel(const double* __restrict__ xs, int n, const double* __restrict__ xt,
+                                    const double* __restrict__ gamma, int l, const double* __restrict__ qs, int m,
+                                    int d, double twobw, double bw, double lambda2, double* __restrict__ u,
+                                    double* __restrict__ tmap) {
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (j >= m) return;
+  double q[MAP_MAXD], S[MAP_MAXD], F[MAP_MAXD];
+  for (int k = 0; k < d; ++k) {
+    q[k] = qs[(long)j * d + k];
+    S[k] = 0.0;
+    F[k] = 0.0;
+  }
+  double emb = 0.0, wgt = 0.0;
+  for (int i = lane; i < n; i += 32) {
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double t = __dsub_rn(xs[(long)i * d + k], q[k]);
+      s = __dadd_rn(s, __dmul_rn(t, t));
+    }
+    const double kv = exp(-s / twobw);
+    emb += kv;
+    for (int k = 0; k < d; ++k) S[k] += kv * xs[(long)i * d + k];
+  }
+  for (int i = lane; i < l; i += 32) {
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double t = __dsub_rn(xt[(long)i * d + k], q[k]);
+      s = __dadd_rn(s, __dmul_rn(t, t));
+    }
+    const double kv = gamma[i] * exp(-s / twobw);
+    wgt += kv;
+    for (int k = 0; k < d; ++k) F[k] += kv * xt[(long)i * d + k];
+  }
+  emb = warp_sum(emb) / n;
+  wgt = warp_sum(wgt);
+  const double tl = 2.0 * lambda2;
+  for (int k = 0; k < d; ++k) {
+    const double sk = warp_sum(S[k]) / n - emb * q[k];
+    const double fk = warp_sum(F[k]) - wgt * q[k];
+    if (lane == 0) tmap[(long)j * d + k] = q[k] - (sk - fk) / (tl * bw);
+  }
+  if (lane == 0) u[j] = (emb - wgt) / tl;
+}
+
+void evaluate_map_device(const double* xs, int n, const double* xt, const double* gamma, int l, const double* qs,
+                         int m, int d, double bw, double lambda2, double* u, double* tmap, cudaStream_t st) {
+  kot_require(d >= 1 && d <= MAP_MAXD, KOT_EINVAL, "query dimension must be in [1, 64]");
+  evaluate_map_kernel<<<ceil_div(m, 4), 128, 0, st>>>(xs, n, xt, gamma, l, qs, m, d, 2.0 * bw, bw, lambda2, u,
+                                                      tmap);
+  KOT_LAUNCH_CHECK();
+}
+
+}  // namespace kot

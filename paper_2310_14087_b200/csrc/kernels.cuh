@@ -11,6 +11,9 @@ void assemble_device(const double* xs, int nx, const double* ys, int ny, const d
                      int d, double bw, double lambda2, double* Q, double* Kmat, double* embed, double* z,
                      double* q_sq, double* scratch, cudaStream_t st);
 
+void evaluate_map_device(const double* xs, int n, const double* xt, const double* gamma, int l, const double* qs,
+                         int m, int d, double bw, double lambda2, double* u, double* tmap, cudaStream_t st);
+
 // ---------------------------------------------------------------- chol.cu
 // Upper R with RᵀR = sym(K) + jitter·I (row-major).  work: n*n doubles; dscal: 1 device double.
 double cholesky_psd_device(const double* K, int n, double* R, double* work, double* dscal, int* dflag,
@@ -35,6 +38,8 @@ struct EigWork {
 };
 // Z symmetric (n×n, row-major, device).  Outputs: P (columns = eigenvectors,
 // descending eigenvalues), vals (descending), *dk = #(vals > 0).
-void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigWork& w, cudaStream_t st);
+// lane: 0 = latency-critical caller (always keeps a co-residency slot), 1 = background.
+void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigWork& w, cudaStream_t st,
+                  int lane = 0);
 
 }  // namespace kot

@@ -8,7 +8,9 @@
 // the control flow (norms, pAp, flags) cross to the host.
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <exception>
+#include <mutex>
 #include <thread>
 #include <utility>
 #include <vector>
@@ -220,11 +222,140 @@ static void copy_state(Problem& p, Bufs& b, Decomp& dw, const Decomp& dv) {
   dw.k = dv.k;
 }
 
+// ------------------------------------------------------------ EG pipeline
+//
+// The safeguard sequence v_{j+1} = eg_step(v_j) (eg.py:34-41) never depends on
+// the Newton iterate: solver.py:186-192 copies v into w on an EG acceptance but
+// never the other way.  So v_1, v_2, … and their residuals are produced ahead
+// of the Newton chain by two host threads on their own streams (thread A: EG
+// steps, thread B: residual at v_j), and the solve loop consumes slot j at the
+// iteration whose safeguard step produces v_j.  Same operations, same values,
+// same acceptance logic; only the schedule changes (3 concurrent chains).
+struct EgSlot {
+  double *g = nullptr, *X = nullptr, *r1 = nullptr, *r2 = nullptr, *P = nullptr, *vals = nullptr;
+  int k = 0;
+  double res = 0.0, eg_ms = 0.0, resid_ms = 0.0;
+  std::exception_ptr err = nullptr;
+};
+
+class EgPipeline {
+ public:
+  EgPipeline(Problem& p, double stepsize) : p_(p), s_(stepsize) {
+    const int n = p.n;
+    const long nn = (long)n * n;
+    for (auto& sl : slots_) {
+      sl.g = p.alloc(n);
+      sl.X = p.alloc(nn);
+      sl.r1 = p.alloc(n);
+      sl.r2 = p.alloc(nn);
+      sl.P = p.alloc(nn);
+      sl.vals = p.alloc(n);
+    }
+    Problem& a = p.aux();
+    Problem& bb = p.aux2();
+    KOT_CUDA(cudaMemsetAsync(v0g_ = p.alloc(n), 0, sizeof(double) * n, p.st));
+    KOT_CUDA(cudaMemsetAsync(v0X_ = p.alloc(nn), 0, sizeof(double) * nn, p.st));
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+    ta_ = std::thread([this, &a] { run_steps(a); });
+    tb_ = std::thread([this, &bb] { run_residuals(bb); });
+  }
+  ~EgPipeline() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    ta_.join();
+    tb_.join();
+  }
+  // Slot of v_j (j >= 1) once its residual is evaluated.  Also releases v_{j-2}.
+  EgSlot& acquire(int j) {
+    std::unique_lock<std::mutex> lk(mu_);
+    consumed_ = std::max(consumed_, j - 2);  // v_{j-1} stays valid (stale r_v / decomp_v reuse)
+    cv_.notify_all();
+    cv_.wait(lk, [&] { return evaluated_ >= j || failed_at_ == j; });
+    return slots_[j % kDepth];
+  }
+
+ private:
+  static constexpr int kDepth = 4;
+  Problem& p_;
+  double s_;
+  EgSlot slots_[kDepth];
+  double *v0g_ = nullptr, *v0X_ = nullptr;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  bool stop_ = false;
+  int produced_ = 0, evaluated_ = 0, consumed_ = 0, failed_at_ = -1;
+  std::thread ta_, tb_;
+
+  void run_steps(Problem& a) {
+    for (int j = 1;; ++j) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        // slot j%D is reusable once v_{j-D} was consumed (released) by the solve loop
+        cv_.wait(lk, [&] { return stop_ || (j - kDepth <= consumed_ && failed_at_ < 0); });
+        if (stop_ || failed_at_ >= 0) return;
+      }
+      EgSlot& out = slots_[j % kDepth];
+      const double* gin = (j == 1) ? v0g_ : slots_[(j - 1) % kDepth].g;
+      const double* Xin = (j == 1) ? v0X_ : slots_[(j - 1) % kDepth].X;
+      try {
+        KOT_CUDA(cudaSetDevice(a.device));
+        const auto t0 = clk::now();
+        eg_step(a, gin, Xin, s_, out.g, out.X);
+        KOT_CUDA(cudaStreamSynchronize(a.st));
+        out.eg_ms = ms_since(t0);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu_);
+        out.err = std::current_exception();
+        failed_at_ = j;
+        cv_.notify_all();
+        return;
+      }
+      std::lock_guard<std::mutex> lk(mu_);
+      produced_ = j;
+      cv_.notify_all();
+    }
+  }
+
+  void run_residuals(Problem& b) {
+    for (int j = 1;; ++j) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || produced_ >= j || failed_at_ >= 0; });
+        if (stop_ || (produced_ < j)) return;
+      }
+      EgSlot& sl = slots_[j % kDepth];
+      try {
+        KOT_CUDA(cudaSetDevice(b.device));
+        const auto t0 = clk::now();
+        Decomp dc{sl.P, sl.vals, 0};
+        sl.res = residual_parts(b, sl.g, sl.X, sl.r1, sl.r2, dc);
+        sl.k = dc.k;
+        sl.resid_ms = ms_since(t0);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu_);
+        sl.err = std::current_exception();
+        failed_at_ = j;
+        cv_.notify_all();
+        return;
+      }
+      std::lock_guard<std::mutex> lk(mu_);
+      evaluated_ = j;
+      cv_.notify_all();
+    }
+  }
+};
+
 // One pass of the solver.py:142-222 loop body on the current buffers.
 // Returns false if a non-finite residual was met (SolverNumericsError).
 struct LoopState {
   double res_w, res_v, theta;
   Decomp dw, dv, dt;
+  EgPipeline* pipe = nullptr;  // when set, v comes from the pipeline (slot vj)
+  int vj = 0;
+  EgSlot* vslot = nullptr;     // slot of the current v (for EG acceptance)
 };
 
 static bool loop_body(Problem& p, const SolverCfg& cfg, LoopState& s, int k, IterRecord& rec, IterCallback cb,
@@ -242,7 +373,7 @@ static bool loop_body(Problem& p, const SolverCfg& cfg, LoopState& s, int k, Ite
   std::exception_ptr eg_err = nullptr;
   double eg_resid_ms = 0.0;
   std::thread eg_thread;
-  if (do_eg) {
+  if (do_eg && !s.pipe) {
     Problem& a = p.aux();
     eg_thread = std::thread([&]() {
       try {
@@ -280,6 +411,15 @@ static bool loop_body(Problem& p, const SolverCfg& cfg, LoopState& s, int k, Ite
     nt_err = std::current_exception();
   }
   if (eg_thread.joinable()) eg_thread.join();
+  if (do_eg && s.pipe) {
+    EgSlot& sl = s.pipe->acquire(++s.vj);
+    if (sl.err) eg_err = sl.err;
+    s.vslot = &sl;
+    s.res_v = sl.res;
+    s.dv = Decomp{sl.P, sl.vals, sl.k};
+    eg_ms = sl.eg_ms;
+    eg_resid_ms = sl.resid_ms;
+  }
   if (eg_err) std::rethrow_exception(eg_err);
   if (nt_err) std::rethrow_exception(nt_err);
   resid_ms += eg_resid_ms;
@@ -322,7 +462,18 @@ static bool loop_body(Problem& p, const SolverCfg& cfg, LoopState& s, int k, Ite
     s.res_w = res_t;
   } else {
     acc_ssn = 0;
-    copy_state(p, b, s.dw, s.dv);
+    if (s.pipe) {  // w ← v.copy() from the pipeline slot of the current v
+      EgSlot& sl = *s.vslot;
+      KOT_CUDA(cudaMemcpyAsync(b.gw, sl.g, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
+      KOT_CUDA(cudaMemcpyAsync(b.Xw, sl.X, sizeof(double) * nn, cudaMemcpyDeviceToDevice, p.st));
+      KOT_CUDA(cudaMemcpyAsync(b.r1w, sl.r1, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
+      KOT_CUDA(cudaMemcpyAsync(b.r2w, sl.r2, sizeof(double) * nn, cudaMemcpyDeviceToDevice, p.st));
+      KOT_CUDA(cudaMemcpyAsync(s.dw.P, sl.P, sizeof(double) * nn, cudaMemcpyDeviceToDevice, p.st));
+      KOT_CUDA(cudaMemcpyAsync(s.dw.vals, sl.vals, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
+      s.dw.k = sl.k;
+    } else {
+      copy_state(p, b, s.dw, s.dv);
+    }
     s.res_w = s.res_v;
   }
   rec.iteration = k;
@@ -381,6 +532,11 @@ SolveResult solve(Problem& p, const SolverCfg& cfg, IterCallback cb, void* user,
   int k = 0;
   bool conv = res0 <= cfg.residual_tol;
   bool finite = std::isfinite(res0);
+  std::unique_ptr<EgPipeline> pipe;
+  if (!pure_eg && finite && !conv) {
+    pipe.reset(new EgPipeline(p, cfg.eg_stepsize));
+    s.pipe = pipe.get();
+  }
   while (finite && !conv && k < cfg.max_iter) {
     IterRecord rec{};
     if (pure_eg) {
@@ -434,6 +590,7 @@ struct Session {
   HostProbe hp;
   int k = 0;
   bool conv = false;
+  std::unique_ptr<EgPipeline> pipe;
 };
 
 Session* session_begin(Problem& p, const SolverCfg& cfg) {
@@ -452,6 +609,8 @@ Session* session_begin(Problem& p, const SolverCfg& cfg) {
     delete se;
     throw KotError(KOT_ENUMERICS, "non-finite residual in solver iterate");
   }
+  se->pipe.reset(new EgPipeline(p, cfg.eg_stepsize));
+  se->s.pipe = se->pipe.get();
   return se;
 }
 

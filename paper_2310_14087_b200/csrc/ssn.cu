@@ -53,6 +53,7 @@ void Problem::init_scratch() {
 Problem::~Problem() {
   if (st) cudaStreamSynchronize(st);
   aux_.reset();
+  aux2_.reset();
   eig.reset();
   for (double* p : owned) cudaFree(p);
   if (hsc) cudaFreeHost(hsc);
@@ -67,7 +68,11 @@ static std::unique_ptr<Problem> make_problem(int n, int device) {
   std::unique_ptr<Problem> p(new Problem());
   p->n = n;
   p->device = device;
-  KOT_CUDA(cudaStreamCreateWithFlags(&p->st, cudaStreamNonBlocking));
+  {  // the Newton chain (critical path) gets the highest stream priority
+    int lo = 0, hi = 0;
+    KOT_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    KOT_CUDA(cudaStreamCreateWithPriority(&p->st, cudaStreamNonBlocking, hi));
+  }
   const long nn = (long)n * n;
   p->Q = p->alloc(nn);
   p->z = p->alloc(n);
@@ -484,7 +489,7 @@ void phi_adjoint(Problem& p, const double* g, double* out) { phi_adjoint_ex(p, g
 
 void eigh(Problem& p, const double* Z, Decomp& dc) {
   ProfScope ps("eigh", p.st, 14.0 / 3.0 * p.n * (double)p.n * p.n);
-  syevd_device(Z, p.n, dc.P, dc.vals, p.dk, *p.eig, p.st);
+  syevd_device(Z, p.n, dc.P, dc.vals, p.dk, *p.eig, p.st, p.lane);
   KOT_CUDA(cudaMemcpyAsync(p.hk, p.dk, sizeof(int), cudaMemcpyDeviceToHost, p.st));
   KOT_CUDA(cudaStreamSynchronize(p.st));
   dc.k = p.hk[0];
@@ -610,25 +615,35 @@ void eg_step(Problem& p, const double* g, const double* X, double s, double* g_o
   proj(p, dc, nullptr, X_out);
 }
 
+static void make_context(Problem& src, std::unique_ptr<Problem>& dst) {
+  KOT_CUDA(cudaSetDevice(src.device));
+  dst.reset(new Problem());
+  Problem& a = *dst;
+  a.n = src.n;
+  a.device = src.device;
+  a.l1 = src.l1;
+  a.l2 = src.l2;
+  a.q_sq = src.q_sq;
+  a.jitter = src.jitter;
+  a.has_embed = src.has_embed;
+  a.Q = src.Q;  // shared, not owned
+  a.z = src.z;
+  a.R = src.R;
+  a.embed = src.embed;
+  a.lane = 1;
+  int lo = 0, hi = 0;
+  KOT_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  KOT_CUDA(cudaStreamCreateWithPriority(&a.st, cudaStreamNonBlocking, lo));
+  a.init_scratch();
+}
+
+Problem& Problem::aux2() {
+  if (!aux2_) make_context(*this, aux2_);
+  return *aux2_;
+}
+
 Problem& Problem::aux() {
-  if (!aux_) {
-    KOT_CUDA(cudaSetDevice(device));
-    aux_.reset(new Problem());
-    Problem& a = *aux_;
-    a.n = n;
-    a.device = device;
-    a.l1 = l1;
-    a.l2 = l2;
-    a.q_sq = q_sq;
-    a.jitter = jitter;
-    a.has_embed = has_embed;
-    a.Q = Q;  // shared, not owned
-    a.z = z;
-    a.R = R;
-    a.embed = embed;
-    KOT_CUDA(cudaStreamCreateWithFlags(&a.st, cudaStreamNonBlocking));
-    a.init_scratch();
-  }
+  if (!aux_) make_context(*this, aux_);
   return *aux_;
 }
 

@@ -44,6 +44,7 @@ struct Bufs {
 struct Problem {
   int n = 0;
   int device = 0;
+  int lane = 0;  // 0: Newton chain (priority), 1: EG pipeline contexts
   double l1 = 0, l2 = 0, q_sq = 0, jitter = 0;
   bool has_embed = false;
   cudaStream_t st = nullptr;
@@ -68,8 +69,9 @@ struct Problem {
   Bufs& bufs();
   // second execution context (own stream + scratch, shared instance data) on
   // which the EG safeguard chain runs concurrently with the Newton chain
-  std::unique_ptr<Problem> aux_;
+  std::unique_ptr<Problem> aux_, aux2_;
   Problem& aux();
+  Problem& aux2();
   double* alloc(long count);
   void init_scratch();
   ~Problem();

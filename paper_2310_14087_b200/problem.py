@@ -238,6 +238,30 @@ def residual_parts(pd: ProblemData, w: IteratePair) -> tuple[IteratePair, Residu
     return IteratePair(r1, r2), ResidualInfo(ev, int(k.value))
 
 
+def evaluate_map(pd: ProblemData, samples_mu: SampleSet, gamma_hat, queries) -> tuple[np.ndarray, np.ndarray]:
+    """Dual potential u and transport map T = id − ∇u at query points (problem.py:254-284), on the GPU."""
+    if pd.filling is None or pd.spec_x is None:
+        raise ValueError("instance carries no filling points / kernel specs")
+    q = _lib.f64(np.atleast_2d(np.asarray(queries, dtype=float)))
+    if q.shape[1] != pd.spec_x.input_dim:
+        raise ValueError("query dimension mismatch")
+    xs, xt = _lib.f64(samples_mu.points), _lib.f64(pd.filling.x_tilde)
+    g = _lib.f64(gamma_hat, (pd.n,))
+    m, d = q.shape
+    u, t = np.empty(m), np.empty((m, d))
+    dev = pd._dev.device if pd._dev is not None else _lib.default_device()
+    _lib.check(_lib.lib().kot_evaluate_map(_lib.ptr(xs), xs.shape[0], _lib.ptr(xt), _lib.ptr(g), pd.n, _lib.ptr(q),
+                                           m, d, float(pd.spec_x.bandwidth_sq), float(pd.lambda2), dev,
+                                           _lib.ptr(u), _lib.ptr(t)))
+    return u, t
+
+
+def potential_and_map(pd: ProblemData, samples_mu: SampleSet, gamma_hat, query) -> tuple[float, np.ndarray]:
+    """Single-point wrapper around :func:`evaluate_map` (problem.py:287-295)."""
+    u, t = evaluate_map(pd, samples_mu, gamma_hat, np.atleast_2d(query))
+    return float(u[0]), t[0]
+
+
 def residual(pd: ProblemData, w: IteratePair) -> IteratePair:
     """Nonsmooth KKT residual (problem.py:217-219)."""
     return residual_parts(pd, w)[0]
@@ -245,4 +269,4 @@ def residual(pd: ProblemData, w: IteratePair) -> IteratePair:
 
 __all__ = ["FillingPoints", "IteratePair", "ProblemData", "DeviceProblem", "SpectralDecomp", "zero_pair",
            "build_kernel_specs", "assemble", "phi_forward", "phi_adjoint", "objective", "ot_estimate",
-           "residual_parts", "residual", "ResidualInfo"]
+           "residual_parts", "residual", "ResidualInfo", "evaluate_map", "potential_and_map"]

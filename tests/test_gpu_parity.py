@@ -389,3 +389,16 @@ def test_tight_profile_end_state(cfg1):
     assert obj == pytest.approx(float(cfg1["tight_objective"]), rel=1e-8)
     assert rel(rep.gamma_hat, cfg1["tight_gamma"]) <= 1e-6
     assert rep.ot_estimate == pytest.approx(float(cfg1["tight_ot"]), rel=1e-8)
+
+
+def test_evaluate_map(cfg1):
+    """§8(f) next #1: potentials / Monge map at query points vs the reference (problem.py:254-284)."""
+    sx, sy, sxy = K.build_kernel_specs(2, float(cfg1["bw_sq"]))
+    pd = gpu_pd(cfg1)
+    pd.filling = K.FillingPoints(cfg1["xt"], cfg1["yt"])
+    pd.spec_x = sx
+    u, t = GP.evaluate_map(pd, K.SampleSet(cfg1["xs"]), cfg1["tight_gamma"], cfg1["map_queries"])
+    assert rel(u, cfg1["map_u"]) <= 1e-12
+    assert rel(t, cfg1["map_t"]) <= 1e-12
+    u1, t1 = GP.potential_and_map(pd, K.SampleSet(cfg1["xs"]), cfg1["tight_gamma"], cfg1["map_queries"][0])
+    assert u1 == pytest.approx(float(cfg1["map_u"][0]), rel=1e-12)

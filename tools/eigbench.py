@@ -1,4 +1,10 @@
 """Isolated eigensolver timing (library phase profiler), n from argv."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
 import sys
 
 import numpy as np

@@ -1,4 +1,10 @@
 """Quick GPU probe: assemble a config, run a few SSN iterations with the phase profiler on."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
 import json
 import sys
 import time

@@ -1,4 +1,10 @@
 """Diagnostic: tight-profile cfg1 solve to 1e-10 on the GPU, iteration count + residual checkpoints."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
 import numpy as np
 
 import paper_2310_14087_b200 as K
