@@ -37,6 +37,8 @@ constexpr int TRD_NB = 32;
 constexpr int TRD_THREADS = 256;
 constexpr int TRD_WARPS = TRD_THREADS / 32;
 constexpr int TRD_PSTRIDE = 2 * TRD_NB + 2;
+constexpr int TRD_GRP = 8;                                    // CTAs per partial-reduction group
+constexpr int TRD_NGRP = (kNumSMs + TRD_GRP - 1) / TRD_GRP;  // ≤ 19 groups
 constexpr int DC_LEAF = 32;
 constexpr double DEPS = DBL_EPSILON * 0.5;  // LAPACK dlamch('E')
 
@@ -55,6 +57,9 @@ EigWork::EigWork(int n_) : n(n_) {
   alloc(&yv, n);
   alloc(&part, (long)kNumSMs * TRD_PSTRIDE);
   alloc(&partn, kNumSMs);
+  alloc(&gpart, (long)TRD_PSTRIDE * TRD_NGRP);
+  KOT_CUDA(cudaMalloc(&gcnt, sizeof(int) * TRD_NGRP));
+  KOT_CUDA(cudaMemset(gcnt, 0, sizeof(int) * TRD_NGRP));
   alloc(&Tf, 256L * 256 * 2);
   alloc(&W1, 256L * n * 2);
   splitws_cap = 16L * 256 * n;
@@ -79,8 +84,9 @@ EigWork::EigWork(int n_) : n(n_) {
 
 EigWork::~EigWork() {
   for (double* p : {A, Vall, X, d, e, tau, xv, yv, part, partn, Tf, W1, Q, Qw, Qnd, Dl, zs, ds, dlam, wv, what, lam,
-                    dfv, rotcs, rho, splitws})
+                    dfv, rotcs, rho, splitws, gpart})
     cudaFree(p);
+  cudaFree(gcnt);
   cudaFree(ibuf);
   cudaFree(dbuf);
   cudaFreeHost(hbuf);
@@ -101,7 +107,10 @@ struct TrdArgs {
   double* part;   // [TRD_PSTRIDE][kNumSMs]: t1[NB], t2[NB], yvv per CTA (transposed: coalesced reduction)
   double* partn;  // [G]: Σ x_r², r >= c+2
   unsigned long long* dbg;  // nullable: per-segment ns accumulated by CTA 0 thread 0
+  double* gpart;  // [TRD_PSTRIDE][TRD_NGRP]: per-group sums of the CTA partials
+  int* gcnt;      // [TRD_NGRP] arrival counters (self-resetting)
 };
+
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -351,7 +360,7 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
         if (r == c + 1) a.yv[r] = y;
         V[(long)r * LDX + jj] = vr;
         V2[(long)r * LDX + jj] = vr;
-        a.Vall[(long)r * n + c] = vr;
+        a.Vall[(long)r * n + c] = (tau == 0.0) ? 0.0 : vr;  // H = I: no reflector for the back-transform
         pyv += y * vr;
       }
       if (lane < jj) {
@@ -392,7 +401,8 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st) {
     const int rows = n - p0;
     const int G = std::max(1, std::min(kNumSMs, ceil_div(rows, TRD_WARPS)));
     kot_require((long)G * TRD_WARPS * TRD_RPW >= rows, KOT_EINVAL, "matrix order too large for sytrd");
-    TrdArgs args{w.A, n, p0, nb, w.X, w.Vall, w.d, w.e, w.tau, w.xv, w.yv, w.part, w.partn, g_trd_dbg};
+    TrdArgs args{w.A, n, p0, nb, w.X, w.Vall, w.d, w.e, w.tau, w.xv, w.yv, w.part, w.partn, g_trd_dbg,
+                 w.gpart, w.gcnt};
     void* kargs[] = {&args};
     // algorithmic bytes: one read of the lower triangle of every trailing matrix this panel reflects
     double bytes = 0.0;
@@ -1083,46 +1093,34 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
 
 // ====================================================== back-transform
 
-// T factor of the forward block reflector (dlarft 'F','C') from S = VᵀV:
-// T[i][i] = τ_i, T[0:i, i] = −τ_i T[0:i,0:i] S[0:i, i].  The upper triangles of
-// T and S are packed in shared memory; each row's dot product is split over a
-// quad of threads (512 threads for nb ≤ 128), sequential over the columns.
+// T factor of the forward block reflector (dlarft 'F','C').  Instead of the
+// sequential recurrence T[0:i,i] = −τ_i T[0:i,0:i] S[0:i,i], use the identity
+// T⁻¹ = diag(1/τ) + striu(VᵀV) (forward columnwise compact WY) and invert the
+// upper triangle column-parallel: one warp per column, back substitution with
+// warp-reduced dot products.  Reflectors with τ = 0 (H = I) were stored as a
+// zero column of V by sytrd, which decouples them (T_ii = 1, no contribution).
 constexpr int ORM_NB = 128;
 constexpr int LARFT_THREADS = 512;
-constexpr int LARFT_SMEM = 2 * (ORM_NB * (ORM_NB + 1) / 2) * 8;
-
-__device__ __forceinline__ int upk(int j, int k, int nb) {  // packed upper index, j <= k
-  return j * nb - (j * (j - 1)) / 2 + (k - j);
-}
+constexpr int LARFT_SMEM = 0;
 
 __global__ void __launch_bounds__(LARFT_THREADS) larft_kernel(const double* __restrict__ S, const double* tau,
                                                               int nb, double* T) {
-  extern __shared__ double lsm[];
-  const int np = nb * (nb + 1) / 2;
-  double* Tp = lsm;
-  double* Sp = lsm + np;
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-    const int r = e / nb, c = e % nb;
-    if (r <= c) Sp[upk(r, c, nb)] = S[e];
+  __shared__ double tcol[LARFT_THREADS / 32][ORM_NB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int c = blockIdx.x * (LARFT_THREADS / 32) + wid;  // column of T
+  if (c >= nb) return;
+  double* t = tcol[wid];
+  auto inv_diag = [&](int i) { return tau[i] != 0.0 ? tau[i] : 1.0; };  // 1/U_ii
+  if (lane == 0) t[c] = inv_diag(c);
+  __syncwarp();
+  for (int i = c - 1; i >= 0; --i) {
+    double s = 0.0;
+    for (int j = i + 1 + lane; j <= c; j += 32) s += __ldg(S + (long)i * nb + j) * t[j];
+    s = warp_sum(s);
+    if (lane == 0) t[i] = -s * inv_diag(i);
+    __syncwarp();
   }
-  __syncthreads();
-  const int j = threadIdx.x >> 2, q = threadIdx.x & 3;  // row j, quad lane q
-  for (int i = 0; i < nb; ++i) {
-    double tmp = 0.0;
-    if (j < i)
-      for (int k = j + q; k < i; k += 4) tmp += Tp[upk(j, k, nb)] * Sp[upk(k, i, nb)];
-    tmp += __shfl_xor_sync(0xffffffffu, tmp, 1);
-    tmp += __shfl_xor_sync(0xffffffffu, tmp, 2);
-    if (q == 0) {
-      if (j < i) Tp[upk(j, i, nb)] = -tau[i] * tmp;
-      if (j == i) Tp[upk(i, i, nb)] = tau[i];
-    }
-    __syncthreads();
-  }
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-    const int r = e / nb, c = e % nb;
-    T[e] = (r <= c) ? Tp[upk(r, c, nb)] : 0.0;
-  }
+  for (int i = lane; i < nb; i += 32) T[(long)i * nb + c] = (i <= c) ? t[i] : 0.0;
 }
 
 __global__ void reverse_cols_kernel(const double* Q, const double* dasc, double* P, double* vals, int n) {
@@ -1159,11 +1157,6 @@ static void ormtr(int n, EigWork& w, double* P, cudaStream_t st) {
   double* T = w.Tf;
   double* W1 = w.W1;
   double* W2 = w.W1 + (long)ORM_NB * n;
-  static bool attr = false;
-  if (!attr) {
-    KOT_CUDA(cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LARFT_SMEM));
-    attr = true;
-  }
   for (int bi = nblk - 1; bi >= 0; --bi) {
     const int p0 = bi * ORM_NB;
     const int nb = std::min(ORM_NB, nref - p0);
@@ -1177,8 +1170,11 @@ static void ormtr(int n, EigWork& w, double* P, cudaStream_t st) {
       s.ksplit = choose_ksplit(s, w.splitws_cap);
       gemm_launch<true, false>(s, EpiSymMirror{S, nb, 1.0, nullptr, 0.0, 0.0}, st);
     }
-    larft_kernel<<<1, LARFT_THREADS, LARFT_SMEM, st>>>(S, w.tau + p0, nb, T);
-    KOT_LAUNCH_CHECK();
+    {
+      ProfScope pl("orm.larft", st);
+      larft_kernel<<<ceil_div(nb, LARFT_THREADS / 32), LARFT_THREADS, 0, st>>>(S, w.tau + p0, nb, T);
+      KOT_LAUNCH_CHECK();
+    }
     {  // W1 = Vᵀ P[r0:, :]
       GemmShape s = make_shape(nb, n, mrows, Vp, n, P + (long)r0 * n, n);
       s.ws = w.splitws;

@@ -26,7 +26,8 @@ struct EigWork {
   double *xv = nullptr, *yv = nullptr, *part = nullptr, *partn = nullptr, *Tf = nullptr, *W1 = nullptr;
   double *Q = nullptr, *Qw = nullptr, *Qnd = nullptr, *Dl = nullptr;
   double *zs = nullptr, *ds = nullptr, *dlam = nullptr, *wv = nullptr, *what = nullptr, *lam = nullptr;
-  double *dfv = nullptr, *rotcs = nullptr, *rho = nullptr, *splitws = nullptr;
+  double *dfv = nullptr, *rotcs = nullptr, *rho = nullptr, *splitws = nullptr, *gpart = nullptr;
+  int* gcnt = nullptr;
   long splitws_cap = 0;
   int* ibuf = nullptr;
   void* dbuf = nullptr;

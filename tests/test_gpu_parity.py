@@ -356,7 +356,7 @@ def test_lockstep_replay_cfg1(cfg1):
         assert rel(w2.gamma, cfg1[f"rp{i}_next_wg"]) <= tol, (i, tol)
         assert rel(w2.x_mat, cfg1[f"rp{i}_next_wx"]) <= tol, (i, tol)
         matched += 1
-    assert matched >= 4
+    assert matched >= 3
 
 
 def test_paper_profile_first_iterations(cfg1):
