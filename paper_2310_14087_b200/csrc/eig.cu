@@ -1101,23 +1101,28 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
 // zero column of V by sytrd, which decouples them (T_ii = 1, no contribution).
 constexpr int ORM_NB = 128;
 constexpr int LARFT_THREADS = 512;
-constexpr int LARFT_SMEM = 0;
+constexpr int LARFT_LDS = ORM_NB + 1;
+constexpr int LARFT_SMEM = ORM_NB * LARFT_LDS * 8;  // S staged in shared memory
 
-__global__ void __launch_bounds__(LARFT_THREADS) larft_kernel(const double* __restrict__ S, const double* tau,
+__global__ void __launch_bounds__(LARFT_THREADS) larft_kernel(const double* __restrict__ Sg, const double* tau,
                                                               int nb, double* T) {
+  extern __shared__ double S_s[];  // [nb][LARFT_LDS]
   __shared__ double tcol[LARFT_THREADS / 32][ORM_NB];
+  __shared__ double dinv[ORM_NB];  // 1/U_ii = τ_i (1 for τ_i = 0)
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) S_s[(e / nb) * LARFT_LDS + e % nb] = Sg[e];
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) dinv[i] = tau[i] != 0.0 ? tau[i] : 1.0;
+  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int c = blockIdx.x * (LARFT_THREADS / 32) + wid;  // column of T
   if (c >= nb) return;
   double* t = tcol[wid];
-  auto inv_diag = [&](int i) { return tau[i] != 0.0 ? tau[i] : 1.0; };  // 1/U_ii
-  if (lane == 0) t[c] = inv_diag(c);
+  if (lane == 0) t[c] = dinv[c];
   __syncwarp();
   for (int i = c - 1; i >= 0; --i) {
     double s = 0.0;
-    for (int j = i + 1 + lane; j <= c; j += 32) s += __ldg(S + (long)i * nb + j) * t[j];
+    for (int j = i + 1 + lane; j <= c; j += 32) s += S_s[i * LARFT_LDS + j] * t[j];
     s = warp_sum(s);
-    if (lane == 0) t[i] = -s * inv_diag(i);
+    if (lane == 0) t[i] = -s * dinv[i];
     __syncwarp();
   }
   for (int i = lane; i < nb; i += 32) T[(long)i * nb + c] = (i <= c) ? t[i] : 0.0;
@@ -1172,7 +1177,12 @@ static void ormtr(int n, EigWork& w, double* P, cudaStream_t st) {
     }
     {
       ProfScope pl("orm.larft", st);
-      larft_kernel<<<ceil_div(nb, LARFT_THREADS / 32), LARFT_THREADS, 0, st>>>(S, w.tau + p0, nb, T);
+      static bool attr = false;
+      if (!attr) {
+        KOT_CUDA(cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LARFT_SMEM));
+        attr = true;
+      }
+      larft_kernel<<<ceil_div(nb, LARFT_THREADS / 32), LARFT_THREADS, LARFT_SMEM, st>>>(S, w.tau + p0, nb, T);
       KOT_LAUNCH_CHECK();
     }
     {  // W1 = Vᵀ P[r0:, :]

@@ -20,7 +20,13 @@
 
 namespace kot {
 
-constexpr int GB_M = 64, GB_N = 64, GB_K = 16, G_STAGES = 3, G_THREADS = 128;
+#ifndef KOT_GEMM_STAGES
+#define KOT_GEMM_STAGES 4
+#endif
+#ifndef KOT_GEMM_BK
+#define KOT_GEMM_BK 8
+#endif
+constexpr int GB_M = 64, GB_N = 64, GB_K = KOT_GEMM_BK, G_STAGES = KOT_GEMM_STAGES, G_THREADS = 128;
 constexpr int G_PADK = GB_K + 4;  // stride ≡ 4 (mod 16) doubles → conflict-free fragment loads
 constexpr int G_PADM = GB_M + 4;
 constexpr int G_PADN = GB_N + 4;
