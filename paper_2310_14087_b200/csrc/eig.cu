@@ -65,9 +65,10 @@ EigWork::EigWork(int n_) : n(n_) {
   splitws_cap = 16L * 256 * n;
   alloc(&splitws, splitws_cap);
   alloc(&Q, nn);
-  alloc(&Qw, nn);
-  alloc(&Qnd, nn);
-  alloc(&Dl, nn);
+  alloc(&Qw, nn + 2L * n + 8);
+  alloc(&Qnd, nn + 2L * n + 8);
+  alloc(&Dl, nn + 2L * n + 8);
+  alloc(&Uw, nn + 2L * n + 8);
   alloc(&zs, n);
   alloc(&ds, n);
   alloc(&dlam, n);
@@ -83,7 +84,7 @@ EigWork::EigWork(int n_) : n(n_) {
 }
 
 EigWork::~EigWork() {
-  for (double* p : {A, Vall, X, d, e, tau, xv, yv, part, partn, Tf, W1, Q, Qw, Qnd, Dl, zs, ds, dlam, wv, what, lam,
+  for (double* p : {A, Vall, X, d, e, tau, xv, yv, part, partn, Tf, W1, Q, Qw, Qnd, Dl, Uw, zs, ds, dlam, wv, what, lam,
                     dfv, rotcs, rho, splitws, gpart})
     cudaFree(p);
   cudaFree(gcnt);
@@ -525,6 +526,8 @@ __global__ void dc_leaf_kernel(double* d, const double* e, const int* leaf_off, 
     for (int i = 0; i < m; ++i) d[o + i] = dd[i];
 }
 
+constexpr int MS = 8;  // meta ints per merge: K, ndefl, nrot, c1 (top-only), c12 (top-only + mixed)
+
 struct MergeDesc {
   int o, n1, n2;
   long off;  // offset of this merge's K×K / n×K scratch (prefix of n_m²)
@@ -567,7 +570,7 @@ __device__ __forceinline__ int rank_le(const double* a, int n, double v) {  // #
 __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
     const MergeDesc* md, const double* Q, int ldq, const double* d, const double* e, double* zs, double* ds,
     double* dlam, double* wv, double* dfv, double* rotcs, double* rho_out, int* perm, int* ndcol, int* dcol,
-    int* rot, int* meta) {
+    int* rot, int* meta, int* pidx) {
   extern __shared__ double psm[];
   __shared__ double red[32];
   const MergeDesc m = md[blockIdx.x];
@@ -601,15 +604,12 @@ __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) perm[o + i] = P[i];
-  if (threadIdx.x != 0) return;
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
     zmax = fmax(zmax, red[w]);
     dmax = fmax(dmax, red[16 + w]);
   }
   const double rho = fabs(2.0 * esplit);
-  rho_out[blockIdx.x] = rho;
   const double tol = 8.0 * DEPS * fmax(dmax, zmax);
-  int K = 0, nd = 0, nr = 0;
   int* NDC = ndcol + o;
   int* DC = dcol + o;
   int* RT = rot + 2 * o;
@@ -617,6 +617,93 @@ __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
   double* RCS = rotcs + 2 * o;
   double* WV = wv + o;
   double* DL = dlam + o;
+  // ---- parallel fast path: if no close pair of non-small z triggers a deflation rotation, the
+  // sequential dlaed2 scan reduces to "non-small → secular, small → deflated", in sorted order.
+  __shared__ int trig_sh, tot_sh;
+  __shared__ int csum[DC_PREP_THREADS];
+  int* prevnz = reinterpret_cast<int*>(Du);  // Du is dead after the merge: reuse as int scratch
+  if (threadIdx.x == 0) trig_sh = (rho * zmax <= tol) ? 1 : 0;  // everything deflates: sequential path
+  __syncthreads();
+  const int chunk = (n + blockDim.x - 1) / blockDim.x;
+  const int j0 = threadIdx.x * chunk, j1 = min(n, j0 + chunk);
+  {  // previous non-small index (chunk-local scan, then carry from the left chunks)
+    int last = -1, cnt = 0;
+    for (int j = j0; j < j1; ++j) {
+      prevnz[j] = last;
+      if (!(rho * fabs(Z[j]) <= tol)) {
+        last = j;
+        ++cnt;
+      }
+    }
+    csum[threadIdx.x] = last;
+    __syncthreads();
+    int carry = -1;
+    for (int q = threadIdx.x - 1; q >= 0 && carry < 0; --q) carry = csum[q];
+    for (int j = j0; j < j1 && (prevnz[j] < 0); ++j) prevnz[j] = carry;
+    __syncthreads();
+    csum[threadIdx.x] = cnt;
+  }
+  for (int j = j0; j < j1; ++j) {
+    if (rho * fabs(Z[j]) <= tol) continue;
+    const int pj = prevnz[j];
+    if (pj < 0) continue;
+    double s = Z[pj], c = Z[j];
+    const double tau = hypot(c, s);
+    const double t = D[j] - D[pj];
+    c /= tau;
+    s = -s / tau;
+    if (fabs(t * c * s) <= tol) trig_sh = 1;
+  }
+  __syncthreads();
+  if (!trig_sh) {
+    __shared__ int ctop[DC_PREP_THREADS];
+    int tops = 0;
+    for (int j = j0; j < j1; ++j)
+      if (!(rho * fabs(Z[j]) <= tol) && P[j] < n1) ++tops;
+    ctop[threadIdx.x] = tops;
+    __syncthreads();
+    // exclusive prefixes of the non-small and top-only counts over chunks
+    if (threadIdx.x == 0) {
+      int acc = 0, acct = 0;
+      for (int q = 0; q < (int)blockDim.x; ++q) {
+        const int v = csum[q], vt = ctop[q];
+        csum[q] = acc;
+        ctop[q] = acct;
+        acc += v;
+        acct += vt;
+      }
+      tot_sh = acct;
+      rho_out[blockIdx.x] = rho;
+      meta[MS * blockIdx.x + 0] = acc;
+      meta[MS * blockIdx.x + 1] = n - acc;
+      meta[MS * blockIdx.x + 2] = 0;
+      meta[MS * blockIdx.x + 3] = acct;  // no rotations: no mixed columns
+      meta[MS * blockIdx.x + 4] = acct;
+    }
+    __syncthreads();
+    const int c1 = tot_sh;
+    int kpos = csum[threadIdx.x], tpos = ctop[threadIdx.x];
+    for (int j = j0; j < j1; ++j) {
+      if (!(rho * fabs(Z[j]) <= tol)) {
+        NDC[kpos] = j;
+        DL[kpos] = D[j];
+        WV[kpos] = Z[j];
+        // GEMM order: top-only columns first, then bottom-only
+        pidx[o + kpos] = (P[j] < n1) ? tpos++ : c1 + (kpos - tpos);
+        ++kpos;
+      } else {
+        const int dpos = j - kpos;  // deflated entries are already ascending (D sorted)
+        DC[dpos] = j;
+        DFV[dpos] = D[j];
+      }
+    }
+    return;
+  }
+  if (threadIdx.x != 0) return;
+  rho_out[blockIdx.x] = rho;
+  int* mask = prevnz;  // origin of each sorted column: 1 top child, 2 bottom child, 3 mixed by rotation
+  for (int j = 0; j < n; ++j) mask[j] = (P[j] < n1) ? 1 : 2;
+  int K = 0, nd = 0, nr = 0;
   if (rho * zmax <= tol) {
     for (int k = 0; k < n; ++k) {
       DC[nd] = k;
@@ -644,6 +731,7 @@ __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
       if (fabs(t * c * s) <= tol) {
         Z[j] = tau;
         Z[pj] = 0.0;
+        mask[j] |= mask[pj];
         RT[2 * nr] = pj;
         RT[2 * nr + 1] = j;
         RCS[2 * nr] = c;
@@ -684,9 +772,24 @@ __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
     DFV[j + 1] = v;
     DC[j + 1] = cidx;
   }
-  meta[4 * blockIdx.x + 0] = K;
-  meta[4 * blockIdx.x + 1] = nd;
-  meta[4 * blockIdx.x + 2] = nr;
+  {  // GEMM order of the secular columns: top-only, mixed, bottom-only
+    int c1 = 0, c2 = 0;
+    for (int k = 0; k < K; ++k) {
+      const int mk = mask[NDC[k]];
+      c1 += (mk == 1);
+      c2 += (mk == 3);
+    }
+    int i1 = 0, i2 = c1, i3 = c1 + c2;
+    for (int k = 0; k < K; ++k) {
+      const int mk = mask[NDC[k]];
+      pidx[o + k] = (mk == 1) ? i1++ : (mk == 3) ? i2++ : i3++;
+    }
+    meta[MS * blockIdx.x + 3] = c1;
+    meta[MS * blockIdx.x + 4] = c1 + c2;
+  }
+  meta[MS * blockIdx.x + 0] = K;
+  meta[MS * blockIdx.x + 1] = nd;
+  meta[MS * blockIdx.x + 2] = nr;
   (void)zs;
   (void)ds;
 }
@@ -697,13 +800,13 @@ __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
 // coalesced stores.
 __global__ void dc_merge_vec_kernel(const MergeDesc* md, const double* Q, double* Qdf, double* Qnd, int ldq,
                                     const int* perm, const int* ndcol, const int* dcol, const int* rot,
-                                    const double* rotcs, const int* meta) {
+                                    const double* rotcs, const int* meta, const int* pidx) {
   extern __shared__ double rowsm[];
   const MergeDesc m = md[blockIdx.y];
   const int o = m.o, n = m.n1 + m.n2;
   const int r = blockIdx.x;
   if (r >= n) return;
-  const int K = meta[4 * blockIdx.y], nd = meta[4 * blockIdx.y + 1], nr = meta[4 * blockIdx.y + 2];
+  const int K = meta[MS * blockIdx.y], nd = meta[MS * blockIdx.y + 1], nr = meta[MS * blockIdx.y + 2];
   const double* qrow = Q + (long)(o + r) * ldq + o;
   const int* P = perm + o;
   for (int j = threadIdx.x; j < n; j += blockDim.x) rowsm[j] = qrow[P[j]];
@@ -720,8 +823,8 @@ __global__ void dc_merge_vec_kernel(const MergeDesc* md, const double* Q, double
     }
   }
   __syncthreads();
-  double* ndrow = Qnd + m.off + (long)r * K;
-  for (int k = threadIdx.x; k < K; k += blockDim.x) ndrow[k] = rowsm[ndcol[o + k]];
+  double* ndrow = Qnd + m.off + (long)r * (n + (n & 1));  // static even ld (K ≤ n), 16 B aligned
+  for (int k = threadIdx.x; k < K; k += blockDim.x) ndrow[pidx[o + k]] = rowsm[ndcol[o + k]];
   double* dfrow = Qdf + m.off + (long)r * nd;
   for (int t = threadIdx.x; t < nd; t += blockDim.x) dfrow[t] = rowsm[dcol[o + t]];
 }
@@ -732,19 +835,17 @@ struct RootRef {
 
 // Secular equation 1 + ρ Σ w_i²/(d_i − λ) = 0, one warp per root.
 // Stores λ_j and column j of Δ (Δ_ij = d_i − λ_j, computed from the origin pole).
-__global__ void dc_secular_kernel(const MergeDesc* md, const RootRef* roots, int nroots, const int* meta,
-                                  const double* dlam, const double* wv, const double* rho_arr, double* lam,
-                                  double* Dl, int* err) {
-  const int rid = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  if (rid >= nroots) return;
+__global__ void dc_secular_kernel(const MergeDesc* md, const int* meta, const double* dlam, const double* wv,
+                                  const double* rho_arr, double* lam, double* Dl, int* err) {
   const int lane = threadIdx.x & 31;
-  const RootRef rr = roots[rid];
-  const MergeDesc m = md[rr.merge];
-  const int K = meta[4 * rr.merge];
-  const int j = rr.j;
+  const int mi = blockIdx.y;
+  const MergeDesc m = md[mi];
+  const int K = meta[MS * mi];
+  const int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (j >= K) return;
   const double* dl = dlam + m.o;
   const double* w = wv + m.o;
-  const double rho = rho_arr[rr.merge];
+  const double rho = rho_arr[mi];
   double* delta = Dl + m.off + (long)j * K;
   if (K == 1) {
     if (lane == 0) {
@@ -850,15 +951,13 @@ __global__ void dc_secular_kernel(const MergeDesc* md, const RootRef* roots, int
 }
 
 // Gu–Eisenstat: ŵ_i = sign(w_i) sqrt(−Δ_ii Π_{j≠i} Δ_ij/(d_i − d_j)); warp per i.
-__global__ void dc_what_kernel(const MergeDesc* md, const RootRef* rows, int nrows, const int* meta,
-                               const double* dlam, const double* wv, const double* Dl, double* what) {
-  const int rid = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  if (rid >= nrows) return;
+__global__ void dc_what_kernel(const MergeDesc* md, const int* meta, const double* dlam, const double* wv,
+                               const double* Dl, double* what) {
   const int lane = threadIdx.x & 31;
-  const RootRef rr = rows[rid];
-  const MergeDesc m = md[rr.merge];
-  const int K = meta[4 * rr.merge];
-  const int i = rr.j;
+  const MergeDesc m = md[blockIdx.y];
+  const int K = meta[MS * blockIdx.y];
+  const int i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (i >= K) return;
   const double* dl = dlam + m.o;
   const double* D = Dl + m.off;
   double p = 1.0;
@@ -871,26 +970,28 @@ __global__ void dc_what_kernel(const MergeDesc* md, const RootRef* rows, int nro
   if (lane == 0) what[m.o + i] = copysign(sqrt(fmax(-p, 0.0)), wv[m.o + i]);
 }
 
-// Column j of U: u_i = ŵ_i/Δ_ij normalised (in place over Δ); warp per column.
-__global__ void dc_vec_kernel(const MergeDesc* md, const RootRef* roots, int nroots, const int* meta,
-                              const double* what, double* Dl) {
-  const int rid = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  if (rid >= nroots) return;
+// Column j of U: u_i = ŵ_i/Δ_ij normalised; written to Uw with its rows in the
+// GEMM order π (top-only, mixed, bottom-only columns of Qnd); warp per column.
+__global__ void dc_vec_kernel(const MergeDesc* md, const int* meta, const double* what, const double* Dl,
+                              double* Uw, const int* pidx) {
   const int lane = threadIdx.x & 31;
-  const RootRef rr = roots[rid];
-  const MergeDesc m = md[rr.merge];
-  const int K = meta[4 * rr.merge];
-  double* col = Dl + m.off + (long)rr.j * K;
+  const MergeDesc m = md[blockIdx.y];
+  const int K = meta[MS * blockIdx.y];
+  const int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (j >= K) return;
+  const int nm_ = m.n1 + m.n2;
+  const double* col = Dl + m.off + (long)j * K;
+  double* ucol = Uw + m.off + (long)j * (nm_ + (nm_ & 1));
   const double* wh = what + m.o;
+  const int* pi = pidx + m.o;
   double s = 0.0;
   for (int i = lane; i < K; i += 32) {
     const double u = wh[i] / col[i];
-    col[i] = u;
     s += u * u;
   }
   s = warp_sum(s);
   const double inv = 1.0 / sqrt(s);
-  for (int i = lane; i < K; i += 32) col[i] *= inv;
+  for (int i = lane; i < K; i += 32) ucol[pi[i]] = (wh[i] / col[i]) * inv;
 }
 
 // Merge the ascending roots with the ascending deflated values (parallel
@@ -901,7 +1002,7 @@ __global__ void dc_order_kernel(const MergeDesc* md, const int* meta, const doub
                                 int* colmap) {
   const MergeDesc m = md[blockIdx.x];
   const int o = m.o;
-  const int K = meta[4 * blockIdx.x], nd = meta[4 * blockIdx.x + 1];
+  const int K = meta[MS * blockIdx.x], nd = meta[MS * blockIdx.x + 1];
   const double* L = lam + o;
   const double* F = dfv + o;
   for (int a = threadIdx.x; a < K; a += blockDim.x) {
@@ -920,7 +1021,7 @@ __global__ void dc_copy_deflated_kernel(const MergeDesc* md, const int* meta, co
                                         const int* colmap) {
   const MergeDesc m = md[blockIdx.y];
   const int o = m.o, n = m.n1 + m.n2;
-  const int K = meta[4 * blockIdx.y], nd = meta[4 * blockIdx.y + 1];
+  const int K = meta[MS * blockIdx.y], nd = meta[MS * blockIdx.y + 1];
   const long total = (long)n * nd;
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
     const int r = (int)(e / nd), t = (int)(e % nd);
@@ -932,9 +1033,9 @@ struct EpiColMap {
   static constexpr bool kRowDot = false;
   double* Q;
   long ldq;
-  int o;
+  int o, roff;
   const int* colmap;  // colmap[o + c]
-  __device__ void store(int r, int c, double v) const { Q[(long)(o + r) * ldq + o + colmap[o + c]] = v; }
+  __device__ void store(int r, int c, double v) const { Q[(long)(o + roff + r) * ldq + o + colmap[o + c]] = v; }
   __device__ double rowdot_weight(int, int) const { return 0; }
   __device__ void rowdot_store(int, int, double) const {}
 };
@@ -967,6 +1068,7 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
   int* rot = ib + 3L * n;     // 2n
   int* colmap = ib + 5L * n;  // n
   int* err = ib + 6L * n;     // 1
+  int* pidx = ib + 7L * n;    // n: GEMM column order of the secular columns
   KOT_CUDA(cudaMemsetAsync(w.Q, 0, sizeof(double) * n * n, st));
   KOT_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
   // host-pinned staging regions (distinct per purpose: copies are asynchronous)
@@ -1003,28 +1105,41 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
   ProfScope ps_leaf("dc.leaf", st);
   dc_leaf_kernel<<<ceil_div(nleaves, 4), 128, 0, st>>>(w.d, w.e, dloff, dllen, nleaves, w.Q, n, err);
   KOT_LAUNCH_CHECK();
-  // per-level device descriptors after the packed ints (8-byte aligned)
+  // all levels' merge descriptors uploaded once; each level gets its own meta region, so the
+  // whole merge tree runs without a host round trip (kernels read K from device memory)
   const size_t packed_bytes = ((sizeof(int) * packed.size() + 63) / 64) * 64;
-  MergeDesc* dms = reinterpret_cast<MergeDesc*>(d_desc_base + packed_bytes);
-
+  std::vector<std::vector<MergeDesc>> levels;
   for (int depth = maxdepth; depth >= 0; --depth) {
     std::vector<MergeDesc> ms;
     long off = 0;
     for (auto& nd : nodes)
       if (!nd.leaf && nd.depth == depth) {
         ms.push_back({nd.o, nd.n / 2, nd.n - nd.n / 2, off});
-        off += (long)nd.n * nd.n;
+        off += (long)nd.n * (nd.n + 1);  // room for an even leading dimension
+        off += off & 1;                  // keep every region 16 B aligned
       }
-    if (ms.empty()) continue;
+    if (!ms.empty()) levels.push_back(ms);
+  }
+  size_t ndesc = 0;
+  for (auto& l : levels) ndesc += l.size();
+  MergeDesc* dms_all = reinterpret_cast<MergeDesc*>(d_desc_base + packed_bytes);
+  int* dmeta_all = reinterpret_cast<int*>(dms_all + ndesc);
+  {
+    size_t k = 0;
+    for (auto& l : levels)
+      for (auto& m : l) reinterpret_cast<MergeDesc*>(h_desc)[k++] = m;
+    KOT_CUDA(cudaMemcpyAsync(dms_all, h_desc, sizeof(MergeDesc) * ndesc, cudaMemcpyHostToDevice, st));
+  }
+  size_t base = 0;
+  for (auto& ms : levels) {
     const int nm = (int)ms.size();
+    MergeDesc* dms = dms_all + base;
+    int* dmeta = dmeta_all + MS * base;
+    base += nm;
     int maxm = 0;
     for (auto& mm : ms) maxm = std::max(maxm, mm.n1 + mm.n2);
-    int* dmeta = reinterpret_cast<int*>(dms + nm);
-    RootRef* droots = reinterpret_cast<RootRef*>(dmeta + 4 * nm);
-    memcpy(h_desc, ms.data(), sizeof(MergeDesc) * nm);
-    KOT_CUDA(cudaMemcpyAsync(dms, h_desc, sizeof(MergeDesc) * nm, cudaMemcpyHostToDevice, st));
-    ProfScope ps_prep("dc.prep", st);
     {
+      ProfScope ps_prep("dc.prep", st);
       const size_t smem = (size_t)maxm * (3 * sizeof(double) + sizeof(int));
       static size_t prep_attr = 0;
       if (smem > 48 * 1024 && smem > prep_attr) {
@@ -1032,41 +1147,30 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
         prep_attr = smem;
       }
       dc_merge_prep_kernel<<<nm, DC_PREP_THREADS, smem, st>>>(dms, w.Q, n, w.d, w.e, w.zs, w.ds, w.dlam, w.wv,
-                                                              w.dfv, w.rotcs, w.rho, perm, ndcol, dcol, rot, dmeta);
+                                                              w.dfv, w.rotcs, w.rho, perm, ndcol, dcol, rot, dmeta,
+                                                              pidx);
+      KOT_LAUNCH_CHECK();
     }
-    KOT_LAUNCH_CHECK();
-    std::vector<int> meta(4 * nm);
-    KOT_CUDA(cudaMemcpyAsync(meta.data(), dmeta, sizeof(int) * 4 * nm, cudaMemcpyDeviceToHost, st));
-    KOT_CUDA(cudaStreamSynchronize(st));
-    int maxn = 0;
-    std::vector<RootRef> roots;
-    for (int i = 0; i < nm; ++i) {
-      maxn = std::max(maxn, ms[i].n1 + ms[i].n2);
-      for (int j = 0; j < meta[4 * i]; ++j) roots.push_back({i, j});
-    }
-    ProfScope ps_vec("dc.gather_rot", st);
     {
-      const size_t smem = (size_t)maxn * sizeof(double);
+      ProfScope ps_vec("dc.gather_rot", st);
+      const size_t smem = (size_t)maxm * sizeof(double);
       static size_t vec_attr = 0;
       if (smem > 48 * 1024 && smem > vec_attr) {
         KOT_CUDA(cudaFuncSetAttribute(dc_merge_vec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         vec_attr = smem;
       }
-      dc_merge_vec_kernel<<<dim3(maxn, nm), 256, smem, st>>>(dms, w.Q, w.Qw, w.Qnd, n, perm, ndcol, dcol, rot,
-                                                             w.rotcs, dmeta);
+      dc_merge_vec_kernel<<<dim3(maxm, nm), 256, smem, st>>>(dms, w.Q, w.Qw, w.Qnd, n, perm, ndcol, dcol, rot,
+                                                             w.rotcs, dmeta, pidx);
+      KOT_LAUNCH_CHECK();
     }
-    KOT_LAUNCH_CHECK();
-    const int nr = (int)roots.size();
-    if (nr > 0) {
-      memcpy(h_roots, roots.data(), sizeof(RootRef) * nr);
-      KOT_CUDA(cudaMemcpyAsync(droots, h_roots, sizeof(RootRef) * nr, cudaMemcpyHostToDevice, st));
+    {
       ProfScope ps_sec("dc.secular", st);
-      dc_secular_kernel<<<ceil_div(nr, 8), 256, 0, st>>>(dms, droots, nr, dmeta, w.dlam, w.wv, w.rho, w.lam, w.Dl,
-                                                          err);
+      const dim3 grid(ceil_div(maxm, 8), nm);
+      dc_secular_kernel<<<grid, 256, 0, st>>>(dms, dmeta, w.dlam, w.wv, w.rho, w.lam, w.Dl, err);
       KOT_LAUNCH_CHECK();
-      dc_what_kernel<<<ceil_div(nr, 8), 256, 0, st>>>(dms, droots, nr, dmeta, w.dlam, w.wv, w.Dl, w.what);
+      dc_what_kernel<<<grid, 256, 0, st>>>(dms, dmeta, w.dlam, w.wv, w.Dl, w.what);
       KOT_LAUNCH_CHECK();
-      dc_vec_kernel<<<ceil_div(nr, 8), 256, 0, st>>>(dms, droots, nr, dmeta, w.what, w.Dl);
+      dc_vec_kernel<<<grid, 256, 0, st>>>(dms, dmeta, w.what, w.Dl, w.Uw, pidx);
       KOT_LAUNCH_CHECK();
     }
     ProfScope ps_ord("dc.order_gemm", st);
@@ -1075,12 +1179,27 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
     dc_copy_deflated_kernel<<<dim3(64, nm), 256, 0, st>>>(dms, dmeta, w.Qw, w.Q, n, colmap);
     KOT_LAUNCH_CHECK();
     for (int i = 0; i < nm; ++i) {
-      const int K = meta[4 * i];
-      if (K == 0) continue;
-      const int nn = ms[i].n1 + ms[i].n2;
-      GemmShape s = make_shape(nn, K, K, w.Qnd + ms[i].off, K, w.Dl + ms[i].off, K);
-      EpiColMap epi{w.Q, n, ms[i].o, colmap};
-      gemm_launch<false, true>(s, epi, st);
+      // Q_new = Qnd·U with Qnd's columns ordered (top-only | mixed | bottom-only): the top rows only
+      // see the first c12 columns, the bottom rows only the last K − c1 (dlaed3 structure).  K, c1,
+      // c12 are read on the device; the grids are sized for K ≤ n_m.
+      const int n1 = ms[i].n1, n2 = ms[i].n2, nn = n1 + n2;
+      const int ld = nn + (nn & 1);
+      const double* Qnd = w.Qnd + ms[i].off;
+      const double* U = w.Uw + ms[i].off;
+      const int* mt = dmeta + MS * i;
+      {
+        GemmShape s = make_shape(n1, nn, nn, Qnd, ld, U, ld);
+        s.dN = mt;       // K
+        s.dK = mt + 4;   // c12
+        gemm_launch<false, true>(s, EpiColMap{w.Q, n, ms[i].o, 0, colmap}, st);
+      }
+      {  // the top-only columns are exact zeros in the bottom rows, so an aligned K start is harmless
+        GemmShape s = make_shape(n2, nn, nn, Qnd + (long)n1 * ld, ld, U, ld);
+        s.dN = mt;
+        s.dK = mt;       // K
+        s.dKstart = mt + 3;  // c1
+        gemm_launch<false, true>(s, EpiColMap{w.Q, n, ms[i].o, n1, colmap}, st);
+      }
     }
   }
   int herr = 0;

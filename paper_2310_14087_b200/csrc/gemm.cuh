@@ -48,6 +48,12 @@ struct GemmShape {
   //   k_begin = max(kb_m ? m0 : 0, kb_n ? n0 : 0)
   //   k_end   = min(K, ke_m ? m0+BM : K, ke_n ? n0+BN : K)
   int kb_m, kb_n, ke_m, ke_n;
+  int kstart;     // K range starts at max(..., kstart), rounded down to the k-tile
+  // device-side overrides (nullable), read at kernel start: the grid is sized for the static
+  // N/K (upper bounds) and tiles beyond the actual size exit (no host round trip needed)
+  const int* dN;
+  const int* dK;
+  const int* dKstart;
   int sym_tiles;  // enumerate only tiles with tm <= tn (symmetric outputs)
   // split-K: grid.y = ksplit partial products written to ws[split][M][N] (ld N),
   // then reduced in fixed order by splitk_reduce_kernel (deterministic).
@@ -104,6 +110,10 @@ __device__ __forceinline__ void load_tile(double* sm, int pad, const double* g, 
 template <bool TA, bool TB, int VEC, class Epi>
 __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi epi) {
   extern __shared__ __align__(16) double gsm[];
+  const int tiles_n_grid = (s.N + GB_N - 1) / GB_N;  // grid layout uses the static bound
+  if (s.dN) s.N = *s.dN;
+  if (s.dK) s.K = *s.dK;
+  if (s.dKstart) s.kstart = *s.dKstart;
   double* As = gsm;
   double* Bs = gsm + G_STAGES * G_ATILE;
   double* Ks = gsm + G_STAGES * (G_ATILE + G_BTILE);
@@ -114,8 +124,8 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
   if (s.sym_tiles) {
     int t = blockIdx.x;
     tm = 0;
-    while (t >= tiles_n - tm) {
-      t -= tiles_n - tm;
+    while (t >= tiles_n_grid - tm) {
+      t -= tiles_n_grid - tm;
       ++tm;
     }
     tn = tm + t;
@@ -129,6 +139,7 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
   int kbeg = 0, kend = s.K;
   if (s.kb_m) kbeg = max(kbeg, m0);
   if (s.kb_n) kbeg = max(kbeg, n0);
+  kbeg = max(kbeg, s.kstart);
   if (s.ke_m) kend = min(kend, m0 + GB_M);
   if (s.ke_n) kend = min(kend, n0 + GB_N);
   kbeg = (kbeg / GB_K) * GB_K;
@@ -297,6 +308,7 @@ inline double gemm_alg_flops(const GemmShape& s) {
       int kb = 0, ke = s.K;
       if (s.kb_m) kb = std::max(kb, m0);
       if (s.kb_n) kb = std::max(kb, n0);
+      kb = std::max(kb, s.kstart);
       if (s.ke_m) ke = std::min(ke, m0 + GB_M);
       if (s.ke_n) ke = std::min(ke, n0 + GB_N);
       if (ke > kb) f += 2.0 * std::min(GB_M, s.M - m0) * std::min(GB_N, s.N - n0) * (double)(ke - kb);
@@ -360,6 +372,7 @@ inline GemmShape make_shape(int M, int N, int K, const double* A, long lda, cons
   s.ldb = ldb;
   s.ksplit = 1;
   s.ws = nullptr;
+  s.dN = s.dK = s.dKstart = nullptr;
   return s;
 }
 

@@ -24,7 +24,7 @@ struct EigWork {
   int n;
   double *A = nullptr, *Vall = nullptr, *X = nullptr, *d = nullptr, *e = nullptr, *tau = nullptr;
   double *xv = nullptr, *yv = nullptr, *part = nullptr, *partn = nullptr, *Tf = nullptr, *W1 = nullptr;
-  double *Q = nullptr, *Qw = nullptr, *Qnd = nullptr, *Dl = nullptr;
+  double *Q = nullptr, *Qw = nullptr, *Qnd = nullptr, *Dl = nullptr, *Uw = nullptr;
   double *zs = nullptr, *ds = nullptr, *dlam = nullptr, *wv = nullptr, *what = nullptr, *lam = nullptr;
   double *dfv = nullptr, *rotcs = nullptr, *rho = nullptr, *splitws = nullptr, *gpart = nullptr;
   int* gcnt = nullptr;
