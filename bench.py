@@ -39,6 +39,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 DMMA_PEAK_TFLOPS = 37.12  # measured, profiles/r01/fp64_peak_microbench.txt (mma.sync m8n8k4 f64)
+SYTRD_TRAFFIC_BYTES = 14.866176e6 + 8.448e3  # ncu --set full, profiles/r01/ncu_full_r01_summary.txt
 
 
 def peaks():
@@ -299,26 +300,30 @@ def run_gpu(args):
         return 0
 
     # ---------------- roofline of the dominant kernel
+    # Dominant by serialized kernel time (ncu launch list, profiles/): the cooperative Householder
+    # panel kernel of the eigensolver.  The live CUDA-event timing below is per launch on the stream
+    # it runs on; the GEMM core is reported as a secondary roofline.
     hbm, peak_kind = peaks()
-    kern = {k: v for k, v in prof.items() if k in ("sytrd_panel", "gemm_dmma")}
-    dom = max(kern, key=lambda k: kern[k]["ms"]) if kern else None
-    roof = None
-    if dom == "sytrd_panel":
-        e = kern[dom]
+    roof = roof_gemm = None
+    if "sytrd_panel" in prof:
+        e = prof["sytrd_panel"]
         ach = e["bytes"] / e["calls"] / (e["ms"] / e["calls"] * 1e-3) / 1e9
         roof = {"kernel": "sytrd_panel_kernel (cooperative Householder panel: column update + symv)",
                 "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "traffic": SYTRD_TRAFFIC_BYTES, "traffic_note": "ncu --set full, one mid panel launch at l=2000 "
+                "(dram read+write; the trailing matrix is L2-resident)",
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                 "algorithmic": "per launch: sum over its 32 columns of one lower-triangle read of the "
                                "trailing matrix, 8*m(m+1)/2 B",
-                "share_of_step": e["ms"] / ms, "avg_launch_ms": e["ms"] / e["calls"]}
-    elif dom == "gemm_dmma":
-        e = kern[dom]
+                "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"],
+                "note": "latency-bound: 2 grid barriers + ~4 dependent L2 round trips per column"}
+    if "gemm_dmma" in prof:
+        e = prof["gemm_dmma"]
         ach = e["flops"] / (e["ms"] * 1e-3) / 1e12
-        roof = {"kernel": "gemm_dmma_kernel (mma.sync m8n8k4 f64, all shapes)", "bound": "tensor",
-                "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
-                "traffic": None, "peak_source": "measured DMMA microbenchmark (MEASURED_PEAKS.json has no FP64)",
-                "share_of_step": e["ms"] / ms, "avg_launch_ms": e["ms"] / e["calls"]}
+        roof_gemm = {"kernel": "gemm_dmma_kernel (mma.sync m8n8k4 f64, all shapes)", "bound": "tensor",
+                     "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
+                     "traffic": None, "peak_source": "measured DMMA microbenchmark (MEASURED_PEAKS.json has no FP64)",
+                     "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"]}
     phases = {k: {"ms_per_step": v["ms"] / max(done, 1), "calls_per_step": v["calls"] / max(done, 1),
                   **({"tflops": v["flops"] / (v["ms"] * 1e-3) / 1e12} if v["flops"] and v["ms"] else {})}
               for k, v in prof.items()}
@@ -342,6 +347,7 @@ def run_gpu(args):
                 "iterations": rep.iterations},
         "gpu_launches": int(launches),
         "roofline": roof,
+        "roofline_gemm": roof_gemm,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
         "phases": phases,
