@@ -121,6 +121,22 @@ void kot_session_end(kot_session* s);
 /* the cudaStream_t (as void*) every kernel of this problem is launched on */
 void* kot_problem_stream(kot_problem* p);
 
+/* ---- row sharding of the CG matvec over NCCL (BASELINE config 4) ----------
+ * Replaces nothing in the reference (kot is single-process); the sharded solve
+ * is the same kot.solver.solve (solver.py:114) with its structure-reduced
+ * middle operator (newton.py:70-95) split by rows of B = R·P across `world`
+ * processes, one GPU each.  Every rank calls the same entry points on the same
+ * problem; results are identical on all ranks.
+ *   kot_nccl_unique_id: rank 0 creates the 128-byte ncclUniqueId, the caller
+ *                       broadcasts it (torch.distributed / MPI / files).
+ *   kot_problem_shard:  collective over `world` ranks; world <= 1 unshards.
+ *                       id128 == NULL with world > 1 is a single-device test hook:
+ *                       every row block is computed in turn, no communication.
+ * NCCL (libnccl.so.2) is dlopen'ed on first use. */
+int kot_nccl_unique_id(char* out128);
+int kot_problem_shard(kot_problem* p, const char* id128, int rank, int world);
+int kot_problem_shard_info(const kot_problem* p, int* rank, int* world, int* row0, int* row1);
+
 /* ---- phase profiler (CUDA events around library phases; off by default) --- */
 typedef struct {
   char name[32];

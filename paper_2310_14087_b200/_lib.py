@@ -72,6 +72,9 @@ _SIGS = {
     "kot_session_result": (C.c_int, [C.c_void_p, dptr, dptr, C.POINTER(ReportC)]),
     "kot_session_end": (None, [C.c_void_p]),
     "kot_problem_stream": (C.c_void_p, [C.c_void_p]),
+    "kot_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "kot_problem_shard": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_int]),
+    "kot_problem_shard_info": (C.c_int, [C.c_void_p, iptr, iptr, iptr, iptr]),
     "kot_profile_enable": (C.c_int, [C.c_int]),
     "kot_profile_read": (C.c_int, [C.POINTER(ProfEntryC), C.c_int]),
     "kot_gram": (C.c_int, [dptr, C.c_int, C.c_int, C.c_double, C.c_int, dptr]),

@@ -215,6 +215,31 @@ void kot_session_end(kot_session* s) {
 
 void* kot_problem_stream(kot_problem* h) { return (void*)h->p->st; }
 
+int kot_nccl_unique_id(char* out128) {
+  return guarded([&] { kot::nccl_unique_id(out128); });
+}
+
+int kot_problem_shard(kot_problem* h, const char* id128, int rank, int world) {
+  return guarded([&] {
+    if (world <= 1)
+      kot::problem_unshard(*h->p);
+    else if (id128 == nullptr)
+      kot::problem_shard_emulate(*h->p, world);
+    else
+      kot::problem_shard(*h->p, id128, rank, world);
+  });
+}
+
+int kot_problem_shard_info(const kot_problem* h, int* rank, int* world, int* row0, int* row1) {
+  return guarded([&] {
+    const kot::Problem& p = *h->p;
+    if (rank) *rank = p.shard_rank;
+    if (world) *world = p.shard_world;
+    if (row0) *row0 = p.shard_world > 1 ? p.row0 : 0;
+    if (row1) *row1 = p.shard_world > 1 ? p.row1 : p.n;
+  });
+}
+
 // ------------------------------------------------------------ operators
 
 namespace {

@@ -52,6 +52,12 @@ void Problem::init_scratch() {
 
 Problem::~Problem() {
   if (st) cudaStreamSynchronize(st);
+  if (nccl_comm) {
+    try {
+      problem_unshard(*this);
+    } catch (...) {
+    }
+  }
   aux_.reset();
   aux2_.reset();
   eig.reset();
@@ -79,6 +85,7 @@ static std::unique_ptr<Problem> make_problem(int n, int device) {
   p->R = p->alloc(nn);
   p->embed = p->alloc(n);
   p->init_scratch();
+  p->row1 = n;
   return p;
 }
 
@@ -257,12 +264,13 @@ void jac_bottom(Problem& p, long count, const double* a, const double* b, double
 
 struct FinArgs {
   int n, mode, tiles, tri;
+  int r0, r1;  // rows computed (row sharding); default [0, n)
   const double* Q;
   const double* G2;  // nullable: + (G2·u)/μ  (structure-reduced NONPOS matvec)
   const double* u;
   const double* partial;
   const double* z;
-  const double* r1;
+  const double* r1v;
   double l2, mu, phsign;
   double* out;
 };
@@ -271,7 +279,7 @@ struct FinArgs {
 __global__ void finalize_kernel(FinArgs f) {
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
-  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < f.n; r += gridDim.x * warps) {
+  for (int r = f.r0 + blockIdx.x * warps + (threadIdx.x >> 5); r < f.r1; r += gridDim.x * warps) {
     double qv = 0.0, ph = 0.0, gv = 0.0;
     if (f.Q) {
       const double* qr = f.Q + (long)r * f.n;
@@ -298,9 +306,9 @@ __global__ void finalize_kernel(FinArgs f) {
         o = __dadd_rn(__dadd_rn(qv / two_l2, __dmul_rn(f.mu, f.u[r])), mid);
         break;
       }
-      case FIN_A1: o = __dsub_rn(-f.r1[r], ph / (f.mu + 1.0)); break;
+      case FIN_A1: o = __dsub_rn(-f.r1v[r], ph / (f.mu + 1.0)); break;
       case FIN_JTOP:
-        o = __dadd_rn(__dsub_rn(__dadd_rn(qv / two_l2, __dmul_rn(f.mu, f.u[r])), ph), f.r1[r]);
+        o = __dadd_rn(__dsub_rn(__dadd_rn(qv / two_l2, __dmul_rn(f.mu, f.u[r])), ph), f.r1v[r]);
         break;
       case FIN_PHI: o = ph; break;
       case FIN_GRAD: o = __dsub_rn(qv, f.z[r]) / two_l2; break;
@@ -317,6 +325,8 @@ void finalize(Problem& p, int mode, const double* u, bool with_phi, const double
   f.mode = mode;
   f.tiles = ceil_div(p.n, GB_N);
   f.tri = 1;
+  f.r0 = 0;
+  f.r1 = p.n;
   f.G2 = nullptr;
   f.phsign = 1.0;
   const bool need_q = (mode == FIN_RES || mode == FIN_MATVEC || mode == FIN_JTOP || mode == FIN_GRAD || mode == FIN_QV);
@@ -324,7 +334,7 @@ void finalize(Problem& p, int mode, const double* u, bool with_phi, const double
   f.u = u;
   f.partial = with_phi ? p.partial : nullptr;
   f.z = p.z;
-  f.r1 = r1;
+  f.r1v = r1;
   f.l2 = p.l2;
   f.mu = mu;
   f.out = out;
@@ -390,6 +400,21 @@ struct EpiSquareMirror {
   __device__ void rowdot_store(int, int, double) const {}
 };
 
+// Row blocks of B this process computes: its own block under NCCL sharding, every
+// block in turn under the single-device emulation hook (emul_world > 1), else [0, n).
+static std::vector<std::pair<int, int>> row_blocks(const Problem& p) {
+  std::vector<std::pair<int, int>> v;
+  if (p.nccl_comm) {
+    v.emplace_back(p.row0, p.row1);
+  } else if (p.emul_world > 1) {
+    const int blk = (p.n + p.emul_world - 1) / p.emul_world;
+    for (int g = 0; g < p.emul_world; ++g) v.emplace_back(std::min(p.n, g * blk), std::min(p.n, (g + 1) * blk));
+  } else {
+    v.emplace_back(0, p.n);
+  }
+  return v;
+}
+
 void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m) {
   const int n = p.n;
   Bufs& b = p.bufs();
@@ -403,10 +428,13 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m) {
   if (direct) return;
   m.pos = dc.k <= n - dc.k;
   m.B = b.Bm;
-  {  // B = R P   (R upper triangular: K range starts at the row tile)
-    GemmShape s = make_shape(n, n, n, p.R, n, dc.P, n);
-    s.kb_m = 1;
-    gemm_launch<false, false>(s, EpiAxpby{b.Bm, n, 1.0, 0.0}, p.st);
+  for (const auto& [r0, r1] : row_blocks(p)) {  // B = R P for the row blocks this process owns
+    if (r1 > r0) {  // R upper triangular: the K range starts at the block's first row
+      GemmShape s = make_shape(r1 - r0, n, n, p.R + (long)r0 * n, n, dc.P, n);
+      s.kb_m = 1;
+      s.kstart = r0;
+      gemm_launch<false, false>(s, EpiAxpby{b.Bm + (long)r0 * n, n, 1.0, 0.0}, p.st);
+    }
   }
   if (!m.pos && p.G2 == nullptr) {
     p.G2 = p.alloc((long)n * n);
@@ -421,21 +449,33 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m) {
 void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* out) {
   const int n = p.n, k = m.dc.k;
   const int ks = m.pos ? k : n - k;
-  const double nn = n;
-  ProfScope ps("matvec", p.st, 4.0 * ks * nn * nn + 2.0 * nn * nn);
+  const bool nccl = p.nccl_comm != nullptr;
+  const auto blocks = row_blocks(p);
+  const double nn = n, own = nccl ? p.row1 - p.row0 : n;
+  ProfScope ps("matvec", p.st, 4.0 * ks * nn * own + 2.0 * nn * own);
   Bufs& b = p.bufs();
+  const double* Bsub = m.pos ? m.B : m.B + k;
   if (ks > 0) {
-    const double* Bsub = m.pos ? m.B : m.B + k;
-    {  // C = B_subᵀ diag(v) B, coefficients in the epilogue → T̃ (ks × n)
-      GemmShape s = make_shape(ks, n, n, Bsub, n, m.B, n);
-      s.kscale = v;
+    // C = B_subᵀ diag(v) B summed over row blocks, coefficients in the epilogue → T̃ (ks × n).
+    // W∘ is linear in C, so the coefficient-scaled block partials simply add.
+    bool first = true;
+    for (const auto& [r0, r1] : blocks) {
+      if (r1 <= r0) continue;
+      double* dst = first ? b.Ct : p.shard_tmp;
+      GemmShape s = make_shape(ks, n, r1 - r0, Bsub + (long)r0 * n, n, m.B + (long)r0 * n, n);
+      s.kscale = v + r0;
       s.ws = p.splitws;
       s.ksplit = choose_ksplit(s, p.splitws_cap);
-      gemm_launch<true, false>(s, EpiMvCoef{b.Ct, n, m.dc.vals, k, m.pos ? 1 : 0, m.mu}, p.st);
+      gemm_launch<true, false>(s, EpiMvCoef{dst, n, m.dc.vals, k, m.pos ? 1 : 0, m.mu}, p.st);
+      if (!first) axpby(p, (long)ks * n, 1.0, b.Ct, 1.0, p.shard_tmp, b.Ct);
+      first = false;
     }
-    {  // y_i = Σ_a (B T̃ᵀ)_ia B_sub[i][a]
-      GemmShape s = make_shape(n, ks, n, m.B, n, b.Ct, n);
-      gemm_launch<false, true>(s, EpiRowDot{Bsub, n, p.partial, n}, p.st);
+    if (first) KOT_CUDA(cudaMemsetAsync(b.Ct, 0, sizeof(double) * ks * n, p.st));
+    if (nccl) shard_allreduce_sum(p, b.Ct, (long)ks * n);  // Σ over ranks
+    for (const auto& [r0, r1] : blocks) {  // y_i = Σ_a (B T̃ᵀ)_ia B_sub[i][a] for the block's rows
+      if (r1 <= r0) continue;
+      GemmShape s = make_shape(r1 - r0, ks, n, m.B + (long)r0 * n, n, b.Ct, n);
+      gemm_launch<false, true>(s, EpiRowDot{Bsub + (long)r0 * n, n, p.partial + r0, n}, p.st);
     }
   }
   FinArgs f;
@@ -448,13 +488,21 @@ void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* o
   f.u = v;
   f.partial = ks > 0 ? p.partial : nullptr;
   f.z = p.z;
-  f.r1 = nullptr;
+  f.r1v = nullptr;
   f.l2 = p.l2;
   f.mu = m.mu;
   f.phsign = 1.0;
-  f.out = out;
-  finalize_kernel<<<std::min(ceil_div(n, 8), 8 * kNumSMs), 256, 0, p.st>>>(f);
-  KOT_LAUNCH_CHECK();
+  f.out = nccl ? p.ygather : out;  // r0 = rank·block: own rows land at ygather[r0 …]
+  f.r0 = blocks.front().first;
+  f.r1 = blocks.back().second;
+  if (f.r1 > f.r0) {
+    finalize_kernel<<<std::min(ceil_div(f.r1 - f.r0, 8), 8 * kNumSMs), 256, 0, p.st>>>(f);
+    KOT_LAUNCH_CHECK();
+  }
+  if (nccl) {
+    shard_allgather(p, p.ygather, p.shard_block);
+    KOT_CUDA(cudaMemcpyAsync(out, p.ygather, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
+  }
 }
 
 // Φ(X) row-dot partials: tile (tm, tn>=tm) of R·X contracted against R.

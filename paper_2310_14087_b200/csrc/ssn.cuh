@@ -69,6 +69,12 @@ struct Problem {
   Bufs& bufs();
   // second execution context (own stream + scratch, shared instance data) on
   // which the EG safeguard chain runs concurrently with the Newton chain
+  // row sharding of the CG matvec (config 4): NCCL communicator and this rank's row block
+  void* nccl_comm = nullptr;
+  int shard_rank = 0, shard_world = 1, shard_block = 0, row0 = 0, row1 = -1;
+  double* ygather = nullptr;  // shard_block·world doubles
+  int emul_world = 1;          // test hook: all row blocks in turn on one device, no NCCL
+  double* shard_tmp = nullptr;  // (⌊ℓ/2⌋+1)·ℓ block partial of T̃ (emulation only)
   std::unique_ptr<Problem> aux_, aux2_;
   Problem& aux();
   Problem& aux2();
@@ -103,6 +109,13 @@ struct MvCtx {
   double* B = nullptr;
 };
 void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m);
+// shard.cu
+void nccl_unique_id(char* out128);
+void problem_shard(Problem& p, const char* id128, int rank, int world);
+void problem_unshard(Problem& p);
+void problem_shard_emulate(Problem& p, int world);
+void shard_allreduce_sum(Problem& p, double* buf, long count);
+void shard_allgather(Problem& p, double* buf, long block);
 void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* out);
 
 struct NewtonOut {

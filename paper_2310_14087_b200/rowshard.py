@@ -1,0 +1,69 @@
+"""Row sharding of the Newton-CG matvec across GPUs (BASELINE config 4, ℓ = 8192).
+
+SURVEY.md §8(e).  The reference's middle operator (newton.py:70-95,
+psdcone.py:113-121) applied through B = R·P is a sum over the rows i of B:
+
+    T̃ = W∘(B_αᵀ diag(v) B) = Σ_g W∘(B_{g,α}ᵀ diag(v_g) B_g)
+    y_i = Σ_a (B T̃ᵀ)_ia B_ia
+
+so rank g keeps the row block [g·⌈ℓ/N⌉, (g+1)·⌈ℓ/N⌉) of B, computes its
+partial T̃ (one DMMA GEMM), the partials are summed with one NCCL all-reduce
+(k·ℓ doubles) and each rank forms its own y rows, all-gathered (ℓ doubles).
+Everything else (eigensolve, Φ, EG, CG vectors) stays replicated, so every
+rank takes identical control decisions and returns identical results.
+
+The NCCL communicator is created by the library itself from an ncclUniqueId
+that rank 0 draws and ``torch.distributed`` broadcasts (any process group,
+gloo or nccl, can carry the 128 bytes).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+from . import _lib
+
+
+def row_block(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows [r0, r1) owned by ``rank`` (shard.cu:problem_shard)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("invalid rank/world")
+    block = -(-n // world)
+    r0 = min(n, rank * block)
+    return r0, min(n, r0 + block)
+
+
+def unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _lib.check(_lib.lib().kot_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_rows(pd, group=None, device: int | None = None) -> tuple[int, int]:
+    """Collective: split ``pd``'s CG matvec over the ranks of ``group`` (torch.distributed).
+
+    Returns this rank's row block.  With a world of one this is a no-op."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dp = pd.device_problem(device)
+    if world == 1:
+        _lib.check(_lib.lib().kot_problem_shard(dp.handle, None, 0, 1))
+        return 0, pd.n
+    obj = [unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    _lib.check(_lib.lib().kot_problem_shard(dp.handle, obj[0], rank, world))
+    return shard_info(pd)[2:]
+
+
+def shard_info(pd) -> tuple[int, int, int, int]:
+    """(rank, world, r0, r1) of the device problem."""
+    v = [C.c_int() for _ in range(4)]
+    _lib.check(_lib.lib().kot_problem_shard_info(pd.device_problem().handle, *[C.byref(x) for x in v]))
+    return tuple(x.value for x in v)
+
+
+def emulate_shards(pd, world: int) -> None:
+    """Single-device test hook: compute the ``world`` row blocks in turn (no NCCL)."""
+    _lib.check(_lib.lib().kot_problem_shard(pd.device_problem().handle, None, 0, int(world)))

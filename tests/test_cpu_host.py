@@ -241,3 +241,60 @@ def test_multiprocess_gather_gloo():
     for seed, it, gam in got:
         ref = fake_result(seed)
         assert it == ref.iterations and np.array_equal(gam, ref.gamma_hat)
+
+
+# ------------------------------------------------------ row sharding (config 4)
+
+def test_row_blocks_partition():
+    from paper_2310_14087_b200.rowshard import row_block
+    for n in (1, 7, 64, 8192, 8191):
+        for world in (1, 2, 3, 8):
+            blocks = [row_block(n, r, world) for r in range(world)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == n
+            for (a0, a1), (b0, b1) in zip(blocks, blocks[1:]):
+                assert a1 == b0 and a0 <= a1
+            block = -(-n // world)
+            assert all(r0 == min(n, g * block) for g, (r0, _) in enumerate(blocks))  # allgather layout
+    with pytest.raises(ValueError):
+        row_block(5, 2, 2)
+
+
+@pytest.mark.parametrize("n_pos", [2, 9])
+def test_row_block_decomposition_of_middle_operator(n_pos):
+    """NumPy restatement of what each rank computes (shard.cu / ssn.cu middle_operator_fast):
+    per-block coefficient-scaled partial T̃_g, summed (the all-reduce), then per-block rows of y
+    (the all-gather) — equals the oracle's Φ∘𝒯∘Φ* middle operator."""
+    from conftest import symmetric_with_signs
+    from paper_2310_14087_b200.rowshard import row_block
+    rng = np.random.default_rng(n_pos)
+    n = 11
+    a = rng.standard_normal((n, n))
+    r = np.triu(a) + 3 * np.eye(n)
+    q = a @ a.T + np.eye(n)
+    po = O.Problem(q=q, z=rng.standard_normal(n), q_sq=1.0, r=r, l1=0.5, l2=0.4, embed=None)
+    dc = O.sym_eig(symmetric_with_signs(rng, n, n_pos))
+    mu = 0.3
+    op = O.eliminator(dc, O.cross_coeffs(dc), mu)
+    v = rng.standard_normal(n)
+    ref = O.middle_operator(po, op, mu)(v) - (q @ v) / (2 * 0.4) - mu * v
+    vals, p = dc.vals, dc.vecs
+    k = int(np.sum(vals > 0))
+    b = r @ p
+    # coefficient matrix W in the eigenbasis (psdcone.py:113-121)
+    w = np.zeros((n, n))
+    for i in range(n):
+        for j in range(n):
+            if i < k and j < k:
+                w[i, j] = 1.0 / mu
+            elif (i < k) != (j < k):
+                a_, b_ = (i, j) if i < k else (j, i)
+                eta = vals[a_] / (vals[a_] - vals[b_])
+                w[i, j] = eta / (mu + 1.0 - eta)
+    for world in (1, 2, 4):
+        t = sum(w * (b[r0:r1].T @ np.diag(v[r0:r1]) @ b[r0:r1])
+                for r0, r1 in (row_block(n, g, world) for g in range(world)))
+        y = np.empty(n)
+        for g in range(world):
+            r0, r1 = row_block(n, g, world)
+            y[r0:r1] = np.einsum("ia,ab,ib->i", b[r0:r1], t, b[r0:r1])
+        assert np.allclose(y, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())

@@ -429,3 +429,71 @@ def test_evaluate_map(cfg1):
     assert rel(t, cfg1["map_t"]) <= 1e-12
     u1, t1 = GP.potential_and_map(pd, K.SampleSet(cfg1["xs"]), cfg1["tight_gamma"], cfg1["map_queries"][0])
     assert u1 == pytest.approx(float(cfg1["map_u"][0]), rel=1e-12)
+
+
+# ------------------------------------------------ row-sharded CG matvec (config 4)
+
+@pytest.mark.parametrize("world", [2, 3, 7])
+@pytest.mark.parametrize("shift", [-5.0, 5.0])
+def test_row_sharded_middle_operator(cfg1, world, shift):
+    """The row-block decomposition of the structure-reduced matvec (rowshard.py), every block
+    computed in turn on one device (the single-GPU hook of kot_problem_shard), vs the oracle, for
+    the POS and NONPOS branches and block sizes that do not align with the GEMM tiles."""
+    from paper_2310_14087_b200 import rowshard
+    pd = gpu_pd(cfg1)
+    po = oracle_pd(cfg1)
+    rowshard.emulate_shards(pd, world)
+    rng = np.random.default_rng(11)
+    x = cfg1["op_x"] + shift * np.eye(pd.n) * np.abs(np.diag(cfg1["op_x"])).mean()
+    g = cfg1["op_g"]
+    v = rng.standard_normal(pd.n)
+    out, mu = GN.middle_operator_at(pd, GP.IteratePair(g, x), 0.7, v)
+    r, dc = O.residual_parts(po, O.Pair(g, x))
+    ctx = O.newton_context(dc, r.norm(), 0.7)
+    ref = O.middle_operator(po, ctx.op, ctx.mu)(v)
+    assert rel(out, ref) <= 1e-11, (world, dc.k, rel(out, ref))
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_row_sharded_matches_unsharded_large(world):
+    """ℓ = 700 (several 64-row tiles per block, ragged last block): sharded = unsharded to 1e-12."""
+    from paper_2310_14087_b200 import configs, rowshard
+    wl = configs.config3(n=700)
+    sx, sy, sxy = K.build_kernel_specs(wl.d, wl.bandwidth_sq)
+    pd = K.assemble(K.SampleSet(wl.xs), K.SampleSet(wl.ys), K.FillingPoints(wl.xt, wl.yt), wl.lambda1,
+                    wl.lambda2, sx, sy, sxy)
+    rng = np.random.default_rng(3)
+    for shift in (-0.2, 0.2):
+        x = random_symmetric(rng, pd.n, 1.0 / pd.n) + shift * np.eye(pd.n) / pd.n
+        w = GP.IteratePair(rng.standard_normal(pd.n) * 1e-2, x)
+        v = rng.standard_normal(pd.n)
+        rowshard.emulate_shards(pd, 1)
+        ref, _ = GN.middle_operator_at(pd, w, 0.3, v)
+        rowshard.emulate_shards(pd, world)
+        out, _ = GN.middle_operator_at(pd, w, 0.3, v)
+        assert rel(out, ref) <= 1e-12, (world, shift, rel(out, ref))
+
+
+def test_row_sharded_iteration_replay(cfg1):
+    """One full converged-CG iteration through the sharded matvec agrees with the oracle to 1e-8."""
+    from paper_2310_14087_b200 import rowshard
+    pd = gpu_pd(cfg1)
+    rowshard.emulate_shards(pd, 3)
+    newton = K.NewtonConfig(cg_tol=1e-14, cg_max=3000, cg_restarts=0)
+    cfg = K.SolverConfig(newton=newton, eg=EgConfig(float(cfg1["eg_stepsize"])), residual_tol=1e-12, max_iter=40)
+    ocfg = O.SolverCfg(newton=O.NewtonCfg(cg_tol=1e-14, cg_max=3000, cg_restarts=0),
+                       eg_stepsize=float(cfg1["eg_stepsize"]), residual_tol=1e-12, max_iter=40)
+    po = oracle_pd(cfg1)
+    for i in (0, 10):
+        w = GP.IteratePair(cfg1[f"rp{i}_wg"], cfg1[f"rp{i}_wx"])
+        v = GP.IteratePair(cfg1[f"rp{i}_vg"], cfg1[f"rp{i}_vx"])
+        theta = float(cfg1[f"rp{i}_theta"])
+        ow = O.Pair(w.gamma.copy(), w.x_mat.copy())
+        r_w, dc_w = O.residual_parts(po, ow)
+        st0 = O.State(ow, O.Pair(v.gamma.copy(), v.x_mat.copy()), r_w, dc_w, r_w.norm(), None, None, r_w.norm(),
+                      theta)
+        ost, orec, _ = O.iterate_once(po, st0, i, ocfg)
+        w2, v2, th2, rec = GS.iterate(pd, cfg, w, v, theta, i)
+        assert rec.accepted == orec.accepted, i
+        assert rel(w2.gamma, ost.w.g) <= 1e-8, i
+        assert rel(w2.x_mat, ost.w.x) <= 1e-8, i

@@ -17,7 +17,7 @@ from paper_2310_14087_b200 import _lib, configs, solver
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 n = int(sys.argv[3]) if len(sys.argv) > 3 else None
-wl = {"cfg1": configs.config1, "cfg2": configs.config2, "cfg3": configs.config3}[cfg_name]()
+wl = {"cfg1": configs.config1, "cfg2": configs.config2, "cfg3": configs.config3, "cfg4": configs.config4}[cfg_name]()
 if n and cfg_name == "cfg3":
     wl = configs.config3(n=n)
 sx, sy, sxy = K.build_kernel_specs(wl.d, wl.bandwidth_sq)
