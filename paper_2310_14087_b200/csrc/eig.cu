@@ -392,6 +392,17 @@ __global__ void set_last_diag_kernel(const double* A, int n, double* d) { d[n - 
 
 unsigned long long* g_trd_dbg = nullptr;  // set by kot_debug_sytrd_timing
 
+// CTAs of the cooperative panel kernel (≤ one per SM).  KOT_TRD_GRID lowers it
+// (diagnostic: fewer SMs per eigensolve, more eigensolves co-resident).
+static int trd_grid_cap() {
+  static const int cap = [] {
+    const char* e = std::getenv("KOT_TRD_GRID");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? std::min(v, kNumSMs) : kNumSMs;
+  }();
+  return cap;
+}
+
 static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st) {
   KOT_CUDA(cudaMemcpyAsync(w.A, Z, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
   KOT_CUDA(cudaMemsetAsync(w.Vall, 0, sizeof(double) * n * n, st));
@@ -400,7 +411,7 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st) {
     const int nb = std::min(TRD_NB, n - 1 - p0);
     KOT_CUDA(cudaMemsetAsync(w.X, 0, sizeof(double) * n * 3 * TRD_NB, st));
     const int rows = n - p0;
-    const int G = std::max(1, std::min(kNumSMs, ceil_div(rows, TRD_WARPS)));
+    const int G = std::max(1, std::min(trd_grid_cap(), ceil_div(rows, TRD_WARPS)));
     kot_require((long)G * TRD_WARPS * TRD_RPW >= rows, KOT_EINVAL, "matrix order too large for sytrd");
     TrdArgs args{w.A, n, p0, nb, w.X, w.Vall, w.d, w.e, w.tau, w.xv, w.yv, w.part, w.partn, g_trd_dbg,
                  w.gpart, w.gcnt};
@@ -1365,7 +1376,8 @@ static int sytrd_coresident_cap(int n) {
     KOT_CUDA(cudaFuncSetAttribute(sytrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   KOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sytrd_panel_kernel, TRD_THREADS, smem));
-  return std::max(1, per_sm);
+  const int g = std::max(1, std::min(trd_grid_cap(), ceil_div(n, TRD_WARPS)));
+  return std::max(1, per_sm * kNumSMs / g);
 }
 
 void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigWork& w, cudaStream_t st,

@@ -71,6 +71,14 @@ void prof_end(int tok, cudaStream_t st, double flops, double bytes) {
   if (g_pending.size() > 4096) resolve_locked();
 }
 
+void prof_host(const char* name, double ms) {
+  if (!g_on) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  Entry& e = g_entries[entry_of(name)];
+  e.ms += ms;
+  e.calls += 1;
+}
+
 }  // namespace kot
 
 extern "C" int kot_profile_enable(int on) {

@@ -10,6 +10,8 @@ bool prof_enabled();
 // open a scope: returns a token (or -1 when disabled)
 int prof_begin(const char* name, cudaStream_t st);
 void prof_end(int token, cudaStream_t st, double flops, double bytes = 0.0);
+// host-side wall time (e.g. the solve loop waiting for the EG pipeline)
+void prof_host(const char* name, double ms);
 
 struct ProfScope {
   int tok;

@@ -306,6 +306,7 @@ class EgPipeline {
         eg_step(a, gin, Xin, s_, out.g, out.X);
         KOT_CUDA(cudaStreamSynchronize(a.st));
         out.eg_ms = ms_since(t0);
+        prof_host("host.pipe_eg", out.eg_ms);
       } catch (...) {
         std::lock_guard<std::mutex> lk(mu_);
         out.err = std::current_exception();
@@ -334,6 +335,7 @@ class EgPipeline {
         sl.res = residual_parts(b, sl.g, sl.X, sl.r1, sl.r2, dc);
         sl.k = dc.k;
         sl.resid_ms = ms_since(t0);
+        prof_host("host.pipe_resid", sl.resid_ms);
       } catch (...) {
         std::lock_guard<std::mutex> lk(mu_);
         sl.err = std::current_exception();
@@ -402,17 +404,21 @@ static bool loop_body(Problem& p, const SolverCfg& cfg, LoopState& s, int k, Ite
     st = newton_direction(p, b.r1w, b.r2w, s.res_w, s.dw, mu, cfg, b.dg, b.dX);
     KOT_CUDA(cudaStreamSynchronize(p.st));
     newton_ms = ms_since(t0);
+    prof_host("host.newton", newton_ms);
     axpby(p, n, 1.0, b.gw, 1.0, b.dg, b.gt);
     axpby(p, nn, 1.0, b.Xw, 1.0, b.dX, b.Xt);
     t0 = clk::now();
     res_t = residual_parts(p, b.gt, b.Xt, b.r1t, b.r2t, s.dt);
     resid_ms += ms_since(t0);
+    prof_host("host.trial_resid", resid_ms);
   } catch (...) {
     nt_err = std::current_exception();
   }
   if (eg_thread.joinable()) eg_thread.join();
   if (do_eg && s.pipe) {
+    const auto tw = clk::now();
     EgSlot& sl = s.pipe->acquire(++s.vj);
+    prof_host("host.eg_wait", ms_since(tw));
     if (sl.err) eg_err = sl.err;
     s.vslot = &sl;
     s.res_v = sl.res;
