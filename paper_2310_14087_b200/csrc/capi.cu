@@ -341,6 +341,19 @@ int kot_sym_eig(const double* z, int n, int device, double* vecs, double* vals, 
   });
 }
 
+int kot_debug_tridiag(const double* z, int n, int device, int stages, double* d_out, double* e_out) {
+  return guarded([&] {
+    auto p = scratch_problem(n, device);
+    const long nn = (long)n * n;
+    up(*p, p->M1, z, nn);
+    kot::symmetrize(*p, p->M1, p->M2);
+    kot::tridiag_device(p->M2, n, *p->eig, p->st, stages);
+    down(*p, d_out, p->eig->d, n);
+    down(*p, e_out, p->eig->e, n - 1);
+    KOT_CUDA(cudaStreamSynchronize(p->st));
+  });
+}
+
 int kot_proj_psd(const double* z, int n, int device, double* out) {
   return guarded([&] {
     auto p = scratch_problem(n, device);

@@ -81,11 +81,17 @@ EigWork::EigWork(int n_) : n(n_) {
   KOT_CUDA(cudaMalloc(&ibuf, sizeof(int) * (8L * n + 64)));
   KOT_CUDA(cudaMalloc(&dbuf, 16L * n + 4096 + 64L * n));
   KOT_CUDA(cudaMallocHost(&hbuf, sizeof(int) * (12L * n + 512)));
+  if (n >= 3) {
+    const long q2 = two_stage_q2_size(n);
+    alloc(&Vq2, q2);
+    alloc(&Tq2, two_stage_t_size(n));
+    alloc(&tq2, q2 / 16);
+  }
 }
 
 EigWork::~EigWork() {
   for (double* p : {A, Vall, X, d, e, tau, xv, yv, part, partn, Tf, W1, Q, Qw, Qnd, Dl, Uw, zs, ds, dlam, wv, what, lam,
-                    dfv, rotcs, rho, splitws, gpart})
+                    dfv, rotcs, rho, splitws, gpart, Vq2, Tq2, tq2})
     cudaFree(p);
   cudaFree(gcnt);
   cudaFree(ibuf);
@@ -1380,18 +1386,43 @@ static int sytrd_coresident_cap(int n) {
   return std::max(1, per_sm * kNumSMs / g);
 }
 
+// Two-stage reduction (eig2.cu) from this order up; KOT_EIG_STAGES=1|2 overrides.
+bool use_two_stage(int n) {
+  static const int forced = [] {
+    const char* e = std::getenv("KOT_EIG_STAGES");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 1) return false;
+  if (forced == 2) return n >= 3;
+  return n >= 64;
+}
+
+static void one_stage_tridiag(const double* Z, int n, EigWork& w, cudaStream_t st, int lane) {
+  ProfScope ps("eig.sytrd", st, 4.0 / 3.0 * n * (double)n * n);
+  CoopGate gate(sytrd_coresident_cap(n), lane);
+  sytrd(Z, n, w, st);
+  KOT_CUDA(cudaStreamSynchronize(st));  // the gate is held until the grids have retired
+}
+
+void tridiag_device(const double* Z, int n, EigWork& w, cudaStream_t st, int stages) {
+  kot_require(n >= 2, KOT_EINVAL, "order must be >= 2");
+  if (stages == 2 && n >= 3)
+    two_stage_tridiag(Z, n, w, st);
+  else
+    one_stage_tridiag(Z, n, w, st, 0);
+}
+
 void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigWork& w, cudaStream_t st,
                   int lane) {
   if (n == 1) {
     eig1_kernel<<<1, 1, 0, st>>>(Z, P, vals);
     KOT_LAUNCH_CHECK();
   } else {
-    {
-      ProfScope ps("eig.sytrd", st, 4.0 / 3.0 * n * (double)n * n);
-      CoopGate gate(sytrd_coresident_cap(n), lane);
-      sytrd(Z, n, w, st);
-      KOT_CUDA(cudaStreamSynchronize(st));  // the gate is held until the grids have retired
-    }
+    const bool two = use_two_stage(n);
+    if (two)
+      two_stage_tridiag(Z, n, w, st);
+    else
+      one_stage_tridiag(Z, n, w, st, lane);
     {
       ProfScope ps("eig.stedc", st);
       stedc(n, w, st);
@@ -1399,6 +1430,7 @@ void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigW
     ProfScope ps("eig.ormtr", st, 2.0 * n * (double)n * n);
     reverse_cols_kernel<<<std::min(ceil_div((long)n * n, 256), 2048), 256, 0, st>>>(w.Q, w.d, P, vals, n);
     KOT_LAUNCH_CHECK();
+    if (two) two_stage_q2_apply(n, w, P, st);
     ormtr(n, w, P, st);
   }
   count_pos_kernel<<<1, 256, 0, st>>>(vals, n, dk);

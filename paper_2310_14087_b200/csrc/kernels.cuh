@@ -28,6 +28,7 @@ struct EigWork {
   double *zs = nullptr, *ds = nullptr, *dlam = nullptr, *wv = nullptr, *what = nullptr, *lam = nullptr;
   double *dfv = nullptr, *rotcs = nullptr, *rho = nullptr, *splitws = nullptr, *gpart = nullptr;
   int* gcnt = nullptr;
+  double *Vq2 = nullptr, *tq2 = nullptr, *Tq2 = nullptr;  // two-stage: stage-2 reflectors, τ, group T
   long splitws_cap = 0;
   int* ibuf = nullptr;
   void* dbuf = nullptr;
@@ -40,6 +41,15 @@ struct EigWork {
 // Z symmetric (n×n, row-major, device).  Outputs: P (columns = eigenvectors,
 // descending eigenvalues), vals (descending), *dk = #(vals > 0).
 // lane: 0 = latency-critical caller (always keeps a co-residency slot), 1 = background.
+// two-stage tridiagonalisation (eig2.cu): Z → (w.d, w.e), stage-1 reflectors in
+// w.Vall/w.tau (ormtr layout), stage-2 reflectors in w.Vq2/w.tq2
+long two_stage_q2_size(int n);
+long two_stage_t_size(int n);
+void two_stage_tridiag(const double* Z, int n, EigWork& w, cudaStream_t st);
+void two_stage_q2_apply(int n, EigWork& w, double* P, cudaStream_t st);  // P ← Q2 P
+bool use_two_stage(int n);
+// tridiagonal form only (debug/tests): stages = 1 (one-stage sytrd) or 2
+void tridiag_device(const double* Z, int n, EigWork& w, cudaStream_t st, int stages);
 void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigWork& w, cudaStream_t st,
                   int lane = 0);
 

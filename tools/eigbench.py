@@ -37,6 +37,23 @@ linalg.sym_eig(z)
 L.kot_debug_sytrd_timing(0, buf)
 names = ["Q:partials+prefetch", "Q:finish W", "Q:col update+partn", "grid.sync#1", "S:norm+householder",
          "S:scale+symv+partials", "S:part write", "grid.sync#2"]
-tot = sum(buf)
+tot = sum(buf) or 1
 for nm, v in zip(names, buf):
     print(f"  {nm:24s} {v/1e6:8.3f} ms  {v/tot*100:5.1f}%  ({v/1e3/(n-1):.2f} us/col)")
+
+# per-segment cycles of the bulge-chasing kernel (every CTA × warp)
+f = getattr(L, "kot_debug_sb2st_timing", None)
+if f is not None:
+    buf2 = (C.c_ulonglong * (16 * 8 * 8))()
+    f(1, buf2)
+    linalg.sym_eig(z)
+    f(0, buf2)
+    a = np.array(buf2[:], dtype=float).reshape(16, 8, 8)
+    names = ["enum/idle", "load", "(1) C·Hp", "(2) house+bcast", "(3) C left", "(4) D two-sided", "store+slot",
+             "cluster.sync"]
+    busy = a[:, :, :7].sum(axis=2)
+    print("  sb2st busy Mcyc per CTA (max over warps):", np.round(busy.max(axis=1) / 1e6, 2))
+    print("  sb2st sync Mcyc per CTA (warp 0):", np.round(a[:, 0, 7] / 1e6, 2))
+    w = np.unravel_index(np.argmax(busy), busy.shape)
+    for k, nm in enumerate(names):
+        print(f"  sb2st busiest warp {w}: {nm:18s} {a[w[0], w[1], k]/1e6:9.3f} Mcyc")
