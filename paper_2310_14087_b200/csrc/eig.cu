@@ -81,12 +81,16 @@ EigWork::EigWork(int n_) : n(n_) {
   KOT_CUDA(cudaMalloc(&ibuf, sizeof(int) * (8L * n + 64)));
   KOT_CUDA(cudaMalloc(&dbuf, 16L * n + 4096 + 64L * n));
   KOT_CUDA(cudaMallocHost(&hbuf, sizeof(int) * (12L * n + 512)));
-  if (n >= 3) {
-    const long q2 = two_stage_q2_size(n);
-    alloc(&Vq2, q2);
-    alloc(&Tq2, two_stage_t_size(n));
-    alloc(&tq2, q2 / 16);
-  }
+}
+
+// two-stage buffers on first use (the default one-stage path never touches them)
+void EigWork::ensure_two_stage() {
+  if (Vq2 || n < 3) return;
+  auto alloc = [&](double** p, long cnt) { KOT_CUDA(cudaMalloc(p, std::max(cnt, 1L) * sizeof(double))); };
+  const long q2 = two_stage_q2_size(n);
+  alloc(&Vq2, q2);
+  alloc(&Tq2, two_stage_t_size(n));
+  alloc(&tq2, q2 / 16);
 }
 
 EigWork::~EigWork() {
@@ -1386,15 +1390,21 @@ static int sytrd_coresident_cap(int n) {
   return std::max(1, per_sm * kNumSMs / g);
 }
 
-// Two-stage reduction (eig2.cu) from this order up; KOT_EIG_STAGES=1|2 overrides.
-bool use_two_stage(int n) {
-  static const int forced = [] {
+// Which tridiagonalisation an eigensolve uses.  Measured on B200 (eigbench,
+// DESIGN.md): the one-stage sytrd is faster at ℓ = 2000 (35 vs 45 ms), 4096 and
+// 8192; the two-stage path (eig2.cu) keeps its latency-bound parts on ≤ 16 SMs
+// but its back-transform is not yet tensor-core bound, and running it beside the
+// one-stage grids slowed the Newton chain (probe: 80 vs 47 ms per trial
+// residual).  So the default is one-stage; KOT_EIG_STAGES=2 (or
+// kot_debug_eig_stages) selects the two-stage reduction.
+static int g_eig_stages = -1;  // −1: read KOT_EIG_STAGES once
+bool use_two_stage(int n, int lane) {
+  (void)lane;
+  if (g_eig_stages < 0) {
     const char* e = std::getenv("KOT_EIG_STAGES");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (forced == 1) return false;
-  if (forced == 2) return n >= 3;
-  return n >= 64;
+    g_eig_stages = e ? std::atoi(e) : 1;
+  }
+  return g_eig_stages == 2 && n >= 3;
 }
 
 static void one_stage_tridiag(const double* Z, int n, EigWork& w, cudaStream_t st, int lane) {
@@ -1418,7 +1428,7 @@ void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigW
     eig1_kernel<<<1, 1, 0, st>>>(Z, P, vals);
     KOT_LAUNCH_CHECK();
   } else {
-    const bool two = use_two_stage(n);
+    const bool two = use_two_stage(n, lane);
     if (two)
       two_stage_tridiag(Z, n, w, st);
     else
@@ -1456,4 +1466,10 @@ extern "C" int kot_debug_sytrd_timing(int on, unsigned long long* out8) {
   } catch (const KotError& e) {
     return e.code;
   }
+}
+
+// test hook: 1 = one-stage, 2 = two-stage tridiagonalisation for subsequent eigensolves
+extern "C" int kot_debug_eig_stages(int stages) {
+  kot::g_eig_stages = (stages == 2) ? 2 : 1;
+  return 0;
 }

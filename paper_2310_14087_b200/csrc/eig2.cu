@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "gemm.cuh"
 #include "kernels.cuh"
@@ -39,9 +40,9 @@ namespace kot {
 
 constexpr int SB = 16;            // band width
 constexpr int SB_LDX = 3 * SB;    // stage-1 GEMM operand rows [V | W | V]
-constexpr int PQR_THREADS = 256;  // 16 columns × 16 row groups
+constexpr int PQR_THREADS = 512;  // 16 warps (column q) × 32 lanes (row group)
 constexpr int PQR_LD = SB + 1;
-constexpr int PQR_MAXCS = 8;
+constexpr int PQR_MAXCS = 16;
 constexpr int SB2_LDB = 2 * SB;   // band column: d = r − c ∈ [0, 2·SB)  (bulge reaches 2·SB − 1)
 
 static int eig_nt(int n) { return (n - 2) / SB + 1; }           // tasks per sweep (max)
@@ -58,135 +59,153 @@ __device__ __forceinline__ double half_sum(double v, unsigned mask) {
 }
 
 // Householder QR of the sub-panel A[j+SB:, j:j+SB] on one cluster (rows split
-// over the CTAs).  Writes R into A, the reflectors (explicit, zero above the
-// unit entry, zero column if τ = 0) into Vall (ormtr layout) and Xs, τ, and
-// the panel's T (forward, columnwise) into Tp.
+// over the CTAs, thread (q, rg) = column q × row group rg).  Per column: one
+// cluster barrier for ‖x‖²/α, one for the 15 dot products vᵀP[:, q]; each
+// half-warp gathers the CTA partials through DSMEM and reduces them in a fixed
+// lane order, so every CTA derives bit-identical β, τ.  Writes R into A, the
+// reflectors (explicit, zero above the unit entry, zero column if τ = 0) into
+// Vall (ormtr layout) and Xs, τ, and the panel's T (forward, columnwise) into Tp.
+constexpr int PQR_RPT = 16;  // rows per lane: ≤ 32·16 = 512 rows per CTA
+unsigned long long* g_pqr_dbg = nullptr;
 __global__ void __launch_bounds__(PQR_THREADS) sy2sb_panel_kernel(double* A, int n, int j, double* Vall,
-                                                                  double* tau_out, double* Xs, double* Tp) {
+                                                                  double* tau_out, double* Xs, double* Tp,
+                                                                  unsigned long long* dbg) {
   cg::cluster_group cl = cg::this_cluster();
+  const bool timing = dbg && threadIdx.x == 0 && cl.block_rank() == 0;
+  long long tl = timing ? clock64() : 0;
+  unsigned long long tseg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define PQM(k_)                     \
+  if (timing) {                     \
+    const long long t_ = clock64(); \
+    tseg[k_] += t_ - tl;            \
+    tl = t_;                        \
+  }
   const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   extern __shared__ double P[];  // [rows][PQR_LD]
-  __shared__ double red[2][2 * SB];
-  __shared__ double tot[SB];
-  __shared__ double Ts[SB][SB + 1];
+  __shared__ double red_n[2];
+  __shared__ double red_d[SB];
+  __shared__ double Sk[SB][SB + 1];
   __shared__ double taus[SB];
-  __shared__ double sc[4];
-  __shared__ double gath[PQR_MAXCS][2 * SB];
+  __shared__ double Ts[SB][SB + 1];
   const int m = n - j - SB;
   const int kb = min(SB, m);
   const int rc = (m + CS - 1) / CS;
   const int lo = rank * rc, hi = min(m, lo + rc);
-  const int tid = threadIdx.x, q = tid >> 4, rg = tid & 15;
-  const unsigned hmask = 0xffffu << (16 * ((tid >> 4) & 1));
+  const int tid = threadIdx.x, q = tid >> 5, rg = tid & 31;
   for (int e = tid; e < (hi - lo) * SB; e += blockDim.x) {
     const int rr = e / SB, cc = e % SB;
     P[rr * PQR_LD + cc] = A[(long)(j + SB + lo + rr) * n + j + cc];
   }
-  for (int e = tid; e < SB * (SB + 1); e += blockDim.x) (&Ts[0][0])[e] = 0.0;
   if (tid < SB) taus[tid] = 0.0;
   __syncthreads();
-  int par = 0;
-  for (int k = 0; k < kb; ++k) {
-    // ---- (a) ‖x[1:]‖² and α = P[k][k] (owner only; the others add zeros)
-    if (q == k) {
-      double s = 0.0;
-      for (int r = lo + rg; r < hi; r += 16)
-        if (r > k) {
-          const double x = P[(r - lo) * PQR_LD + k];
-          s += x * x;
-        }
-      s = half_sum(s, hmask);
-      if (rg == 0) {
-        red[par][0] = s;
-        red[par][1] = (k >= lo && k < hi) ? P[(k - lo) * PQR_LD + k] : 0.0;
+  if (q == 0) {  // ‖x[1:]‖² and α of column 0
+    double s = 0.0;
+#pragma unroll 4
+    for (int jj = 0; jj < PQR_RPT; ++jj) {
+      const int r = lo + rg + 32 * jj;
+      if (r < hi && r > 0) {
+        const double x = P[(r - lo) * PQR_LD];
+        s += x * x;
       }
     }
-    cl.sync();
-    if (tid < 32) {  // fixed-order gather over the cluster: identical on every CTA
-      double xn = 0.0, al = 0.0;
-      if (tid < CS) {
-        const double* rr = cl.map_shared_rank(&red[par][0], tid);
-        xn = rr[0];
-        al = rr[1];
-      }
-      if (tid < CS) {
-        gath[tid][0] = xn;
-        gath[tid][1] = al;
-      }
-      __syncwarp();
-      if (tid == 0) {
-        double xn2 = 0.0, alpha = 0.0;
-        for (int c = 0; c < CS; ++c) {
-          xn2 += gath[c][0];
-          alpha += gath[c][1];
-        }
-        double beta, tau, scale;
-        if (xn2 == 0.0) {
-          tau = 0.0;
-          beta = alpha;
-          scale = 1.0;
-        } else {
-          beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
-          tau = (beta - alpha) / beta;
-          scale = 1.0 / (alpha - beta);
-        }
-        sc[0] = tau;
-        sc[1] = beta;
-        sc[2] = scale;
-        taus[k] = tau;
-      }
+    s = warp_sum(s);
+    if (rg == 0) {
+      red_n[0] = s;
+      red_n[1] = (lo == 0 && hi > 0) ? P[0] : 0.0;
     }
-    __syncthreads();
-    par ^= 1;
-    const double tau = sc[0], beta = sc[1], scale = sc[2];
-    // ---- (b) v = x / (α − β) below the diagonal, β on it
-    for (int r = lo + tid; r < hi; r += blockDim.x) {
-      if (r > k) P[(r - lo) * PQR_LD + k] *= scale;
-      if (r == k) P[(r - lo) * PQR_LD + k] = beta;
-    }
-    __syncthreads();
-    // ---- (c) s_q = Σ_{r ≥ k} v_r P[r][q]  (q > k: reflector applied to column q; q < k: T column)
-    {
-      double s = 0.0;
-      if (q != k)
-        for (int r = lo + rg; r < hi; r += 16)
-          if (r >= k) {
-            const double v = (r == k) ? 1.0 : P[(r - lo) * PQR_LD + k];
-            s += v * P[(r - lo) * PQR_LD + q];
-          }
-      s = half_sum(s, hmask);
-      if (rg == 0) red[par][q] = s;
-    }
-    cl.sync();
-    for (int e = tid; e < CS * SB; e += blockDim.x) {
-      const int c = e / SB, qq = e % SB;
-      gath[c][qq] = cl.map_shared_rank(&red[par][0], c)[qq];
-    }
-    __syncthreads();
-    if (tid < SB) {
-      double s = 0.0;
-      for (int c = 0; c < CS; ++c) s += gath[c][tid];
-      tot[tid] = s;
-    }
-    __syncthreads();
-    par ^= 1;
-    // ---- (d) P[:, q>k] −= τ v s_qᵀ;  T[0:k, k] = −τ T[0:k,0:k] s[0:k];  T[k][k] = τ
-    if (tau != 0.0)
-      for (int e = tid; e < (hi - lo) * SB; e += blockDim.x) {
-        const int rr = e / SB, cc = e % SB, r = lo + rr;
-        if (cc > k && r >= k) {
-          const double v = (r == k) ? 1.0 : P[rr * PQR_LD + k];
-          P[rr * PQR_LD + cc] -= tau * v * tot[cc];
-        }
-      }
-    if (tid < k) {
-      double s = 0.0;
-      for (int l = tid; l < k; ++l) s += Ts[tid][l] * tot[l];
-      Ts[tid][k] = -tau * s;
-    }
-    if (tid == k) Ts[k][k] = tau;
-    __syncthreads();
   }
+  PQM(0)
+  for (int k = 0; k < kb; ++k) {
+    cl.sync();
+    PQM(1)
+    double xn2 = 0.0, alpha = 0.0;
+    if (rg < CS) {
+      const double* rn = cl.map_shared_rank(red_n, rg);
+      xn2 = rn[0];
+      alpha = rn[1];
+    }
+    xn2 = warp_sum(xn2);
+    alpha = warp_sum(alpha);
+    double beta, tau, scale;
+    if (xn2 == 0.0) {
+      tau = 0.0;
+      beta = alpha;
+      scale = 1.0;
+    } else {
+      beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    PQM(2)
+    // dots s_q = Σ_{r ≥ k} v_r P[r][q]  (q > k: apply to column q; q < k: T column), v cached per row
+    double vc[PQR_RPT];
+    double s = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < PQR_RPT; ++jj) {
+      const int r = lo + rg + 32 * jj;
+      double v = 0.0;
+      if (r < hi && r >= k) {
+        v = (r == k) ? 1.0 : P[(r - lo) * PQR_LD + k] * scale;
+        if (q != k) s += v * P[(r - lo) * PQR_LD + q];
+      }
+      vc[jj] = v;
+    }
+    s = warp_sum(s);
+    if (rg == 0) red_d[q] = s;
+    PQM(3)
+    cl.sync();
+    PQM(4)
+    double tq = (rg < CS) ? cl.map_shared_rank(red_d, rg)[q] : 0.0;
+    tq = warp_sum(tq);
+    if (rg == 0 && q < k) Sk[k][q] = tq;
+    if (tid == 0) taus[k] = tau;
+    if (q > k && tau != 0.0) {
+      const double f = tau * tq;
+#pragma unroll
+      for (int jj = 0; jj < PQR_RPT; ++jj) {
+        const int r = lo + rg + 32 * jj;
+        if (r < hi && r >= k) P[(r - lo) * PQR_LD + q] -= f * vc[jj];
+      }
+    } else if (q == k) {
+#pragma unroll
+      for (int jj = 0; jj < PQR_RPT; ++jj) {
+        const int r = lo + rg + 32 * jj;
+        if (r < hi && r >= k) P[(r - lo) * PQR_LD + k] = (r == k) ? beta : vc[jj];
+      }
+    }
+    PQM(5)
+    if (q == k + 1 && k + 1 < kb) {  // next column's ‖x[1:]‖² and α, from the just-updated values
+      double s2 = 0.0;
+#pragma unroll 4
+      for (int jj = 0; jj < PQR_RPT; ++jj) {
+        const int r = lo + rg + 32 * jj;
+        if (r < hi && r > k + 1) {
+          const double x = P[(r - lo) * PQR_LD + k + 1];
+          s2 += x * x;
+        }
+      }
+      s2 = warp_sum(s2);
+      if (rg == 0) {
+        red_n[0] = s2;
+        red_n[1] = (k + 1 >= lo && k + 1 < hi) ? P[(k + 1 - lo) * PQR_LD + k + 1] : 0.0;
+      }
+    }
+  }
+  PQM(6)
+  __syncthreads();
+  if (tid < SB) {  // T row l: T[l][k] = −τ_k Σ_{l ≤ m < k} T[l][m] s_k[m]
+    const int l = tid;
+    for (int c = 0; c < SB; ++c) Ts[l][c] = 0.0;
+    if (l < kb) {
+      Ts[l][l] = taus[l];
+      for (int c = l + 1; c < kb; ++c) {
+        double acc = 0.0;
+        for (int mm = l; mm < c; ++mm) acc += Ts[l][mm] * Sk[c][mm];
+        Ts[l][c] = -taus[c] * acc;
+      }
+    }
+  }
+  __syncthreads();
   // ---- outputs
   for (int e = tid; e < (hi - lo) * SB; e += blockDim.x) {
     const int rr = e / SB, cc = e % SB, r = lo + rr;
@@ -203,19 +222,119 @@ __global__ void __launch_bounds__(PQR_THREADS) sy2sb_panel_kernel(double* A, int
     if (tid < SB) tau_out[j + tid] = taus[tid];
     for (int e = tid; e < SB * SB; e += blockDim.x) Tp[e] = Ts[e / SB][e % SB];
   }
-  cl.sync();  // no CTA leaves while others may still read its red[]
+  cl.sync();  // no CTA leaves while others may still read its red_n / red_d
+  PQM(7)
+  if (timing)
+    for (int k2 = 0; k2 < 8; ++k2) atomicAdd(dbg + k2, tseg[k2]);
+#undef PQM
 }
 
-// W = Xw T − ½ V M with M = Tᵀ (Vᵀ Xw) T; Xw (rows r0.., cols SB..2SB of Xs) is overwritten by W.
-__global__ void __launch_bounds__(256) sy2sb_w_kernel(double* Xs, int r0, int m, const double* Tp, const double* S) {
-  __shared__ double T[SB][SB + 1], TS[SB][SB + 1], M[SB][SB + 1];
+// Xw = A22 V for a 32-row block and one K-split (partial), plus the partial
+// S = V[rows]ᵀ Xw_partial[rows]; both reduced in fixed order by sy2sb_w_kernel.
+// A22 and V chunks stream through a 2-stage cp.async pipeline (8-byte copies:
+// A22 rows need not be 16-byte aligned).
+constexpr int XW_ROWS = 32;
+constexpr int XW_KC = 48;
+__global__ void __launch_bounds__(256) sy2sb_xw_kernel(const double* __restrict__ A22, int lda, int m,
+                                                       const double* __restrict__ X0, double* Xwp,
+                                                       double* Spart) {
+  __shared__ double Ak[2][XW_ROWS][XW_KC + 1];
+  __shared__ double Vk[2][XW_KC][SB + 1];
+  __shared__ double Xo[XW_ROWS][SB + 1];
+  const int tid = threadIdx.x;
+  const int rb = blockIdx.x * XW_ROWS;
+  const int ks = gridDim.y, kid = blockIdx.y;
+  const int kchunk = ((m + ks - 1) / ks + XW_KC - 1) / XW_KC * XW_KC;
+  const int k0 = kid * kchunk, k1 = min(m, k0 + kchunk);
+  const int r = tid >> 3, cg0 = tid & 7;
+  auto issue = [&](int kb, int buf) {
+    const int kn = min(XW_KC, k1 - kb);
+    for (int e = tid; e < XW_ROWS * XW_KC; e += 256) {
+      const int rr = e / XW_KC, kk = e % XW_KC;
+      const bool ok = rb + rr < m && kk < kn;
+      cp_async_8(&Ak[buf][rr][kk], ok ? A22 + (long)(rb + rr) * lda + kb + kk : A22, ok ? 8 : 0);
+    }
+    for (int e = tid; e < XW_KC * SB; e += 256) {
+      const int kk = e / SB, c = e % SB;
+      const bool ok = kk < kn;
+      cp_async_8(&Vk[buf][kk][c], ok ? X0 + (long)(kb + kk) * SB_LDX + c : X0, ok ? 8 : 0);
+    }
+    cp_async_commit();
+  };
+  double acc0 = 0.0, acc1 = 0.0;
+  int buf = 0;
+  if (k0 < k1) issue(k0, 0);
+  for (int kb = k0; kb < k1; kb += XW_KC) {
+    if (kb + XW_KC < k1) {
+      issue(kb + XW_KC, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll 8
+    for (int kk = 0; kk < XW_KC; kk += 2) {
+      const double a0 = Ak[buf][r][kk], a1 = Ak[buf][r][kk + 1];
+      p0 += a0 * Vk[buf][kk][cg0];
+      q0 += a0 * Vk[buf][kk][cg0 + 8];
+      p1 += a1 * Vk[buf][kk + 1][cg0];
+      q1 += a1 * Vk[buf][kk + 1][cg0 + 8];
+    }
+    acc0 += p0 + p1;
+    acc1 += q0 + q1;
+    __syncthreads();
+    buf ^= 1;
+  }
+  Xo[r][cg0] = acc0;
+  Xo[r][cg0 + 8] = acc1;
+  if (rb + r < m) {
+    Xwp[((long)kid * m + rb + r) * SB + cg0] = acc0;
+    Xwp[((long)kid * m + rb + r) * SB + cg0 + 8] = acc1;
+  }
+  for (int e = tid; e < XW_ROWS * SB; e += 256) {
+    const int rr = e / SB, c = e % SB;
+    Vk[0][rr][c] = (rb + rr < m) ? X0[(long)(rb + rr) * SB_LDX + c] : 0.0;
+  }
+  __syncthreads();
+  {
+    const int a = tid >> 4, c = tid & 15;
+    double sacc = 0.0;
+    for (int rr = 0; rr < XW_ROWS; ++rr) sacc += Vk[0][rr][a] * Xo[rr][c];
+    Spart[((long)kid * gridDim.x + blockIdx.x) * SB * SB + tid] = sacc;
+  }
+}
+
+// Fixed-order sum of the S partials (one CTA of 1024 threads: 4 interleaved chains per entry,
+// each with 8 loads in flight).
+__global__ void __launch_bounds__(1024) sy2sb_sred_kernel(const double* __restrict__ Spart, int nparts, double* S) {
+  __shared__ double part[4][SB * SB];
+  const int e = threadIdx.x & 255, g = threadIdx.x >> 8;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int p = g;
+  for (; p + 28 < nparts; p += 32) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] += __ldg(Spart + (long)(p + 4 * u) * SB * SB + e);
+  }
+  for (int u = 0; p < nparts; p += 4, ++u) acc[u & 7] += __ldg(Spart + (long)p * SB * SB + e);
+  part[g][e] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  __syncthreads();
+  if (g == 0) S[e] = (part[0][e] + part[1][e]) + (part[2][e] + part[3][e]);
+}
+
+// W = Xw T − ½ V M with M = Tᵀ S T, S = Σ partials (fixed order), Xw = Σ_k Xwp[k] (fixed order);
+// W overwrites columns SB..2SB of Xs.
+__global__ void __launch_bounds__(256) sy2sb_w_kernel(double* Xs, int r0, int m, const double* Tp,
+                                                      const double* Sg, const double* Xwp, int ks) {
+  __shared__ double T[SB][SB + 1], TS[SB][SB + 1], M[SB][SB + 1], S[SB][SB + 1];
   __shared__ double xw[16][SB + 1], vv[16][SB + 1];
   const int tid = threadIdx.x, a = tid >> 4, c = tid & 15;
   T[a][c] = Tp[a * SB + c];
+  S[a][c] = Sg[tid];
   __syncthreads();
   {
     double s = 0.0;
-    for (int k = 0; k < SB; ++k) s += T[k][a] * S[k * SB + c];
+    for (int k = 0; k < SB; ++k) s += T[k][a] * S[k][c];
     TS[a][c] = s;
   }
   __syncthreads();
@@ -228,7 +347,9 @@ __global__ void __launch_bounds__(256) sy2sb_w_kernel(double* Xs, int r0, int m,
     const int r = rb + a;
     __syncthreads();
     if (r < m) {
-      xw[a][c] = Xs[(long)(r0 + r) * SB_LDX + SB + c];
+      double x = 0.0;
+      for (int k = 0; k < ks; ++k) x += Xwp[((long)k * m + r) * SB + c];
+      xw[a][c] = x;
       vv[a][c] = Xs[(long)(r0 + r) * SB_LDX + c];
     }
     __syncthreads();
@@ -243,7 +364,69 @@ __global__ void __launch_bounds__(256) sy2sb_w_kernel(double* Xs, int r0, int m,
   }
 }
 
-static int pqr_cluster(int m) { return std::max(1, std::min(PQR_MAXCS, (m + 255) / 256)); }
+// A22 −= V Wᵀ + W Vᵀ for one 64×64 lower tile (tm ≥ tn) + its mirror: K = 2·SB = 32,
+// both operands staged whole in shared memory, one triangle computed (exact symmetry).
+constexpr int S2K_T = 64;
+constexpr int S2K_LD = 2 * SB + 1;
+constexpr int S2K_SMEM = (2 * S2K_T * S2K_LD + S2K_T * (S2K_T + 1)) * 8;
+__global__ void __launch_bounds__(256) sy2sb_syr2k_kernel(double* C, int ldc, int m, const double* __restrict__ X0) {
+  extern __shared__ double s2k[];
+  double (*Ash)[S2K_LD] = reinterpret_cast<double (*)[S2K_LD]>(s2k);
+  double (*Bsh)[S2K_LD] = reinterpret_cast<double (*)[S2K_LD]>(s2k + S2K_T * S2K_LD);
+  double (*Ct)[S2K_T + 1] = reinterpret_cast<double (*)[S2K_T + 1]>(s2k + 2 * S2K_T * S2K_LD);
+  // blockIdx.x → lower tile (tm, tn), tm ≥ tn
+  const int b = blockIdx.x;
+  int tm = (int)((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
+  while ((tm + 1) * (tm + 2) / 2 <= b) ++tm;
+  while (tm * (tm + 1) / 2 > b) --tm;
+  const int tn = b - tm * (tm + 1) / 2;
+  const int i0 = tm * S2K_T, j0 = tn * S2K_T;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < S2K_T * 2 * SB; e += 256) {
+    const int rr = e / (2 * SB), k = e % (2 * SB);
+    Ash[rr][k] = (i0 + rr < m) ? __ldg(X0 + (long)(i0 + rr) * SB_LDX + k) : 0.0;       // [V | W]
+    Bsh[rr][k] = (j0 + rr < m) ? __ldg(X0 + (long)(j0 + rr) * SB_LDX + SB + k) : 0.0;  // [W | V]
+  }
+  __syncthreads();
+  const int tr = tid >> 4, tc = tid & 15;
+  double acc[4][4] = {};
+#pragma unroll 4
+  for (int k = 0; k < 2 * SB; ++k) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) av[v] = Ash[tr + 16 * v][k];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) bv[u] = Bsh[tc + 16 * u][k];
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[v][u] += av[v] * bv[u];
+  }
+#pragma unroll
+  for (int v = 0; v < 4; ++v)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + tr + 16 * v, j = j0 + tc + 16 * u;
+      double o = 0.0;
+      if (i < m && j < m && i >= j) {
+        o = C[(long)i * ldc + j] - acc[v][u];
+        C[(long)i * ldc + j] = o;
+      }
+      Ct[tr + 16 * v][tc + 16 * u] = o;
+    }
+  __syncthreads();
+  // mirror: C[j][i] = C[i][j] for i > j, coalesced along i
+#pragma unroll
+  for (int v = 0; v < 4; ++v)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int jj = tr + 16 * v, ii = tc + 16 * u;  // row j0+jj, column i0+ii
+      const int i = i0 + ii, j = j0 + jj;
+      if (i < m && j < m && i > j) C[(long)j * ldc + i] = Ct[ii][jj];
+    }
+}
+
+static int pqr_cluster(int m) { return std::max(1, std::min(PQR_MAXCS, (m + 191) / 192)); }
 
 static void sy2sb(const double* Z, int n, EigWork& w, cudaStream_t st) {
   KOT_CUDA(cudaMemcpyAsync(w.A, Z, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
@@ -251,15 +434,21 @@ static void sy2sb(const double* Z, int n, EigWork& w, cudaStream_t st) {
   KOT_CUDA(cudaMemsetAsync(w.tau, 0, sizeof(double) * n, st));
   double* Xs = w.X;      // n × SB_LDX
   double* Tp = w.Tf;     // SB × SB
-  double* S = w.Tf + SB * SB;
+  double* Sred = w.Tf + SB * SB;
   static int smem_set = 0;
+  static bool s2k_attr = false;
+  if (!s2k_attr) {
+    KOT_CUDA(cudaFuncSetAttribute(sy2sb_syr2k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, S2K_SMEM));
+    s2k_attr = true;
+  }
   for (int j = 0; j + SB + 1 < n; j += SB) {
     const int m = n - j - SB;
     const int cs = pqr_cluster(m);
-    kot_require(cs <= PQR_MAXCS, KOT_EINVAL, "matrix order too large for the band reduction");
+    kot_require(ceil_div(m, cs) <= 32 * PQR_RPT, KOT_EINVAL, "matrix order too large for the band reduction");
     const int rows = (m + cs - 1) / cs;
     const size_t smem = sizeof(double) * std::max(rows, 1) * PQR_LD;
     if ((int)smem > smem_set) {
+      KOT_CUDA(cudaFuncSetAttribute(sy2sb_panel_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       KOT_CUDA(cudaFuncSetAttribute(sy2sb_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       smem_set = (int)smem;
     }
@@ -277,30 +466,28 @@ static void sy2sb(const double* Z, int n, EigWork& w, cudaStream_t st) {
       cfg.attrs = at;
       cfg.numAttrs = 1;
       ProfScope ps("sy2sb_panel", st);
-      KOT_CUDA(cudaLaunchKernelEx(&cfg, sy2sb_panel_kernel, w.A, n, j, w.Vall, w.tau, Xs, Tp));
+      KOT_CUDA(cudaLaunchKernelEx(&cfg, sy2sb_panel_kernel, w.A, n, j, w.Vall, w.tau, Xs, Tp, g_pqr_dbg));
       KOT_LAUNCH_CHECK();
     }
     const int r0 = j + SB;
     double* A22 = w.A + (long)r0 * n + r0;
     double* X0 = Xs + (long)r0 * SB_LDX;
-    {  // Xw = A22 V
-      GemmShape s = make_shape(m, SB, m, A22, n, X0, SB_LDX);
-      s.ws = w.splitws;
-      s.ksplit = choose_ksplit(s, w.splitws_cap);
-      gemm_launch<false, false>(s, EpiAxpby{X0 + SB, SB_LDX, 1.0, 0.0}, st);
+    {  // Xw = A22 V (row blocks × K-splits) and the partial S = Vᵀ Xw; then W
+      const int nb = ceil_div(m, XW_ROWS);
+      const int ks = std::max(1, std::min(2, m / 512));
+      double* Xwp = w.W1;       // [ks][m][SB]
+      double* Spart = w.splitws;  // [ks·nb][SB·SB]
+      sy2sb_xw_kernel<<<dim3(nb, ks), 256, 0, st>>>(A22, n, m, X0, Xwp, Spart);
+      KOT_LAUNCH_CHECK();
+      sy2sb_sred_kernel<<<1, 1024, 0, st>>>(Spart, ks * nb, Sred);
+      KOT_LAUNCH_CHECK();
+      sy2sb_w_kernel<<<std::min(ceil_div(m, 16), 2 * kNumSMs), 256, 0, st>>>(Xs, r0, m, Tp, Sred, Xwp, ks);
+      KOT_LAUNCH_CHECK();
     }
-    {  // S = Vᵀ Xw
-      GemmShape s = make_shape(SB, SB, m, X0, SB_LDX, X0 + SB, SB_LDX);
-      s.ws = w.splitws;
-      s.ksplit = choose_ksplit(s, w.splitws_cap);
-      gemm_launch<true, false>(s, EpiAxpby{S, SB, 1.0, 0.0}, st);
-    }
-    sy2sb_w_kernel<<<std::min(ceil_div(m, 16), 2 * kNumSMs), 256, 0, st>>>(Xs, r0, m, Tp, S);
-    KOT_LAUNCH_CHECK();
     {  // A22 −= V Wᵀ + W Vᵀ  (one triangle + mirror)
-      GemmShape s = make_shape(m, m, 2 * SB, X0, SB_LDX, X0 + SB, SB_LDX);
-      s.sym_tiles = 1;
-      gemm_launch<false, true>(s, EpiSymMirror{A22, n, -1.0, A22, 1.0, 0.0}, st);
+      const int nt = ceil_div(m, S2K_T);
+      sy2sb_syr2k_kernel<<<nt * (nt + 1) / 2, 256, S2K_SMEM, st>>>(A22, n, m, X0);
+      KOT_LAUNCH_CHECK();
     }
   }
 }
@@ -336,7 +523,8 @@ __device__ __forceinline__ double warp_house(double x, int lane, double& tau, do
     beta = alpha;
     scale = 1.0;
   } else {
-    beta = -copysign(hypot(alpha, sqrt(s)), alpha);
+    // band entries are O(‖A‖): no over/underflow guard (hypot) needed on this path
+    beta = -copysign(sqrt(fma(alpha, alpha, s)), alpha);
     tau = (beta - alpha) / beta;
     scale = 1.0 / (alpha - beta);
   }
@@ -359,31 +547,43 @@ __device__ __forceinline__ void dsm_st(uint32_t a, double v) {
 
 constexpr int SB2_WARPS = 8;
 constexpr int SB2_NTHREADS = 32 * SB2_WARPS;
-constexpr int SB2_SLOT = SB + 1;  // v[16], τ
-constexpr int SB2_NSLOT = 64;     // slots per step parity, keyed by t mod 64
 
 __device__ __forceinline__ double sum16(const double (&p)[16]) {
   return ((((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]))) +
           (((p[8] + p[9]) + (p[10] + p[11])) + ((p[12] + p[13]) + (p[14] + p[15]))));
 }
 
-// Bulge chasing, one warp per task.  Lanes 0–15 hold the rows of the off-diagonal
-// block C (or, for t = 0, the column being annihilated), lanes 16–31 the rows of
-// the symmetric diagonal block D, all in registers.  The reflector of task
-// (i, t−1), needed by (i, t) one step later, is handed over through a DSMEM slot
-// of the producing CTA (slot [s & 1][t & 63]: within a CTA the live t's span < 64).
+__device__ __forceinline__ void dsm_st_release_u64(uint32_t a, unsigned long long v) {
+  asm volatile("st.release.cluster.shared::cluster.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long dsm_ld_acquire_u64(uint32_t a) {
+  unsigned long long v;
+  asm volatile("ld.acquire.cluster.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+
+// Bulge chasing, one warp per SWEEP: warp g of the cluster chases sweeps g, g+W, g+2W, …
+// (W = warps in the cluster) all the way down, keeping the previous reflector in
+// registers.  Task (i, t) only has to wait for task (i−1, t+1): the predecessor
+// sweep's warp publishes (sweep+1, tasks done) with a cluster-scope release store
+// in its CTA's shared memory, the successor polls it with acquire loads.  Tasks
+// running concurrently under this rule are element-disjoint (wavefront argument,
+// tools/twostage_proto.py).  Lanes 0–15 hold the rows of the off-diagonal block
+// C (or the column being annihilated for t = 0), lanes 16–31 the rows of the
+// diagonal block D, in registers; the band lives in the cluster's shared memory.
 __global__ void __launch_bounds__(SB2_NTHREADS, 1) sb2st_kernel(Sb2Args a) {
   cg::cluster_group cl = cg::this_cluster();
   const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   extern __shared__ double sm[];
   const int n = a.n, cw = a.cw;
-  double* AB = sm;                                // [cw][SB2_LDB]
-  double* slots = sm + (long)cw * SB2_LDB;        // [2][SB2_NSLOT][SB2_SLOT]
-  __shared__ uint32_t cbase[16], sbase[16];  // shared::cluster addresses of AB / slots in every CTA
+  double* AB = sm;  // [cw][SB2_LDB]
+  __shared__ unsigned long long prog[SB2_WARPS];
+  __shared__ uint32_t cbase[16], pbase[16];  // shared::cluster addresses of AB / prog in every CTA
   if (threadIdx.x < CS) {
     cbase[threadIdx.x] = dsm_map(AB, threadIdx.x);
-    sbase[threadIdx.x] = dsm_map(slots, threadIdx.x);
+    pbase[threadIdx.x] = dsm_map(prog, threadIdx.x);
   }
+  if (threadIdx.x < SB2_WARPS) prog[threadIdx.x] = 0ull;
   const int c0 = rank * cw, c1 = min(n, c0 + cw);
   for (int e = threadIdx.x; e < cw * SB2_LDB; e += blockDim.x) {
     const int c = c0 + e / SB2_LDB, dd = e % SB2_LDB;
@@ -393,35 +593,42 @@ __global__ void __launch_bounds__(SB2_NTHREADS, 1) sb2st_kernel(Sb2Args a) {
   const int r = lane & 15;
   const bool isC = lane < 16;
   const unsigned full = 0xffffffffu;
+  const int W = CS * SB2_WARPS, g = rank * SB2_WARPS + warp;
+  const int gp = (g + W - 1) % W;  // warp chasing the previous sweep
   cl.sync();
-
-  const int smax = 2 * n - 6;
-  const bool timing = a.dbg && (threadIdx.x & 31) == 0;
+  const uint32_t my_prog = pbase[rank] + (uint32_t)(warp * 8);
+  const uint32_t pred_prog = pbase[gp / SB2_WARPS] + (uint32_t)((gp % SB2_WARPS) * 8);
+  const bool timing = a.dbg && lane == 0;
   unsigned long long tseg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tl = timing ? clock64() : 0;
-#define SBM(k)                        \
-  if (timing) {                       \
-    const long long t_ = clock64();   \
-    tseg[k] += t_ - tl;               \
-    tl = t_;                          \
+#define SBM(k)                      \
+  if (timing) {                     \
+    const long long t_ = clock64(); \
+    tseg[k] += t_ - tl;             \
+    tl = t_;                        \
   }
-  for (int s = 0; s <= smax; ++s) {
-    // tasks whose anchor column lies in [c0, c1): t = 0 (anchor i) and t ≥ 1 (anchor i + 1 + (t−1)·SB)
-    const bool has0 = !(s & 1) && s / 2 <= n - 3 && s / 2 >= c0 && s / 2 < c1;
-    int tlo = max(max(1, s - 2 * (n - 3)), cdiv(2 * c0 - s - 2 + 2 * SB, 2 * SB - 1));
-    int thi = min(min(s, fdiv(2 * n - 4 - s, 2 * SB - 1)), fdiv(2 * c1 - s - 3 + 2 * SB, 2 * SB - 1));
-    if ((tlo & 1) != (s & 1)) ++tlo;
-    if ((thi & 1) != (s & 1)) --thi;
-    const int ntask = (thi >= tlo ? (thi - tlo) / 2 + 1 : 0) + (has0 ? 1 : 0);
-    for (int idx = warp; idx < ntask; idx += SB2_WARPS) {
-      int i, t;
-      if (has0 && idx == 0) {
-        t = 0;
-        i = s / 2;
-      } else {
-        t = tlo + 2 * (idx - (has0 ? 1 : 0));
-        i = (s - t) / 2;
+  for (int i = g; i <= n - 3; i += W) {
+    const int tmax = (n - 2 - i) / SB;
+    const int tmaxp = (i > 0) ? (n - 1 - i) / SB : 0;  // predecessor's last task
+    double vp[16];
+    double taup = 0.0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) vp[c] = 0.0;
+    for (int t = 0; t <= tmax; ++t) {
+      // ---- wait for task (i−1, t+1) (or the whole predecessor sweep near the end)
+      if (i > 0) {
+        const unsigned need = (unsigned)min(t + 2, tmaxp + 1);
+        if (lane == 0) {
+          while (true) {
+            const unsigned long long pv = dsm_ld_acquire_u64(pred_prog);
+            const unsigned ps = (unsigned)(pv >> 32), pd = (unsigned)pv;
+            if (ps > (unsigned)i || (ps == (unsigned)i && pd >= need)) break;
+            __nanosleep(32);  // keep the spinning warps off the issue slots / LSU of the working ones
+          }
+        }
+        __syncwarp();
       }
+      SBM(0)
       const int stp = i + 1 + (t - 1) * SB;  // C columns (t ≥ 1)
       const int st = (t == 0) ? i + 1 : stp + SB;
       const int ed = min(st + SB - 1, n - 1), len = ed - st + 1;
@@ -432,11 +639,9 @@ __global__ void __launch_bounds__(SB2_NTHREADS, 1) sb2st_kernel(Sb2Args a) {
       const int split = (o0 + 1) * cw;
       const uint32_t b0 = cbase[o0] - (uint32_t)(o0 * cw * SB2_LDB * 8);
       const uint32_t b1 = (o0 + 1 < CS) ? cbase[o0 + 1] - (uint32_t)(split * SB2_LDB * 8) : 0u;
-      // shared::cluster address of band element (column c, d = row − c)
       auto ea = [&](int c, int d) -> uint32_t { return (c < split ? b0 : b1) + (uint32_t)((c * SB2_LDB + d) * 8); };
       double row[16];
       double x = 0.0;
-      SBM(0)
       // ---- load
       if (isC) {
         if (t == 0) {
@@ -454,15 +659,7 @@ __global__ void __launch_bounds__(SB2_NTHREADS, 1) sb2st_kernel(Sb2Args a) {
         }
       }
       SBM(1)
-      if (t > 0) {
-        // ---- (1) C ← C H_p  with the reflector of (i, t−1) from its producer's slot
-        const int pa = (t == 1) ? i : i + 1 + (t - 2) * SB;
-        const uint32_t ps =
-            sbase[pa / cw] + (uint32_t)(((((s - 1) & 1) * SB2_NSLOT + ((t - 1) & (SB2_NSLOT - 1))) * SB2_SLOT) * 8);
-        double vp[16];
-#pragma unroll
-        for (int c = 0; c < 16; ++c) vp[c] = dsm_ld(ps + 8 * c);
-        const double taup = dsm_ld(ps + 8 * SB);
+      if (t > 0) {  // ---- (1) C ← C H_p
         if (isC && taup != 0.0) {
           double p[16];
 #pragma unroll
@@ -530,7 +727,7 @@ __global__ void __launch_bounds__(SB2_NTHREADS, 1) sb2st_kernel(Sb2Args a) {
         }
       }
       SBM(5)
-      // ---- store
+      // ---- store, publish, record
       if (isC) {
         if (t > 0 && r < len) {
 #pragma unroll
@@ -541,27 +738,22 @@ __global__ void __launch_bounds__(SB2_NTHREADS, 1) sb2st_kernel(Sb2Args a) {
         for (int c = 0; c < 16; ++c)
           if (c <= r) dsm_st(ea(st + c, r - c), row[c]);
       }
-      // ---- hand the reflector to (i, t+1) and record it for the back-transform
-      double* slot = slots + (((s & 1) * SB2_NSLOT + (t & (SB2_NSLOT - 1))) * SB2_SLOT);
+      __syncwarp();
+      if (lane == 0) dsm_st_release_u64(my_prog, ((unsigned long long)(i + 1) << 32) | (unsigned)(t + 1));
       const long qi = q2_index(i, t, a.NT);
-      if (isC) {
-        const double vs = (tau != 0.0) ? vmine : 0.0;
-        slot[r] = vs;
-        if (r < len) a.Vq2[qi * SB + r] = vs;
-        if (r == 0) {
-          slot[SB] = tau;
-          a.tq2[qi] = tau;
-        }
-      }
+      const double vs = (tau != 0.0) ? vmine : 0.0;
+      if (isC && r < len) a.Vq2[qi * SB + r] = vs;
+      if (lane == 0) a.tq2[qi] = tau;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) vp[c] = (tau != 0.0) ? v[c] : 0.0;
+      taup = tau;
       SBM(6)
     }
-    SBM(0)
-    cl.sync();
-    SBM(7)
   }
   if (timing)
     for (int k = 0; k < 8; ++k) atomicAdd(a.dbg + (rank * SB2_WARPS + warp) * 8 + k, tseg[k]);
 #undef SBM
+  cl.sync();
   for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
     const double* cc = AB + (long)(c - c0) * SB2_LDB;
     a.d[c] = cc[0];
@@ -570,12 +762,19 @@ __global__ void __launch_bounds__(SB2_NTHREADS, 1) sb2st_kernel(Sb2Args a) {
   cl.sync();
 }
 
-static int sb2_cluster(int n) { return std::max(1, std::min(16, (n + 127) / 128)); }
+static int sb2_cluster(int n) {
+  static const int forced = [] {
+    const char* e = std::getenv("KOT_SB2_CS");  // diagnostic override
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced > 0) return std::min(16, forced);
+  return std::max(1, std::min(16, (n + 127) / 128));
+}
 
 static void sb2st(int n, EigWork& w, cudaStream_t st) {
   const int cs = sb2_cluster(n);
   const int cw = (n + cs - 1) / cs;
-  const size_t smem = sizeof(double) * ((size_t)cw * SB2_LDB + 2 * SB2_NSLOT * SB2_SLOT);
+  const size_t smem = sizeof(double) * ((size_t)cw * SB2_LDB);
   kot_require(smem <= 220 * 1024, KOT_EINVAL, "matrix order too large for the bulge-chasing cluster");
   static size_t smem_set = 0;
   if (smem > smem_set) {
@@ -604,6 +803,7 @@ static void sb2st(int n, EigWork& w, cudaStream_t st) {
 }
 
 void two_stage_tridiag(const double* Z, int n, EigWork& w, cudaStream_t st) {
+  w.ensure_two_stage();
   {
     ProfScope ps("eig.sy2sb", st, 4.0 / 3.0 * n * (double)n * n);
     sy2sb(Z, n, w, st);
@@ -777,6 +977,20 @@ extern "C" int kot_debug_sb2st_timing(int on, unsigned long long* out8) {
     cudaMemcpy(out8, g_sb2_dbg, 16 * 8 * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     cudaFree(g_sb2_dbg);
     g_sb2_dbg = nullptr;
+  }
+  return 0;
+}
+
+extern "C" int kot_debug_pqr_timing(int on, unsigned long long* out8) {
+  using namespace kot;
+  if (on) {
+    if (!g_pqr_dbg && cudaMalloc(&g_pqr_dbg, 8 * sizeof(unsigned long long)) != cudaSuccess) return 6;
+    cudaMemset(g_pqr_dbg, 0, 8 * sizeof(unsigned long long));
+  } else if (g_pqr_dbg) {
+    cudaDeviceSynchronize();
+    cudaMemcpy(out8, g_pqr_dbg, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaFree(g_pqr_dbg);
+    g_pqr_dbg = nullptr;
   }
   return 0;
 }

@@ -34,6 +34,7 @@ struct EigWork {
   void* dbuf = nullptr;
   int* hbuf = nullptr;
   explicit EigWork(int n);
+  void ensure_two_stage();
   ~EigWork();
   EigWork(const EigWork&) = delete;
   EigWork& operator=(const EigWork&) = delete;
@@ -47,7 +48,7 @@ long two_stage_q2_size(int n);
 long two_stage_t_size(int n);
 void two_stage_tridiag(const double* Z, int n, EigWork& w, cudaStream_t st);
 void two_stage_q2_apply(int n, EigWork& w, double* P, cudaStream_t st);  // P ← Q2 P
-bool use_two_stage(int n);
+bool use_two_stage(int n, int lane);
 // tridiagonal form only (debug/tests): stages = 1 (one-stage sytrd) or 2
 void tridiag_device(const double* Z, int n, EigWork& w, cudaStream_t st, int stages);
 void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigWork& w, cudaStream_t st,

@@ -537,3 +537,37 @@ def test_tridiagonal_form_preserves_spectrum(n, stages):
     ref = np.linalg.eigvalsh(z)
     got = np.linalg.eigvalsh(t)
     assert np.max(np.abs(got - ref)) <= 1e-12 * np.abs(ref).max() * max(1.0, n / 100), (n, stages)
+
+
+@pytest.fixture
+def two_stage():
+    from paper_2310_14087_b200 import _lib
+    f = _lib.lib().kot_debug_eig_stages
+    f(2)
+    yield
+    f(1)
+
+
+@pytest.mark.parametrize("n", [64, 65, 300, 1100])
+def test_two_stage_sym_eig(two_stage, n):
+    """Full eigendecomposition through the two-stage reduction (+ Q2, Q1 back-transforms)."""
+    rng = np.random.default_rng(100 + n)
+    z = random_symmetric(rng, n)
+    dc = GL.sym_eig(z)
+    ref = np.sort(np.linalg.eigvalsh(z))[::-1]
+    scale = np.abs(ref).max()
+    assert np.max(np.abs(dc.eigvals - ref)) <= 1e-13 * scale * max(1.0, n / 100)
+    p = dc.eigvecs
+    assert np.linalg.norm(p.T @ p - np.eye(n)) <= 1e-12 * n
+    assert np.linalg.norm(p @ np.diag(dc.eigvals) @ p.T - z) <= 1e-13 * scale * n
+
+
+def test_two_stage_residual_and_middle_operator(two_stage, cfg1):
+    pd = gpu_pd(cfg1)
+    po = oracle_pd(cfg1)
+    w = GP.IteratePair(cfg1["op_g"], cfg1["op_x"])
+    out, mu = GN.middle_operator_at(pd, w, float(cfg1["op_theta"]), cfg1["op_v"])
+    assert rel(out, cfg1["op_middle"]) <= 1e-11
+    r, dc = O.residual_parts(po, O.Pair(cfg1["op_g"], cfg1["op_x"]))
+    rg, _ = GP.residual_parts(pd, w)
+    assert rel(rg.gamma, r.g) <= 1e-11 and rel(rg.x_mat, r.x) <= 1e-11

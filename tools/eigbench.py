@@ -57,3 +57,12 @@ if f is not None:
     w = np.unravel_index(np.argmax(busy), busy.shape)
     for k, nm in enumerate(names):
         print(f"  sb2st busiest warp {w}: {nm:18s} {a[w[0], w[1], k]/1e6:9.3f} Mcyc")
+f = getattr(L, "kot_debug_pqr_timing", None)
+if f is not None:
+    b3 = (C.c_ulonglong * 8)()
+    f(1, b3)
+    linalg.sym_eig(z)
+    f(0, b3)
+    names = ["load+prologue", "sync#1", "gather+house", "dots", "sync#2", "gather+update", "next norm", "T+out+sync"]
+    for nm, v in zip(names, b3):
+        print(f"  panel {nm:16s} {v / 1e6:8.3f} Mcyc  ({v / max(1, (n // 16)) / 16:8.1f} cyc/col)")
