@@ -868,17 +868,22 @@ __global__ void __launch_bounds__(32 * QL_WARPS) q2_larft_kernel(const double* _
 // One wave of the Q2 back-transform.  Groups G(I, t) with t − I = wave touch
 // disjoint row windows (tools/twostage_proto.py: apply_q2_waves), so a wave is a
 // batch of independent (I − V T Vᵀ) updates: blockIdx.y picks the group,
-// blockIdx.x a 64-column tile of P.
+// blockIdx.x a 64-column tile of P.  The three products (Y = VᵀW, Y ← T Y,
+// W −= V Y) run on the FP64 tensor cores (mma m8n8k4), with K ranges cut to the
+// band of V and the upper triangle of T.
 constexpr int QW_COLS = 64;
-constexpr int QW_LD = QW_COLS + 1;
-constexpr int QW_SMEM = QG_ROWS * QW_LD * 8;
+constexpr int QW_RW = 48;                 // window rows incl. zero padding (≥ QG_ROWS)
+constexpr int QW_LDW = QW_COLS + 4;       // stride ≡ 4 (mod 16) doubles
+constexpr int QW_LDV = QG + 4;
+constexpr int QW_SMEM = (QW_RW * QW_LDW + QW_RW * QW_LDV + QG * QW_LDV + 2 * QG * QW_LDW) * 8;
 __global__ void __launch_bounds__(256) q2_wave_kernel(double* P, int n, const double* __restrict__ Vq2,
                                                       const double* __restrict__ Tq2, int NT, int wave, int Ilo) {
-  extern __shared__ double qw_dyn[];
-  double (*W)[QW_LD] = reinterpret_cast<double (*)[QW_LD]>(qw_dyn);  // [QG_ROWS][QW_LD]
-  __shared__ double Y[QG][QW_LD];
-  __shared__ double Vw[QG][SB + 1];
-  __shared__ double T[QG][QG + 1];
+  extern __shared__ double qw[];
+  double* W = qw;                        // [QW_RW][QW_LDW]
+  double* Vd = W + QW_RW * QW_LDW;       // [QW_RW][QW_LDV]: Vd[ρ][j] = v_j[ρ − j]
+  double* T = Vd + QW_RW * QW_LDV;       // [QG][QW_LDV]
+  double* Y = T + QG * QW_LDV;           // [QG][QW_LDW]
+  double* Y2 = Y + QG * QW_LDW;          // [QG][QW_LDW]
   const int I = Ilo + blockIdx.y;
   const int t = wave + I;
   const int ilo = I * QG;
@@ -887,57 +892,66 @@ __global__ void __launch_bounds__(256) q2_wave_kernel(double* P, int n, const do
   const int c0 = blockIdx.x * QW_COLS;
   const int wc = min(QW_COLS, n - c0);
   const int tid = threadIdx.x;
-  for (int e = tid; e < nr * QW_COLS; e += 256) {
+  for (int e = tid; e < QW_RW * QW_COLS; e += 256) {
     const int rr = e / QW_COLS, c = e % QW_COLS;
-    W[rr][c] = (c < wc) ? P[(long)(r0 + rr) * n + c0 + c] : 0.0;
+    W[rr * QW_LDW + c] = (rr < nr && c < wc) ? P[(long)(r0 + rr) * n + c0 + c] : 0.0;
   }
-  for (int e = tid; e < QG * SB; e += 256) {
-    const int jj = e / SB, q = e % SB, i = ilo + jj;
-    Vw[jj][q] = (i <= n - 3) ? __ldg(q2_vec(Vq2, i, t, NT) + q) : 0.0;
+  for (int e = tid; e < QW_RW * QG; e += 256) {
+    const int rho = e / QG, jj = e % QG, q = rho - jj, i = ilo + jj;
+    Vd[rho * QW_LDV + jj] = (q >= 0 && q < SB && i <= n - 3 && rho < nr) ? __ldg(q2_vec(Vq2, i, t, NT) + q) : 0.0;
   }
   const double* Tg = Tq2 + ((long)I * NT + t) * QG * QG;
-  for (int e = tid; e < QG * QG; e += 256) T[e / QG][e % QG] = __ldg(Tg + e);
+  for (int e = tid; e < QG * QG; e += 256) T[(e / QG) * QW_LDV + e % QG] = __ldg(Tg + e);
   __syncthreads();
-  // thread → (row j, columns cb + 8u): lanes of a warp read consecutive doubles
-  const int jj = tid >> 3, cb = tid & 7;
-  // Y = Vᵀ W
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
+  // ---- Y = Vᵀ W: warp → row tile jt = warp/2, column tiles 4·(warp%2) .. +3
   {
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int q = 0; q < SB && jj + q < nr; ++q) {
-      const double v = Vw[jj][q];
+    const int jt = warp >> 1, ct0 = (warp & 1) * 4;
+    double acc[4][2] = {};
+    const int kb = 8 * jt, ke = min(QW_RW, 8 * jt + 8 + SB - 1);
+    for (int k0 = kb; k0 < ke; k0 += 4) {
+      const double a = Vd[(k0 + tq) * QW_LDV + jt * 8 + g];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc[u] += v * W[jj + q][cb + 8 * u];
+      for (int u = 0; u < 4; ++u) dmma(acc[u][0], acc[u][1], a, W[(k0 + tq) * QW_LDW + (ct0 + u) * 8 + g]);
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) Y[jj][cb + 8 * u] = acc[u];
+    for (int u = 0; u < 4; ++u) {
+      Y[(jt * 8 + g) * QW_LDW + (ct0 + u) * 8 + 2 * tq] = acc[u][0];
+      Y[(jt * 8 + g) * QW_LDW + (ct0 + u) * 8 + 2 * tq + 1] = acc[u][1];
+    }
   }
   __syncthreads();
-  // Y ← T Y (upper triangular)
+  // ---- Y2 = T Y  (T upper triangular: K from the row tile on)
   {
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int l = jj; l < QG; ++l) {
-      const double tv = T[jj][l];
+    const int jt = warp >> 1, ct0 = (warp & 1) * 4;
+    double acc[4][2] = {};
+    for (int k0 = 8 * jt; k0 < QG; k0 += 4) {
+      const double a = T[(jt * 8 + g) * QW_LDV + k0 + tq];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc[u] += tv * Y[l][cb + 8 * u];
+      for (int u = 0; u < 4; ++u) dmma(acc[u][0], acc[u][1], a, Y[(k0 + tq) * QW_LDW + (ct0 + u) * 8 + g]);
     }
-    __syncthreads();
 #pragma unroll
-    for (int u = 0; u < 8; ++u) Y[jj][cb + 8 * u] = acc[u];
+    for (int u = 0; u < 4; ++u) {
+      Y2[(jt * 8 + g) * QW_LDW + (ct0 + u) * 8 + 2 * tq] = acc[u][0];
+      Y2[(jt * 8 + g) * QW_LDW + (ct0 + u) * 8 + 2 * tq + 1] = acc[u][1];
+    }
   }
   __syncthreads();
-  // W −= V Y: row ρ gets Σ_{j ∈ [ρ−SB+1, ρ]} v_j[ρ − j] Y[j]
-  for (int e = tid; e < nr * 8; e += 256) {
-    const int rho = e >> 3, cc = e & 7;
-    const int jlo = max(0, rho - SB + 1), jhi = min(QG - 1, rho);
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int j = jlo; j <= jhi; ++j) {
-      const double v = Vw[j][rho - j];
+  // ---- W −= V Y2: warp → column tile ct = warp, row tiles 0..5 (K = j ∈ [8ρt − SB + 1, 8ρt + 7])
+  {
+    const int ct = warp;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc[u] += v * Y[j][cc + 8 * u];
+    for (int pt = 0; pt < QW_RW / 8; ++pt) {
+      double acc0 = 0.0, acc1 = 0.0;
+      const int kb = max(0, (8 * pt - SB + 1) & ~3), ke = min(QG, 8 * pt + 8);
+      for (int k0 = kb; k0 < ke; k0 += 4)
+        dmma(acc0, acc1, Vd[(pt * 8 + g) * QW_LDV + k0 + tq], Y2[(k0 + tq) * QW_LDW + ct * 8 + g]);
+      const int rho = pt * 8 + g, c = ct * 8 + 2 * tq;
+      if (rho < nr) {
+        if (c < wc) P[(long)(r0 + rho) * n + c0 + c] = W[rho * QW_LDW + c] - acc0;
+        if (c + 1 < wc) P[(long)(r0 + rho) * n + c0 + c + 1] = W[rho * QW_LDW + c + 1] - acc1;
+      }
     }
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (cc + 8 * u < wc) P[(long)(r0 + rho) * n + c0 + cc + 8 * u] = W[rho][cc + 8 * u] - acc[u];
   }
 }
 
