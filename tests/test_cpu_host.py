@@ -298,3 +298,38 @@ def test_row_block_decomposition_of_middle_operator(n_pos):
             r0, r1 = row_block(n, g, world)
             y[r0:r1] = np.einsum("ia,ab,ib->i", b[r0:r1], t, b[r0:r1])
         assert np.allclose(y, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
+def _uid_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2310_14087_b200 import rowshard
+    obj = [rowshard.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)  # what rowshard.shard_rows does before kot_problem_shard
+    q.put((rank, obj[0], rowshard.row_block(8192, rank, world)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_nccl_unique_id_broadcast_gloo():
+    """Rank 0's 128-byte ncclUniqueId (libkotgpu dlopens NCCL; no GPU needed) reaches every rank."""
+    from paper_2310_14087_b200 import rowshard
+    try:
+        rowshard.unique_id()
+    except Exception as exc:  # libnccl absent in this environment
+        pytest.skip(f"NCCL unavailable: {exc}")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_uid_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=120) for _ in range(2)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert len(got[0][1]) == 128 and got[0][1] == got[1][1]
+    assert got[0][2] == (0, 4096) and got[1][2] == (4096, 8192)
