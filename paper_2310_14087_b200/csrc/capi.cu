@@ -245,8 +245,8 @@ int kot_problem_shard_info(const kot_problem* h, int* rank, int* world, int* row
 namespace {
 struct DevBuf {
   double* p = nullptr;
-  explicit DevBuf(long count) { KOT_CUDA(cudaMalloc(&p, std::max(count, 1L) * sizeof(double))); }
-  ~DevBuf() { cudaFree(p); }
+  explicit DevBuf(long count) : p(static_cast<double*>(kot::dev_alloc(std::max(count, 1L) * sizeof(double)))) {}
+  ~DevBuf() { kot::dev_free(p); }
 };
 }  // namespace
 

@@ -77,6 +77,17 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 
 inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
 
+// Device / pinned-host allocations of the library (alloc.cu).  Device memory
+// comes from the device's stream-ordered pool with a high release threshold and
+// pinned host buffers from a size-keyed free list, so creating a problem or an
+// execution context after the first one costs no cudaMalloc/cudaFree (and no
+// implicit device synchronisation) — this is what keeps solve()'s end-to-end
+// time close to the device time.  Callers free only after their streams are idle.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p);
+void* host_alloc_pinned(size_t bytes);
+void host_free_pinned(void* p, size_t bytes);
+
 constexpr int kNumSMs = 148;
 
 }  // namespace kot

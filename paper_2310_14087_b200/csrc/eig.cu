@@ -46,7 +46,7 @@ constexpr double DEPS = DBL_EPSILON * 0.5;  // LAPACK dlamch('E')
 
 EigWork::EigWork(int n_) : n(n_) {
   const long nn = (long)n * n;
-  auto alloc = [&](double** p, long cnt) { KOT_CUDA(cudaMalloc(p, std::max(cnt, 1L) * sizeof(double))); };
+  auto alloc = [&](double** p, long cnt) { *p = static_cast<double*>(dev_alloc(std::max(cnt, 1L) * sizeof(double))); };
   alloc(&A, nn);
   alloc(&Vall, nn);
   alloc(&X, (long)n * 3 * TRD_NB);
@@ -58,8 +58,7 @@ EigWork::EigWork(int n_) : n(n_) {
   alloc(&part, (long)kNumSMs * TRD_PSTRIDE);
   alloc(&partn, kNumSMs);
   alloc(&gpart, (long)TRD_PSTRIDE * TRD_NGRP);
-  KOT_CUDA(cudaMalloc(&gcnt, sizeof(int) * TRD_NGRP));
-  KOT_CUDA(cudaMemset(gcnt, 0, sizeof(int) * TRD_NGRP));
+  gcnt = static_cast<int*>(dev_alloc(sizeof(int) * TRD_NGRP));
   alloc(&Tf, 256L * 256 * 2);
   alloc(&W1, 256L * n * 2);
   splitws_cap = 16L * 256 * n;
@@ -78,15 +77,15 @@ EigWork::EigWork(int n_) : n(n_) {
   alloc(&dfv, n);
   alloc(&rotcs, 2L * n);
   alloc(&rho, n);
-  KOT_CUDA(cudaMalloc(&ibuf, sizeof(int) * (8L * n + 64)));
-  KOT_CUDA(cudaMalloc(&dbuf, 16L * n + 4096 + 64L * n));
-  KOT_CUDA(cudaMallocHost(&hbuf, sizeof(int) * (12L * n + 512)));
+  ibuf = static_cast<int*>(dev_alloc(sizeof(int) * (8L * n + 64)));
+  dbuf = dev_alloc(16L * n + 4096 + 64L * n);
+  hbuf = static_cast<int*>(host_alloc_pinned(sizeof(int) * (12L * n + 512)));
 }
 
 // two-stage buffers on first use (the default one-stage path never touches them)
 void EigWork::ensure_two_stage() {
   if (Vq2 || n < 3) return;
-  auto alloc = [&](double** p, long cnt) { KOT_CUDA(cudaMalloc(p, std::max(cnt, 1L) * sizeof(double))); };
+  auto alloc = [&](double** p, long cnt) { *p = static_cast<double*>(dev_alloc(std::max(cnt, 1L) * sizeof(double))); };
   const long q2 = two_stage_q2_size(n);
   alloc(&Vq2, q2);
   alloc(&Tq2, two_stage_t_size(n));
@@ -96,11 +95,11 @@ void EigWork::ensure_two_stage() {
 EigWork::~EigWork() {
   for (double* p : {A, Vall, X, d, e, tau, xv, yv, part, partn, Tf, W1, Q, Qw, Qnd, Dl, Uw, zs, ds, dlam, wv, what, lam,
                     dfv, rotcs, rho, splitws, gpart, Vq2, Tq2, tq2})
-    cudaFree(p);
-  cudaFree(gcnt);
-  cudaFree(ibuf);
-  cudaFree(dbuf);
-  cudaFreeHost(hbuf);
+    dev_free(p);
+  dev_free(gcnt);
+  dev_free(ibuf);
+  dev_free(dbuf);
+  host_free_pinned(hbuf, sizeof(int) * (12L * n + 512));
 }
 
 // ================================================================= sytrd
@@ -1399,12 +1398,13 @@ static int sytrd_coresident_cap(int n) {
 // kot_debug_eig_stages) selects the two-stage reduction.
 static int g_eig_stages = -1;  // −1: read KOT_EIG_STAGES once
 bool use_two_stage(int n, int lane) {
-  (void)lane;
   if (g_eig_stages < 0) {
     const char* e = std::getenv("KOT_EIG_STAGES");
     g_eig_stages = e ? std::atoi(e) : 1;
   }
-  return g_eig_stages == 2 && n >= 3;
+  if (n < 3) return false;
+  // 3: hybrid — background (lane ≠ 0) eigensolves two-stage, the Newton chain one-stage
+  return g_eig_stages == 2 || (g_eig_stages == 3 && lane != 0);
 }
 
 static void one_stage_tridiag(const double* Z, int n, EigWork& w, cudaStream_t st, int lane) {
@@ -1470,6 +1470,6 @@ extern "C" int kot_debug_sytrd_timing(int on, unsigned long long* out8) {
 
 // test hook: 1 = one-stage, 2 = two-stage tridiagonalisation for subsequent eigensolves
 extern "C" int kot_debug_eig_stages(int stages) {
-  kot::g_eig_stages = (stages == 2) ? 2 : 1;
+  kot::g_eig_stages = (stages == 2 || stages == 3) ? stages : 1;
   return 0;
 }

@@ -24,8 +24,7 @@ namespace kot {
 // ---------------------------------------------------------------- Problem
 
 double* Problem::alloc(long count) {
-  double* p = nullptr;
-  KOT_CUDA(cudaMalloc(&p, std::max(count, 1L) * sizeof(double)));
+  double* p = static_cast<double*>(dev_alloc(std::max(count, 1L) * sizeof(double)));
   owned.push_back(p);
   return p;
 }
@@ -43,10 +42,10 @@ void Problem::init_scratch() {
   splitws_cap = 16L * 256 * n;
   splitws = alloc(splitws_cap);
   dsc = alloc(64);
-  KOT_CUDA(cudaMallocHost(&hsc, 64 * sizeof(double)));
-  KOT_CUDA(cudaMalloc(&dk, 16 * sizeof(int)));
+  hsc = static_cast<double*>(host_alloc_pinned(64 * sizeof(double)));
+  dk = static_cast<int*>(dev_alloc(16 * sizeof(int)));
   dflag = dk + 8;
-  KOT_CUDA(cudaMallocHost(&hk, 16 * sizeof(int)));
+  hk = static_cast<int*>(host_alloc_pinned(16 * sizeof(int)));
   eig.reset(new EigWork(n));
 }
 
@@ -61,10 +60,10 @@ Problem::~Problem() {
   aux_.reset();
   aux2_.reset();
   eig.reset();
-  for (double* p : owned) cudaFree(p);
-  if (hsc) cudaFreeHost(hsc);
-  if (dk) cudaFree(dk);
-  if (hk) cudaFreeHost(hk);
+  for (double* p : owned) dev_free(p);
+  host_free_pinned(hsc, 64 * sizeof(double));
+  dev_free(dk);
+  host_free_pinned(hk, 16 * sizeof(int));
   if (st) cudaStreamDestroy(st);
 }
 
