@@ -401,18 +401,25 @@ __global__ void set_last_diag_kernel(const double* A, int n, double* d) { d[n - 
 
 unsigned long long* g_trd_dbg = nullptr;  // set by kot_debug_sytrd_timing
 
-// CTAs of the cooperative panel kernel (≤ one per SM).  KOT_TRD_GRID lowers it
-// (diagnostic: fewer SMs per eigensolve, more eigensolves co-resident).
-static int trd_grid_cap() {
-  static const int cap = [] {
-    const char* e = std::getenv("KOT_TRD_GRID");
-    const int v = e ? std::atoi(e) : 0;
-    return v > 0 ? std::min(v, kNumSMs) : kNumSMs;
-  }();
-  return cap;
+// CTAs of the cooperative panel kernel (≤ one per SM).  The latency-critical
+// caller (lane 0, Newton chain) uses every SM; background eigensolves (lane 1,
+// EG pipeline) use KOT_TRD_GRID_BG CTAs so that they leave SMs to the Newton
+// chain's kernels.  KOT_TRD_GRID caps both (diagnostic).
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  const int v = e ? std::atoi(e) : 0;
+  return v > 0 ? v : dflt;
+}
+static int trd_grid_cap(int lane) {
+  static const int cap = std::min(env_int("KOT_TRD_GRID", kNumSMs), kNumSMs);
+  static const int cap_bg = std::min(env_int("KOT_TRD_GRID_BG", 48), cap);  // measured best (probe cfg3: 148 → 7.2, 74 → 7.7, 48 → 7.9, 32 → 7.8 it/s)
+  return lane == 0 ? cap : cap_bg;
+}
+static int trd_grid(int rows, int lane) {
+  return std::max(1, std::min(trd_grid_cap(lane), ceil_div(rows, TRD_WARPS)));
 }
 
-static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st) {
+static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane) {
   KOT_CUDA(cudaMemcpyAsync(w.A, Z, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
   KOT_CUDA(cudaMemsetAsync(w.Vall, 0, sizeof(double) * n * n, st));
   static int smem_set_for = 0;
@@ -420,7 +427,7 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st) {
     const int nb = std::min(TRD_NB, n - 1 - p0);
     KOT_CUDA(cudaMemsetAsync(w.X, 0, sizeof(double) * n * 3 * TRD_NB, st));
     const int rows = n - p0;
-    const int G = std::max(1, std::min(trd_grid_cap(), ceil_div(rows, TRD_WARPS)));
+    const int G = trd_grid(rows, lane);
     kot_require((long)G * TRD_WARPS * TRD_RPW >= rows, KOT_EINVAL, "matrix order too large for sytrd");
     TrdArgs args{w.A, n, p0, nb, w.X, w.Vall, w.d, w.e, w.tau, w.xv, w.yv, w.part, w.partn, g_trd_dbg,
                  w.gpart, w.gcnt};
@@ -1349,44 +1356,39 @@ __global__ void eig1_kernel(const double* Z, double* P, double* vals) {
 
 // Cooperative sytrd grids from different streams/host threads must never need
 // more co-resident CTAs than the SMs can hold at once (their blocks spin on a
-// grid barrier).  This process-wide gate admits at most `cap` concurrent
-// sytrd calls, cap = co-resident panel CTAs per SM for this n.
+// grid barrier).  This process-wide gate accounts CTA slots (occupancy × SMs):
+// a grid is admitted when its CTAs fit, and background grids (lane ≠ 0) may
+// only use what is left after reserving one full lane-0 grid, so a Newton-chain
+// eigensolve never queues behind the EG pipeline.
 namespace {
 std::mutex g_coop_mu;
 std::condition_variable g_coop_cv;
-int g_coop_active = 0, g_coop_bg = 0;
-// Background (lane 1) callers may hold at most cap−1 slots, so a lane-0
-// (Newton-chain) eigensolve never queues behind the EG pipeline.
+int g_coop_used = 0;
 struct CoopGate {
-  int lane;
-  CoopGate(int cap, int lane_) : lane(lane_) {
+  int slots;
+  CoopGate(int total, int want, int reserve, int lane) : slots(want) {
     std::unique_lock<std::mutex> lk(g_coop_mu);
-    if (lane == 0 || cap < 2)
-      g_coop_cv.wait(lk, [&] { return g_coop_active < cap; });
-    else
-      g_coop_cv.wait(lk, [&] { return g_coop_active < cap && g_coop_bg < cap - 1; });
-    ++g_coop_active;
-    if (lane != 0) ++g_coop_bg;
+    const int limit = (lane == 0) ? total : total - reserve;
+    g_coop_cv.wait(lk, [&] { return g_coop_used + want <= limit || g_coop_used == 0; });
+    g_coop_used += want;
   }
   ~CoopGate() {
     {
       std::lock_guard<std::mutex> lk(g_coop_mu);
-      --g_coop_active;
-      if (lane != 0) --g_coop_bg;
+      g_coop_used -= slots;
     }
     g_coop_cv.notify_all();
   }
 };
 }  // namespace
 
-static int sytrd_coresident_cap(int n) {
+static int sytrd_per_sm(int n) {
   const size_t smem = sizeof(double) * (std::max(n, 1) + 3L * TRD_WARPS * TRD_RPW * TRD_NB);
   if (smem > 48 * 1024)
     KOT_CUDA(cudaFuncSetAttribute(sytrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   KOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sytrd_panel_kernel, TRD_THREADS, smem));
-  const int g = std::max(1, std::min(trd_grid_cap(), ceil_div(n, TRD_WARPS)));
-  return std::max(1, per_sm * kNumSMs / g);
+  return std::max(1, per_sm);
 }
 
 // Which tridiagonalisation an eigensolve uses.  Measured on B200 (eigbench,
@@ -1409,8 +1411,9 @@ bool use_two_stage(int n, int lane) {
 
 static void one_stage_tridiag(const double* Z, int n, EigWork& w, cudaStream_t st, int lane) {
   ProfScope ps("eig.sytrd", st, 4.0 / 3.0 * n * (double)n * n);
-  CoopGate gate(sytrd_coresident_cap(n), lane);
-  sytrd(Z, n, w, st);
+  const int total = sytrd_per_sm(n) * kNumSMs;
+  CoopGate gate(total, trd_grid(n, lane), trd_grid(n, 0), lane);
+  sytrd(Z, n, w, st, lane);
   KOT_CUDA(cudaStreamSynchronize(st));  // the gate is held until the grids have retired
 }
 
