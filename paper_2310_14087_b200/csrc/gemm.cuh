@@ -26,7 +26,13 @@ namespace kot {
 #ifndef KOT_GEMM_BK
 #define KOT_GEMM_BK 8
 #endif
-constexpr int GB_M = 64, GB_N = 64, GB_K = KOT_GEMM_BK, G_STAGES = KOT_GEMM_STAGES, G_THREADS = 128;
+#ifndef KOT_GEMM_WARPS
+#define KOT_GEMM_WARPS 4
+#endif
+constexpr int GB_M = 64, GB_N = 64, GB_K = KOT_GEMM_BK, G_STAGES = KOT_GEMM_STAGES;
+// warps split the 64×64 tile 2 ways along N; along M into G_WARPS/2 strips of G_WM rows
+constexpr int G_WARPS = KOT_GEMM_WARPS, G_THREADS = 32 * G_WARPS;
+constexpr int G_WM = GB_M / (G_WARPS / 2), G_MI = G_WM / 8;
 constexpr int G_PADK = GB_K + 4;  // stride ≡ 4 (mod 16) doubles → conflict-free fragment loads
 constexpr int G_PADM = GB_M + 4;
 constexpr int G_PADN = GB_N + 4;
@@ -153,11 +159,11 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp >> 1) * G_WM, wn = (warp & 1) * 32;
 
-  double acc[4][4][2];
+  double acc[G_MI][4][2];
 #pragma unroll
-  for (int i = 0; i < 4; i++)
+  for (int i = 0; i < G_MI; i++)
 #pragma unroll
     for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
@@ -199,10 +205,10 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
     const double* ks = Ks + stage * GB_K;
 #pragma unroll
     for (int kk = 0; kk < GB_K; kk += 4) {
-      double a[4], b[4];
+      double a[G_MI], b[4];
       const double kscl = (s.kscale != nullptr) ? ks[kk + t] : 1.0;
 #pragma unroll
-      for (int i = 0; i < 4; i++) {
+      for (int i = 0; i < G_MI; i++) {
         const int m = wm + i * 8 + g;
         a[i] = (TA ? as[(kk + t) * G_PADM + m] : as[m * G_PADK + kk + t]) * kscl;
       }
@@ -212,7 +218,7 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
         b[j] = TB ? bs[n * G_PADK + kk + t] : bs[(kk + t) * G_PADN + n];
       }
 #pragma unroll
-      for (int i = 0; i < 4; i++)
+      for (int i = 0; i < G_MI; i++)
 #pragma unroll
         for (int j = 0; j < 4; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
@@ -224,7 +230,7 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
     __syncthreads();
     double* red = gsm;  // reuse: [2][GB_M]
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
+    for (int i = 0; i < G_MI; i++) {
       const int r = m0 + wm + i * 8 + g;
       double p = 0.0;
 #pragma unroll
@@ -239,14 +245,14 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
       if (t == 0) red[(warp & 1) * GB_M + wm + i * 8 + g] = p;
     }
     __syncthreads();
-    if (threadIdx.x < GB_M) {
-      const int r = m0 + threadIdx.x;
-      if (r < s.M) epi.rowdot_store(tn, r, red[threadIdx.x] + red[GB_M + threadIdx.x]);
+    for (int q = threadIdx.x; q < GB_M; q += G_THREADS) {
+      const int r = m0 + q;
+      if (r < s.M) epi.rowdot_store(tn, r, red[q] + red[GB_M + q]);
     }
   } else if (s.ksplit > 1) {
     double* ws = s.ws + (long)blockIdx.y * s.M * s.N;
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
+    for (int i = 0; i < G_MI; i++) {
       const int r = m0 + wm + i * 8 + g;
       if (r >= s.M) continue;
 #pragma unroll
@@ -259,7 +265,7 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
+    for (int i = 0; i < G_MI; i++) {
       const int r = m0 + wm + i * 8 + g;
       if (r >= s.M) continue;
 #pragma unroll
