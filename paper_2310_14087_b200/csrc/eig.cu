@@ -416,7 +416,9 @@ static int trd_grid_cap(int lane) {
   return lane == 0 ? cap : cap_bg;
 }
 static int trd_grid(int rows, int lane) {
-  return std::max(1, std::min(trd_grid_cap(lane), ceil_div(rows, TRD_WARPS)));
+  // never below what the per-warp row capacity needs (TRD_RPW rows per warp)
+  const int need = ceil_div(rows, TRD_WARPS * TRD_RPW);
+  return std::max(need, std::max(1, std::min(trd_grid_cap(lane), ceil_div(rows, TRD_WARPS))));
 }
 
 static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane) {
