@@ -229,39 +229,44 @@ __global__ void __launch_bounds__(PQR_THREADS) sy2sb_panel_kernel(double* A, int
 #undef PQM
 }
 
-// Xw = A22 V for a 32-row block and one K-split (partial), plus the partial
-// S = V[rows]ᵀ Xw_partial[rows]; both reduced in fixed order by sy2sb_w_kernel.
-// A22 and V chunks stream through a 2-stage cp.async pipeline (8-byte copies:
-// A22 rows need not be 16-byte aligned).
-constexpr int XW_ROWS = 32;
-constexpr int XW_KC = 48;
-__global__ void __launch_bounds__(256) sy2sb_xw_kernel(const double* __restrict__ A22, int lda, int m,
+// Xw = A22 V for a 64-row block and one K-split (partial) on the FP64 tensor cores
+// (mma m8n8k4; 4 warps × 2×2 8×8 tiles), plus the partial S = V[rows]ᵀ Xw_partial[rows];
+// both reduced in fixed order afterwards.  A22 and V chunks stream through a 2-stage
+// cp.async pipeline (8-byte copies: A22 rows need not be 16-byte aligned).
+constexpr int XW_ROWS = 64;
+constexpr int XW_KC = 32;
+constexpr int XW_LDA = XW_KC + 4;
+constexpr int XW_LDV = SB + 4;
+__global__ void __launch_bounds__(128) sy2sb_xw_kernel(const double* __restrict__ A22, int lda, int m,
                                                        const double* __restrict__ X0, double* Xwp,
                                                        double* Spart) {
-  __shared__ double Ak[2][XW_ROWS][XW_KC + 1];
-  __shared__ double Vk[2][XW_KC][SB + 1];
-  __shared__ double Xo[XW_ROWS][SB + 1];
+  __shared__ double Ak[2][XW_ROWS][XW_LDA];
+  __shared__ double Vk[2][XW_KC][XW_LDV];
+  // after the K loop the A stages are reused for the Xw tile and the V rows
+  double (*Xo)[SB + 1] = reinterpret_cast<double (*)[SB + 1]>(&Ak[0][0][0]);
+  double (*Vr)[SB + 1] = reinterpret_cast<double (*)[SB + 1]>(&Ak[0][0][0] + XW_ROWS * (SB + 1));
   const int tid = threadIdx.x;
   const int rb = blockIdx.x * XW_ROWS;
   const int ks = gridDim.y, kid = blockIdx.y;
   const int kchunk = ((m + ks - 1) / ks + XW_KC - 1) / XW_KC * XW_KC;
   const int k0 = kid * kchunk, k1 = min(m, k0 + kchunk);
-  const int r = tid >> 3, cg0 = tid & 7;
   auto issue = [&](int kb, int buf) {
     const int kn = min(XW_KC, k1 - kb);
-    for (int e = tid; e < XW_ROWS * XW_KC; e += 256) {
+    for (int e = tid; e < XW_ROWS * XW_KC; e += 128) {
       const int rr = e / XW_KC, kk = e % XW_KC;
       const bool ok = rb + rr < m && kk < kn;
       cp_async_8(&Ak[buf][rr][kk], ok ? A22 + (long)(rb + rr) * lda + kb + kk : A22, ok ? 8 : 0);
     }
-    for (int e = tid; e < XW_KC * SB; e += 256) {
+    for (int e = tid; e < XW_KC * SB; e += 128) {
       const int kk = e / SB, c = e % SB;
       const bool ok = kk < kn;
       cp_async_8(&Vk[buf][kk][c], ok ? X0 + (long)(kb + kk) * SB_LDX + c : X0, ok ? 8 : 0);
     }
     cp_async_commit();
   };
-  double acc0 = 0.0, acc1 = 0.0;
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
+  const int rt0 = warp * 2;  // row tiles rt0, rt0+1; column tiles 0, 1
+  double acc[2][2][2] = {};
   int buf = 0;
   if (k0 < k1) issue(k0, 0);
   for (int kb = k0; kb < k1; kb += XW_KC) {
@@ -272,36 +277,41 @@ __global__ void __launch_bounds__(256) sy2sb_xw_kernel(const double* __restrict_
       cp_async_wait<0>();
     }
     __syncthreads();
-    double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
-#pragma unroll 8
-    for (int kk = 0; kk < XW_KC; kk += 2) {
-      const double a0 = Ak[buf][r][kk], a1 = Ak[buf][r][kk + 1];
-      p0 += a0 * Vk[buf][kk][cg0];
-      q0 += a0 * Vk[buf][kk][cg0 + 8];
-      p1 += a1 * Vk[buf][kk + 1][cg0];
-      q1 += a1 * Vk[buf][kk + 1][cg0 + 8];
+#pragma unroll
+    for (int kk = 0; kk < XW_KC; kk += 4) {
+      const double a0 = Ak[buf][rt0 * 8 + g][kk + tq], a1 = Ak[buf][rt0 * 8 + 8 + g][kk + tq];
+      const double b0 = Vk[buf][kk + tq][g], b1 = Vk[buf][kk + tq][8 + g];
+      dmma(acc[0][0][0], acc[0][0][1], a0, b0);
+      dmma(acc[0][1][0], acc[0][1][1], a0, b1);
+      dmma(acc[1][0][0], acc[1][0][1], a1, b0);
+      dmma(acc[1][1][0], acc[1][1][1], a1, b1);
     }
-    acc0 += p0 + p1;
-    acc1 += q0 + q1;
     __syncthreads();
     buf ^= 1;
   }
-  Xo[r][cg0] = acc0;
-  Xo[r][cg0 + 8] = acc1;
-  if (rb + r < m) {
-    Xwp[((long)kid * m + rb + r) * SB + cg0] = acc0;
-    Xwp[((long)kid * m + rb + r) * SB + cg0 + 8] = acc1;
-  }
-  for (int e = tid; e < XW_ROWS * SB; e += 256) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int jt = 0; jt < 2; ++jt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rr = (rt0 + i) * 8 + g, c = jt * 8 + 2 * tq + h;
+        Xo[rr][c] = acc[i][jt][h];
+        if (rb + rr < m) Xwp[((long)kid * m + rb + rr) * SB + c] = acc[i][jt][h];
+      }
+  for (int e = tid; e < XW_ROWS * SB; e += 128) {
     const int rr = e / SB, c = e % SB;
-    Vk[0][rr][c] = (rb + rr < m) ? X0[(long)(rb + rr) * SB_LDX + c] : 0.0;
+    Vr[rr][c] = (rb + rr < m) ? X0[(long)(rb + rr) * SB_LDX + c] : 0.0;
   }
   __syncthreads();
-  {
-    const int a = tid >> 4, c = tid & 15;
-    double sacc = 0.0;
-    for (int rr = 0; rr < XW_ROWS; ++rr) sacc += Vk[0][rr][a] * Xo[rr][c];
-    Spart[((long)kid * gridDim.x + blockIdx.x) * SB * SB + tid] = sacc;
+  for (int e = tid; e < SB * SB; e += 128) {
+    const int a = e >> 4, c = e & 15;
+    double s0 = 0.0, s1 = 0.0;
+    for (int rr = 0; rr < XW_ROWS; rr += 2) {
+      s0 += Vr[rr][a] * Xo[rr][c];
+      s1 += Vr[rr + 1][a] * Xo[rr + 1][c];
+    }
+    Spart[((long)kid * gridDim.x + blockIdx.x) * SB * SB + e] = s0 + s1;
   }
 }
 
@@ -388,34 +398,38 @@ __global__ void __launch_bounds__(256) sy2sb_syr2k_kernel(double* C, int ldc, in
     Bsh[rr][k] = (j0 + rr < m) ? __ldg(X0 + (long)(j0 + rr) * SB_LDX + SB + k) : 0.0;  // [W | V]
   }
   __syncthreads();
-  const int tr = tid >> 4, tc = tid & 15;
-  double acc[4][4] = {};
-#pragma unroll 4
-  for (int k = 0; k < 2 * SB; ++k) {
-    double av[4], bv[4];
+  // 8 warps × (2 row tiles × 4 column tiles) of 8×8 on the FP64 tensor cores, K = 2·SB = 32
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
+  const int rt0 = (warp >> 1) * 2, ct0 = (warp & 1) * 4;
+  double acc[2][4][2] = {};
 #pragma unroll
-    for (int v = 0; v < 4; ++v) av[v] = Ash[tr + 16 * v][k];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) bv[u] = Bsh[tc + 16 * u][k];
-#pragma unroll
-    for (int v = 0; v < 4; ++v)
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[v][u] += av[v] * bv[u];
-  }
-#pragma unroll
-  for (int v = 0; v < 4; ++v)
+  for (int k0 = 0; k0 < 2 * SB; k0 += 4) {
+    const double a0 = Ash[rt0 * 8 + g][k0 + tq], a1 = Ash[rt0 * 8 + 8 + g][k0 + tq];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int i = i0 + tr + 16 * v, j = j0 + tc + 16 * u;
-      double o = 0.0;
-      if (i < m && j < m && i >= j) {
-        o = C[(long)i * ldc + j] - acc[v][u];
-        C[(long)i * ldc + j] = o;
-      }
-      Ct[tr + 16 * v][tc + 16 * u] = o;
+      const double bv = Bsh[(ct0 + u) * 8 + g][k0 + tq];
+      dmma(acc[0][u][0], acc[0][u][1], a0, bv);
+      dmma(acc[1][u][0], acc[1][u][1], a1, bv);
     }
+  }
+#pragma unroll
+  for (int v = 0; v < 2; ++v)
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int li = (rt0 + v) * 8 + g, lj = (ct0 + u) * 8 + 2 * tq + h;
+        const int i = i0 + li, j = j0 + lj;
+        double o = 0.0;
+        if (i < m && j < m && i >= j) {
+          o = C[(long)i * ldc + j] - acc[v][u][h];
+          C[(long)i * ldc + j] = o;
+        }
+        Ct[li][lj] = o;
+      }
   __syncthreads();
   // mirror: C[j][i] = C[i][j] for i > j, coalesced along i
+  const int tr = tid >> 4, tc = tid & 15;
 #pragma unroll
   for (int v = 0; v < 4; ++v)
 #pragma unroll
@@ -477,7 +491,7 @@ static void sy2sb(const double* Z, int n, EigWork& w, cudaStream_t st) {
       const int ks = std::max(1, std::min(2, m / 512));
       double* Xwp = w.W1;       // [ks][m][SB]
       double* Spart = w.splitws;  // [ks·nb][SB·SB]
-      sy2sb_xw_kernel<<<dim3(nb, ks), 256, 0, st>>>(A22, n, m, X0, Xwp, Spart);
+      sy2sb_xw_kernel<<<dim3(nb, ks), 128, 0, st>>>(A22, n, m, X0, Xwp, Spart);
       KOT_LAUNCH_CHECK();
       sy2sb_sred_kernel<<<1, 1024, 0, st>>>(Spart, ks * nb, Sred);
       KOT_LAUNCH_CHECK();
@@ -872,15 +886,17 @@ __global__ void __launch_bounds__(32 * QL_WARPS) q2_larft_kernel(const double* _
 // W −= V Y) run on the FP64 tensor cores (mma m8n8k4), with K ranges cut to the
 // band of V and the upper triangle of T.
 constexpr int QW_COLS = 64;
+constexpr int QW_TPC = 4;                 // column tiles per CTA (V, T loaded once, W double-buffered)
 constexpr int QW_RW = 48;                 // window rows incl. zero padding (≥ QG_ROWS)
 constexpr int QW_LDW = QW_COLS + 4;       // stride ≡ 4 (mod 16) doubles
 constexpr int QW_LDV = QG + 4;
-constexpr int QW_SMEM = (QW_RW * QW_LDW + QW_RW * QW_LDV + QG * QW_LDV + 2 * QG * QW_LDW) * 8;
+constexpr int QW_SMEM = (2 * QW_RW * QW_LDW + QW_RW * QW_LDV + QG * QW_LDV + 2 * QG * QW_LDW) * 8;
 __global__ void __launch_bounds__(256) q2_wave_kernel(double* P, int n, const double* __restrict__ Vq2,
-                                                      const double* __restrict__ Tq2, int NT, int wave, int Ilo) {
+                                                      const double* __restrict__ Tq2, int NT, int wave, int Ilo,
+                                                      int tile0, int tile1) {
   extern __shared__ double qw[];
-  double* W = qw;                        // [QW_RW][QW_LDW]
-  double* Vd = W + QW_RW * QW_LDW;       // [QW_RW][QW_LDV]: Vd[ρ][j] = v_j[ρ − j]
+  double* Wb = qw;                       // [2][QW_RW][QW_LDW]
+  double* Vd = Wb + 2 * QW_RW * QW_LDW;  // [QW_RW][QW_LDV]: Vd[ρ][j] = v_j[ρ − j]
   double* T = Vd + QW_RW * QW_LDV;       // [QG][QW_LDV]
   double* Y = T + QG * QW_LDV;           // [QG][QW_LDW]
   double* Y2 = Y + QG * QW_LDW;          // [QG][QW_LDW]
@@ -889,69 +905,84 @@ __global__ void __launch_bounds__(256) q2_wave_kernel(double* P, int n, const do
   const int ilo = I * QG;
   const int r0 = ilo + 1 + t * SB;
   const int nr = min(QG_ROWS, n - r0);
-  const int c0 = blockIdx.x * QW_COLS;
-  const int wc = min(QW_COLS, n - c0);
+  const int tbeg = tile0 + blockIdx.x * QW_TPC, tend = min(tile1, tbeg + QW_TPC);
   const int tid = threadIdx.x;
-  for (int e = tid; e < QW_RW * QW_COLS; e += 256) {
-    const int rr = e / QW_COLS, c = e % QW_COLS;
-    W[rr * QW_LDW + c] = (rr < nr && c < wc) ? P[(long)(r0 + rr) * n + c0 + c] : 0.0;
-  }
+  auto issue = [&](int tile, int buf) {
+    const int c0 = tile * QW_COLS, wc = min(QW_COLS, n - c0);
+    double* W = Wb + buf * QW_RW * QW_LDW;
+    for (int e = tid; e < QW_RW * QW_COLS; e += 256) {
+      const int rr = e / QW_COLS, c = e % QW_COLS;
+      const bool ok = rr < nr && c < wc;
+      cp_async_8(W + rr * QW_LDW + c, ok ? P + (long)(r0 + rr) * n + c0 + c : P, ok ? 8 : 0);
+    }
+    cp_async_commit();
+  };
+  if (tbeg < tend) issue(tbeg, 0);
   for (int e = tid; e < QW_RW * QG; e += 256) {
     const int rho = e / QG, jj = e % QG, q = rho - jj, i = ilo + jj;
     Vd[rho * QW_LDV + jj] = (q >= 0 && q < SB && i <= n - 3 && rho < nr) ? __ldg(q2_vec(Vq2, i, t, NT) + q) : 0.0;
   }
   const double* Tg = Tq2 + ((long)I * NT + t) * QG * QG;
   for (int e = tid; e < QG * QG; e += 256) T[(e / QG) * QW_LDV + e % QG] = __ldg(Tg + e);
-  __syncthreads();
   const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
-  // ---- Y = Vᵀ W: warp → row tile jt = warp/2, column tiles 4·(warp%2) .. +3
-  {
-    const int jt = warp >> 1, ct0 = (warp & 1) * 4;
-    double acc[4][2] = {};
-    const int kb = 8 * jt, ke = min(QW_RW, 8 * jt + 8 + SB - 1);
-    for (int k0 = kb; k0 < ke; k0 += 4) {
-      const double a = Vd[(k0 + tq) * QW_LDV + jt * 8 + g];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) dmma(acc[u][0], acc[u][1], a, W[(k0 + tq) * QW_LDW + (ct0 + u) * 8 + g]);
+  int buf = 0;
+  for (int tile = tbeg; tile < tend; ++tile, buf ^= 1) {
+    if (tile + 1 < tend) {
+      issue(tile + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
+    __syncthreads();
+    const double* W = Wb + buf * QW_RW * QW_LDW;
+    const int c0 = tile * QW_COLS, wc = min(QW_COLS, n - c0);
+    {  // ---- Y = Vᵀ W: warp → row tile jt = warp/2, column tiles 4·(warp%2) .. +3
+      const int jt = warp >> 1, ct0 = (warp & 1) * 4;
+      double acc[4][2] = {};
+      const int kb = 8 * jt, ke = min(QW_RW, 8 * jt + 8 + SB - 1);
+      for (int k0 = kb; k0 < ke; k0 += 4) {
+        const double a = Vd[(k0 + tq) * QW_LDV + jt * 8 + g];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      Y[(jt * 8 + g) * QW_LDW + (ct0 + u) * 8 + 2 * tq] = acc[u][0];
-      Y[(jt * 8 + g) * QW_LDW + (ct0 + u) * 8 + 2 * tq + 1] = acc[u][1];
-    }
-  }
-  __syncthreads();
-  // ---- Y2 = T Y  (T upper triangular: K from the row tile on)
-  {
-    const int jt = warp >> 1, ct0 = (warp & 1) * 4;
-    double acc[4][2] = {};
-    for (int k0 = 8 * jt; k0 < QG; k0 += 4) {
-      const double a = T[(jt * 8 + g) * QW_LDV + k0 + tq];
+        for (int u = 0; u < 4; ++u) dmma(acc[u][0], acc[u][1], a, W[(k0 + tq) * QW_LDW + (ct0 + u) * 8 + g]);
+      }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) dmma(acc[u][0], acc[u][1], a, Y[(k0 + tq) * QW_LDW + (ct0 + u) * 8 + g]);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      Y2[(jt * 8 + g) * QW_LDW + (ct0 + u) * 8 + 2 * tq] = acc[u][0];
-      Y2[(jt * 8 + g) * QW_LDW + (ct0 + u) * 8 + 2 * tq + 1] = acc[u][1];
-    }
-  }
-  __syncthreads();
-  // ---- W −= V Y2: warp → column tile ct = warp, row tiles 0..5 (K = j ∈ [8ρt − SB + 1, 8ρt + 7])
-  {
-    const int ct = warp;
-#pragma unroll
-    for (int pt = 0; pt < QW_RW / 8; ++pt) {
-      double acc0 = 0.0, acc1 = 0.0;
-      const int kb = max(0, (8 * pt - SB + 1) & ~3), ke = min(QG, 8 * pt + 8);
-      for (int k0 = kb; k0 < ke; k0 += 4)
-        dmma(acc0, acc1, Vd[(pt * 8 + g) * QW_LDV + k0 + tq], Y2[(k0 + tq) * QW_LDW + ct * 8 + g]);
-      const int rho = pt * 8 + g, c = ct * 8 + 2 * tq;
-      if (rho < nr) {
-        if (c < wc) P[(long)(r0 + rho) * n + c0 + c] = W[rho * QW_LDW + c] - acc0;
-        if (c + 1 < wc) P[(long)(r0 + rho) * n + c0 + c + 1] = W[rho * QW_LDW + c + 1] - acc1;
+      for (int u = 0; u < 4; ++u) {
+        Y[(jt * 8 + g) * QW_LDW + (ct0 + u) * 8 + 2 * tq] = acc[u][0];
+        Y[(jt * 8 + g) * QW_LDW + (ct0 + u) * 8 + 2 * tq + 1] = acc[u][1];
       }
     }
+    __syncthreads();
+    {  // ---- Y2 = T Y  (T upper triangular: K from the row tile on)
+      const int jt = warp >> 1, ct0 = (warp & 1) * 4;
+      double acc[4][2] = {};
+      for (int k0 = 8 * jt; k0 < QG; k0 += 4) {
+        const double a = T[(jt * 8 + g) * QW_LDV + k0 + tq];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma(acc[u][0], acc[u][1], a, Y[(k0 + tq) * QW_LDW + (ct0 + u) * 8 + g]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        Y2[(jt * 8 + g) * QW_LDW + (ct0 + u) * 8 + 2 * tq] = acc[u][0];
+        Y2[(jt * 8 + g) * QW_LDW + (ct0 + u) * 8 + 2 * tq + 1] = acc[u][1];
+      }
+    }
+    __syncthreads();
+    {  // ---- W −= V Y2: warp → column tile ct = warp, row tiles 0..5 (K = j ∈ [8ρt − SB + 1, 8ρt + 7])
+      const int ct = warp;
+#pragma unroll
+      for (int pt = 0; pt < QW_RW / 8; ++pt) {
+        double acc0 = 0.0, acc1 = 0.0;
+        const int kb = max(0, (8 * pt - SB + 1) & ~3), ke = min(QG, 8 * pt + 8);
+        for (int k0 = kb; k0 < ke; k0 += 4)
+          dmma(acc0, acc1, Vd[(pt * 8 + g) * QW_LDV + k0 + tq], Y2[(k0 + tq) * QW_LDW + ct * 8 + g]);
+        const int rho = pt * 8 + g, c = ct * 8 + 2 * tq;
+        if (rho < nr) {
+          if (c < wc) P[(long)(r0 + rho) * n + c0 + c] = W[rho * QW_LDW + c] - acc0;
+          if (c + 1 < wc) P[(long)(r0 + rho) * n + c0 + c + 1] = W[rho * QW_LDW + c + 1] - acc1;
+        }
+      }
+    }
+    __syncthreads();  // W[buf] and Y/Y2 are rewritten by the next tile
   }
 }
 
@@ -968,14 +999,26 @@ void two_stage_q2_apply(int n, EigWork& w, double* P, cudaStream_t st) {
   }
   q2_larft_kernel<<<ceil_div(ng, QL_WARPS), 32 * QL_WARPS, 0, st>>>(w.Vq2, w.tq2, w.Tq2, n, NT, ng);
   KOT_LAUNCH_CHECK();
-  // waves t − I = wv; group (I, t) exists for 0 ≤ t ≤ tmax(I) = (n − 2 − I·QG)/SB
-  for (int wv = -(NI - 1); wv <= (n - 2) / SB; ++wv) {
-    int Ilo = std::max(0, -wv), Ihi = NI - 1;
-    while (Ihi >= Ilo && wv + Ihi > (n - 2 - Ihi * QG) / SB) --Ihi;
-    if (Ihi < Ilo) continue;
-    dim3 grid(ceil_div(n, QW_COLS), Ihi - Ilo + 1);
-    q2_wave_kernel<<<grid, 256, QW_SMEM, st>>>(P, n, w.Vq2, w.Tq2, NT, wv, Ilo);
-    KOT_LAUNCH_CHECK();
+  // Column batches sized so that the batch's columns of P (n × width doubles) stay resident in
+  // L2 across all waves: every wave re-reads the rows it updates, so without batching P streams
+  // from HBM once per wave at large ℓ.  Waves t − I = wv; group (I, t) exists for
+  // 0 ≤ t ≤ tmax(I) = (n − 2 − I·QG)/SB.
+  static const long l2_budget = [] {
+    const char* e = std::getenv("KOT_Q2_BATCH_MB");  // diagnostic: column batching of P
+    return (e ? std::atol(e) : 4096L) << 20;
+  }();
+  const int tiles = ceil_div(n, QW_COLS);
+  const int btiles = std::max(1, std::min(tiles, (int)(l2_budget / ((long)n * QW_COLS * 8))));
+  for (int tb = 0; tb < tiles; tb += btiles) {
+    const int nt = std::min(btiles, tiles - tb);
+    for (int wv = -(NI - 1); wv <= (n - 2) / SB; ++wv) {
+      int Ilo = std::max(0, -wv), Ihi = NI - 1;
+      while (Ihi >= Ilo && wv + Ihi > (n - 2 - Ihi * QG) / SB) --Ihi;
+      if (Ihi < Ilo) continue;
+      dim3 grid(ceil_div(nt, QW_TPC), Ihi - Ilo + 1);
+      q2_wave_kernel<<<grid, 256, QW_SMEM, st>>>(P, n, w.Vq2, w.Tq2, NT, wv, Ilo, tb, tb + nt);
+      KOT_LAUNCH_CHECK();
+    }
   }
 }
 
