@@ -1393,22 +1393,27 @@ static int sytrd_per_sm(int n) {
   return std::max(1, per_sm);
 }
 
-// Which tridiagonalisation an eigensolve uses.  Measured on B200 (eigbench,
-// DESIGN.md): the one-stage sytrd is faster at ℓ = 2000 (35 vs 45 ms), 4096 and
-// 8192; the two-stage path (eig2.cu) keeps its latency-bound parts on ≤ 16 SMs
-// but its back-transform is not yet tensor-core bound, and running it beside the
-// one-stage grids slowed the Newton chain (probe: 80 vs 47 ms per trial
-// residual).  So the default is one-stage; KOT_EIG_STAGES=2 (or
-// kot_debug_eig_stages) selects the two-stage reduction.
-static int g_eig_stages = -1;  // −1: read KOT_EIG_STAGES once
+// Which tridiagonalisation an eigensolve uses (measured on B200, DESIGN.md §3/§5).
+// Below ℓ ≈ 3000 the one-stage sytrd wins (ℓ = 2000: 35 vs 42 ms alone, 7.9 vs
+// 5.2 it/s in the solver); from ℓ = 3000 on the two-stage path wins in the solver
+// (3000: 3.39 vs 3.26 it/s; 4096: 1.60 vs 1.51; 8192: 0.435 vs 0.316 it/s): the
+// one-stage panel streams the whole trailing matrix from HBM once per column,
+// the two-stage path once per 16-column panel.  KOT_EIG_STAGES=1|2 (or
+// kot_debug_eig_stages) forces either; 3 = two-stage for background eigensolves only.
+constexpr int kTwoStageMinOrder = 3000;
+static int g_eig_stages = -1;  // −1: read KOT_EIG_STAGES once (0 = automatic)
 bool use_two_stage(int n, int lane) {
   if (g_eig_stages < 0) {
     const char* e = std::getenv("KOT_EIG_STAGES");
-    g_eig_stages = e ? std::atoi(e) : 1;
+    g_eig_stages = e ? std::atoi(e) : 0;
   }
   if (n < 3) return false;
-  // 3: hybrid — background (lane ≠ 0) eigensolves two-stage, the Newton chain one-stage
-  return g_eig_stages == 2 || (g_eig_stages == 3 && lane != 0);
+  switch (g_eig_stages) {
+    case 1: return false;
+    case 2: return true;
+    case 3: return lane != 0;
+    default: return n >= kTwoStageMinOrder;
+  }
 }
 
 static void one_stage_tridiag(const double* Z, int n, EigWork& w, cudaStream_t st, int lane) {
@@ -1473,8 +1478,8 @@ extern "C" int kot_debug_sytrd_timing(int on, unsigned long long* out8) {
   }
 }
 
-// test hook: 1 = one-stage, 2 = two-stage tridiagonalisation for subsequent eigensolves
+// test hook: 0 = automatic, 1 = one-stage, 2 = two-stage, 3 = two-stage for background eigensolves
 extern "C" int kot_debug_eig_stages(int stages) {
-  kot::g_eig_stages = (stages == 2 || stages == 3) ? stages : 1;
+  kot::g_eig_stages = (stages >= 0 && stages <= 3) ? stages : 0;
   return 0;
 }

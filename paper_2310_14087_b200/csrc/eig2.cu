@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(SB2_NTHREADS, 1) sb2st_kernel(Sb2Args a) {
     }
   }
   if (timing)
-    for (int k = 0; k < 8; ++k) atomicAdd(a.dbg + (rank * SB2_WARPS + warp) * 8 + k, tseg[k]);
+    for (int k = 0; k < 8; ++k) atomicAdd(a.dbg + (rank * 32 + warp) * 8 + k, tseg[k]);
 #undef SBM
   cl.sync();
   for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
@@ -1027,11 +1027,11 @@ void two_stage_q2_apply(int n, EigWork& w, double* P, cudaStream_t st) {
 extern "C" int kot_debug_sb2st_timing(int on, unsigned long long* out8) {
   using namespace kot;
   if (on) {
-    if (!g_sb2_dbg && cudaMalloc(&g_sb2_dbg, 16 * 8 * 8 * sizeof(unsigned long long)) != cudaSuccess) return 6;
-    cudaMemset(g_sb2_dbg, 0, 16 * 8 * 8 * sizeof(unsigned long long));
+    if (!g_sb2_dbg && cudaMalloc(&g_sb2_dbg, 16 * 32 * 8 * sizeof(unsigned long long)) != cudaSuccess) return 6;
+    cudaMemset(g_sb2_dbg, 0, 16 * 32 * 8 * sizeof(unsigned long long));
   } else if (g_sb2_dbg) {
     cudaDeviceSynchronize();
-    cudaMemcpy(out8, g_sb2_dbg, 16 * 8 * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaMemcpy(out8, g_sb2_dbg, 16 * 32 * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     cudaFree(g_sb2_dbg);
     g_sb2_dbg = nullptr;
   }

@@ -545,7 +545,7 @@ def two_stage():
     f = _lib.lib().kot_debug_eig_stages
     f(2)
     yield
-    f(1)
+    f(0)
 
 
 @pytest.mark.parametrize("n", [64, 65, 300, 1100])

@@ -44,11 +44,11 @@ for nm, v in zip(names, buf):
 # per-segment cycles of the bulge-chasing kernel (every CTA × warp)
 f = getattr(L, "kot_debug_sb2st_timing", None)
 if f is not None:
-    buf2 = (C.c_ulonglong * (16 * 8 * 8))()
+    buf2 = (C.c_ulonglong * (16 * 32 * 8))()
     f(1, buf2)
     linalg.sym_eig(z)
     f(0, buf2)
-    a = np.array(buf2[:], dtype=float).reshape(16, 8, 8)
+    a = np.array(buf2[:], dtype=float).reshape(16, 32, 8)
     names = ["enum/idle", "load", "(1) C·Hp", "(2) house+bcast", "(3) C left", "(4) D two-sided", "store+slot",
              "cluster.sync"]
     busy = a[:, :, :7].sum(axis=2)
