@@ -315,21 +315,15 @@ __global__ void __launch_bounds__(128) sy2sb_xw_kernel(const double* __restrict_
   }
 }
 
-// Fixed-order sum of the S partials (one CTA of 1024 threads: 4 interleaved chains per entry,
-// each with 8 loads in flight).
-__global__ void __launch_bounds__(1024) sy2sb_sred_kernel(const double* __restrict__ Spart, int nparts, double* S) {
-  __shared__ double part[4][SB * SB];
-  const int e = threadIdx.x & 255, g = threadIdx.x >> 8;
+// Fixed-order sum of the S partials, first level: CTA b sums partials b, b + G, b + 2G, …
+// (all loads of a thread issued together); the W kernel adds the G level-1 sums in order.
+constexpr int SRED_G = 16;
+__global__ void __launch_bounds__(256) sy2sb_sred_kernel(const double* __restrict__ Spart, int nparts, double* S1) {
+  const int e = threadIdx.x, b = blockIdx.x;
   double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int p = g;
-  for (; p + 28 < nparts; p += 32) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u] += __ldg(Spart + (long)(p + 4 * u) * SB * SB + e);
-  }
-  for (int u = 0; p < nparts; p += 4, ++u) acc[u & 7] += __ldg(Spart + (long)p * SB * SB + e);
-  part[g][e] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-  __syncthreads();
-  if (g == 0) S[e] = (part[0][e] + part[1][e]) + (part[2][e] + part[3][e]);
+  int p = b, u = 0;
+  for (; p < nparts; p += SRED_G, ++u) acc[u & 7] += __ldg(Spart + (long)p * SB * SB + e);
+  S1[b * SB * SB + e] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
 }
 
 // W = Xw T − ½ V M with M = Tᵀ S T, S = Σ partials (fixed order), Xw = Σ_k Xwp[k] (fixed order);
@@ -340,7 +334,15 @@ __global__ void __launch_bounds__(256) sy2sb_w_kernel(double* Xs, int r0, int m,
   __shared__ double xw[16][SB + 1], vv[16][SB + 1];
   const int tid = threadIdx.x, a = tid >> 4, c = tid & 15;
   T[a][c] = Tp[a * SB + c];
-  S[a][c] = Sg[tid];
+  {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int b = 0; b < SRED_G; b += 2) {
+      s0 += Sg[b * SB * SB + tid];
+      s1 += Sg[(b + 1) * SB * SB + tid];
+    }
+    S[a][c] = s0 + s1;
+  }
   __syncthreads();
   {
     double s = 0.0;
@@ -448,7 +450,7 @@ static void sy2sb(const double* Z, int n, EigWork& w, cudaStream_t st) {
   KOT_CUDA(cudaMemsetAsync(w.tau, 0, sizeof(double) * n, st));
   double* Xs = w.X;      // n × SB_LDX
   double* Tp = w.Tf;     // SB × SB
-  double* Sred = w.Tf + SB * SB;
+  double* Sred = w.Tf + SB * SB;  // SRED_G level-1 sums of S
   static int smem_set = 0;
   static bool s2k_attr = false;
   if (!s2k_attr) {
@@ -493,7 +495,7 @@ static void sy2sb(const double* Z, int n, EigWork& w, cudaStream_t st) {
       double* Spart = w.splitws;  // [ks·nb][SB·SB]
       sy2sb_xw_kernel<<<dim3(nb, ks), 128, 0, st>>>(A22, n, m, X0, Xwp, Spart);
       KOT_LAUNCH_CHECK();
-      sy2sb_sred_kernel<<<1, 1024, 0, st>>>(Spart, ks * nb, Sred);
+      sy2sb_sred_kernel<<<SRED_G, 256, 0, st>>>(Spart, ks * nb, Sred);
       KOT_LAUNCH_CHECK();
       sy2sb_w_kernel<<<std::min(ceil_div(m, 16), 2 * kNumSMs), 256, 0, st>>>(Xs, r0, m, Tp, Sred, Xwp, ks);
       KOT_LAUNCH_CHECK();

@@ -571,3 +571,20 @@ def test_two_stage_residual_and_middle_operator(two_stage, cfg1):
     r, dc = O.residual_parts(po, O.Pair(cfg1["op_g"], cfg1["op_x"]))
     rg, _ = GP.residual_parts(pd, w)
     assert rel(rg.gamma, r.g) <= 1e-11 and rel(rg.x_mat, r.x) <= 1e-11
+
+
+def test_sym_eig_default_two_stage_order():
+    """ℓ ≥ 3000 uses the two-stage reduction by default: full decomposition accuracy at ℓ = 3001."""
+    n = 3001
+    rng = np.random.default_rng(7)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    vals = np.concatenate([np.linspace(1, 50, n // 2), -np.logspace(-6, 0, n - n // 2)])
+    z = (q * vals) @ q.T
+    z = 0.5 * (z + z.T)
+    dc = GL.sym_eig(z)
+    ref = np.sort(vals)[::-1]
+    assert np.max(np.abs(dc.eigvals - ref)) <= 2e-12 * np.abs(ref).max()
+    p = dc.eigvecs
+    assert np.linalg.norm(p.T @ p - np.eye(n)) <= 1e-10
+    assert np.linalg.norm((p * dc.eigvals) @ p.T - z) / np.linalg.norm(z) <= 1e-13
+    assert dc.pos_idx.size == n // 2
