@@ -349,6 +349,16 @@ def run_gpu(args):
                                "trailing matrix, 8*m(m+1)/2 B",
                 "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"],
                 "note": "latency-bound: 2 grid barriers + ~4 dependent L2 round trips per column"}
+    if roof is None and "eig.q2" in prof:  # two-stage path (l >= 3000): the tensor-core Q2 back-transform
+        e = prof["eig.q2"]
+        ach = e["flops"] / (e["ms"] * 1e-3) / 1e12
+        roof = {"kernel": "q2_wave_kernel sequence (two-stage eigensolver, stage-2 back-transform, mma m8n8k4 f64)",
+                "bound": "tensor", "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": ach / DMMA_PEAK_TFLOPS, "traffic": None,
+                "algorithmic": "2 l^3 FLOPs per eigensolve (the applied reflectors' useful work; the banded blocks "
+                               "execute about 2.5x that)",
+                "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"],
+                "note": "timed per eigensolve (one Q2 application = one wave sequence)"}
     if "gemm_dmma" in prof:
         e = prof["gemm_dmma"]
         ach = e["flops"] / (e["ms"] * 1e-3) / 1e12
