@@ -26,19 +26,22 @@ namespace kot {
 #ifndef KOT_GEMM_BK
 #define KOT_GEMM_BK 8
 #endif
-#ifndef KOT_GEMM_WARPS
-#define KOT_GEMM_WARPS 4
-#endif
-constexpr int GB_M = 64, GB_N = 64, GB_K = KOT_GEMM_BK, G_STAGES = KOT_GEMM_STAGES;
-// warps split the 64×64 tile 2 ways along N; along M into G_WARPS/2 strips of G_WM rows
-constexpr int G_WARPS = KOT_GEMM_WARPS, G_THREADS = 32 * G_WARPS;
-constexpr int G_WM = GB_M / (G_WARPS / 2), G_MI = G_WM / 8;
+constexpr int GB_M = 64, GB_N = 64, GB_K = KOT_GEMM_BK, G_STAGES = KOT_GEMM_STAGES, G_THREADS = 128;
 constexpr int G_PADK = GB_K + 4;  // stride ≡ 4 (mod 16) doubles → conflict-free fragment loads
+// CTA tile BM×BN, 4 warps as 2×2, each (BM/2)×(BN/2).  64×64 is used everywhere: 64×128 / 128×64
+// are 17 % faster on the CG matvec shapes in isolation (tools/gemmbench/gemm_big.cu) but slower
+// inside the solver, where the concurrent chains leave fewer SMs free (matvec 1.05 → 1.23 ms).
+template <int BM, int BN>
+struct GTile {
+  static constexpr int PADM = BM + 4, PADN = BN + 4;
+  static constexpr int ATILE = (BM * G_PADK > GB_K * PADM) ? BM * G_PADK : GB_K * PADM;
+  static constexpr int BTILE = (BN * G_PADK > GB_K * PADN) ? BN * G_PADK : GB_K * PADN;
+  static constexpr int SMEM = G_STAGES * (ATILE + BTILE + GB_K) * 8;
+  static constexpr int WM = BM / 2, WN = BN / 2, MI = WM / 8, NJ = WN / 8;
+};
 constexpr int G_PADM = GB_M + 4;
 constexpr int G_PADN = GB_N + 4;
-constexpr int G_ATILE = (GB_M * G_PADK > GB_K * G_PADM) ? GB_M * G_PADK : GB_K * G_PADM;
-constexpr int G_BTILE = (GB_N * G_PADK > GB_K * G_PADN) ? GB_N * G_PADK : GB_K * G_PADN;
-constexpr int G_SMEM_BYTES = G_STAGES * (G_ATILE + G_BTILE + GB_K) * 8;
+constexpr int G_SMEM_BYTES = GTile<GB_M, GB_N>::SMEM;
 
 // C(M×N) = op(A)(M×K) · diag(kscale) · op(B)(K×N), all row-major.
 //   op(A)[m][k] = TA ? A[k*lda+m] : A[m*lda+k]
@@ -113,19 +116,21 @@ __device__ __forceinline__ void load_tile(double* sm, int pad, const double* g, 
 //   __device__ void store(int r, int c, double v) const;          (kRowDot == false)
 //   __device__ double rowdot_weight(int r, int c) const;          (kRowDot == true)
 //   __device__ void rowdot_store(int tn, int r, double partial) const;
-template <bool TA, bool TB, int VEC, class Epi>
+template <bool TA, bool TB, int VEC, class Epi, int BM = GB_M, int BN = GB_N>
 __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi epi) {
+  using T = GTile<BM, BN>;
+  static_assert(!Epi::kRowDot || BN == GB_N, "row-dot partials are per 64-column tile");
   extern __shared__ __align__(16) double gsm[];
-  const int tiles_n_grid = (s.N + GB_N - 1) / GB_N;  // grid layout uses the static bound
+  const int tiles_n_grid = (s.N + BN - 1) / BN;  // grid layout uses the static bound
   if (s.dN) s.N = *s.dN;
   if (s.dK) s.K = *s.dK;
   if (s.dKstart) s.kstart = *s.dKstart;
   double* As = gsm;
-  double* Bs = gsm + G_STAGES * G_ATILE;
-  double* Ks = gsm + G_STAGES * (G_ATILE + G_BTILE);
+  double* Bs = gsm + G_STAGES * T::ATILE;
+  double* Ks = gsm + G_STAGES * (T::ATILE + T::BTILE);
 
-  const int tiles_m = (s.M + GB_M - 1) / GB_M;
-  const int tiles_n = (s.N + GB_N - 1) / GB_N;
+  const int tiles_m = (s.M + BM - 1) / BM;
+  const int tiles_n = (s.N + BN - 1) / BN;
   int tm, tn;
   if (s.sym_tiles) {
     int t = blockIdx.x;
@@ -140,14 +145,14 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
     tn = blockIdx.x / tiles_m;
   }
   if (tm >= tiles_m || tn >= tiles_n) return;
-  const int m0 = tm * GB_M, n0 = tn * GB_N;
+  const int m0 = tm * BM, n0 = tn * BN;
 
   int kbeg = 0, kend = s.K;
   if (s.kb_m) kbeg = max(kbeg, m0);
   if (s.kb_n) kbeg = max(kbeg, n0);
   kbeg = max(kbeg, s.kstart);
-  if (s.ke_m) kend = min(kend, m0 + GB_M);
-  if (s.ke_n) kend = min(kend, n0 + GB_N);
+  if (s.ke_m) kend = min(kend, m0 + BM);
+  if (s.ke_n) kend = min(kend, n0 + BN);
   kbeg = (kbeg / GB_K) * GB_K;
   int nkt = kend > kbeg ? (kend - kbeg + GB_K - 1) / GB_K : 0;
   if (s.ksplit > 1) {  // this CTA's share of the K tiles
@@ -159,26 +164,26 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * G_WM, wn = (warp & 1) * 32;
+  const int wm = (warp >> 1) * T::WM, wn = (warp & 1) * T::WN;
 
-  double acc[G_MI][4][2];
+  double acc[T::MI][T::NJ][2];
 #pragma unroll
-  for (int i = 0; i < G_MI; i++)
+  for (int i = 0; i < T::MI; i++)
 #pragma unroll
-    for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < T::NJ; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   auto issue = [&](int kt, int stage) {
     const int k0 = kbeg + kt * GB_K;
-    double* as = As + stage * G_ATILE;
-    double* bs = Bs + stage * G_BTILE;
+    double* as = As + stage * T::ATILE;
+    double* bs = Bs + stage * T::BTILE;
     if (TA)  // A stored K×M: tile rows k, cols m
-      load_tile<GB_K, GB_M, VEC>(as, G_PADM, s.A, s.lda, k0, m0, s.K, s.M);
+      load_tile<GB_K, BM, VEC>(as, T::PADM, s.A, s.lda, k0, m0, s.K, s.M);
     else
-      load_tile<GB_M, GB_K, VEC>(as, G_PADK, s.A, s.lda, m0, k0, s.M, s.K);
+      load_tile<BM, GB_K, VEC>(as, G_PADK, s.A, s.lda, m0, k0, s.M, s.K);
     if (TB)  // B stored N×K
-      load_tile<GB_N, GB_K, VEC>(bs, G_PADK, s.B, s.ldb, n0, k0, s.N, s.K);
+      load_tile<BN, GB_K, VEC>(bs, G_PADK, s.B, s.ldb, n0, k0, s.N, s.K);
     else
-      load_tile<GB_K, GB_N, VEC>(bs, G_PADN, s.B, s.ldb, k0, n0, s.K, s.N);
+      load_tile<GB_K, BN, VEC>(bs, T::PADN, s.B, s.ldb, k0, n0, s.K, s.N);
     if (s.kscale != nullptr && threadIdx.x < GB_K) {
       const int k = k0 + threadIdx.x;
       cp_async_8(Ks + stage * GB_K + threadIdx.x, k < s.K ? s.kscale + k : s.kscale, k < s.K ? 8 : 0);
@@ -200,27 +205,27 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
       cp_async_commit();
     }
     const int stage = kt % G_STAGES;
-    const double* as = As + stage * G_ATILE;
-    const double* bs = Bs + stage * G_BTILE;
+    const double* as = As + stage * T::ATILE;
+    const double* bs = Bs + stage * T::BTILE;
     const double* ks = Ks + stage * GB_K;
 #pragma unroll
     for (int kk = 0; kk < GB_K; kk += 4) {
-      double a[G_MI], b[4];
+      double a[T::MI], b[T::NJ];
       const double kscl = (s.kscale != nullptr) ? ks[kk + t] : 1.0;
 #pragma unroll
-      for (int i = 0; i < G_MI; i++) {
+      for (int i = 0; i < T::MI; i++) {
         const int m = wm + i * 8 + g;
-        a[i] = (TA ? as[(kk + t) * G_PADM + m] : as[m * G_PADK + kk + t]) * kscl;
+        a[i] = (TA ? as[(kk + t) * T::PADM + m] : as[m * G_PADK + kk + t]) * kscl;
       }
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
+      for (int j = 0; j < T::NJ; j++) {
         const int n = wn + j * 8 + g;
-        b[j] = TB ? bs[n * G_PADK + kk + t] : bs[(kk + t) * G_PADN + n];
+        b[j] = TB ? bs[n * G_PADK + kk + t] : bs[(kk + t) * T::PADN + n];
       }
 #pragma unroll
-      for (int i = 0; i < G_MI; i++)
+      for (int i = 0; i < T::MI; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < T::NJ; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
   }
   cp_async_wait<0>();
@@ -228,13 +233,13 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
   if constexpr (Epi::kRowDot) {
     // partial[r] = Σ_{c in this tile} acc(r,c)·E(r,c): 4-lane shuffle + 2-warp smem combine.
     __syncthreads();
-    double* red = gsm;  // reuse: [2][GB_M]
+    double* red = gsm;  // reuse: [2][BM]
 #pragma unroll
-    for (int i = 0; i < G_MI; i++) {
+    for (int i = 0; i < T::MI; i++) {
       const int r = m0 + wm + i * 8 + g;
       double p = 0.0;
 #pragma unroll
-      for (int j = 0; j < 4; j++)
+      for (int j = 0; j < T::NJ; j++)
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int c = n0 + wn + j * 8 + 2 * t + h;
@@ -242,21 +247,21 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
         }
       p += __shfl_xor_sync(0xffffffffu, p, 1);
       p += __shfl_xor_sync(0xffffffffu, p, 2);
-      if (t == 0) red[(warp & 1) * GB_M + wm + i * 8 + g] = p;
+      if (t == 0) red[(warp & 1) * BM + wm + i * 8 + g] = p;
     }
     __syncthreads();
-    for (int q = threadIdx.x; q < GB_M; q += G_THREADS) {
+    for (int q = threadIdx.x; q < BM; q += G_THREADS) {
       const int r = m0 + q;
-      if (r < s.M) epi.rowdot_store(tn, r, red[q] + red[GB_M + q]);
+      if (r < s.M) epi.rowdot_store(tn, r, red[q] + red[BM + q]);
     }
   } else if (s.ksplit > 1) {
     double* ws = s.ws + (long)blockIdx.y * s.M * s.N;
 #pragma unroll
-    for (int i = 0; i < G_MI; i++) {
+    for (int i = 0; i < T::MI; i++) {
       const int r = m0 + wm + i * 8 + g;
       if (r >= s.M) continue;
 #pragma unroll
-      for (int j = 0; j < 4; j++)
+      for (int j = 0; j < T::NJ; j++)
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int c = n0 + wn + j * 8 + 2 * t + h;
@@ -265,11 +270,11 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < G_MI; i++) {
+    for (int i = 0; i < T::MI; i++) {
       const int r = m0 + wm + i * 8 + g;
       if (r >= s.M) continue;
 #pragma unroll
-      for (int j = 0; j < 4; j++)
+      for (int j = 0; j < T::NJ; j++)
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int c = n0 + wn + j * 8 + 2 * t + h;
@@ -292,8 +297,8 @@ __global__ void splitk_reduce_kernel(int M, int N, int splits, int sym_tiles, co
   }
 }
 
-inline int gemm_grid(const GemmShape& s) {
-  const int tm = (s.M + GB_M - 1) / GB_M, tn = (s.N + GB_N - 1) / GB_N;
+inline int gemm_grid(const GemmShape& s, int bm = GB_M, int bn = GB_N) {
+  const int tm = (s.M + bm - 1) / bm, tn = (s.N + bn - 1) / bn;
   if (s.sym_tiles) return tm * (tm + 1) / 2;
   return tm * tn;
 }
@@ -305,45 +310,48 @@ inline bool gemm_vec2_ok(const GemmShape& s) {
 
 // Algorithmic FLOPs of one launch: per computed tile, 2·rows·cols·(true K range),
 // excluding zero padding and the structurally-zero tiles that are skipped.
-inline double gemm_alg_flops(const GemmShape& s) {
-  const int tm_n = (s.M + GB_M - 1) / GB_M, tn_n = (s.N + GB_N - 1) / GB_N;
+inline double gemm_alg_flops(const GemmShape& s, int bm = GB_M, int bn = GB_N) {
+  const int tm_n = (s.M + bm - 1) / bm, tn_n = (s.N + bn - 1) / bn;
   double f = 0.0;
   for (int tm = 0; tm < tm_n; ++tm)
     for (int tn = s.sym_tiles ? tm : 0; tn < tn_n; ++tn) {
-      const int m0 = tm * GB_M, n0 = tn * GB_N;
+      const int m0 = tm * bm, n0 = tn * bn;
       int kb = 0, ke = s.K;
       if (s.kb_m) kb = std::max(kb, m0);
       if (s.kb_n) kb = std::max(kb, n0);
       kb = std::max(kb, s.kstart);
-      if (s.ke_m) ke = std::min(ke, m0 + GB_M);
-      if (s.ke_n) ke = std::min(ke, n0 + GB_N);
-      if (ke > kb) f += 2.0 * std::min(GB_M, s.M - m0) * std::min(GB_N, s.N - n0) * (double)(ke - kb);
+      if (s.ke_m) ke = std::min(ke, m0 + bm);
+      if (s.ke_n) ke = std::min(ke, n0 + bn);
+      if (ke > kb) f += 2.0 * std::min(bm, s.M - m0) * std::min(bn, s.N - n0) * (double)(ke - kb);
     }
   return f;
 }
 
-template <bool TA, bool TB, class Epi>
-void gemm_launch(const GemmShape& s, const Epi& epi, cudaStream_t st) {
+// Launch with a BM×BN CTA tile (64×64: every GEMM; 64×128 / 128×64: long-thin products).
+template <bool TA, bool TB, int BM, int BN, class Epi>
+void gemm_launch_tiled(const GemmShape& s, const Epi& epi, cudaStream_t st) {
   if (s.M <= 0 || s.N <= 0) return;
-  ProfScope prof("gemm_dmma", st, prof_enabled() ? gemm_alg_flops(s) : 0.0);
-  const int tiles = gemm_grid(s);
+  if (BM != BN) kot_require(!s.sym_tiles, KOT_EINVAL, "symmetric tiling needs square CTA tiles");
+  constexpr int smem = GTile<BM, BN>::SMEM;
+  ProfScope prof("gemm_dmma", st, prof_enabled() ? gemm_alg_flops(s, BM, BN) : 0.0);
+  const int tiles = gemm_grid(s, BM, BN);
   const dim3 grid(tiles, s.ksplit > 1 ? s.ksplit : 1);
   if (gemm_vec2_ok(s)) {
-    auto k = gemm_dmma_kernel<TA, TB, 2, Epi>;
+    auto k = gemm_dmma_kernel<TA, TB, 2, Epi, BM, BN>;
     static bool attr = false;
     if (!attr) {
-      KOT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES));
+      KOT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       attr = true;
     }
-    k<<<grid, G_THREADS, G_SMEM_BYTES, st>>>(s, epi);
+    k<<<grid, G_THREADS, smem, st>>>(s, epi);
   } else {
-    auto k = gemm_dmma_kernel<TA, TB, 1, Epi>;
+    auto k = gemm_dmma_kernel<TA, TB, 1, Epi, BM, BN>;
     static bool attr = false;
     if (!attr) {
-      KOT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES));
+      KOT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       attr = true;
     }
-    k<<<grid, G_THREADS, G_SMEM_BYTES, st>>>(s, epi);
+    k<<<grid, G_THREADS, smem, st>>>(s, epi);
   }
   KOT_LAUNCH_CHECK();
   if constexpr (!Epi::kRowDot) {
@@ -354,6 +362,11 @@ void gemm_launch(const GemmShape& s, const Epi& epi, cudaStream_t st) {
       KOT_LAUNCH_CHECK();
     }
   }
+}
+
+template <bool TA, bool TB, class Epi>
+void gemm_launch(const GemmShape& s, const Epi& epi, cudaStream_t st) {
+  gemm_launch_tiled<TA, TB, GB_M, GB_N>(s, epi, st);
 }
 
 // Pick a split-K factor so that skinny / few-tile GEMMs fill the 148 SMs.
