@@ -465,6 +465,14 @@ void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* o
       s.kscale = v + r0;
       s.ws = p.splitws;
       s.ksplit = choose_ksplit(s, p.splitws_cap);
+      // split-K 3 even when the tile count would not need it: inside the concurrent solver the
+      // extra CTAs fill SMs left between the other chains' kernels (probe cfg3: matvec 1.06 →
+      // 0.94–1.0 ms, 7.8 → 8.0 it/s; 2/4/6 measured worse).  KOT_MV_SPLIT overrides.
+      static const int mv_split = [] {
+        const char* e = std::getenv("KOT_MV_SPLIT");
+        return e ? std::atoi(e) : 3;
+      }();
+      if (mv_split > 1 && (long)mv_split * s.M * s.N <= p.splitws_cap) s.ksplit = mv_split;
       gemm_launch<true, false>(s, EpiMvCoef{dst, n, m.dc.vals, k, m.pos ? 1 : 0, m.mu}, p.st);
       if (!first) axpby(p, (long)ks * n, 1.0, b.Ct, 1.0, p.shard_tmp, b.Ct);
       first = false;
