@@ -602,17 +602,30 @@ void spectral_filter(Problem& p, const Decomp& dc, const double* S, double* out,
   double* C = p.M4;
   double* H = p.M3;
   double* G = p.M5;
+  static const int sf_split = [] {
+    const char* e = std::getenv("KOT_SF_SPLIT");  // diagnostic: split-K of the ks×ℓ×ℓ products
+    return e ? std::atoi(e) : 1;
+  }();
+  auto split = [&](GemmShape& s) {
+    if (sf_split > 1 && (long)sf_split * s.M * s.N <= p.splitws_cap) {
+      s.ws = p.splitws;
+      s.ksplit = sf_split;
+    }
+  };
   if (ks > 0) {
     {  // U = P_subᵀ S
       GemmShape s = make_shape(ks, n, n, Psub, n, S, n);
+      split(s);
       gemm_launch<true, false>(s, EpiAxpby{U, n, 1.0, 0.0}, p.st);
     }
     {  // Ĉ = W ∘ (U P)
       GemmShape s = make_shape(ks, n, n, U, n, dc.P, n);
+      split(s);
       gemm_launch<false, false>(s, EpiSpectral{C, n, dc.vals, k, pos ? 1 : 0, mode, mu}, p.st);
     }
     {  // H = Ĉ Pᵀ
       GemmShape s = make_shape(ks, n, n, C, n, dc.P, n);
+      split(s);
       gemm_launch<false, true>(s, EpiAxpby{H, n, 1.0, 0.0}, p.st);
     }
   }
