@@ -90,12 +90,21 @@ void EigWork::ensure_two_stage() {
   alloc(&Vq2, q2);
   alloc(&Tq2, two_stage_t_size(n));
   alloc(&tq2, q2 / 16);
+  KOT_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+  KOT_CUDA(cudaEventCreateWithFlags(&ev_w, cudaEventDisableTiming));
+  KOT_CUDA(cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming));
 }
 
 EigWork::~EigWork() {
   for (double* p : {A, Vall, X, d, e, tau, xv, yv, part, partn, Tf, W1, Q, Qw, Qnd, Dl, Uw, zs, ds, dlam, wv, what, lam,
                     dfv, rotcs, rho, splitws, gpart, Vq2, Tq2, tq2})
     dev_free(p);
+  if (st2) {
+    cudaStreamSynchronize(st2);
+    cudaStreamDestroy(st2);
+  }
+  if (ev_w) cudaEventDestroy(ev_w);
+  if (ev_rest) cudaEventDestroy(ev_rest);
   dev_free(gcnt);
   dev_free(ibuf);
   dev_free(dbuf);

@@ -381,17 +381,29 @@ __global__ void __launch_bounds__(256) sy2sb_w_kernel(double* Xs, int r0, int m,
 constexpr int S2K_T = 64;
 constexpr int S2K_LD = 2 * SB + 1;
 constexpr int S2K_SMEM = (2 * S2K_T * S2K_LD + S2K_T * (S2K_T + 1)) * 8;
-__global__ void __launch_bounds__(256) sy2sb_syr2k_kernel(double* C, int ldc, int m, const double* __restrict__ X0) {
+// Tile sets: mode 0 = every lower tile; 1 = column strip 0 only (the next panel's columns, for the
+// look-ahead); 2 = the lower tiles right of strip 0.
+__global__ void __launch_bounds__(256) sy2sb_syr2k_kernel(double* C, int ldc, int m, const double* __restrict__ X0,
+                                                          int mode) {
   extern __shared__ double s2k[];
   double (*Ash)[S2K_LD] = reinterpret_cast<double (*)[S2K_LD]>(s2k);
   double (*Bsh)[S2K_LD] = reinterpret_cast<double (*)[S2K_LD]>(s2k + S2K_T * S2K_LD);
   double (*Ct)[S2K_T + 1] = reinterpret_cast<double (*)[S2K_T + 1]>(s2k + 2 * S2K_T * S2K_LD);
-  // blockIdx.x → lower tile (tm, tn), tm ≥ tn
-  const int b = blockIdx.x;
-  int tm = (int)((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
-  while ((tm + 1) * (tm + 2) / 2 <= b) ++tm;
-  while (tm * (tm + 1) / 2 > b) --tm;
-  const int tn = b - tm * (tm + 1) / 2;
+  int tm, tn;
+  if (mode == 1) {
+    tm = blockIdx.x;
+    tn = 0;
+  } else {  // blockIdx.x → lower tile (tm, tn), tm ≥ tn, of the (sub)triangle
+    const int b = blockIdx.x;
+    tm = (int)((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
+    while ((tm + 1) * (tm + 2) / 2 <= b) ++tm;
+    while (tm * (tm + 1) / 2 > b) --tm;
+    tn = b - tm * (tm + 1) / 2;
+    if (mode == 2) {
+      ++tm;
+      ++tn;
+    }
+  }
   const int i0 = tm * S2K_T, j0 = tn * S2K_T;
   const int tid = threadIdx.x;
   for (int e = tid; e < S2K_T * 2 * SB; e += 256) {
@@ -448,7 +460,12 @@ static void sy2sb(const double* Z, int n, EigWork& w, cudaStream_t st) {
   KOT_CUDA(cudaMemcpyAsync(w.A, Z, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
   KOT_CUDA(cudaMemsetAsync(w.Vall, 0, sizeof(double) * n * n, st));
   KOT_CUDA(cudaMemsetAsync(w.tau, 0, sizeof(double) * n, st));
-  double* Xs = w.X;      // n × SB_LDX
+  // Look-ahead: after panel p's W is known, the update of the next panel's columns (tile strip 0)
+  // runs on the main stream, so panel p+1's QR can start while the rest of the rank-32 update runs
+  // on a second stream; Xs is double-buffered (panel parity) because that update still reads it.
+  w.ensure_two_stage();
+  cudaStream_t sb = w.st2;
+  double* Xs = w.X;      // n × SB_LDX, two buffers
   double* Tp = w.Tf;     // SB × SB
   double* Sred = w.Tf + SB * SB;  // SRED_G level-1 sums of S
   static int smem_set = 0;
@@ -457,8 +474,10 @@ static void sy2sb(const double* Z, int n, EigWork& w, cudaStream_t st) {
     KOT_CUDA(cudaFuncSetAttribute(sy2sb_syr2k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, S2K_SMEM));
     s2k_attr = true;
   }
-  for (int j = 0; j + SB + 1 < n; j += SB) {
+  int pidx = 0;
+  for (int j = 0; j + SB + 1 < n; j += SB, ++pidx) {
     const int m = n - j - SB;
+    Xs = w.X + (long)(pidx & 1) * n * SB_LDX;
     const int cs = pqr_cluster(m);
     kot_require(ceil_div(m, cs) <= 32 * PQR_RPT, KOT_EINVAL, "matrix order too large for the band reduction");
     const int rows = (m + cs - 1) / cs;
@@ -493,6 +512,7 @@ static void sy2sb(const double* Z, int n, EigWork& w, cudaStream_t st) {
       const int ks = std::max(1, std::min(2, m / 512));
       double* Xwp = w.W1;       // [ks][m][SB]
       double* Spart = w.splitws;  // [ks·nb][SB·SB]
+      if (pidx > 0) KOT_CUDA(cudaStreamWaitEvent(st, w.ev_rest, 0));  // A22 fully updated by panel p−1
       sy2sb_xw_kernel<<<dim3(nb, ks), 128, 0, st>>>(A22, n, m, X0, Xwp, Spart);
       KOT_LAUNCH_CHECK();
       sy2sb_sred_kernel<<<SRED_G, 256, 0, st>>>(Spart, ks * nb, Sred);
@@ -500,12 +520,20 @@ static void sy2sb(const double* Z, int n, EigWork& w, cudaStream_t st) {
       sy2sb_w_kernel<<<std::min(ceil_div(m, 16), 2 * kNumSMs), 256, 0, st>>>(Xs, r0, m, Tp, Sred, Xwp, ks);
       KOT_LAUNCH_CHECK();
     }
-    {  // A22 −= V Wᵀ + W Vᵀ  (one triangle + mirror)
+    {  // A22 −= V Wᵀ + W Vᵀ  (one triangle + mirror): strip 0 now, the rest beside the next panel's QR
       const int nt = ceil_div(m, S2K_T);
-      sy2sb_syr2k_kernel<<<nt * (nt + 1) / 2, 256, S2K_SMEM, st>>>(A22, n, m, X0);
+      sy2sb_syr2k_kernel<<<nt, 256, S2K_SMEM, st>>>(A22, n, m, X0, 1);
       KOT_LAUNCH_CHECK();
+      if (nt > 1) {
+        KOT_CUDA(cudaEventRecord(w.ev_w, st));
+        KOT_CUDA(cudaStreamWaitEvent(sb, w.ev_w, 0));
+        sy2sb_syr2k_kernel<<<(nt - 1) * nt / 2, 256, S2K_SMEM, sb>>>(A22, n, m, X0, 2);
+        KOT_LAUNCH_CHECK();
+      }
+      KOT_CUDA(cudaEventRecord(w.ev_rest, sb));
     }
   }
+  KOT_CUDA(cudaStreamWaitEvent(st, w.ev_rest, 0));
 }
 
 // ============================================================== stage 2

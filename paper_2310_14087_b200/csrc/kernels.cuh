@@ -29,6 +29,8 @@ struct EigWork {
   double *dfv = nullptr, *rotcs = nullptr, *rho = nullptr, *splitws = nullptr, *gpart = nullptr;
   int* gcnt = nullptr;
   double *Vq2 = nullptr, *tq2 = nullptr, *Tq2 = nullptr;  // two-stage: stage-2 reflectors, τ, group T
+  cudaStream_t st2 = nullptr;  // two-stage: look-ahead stream
+  cudaEvent_t ev_w = nullptr, ev_rest = nullptr;
   long splitws_cap = 0;
   int* ibuf = nullptr;
   void* dbuf = nullptr;
