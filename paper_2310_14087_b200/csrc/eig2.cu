@@ -509,7 +509,7 @@ static void sy2sb(const double* Z, int n, EigWork& w, cudaStream_t st) {
     double* X0 = Xs + (long)r0 * SB_LDX;
     {  // Xw = A22 V (row blocks × K-splits) and the partial S = Vᵀ Xw; then W
       const int nb = ceil_div(m, XW_ROWS);
-      const int ks = std::max(1, std::min(2, m / 512));
+      const int ks = std::max(1, std::min(8, m / 1024));  // K-splits: keep ≥ ~2 CTAs per SM busy at large m
       double* Xwp = w.W1;       // [ks][m][SB]
       double* Spart = w.splitws;  // [ks·nb][SB·SB]
       if (pidx > 0) KOT_CUDA(cudaStreamWaitEvent(st, w.ev_rest, 0));  // A22 fully updated by panel p−1
