@@ -1375,18 +1375,28 @@ namespace {
 std::mutex g_coop_mu;
 std::condition_variable g_coop_cv;
 int g_coop_used = 0;
+int g_coop_fg = 0;  // lane-0 grids in flight
 struct CoopGate {
-  int slots;
-  CoopGate(int total, int want, int reserve, int lane) : slots(want) {
+  int slots, lane;
+  CoopGate(int total, int want, int reserve, int lane_) : slots(want), lane(lane_) {
+    static const bool yield_bg = [] {  // diagnostic: background grids wait while a lane-0 grid runs
+      const char* e = std::getenv("KOT_COOP_YIELD");
+      return e && std::atoi(e) > 0;
+    }();
     std::unique_lock<std::mutex> lk(g_coop_mu);
     const int limit = (lane == 0) ? total : total - reserve;
-    g_coop_cv.wait(lk, [&] { return g_coop_used + want <= limit || g_coop_used == 0; });
+    g_coop_cv.wait(lk, [&] {
+      if (lane != 0 && yield_bg && g_coop_fg > 0) return false;
+      return g_coop_used + want <= limit || g_coop_used == 0;
+    });
     g_coop_used += want;
+    if (lane == 0) ++g_coop_fg;
   }
   ~CoopGate() {
     {
       std::lock_guard<std::mutex> lk(g_coop_mu);
       g_coop_used -= slots;
+      if (lane == 0) --g_coop_fg;
     }
     g_coop_cv.notify_all();
   }
