@@ -1,4 +1,5 @@
 // Pooled device / pinned-host allocation for libkotgpu (see common.cuh).
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -71,6 +72,21 @@ void host_free_pinned(void* p, size_t bytes) {
   if (!p) return;
   std::lock_guard<std::mutex> lk(g_mu);
   g_pinned_free[bytes].push_back(p);
+}
+
+namespace {
+std::map<std::pair<int, const void*>, int> g_smem_attr;
+}
+
+void ensure_smem_attr(const void* func, int bytes, bool nonportable_cluster) {
+  int dev = 0;
+  KOT_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  int& have = g_smem_attr[{dev, func}];
+  if (have >= bytes && have > 0) return;
+  if (nonportable_cluster) KOT_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (bytes > 48 * 1024) KOT_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = std::max(bytes, 1);
 }
 
 }  // namespace kot

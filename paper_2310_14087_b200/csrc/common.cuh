@@ -88,6 +88,11 @@ void dev_free(void* p);
 void* host_alloc_pinned(size_t bytes);
 void host_free_pinned(void* p, size_t bytes);
 
+// Raise `func`'s dynamic shared-memory limit to at least `bytes` on the CURRENT device (function
+// attributes are per device), optionally allowing non-portable cluster sizes; cached per
+// (device, kernel), thread-safe.
+void ensure_smem_attr(const void* func, int bytes, bool nonportable_cluster = false);
+
 constexpr int kNumSMs = 148;
 
 }  // namespace kot

@@ -433,7 +433,6 @@ static int trd_grid(int rows, int lane) {
 static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane) {
   KOT_CUDA(cudaMemcpyAsync(w.A, Z, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
   KOT_CUDA(cudaMemsetAsync(w.Vall, 0, sizeof(double) * n * n, st));
-  static int smem_set_for = 0;
   for (int p0 = 0; p0 < n - 1; p0 += TRD_NB) {
     const int nb = std::min(TRD_NB, n - 1 - p0);
     KOT_CUDA(cudaMemsetAsync(w.X, 0, sizeof(double) * n * 3 * TRD_NB, st));
@@ -447,10 +446,7 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
     double bytes = 0.0;
     for (int c = p0; c < p0 + nb; ++c) bytes += 8.0 * 0.5 * (double)(n - c - 1) * (n - c);
     const size_t smem = sizeof(double) * (std::max(rows, 1) + 3L * TRD_WARPS * TRD_RPW * TRD_NB);
-    if (smem > 48 * 1024 && smem_set_for < (int)smem) {
-      KOT_CUDA(cudaFuncSetAttribute(sytrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      smem_set_for = (int)smem;
-    }
+    ensure_smem_attr((const void*)sytrd_panel_kernel, (int)smem);
     {
       ProfScope pscope("sytrd_panel", st, 0.0, bytes);
       KOT_CUDA(cudaLaunchCooperativeKernel((void*)sytrd_panel_kernel, G, TRD_THREADS, kargs, smem, st));
@@ -1112,7 +1108,6 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
   // host-pinned staging regions (distinct per purpose: copies are asynchronous)
   int* h_packed = w.hbuf;                                           // <= 2n + 8 ints
   char* h_desc = reinterpret_cast<char*>(w.hbuf + 2L * n + 64);      // <= n/16 descs
-  char* h_roots = reinterpret_cast<char*>(w.hbuf + 8L * n + 128);    // <= n RootRef
   char* d_desc_base = reinterpret_cast<char*>(w.dbuf);
   std::vector<int> splits, loff, llen;
   int maxdepth = 0;
@@ -1179,11 +1174,7 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
     {
       ProfScope ps_prep("dc.prep", st);
       const size_t smem = (size_t)maxm * (3 * sizeof(double) + sizeof(int));
-      static size_t prep_attr = 0;
-      if (smem > 48 * 1024 && smem > prep_attr) {
-        KOT_CUDA(cudaFuncSetAttribute(dc_merge_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        prep_attr = smem;
-      }
+      ensure_smem_attr((const void*)dc_merge_prep_kernel, (int)smem);
       dc_merge_prep_kernel<<<nm, DC_PREP_THREADS, smem, st>>>(dms, w.Q, n, w.d, w.e, w.zs, w.ds, w.dlam, w.wv,
                                                               w.dfv, w.rotcs, w.rho, perm, ndcol, dcol, rot, dmeta,
                                                               pidx);
@@ -1192,11 +1183,7 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
     {
       ProfScope ps_vec("dc.gather_rot", st);
       const size_t smem = (size_t)maxm * sizeof(double);
-      static size_t vec_attr = 0;
-      if (smem > 48 * 1024 && smem > vec_attr) {
-        KOT_CUDA(cudaFuncSetAttribute(dc_merge_vec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        vec_attr = smem;
-      }
+      ensure_smem_attr((const void*)dc_merge_vec_kernel, (int)smem);
       dc_merge_vec_kernel<<<dim3(maxm, nm), 256, smem, st>>>(dms, w.Q, w.Qw, w.Qnd, n, perm, ndcol, dcol, rot,
                                                              w.rotcs, dmeta, pidx);
       KOT_LAUNCH_CHECK();
@@ -1334,11 +1321,7 @@ static void ormtr(int n, EigWork& w, double* P, cudaStream_t st) {
     }
     {
       ProfScope pl("orm.larft", st);
-      static bool attr = false;
-      if (!attr) {
-        KOT_CUDA(cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LARFT_SMEM));
-        attr = true;
-      }
+      ensure_smem_attr((const void*)larft_kernel, LARFT_SMEM);
       larft_kernel<<<ceil_div(nb, LARFT_THREADS / 32), LARFT_THREADS, LARFT_SMEM, st>>>(S, w.tau + p0, nb, T);
       KOT_LAUNCH_CHECK();
     }
@@ -1405,8 +1388,7 @@ struct CoopGate {
 
 static int sytrd_per_sm(int n) {
   const size_t smem = sizeof(double) * (std::max(n, 1) + 3L * TRD_WARPS * TRD_RPW * TRD_NB);
-  if (smem > 48 * 1024)
-    KOT_CUDA(cudaFuncSetAttribute(sytrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_smem_attr((const void*)sytrd_panel_kernel, (int)smem);
   int per_sm = 0;
   KOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sytrd_panel_kernel, TRD_THREADS, smem));
   return std::max(1, per_sm);

@@ -468,12 +468,7 @@ static void sy2sb(const double* Z, int n, EigWork& w, cudaStream_t st) {
   double* Xs = w.X;      // n × SB_LDX, two buffers
   double* Tp = w.Tf;     // SB × SB
   double* Sred = w.Tf + SB * SB;  // SRED_G level-1 sums of S
-  static int smem_set = 0;
-  static bool s2k_attr = false;
-  if (!s2k_attr) {
-    KOT_CUDA(cudaFuncSetAttribute(sy2sb_syr2k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, S2K_SMEM));
-    s2k_attr = true;
-  }
+  ensure_smem_attr((const void*)sy2sb_syr2k_kernel, S2K_SMEM);
   int pidx = 0;
   for (int j = 0; j + SB + 1 < n; j += SB, ++pidx) {
     const int m = n - j - SB;
@@ -482,11 +477,7 @@ static void sy2sb(const double* Z, int n, EigWork& w, cudaStream_t st) {
     kot_require(ceil_div(m, cs) <= 32 * PQR_RPT, KOT_EINVAL, "matrix order too large for the band reduction");
     const int rows = (m + cs - 1) / cs;
     const size_t smem = sizeof(double) * std::max(rows, 1) * PQR_LD;
-    if ((int)smem > smem_set) {
-      KOT_CUDA(cudaFuncSetAttribute(sy2sb_panel_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      KOT_CUDA(cudaFuncSetAttribute(sy2sb_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      smem_set = (int)smem;
-    }
+    ensure_smem_attr((const void*)sy2sb_panel_kernel, (int)smem, true);
     {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(cs);
@@ -820,12 +811,7 @@ static void sb2st(int n, EigWork& w, cudaStream_t st) {
   const int cw = (n + cs - 1) / cs;
   const size_t smem = sizeof(double) * ((size_t)cw * SB2_LDB);
   kot_require(smem <= 220 * 1024, KOT_EINVAL, "matrix order too large for the bulge-chasing cluster");
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
-    KOT_CUDA(cudaFuncSetAttribute(sb2st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    KOT_CUDA(cudaFuncSetAttribute(sb2st_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    smem_set = smem;
-  }
+  ensure_smem_attr((const void*)sb2st_kernel, (int)smem, true);
   const long q2 = two_stage_q2_size(n);
   KOT_CUDA(cudaMemsetAsync(w.Vq2, 0, sizeof(double) * q2, st));
   KOT_CUDA(cudaMemsetAsync(w.tq2, 0, sizeof(double) * (q2 / SB), st));
@@ -1022,11 +1008,7 @@ void two_stage_q2_apply(int n, EigWork& w, double* P, cudaStream_t st) {
   const int NT = eig_nt(n);
   const int NI = q2_ngroups_i(n);
   const int ng = NI * NT;
-  static bool attr = false;
-  if (!attr) {
-    KOT_CUDA(cudaFuncSetAttribute(q2_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, QW_SMEM));
-    attr = true;
-  }
+  ensure_smem_attr((const void*)q2_wave_kernel, QW_SMEM);
   q2_larft_kernel<<<ceil_div(ng, QL_WARPS), 32 * QL_WARPS, 0, st>>>(w.Vq2, w.tq2, w.Tq2, n, NT, ng);
   KOT_LAUNCH_CHECK();
   // Column batches sized so that the batch's columns of P (n × width doubles) stay resident in

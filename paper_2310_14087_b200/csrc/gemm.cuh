@@ -338,19 +338,11 @@ void gemm_launch_tiled(const GemmShape& s, const Epi& epi, cudaStream_t st) {
   const dim3 grid(tiles, s.ksplit > 1 ? s.ksplit : 1);
   if (gemm_vec2_ok(s)) {
     auto k = gemm_dmma_kernel<TA, TB, 2, Epi, BM, BN>;
-    static bool attr = false;
-    if (!attr) {
-      KOT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = true;
-    }
+    ensure_smem_attr((const void*)k, smem);
     k<<<grid, G_THREADS, smem, st>>>(s, epi);
   } else {
     auto k = gemm_dmma_kernel<TA, TB, 1, Epi, BM, BN>;
-    static bool attr = false;
-    if (!attr) {
-      KOT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = true;
-    }
+    ensure_smem_attr((const void*)k, smem);
     k<<<grid, G_THREADS, smem, st>>>(s, epi);
   }
   KOT_LAUNCH_CHECK();

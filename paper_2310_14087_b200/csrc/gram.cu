@@ -179,8 +179,7 @@ void gram_square(const double* P0, const double* P1, int n, int d, double bw0, d
   const int tiles = (n + GT - 1) / GT;
   const int D = pair ? 2 * d : d;
   const size_t smem = 2 * GT * (D + 1) * sizeof(double);
-  if (smem > 48 * 1024)
-    KOT_CUDA(cudaFuncSetAttribute(gram_square_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_smem_attr((const void*)gram_square_kernel, (int)smem);
   gram_square_kernel<<<tiles * (tiles + 1) / 2, 256, smem, st>>>(P0, P1, n, d, 2.0 * bw0,
                                                                2.0 * bw1, nsets, pair ? 1 : 0, out);
   KOT_LAUNCH_CHECK();
