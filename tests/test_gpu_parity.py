@@ -588,3 +588,28 @@ def test_sym_eig_default_two_stage_order():
     assert np.linalg.norm(p.T @ p - np.eye(n)) <= 1e-10
     assert np.linalg.norm((p * dc.eigvals) @ p.T - z) / np.linalg.norm(z) <= 1e-13
     assert dc.pos_idx.size == n // 2
+
+
+def test_two_stage_iteration_replay_converged_cg(two_stage, cfg1):
+    """One full SSN iteration (EG step, residuals, converged-CG Newton step, acceptance) with every
+    eigensolve going through the two-stage reduction agrees with the oracle to 1e-8."""
+    pd = gpu_pd(cfg1)
+    newton = K.NewtonConfig(cg_tol=1e-14, cg_max=3000, cg_restarts=0)
+    cfg = K.SolverConfig(newton=newton, eg=EgConfig(float(cfg1["eg_stepsize"])), residual_tol=1e-12, max_iter=40)
+    ocfg = O.SolverCfg(newton=O.NewtonCfg(cg_tol=1e-14, cg_max=3000, cg_restarts=0),
+                       eg_stepsize=float(cfg1["eg_stepsize"]), residual_tol=1e-12, max_iter=40)
+    po = oracle_pd(cfg1)
+    for i in (0, 10, 20):
+        w = GP.IteratePair(cfg1[f"rp{i}_wg"], cfg1[f"rp{i}_wx"])
+        v = GP.IteratePair(cfg1[f"rp{i}_vg"], cfg1[f"rp{i}_vx"])
+        theta = float(cfg1[f"rp{i}_theta"])
+        ow = O.Pair(w.gamma.copy(), w.x_mat.copy())
+        r_w, dc_w = O.residual_parts(po, ow)
+        st0 = O.State(ow, O.Pair(v.gamma.copy(), v.x_mat.copy()), r_w, dc_w, r_w.norm(), None, None, r_w.norm(),
+                      theta)
+        ost, orec, _ = O.iterate_once(po, st0, i, ocfg)
+        w2, v2, th2, rec = GS.iterate(pd, cfg, w, v, theta, i)
+        assert rec.accepted == orec.accepted and th2 == pytest.approx(ost.theta, rel=1e-12), i
+        assert rel(w2.gamma, ost.w.g) <= 1e-8, i
+        assert rel(w2.x_mat, ost.w.x) <= 1e-8, i
+        assert rel(v2.x_mat, ost.v.x) <= 1e-9, i
