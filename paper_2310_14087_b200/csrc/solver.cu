@@ -11,6 +11,7 @@
 #include <condition_variable>
 #include <exception>
 #include <mutex>
+#include <memory>
 #include <thread>
 #include <utility>
 #include <vector>
@@ -136,6 +137,7 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
   kot_require(rn > 0.0, KOT_EINVAL, "direction requires a nonzero residual");
   ProfScope ps("newton", p.st);
   // filt = r2 + 𝒯[r2];  a1 = −r1 − Φ(filt)/(μ+1);  ã2 = −filt/(μ+1)   (newton.py:161-163)
+  auto ppre = std::make_unique<ProfScope>("newton.prologue", p.st);
   spectral_filter(p, dc, r2, p.M2, mu, 0);
   axpby(p, nn, 1.0, r2, 1.0, p.M2, b.filt);
   phi_partials(p, b.filt);
@@ -146,6 +148,7 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
   KOT_CUDA(cudaMemsetAsync(b.sol, 0, sizeof(double) * n, p.st));
   MvCtx mv;
   matvec_prepare(p, dc, mu, mv);
+  ppre.reset();  // end of the prologue scope
   NewtonOut out{0, 0, 0, INFINITY, 0.0, 0.0};
   const auto t0 = clk::now();
   for (int att = 0; att <= cfg.cg_restarts; ++att) {
@@ -168,6 +171,7 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
     KOT_CUDA(cudaStreamSynchronize(p.st));
     out.cg_ms = ms_since(t0);
     // dw = (sol, ã2 − 𝒯[Φ*(sol)])
+    ProfScope pcrit("newton.criterion", p.st);
     KOT_CUDA(cudaMemcpyAsync(dg, b.sol, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
     phi_adjoint(p, b.sol, p.M1);
     spectral_filter(p, dc, p.M1, p.M2, mu, 0);
