@@ -421,7 +421,9 @@ static int env_int(const char* name, int dflt) {
 }
 static int trd_grid_cap(int lane) {
   static const int cap = std::min(env_int("KOT_TRD_GRID", kNumSMs), kNumSMs);
-  static const int cap_bg = std::min(env_int("KOT_TRD_GRID_BG", 48), cap);  // measured best (probe cfg3: 148 → 7.2, 74 → 7.7, 48 → 7.9, 32 → 7.8 it/s)
+  // measured (probe cfg3, speculative Newton criterion): 48 → 7.9, 56 → 8.2, 64 → 8.25, 72 → 8.0,
+  // 80+ → 7.1–7.2 it/s (two background grids no longer fit beside a full lane-0 grid)
+  static const int cap_bg = std::min(env_int("KOT_TRD_GRID_BG", 64), cap);
   return lane == 0 ? cap : cap_bg;
 }
 static int trd_grid(int rows, int lane) {

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <condition_variable>
 #include <exception>
+#include <functional>
 #include <mutex>
 #include <memory>
 #include <thread>
@@ -91,10 +92,13 @@ __global__ void __launch_bounds__(CG_THREADS) cg_step_kernel(int n, double* x, d
 struct CgOut {
   int iters;
   double res;
+  bool aborted = false;
 };
 
-// x (= b.cx) solves A x = rhs to tol·‖rhs‖ with A = middle operator.
-static CgOut cg_solve(Problem& p, const MvCtx& mv, const double* rhs, double tol, int max_iter) {
+// x (= b.cx) solves A x = rhs to tol·‖rhs‖ with A = middle operator.  `abort` (nullable) is polled
+// after every iteration; when it returns true the solve stops early (speculative attempt discarded).
+static CgOut cg_solve(Problem& p, const MvCtx& mv, const double* rhs, double tol, int max_iter,
+                      const std::function<bool()>* abort = nullptr) {
   Bufs& b = p.bufs();
   const int n = p.n;
   kot_require(max_iter >= 1, KOT_EINVAL, "max_iter must be >= 1");
@@ -122,6 +126,7 @@ static CgOut cg_solve(Problem& p, const MvCtx& mv, const double* rhs, double tol
     res = p.hsc[SC_RES];
     if (flag == 3) throw KotError(KOT_ECG, "non-finite residual in conjugate gradient");
     if (res <= target) return {it, res};
+    if (abort && (*abort)()) return {it, res, true};
   }
   if (it > max_iter) it = max_iter;
   return {it, res};
@@ -129,6 +134,39 @@ static CgOut cg_solve(Problem& p, const MvCtx& mv, const double* rhs, double tol
 
 // --------------------------------------------------------------- Newton
 
+// Criterion ‖(J+μI)dw + r‖ ≤ τ min(1, κ‖r‖‖dw‖) for dw = (sol, ã2 − 𝒯[Φ*(sol)]) (newton.py:131-141,
+// problem.py:222-236), enqueued on the criterion context q after `after` (recorded on p's stream):
+// dw into q.crit_dg / q.crit_dX, the four squared norms into q.hsc[0..3], completion = q.crit_done.
+static void criterion_enqueue(Problem& p, Problem& q, const double* r1, const double* r2, const Decomp& dc,
+                              double mu) {
+  Bufs& b = p.bufs();
+  const int n = p.n;
+  const long nn = (long)n * n;
+  KOT_CUDA(cudaEventRecord(q.crit_after, p.st));
+  KOT_CUDA(cudaStreamWaitEvent(q.st, q.crit_after, 0));
+  ProfScope pcrit("newton.criterion", q.st);
+  KOT_CUDA(cudaMemcpyAsync(q.crit_dg, b.sol, sizeof(double) * n, cudaMemcpyDeviceToDevice, q.st));
+  phi_adjoint(q, b.sol, q.M1);
+  spectral_filter(q, dc, q.M1, q.M2, mu, 0);
+  axpby(q, nn, 1.0, b.a2t, -1.0, q.M2, q.crit_dX);
+  phi_partials(q, q.crit_dX);
+  finalize(q, FIN_JTOP, q.crit_dg, true, r1, mu, q.crit_e1);
+  phi_adjoint_ex(q, q.crit_dg, q.M1, 1.0, q.crit_dX, -1.0, 0.0);  // Φ*(dγ) − dX
+  spectral_filter(q, dc, q.M1, q.M2, mu, 1);                       // M[·]
+  jac_bottom(q, nn, q.M2, q.crit_dX, mu, r2, q.M1);
+  dev_reduce(q, q.crit_e1, nullptr, n, 0, true);
+  dev_reduce(q, q.M1, nullptr, nn, 1, true);
+  dev_reduce(q, q.crit_dg, nullptr, n, 2, true);
+  dev_reduce(q, q.crit_dX, nullptr, nn, 3, true);
+  KOT_CUDA(cudaMemcpyAsync(q.hsc, q.dsc, sizeof(double) * 4, cudaMemcpyDeviceToHost, q.st));
+  KOT_CUDA(cudaEventRecord(q.crit_done, q.st));
+}
+
+// Algorithm 1 (newton.py:144-195).  Attempt a+1 only runs when attempt a's criterion fails, and its
+// right-hand side a1 − M(sol) does not depend on that criterion: so the criterion of attempt a runs
+// on the criterion context while attempt a+1 already starts on the main stream.  If the criterion
+// turns out met, the speculative attempt is discarded before it touches `sol` — same arithmetic,
+// same results, the criterion's latency off the critical path whenever it fails.
 NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, double rn, const Decomp& dc, double mu,
                            const SolverCfg& cfg, double* dg, double* dX) {
   Bufs& b = p.bufs();
@@ -148,52 +186,84 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
   KOT_CUDA(cudaMemsetAsync(b.sol, 0, sizeof(double) * n, p.st));
   MvCtx mv;
   matvec_prepare(p, dc, mu, mv);
-  ppre.reset();  // end of the prologue scope
+  ppre.reset();
+  Problem& q = p.crit();
   NewtonOut out{0, 0, 0, INFINITY, 0.0, 0.0};
   const auto t0 = clk::now();
-  for (int att = 0; att <= cfg.cg_restarts; ++att) {
-    out.attempts = att + 1;
-    const double* rhs = b.a1;
-    if (att) {
-      if (mv.direct)
-        middle_operator(p, dc, mu, b.sol, b.e3);
-      else
-        middle_operator_fast(p, mv, b.sol, b.e3);
-      axpby(p, n, 1.0, b.a1, -1.0, b.e3, b.rhs);
-      rhs = b.rhs;
+  bool pending = false;  // criterion of attempt `att − 1` in flight on q
+  bool pending_met = false;
+  auto read_crit = [&]() {
+    out.lhs = q.hsc[0] + q.hsc[1];
+    const double dwn = q.hsc[2] + q.hsc[3];
+    out.rhs = cfg.tau * std::min(1.0, cfg.kappa * rn * dwn);
+    out.met = out.lhs <= out.rhs;
+  };
+  auto resolve = [&](bool wait) {  // true once the pending criterion is known
+    if (!pending) return true;
+    if (wait) {
+      KOT_CUDA(cudaEventSynchronize(q.crit_done));
+    } else if (cudaEventQuery(q.crit_done) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return false;
     }
-    const double bn = dev_norm(p, rhs, n);
-    if (bn > 0.0 && a1n > 0.0) {
-      const CgOut c = cg_solve(p, mv, rhs, rel * a1n / bn, cfg.cg_max);
+    read_crit();
+    pending = false;
+    pending_met = out.met;
+    return true;
+  };
+  auto finish = [&]() {  // the accepted attempt's dw (in q's outputs) → caller's buffers
+    KOT_CUDA(cudaStreamWaitEvent(p.st, q.crit_done, 0));
+    KOT_CUDA(cudaMemcpyAsync(dg, q.crit_dg, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
+    KOT_CUDA(cudaMemcpyAsync(dX, q.crit_dX, sizeof(double) * nn, cudaMemcpyDeviceToDevice, p.st));
+    out.cg_ms = ms_since(t0);
+  };
+  const std::function<bool()> abort_if_met = [&]() { return resolve(false) && pending_met; };
+  for (int att = 0; att <= cfg.cg_restarts; ++att) {
+    const bool speculative = pending;
+    CgOut c{0, 0.0};
+    bool ran = false;
+    try {
+      const double* rhs = b.a1;
+      if (att) {
+        if (mv.direct)
+          middle_operator(p, dc, mu, b.sol, b.e3);
+        else
+          middle_operator_fast(p, mv, b.sol, b.e3);
+        axpby(p, n, 1.0, b.a1, -1.0, b.e3, b.rhs);
+        rhs = b.rhs;
+      }
+      const double bn = dev_norm(p, rhs, n);
+      if (bn > 0.0 && a1n > 0.0) {
+        c = cg_solve(p, mv, rhs, rel * a1n / bn, cfg.cg_max, speculative ? &abort_if_met : nullptr);
+        ran = true;
+      }
+    } catch (...) {
+      // a speculative attempt's failure only counts if its predecessor's criterion failed
+      if (speculative && resolve(true) && pending_met) {
+        finish();
+        return out;
+      }
+      throw;
+    }
+    if (speculative) {  // attempt att−1's criterion decides whether this attempt happened at all
+      resolve(true);
+      if (pending_met) {
+        finish();
+        return out;
+      }
+    }
+    out.attempts = att + 1;
+    if (ran) {
       axpby(p, n, 1.0, b.sol, 1.0, b.cx, b.sol);
       out.cg_iters += c.iters;
     }
-    KOT_CUDA(cudaStreamSynchronize(p.st));
-    out.cg_ms = ms_since(t0);
-    // dw = (sol, ã2 − 𝒯[Φ*(sol)])
-    ProfScope pcrit("newton.criterion", p.st);
-    KOT_CUDA(cudaMemcpyAsync(dg, b.sol, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
-    phi_adjoint(p, b.sol, p.M1);
-    spectral_filter(p, dc, p.M1, p.M2, mu, 0);
-    axpby(p, nn, 1.0, b.a2t, -1.0, p.M2, dX);
-    // criterion ‖(J+μI)dw + r‖ ≤ τ min(1, κ‖r‖‖dw‖)   (newton.py:131-141, problem.py:222-236)
-    phi_partials(p, dX);
-    finalize(p, FIN_JTOP, dg, true, r1, mu, b.e1);
-    phi_adjoint_ex(p, dg, p.M1, 1.0, dX, -1.0, 0.0);  // Φ*(dγ) − dX
-    spectral_filter(p, dc, p.M1, p.M2, mu, 1);         // M[·]
-    jac_bottom(p, nn, p.M2, dX, mu, r2, p.M1);
-    dev_reduce(p, b.e1, nullptr, n, 0, true);
-    dev_reduce(p, p.M1, nullptr, nn, 1, true);
-    dev_reduce(p, dg, nullptr, n, 2, true);
-    dev_reduce(p, dX, nullptr, nn, 3, true);
-    fetch(p, 4);
-    out.lhs = p.hsc[0] + p.hsc[1];
-    const double dwn = p.hsc[2] + p.hsc[3];
-    out.rhs = cfg.tau * std::min(1.0, cfg.kappa * rn * dwn);
-    out.met = out.lhs <= out.rhs;
-    if (out.met) break;
+    criterion_enqueue(p, q, r1, r2, dc, mu);
+    pending = true;
+    if (att == cfg.cg_restarts) break;
     rel /= 10.0;
   }
+  resolve(true);
+  finish();
   return out;
 }
 

@@ -46,7 +46,7 @@ void Problem::init_scratch() {
   dk = static_cast<int*>(dev_alloc(16 * sizeof(int)));
   dflag = dk + 8;
   hk = static_cast<int*>(host_alloc_pinned(16 * sizeof(int)));
-  eig.reset(new EigWork(n));
+  if (with_eig) eig.reset(new EigWork(n));
 }
 
 Problem::~Problem() {
@@ -59,6 +59,9 @@ Problem::~Problem() {
   }
   aux_.reset();
   aux2_.reset();
+  crit_.reset();
+  if (crit_done) cudaEventDestroy(crit_done);
+  if (crit_after) cudaEventDestroy(crit_after);
   eig.reset();
   for (double* p : owned) dev_free(p);
   host_free_pinned(hsc, 64 * sizeof(double));
@@ -683,10 +686,12 @@ void eg_step(Problem& p, const double* g, const double* X, double s, double* g_o
   proj(p, dc, nullptr, X_out);
 }
 
-static void make_context(Problem& src, std::unique_ptr<Problem>& dst) {
+static void make_context(Problem& src, std::unique_ptr<Problem>& dst, bool high_priority = false,
+                         bool with_eig = true) {
   KOT_CUDA(cudaSetDevice(src.device));
   dst.reset(new Problem());
   Problem& a = *dst;
+  a.with_eig = with_eig;
   a.n = src.n;
   a.device = src.device;
   a.l1 = src.l1;
@@ -698,11 +703,24 @@ static void make_context(Problem& src, std::unique_ptr<Problem>& dst) {
   a.z = src.z;
   a.R = src.R;
   a.embed = src.embed;
-  a.lane = 1;
+  a.lane = high_priority ? 0 : 1;
   int lo = 0, hi = 0;
   KOT_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  KOT_CUDA(cudaStreamCreateWithPriority(&a.st, cudaStreamNonBlocking, lo));
+  KOT_CUDA(cudaStreamCreateWithPriority(&a.st, cudaStreamNonBlocking, high_priority ? hi : lo));
   a.init_scratch();
+}
+
+Problem& Problem::crit() {
+  if (!crit_) {
+    make_context(*this, crit_, true, false);
+    Problem& c = *crit_;
+    c.crit_dg = c.alloc(n);
+    c.crit_dX = c.alloc((long)n * n);
+    c.crit_e1 = c.alloc(n);
+    KOT_CUDA(cudaEventCreateWithFlags(&c.crit_done, cudaEventDisableTiming));
+    KOT_CUDA(cudaEventCreateWithFlags(&c.crit_after, cudaEventDisableTiming));
+  }
+  return *crit_;
 }
 
 Problem& Problem::aux2() {

@@ -75,9 +75,15 @@ struct Problem {
   double* ygather = nullptr;  // shard_block·world doubles
   int emul_world = 1;          // test hook: all row blocks in turn on one device, no NCCL
   double* shard_tmp = nullptr;  // (⌊ℓ/2⌋+1)·ℓ block partial of T̃ (emulation only)
-  std::unique_ptr<Problem> aux_, aux2_;
+  std::unique_ptr<Problem> aux_, aux2_, crit_;
   Problem& aux();
   Problem& aux2();
+  // high-priority context for the speculative Newton criterion (no eigensolver workspace):
+  // its stream, scratch, outputs (crit_dg, crit_dX, crit_e1) and completion event
+  Problem& crit();
+  double *crit_dg = nullptr, *crit_dX = nullptr, *crit_e1 = nullptr;
+  cudaEvent_t crit_done = nullptr, crit_after = nullptr;
+  bool with_eig = true;
   double* alloc(long count);
   void init_scratch();
   ~Problem();
