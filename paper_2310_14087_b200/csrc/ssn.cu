@@ -723,13 +723,31 @@ Problem& Problem::crit() {
   return *crit_;
 }
 
+// Background (EG pipeline) contexts: lowest stream priority at moderate ℓ, where the Newton chain
+// is the critical path (cfg3: 8.30 vs 8.12 it/s); highest from ℓ = 4096, where the pipeline's two
+// sequential eigensolves per EG step are (cfg4: 0.453 vs 0.437 it/s).  KOT_EG_PRIORITY=low|high.
+static bool eg_high_priority(int n) {
+  static const int v = [] {
+    const char* e = std::getenv("KOT_EG_PRIORITY");
+    if (!e) return -1;
+    return std::string(e) == "high" ? 1 : 0;
+  }();
+  return v < 0 ? n >= 4096 : v == 1;
+}
+
 Problem& Problem::aux2() {
-  if (!aux2_) make_context(*this, aux2_);
+  if (!aux2_) {
+    make_context(*this, aux2_, eg_high_priority(n));
+    aux2_->lane = 1;
+  }
   return *aux2_;
 }
 
 Problem& Problem::aux() {
-  if (!aux_) make_context(*this, aux_);
+  if (!aux_) {
+    make_context(*this, aux_, eg_high_priority(n));
+    aux_->lane = 1;
+  }
   return *aux_;
 }
 
