@@ -424,7 +424,10 @@ static int trd_grid_cap(int lane) {
   // measured (probe cfg3, speculative Newton criterion): 48 → 7.9, 56 → 8.2, 64 → 8.25, 72 → 8.0,
   // 80+ → 7.1–7.2 it/s (two background grids no longer fit beside a full lane-0 grid)
   static const int cap_bg = std::min(env_int("KOT_TRD_GRID_BG", 64), cap);
-  return lane == 0 ? cap : cap_bg;
+  // lane 2 = the EG pipeline's residual thread (one eigensolve per step, slack), lane 1 = its EG-step
+  // thread (two sequential eigensolves per step, the pipeline's critical chain)
+  static const int cap_bg2 = std::min(env_int("KOT_TRD_GRID_BG2", cap_bg), cap);
+  return lane == 0 ? cap : (lane == 2 ? cap_bg2 : cap_bg);
 }
 static int trd_grid(int rows, int lane) {
   // never below what the per-warp row capacity needs (TRD_RPW rows per warp)

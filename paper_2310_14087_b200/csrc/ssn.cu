@@ -738,7 +738,7 @@ static bool eg_high_priority(int n) {
 Problem& Problem::aux2() {
   if (!aux2_) {
     make_context(*this, aux2_, eg_high_priority(n));
-    aux2_->lane = 1;
+    aux2_->lane = 2;  // residual thread of the EG pipeline
   }
   return *aux2_;
 }
