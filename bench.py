@@ -416,9 +416,9 @@ def run_batch(args):
     """Config 5: a batch of independent problems sharded over ranks, `--concurrency` solves per GPU,
     records gathered to rank 0.  Metric: completed OT problems/s (whole job)."""
     # several solves share the GPU: thinner cooperative panel grids let their eigensolves run side by
-    # side (measured: 12 problems x 100 iterations, 0.45 problems/s at 148 CTAs x 3 concurrent ->
-    # 0.60 at 64 CTAs x 4 concurrent)
-    os.environ.setdefault("KOT_TRD_GRID", "64")
+    # side (measured, 16 problems x 100 iterations: 0.45 problems/s at 148 CTAs x 3 concurrent,
+    # 0.53 at 64 x 4, 0.60 at 48 x 6, 0.59 at 40 x 8)
+    os.environ.setdefault("KOT_TRD_GRID", "48")
     world, rank, local = dist_setup(args.gpus)
     os.environ["KOT_DEVICE"] = str(local)
     import torch
@@ -476,7 +476,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-6 leg")
     ap.add_argument("--batch", type=int, default=16, help="cfg5: number of problems")
-    ap.add_argument("--concurrency", type=int, default=4, help="cfg5: concurrent solves per GPU")
+    ap.add_argument("--concurrency", type=int, default=6, help="cfg5: concurrent solves per GPU")
     ap.add_argument("--tol", type=float, default=1e-6, help="cfg5: residual tolerance")
     ap.add_argument("--max-iter", type=int, default=300, help="cfg5: max SSN iterations per problem")
     args = ap.parse_args()
