@@ -1304,7 +1304,8 @@ __global__ void count_pos_kernel(const double* vals, int n, int* k) {
 // Back-transform P ← H_0 H_1 ⋯ H_{n−2} P in compact-WY blocks of ORM_NB
 // reflectors (I − V T Vᵀ), last block first: W1 = Vᵀ P (split-K), W2 = T W1,
 // P −= V W2.
-static void ormtr(int n, EigWork& w, double* P, cudaStream_t st) {
+// dcols (nullable, device): only the first *dcols columns of P are transformed.
+static void ormtr(int n, EigWork& w, double* P, cudaStream_t st, const int* dcols = nullptr) {
   const int nref = n - 1;  // reflectors 0..n-2
   const int nblk = (nref + ORM_NB - 1) / ORM_NB;
   double* S = w.Tf + ORM_NB * ORM_NB;
@@ -1332,17 +1333,20 @@ static void ormtr(int n, EigWork& w, double* P, cudaStream_t st) {
     }
     {  // W1 = Vᵀ P[r0:, :]
       GemmShape s = make_shape(nb, n, mrows, Vp, n, P + (long)r0 * n, n);
+      s.dN = dcols;
       s.ws = w.splitws;
       s.ksplit = choose_ksplit(s, w.splitws_cap);
       gemm_launch<true, false>(s, EpiAxpby{W1, n, 1.0, 0.0}, st);
     }
     {  // W2 = T W1   (T upper triangular: K range starts at the row tile)
       GemmShape s = make_shape(nb, n, nb, T, nb, W1, n);
+      s.dN = dcols;
       s.kb_m = 1;
       gemm_launch<false, false>(s, EpiAxpby{W2, n, 1.0, 0.0}, st);
     }
     {  // P[r0:, :] −= V W2
       GemmShape s = make_shape(mrows, n, nb, Vp, n, W2, n);
+      s.dN = dcols;
       gemm_launch<false, false>(s, EpiAxpby{P + (long)r0 * n, n, -1.0, 1.0}, st);
     }
   }
@@ -1439,7 +1443,7 @@ void tridiag_device(const double* Z, int n, EigWork& w, cudaStream_t st, int sta
 }
 
 void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigWork& w, cudaStream_t st,
-                  int lane) {
+                  int lane, bool alpha_only) {
   if (n == 1) {
     eig1_kernel<<<1, 1, 0, st>>>(Z, P, vals);
     KOT_LAUNCH_CHECK();
@@ -1456,8 +1460,15 @@ void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigW
     ProfScope ps("eig.ormtr", st, 2.0 * n * (double)n * n);
     reverse_cols_kernel<<<std::min(ceil_div((long)n * n, 256), 2048), 256, 0, st>>>(w.Q, w.d, P, vals, n);
     KOT_LAUNCH_CHECK();
-    if (two) two_stage_q2_apply(n, w, P, st);
-    ormtr(n, w, P, st);
+    // α-only (PSD projection): the back-transforms act on the σ > 0 columns only (k read on device)
+    const int* dcols = nullptr;
+    if (alpha_only) {
+      count_pos_kernel<<<1, 256, 0, st>>>(vals, n, dk);
+      KOT_LAUNCH_CHECK();
+      dcols = dk;
+    }
+    if (two) two_stage_q2_apply(n, w, P, st, dcols);
+    ormtr(n, w, P, st, dcols);
   }
   count_pos_kernel<<<1, 256, 0, st>>>(vals, n, dk);
   KOT_LAUNCH_CHECK();

@@ -909,7 +909,7 @@ constexpr int QW_LDV = QG + 4;
 constexpr int QW_SMEM = (2 * QW_RW * QW_LDW + QW_RW * QW_LDV + QG * QW_LDV + 2 * QG * QW_LDW) * 8;
 __global__ void __launch_bounds__(256) q2_wave_kernel(double* P, int n, const double* __restrict__ Vq2,
                                                       const double* __restrict__ Tq2, int NT, int wave, int Ilo,
-                                                      int tile0, int tile1) {
+                                                      int tile0, int tile1, const int* dcols) {
   extern __shared__ double qw[];
   double* Wb = qw;                       // [2][QW_RW][QW_LDW]
   double* Vd = Wb + 2 * QW_RW * QW_LDW;  // [QW_RW][QW_LDV]: Vd[ρ][j] = v_j[ρ − j]
@@ -921,7 +921,10 @@ __global__ void __launch_bounds__(256) q2_wave_kernel(double* P, int n, const do
   const int ilo = I * QG;
   const int r0 = ilo + 1 + t * SB;
   const int nr = min(QG_ROWS, n - r0);
-  const int tbeg = tile0 + blockIdx.x * QW_TPC, tend = min(tile1, tbeg + QW_TPC);
+  const int tbeg = tile0 + blockIdx.x * QW_TPC;
+  int tend = min(tile1, tbeg + QW_TPC);
+  if (dcols) tend = min(tend, (*dcols + QW_COLS - 1) / QW_COLS);  // α-only back-transform
+  if (tbeg >= tend) return;
   const int tid = threadIdx.x;
   auto issue = [&](int tile, int buf) {
     const int c0 = tile * QW_COLS, wc = min(QW_COLS, n - c0);
@@ -1002,7 +1005,7 @@ __global__ void __launch_bounds__(256) q2_wave_kernel(double* P, int n, const do
   }
 }
 
-void two_stage_q2_apply(int n, EigWork& w, double* P, cudaStream_t st) {
+void two_stage_q2_apply(int n, EigWork& w, double* P, cudaStream_t st, const int* dcols) {
   if (n < 3) return;
   ProfScope ps("eig.q2", st, 2.0 * n * (double)n * n);
   const int NT = eig_nt(n);
@@ -1028,7 +1031,7 @@ void two_stage_q2_apply(int n, EigWork& w, double* P, cudaStream_t st) {
       while (Ihi >= Ilo && wv + Ihi > (n - 2 - Ihi * QG) / SB) --Ihi;
       if (Ihi < Ilo) continue;
       dim3 grid(ceil_div(nt, QW_TPC), Ihi - Ilo + 1);
-      q2_wave_kernel<<<grid, 256, QW_SMEM, st>>>(P, n, w.Vq2, w.Tq2, NT, wv, Ilo, tb, tb + nt);
+      q2_wave_kernel<<<grid, 256, QW_SMEM, st>>>(P, n, w.Vq2, w.Tq2, NT, wv, Ilo, tb, tb + nt, dcols);
       KOT_LAUNCH_CHECK();
     }
   }

@@ -49,11 +49,14 @@ struct EigWork {
 long two_stage_q2_size(int n);
 long two_stage_t_size(int n);
 void two_stage_tridiag(const double* Z, int n, EigWork& w, cudaStream_t st);
-void two_stage_q2_apply(int n, EigWork& w, double* P, cudaStream_t st);  // P ← Q2 P
+void two_stage_q2_apply(int n, EigWork& w, double* P, cudaStream_t st,
+                        const int* dcols = nullptr);  // P ← Q2 P (first *dcols columns if set)
 bool use_two_stage(int n, int lane);
 // tridiagonal form only (debug/tests): stages = 1 (one-stage sytrd) or 2
 void tridiag_device(const double* Z, int n, EigWork& w, cudaStream_t st, int stages);
+// alpha_only: only the eigenvectors of σ > 0 (the first *dk columns) are back-transformed — enough
+// for the PSD projection; the other columns of P are left unspecified.
 void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigWork& w, cudaStream_t st,
-                  int lane = 0);
+                  int lane = 0, bool alpha_only = false);
 
 }  // namespace kot

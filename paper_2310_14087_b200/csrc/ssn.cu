@@ -545,9 +545,9 @@ void phi_adjoint_ex(Problem& p, const double* g, double* out, double alpha, cons
 
 void phi_adjoint(Problem& p, const double* g, double* out) { phi_adjoint_ex(p, g, out, 1.0, nullptr, 0.0, 0.0); }
 
-void eigh(Problem& p, const double* Z, Decomp& dc) {
+void eigh(Problem& p, const double* Z, Decomp& dc, bool alpha_only) {
   ProfScope ps("eigh", p.st, 14.0 / 3.0 * p.n * (double)p.n * p.n);
-  syevd_device(Z, p.n, dc.P, dc.vals, p.dk, *p.eig, p.st, p.lane);
+  syevd_device(Z, p.n, dc.P, dc.vals, p.dk, *p.eig, p.st, p.lane, alpha_only);
   KOT_CUDA(cudaMemcpyAsync(p.hk, p.dk, sizeof(int), cudaMemcpyDeviceToHost, p.st));
   KOT_CUDA(cudaStreamSynchronize(p.st));
   dc.k = p.hk[0];
@@ -676,13 +676,13 @@ void eg_step(Problem& p, const double* g, const double* X, double s, double* g_o
   finalize(p, FIN_RES, g, true, nullptr, 0.0, b.e1);
   axpby(p, n, 1.0, g, -s, b.e1, b.e2);            // γ½ = γ − s g_vec
   phi_adjoint_ex(p, g, p.M1, -s, X, 1.0, p.l1);     // X − s (Φ*(γ) + λ₁I)
-  eigh(p, p.M1, dc);
+  eigh(p, p.M1, dc, true);                          // projection only: α eigenvectors suffice
   proj(p, dc, nullptr, b.Xh);                       // X½ = Π(·)
   phi_partials(p, b.Xh);
   finalize(p, FIN_RES, b.e2, true, nullptr, 0.0, b.e1);
   phi_adjoint_ex(p, b.e2, p.M1, -s, X, 1.0, p.l1);  // X − s (Φ*(γ½) + λ₁I)
   axpby(p, n, 1.0, g, -s, b.e1, g_out);             // γ − s g_vec(½)
-  eigh(p, p.M1, dc);
+  eigh(p, p.M1, dc, true);
   proj(p, dc, nullptr, X_out);
 }
 

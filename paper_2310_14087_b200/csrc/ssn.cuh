@@ -97,7 +97,7 @@ std::unique_ptr<Problem> problem_assemble(const double* xs, int nx, const double
 // ---- operators (device pointers in/out, all on p.st)
 void phi_forward(Problem& p, const double* X, double* out);
 void phi_adjoint(Problem& p, const double* g, double* out);
-void eigh(Problem& p, const double* Z, Decomp& dc);
+void eigh(Problem& p, const double* Z, Decomp& dc, bool alpha_only = false);
 void proj(Problem& p, const Decomp& dc, const double* X, double* out);  // out = X − Π (X!=null) or Π
 // mode 0: eliminator 𝒯 with μ; mode 1: projection Jacobian M. force_path: -1 auto, 0 POS, 1 NONPOS.
 void spectral_filter(Problem& p, const Decomp& dc, const double* S, double* out, double mu, int mode,
