@@ -321,6 +321,9 @@ def run_gpu(args):
     rep = K.solve(pd_host, cfg_e)
     torch.cuda.synchronize()
     t_e2e = time.perf_counter() - t0
+    if os.environ.get("KOT_BENCH_DEBUG"):
+        print(f"e2e: {t_e2e * 1e3:.1f} ms, solve total_ms {rep.total_ms:.1f}, steps "
+              f"{[round(r.step_ms) for r in rep.trace]}", file=sys.stderr, flush=True)
     barrier(world)
     t_e2e = max_over_ranks(world, t_e2e, local)
     n = pd.n
