@@ -323,7 +323,7 @@ def run_gpu(args):
     t_e2e = time.perf_counter() - t0
     if os.environ.get("KOT_BENCH_DEBUG"):
         print(f"e2e: {t_e2e * 1e3:.1f} ms, solve total_ms {rep.total_ms:.1f}, steps "
-              f"{[round(r.step_ms) for r in rep.trace]}", file=sys.stderr, flush=True)
+              f"{[round(r.step_ms) for r in rep.trace]} {''.join(r.accepted[0] for r in rep.trace)}", file=sys.stderr, flush=True)
     barrier(world)
     t_e2e = max_over_ranks(world, t_e2e, local)
     n = pd.n

@@ -308,6 +308,7 @@ static void copy_state(Problem& p, Bufs& b, Decomp& dw, const Decomp& dv) {
 struct EgSlot {
   double *g = nullptr, *X = nullptr, *r1 = nullptr, *r2 = nullptr, *P = nullptr, *vals = nullptr;
   int k = 0;
+  bool alpha_only = false;  // P holds only the σ > 0 eigenvectors
   double res = 0.0, eg_ms = 0.0, resid_ms = 0.0;
   std::exception_ptr err = nullptr;
 };
@@ -406,7 +407,15 @@ class EgPipeline {
         KOT_CUDA(cudaSetDevice(b.device));
         const auto t0 = clk::now();
         Decomp dc{sl.P, sl.vals, 0};
-        sl.res = residual_parts(b, sl.g, sl.X, sl.r1, sl.r2, dc);
+        // The decomposition at v is only needed if the EG step is accepted (w ← v), which the
+        // trajectories practically never do: compute the σ > 0 part only and
+        // redo the full decomposition on acceptance (same kernels, same input → same result).
+        static const bool kAlpha = [] {
+          const char* e = std::getenv("KOT_PIPE_ALPHA");
+          return !(e && std::atoi(e) == 0);
+        }();
+        sl.res = residual_parts(b, sl.g, sl.X, sl.r1, sl.r2, dc, kAlpha);
+        sl.alpha_only = kAlpha;
         sl.k = dc.k;
         sl.resid_ms = ms_since(t0);
         prof_host("host.pipe_resid", sl.resid_ms);
@@ -546,11 +555,15 @@ static bool loop_body(Problem& p, const SolverCfg& cfg, LoopState& s, int k, Ite
       EgSlot& sl = *s.vslot;
       KOT_CUDA(cudaMemcpyAsync(b.gw, sl.g, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
       KOT_CUDA(cudaMemcpyAsync(b.Xw, sl.X, sizeof(double) * nn, cudaMemcpyDeviceToDevice, p.st));
-      KOT_CUDA(cudaMemcpyAsync(b.r1w, sl.r1, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
-      KOT_CUDA(cudaMemcpyAsync(b.r2w, sl.r2, sizeof(double) * nn, cudaMemcpyDeviceToDevice, p.st));
-      KOT_CUDA(cudaMemcpyAsync(s.dw.P, sl.P, sizeof(double) * nn, cudaMemcpyDeviceToDevice, p.st));
-      KOT_CUDA(cudaMemcpyAsync(s.dw.vals, sl.vals, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
-      s.dw.k = sl.k;
+      if (sl.alpha_only) {  // full decomposition at v for the next Newton step
+        (void)residual_parts(p, b.gw, b.Xw, b.r1w, b.r2w, s.dw);
+      } else {
+        KOT_CUDA(cudaMemcpyAsync(b.r1w, sl.r1, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
+        KOT_CUDA(cudaMemcpyAsync(b.r2w, sl.r2, sizeof(double) * nn, cudaMemcpyDeviceToDevice, p.st));
+        KOT_CUDA(cudaMemcpyAsync(s.dw.P, sl.P, sizeof(double) * nn, cudaMemcpyDeviceToDevice, p.st));
+        KOT_CUDA(cudaMemcpyAsync(s.dw.vals, sl.vals, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
+        s.dw.k = sl.k;
+      }
     } else {
       copy_state(p, b, s.dw, s.dv);
     }

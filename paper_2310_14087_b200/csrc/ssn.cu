@@ -640,7 +640,8 @@ void spectral_filter(Problem& p, const Decomp& dc, const double* S, double* out,
   KOT_LAUNCH_CHECK();
 }
 
-double residual_parts(Problem& p, const double* g, const double* X, double* r1, double* r2, Decomp& dc) {
+double residual_parts(Problem& p, const double* g, const double* X, double* r1, double* r2, Decomp& dc,
+                      bool alpha_only) {
   ProfScope ps("residual", p.st);
   const int n = p.n;
   const long nn = (long)n * n;
@@ -648,7 +649,7 @@ double residual_parts(Problem& p, const double* g, const double* X, double* r1, 
   finalize(p, FIN_RES, g, true, nullptr, 0.0, r1);
   // Z = X − (Φ*(γ) + λ₁ I)
   phi_adjoint_ex(p, g, p.M1, -1.0, X, 1.0, p.l1);
-  eigh(p, p.M1, dc);
+  eigh(p, p.M1, dc, alpha_only);
   proj(p, dc, X, r2);
   dev_reduce(p, r1, nullptr, n, 0, true);
   dev_reduce(p, r2, nullptr, nn, 1, true);

@@ -102,7 +102,9 @@ void proj(Problem& p, const Decomp& dc, const double* X, double* out);  // out =
 // mode 0: eliminator 𝒯 with μ; mode 1: projection Jacobian M. force_path: -1 auto, 0 POS, 1 NONPOS.
 void spectral_filter(Problem& p, const Decomp& dc, const double* S, double* out, double mu, int mode,
                      int force_path = -1);
-double residual_parts(Problem& p, const double* g, const double* X, double* r1, double* r2, Decomp& dc);
+// alpha_only: the decomposition holds only the σ > 0 eigenvectors (enough for r2 and the norm)
+double residual_parts(Problem& p, const double* g, const double* X, double* r1, double* r2, Decomp& dc,
+                      bool alpha_only = false);
 void middle_operator(Problem& p, const Decomp& dc, double mu, const double* v, double* out);
 void eg_step(Problem& p, const double* g, const double* X, double s, double* g_out, double* X_out);
 
