@@ -313,16 +313,21 @@ def run_gpu(args):
                             lambda1=pd.lambda1, lambda2=pd.lambda2, embed_sum=pd.embed_sum.copy())
     cfg_e = K.SolverConfig(newton=newton_cfg(args.profile), eg=K.EgConfig(stepsize), residual_tol=1e-300,
                            max_iter=args.steps)
+    debug = bool(os.environ.get("KOT_BENCH_DEBUG"))
     torch.cuda.synchronize()
     barrier(world)
+    if debug:
+        _lib.profile_enable(True)
     t0 = time.perf_counter()
     if rowshard:  # upload + NCCL communicator setup inside the timed region
         RS.shard_rows(pd_host)
     rep = K.solve(pd_host, cfg_e)
     torch.cuda.synchronize()
     t_e2e = time.perf_counter() - t0
-    if os.environ.get("KOT_BENCH_DEBUG"):
-        print(f"e2e: {t_e2e * 1e3:.1f} ms, solve total_ms {rep.total_ms:.1f}, steps "
+    if debug:
+        hp = {k: round(v["ms"], 1) for k, v in _lib.profile_read().items() if k.startswith("solve.")}
+        _lib.profile_enable(False)
+        print(f"e2e: {t_e2e * 1e3:.1f} ms, solve total_ms {rep.total_ms:.1f} {hp}, steps "
               f"{[round(r.step_ms) for r in rep.trace]} {''.join(r.accepted[0] for r in rep.trace)}", file=sys.stderr, flush=True)
     barrier(world)
     t_e2e = max_over_ranks(world, t_e2e, local)
@@ -397,7 +402,9 @@ def run_gpu(args):
                    "parallelism": f"rowshard{world} (CG matvec rows over NCCL)" if rowshard else f"replicas{world}"},
         "e2e": {"value": e2e_iters / t_e2e, "unit": "iter/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": "paper_2310_14087_b200.solve(ProblemData from host arrays)",
-                "iterations": rep.iterations},
+                "iterations": rep.iterations, "wall_ms": round(t_e2e * 1e3, 1),
+                "solve_ms": round(rep.total_ms, 1),
+                "iterations_ms": round(sum(r.step_ms for r in rep.trace), 1)},
         "gpu_launches": int(launches),
         "roofline": roof,
         "roofline_gemm": roof_gemm,

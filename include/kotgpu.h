@@ -168,7 +168,8 @@ int kot_phi_adjoint(kot_problem* p, const double* gamma, double* out);  /* probl
 int kot_residual_parts(kot_problem* p, const double* gamma, const double* x, double* r1, double* r2,
                        double* eigvals, int* n_pos, double* res_norm);
 /* middle_operator (newton.py:116-128) at the context of w with damping theta.
- * form 0: structure-reduced B = R·P form used by the solver; 1: reference form Φ(𝒯[Φ*(v)]). */
+ * form 0: structure-reduced B = R·P form used by the solver (same-sign block as (G_a∘G_a)v/mu);
+ * 1: reference form Φ(𝒯[Φ*(v)]); 2: structure-reduced, whole sign block in the GEMMs (row-sharded layout). */
 int kot_middle_operator(kot_problem* p, const double* gamma, const double* x, double theta,
                         const double* v, int form, double* out, double* mu_out);
 /* newton_direction (newton.py:144-195) at w with damping theta. */

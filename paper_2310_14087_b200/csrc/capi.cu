@@ -449,9 +449,9 @@ int kot_middle_operator(kot_problem* h, const double* gamma, const double* x, do
     if (form == 1) {
       kot::middle_operator(p, dc, mu, b.e2, b.e1);  // reference form Φ(𝒯[Φ*(v)])
     } else {
-      kot::MvCtx mv;
-      kot::matvec_prepare(p, dc, mu, mv);
-      kot::middle_operator_fast(p, mv, b.e2, b.e1);  // structure-reduced form (the solver's)
+      kot::MvCtx mv;  // structure-reduced form: 0 the solver's, 2 the row-sharding layout
+      kot::matvec_prepare(p, dc, mu, mv, form != 2);
+      kot::middle_operator_fast(p, mv, b.e2, b.e1);
     }
     down(p, out, b.e1, p.n);
     KOT_CUDA(cudaStreamSynchronize(p.st));

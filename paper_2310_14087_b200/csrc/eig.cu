@@ -21,6 +21,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cfloat>
 #include <condition_variable>
 #include <mutex>
@@ -37,8 +38,9 @@ constexpr int TRD_NB = 32;
 constexpr int TRD_THREADS = 256;
 constexpr int TRD_WARPS = TRD_THREADS / 32;
 constexpr int TRD_PSTRIDE = 2 * TRD_NB + 2;
-constexpr int TRD_GRP = 8;                                    // CTAs per partial-reduction group
-constexpr int TRD_NGRP = (kNumSMs + TRD_GRP - 1) / TRD_GRP;  // ≤ 19 groups
+constexpr int TRD_CL = 4;  // CTAs per cluster of the panel kernel (148 = 37 × 4)
+constexpr int TRD_GRP = 8;
+constexpr int TRD_NGRP = (kNumSMs + TRD_GRP - 1) / TRD_GRP;
 constexpr int DC_LEAF = 32;
 constexpr double DEPS = DBL_EPSILON * 0.5;  // LAPACK dlamch('E')
 
@@ -147,6 +149,7 @@ constexpr int TRD_RPW = 8;  // rows per warp: n ≤ TRD_RPW · 8 · 148 = 9472
 
 __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) {
   cg::grid_group grid = cg::this_grid();
+  cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ double dsm[];
   // dynamic smem: [Vs | Ws | Ac] (TRD_WARPS × TRD_RPW × NB each) then the Householder vector (n)
   typedef double RowBlk[TRD_RPW][TRD_NB];
@@ -159,9 +162,11 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
   __shared__ double wrow[TRD_NB], vrow[TRD_NB];
   __shared__ double nrm_sh[TRD_WARPS];
   __shared__ double scal_sh[2];
+  __shared__ double cpart[TRD_PSTRIDE];
 
   const int n = a.n, p0 = a.p0, nb = a.nb;
   const int G = gridDim.x;
+  const int NCL = G / TRD_CL;  // clusters
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int gw = blockIdx.x * TRD_WARPS + wid;
   const int NW = G * TRD_WARPS;
@@ -216,7 +221,7 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
 #pragma unroll
           for (int u = 0; u < GPL; ++u) {
             const int g = lane + 32 * u;
-            v[u] = (need && g < G) ? __ldcg(a.part + (long)q * kNumSMs + g) : 0.0;
+            v[u] = (need && g < NCL) ? __ldcg(a.part + (long)q * kNumSMs + g) : 0.0;
           }
           double s = 0.0;
 #pragma unroll
@@ -294,9 +299,24 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
     // ------------------------------------------------------------ phase S
     const int m = n - c - 1;
     // stage x (unscaled) while warp 0 reduces the norm partials
-    for (int s = threadIdx.x; s < m; s += blockDim.x) vsh[s] = a.xv[c + 1 + s];
+    {  // all loads in flight before the stores (one L2 round trip for m ≤ 2048)
+      constexpr int XB = 8;
+      for (int s0 = threadIdx.x; s0 < m; s0 += XB * TRD_THREADS) {
+        double t[XB];
+#pragma unroll
+        for (int u = 0; u < XB; ++u) {
+          const int s = s0 + u * TRD_THREADS;
+          t[u] = (s < m) ? __ldcg(a.xv + c + 1 + s) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < XB; ++u) {
+          const int s = s0 + u * TRD_THREADS;
+          if (s < m) vsh[s] = t[u];
+        }
+      }
+    }
     if (wid == 0) {
-      const double alpha = a.xv[c + 1];  // issued together with the partial loads
+      const double alpha = __ldcg(a.xv + c + 1);  // issued together with the partial loads
       constexpr int GPL = (kNumSMs + 31) / 32;
       double v[GPL];
 #pragma unroll
@@ -392,10 +412,21 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
     if (lane == 0) sred[wid][2 * TRD_NB] = pyv;
     __syncthreads();
     TRD_MARK(5)
+    // first reduction level inside the cluster (DSMEM), so that every CTA reads G/TRD_CL partials
+    // after the grid barrier instead of G (148 CTAs reading the same 77 KB was the costliest step)
     for (int q = threadIdx.x; q <= 2 * TRD_NB; q += blockDim.x) {
       double s = 0.0;
       for (int w = 0; w < TRD_WARPS; ++w) s += sred[w][q];
-      a.part[(long)q * kNumSMs + blockIdx.x] = s;
+      cpart[q] = s;
+    }
+    cluster.sync();
+    if (cluster.block_rank() == 0) {
+      for (int q = threadIdx.x; q <= 2 * TRD_NB; q += blockDim.x) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < TRD_CL; ++r) s += cluster.map_shared_rank(cpart, r)[q];
+        a.part[(long)q * kNumSMs + blockIdx.x / TRD_CL] = s;
+      }
     }
     TRD_MARK(6)
     grid.sync();
@@ -410,29 +441,36 @@ __global__ void set_last_diag_kernel(const double* A, int n, double* d) { d[n - 
 
 unsigned long long* g_trd_dbg = nullptr;  // set by kot_debug_sytrd_timing
 
-// CTAs of the cooperative panel kernel (≤ one per SM).  The latency-critical
-// caller (lane 0, Newton chain) uses every SM; background eigensolves (lane 1,
-// EG pipeline) use KOT_TRD_GRID_BG CTAs so that they leave SMs to the Newton
-// chain's kernels.  KOT_TRD_GRID caps both (diagnostic).
+// CTAs of the cooperative panel kernel (≤ one per SM, whole clusters).  KOT_TRD_GRID caps every
+// lane, KOT_TRD_GRID_FG/_BG/_BG2 set the per-lane sizes under an EG pipeline (diagnostics).
 static int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   const int v = e ? std::atoi(e) : 0;
   return v > 0 ? v : dflt;
 }
+// Number of live EG pipelines (solver.cu): while one runs, three eigensolve chains share the GPU.
+static std::atomic<int> g_pipelines{0};
+void eig_pipeline_active(int delta) { g_pipelines += delta; }
+
 static int trd_grid_cap(int lane) {
-  static const int cap = std::min(env_int("KOT_TRD_GRID", kNumSMs), kNumSMs);
-  // measured (probe cfg3, speculative Newton criterion): 48 → 7.9, 56 → 8.2, 64 → 8.25, 72 → 8.0,
-  // 80+ → 7.1–7.2 it/s (two background grids no longer fit beside a full lane-0 grid)
-  static const int cap_bg = std::min(env_int("KOT_TRD_GRID_BG", 64), cap);
-  // lane 2 = the EG pipeline's residual thread (one eigensolve per step, slack), lane 1 = its EG-step
-  // thread (two sequential eigensolves per step, the pipeline's critical chain)
-  static const int cap_bg2 = std::min(env_int("KOT_TRD_GRID_BG2", cap_bg), cap);
-  return lane == 0 ? cap : (lane == 2 ? cap_bg2 : cap_bg);
+  static const int cap = std::max(TRD_CL, std::min(env_int("KOT_TRD_GRID", kNumSMs), kNumSMs) / TRD_CL * TRD_CL);
+  // With an EG pipeline running, the three cooperative grids (Newton chain 96, EG step 96, residual
+  // at v 64 CTAs) fit co-resident in the 2 × 148 slots, so no chain waits at the gate for another's
+  // panel (probe cfg3, H-form matvec: 148/64/64 → 8.5, 96/96/64 → 9.6–9.8, 80/96/64 9.7,
+  // 112/96/64 9.4, 96/128/64 9.7, 96/96/48 9.6 it/s).  Alone, lane 0 uses every SM.
+  static const int cap_fg = std::min(env_int("KOT_TRD_GRID_FG", 96), cap);
+  static const int cap_bg = std::min(env_int("KOT_TRD_GRID_BG", 96), cap);
+  // lane 2 = the EG pipeline's residual thread (one eigensolve per step), lane 1 = its EG-step
+  // thread (two sequential eigensolves per step)
+  static const int cap_bg2 = std::min(env_int("KOT_TRD_GRID_BG2", 64), cap);
+  if (lane == 0) return g_pipelines.load() > 0 ? cap_fg : cap;
+  return lane == 2 ? cap_bg2 : cap_bg;
 }
 static int trd_grid(int rows, int lane) {
   // never below what the per-warp row capacity needs (TRD_RPW rows per warp)
   const int need = ceil_div(rows, TRD_WARPS * TRD_RPW);
-  return std::max(need, std::max(1, std::min(trd_grid_cap(lane), ceil_div(rows, TRD_WARPS))));
+  const int g = std::max(need, std::max(1, std::min(trd_grid_cap(lane), ceil_div(rows, TRD_WARPS))));
+  return ceil_div(g, TRD_CL) * TRD_CL;  // whole clusters
 }
 
 static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane) {
@@ -446,7 +484,6 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
     kot_require((long)G * TRD_WARPS * TRD_RPW >= rows, KOT_EINVAL, "matrix order too large for sytrd");
     TrdArgs args{w.A, n, p0, nb, w.X, w.Vall, w.d, w.e, w.tau, w.xv, w.yv, w.part, w.partn, g_trd_dbg,
                  w.gpart, w.gcnt};
-    void* kargs[] = {&args};
     // algorithmic bytes: one read of the lower triangle of every trailing matrix this panel reflects
     double bytes = 0.0;
     for (int c = p0; c < p0 + nb; ++c) bytes += 8.0 * 0.5 * (double)(n - c - 1) * (n - c);
@@ -454,7 +491,21 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
     ensure_smem_attr((const void*)sytrd_panel_kernel, (int)smem);
     {
       ProfScope pscope("sytrd_panel", st, 0.0, bytes);
-      KOT_CUDA(cudaLaunchCooperativeKernel((void*)sytrd_panel_kernel, G, TRD_THREADS, kargs, smem, st));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(TRD_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = TRD_CL;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeCooperative;
+      at[1].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      KOT_CUDA(cudaLaunchKernelEx(&cfg, sytrd_panel_kernel, args));
       KOT_LAUNCH_CHECK();
     }
     // trailing update A22 -= V Wᵀ + W Vᵀ on rows/cols >= p0+nb

@@ -52,6 +52,8 @@ void two_stage_tridiag(const double* Z, int n, EigWork& w, cudaStream_t st);
 void two_stage_q2_apply(int n, EigWork& w, double* P, cudaStream_t st,
                         const int* dcols = nullptr);  // P ← Q2 P (first *dcols columns if set)
 bool use_two_stage(int n, int lane);
+// +1 / −1 when an EG pipeline starts / stops (panel grid sizing for three concurrent chains)
+void eig_pipeline_active(int delta);
 // tridiagonal form only (debug/tests): stages = 1 (one-stage sytrd) or 2
 void tridiag_device(const double* Z, int n, EigWork& w, cudaStream_t st, int stages);
 // alpha_only: only the eigenvectors of σ > 0 (the first *dk columns) are back-transformed — enough

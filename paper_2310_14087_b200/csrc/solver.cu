@@ -331,6 +331,7 @@ class EgPipeline {
     KOT_CUDA(cudaMemsetAsync(v0g_ = p.alloc(n), 0, sizeof(double) * n, p.st));
     KOT_CUDA(cudaMemsetAsync(v0X_ = p.alloc(nn), 0, sizeof(double) * nn, p.st));
     KOT_CUDA(cudaStreamSynchronize(p.st));
+    eig_pipeline_active(+1);
     ta_ = std::thread([this, &a] { run_steps(a); });
     tb_ = std::thread([this, &bb] { run_residuals(bb); });
   }
@@ -342,6 +343,7 @@ class EgPipeline {
     cv_.notify_all();
     ta_.join();
     tb_.join();
+    eig_pipeline_active(-1);
   }
   // Slot of v_j (j >= 1) once its residual is evaluated.  Also releases v_{j-2}.
   EgSlot& acquire(int j) {
@@ -617,9 +619,12 @@ SolveResult solve(Problem& p, const SolverCfg& cfg, IterCallback cb, void* user,
   init_state(p, s);
   SolveResult out{KOT_OK, 0, 0, 0.0, NAN, 0.0};
   HostProbe hp;
+  prof_host("solve.setup", ms_since(t_start));
   // initial residual at the zero pair (solver.py:129-139)
+  const auto t_res0 = clk::now();
   double res0 = pure_eg ? residual_parts(p, b.gv, b.Xv, b.r1v, b.r2v, s.dv)
                         : residual_parts(p, b.gw, b.Xw, b.r1w, b.r2w, s.dw);
+  prof_host("solve.res0", ms_since(t_res0));
   s.res_w = s.res_v = res0;
   s.theta = cfg.theta0;
   int k = 0;
@@ -627,8 +632,10 @@ SolveResult solve(Problem& p, const SolverCfg& cfg, IterCallback cb, void* user,
   bool finite = std::isfinite(res0);
   std::unique_ptr<EgPipeline> pipe;
   if (!pure_eg && finite && !conv) {
+    const auto t_pipe = clk::now();
     pipe.reset(new EgPipeline(p, cfg.eg_stepsize));
     s.pipe = pipe.get();
+    prof_host("solve.pipe_start", ms_since(t_pipe));
   }
   while (finite && !conv && k < cfg.max_iter) {
     IterRecord rec{};

@@ -304,7 +304,7 @@ __global__ void finalize_kernel(FinArgs f) {
       case FIN_RES: o = __dsub_rn(__dsub_rn(qv, f.z[r]) / two_l2, ph); break;
       case FIN_MATVEC: o = __dadd_rn(__dadd_rn(qv / two_l2, __dmul_rn(f.mu, f.u[r])), ph); break;
       case FIN_MATVEC_B: {
-        const double mid = f.G2 ? __dadd_rn(gv / f.mu, -ph) : ph;
+        const double mid = f.G2 ? __dadd_rn(gv / f.mu, f.phsign * ph) : ph;
         o = __dadd_rn(__dadd_rn(qv / two_l2, __dmul_rn(f.mu, f.u[r])), mid);
         break;
       }
@@ -387,6 +387,24 @@ struct EpiMvCoef {
   __device__ void rowdot_store(int, int, double) const {}
 };
 
+// Mixed-sign block only (H form): T̃ = 2ξ∘C on α×ᾱ.  pos: row r = a ∈ α, column c ↔ k + c ∈ ᾱ;
+// else row r ↔ k + r ∈ ᾱ, column c = a ∈ α.  ξ = η/(μ+1−η), η = σ_a/(σ_a − σ_b) (psdcone.py:35-49).
+struct EpiMvOff {
+  static constexpr bool kRowDot = false;
+  double* C;
+  long ldc;
+  const double* vals;
+  int k, pos;
+  double mu;
+  __device__ void store(int r, int c, double v) const {
+    const double sa = pos ? vals[r] : vals[c], sb = pos ? vals[k + c] : vals[k + r];
+    const double eta = sa / (sa - sb);
+    C[(long)r * ldc + c] = 2.0 * ((eta / (mu + 1.0 - eta)) * v);
+  }
+  __device__ double rowdot_weight(int, int) const { return 0; }
+  __device__ void rowdot_store(int, int, double) const {}
+};
+
 // G2 = (R Rᵀ) ∘ (R Rᵀ), once per problem (one triangle, mirrored).
 struct EpiSquareMirror {
   static constexpr bool kRowDot = false;
@@ -417,7 +435,7 @@ static std::vector<std::pair<int, int>> row_blocks(const Problem& p) {
   return v;
 }
 
-void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m) {
+void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allow_hform) {
   const int n = p.n;
   Bufs& b = p.bufs();
   m.dc = dc;
@@ -430,6 +448,12 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m) {
   if (direct) return;
   m.pos = dc.k <= n - dc.k;
   m.B = b.Bm;
+  static const bool full = [] {
+    const char* e = std::getenv("KOT_MATVEC");
+    return e != nullptr && std::string(e) == "full";
+  }();
+  m.hform = allow_hform && !full && p.nccl_comm == nullptr && p.emul_world <= 1;
+  m.H = b.Hm;
   for (const auto& [r0, r1] : row_blocks(p)) {  // B = R P for the row blocks this process owns
     if (r1 > r0) {  // R upper triangular: the K range starts at the block's first row
       GemmShape s = make_shape(r1 - r0, n, n, p.R + (long)r0 * n, n, dc.P, n);
@@ -437,6 +461,19 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m) {
       s.kstart = r0;
       gemm_launch<false, false>(s, EpiAxpby{b.Bm + (long)r0 * n, n, 1.0, 0.0}, p.st);
     }
+  }
+  if (m.hform) {
+    // H = G_α∘G_α, G_α = B_α B_αᵀ (one triangle + mirror, once per Newton step): the α×α block of
+    // W∘(Bᵀdiag(v)B) is the constant 1/μ, so its share of Φ(𝒯[Φ*(v)])_i = Σ_j v_j (b_iα·b_jα)²/μ
+    // is the GEMV (H v)/μ, and only the α×ᾱ block remains for the two GEMMs of every matvec.
+    if (dc.k == 0) {
+      KOT_CUDA(cudaMemsetAsync(m.H, 0, sizeof(double) * n * n, p.st));
+    } else {
+      GemmShape s = make_shape(n, n, dc.k, b.Bm, n, b.Bm, n);
+      s.sym_tiles = 1;
+      gemm_launch<false, true>(s, EpiSquareMirror{m.H, n}, p.st);
+    }
+    return;
   }
   if (!m.pos && p.G2 == nullptr) {
     p.G2 = p.alloc((long)n * n);
@@ -448,14 +485,64 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m) {
   }
 }
 
+// y = Qv/(2λ₂) + μv + (Hv)/μ + Σ_{a∈α, b∈ᾱ} 2ξ_ab (B_{:,a}∘B_{:,b})·C_ab,  C = Bᵀdiag(v)B
+// (one process, no row blocks): two DMMA GEMMs of 2·k(ℓ−k)·ℓ FLOPs each + two GEMVs.
+static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, double* out) {
+  const int n = p.n, k = m.dc.k;
+  const int ks = m.pos ? k : n - k;  // rows of T̃ (the smaller sign block)
+  const int ns = n - ks;
+  const double nn = n;
+  ProfScope ps("matvec", p.st, 4.0 * ks * (double)ns * nn + 4.0 * nn * nn);
+  Bufs& b = p.bufs();
+  const double* Bs = m.pos ? m.B : m.B + k;   // columns of the T̃-row block
+  const double* Bo = m.pos ? m.B + k : m.B;   // columns of the other block
+  if (ks > 0 && ns > 0) {
+    GemmShape s = make_shape(ks, ns, n, Bs, n, Bo, n);
+    s.kscale = v;
+    s.ws = p.splitws;
+    s.ksplit = choose_ksplit(s, p.splitws_cap);
+    static const int mv_split = [] {
+      const char* e = std::getenv("KOT_MV_SPLIT");
+      return e ? std::atoi(e) : 3;
+    }();
+    if (mv_split > 1 && (long)mv_split * s.M * s.N <= p.splitws_cap) s.ksplit = mv_split;
+    gemm_launch<true, false>(s, EpiMvOff{b.Ct, n, m.dc.vals, k, m.pos ? 1 : 0, m.mu}, p.st);
+    GemmShape s2 = make_shape(n, ks, ns, Bo, n, b.Ct, n);
+    gemm_launch<false, true>(s2, EpiRowDot{Bs, n, p.partial, n}, p.st);
+  }
+  FinArgs f;
+  f.n = n;
+  f.mode = FIN_MATVEC_B;
+  f.tiles = (ks > 0 && ns > 0) ? ceil_div(ks, GB_N) : 0;
+  f.tri = 0;
+  f.Q = p.Q;
+  f.G2 = m.H;
+  f.u = v;
+  f.partial = f.tiles > 0 ? p.partial : nullptr;
+  f.z = p.z;
+  f.r1v = nullptr;
+  f.l2 = p.l2;
+  f.mu = m.mu;
+  f.phsign = 1.0;
+  f.out = out;
+  f.r0 = 0;
+  f.r1 = n;
+  finalize_kernel<<<std::min(ceil_div(n, 8), 8 * kNumSMs), 256, 0, p.st>>>(f);
+  KOT_LAUNCH_CHECK();
+}
+
 void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* out) {
   const int n = p.n, k = m.dc.k;
   const int ks = m.pos ? k : n - k;
   const bool nccl = p.nccl_comm != nullptr;
   const auto blocks = row_blocks(p);
   const double nn = n, own = nccl ? p.row1 - p.row0 : n;
-  ProfScope ps("matvec", p.st, 4.0 * ks * nn * own + 2.0 * nn * own);
   Bufs& b = p.bufs();
+  if (m.hform) {
+    middle_operator_hform(p, m, v, out);
+    return;
+  }
+  ProfScope ps("matvec", p.st, 4.0 * ks * nn * own + 2.0 * nn * own);
   const double* Bsub = m.pos ? m.B : m.B + k;
   if (ks > 0) {
     // C = B_subᵀ diag(v) B summed over row blocks, coefficients in the epilogue → T̃ (ks × n).
@@ -501,7 +588,7 @@ void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* o
   f.r1v = nullptr;
   f.l2 = p.l2;
   f.mu = m.mu;
-  f.phsign = 1.0;
+  f.phsign = -1.0;  // complement form: (G2·v)/μ − ph
   f.out = nccl ? p.ygather : out;  // r0 = rank·block: own rows land at ygather[r0 …]
   f.r0 = blocks.front().first;
   f.r1 = blocks.back().second;
@@ -758,7 +845,7 @@ Bufs& Problem::bufs() {
     Bufs& b = *bufs_;
     const long nn = (long)n * n;
     for (double** m : {&b.Xw, &b.Xv, &b.Xt, &b.r2w, &b.r2v, &b.r2t, &b.Pw, &b.Pv, &b.Pt, &b.Pe, &b.Xh, &b.dX,
-                       &b.filt, &b.a2t, &b.Bm, &b.Ct})
+                       &b.filt, &b.a2t, &b.Bm, &b.Ct, &b.Hm})
       *m = alloc(nn);
     for (double** v : {&b.gw, &b.gv, &b.gt, &b.r1w, &b.r1v, &b.r1t, &b.valw, &b.valv, &b.valt, &b.vale, &b.dg,
                        &b.a1, &b.rhs, &b.sol, &b.corr, &b.cx, &b.cr, &b.cp, &b.cap, &b.e1, &b.e2, &b.e3})

@@ -38,7 +38,7 @@ struct Bufs {
   double *Xw, *Xv, *Xt, *r2w, *r2v, *r2t, *Pw, *Pv, *Pt, *Pe, *Xh, *dX, *filt, *a2t;  // n×n
   double *gw, *gv, *gt, *r1w, *r1v, *r1t, *valw, *valv, *valt, *vale, *dg, *a1, *rhs, *sol, *corr;  // n
   double *cx, *cr, *cp, *cap, *e1, *e2, *e3;  // n
-  double *Bm, *Ct;  // n×n: B = R·P, T̃ (structure-reduced matvec)
+  double *Bm, *Ct, *Hm;  // n×n: B = R·P, T̃, H = G_α∘G_α (structure-reduced matvec)
 };
 
 struct Problem {
@@ -114,9 +114,11 @@ struct MvCtx {
   double mu = 0.0;
   bool pos = true;
   bool direct = false;  // diagnostic: KOT_MATVEC=direct uses the reference Φ*→𝒯→Φ chain
+  bool hform = false;   // same-sign block as a GEMV with H = G_α∘G_α (unsharded; KOT_MATVEC=full: off)
   double* B = nullptr;
+  double* H = nullptr;
 };
-void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m);
+void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allow_hform = true);
 // shard.cu
 void nccl_unique_id(char* out128);
 void problem_shard(Problem& p, const char* id128, int rank, int world);

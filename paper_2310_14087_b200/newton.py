@@ -76,13 +76,17 @@ def middle_operator_at(pd: ProblemData, w: IteratePair, theta: float, v, form: s
                        ) -> tuple[np.ndarray, float]:
     """Q v/(2λ₂) + μv + Φ(𝒯[Φ*(v)]) at the context of w (μ = θ‖R(w)‖) (newton.py:95-128).
 
-    ``form="reduced"``: the solver's structure-reduced B = R·P evaluation;
+    ``form="reduced"``: the solver's structure-reduced B = R·P evaluation (same-sign block as
+    the GEMV (G_α∘G_α)v/μ, mixed-sign block as two GEMMs);
+    ``form="blocked"``: the structure-reduced form with the whole smaller sign block in the GEMMs
+    (the row-sharded layout, rowshard.py);
     ``form="direct"``: the reference's Φ* → 𝒯 → Φ chain."""
+    code = {"reduced": 0, "direct": 1, "blocked": 2}[form]
     g, x = _lib.f64(w.gamma, (pd.n,)), _lib.f64(w.x_mat, (pd.n, pd.n))
     vv = _lib.f64(v, (pd.n,))
     out, mu = np.empty(pd.n), C.c_double()
     _lib.check(_lib.lib().kot_middle_operator(pd.device_problem().handle, _lib.ptr(g), _lib.ptr(x), float(theta),
-                                              _lib.ptr(vv), 0 if form == "reduced" else 1, _lib.ptr(out),
+                                              _lib.ptr(vv), code, _lib.ptr(out),
                                               C.byref(mu)))
     return out, float(mu.value)
 

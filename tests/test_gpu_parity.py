@@ -200,7 +200,7 @@ def test_eliminator_and_jacobian_cfg1(cfg1):
     assert rel(mz, cfg1["op_mz"]) <= 1e-11
 
 
-@pytest.mark.parametrize("form", ["reduced", "direct"])
+@pytest.mark.parametrize("form", ["reduced", "blocked", "direct"])
 def test_middle_operator(cfg1, form):
     pd = gpu_pd(cfg1)
     out, mu = GN.middle_operator_at(pd, GP.IteratePair(cfg1["op_g"], cfg1["op_x"]), float(cfg1["op_theta"]),
@@ -209,17 +209,19 @@ def test_middle_operator(cfg1, form):
     assert rel(out, cfg1["op_middle"]) <= 1e-11
 
 
-@pytest.mark.parametrize("shift", [-5.0, 0.0, 5.0])
-def test_middle_operator_both_paths(cfg1, shift):
+@pytest.mark.parametrize("form", ["reduced", "blocked"])
+@pytest.mark.parametrize("shift", [-5.0, 0.0, 5.0, -1e3, 1e3])
+def test_middle_operator_both_paths(cfg1, shift, form):
     """Reduced (B = R·P) vs oracle at states whose spectrum is mostly negative, mixed, mostly
-    positive: exercises the POS and NONPOS (G2 = (RRᵀ)∘(RRᵀ)) branches."""
+    positive, all negative (k = 0), all positive (k = ℓ): exercises the POS and NONPOS
+    (G2 = (RRᵀ)∘(RRᵀ)) branches of both structure-reduced layouts."""
     pd = gpu_pd(cfg1)
     po = oracle_pd(cfg1)
     rng = np.random.default_rng(5)
     x = cfg1["op_x"] + shift * np.eye(pd.n) * np.abs(np.diag(cfg1["op_x"])).mean()
     g = cfg1["op_g"]
     v = rng.standard_normal(pd.n)
-    out, mu = GN.middle_operator_at(pd, GP.IteratePair(g, x), 0.7, v)
+    out, mu = GN.middle_operator_at(pd, GP.IteratePair(g, x), 0.7, v, form=form)
     r, dc = O.residual_parts(po, O.Pair(g, x))
     ctx = O.newton_context(dc, r.norm(), 0.7)
     ref = O.middle_operator(po, ctx.op, ctx.mu)(v)
