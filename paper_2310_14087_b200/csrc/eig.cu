@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
       }
       if (wid < TRD_WARPS - 1) {  // TRD_WARPS−1 warps share the partial columns; every load issued up front
         constexpr int QPW = (2 * TRD_NB + 1 + TRD_WARPS - 2) / (TRD_WARPS - 1);
-        constexpr int GPL = (kNumSMs + 31) / 32;  // partials per lane (G ≤ 148)
+        constexpr int GPL = (kNumSMs / TRD_CL + 31) / 32;  // cluster partials per lane (≤ 37)
         double sq[QPW];
 #pragma unroll
         for (int i = 0; i < QPW; ++i) {

@@ -135,6 +135,10 @@ class ProblemData:
             self._dev = DeviceProblem(h.value, dev)
         return self._dev
 
+    def release_device(self) -> None:
+        """Free the device-resident copy (its memory returns to the library's pool)."""
+        self._dev = None
+
     def pair_gram(self) -> np.ndarray | None:
         """The pair-kernel Gram K (only for instances built by ``assemble``)."""
         return self._kmat
