@@ -1,5 +1,8 @@
 // Pooled device / pinned-host allocation for libkotgpu (see common.cuh).
 #include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -25,7 +28,55 @@ cudaStream_t alloc_stream_locked(int dev) {
   g_alloc_stream[dev] = s;
   return s;
 }
+// Debug canaries (KOT_CANARY=1): every device allocation gets kCanary guard bytes on both sides,
+// filled with 0xAB and verified on free and by canary_check_all (out-of-bounds write detection
+// without a sanitizer).
+constexpr size_t kCanary = 64 * 1024;
+struct Guarded {
+  void* raw;
+  size_t bytes;
+  long seq;
+};
+std::map<void*, Guarded> g_guarded;
+long g_seq = 0;
+bool canary_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("KOT_CANARY");
+    return e && std::atoi(e) > 0;
+  }();
+  return on;
+}
+int check_one(void* user, const Guarded& g, const char* where) {
+  std::vector<unsigned char> h(kCanary);
+  int bad = 0;
+  for (int side = 0; side < 2; ++side) {
+    const char* src = side == 0 ? static_cast<const char*>(g.raw) : static_cast<const char*>(user) + g.bytes;
+    if (cudaMemcpy(h.data(), src, kCanary, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    size_t first = kCanary, last = 0, cnt = 0;
+    for (size_t i = 0; i < kCanary; ++i)
+      if (h[i] != 0xAB) {
+        first = std::min(first, i);
+        last = i;
+        ++cnt;
+      }
+    if (cnt) {
+      std::fprintf(stderr, "[kot canary] %s: alloc #%ld (%zu B) %s guard: %zu bytes changed in [%zu, %zu]\n", where,
+                   g.seq, g.bytes, side == 0 ? "LOW" : "HIGH", cnt, first, last);
+      ++bad;
+    }
+  }
+  return bad;
+}
 }  // namespace
+
+int canary_check_all(const char* where) {
+  if (!canary_on()) return 0;
+  KOT_CUDA(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> lk(g_mu);
+  int bad = 0;
+  for (auto& [u, g] : g_guarded) bad += check_one(u, g, where);
+  return bad;
+}
 
 void* dev_alloc(size_t bytes) {
   int dev = 0;
@@ -36,7 +87,35 @@ void* dev_alloc(size_t bytes) {
     s = alloc_stream_locked(dev);
   }
   void* p = nullptr;
+  if (canary_on()) {
+    const size_t b = ((bytes > 0 ? bytes : 8) + 255) / 256 * 256;
+    KOT_CUDA(cudaMallocAsync(&p, b + 2 * kCanary, s));
+    KOT_CUDA(cudaMemsetAsync(p, 0xAB, b + 2 * kCanary, s));
+    KOT_CUDA(cudaStreamSynchronize(s));
+    void* user = static_cast<char*>(p) + kCanary;
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_guarded[user] = Guarded{p, b, g_seq++};
+    return user;
+  }
   KOT_CUDA(cudaMallocAsync(&p, bytes > 0 ? bytes : 8, s));
+  // diagnostics: KOT_POISON fills fresh allocations (1: NaN bytes, 2: 0x55 bytes), restricted to
+  // allocation numbers [lo, hi) by KOT_POISON_RANGE=lo:hi; KOT_ALLOC_LOG=1 lists the allocations
+  static const int poison = [] {
+    const char* e = std::getenv("KOT_POISON");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const std::pair<long, long> prange = [] {
+    const char* e = std::getenv("KOT_POISON_RANGE");
+    long lo = 0, hi = 1L << 60;
+    if (e) std::sscanf(e, "%ld:%ld", &lo, &hi);
+    return std::make_pair(lo, hi);
+  }();
+  static const bool alog = std::getenv("KOT_ALLOC_LOG") != nullptr;
+  static std::atomic<long> aseq{0};
+  const long seq = aseq++;
+  if (alog) std::fprintf(stderr, "[kot alloc] #%ld %zu B\n", seq, bytes);
+  if (poison && seq >= prange.first && seq < prange.second)
+    KOT_CUDA(cudaMemsetAsync(p, poison == 1 ? 0xFF : 0x55, bytes > 0 ? bytes : 8, s));
   KOT_CUDA(cudaStreamSynchronize(s));  // usable from every stream from here on
   return p;
 }
@@ -49,6 +128,20 @@ void dev_free(void* p) {
   {
     std::lock_guard<std::mutex> lk(g_mu);
     s = alloc_stream_locked(dev);
+  }
+  if (canary_on()) {
+    Guarded g{};
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      auto it = g_guarded.find(p);
+      if (it == g_guarded.end()) return;
+      g = it->second;
+      g_guarded.erase(it);
+    }
+    cudaDeviceSynchronize();
+    check_one(p, g, "free");
+    cudaFreeAsync(g.raw, s);
+    return;
   }
   cudaFreeAsync(p, s);  // back to the pool; the caller's streams are idle
 }

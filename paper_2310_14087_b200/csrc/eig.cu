@@ -38,7 +38,6 @@ constexpr int TRD_NB = 32;
 constexpr int TRD_THREADS = 256;
 constexpr int TRD_WARPS = TRD_THREADS / 32;
 constexpr int TRD_PSTRIDE = 2 * TRD_NB + 2;
-constexpr int TRD_CL = 4;  // CTAs per cluster of the panel kernel (148 = 37 × 4)
 constexpr int TRD_GRP = 8;
 constexpr int TRD_NGRP = (kNumSMs + TRD_GRP - 1) / TRD_GRP;
 constexpr int DC_LEAF = 32;
@@ -149,7 +148,6 @@ constexpr int TRD_RPW = 8;  // rows per warp: n ≤ TRD_RPW · 8 · 148 = 9472
 
 __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) {
   cg::grid_group grid = cg::this_grid();
-  cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ double dsm[];
   // dynamic smem: [Vs | Ws | Ac] (TRD_WARPS × TRD_RPW × NB each) then the Householder vector (n)
   typedef double RowBlk[TRD_RPW][TRD_NB];
@@ -162,11 +160,9 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
   __shared__ double wrow[TRD_NB], vrow[TRD_NB];
   __shared__ double nrm_sh[TRD_WARPS];
   __shared__ double scal_sh[2];
-  __shared__ double cpart[TRD_PSTRIDE];
 
   const int n = a.n, p0 = a.p0, nb = a.nb;
   const int G = gridDim.x;
-  const int NCL = G / TRD_CL;  // clusters
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int gw = blockIdx.x * TRD_WARPS + wid;
   const int NW = G * TRD_WARPS;
@@ -211,7 +207,7 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
       }
       if (wid < TRD_WARPS - 1) {  // TRD_WARPS−1 warps share the partial columns; every load issued up front
         constexpr int QPW = (2 * TRD_NB + 1 + TRD_WARPS - 2) / (TRD_WARPS - 1);
-        constexpr int GPL = (kNumSMs / TRD_CL + 31) / 32;  // cluster partials per lane (≤ 37)
+        constexpr int GPL = (kNumSMs + 31) / 32;  // partials per lane (G ≤ 148)
         double sq[QPW];
 #pragma unroll
         for (int i = 0; i < QPW; ++i) {
@@ -221,7 +217,7 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
 #pragma unroll
           for (int u = 0; u < GPL; ++u) {
             const int g = lane + 32 * u;
-            v[u] = (need && g < NCL) ? __ldcg(a.part + (long)q * kNumSMs + g) : 0.0;
+            v[u] = (need && g < G) ? __ldcg(a.part + (long)q * kNumSMs + g) : 0.0;
           }
           double s = 0.0;
 #pragma unroll
@@ -412,21 +408,10 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
     if (lane == 0) sred[wid][2 * TRD_NB] = pyv;
     __syncthreads();
     TRD_MARK(5)
-    // first reduction level inside the cluster (DSMEM), so that every CTA reads G/TRD_CL partials
-    // after the grid barrier instead of G (148 CTAs reading the same 77 KB was the costliest step)
     for (int q = threadIdx.x; q <= 2 * TRD_NB; q += blockDim.x) {
       double s = 0.0;
       for (int w = 0; w < TRD_WARPS; ++w) s += sred[w][q];
-      cpart[q] = s;
-    }
-    cluster.sync();
-    if (cluster.block_rank() == 0) {
-      for (int q = threadIdx.x; q <= 2 * TRD_NB; q += blockDim.x) {
-        double s = 0.0;
-#pragma unroll
-        for (int r = 0; r < TRD_CL; ++r) s += cluster.map_shared_rank(cpart, r)[q];
-        a.part[(long)q * kNumSMs + blockIdx.x / TRD_CL] = s;
-      }
+      a.part[(long)q * kNumSMs + blockIdx.x] = s;
     }
     TRD_MARK(6)
     grid.sync();
@@ -441,7 +426,7 @@ __global__ void set_last_diag_kernel(const double* A, int n, double* d) { d[n - 
 
 unsigned long long* g_trd_dbg = nullptr;  // set by kot_debug_sytrd_timing
 
-// CTAs of the cooperative panel kernel (≤ one per SM, whole clusters).  KOT_TRD_GRID caps every
+// CTAs of the cooperative panel kernel (≤ one per SM).  KOT_TRD_GRID caps every
 // lane, KOT_TRD_GRID_FG/_BG/_BG2 set the per-lane sizes under an EG pipeline (diagnostics).
 static int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
@@ -453,7 +438,7 @@ static std::atomic<int> g_pipelines{0};
 void eig_pipeline_active(int delta) { g_pipelines += delta; }
 
 static int trd_grid_cap(int lane) {
-  static const int cap = std::max(TRD_CL, std::min(env_int("KOT_TRD_GRID", kNumSMs), kNumSMs) / TRD_CL * TRD_CL);
+  static const int cap = std::min(env_int("KOT_TRD_GRID", kNumSMs), kNumSMs);
   // With an EG pipeline running, the three cooperative grids (Newton chain 96, EG step 96, residual
   // at v 64 CTAs) fit co-resident in the 2 × 148 slots, so no chain waits at the gate for another's
   // panel (probe cfg3, H-form matvec: 148/64/64 → 8.5, 96/96/64 → 9.6–9.8, 80/96/64 9.7,
@@ -470,7 +455,7 @@ static int trd_grid(int rows, int lane) {
   // never below what the per-warp row capacity needs (TRD_RPW rows per warp)
   const int need = ceil_div(rows, TRD_WARPS * TRD_RPW);
   const int g = std::max(need, std::max(1, std::min(trd_grid_cap(lane), ceil_div(rows, TRD_WARPS))));
-  return ceil_div(g, TRD_CL) * TRD_CL;  // whole clusters
+  return g;
 }
 
 static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane) {
@@ -496,15 +481,11 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
       cfg.blockDim = dim3(TRD_THREADS);
       cfg.dynamicSmemBytes = smem;
       cfg.stream = st;
-      cudaLaunchAttribute at[2];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = TRD_CL;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      at[1].id = cudaLaunchAttributeCooperative;
-      at[1].val.cooperative = 1;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
       cfg.attrs = at;
-      cfg.numAttrs = 2;
+      cfg.numAttrs = 1;
       KOT_CUDA(cudaLaunchKernelEx(&cfg, sytrd_panel_kernel, args));
       KOT_LAUNCH_CHECK();
     }

@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
   static_assert(!Epi::kRowDot || BN == GB_N, "row-dot partials are per 64-column tile");
   extern __shared__ __align__(16) double gsm[];
   const int tiles_n_grid = (s.N + BN - 1) / BN;  // grid layout uses the static bound
+  const int n_static = s.N;                        // … and so does the split-K partial layout
   if (s.dN) s.N = *s.dN;
   if (s.dK) s.K = *s.dK;
   if (s.dKstart) s.kstart = *s.dKstart;
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
       if (r < s.M) epi.rowdot_store(tn, r, red[q] + red[BM + q]);
     }
   } else if (s.ksplit > 1) {
-    double* ws = s.ws + (long)blockIdx.y * s.M * s.N;
+    double* ws = s.ws + (long)blockIdx.y * s.M * n_static;
 #pragma unroll
     for (int i = 0; i < T::MI; i++) {
       const int r = m0 + wm + i * 8 + g;
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int c = n0 + wn + j * 8 + 2 * t + h;
-          if (c < s.N) ws[(long)r * s.N + c] = acc[i][j][h];
+          if (c < s.N) ws[(long)r * n_static + c] = acc[i][j][h];
         }
     }
   } else {
@@ -286,10 +287,13 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
 
 template <class Epi>
 __global__ void splitk_reduce_kernel(int M, int N, int splits, int sym_tiles, const double* __restrict__ ws,
-                                     Epi epi) {
+                                     Epi epi, const int* __restrict__ dN) {
+  // ws layout [split][M][N] with the static N; columns ≥ *dN (device-side N) were not computed
+  const int n_act = dN ? *dN : N;
   const long total = (long)M * N;
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
     const int r = (int)(e / N), c = (int)(e % N);
+    if (c >= n_act) continue;
     if (sym_tiles && r / GB_M > c / GB_N) continue;
     double v = 0.0;
     for (int sp = 0; sp < splits; ++sp) v += ws[(long)sp * total + e];
@@ -350,7 +354,7 @@ void gemm_launch_tiled(const GemmShape& s, const Epi& epi, cudaStream_t st) {
     if (s.ksplit > 1) {
       const long total = (long)s.M * s.N;
       splitk_reduce_kernel<Epi><<<(int)std::min<long>((total + 255) / 256, 4L * 148 * 8), 256, 0, st>>>(
-          s.M, s.N, s.ksplit, s.sym_tiles, s.ws, epi);
+          s.M, s.N, s.ksplit, s.sym_tiles, s.ws, epi, s.dN);
       KOT_LAUNCH_CHECK();
     }
   }

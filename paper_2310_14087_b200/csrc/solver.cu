@@ -447,6 +447,8 @@ struct LoopState {
 
 static bool loop_body(Problem& p, const SolverCfg& cfg, LoopState& s, int k, IterRecord& rec, IterCallback cb,
                       void* user, HostProbe* hp) {
+  if (canary_check_all(("before iteration " + std::to_string(k)).c_str()) > 0)
+    throw KotError(KOT_ECUDA, "device canary overwritten (KOT_CANARY)");
   Bufs& b = p.bufs();
   const int n = p.n;
   const long nn = (long)n * n;
@@ -631,7 +633,11 @@ SolveResult solve(Problem& p, const SolverCfg& cfg, IterCallback cb, void* user,
   bool conv = res0 <= cfg.residual_tol;
   bool finite = std::isfinite(res0);
   std::unique_ptr<EgPipeline> pipe;
-  if (!pure_eg && finite && !conv) {
+  static const bool no_pipe = [] {  // diagnostic: EG chain per iteration on a helper thread
+    const char* e = std::getenv("KOT_NO_PIPE");
+    return e && std::atoi(e) > 0;
+  }();
+  if (!pure_eg && finite && !conv && !no_pipe) {
     const auto t_pipe = clk::now();
     pipe.reset(new EgPipeline(p, cfg.eg_stepsize));
     s.pipe = pipe.get();

@@ -50,6 +50,11 @@ void Problem::init_scratch() {
 }
 
 Problem::~Problem() {
+  static const bool devsync = [] {  // diagnostic
+    const char* e = std::getenv("KOT_FREE_DEVSYNC");
+    return e && std::atoi(e) > 0;
+  }();
+  if (devsync) cudaDeviceSynchronize();
   if (st) cudaStreamSynchronize(st);
   if (nccl_comm) {
     try {

@@ -281,6 +281,26 @@ def test_eg_step(cfg1):
     assert np.array_equal(v.x_mat, v.x_mat.T)
 
 
+@pytest.mark.parametrize("n,shift", [(1000, 0.0), (1000, -0.3), (700, 0.2)])
+def test_eg_step_large(n, shift):
+    """EG step at orders where the α-only back-transform (σ > 0 eigenvectors only, column count read
+    on the device) runs its Vᵀ·P products split-K: the partial layout must follow the static column
+    bound and the reduction must skip the uncomputed columns (regression: garbage projections)."""
+    d = random_problem_arrays(11, n=n)
+    rng = np.random.default_rng(n)
+    x = random_symmetric(rng, n) / np.sqrt(n) + shift * np.eye(n)
+    g = rng.standard_normal(n)
+    pd = GP.ProblemData(q_mat=d["q"], z=d["z"], q_sq=d["q_sq"], chol_upper=d["r"], lambda1=d["l1"],
+                        lambda2=d["l2"])
+    po = O.Problem(q=d["q"], z=d["z"], q_sq=d["q_sq"], r=d["r"], l1=d["l1"], l2=d["l2"])
+    s = 0.05
+    for _ in range(2):  # second call: workspaces hold the first call's values
+        v = eg_step(pd, GP.IteratePair(g, x), EgConfig(s))
+    ref = O.eg_step(po, O.Pair(g, x), s)
+    assert rel(v.gamma, ref.g) <= 1e-12
+    assert rel(v.x_mat, ref.x) <= 1e-11
+
+
 def test_objective_and_ot(cfg1):
     pd = gpu_pd(cfg1)
     assert GP.objective(pd, cfg1["op_g"]) == pytest.approx(float(cfg1["op_objective"]), rel=1e-13)
