@@ -50,11 +50,6 @@ void Problem::init_scratch() {
 }
 
 Problem::~Problem() {
-  static const bool devsync = [] {  // diagnostic
-    const char* e = std::getenv("KOT_FREE_DEVSYNC");
-    return e && std::atoi(e) > 0;
-  }();
-  if (devsync) cudaDeviceSynchronize();
   if (st) cudaStreamSynchronize(st);
   if (nccl_comm) {
     try {
@@ -392,6 +387,22 @@ struct EpiMvCoef {
   __device__ void rowdot_store(int, int, double) const {}
 };
 
+// B's columns regrouped as [smaller sign block | pad | other block | pad] (even widths, ld even).
+__global__ void pack_blocks_kernel(const double* __restrict__ B, int n, int k, int pos, int ksp, int ldp,
+                                   double* __restrict__ out) {
+  const long total = (long)n * ldp;
+  const int ks = pos ? k : n - k;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / ldp), c = (int)(i % ldp);
+    int src = -1;
+    if (c < ks)
+      src = pos ? c : k + c;
+    else if (c >= ksp && c - ksp < n - ks)
+      src = pos ? k + (c - ksp) : c - ksp;
+    out[i] = src >= 0 ? B[(long)r * n + src] : 0.0;
+  }
+}
+
 // Mixed-sign block only (H form): T̃ = 2ξ∘C on α×ᾱ.  pos: row r = a ∈ α, column c ↔ k + c ∈ ᾱ;
 // else row r ↔ k + r ∈ ᾱ, column c = a ∈ α.  ξ = η/(μ+1−η), η = σ_a/(σ_a − σ_b) (psdcone.py:35-49).
 struct EpiMvOff {
@@ -468,13 +479,23 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allo
     }
   }
   if (m.hform) {
+    // The sign blocks of B packed side by side with even widths, so that every operand of the
+    // matvec GEMMs is 16-byte aligned (16-byte cp.async) whatever the parity of k.
+    const int k = dc.k, ks = m.pos ? k : n - k, ns = n - ks;
+    const int ksp = ks + (ks & 1), nsp = ns + (ns & 1);
+    m.ldp = ksp + nsp;
+    pack_blocks_kernel<<<ew_grid((long)n * m.ldp), 256, 0, p.st>>>(b.Bm, n, k, m.pos ? 1 : 0, ksp, m.ldp, b.Bp);
+    KOT_LAUNCH_CHECK();
+    m.Bs = b.Bp;
+    m.Bo = b.Bp + ksp;
     // H = G_α∘G_α, G_α = B_α B_αᵀ (one triangle + mirror, once per Newton step): the α×α block of
     // W∘(Bᵀdiag(v)B) is the constant 1/μ, so its share of Φ(𝒯[Φ*(v)])_i = Σ_j v_j (b_iα·b_jα)²/μ
     // is the GEMV (H v)/μ, and only the α×ᾱ block remains for the two GEMMs of every matvec.
-    if (dc.k == 0) {
+    if (k == 0) {
       KOT_CUDA(cudaMemsetAsync(m.H, 0, sizeof(double) * n * n, p.st));
     } else {
-      GemmShape s = make_shape(n, n, dc.k, b.Bm, n, b.Bm, n);
+      const double* Ba = m.pos ? m.Bs : m.Bo;
+      GemmShape s = make_shape(n, n, k, Ba, m.ldp, Ba, m.ldp);
       s.sym_tiles = 1;
       gemm_launch<false, true>(s, EpiSquareMirror{m.H, n}, p.st);
     }
@@ -499,10 +520,11 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
   const double nn = n;
   ProfScope ps("matvec", p.st, 4.0 * ks * (double)ns * nn + 4.0 * nn * nn);
   Bufs& b = p.bufs();
-  const double* Bs = m.pos ? m.B : m.B + k;   // columns of the T̃-row block
-  const double* Bo = m.pos ? m.B + k : m.B;   // columns of the other block
+  const double* Bs = m.Bs;  // columns of the T̃-row block (the smaller sign block)
+  const double* Bo = m.Bo;  // columns of the other block
+  const long ld = m.ldp;
   if (ks > 0 && ns > 0) {
-    GemmShape s = make_shape(ks, ns, n, Bs, n, Bo, n);
+    GemmShape s = make_shape(ks, ns, n, Bs, ld, Bo, ld);
     s.kscale = v;
     s.ws = p.splitws;
     s.ksplit = choose_ksplit(s, p.splitws_cap);
@@ -512,8 +534,8 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
     }();
     if (mv_split > 1 && (long)mv_split * s.M * s.N <= p.splitws_cap) s.ksplit = mv_split;
     gemm_launch<true, false>(s, EpiMvOff{b.Ct, n, m.dc.vals, k, m.pos ? 1 : 0, m.mu}, p.st);
-    GemmShape s2 = make_shape(n, ks, ns, Bo, n, b.Ct, n);
-    gemm_launch<false, true>(s2, EpiRowDot{Bs, n, p.partial, n}, p.st);
+    GemmShape s2 = make_shape(n, ks, ns, Bo, ld, b.Ct, n);
+    gemm_launch<false, true>(s2, EpiRowDot{Bs, ld, p.partial, n}, p.st);
   }
   FinArgs f;
   f.n = n;
@@ -852,6 +874,7 @@ Bufs& Problem::bufs() {
     for (double** m : {&b.Xw, &b.Xv, &b.Xt, &b.r2w, &b.r2v, &b.r2t, &b.Pw, &b.Pv, &b.Pt, &b.Pe, &b.Xh, &b.dX,
                        &b.filt, &b.a2t, &b.Bm, &b.Ct, &b.Hm})
       *m = alloc(nn);
+    b.Bp = alloc((long)n * (n + 2));
     for (double** v : {&b.gw, &b.gv, &b.gt, &b.r1w, &b.r1v, &b.r1t, &b.valw, &b.valv, &b.valt, &b.vale, &b.dg,
                        &b.a1, &b.rhs, &b.sol, &b.corr, &b.cx, &b.cr, &b.cp, &b.cap, &b.e1, &b.e2, &b.e3})
       *v = alloc(n);

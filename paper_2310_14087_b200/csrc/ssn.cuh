@@ -39,6 +39,7 @@ struct Bufs {
   double *gw, *gv, *gt, *r1w, *r1v, *r1t, *valw, *valv, *valt, *vale, *dg, *a1, *rhs, *sol, *corr;  // n
   double *cx, *cr, *cp, *cap, *e1, *e2, *e3;  // n
   double *Bm, *Ct, *Hm;  // n×n: B = R·P, T̃, H = G_α∘G_α (structure-reduced matvec)
+  double* Bp;            // n×(n+2): B's sign blocks packed [smaller | other], 16-B aligned
 };
 
 struct Problem {
@@ -117,6 +118,8 @@ struct MvCtx {
   bool hform = false;   // same-sign block as a GEMV with H = G_α∘G_α (unsharded; KOT_MATVEC=full: off)
   double* B = nullptr;
   double* H = nullptr;
+  const double *Bs = nullptr, *Bo = nullptr;  // H form: packed smaller / other sign block of B
+  long ldp = 0;
 };
 void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allow_hform = true);
 // shard.cu

@@ -17,7 +17,7 @@ start = int(len(data) * (1 - frac))
 for d in data[start:]:
     v = float(d['Metric Value'].replace(',', ''))
     unit = d['Metric Unit']
-    us = v / 1000.0 if unit == 'nsecond' else (v if unit == 'usecond' else v * 1000.0)
+    us = v / 1000.0 if unit in ('nsecond', 'ns') else (v if unit in ('usecond', 'us') else v * 1000.0)
     agg[d['Kernel Name'][:60]][0] += 1
     agg[d['Kernel Name'][:60]][1] += us
 tot = sum(v[1] for v in agg.values())
