@@ -422,6 +422,220 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
 #undef TRD_MARK
 }
 
+// ------------------------------------------------------------ sytrd tail (one cluster)
+//
+// The last m0 ≤ TAIL_MAX columns of the reduction are done by ONE 16-CTA thread-block cluster that
+// holds the whole trailing matrix in its shared memory (rows r ≡ rank mod 16, full symmetric rows):
+// unblocked dsytd2 (lower) — per column a distributed-shared-memory gather of the column + its norm,
+// the Householder scalars computed identically in every CTA, a row-dot symv on the CTA's own rows,
+// a DSMEM gather of y, and the rank-2 update in place.  Two cluster barriers per column instead of
+// the panel kernel's two grid barriers and ~4 dependent L2 round trips (≈9.5 µs/column), and only 16
+// SMs busy, which leaves the rest of the GPU to the solver's other chains.
+constexpr int TAIL_CL = 16;
+constexpr int TAIL_THREADS = 512;
+constexpr int TAIL_MAX = 640;                   // rows per CTA ≤ 40: 40 × 640 × 8 B = 200 KB of smem
+constexpr int TAIL_RPC = TAIL_MAX / TAIL_CL;    // 40
+
+struct TailArgs {
+  const double* A;  // n × n (ld n), trailing block at (c0, c0) fully updated and symmetric
+  int n, c0;
+  double* d;
+  double* e;
+  double* tau;
+  double* Vall;     // reflector c (global index) in column c, rows > c; v_{c+1} = 1
+  unsigned long long* dbg;  // nullable: per-segment ns accumulated by CTA 0 thread 0
+};
+unsigned long long* g_tail_dbg = nullptr;  // set by kot_debug_tail_timing
+
+__device__ __forceinline__ double tail_block_sum(double v, double* sh) {
+  // fixed-order block reduction (identical result in every CTA for identical inputs)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < TAIL_THREADS / 32; ++w) t += sh[w];
+  return t;
+}
+
+__global__ void __launch_bounds__(TAIL_THREADS, 1) sytrd_tail_kernel(TailArgs a) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double tsm[];
+  const int g = (int)cl.block_rank();
+  const int n = a.n, c0 = a.c0, m0 = n - c0;
+  const int nrows = (m0 - g + TAIL_CL - 1) / TAIL_CL;  // own rows r = g + 16 q, q < nrows
+  const int ld = m0 + (m0 & 1);
+  double* Aloc = tsm;                               // nrows × ld
+  double* vfull = Aloc + (long)TAIL_RPC * ld;       // m0
+  double* wfull = vfull + ld;                       // m0 (y, then w)
+  __shared__ double pub_x[TAIL_RPC];                // own rows' column entries (read by the cluster)
+  __shared__ double pub_y[TAIL_RPC];                // own rows' symv results
+  __shared__ double pub_n;                          // own partial Σ x_r², r ≥ c+2
+  __shared__ double red[TAIL_THREADS / 32];
+  __shared__ double scal[3];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+  for (int q = wid; q < nrows; q += TAIL_THREADS / 32) {
+    const double* src = a.A + (long)(c0 + g + TAIL_CL * q) * n + c0;
+    double* dst = Aloc + (long)q * ld;
+    for (int s = lane; s < m0; s += 32) dst[s] = src[s];
+  }
+  __syncthreads();
+
+  const bool timing = (a.dbg != nullptr) && g == 0 && tid == 0;
+  unsigned long long tseg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long tl = timing ? gtimer() : 0;
+#define TAIL_MARK(i)                        \
+  if (timing) {                             \
+    const unsigned long long t_ = gtimer(); \
+    tseg[i] += t_ - tl;                     \
+    tl = t_;                                \
+  }
+  for (int c = 0; c + 1 < m0; ++c) {
+    // (A) publish own entries of column c below the diagonal and the partial norm
+    double pn = 0.0;
+    for (int q = tid; q < nrows; q += TAIL_THREADS) {
+      const int r = g + TAIL_CL * q;
+      const double x = Aloc[(long)q * ld + c];
+      pub_x[q] = x;
+      if (r >= c + 2) pn += x * x;
+      if (r == c) a.d[c0 + c] = x;
+    }
+    pn = tail_block_sum(pn, red);
+    if (tid == 0) pub_n = pn;
+    TAIL_MARK(0)
+    cl.sync();
+    TAIL_MARK(1)
+    // (B) gather the column (registers first: one DSMEM round trip), Householder scalars (dlarfg)
+    // identically in every CTA, then v = x·scale with v_{c+1} = 1
+    constexpr int XPT = (TAIL_MAX + TAIL_THREADS - 1) / TAIL_THREADS;
+    double xr[XPT];
+#pragma unroll
+    for (int u = 0; u < XPT; ++u) {
+      const int r = c + 1 + tid + u * TAIL_THREADS;
+      xr[u] = (r < m0) ? cl.map_shared_rank(pub_x, r % TAIL_CL)[r / TAIL_CL] : 0.0;
+    }
+    const double alpha = cl.map_shared_rank(pub_x, (c + 1) % TAIL_CL)[(c + 1) / TAIL_CL];
+    if (wid == 0) {
+      double t = (lane < TAIL_CL) ? *cl.map_shared_rank(&pub_n, lane) : 0.0;
+      t = warp_sum(t);  // fixed order over the 16 ranks
+      if (lane == 0) scal[0] = t;
+    }
+    __syncthreads();
+    const double xn2 = scal[0];
+    double beta, tau, scale;
+    if (xn2 == 0.0) {  // dlarfg: H = I
+      tau = 0.0;
+      beta = alpha;
+      scale = 1.0;
+    } else {
+      beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    if (g == 0 && tid == 0) {
+      a.e[c0 + c] = beta;
+      a.tau[c0 + c] = tau;
+    }
+#pragma unroll
+    for (int u = 0; u < XPT; ++u) {
+      const int r = c + 1 + tid + u * TAIL_THREADS;
+      if (r < m0) vfull[r] = (r == c + 1) ? 1.0 : xr[u] * scale;
+    }
+    __syncthreads();
+    TAIL_MARK(2)
+    for (int q = tid; q < nrows; q += TAIL_THREADS) {
+      const int r = g + TAIL_CL * q;
+      if (r > c) a.Vall[(long)(c0 + r) * n + c0 + c] = (tau == 0.0) ? 0.0 : vfull[r];
+    }
+    TAIL_MARK(3)
+    if (tau == 0.0) {
+      cl.sync();  // keep the two-barrier rhythm (pub_x is rewritten next column)
+      continue;
+    }
+    // (C) y_r = Σ_{s>c} A_rs v_s for own rows r > c (two rows per warp pass, lane-strided fixed order)
+    for (int q0 = wid; q0 < nrows; q0 += 2 * (TAIL_THREADS / 32)) {
+      const int q1 = q0 + TAIL_THREADS / 32;
+      const bool h0 = g + TAIL_CL * q0 > c, h1 = q1 < nrows && g + TAIL_CL * q1 > c;
+      const double* A0 = Aloc + (long)q0 * ld;
+      const double* A1 = Aloc + (long)(h1 ? q1 : q0) * ld;
+      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+      int s = c + 1 + lane;
+      for (; s + 32 < m0; s += 64) {
+        const double v0 = vfull[s], v1 = vfull[s + 32];
+        a0 += A0[s] * v0;
+        a1 += A0[s + 32] * v1;
+        b0 += A1[s] * v0;
+        b1 += A1[s + 32] * v1;
+      }
+      if (s < m0) {
+        a0 += A0[s] * vfull[s];
+        b0 += A1[s] * vfull[s];
+      }
+      double t0 = a0 + a1, t1 = b0 + b1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+        t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+      }
+      if (lane == 0) {
+        if (h0) pub_y[q0] = t0;
+        if (h1) pub_y[q1] = t1;
+      }
+    }
+    TAIL_MARK(4)
+    cl.sync();
+    TAIL_MARK(5)
+    // (D) gather y (registers), w = τ y − ½ τ² (yᵀv) v
+    double yr[XPT];
+    double pyv = 0.0;
+#pragma unroll
+    for (int u = 0; u < XPT; ++u) {
+      const int r = c + 1 + tid + u * TAIL_THREADS;
+      yr[u] = (r < m0) ? cl.map_shared_rank(pub_y, r % TAIL_CL)[r / TAIL_CL] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < XPT; ++u) {
+      const int r = c + 1 + tid + u * TAIL_THREADS;
+      if (r < m0) pyv += yr[u] * vfull[r];
+    }
+    const double yv = tail_block_sum(pyv, red);
+    const double alpha2 = -0.5 * tau * (tau * yv);
+#pragma unroll
+    for (int u = 0; u < XPT; ++u) {
+      const int r = c + 1 + tid + u * TAIL_THREADS;
+      if (r < m0) wfull[r] = tau * yr[u] + alpha2 * vfull[r];
+    }
+    __syncthreads();
+    TAIL_MARK(6)
+    // (E) A_rs −= v_r w_s + w_r v_s on own rows r > c, columns s > c
+    for (int q = wid; q < nrows; q += TAIL_THREADS / 32) {
+      const int r = g + TAIL_CL * q;
+      if (r <= c) continue;
+      double* Ar = Aloc + (long)q * ld;
+      const double vr = vfull[r], wr = wfull[r];
+      int s = c + 1 + lane;
+      for (; s + 96 < m0; s += 128) {
+        double t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) t[u] = Ar[s + 32 * u] - vr * wfull[s + 32 * u] - wr * vfull[s + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) Ar[s + 32 * u] = t[u];
+      }
+      for (; s < m0; s += 32) Ar[s] = Ar[s] - vr * wfull[s] - wr * vfull[s];
+    }
+    __syncthreads();
+    TAIL_MARK(7)
+  }
+  if (timing)
+    for (int i = 0; i < 8; ++i) a.dbg[i] += tseg[i];
+#undef TAIL_MARK
+  if (g == (m0 - 1) % TAIL_CL && tid == 0) a.d[n - 1] = Aloc[(long)((m0 - 1) / TAIL_CL) * ld + m0 - 1];
+  cl.sync();  // no CTA leaves while its shared memory may still be read
+}
+
 __global__ void set_last_diag_kernel(const double* A, int n, double* d) { d[n - 1] = A[(long)(n - 1) * n + n - 1]; }
 
 unsigned long long* g_trd_dbg = nullptr;  // set by kot_debug_sytrd_timing
@@ -461,7 +675,13 @@ static int trd_grid(int rows, int lane) {
 static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane) {
   KOT_CUDA(cudaMemcpyAsync(w.A, Z, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
   KOT_CUDA(cudaMemsetAsync(w.Vall, 0, sizeof(double) * n * n, st));
-  for (int p0 = 0; p0 < n - 1; p0 += TRD_NB) {
+  static const bool use_tail = [] {
+    const char* e = std::getenv("KOT_TRD_TAIL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  // columns [c0, n) go to the cluster-resident tail kernel (c0 on a panel boundary)
+  const int c0 = !use_tail ? n : (n <= TAIL_MAX ? 0 : ceil_div(n - TAIL_MAX, TRD_NB) * TRD_NB);
+  for (int p0 = 0; p0 < std::min(c0, n - 1); p0 += TRD_NB) {
     const int nb = std::min(TRD_NB, n - 1 - p0);
     KOT_CUDA(cudaMemsetAsync(w.X, 0, sizeof(double) * n * 3 * TRD_NB, st));
     const int rows = n - p0;
@@ -501,8 +721,30 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
       gemm_launch<false, true>(s, epi, st);
     }
   }
-  set_last_diag_kernel<<<1, 1, 0, st>>>(w.A, n, w.d);
-  KOT_LAUNCH_CHECK();
+  if (c0 < n) {
+    const int m0 = n - c0;
+    const size_t smem = sizeof(double) * ((size_t)TAIL_RPC * (m0 + 1) + 2L * (m0 + 1));
+    ensure_smem_attr((const void*)sytrd_tail_kernel, (int)smem, true);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(TAIL_CL);
+    cfg.blockDim = dim3(TAIL_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = TAIL_CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    TailArgs ta{w.A, n, c0, w.d, w.e, w.tau, w.Vall, g_tail_dbg};
+    ProfScope ps("sytrd_tail", st);
+    KOT_CUDA(cudaLaunchKernelEx(&cfg, sytrd_tail_kernel, ta));
+    KOT_LAUNCH_CHECK();
+  } else {
+    set_last_diag_kernel<<<1, 1, 0, st>>>(w.A, n, w.d);
+    KOT_LAUNCH_CHECK();
+  }
 }
 
 // ======================================================== tridiagonal D&C
@@ -1507,6 +1749,24 @@ void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigW
 }
 
 }  // namespace kot
+
+extern "C" int kot_debug_tail_timing(int on, unsigned long long* out8) {
+  using namespace kot;
+  try {
+    if (on) {
+      if (!g_tail_dbg) KOT_CUDA(cudaMalloc(&g_tail_dbg, 8 * sizeof(unsigned long long)));
+      KOT_CUDA(cudaMemset(g_tail_dbg, 0, 8 * sizeof(unsigned long long)));
+    } else if (g_tail_dbg) {
+      KOT_CUDA(cudaDeviceSynchronize());
+      KOT_CUDA(cudaMemcpy(out8, g_tail_dbg, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      cudaFree(g_tail_dbg);
+      g_tail_dbg = nullptr;
+    }
+    return 0;
+  } catch (const KotError& e) {
+    return e.code;
+  }
+}
 
 extern "C" int kot_debug_sytrd_timing(int on, unsigned long long* out8) {
   // on=1: allocate + zero the segment accumulators; on=0: copy them out and disable

@@ -41,6 +41,18 @@ tot = sum(buf) or 1
 for nm, v in zip(names, buf):
     print(f"  {nm:24s} {v/1e6:8.3f} ms  {v/tot*100:5.1f}%  ({v/1e3/(n-1):.2f} us/col)")
 
+# per-segment timing of the cluster-resident tail kernel (CTA 0 thread 0)
+f = getattr(L, "kot_debug_tail_timing", None)
+if f is not None:
+    bt = (C.c_ulonglong * 8)()
+    f(1, bt)
+    linalg.sym_eig(z)
+    f(0, bt)
+    names = ["A:publish+norm", "cluster.sync#1", "B:gather+house", "B:Vall", "C:symv", "cluster.sync#2",
+             "D:gather y+w", "E:rank-2 update"]
+    for nm, v in zip(names, bt):
+        print(f"  tail {nm:18s} {v / 1e6:8.3f} ms")
+
 # per-segment cycles of the bulge-chasing kernel (every CTA × warp)
 f = getattr(L, "kot_debug_sb2st_timing", None)
 if f is not None:
