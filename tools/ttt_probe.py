@@ -31,4 +31,5 @@ first = next((i for i, r in enumerate(res) if r <= tol), None)
 cg = [r.cg_iters for r in rep.trace]
 print(f"{cfg_name} {profile} tol {tol}: {rep.termination} after {rep.iterations} iterations; assemble {t1-t0:.2f} s, "
       f"solve {t2-t1:.2f} s ({rep.iterations/(t2-t1):.2f} it/s), first ≤tol at {first}; mean CG {np.mean(cg):.1f}; "
-      f"final res {rep.residual_norm:.3e}; ot {rep.ot_estimate:.6f}")
+      f"final res {rep.residual_norm:.3e}; ot {rep.ot_estimate:.6f}; EG accepted "
+      f"{sum(1 for r in rep.trace if r.accepted != 'ssn')}; min res {min(res):.3e}")
