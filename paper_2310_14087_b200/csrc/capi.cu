@@ -118,7 +118,14 @@ int kot_problem_download(kot_problem* h, double* q, double* z, double* r_upper, 
   });
 }
 
-void kot_problem_destroy(kot_problem* h) { delete h; }
+void kot_problem_destroy(kot_problem* h) {
+  if (!h) return;
+  try {
+    kot::problem_release(std::move(h->p));  // idle problems are pooled for reuse (bounded)
+  } catch (...) {
+  }
+  delete h;
+}
 
 int kot_solve(kot_problem* h, const kot_solver_cfg* cfg, kot_iter_cb cb, void* user, double* gamma_out,
               double* x_out, kot_iter_record* trace, int trace_cap, kot_report* out) {

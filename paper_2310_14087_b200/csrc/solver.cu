@@ -318,18 +318,26 @@ class EgPipeline {
   EgPipeline(Problem& p, double stepsize) : p_(p), s_(stepsize) {
     const int n = p.n;
     const long nn = (long)n * n;
+    // slot buffers are allocated once per problem and reused by every later solve on it
+    if (p.pipe_bufs.empty()) {
+      for (int i = 0; i < kDepth; ++i)
+        for (long cnt : {(long)n, nn, (long)n, nn, nn, (long)n}) p.pipe_bufs.push_back(p.alloc(cnt));
+      p.pipe_bufs.push_back(p.alloc(n));
+      p.pipe_bufs.push_back(p.alloc(nn));
+    }
+    int b = 0;
     for (auto& sl : slots_) {
-      sl.g = p.alloc(n);
-      sl.X = p.alloc(nn);
-      sl.r1 = p.alloc(n);
-      sl.r2 = p.alloc(nn);
-      sl.P = p.alloc(nn);
-      sl.vals = p.alloc(n);
+      sl.g = p.pipe_bufs[b++];
+      sl.X = p.pipe_bufs[b++];
+      sl.r1 = p.pipe_bufs[b++];
+      sl.r2 = p.pipe_bufs[b++];
+      sl.P = p.pipe_bufs[b++];
+      sl.vals = p.pipe_bufs[b++];
     }
     Problem& a = p.aux();
     Problem& bb = p.aux2();
-    KOT_CUDA(cudaMemsetAsync(v0g_ = p.alloc(n), 0, sizeof(double) * n, p.st));
-    KOT_CUDA(cudaMemsetAsync(v0X_ = p.alloc(nn), 0, sizeof(double) * nn, p.st));
+    KOT_CUDA(cudaMemsetAsync(v0g_ = p.pipe_bufs[b++], 0, sizeof(double) * n, p.st));
+    KOT_CUDA(cudaMemsetAsync(v0X_ = p.pipe_bufs[b++], 0, sizeof(double) * nn, p.st));
     KOT_CUDA(cudaStreamSynchronize(p.st));
     eig_pipeline_active(+1);
     ta_ = std::thread([this, &a] { run_steps(a); });

@@ -11,6 +11,7 @@
 //   residual     problem.py:204-214,  eg_step eg.py:34-41
 //   CG           linalg.py:117-162   → fused single-CTA update kernel
 //   newton       newton.py:116-195
+#include <mutex>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -70,9 +71,52 @@ Problem::~Problem() {
   if (st) cudaStreamDestroy(st);
 }
 
+namespace {
+std::mutex g_pool_mu;
+// idle problems (streams synchronised); never destroyed at process exit (the CUDA runtime and the
+// allocator's own statics may already be gone by then)
+auto& g_pool = *new std::vector<std::unique_ptr<Problem>>();
+constexpr int kPoolPerOrder = 2;
+}  // namespace
+
+void problem_release(std::unique_ptr<Problem> p) {
+  if (!p) return;
+  if (p->nccl_comm != nullptr || p->emul_world > 1) return;  // destroyed (unique_ptr goes out of scope)
+  for (Problem* c : {p.get(), p->aux_.get(), p->aux2_.get(), p->crit_.get()})
+    if (c && c->st) KOT_CUDA(cudaStreamSynchronize(c->st));
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  int same = 0;
+  for (auto& q : g_pool) same += (q->n == p->n && q->device == p->device);
+  if (same < kPoolPerOrder) g_pool.push_back(std::move(p));
+}
+
+static void refresh_children(Problem& p) {
+  for (Problem* c : {p.aux_.get(), p.aux2_.get(), p.crit_.get()}) {
+    if (!c) continue;
+    c->l1 = p.l1;
+    c->l2 = p.l2;
+    c->q_sq = p.q_sq;
+    c->jitter = p.jitter;
+    c->has_embed = p.has_embed;
+    c->g2_valid = false;
+  }
+}
+
 static std::unique_ptr<Problem> make_problem(int n, int device) {
   kot_require(n >= 1, KOT_EINVAL, "problem order must be >= 1");
   KOT_CUDA(cudaSetDevice(device));
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (auto it = g_pool.begin(); it != g_pool.end(); ++it)
+      if ((*it)->n == n && (*it)->device == device) {
+        std::unique_ptr<Problem> p = std::move(*it);
+        g_pool.erase(it);
+        p->Kmat = nullptr;
+        p->g2_valid = false;
+        p->has_embed = false;
+        return p;
+      }
+  }
   std::unique_ptr<Problem> p(new Problem());
   p->n = n;
   p->device = device;
@@ -121,6 +165,7 @@ std::unique_ptr<Problem> problem_from_host(const double* q, const double* z, dou
     p->has_embed = true;
   }
   KOT_CUDA(cudaStreamSynchronize(p->st));
+  refresh_children(*p);
   return p;
 }
 
@@ -134,17 +179,21 @@ std::unique_ptr<Problem> problem_assemble(const double* xs, int nx, const double
   p->l1 = l1;
   p->l2 = l2;
   const long nn = (long)l * l;
-  // host → device staging of the raw points (in M3; freed scratch)
-  double* dxs = p->alloc((long)nx * d);
-  double* dys = p->alloc((long)ny * d);
-  double* dxt = p->alloc((long)l * d);
-  double* dyt = p->alloc((long)l * d);
+  // host → device staging of the raw points (temporaries, freed once the instance is built)
+  struct Tmp {
+    double* p;
+    explicit Tmp(long cnt) : p(static_cast<double*>(dev_alloc(std::max(cnt, 1L) * sizeof(double)))) {}
+    ~Tmp() { dev_free(p); }
+  };
+  Tmp txs((long)nx * d), tys((long)ny * d), txt((long)l * d), tyt((long)l * d), tscratch(nx + ny + 8);
+  double *dxs = txs.p, *dys = tys.p, *dxt = txt.p, *dyt = tyt.p;
   KOT_CUDA(cudaMemcpyAsync(dxs, xs, sizeof(double) * nx * d, cudaMemcpyHostToDevice, p->st));
   KOT_CUDA(cudaMemcpyAsync(dys, ys, sizeof(double) * ny * d, cudaMemcpyHostToDevice, p->st));
   KOT_CUDA(cudaMemcpyAsync(dxt, xt, sizeof(double) * l * d, cudaMemcpyHostToDevice, p->st));
   KOT_CUDA(cudaMemcpyAsync(dyt, yt, sizeof(double) * l * d, cudaMemcpyHostToDevice, p->st));
-  p->Kmat = p->alloc(nn);
-  double* scratch = p->alloc(nx + ny + 8);
+  if (!p->kmat_buf) p->kmat_buf = p->alloc(nn);
+  p->Kmat = p->kmat_buf;
+  double* scratch = tscratch.p;
   assemble_device(dxs, nx, dys, ny, dxt, dyt, l, d, bw, l2, p->Q, p->Kmat, p->embed, p->z, p->dsc, scratch, p->st);
   KOT_CUDA(cudaMemcpyAsync(p->hsc, p->dsc, sizeof(double), cudaMemcpyDeviceToHost, p->st));
   KOT_CUDA(cudaStreamSynchronize(p->st));
@@ -152,6 +201,7 @@ std::unique_ptr<Problem> problem_assemble(const double* xs, int nx, const double
   p->has_embed = true;
   p->jitter = cholesky_psd_device(p->Kmat, l, p->R, p->M1, p->dsc + 32, p->dflag, p->st);
   KOT_CUDA(cudaStreamSynchronize(p->st));
+  refresh_children(*p);
   return p;
 }
 
@@ -501,8 +551,9 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allo
     }
     return;
   }
-  if (!m.pos && p.G2 == nullptr) {
-    p.G2 = p.alloc((long)n * n);
+  if (!m.pos && !p.g2_valid) {
+    if (p.G2 == nullptr) p.G2 = p.alloc((long)n * n);
+    p.g2_valid = true;
     GemmShape s = make_shape(n, n, n, p.R, n, p.R, n);  // (R Rᵀ)_ij = Σ_{k ≥ max(i,j)} R_ik R_jk
     s.kb_m = 1;
     s.kb_n = 1;

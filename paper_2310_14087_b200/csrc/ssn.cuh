@@ -52,6 +52,9 @@ struct Problem {
   // instance data (device)
   double *Q = nullptr, *z = nullptr, *R = nullptr, *embed = nullptr, *Kmat = nullptr;
   double* G2 = nullptr;  // (RRᵀ)∘(RRᵀ), lazily
+  bool g2_valid = false;   // G2 holds the current R's product (reset when a pooled problem is reused)
+  double* kmat_buf = nullptr;  // pair Gram storage (Kmat points here for assembled instances)
+  std::vector<double*> pipe_bufs;  // EG pipeline slots, allocated once per problem (solver.cu)
   // scratch
   std::unique_ptr<EigWork> eig;
   std::vector<double*> owned;
@@ -90,6 +93,10 @@ struct Problem {
   ~Problem();
 };
 
+// Destroyed handles go to a small per-(order, device) pool of idle problems with all their workspace
+// (contexts, eigensolver, solver buffers); a new instance of the same order reuses one and only
+// uploads / assembles its data.  Sharded problems are never pooled.
+void problem_release(std::unique_ptr<Problem> p);
 std::unique_ptr<Problem> problem_from_host(const double* q, const double* z, double q_sq, const double* r,
                                            const double* embed, int n, double l1, double l2, double jitter, int device);
 std::unique_ptr<Problem> problem_assemble(const double* xs, int nx, const double* ys, int ny, const double* xt,

@@ -336,6 +336,48 @@ def test_random_problem_solves(small, seed):
         assert rep.residual_norm == pytest.approx(float(small[p + "res"]), rel=0.05)
 
 
+def _cfg5_like(seed, n):
+    rng = np.random.default_rng(seed)
+    xs = np.clip(rng.normal(0.0, 0.3, (n, 3)), -1, 1)
+    ys = np.clip(rng.normal(0.2, 0.3, (n, 3)), -1, 1)
+    f = rng.uniform(-1, 1, (n, 6))
+    sx, sy, sxy = K.build_kernel_specs(3, 1.0)
+    return K.assemble(K.SampleSet(xs), K.SampleSet(ys), K.FillingPoints(f[:, :3], f[:, 3:]), 1e-3, 1.0 / n,
+                      sx, sy, sxy)
+
+
+def test_pooled_problem_reuse_is_exact():
+    """Released device problems are pooled and reused by the next instance of the same order (all
+    workspace, contexts and EG-pipeline buffers): a solve on a reused problem must be bit-identical
+    to one on a problem whose workspace held another instance's data."""
+    cfg = K.SolverConfig(residual_tol=1e-12, max_iter=6)
+    pa = _cfg5_like(1, 300)
+    K.solve(pa, cfg)
+    pa.release_device()               # → pool
+    pb = _cfg5_like(2, 300)           # reuses pa's workspace (stale data everywhere)
+    rb = K.solve(pb, cfg)
+    pb.release_device()
+    pc = _cfg5_like(2, 300)           # same instance again, on pb's workspace
+    rc = K.solve(pc, cfg)
+    assert np.array_equal(rb.gamma_hat, rc.gamma_hat)
+    assert [r.res_accepted for r in rb.trace] == [r.res_accepted for r in rc.trace]
+    assert np.array_equal(pb.chol_upper, pc.chol_upper) and np.array_equal(pb.q_mat, pc.q_mat)
+
+
+def test_repeated_solves_do_not_grow_device_memory():
+    """The EG pipeline's buffers are allocated once per problem, not once per solve."""
+    torch = pytest.importorskip("torch")
+    pd = _cfg5_like(3, 400)
+    cfg = K.SolverConfig(residual_tol=1e-12, max_iter=3)
+    K.solve(pd, cfg)
+    K.solve(pd, cfg)
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(4):
+        K.solve(pd, cfg)
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < 64 * 2 ** 20, (free0 - free1) / 2 ** 20
+
+
 def test_lockstep_replay_cfg1(cfg1):
     """one GPU iteration from each saved oracle state.
 
