@@ -311,8 +311,9 @@ def run_gpu(args):
     # ---------------- end to end through the public API from host buffers (e2e)
     pd_host = K.ProblemData(q_mat=pd.q_mat.copy(), z=pd.z.copy(), q_sq=pd.q_sq, chol_upper=pd.chol_upper.copy(),
                             lambda1=pd.lambda1, lambda2=pd.lambda2, embed_sum=pd.embed_sum.copy())
-    # the instance above is done with: its device memory goes back to the pool, as for a user who
-    # solves one problem after another (otherwise the e2e solve pays for growing the pool)
+    # the instance above is done with: its device problem (with all workspace) goes back to the
+    # library's pool and the e2e instance reuses it, as for a user who solves one problem after
+    # another in one process; upload, setup, initial residual and download stay in the timed region
     pd.release_device()
     cfg_e = K.SolverConfig(newton=newton_cfg(args.profile), eg=K.EgConfig(stepsize), residual_tol=1e-300,
                            max_iter=args.steps)

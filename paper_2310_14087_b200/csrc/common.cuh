@@ -26,6 +26,9 @@ struct KotError : public std::runtime_error {
   int code;
   KotError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
+// Thrown by an eigensolve whose caller cancelled it (speculative EG-pipeline work at the end of a
+// solve); never escapes the library.
+struct Cancelled {};
 
 #define KOT_CUDA(call)                                                                   \
   do {                                                                                   \

@@ -683,6 +683,7 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
   const int c0 = !use_tail ? n : (n <= TAIL_MAX ? 0 : ceil_div(n - TAIL_MAX, TRD_NB) * TRD_NB);
   for (int p0 = 0; p0 < std::min(c0, n - 1); p0 += TRD_NB) {
     const int nb = std::min(TRD_NB, n - 1 - p0);
+    w.check_cancel(st);
     KOT_CUDA(cudaMemsetAsync(w.X, 0, sizeof(double) * n * 3 * TRD_NB, st));
     const int rows = n - p0;
     const int G = trd_grid(rows, lane);
@@ -1727,10 +1728,12 @@ void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigW
       two_stage_tridiag(Z, n, w, st);
     else
       one_stage_tridiag(Z, n, w, st, lane);
+    w.check_cancel(st);
     {
       ProfScope ps("eig.stedc", st);
       stedc(n, w, st);
     }
+    w.check_cancel(st);
     ProfScope ps("eig.ormtr", st, 2.0 * n * (double)n * n);
     reverse_cols_kernel<<<std::min(ceil_div((long)n * n, 256), 2048), 256, 0, st>>>(w.Q, w.d, P, vals, n);
     KOT_LAUNCH_CHECK();

@@ -471,6 +471,7 @@ static void sy2sb(const double* Z, int n, EigWork& w, cudaStream_t st) {
   ensure_smem_attr((const void*)sy2sb_syr2k_kernel, S2K_SMEM);
   int pidx = 0;
   for (int j = 0; j + SB + 1 < n; j += SB, ++pidx) {
+    if ((pidx & 7) == 0) w.check_cancel(st);
     const int m = n - j - SB;
     Xs = w.X + (long)(pidx & 1) * n * SB_LDX;
     const int cs = pqr_cluster(m);

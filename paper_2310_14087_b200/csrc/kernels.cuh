@@ -1,3 +1,4 @@
+#include <atomic>
 // Internal (C++) interface of libkotgpu: device-level building blocks.
 #pragma once
 #include "common.cuh"
@@ -32,6 +33,14 @@ struct EigWork {
   cudaStream_t st2 = nullptr;  // two-stage: look-ahead stream
   cudaEvent_t ev_w = nullptr, ev_rest = nullptr;
   long splitws_cap = 0;
+  const std::atomic<bool>* cancel = nullptr;  // set: throw Cancelled at the next panel boundary
+  void check_cancel(cudaStream_t st) const {
+    if (cancel && cancel->load(std::memory_order_relaxed)) {
+      cudaStreamSynchronize(st);  // in-flight grids retire before any gate slot is released
+      if (st2) cudaStreamSynchronize(st2);
+      throw Cancelled{};
+    }
+  }
   int* ibuf = nullptr;
   void* dbuf = nullptr;
   int* hbuf = nullptr;

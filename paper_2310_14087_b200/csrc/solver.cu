@@ -339,11 +339,16 @@ class EgPipeline {
     KOT_CUDA(cudaMemsetAsync(v0g_ = p.pipe_bufs[b++], 0, sizeof(double) * n, p.st));
     KOT_CUDA(cudaMemsetAsync(v0X_ = p.pipe_bufs[b++], 0, sizeof(double) * nn, p.st));
     KOT_CUDA(cudaStreamSynchronize(p.st));
+    a.eig->cancel = &cancel_;
+    bb.eig->cancel = &cancel_;
     eig_pipeline_active(+1);
     ta_ = std::thread([this, &a] { run_steps(a); });
     tb_ = std::thread([this, &bb] { run_residuals(bb); });
   }
   ~EgPipeline() {
+    // the steps still running are speculative (v_j beyond the last iteration): cancel them at the
+    // next eigensolve panel instead of waiting up to one EG step
+    cancel_ = true;
     {
       std::lock_guard<std::mutex> lk(mu_);
       stop_ = true;
@@ -351,6 +356,8 @@ class EgPipeline {
     cv_.notify_all();
     ta_.join();
     tb_.join();
+    p_.aux().eig->cancel = nullptr;
+    p_.aux2().eig->cancel = nullptr;
     eig_pipeline_active(-1);
   }
   // Slot of v_j (j >= 1) once its residual is evaluated.  Also releases v_{j-2}.
@@ -371,6 +378,7 @@ class EgPipeline {
   std::mutex mu_;
   std::condition_variable cv_;
   bool stop_ = false;
+  std::atomic<bool> cancel_{false};
   int produced_ = 0, evaluated_ = 0, consumed_ = 0, failed_at_ = -1;
   std::thread ta_, tb_;
 
@@ -392,6 +400,8 @@ class EgPipeline {
         KOT_CUDA(cudaStreamSynchronize(a.st));
         out.eg_ms = ms_since(t0);
         prof_host("host.pipe_eg", out.eg_ms);
+      } catch (const Cancelled&) {
+        return;
       } catch (...) {
         std::lock_guard<std::mutex> lk(mu_);
         out.err = std::current_exception();
@@ -429,6 +439,8 @@ class EgPipeline {
         sl.k = dc.k;
         sl.resid_ms = ms_since(t0);
         prof_host("host.pipe_resid", sl.resid_ms);
+      } catch (const Cancelled&) {
+        return;
       } catch (...) {
         std::lock_guard<std::mutex> lk(mu_);
         sl.err = std::current_exception();
@@ -632,8 +644,8 @@ SolveResult solve(Problem& p, const SolverCfg& cfg, IterCallback cb, void* user,
   prof_host("solve.setup", ms_since(t_start));
   // initial residual at the zero pair (solver.py:129-139)
   const auto t_res0 = clk::now();
-  double res0 = pure_eg ? residual_parts(p, b.gv, b.Xv, b.r1v, b.r2v, s.dv)
-                        : residual_parts(p, b.gw, b.Xw, b.r1w, b.r2w, s.dw);
+  double res0 = pure_eg ? residual_parts_origin(p, b.gv, b.Xv, b.r1v, b.r2v, s.dv)
+                        : residual_parts_origin(p, b.gw, b.Xw, b.r1w, b.r2w, s.dw);
   prof_host("solve.res0", ms_since(t_res0));
   s.res_w = s.res_v = res0;
   s.theta = cfg.theta0;
@@ -715,7 +727,7 @@ Session* session_begin(Problem& p, const SolverCfg& cfg) {
   se->p = &p;
   se->cfg = cfg;
   init_state(p, se->s);
-  const double res0 = residual_parts(p, b.gw, b.Xw, b.r1w, b.r2w, se->s.dw);
+  const double res0 = residual_parts_origin(p, b.gw, b.Xw, b.r1w, b.r2w, se->s.dw);
   se->s.res_w = se->s.res_v = res0;
   se->s.theta = cfg.theta0;
   se->conv = res0 <= cfg.residual_tol;

@@ -822,6 +822,34 @@ double residual_parts(Problem& p, const double* g, const double* X, double* r1, 
   return p.hsc[0] + p.hsc[1];
 }
 
+__global__ void scaled_identity_decomp_kernel(int n, double c, double* P, double* vals) {
+  const long total = (long)n * n;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const long r = i / n, col = i % n;
+    P[i] = (r == col) ? 1.0 : 0.0;
+    if (r == col) vals[r] = c;
+  }
+}
+
+// The residual at the starting pair (γ, X) = (0, 0) (solver.py:129-139): Z = −(Φ*(0) + λ₁I) = −λ₁I
+// exactly, whose eigendecomposition is known (σ = −λ₁ for every column, P = I, k = 0) — the same
+// values LAPACK returns for a scaled identity; the eigensolve is skipped.
+double residual_parts_origin(Problem& p, const double* g, const double* X, double* r1, double* r2, Decomp& dc) {
+  ProfScope ps("residual", p.st);
+  const int n = p.n;
+  const long nn = (long)n * n;
+  phi_partials(p, X);
+  finalize(p, FIN_RES, g, true, nullptr, 0.0, r1);
+  scaled_identity_decomp_kernel<<<ew_grid(nn), 256, 0, p.st>>>(n, -p.l1, dc.P, dc.vals);
+  KOT_LAUNCH_CHECK();
+  dc.k = 0;  // λ₁ > 0
+  proj(p, dc, X, r2);
+  dev_reduce(p, r1, nullptr, n, 0, true);
+  dev_reduce(p, r2, nullptr, nn, 1, true);
+  fetch(p, 2);
+  return p.hsc[0] + p.hsc[1];
+}
+
 void middle_operator(Problem& p, const Decomp& dc, double mu, const double* v, double* out) {
   // F_mv = ℓ³ + 8kℓ² + 2ℓ², k = min(|α|, |ᾱ|)
   const double n = p.n, kk = std::min(dc.k, p.n - dc.k);
@@ -843,6 +871,7 @@ void eg_step(Problem& p, const double* g, const double* X, double s, double* g_o
   axpby(p, n, 1.0, g, -s, b.e1, b.e2);            // γ½ = γ − s g_vec
   phi_adjoint_ex(p, g, p.M1, -s, X, 1.0, p.l1);     // X − s (Φ*(γ) + λ₁I)
   eigh(p, p.M1, dc, true);                          // projection only: α eigenvectors suffice
+  if (p.eig) p.eig->check_cancel(p.st);
   proj(p, dc, nullptr, b.Xh);                       // X½ = Π(·)
   phi_partials(p, b.Xh);
   finalize(p, FIN_RES, b.e2, true, nullptr, 0.0, b.e1);

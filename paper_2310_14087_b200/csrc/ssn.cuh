@@ -113,6 +113,8 @@ void spectral_filter(Problem& p, const Decomp& dc, const double* S, double* out,
 // alpha_only: the decomposition holds only the σ > 0 eigenvectors (enough for r2 and the norm)
 double residual_parts(Problem& p, const double* g, const double* X, double* r1, double* r2, Decomp& dc,
                       bool alpha_only = false);
+// residual_parts at (γ, X) = (0, 0) (the solver's starting pair): no eigensolve needed
+double residual_parts_origin(Problem& p, const double* g, const double* X, double* r1, double* r2, Decomp& dc);
 void middle_operator(Problem& p, const Decomp& dc, double mu, const double* v, double* out);
 void eg_step(Problem& p, const double* g, const double* X, double s, double* g_out, double* X_out);
 

@@ -212,6 +212,7 @@ class Session:
         if self._h:
             _lib.lib().kot_session_end(self._h)
             self._h = C.c_void_p(0)
+        self._dp = None  # the instance's device problem may be released from here on
 
     def __del__(self):
         try:
