@@ -481,7 +481,8 @@ int kot_newton_direction(kot_problem* h, const kot_solver_cfg* cfg, const double
     kot::Decomp dc{b.Pw, b.valw, 0};
     const double res = kot::residual_parts(p, b.gw, b.Xw, b.r1w, b.r2w, dc);
     kot::kot_require(res > 0.0, kot::KOT_EINVAL, "context requires a nonzero residual");
-    const kot::NewtonOut o = kot::newton_direction(p, b.r1w, b.r2w, res, dc, theta * res, c, b.dg, b.dX);
+    kot::NewtonOut o = kot::newton_direction(p, b.r1w, b.r2w, res, dc, theta * res, c, b.dg, b.dX);
+    kot::newton_resolve(p, res, c, o);
     down(p, dgamma, b.dg, p.n);
     down(p, dx, b.dX, nn);
     KOT_CUDA(cudaStreamSynchronize(p.st));

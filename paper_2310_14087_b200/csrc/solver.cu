@@ -149,6 +149,7 @@ static void criterion_enqueue(Problem& p, Problem& q, const double* r1, const do
   phi_adjoint(q, b.sol, q.M1);
   spectral_filter(q, dc, q.M1, q.M2, mu, 0);
   axpby(q, nn, 1.0, b.a2t, -1.0, q.M2, q.crit_dX);
+  KOT_CUDA(cudaEventRecord(q.crit_dx_done, q.st));  // dw is complete; the norms below feed the record
   phi_partials(q, q.crit_dX);
   finalize(q, FIN_JTOP, q.crit_dg, true, r1, mu, q.crit_e1);
   phi_adjoint_ex(q, q.crit_dg, q.M1, 1.0, q.crit_dX, -1.0, 0.0);  // Φ*(dγ) − dX
@@ -262,9 +263,25 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
     if (att == cfg.cg_restarts) break;
     rel /= 10.0;
   }
-  resolve(true);
-  finish();
+  // The last attempt's criterion only feeds the record (met, lhs, rhs): dw is taken as soon as it is
+  // ready and the norms are resolved by the caller (newton_resolve), off the critical path.
+  KOT_CUDA(cudaStreamWaitEvent(p.st, q.crit_dx_done, 0));
+  KOT_CUDA(cudaMemcpyAsync(dg, q.crit_dg, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
+  KOT_CUDA(cudaMemcpyAsync(dX, q.crit_dX, sizeof(double) * nn, cudaMemcpyDeviceToDevice, p.st));
+  out.cg_ms = ms_since(t0);
+  out.crit_pending = true;
   return out;
+}
+
+void newton_resolve(Problem& p, double rn, const SolverCfg& cfg, NewtonOut& out) {
+  if (!out.crit_pending) return;
+  Problem& q = p.crit();
+  KOT_CUDA(cudaEventSynchronize(q.crit_done));
+  out.lhs = q.hsc[0] + q.hsc[1];
+  const double dwn = q.hsc[2] + q.hsc[3];
+  out.rhs = cfg.tau * std::min(1.0, cfg.kappa * rn * dwn);
+  out.met = out.lhs <= out.rhs;
+  out.crit_pending = false;
 }
 
 static double theta_update(double theta, double rho, double dw_sq, const SolverCfg& c) {
@@ -518,6 +535,7 @@ static bool loop_body(Problem& p, const SolverCfg& cfg, LoopState& s, int k, Ite
     res_t = residual_parts(p, b.gt, b.Xt, b.r1t, b.r2t, s.dt);
     resid_ms += ms_since(t0);
     prof_host("host.trial_resid", resid_ms);
+    newton_resolve(p, s.res_w, cfg, st);
   } catch (...) {
     nt_err = std::current_exception();
   }

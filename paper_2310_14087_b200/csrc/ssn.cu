@@ -63,6 +63,7 @@ Problem::~Problem() {
   crit_.reset();
   if (crit_done) cudaEventDestroy(crit_done);
   if (crit_after) cudaEventDestroy(crit_after);
+  if (crit_dx_done) cudaEventDestroy(crit_dx_done);
   eig.reset();
   for (double* p : owned) dev_free(p);
   host_free_pinned(hsc, 64 * sizeof(double));
@@ -914,6 +915,7 @@ Problem& Problem::crit() {
     c.crit_e1 = c.alloc(n);
     KOT_CUDA(cudaEventCreateWithFlags(&c.crit_done, cudaEventDisableTiming));
     KOT_CUDA(cudaEventCreateWithFlags(&c.crit_after, cudaEventDisableTiming));
+    KOT_CUDA(cudaEventCreateWithFlags(&c.crit_dx_done, cudaEventDisableTiming));
   }
   return *crit_;
 }

@@ -86,7 +86,7 @@ struct Problem {
   // its stream, scratch, outputs (crit_dg, crit_dX, crit_e1) and completion event
   Problem& crit();
   double *crit_dg = nullptr, *crit_dX = nullptr, *crit_e1 = nullptr;
-  cudaEvent_t crit_done = nullptr, crit_after = nullptr;
+  cudaEvent_t crit_done = nullptr, crit_after = nullptr, crit_dx_done = nullptr;
   bool with_eig = true;
   double* alloc(long count);
   void init_scratch();
@@ -143,9 +143,13 @@ void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* o
 struct NewtonOut {
   int cg_iters, met, attempts;
   double lhs, rhs, cg_ms;
+  bool crit_pending = false;  // met/lhs/rhs of the last attempt still in flight: newton_resolve
 };
 NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, double res_norm, const Decomp& dc,
                            double mu, const SolverCfg& cfg, double* dg, double* dX);
+// completes met / lhs / rhs of a direction whose last criterion was left running (res_norm as passed
+// to newton_direction)
+void newton_resolve(Problem& p, double res_norm, const SolverCfg& cfg, NewtonOut& out);
 
 // internal helpers shared with solver.cu
 enum FinMode { FIN_RES = 0, FIN_MATVEC = 1, FIN_A1 = 2, FIN_JTOP = 3, FIN_PHI = 4, FIN_GRAD = 5, FIN_QV = 6,
