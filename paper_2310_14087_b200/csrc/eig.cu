@@ -201,9 +201,9 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
       // prefetch row c of V/W (owned elsewhere) while the partials are reduced
       double pv = 0.0, pw = 0.0, pyc = 0.0;
       if (wid == TRD_WARPS - 1 && jj < nb) {
-        if (lane < jj) pv = V[(long)c * LDX + lane];
-        if (lane < m) pw = Wm[(long)c * LDX + lane];
-        pyc = a.yv[c];
+        if (lane < jj) pv = __ldcg(V + (long)c * LDX + lane);
+        if (lane < m) pw = __ldcg(Wm + (long)c * LDX + lane);
+        pyc = __ldcg(a.yv + c);
       }
       if (wid < TRD_WARPS - 1) {  // TRD_WARPS−1 warps share the partial columns; every load issued up front
         constexpr int QPW = (2 * TRD_NB + 1 + TRD_WARPS - 2) / (TRD_WARPS - 1);
