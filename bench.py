@@ -430,9 +430,9 @@ def run_batch(args):
     """Config 5: a batch of independent problems sharded over ranks, `--concurrency` solves per GPU,
     records gathered to rank 0.  Metric: completed OT problems/s (whole job)."""
     # several solves share the GPU: thinner cooperative panel grids let their eigensolves run side by
-    # side (measured, 16 problems x 100 iterations: 0.45 problems/s at 148 CTAs x 3 concurrent,
-    # 0.53 at 64 x 4, 0.60 at 48 x 6, 0.59 at 40 x 8)
-    os.environ.setdefault("KOT_TRD_GRID", "48")
+    # side (measured, 16 problems x 100 iterations, cluster tail: 0.73 problems/s at 64 CTAs, 0.85 at
+    # 48, 0.89 at 32, 0.90 at 24; concurrency 4-8 equal, 3 0.84, 2 0.66, 1 0.36)
+    os.environ.setdefault("KOT_TRD_GRID", "32")
     world, rank, local = dist_setup(args.gpus)
     os.environ["KOT_DEVICE"] = str(local)
     import torch
