@@ -378,6 +378,18 @@ def test_repeated_solves_do_not_grow_device_memory():
     assert free0 - free1 < 64 * 2 ** 20, (free0 - free1) / 2 ** 20
 
 
+def test_solve_report_serialises_exactly(cfg1, tmp_path):
+    """A real solve's report and trace survive the JSON / CSV formats bit-exactly (§8(f) item 3)."""
+    from paper_2310_14087_b200 import report as RP
+    rep = K.solve(gpu_pd(cfg1), K.SolverConfig(eg=EgConfig(float(cfg1["eg_stepsize"])), residual_tol=1e-12,
+                                              max_iter=5))
+    RP.write_report_json(rep, str(tmp_path / "r.json"), include_x=True)
+    RP.write_trace_csv(rep.trace, str(tmp_path / "t.csv"))
+    back = RP.read_report_json(str(tmp_path / "r.json"))
+    assert np.array_equal(back.gamma_hat, rep.gamma_hat) and np.array_equal(back.x_hat, rep.x_hat)
+    assert back.trace == rep.trace == RP.read_trace_csv(str(tmp_path / "t.csv"))
+
+
 def test_lockstep_replay_cfg1(cfg1):
     """one GPU iteration from each saved oracle state.
 
