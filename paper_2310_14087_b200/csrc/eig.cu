@@ -1540,15 +1540,24 @@ __global__ void __launch_bounds__(LARFT_THREADS) larft_kernel(const double* __re
   const int c = blockIdx.x * (LARFT_THREADS / 32) + wid;  // column of T
   if (c >= nb) return;
   double* t = tcol[wid];
-  if (lane == 0) t[c] = dinv[c];
-  __syncwarp();
-  for (int i = c - 1; i >= 0; --i) {
-    double s = 0.0;
-    for (int j = i + 1 + lane; j <= c; j += 32) s += S_s[i * LARFT_LDS + j] * t[j];
-    s = warp_sum(s);
-    if (lane == 0) t[i] = -s * dinv[i];
-    __syncwarp();
+  // Back substitution by columns: lane L keeps the running sums of rows L, L+32, L+64, L+96; once
+  // t_j is known (computed by its owner lane and broadcast), every row i < j adds S_ij t_j.  One
+  // shuffle + one FMA per step instead of a warp reduction per step.
+  static_assert(ORM_NB <= 128, "4 rows per lane");
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (int j = c; j >= 0; --j) {
+    const int q = j >> 5;
+    const double sq = q == 0 ? s0 : (q == 1 ? s1 : (q == 2 ? s2 : s3));
+    const double cand = (j == c) ? dinv[c] : -sq * dinv[j];
+    const double tj = __shfl_sync(0xffffffffu, cand, j & 31);
+    if (lane == (j & 31)) t[j] = tj;
+    const int i0 = lane, i1 = lane + 32, i2 = lane + 64, i3 = lane + 96;
+    if (i0 < j) s0 += S_s[j * LARFT_LDS + i0] * tj;  // S = VᵀV symmetric: row j, conflict-free
+    if (i1 < j) s1 += S_s[j * LARFT_LDS + i1] * tj;  // S = VᵀV symmetric: row j, conflict-free
+    if (i2 < j) s2 += S_s[j * LARFT_LDS + i2] * tj;  // S = VᵀV symmetric: row j, conflict-free
+    if (i3 < j) s3 += S_s[j * LARFT_LDS + i3] * tj;  // S = VᵀV symmetric: row j, conflict-free
   }
+  __syncwarp();
   for (int i = lane; i < nb; i += 32) T[(long)i * nb + c] = (i <= c) ? t[i] : 0.0;
 }
 
