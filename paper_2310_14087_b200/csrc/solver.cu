@@ -353,11 +353,13 @@ class EgPipeline {
     }
     Problem& a = p.aux();
     Problem& bb = p.aux2();
+    Problem& a3 = p.aux3();
     KOT_CUDA(cudaMemsetAsync(v0g_ = p.pipe_bufs[b++], 0, sizeof(double) * n, p.st));
     KOT_CUDA(cudaMemsetAsync(v0X_ = p.pipe_bufs[b++], 0, sizeof(double) * nn, p.st));
     KOT_CUDA(cudaStreamSynchronize(p.st));
     a.eig->cancel = &cancel_;
     bb.eig->cancel = &cancel_;
+    a3.eig->cancel = &cancel_;
     eig_pipeline_active(+1);
     ta_ = std::thread([this, &a] { run_steps(a); });
     tb_ = std::thread([this, &bb] { run_residuals(bb); });
@@ -375,6 +377,7 @@ class EgPipeline {
     tb_.join();
     p_.aux().eig->cancel = nullptr;
     p_.aux2().eig->cancel = nullptr;
+    p_.aux3().eig->cancel = nullptr;
     eig_pipeline_active(-1);
   }
   // Slot of v_j (j >= 1) once its residual is evaluated.  Also releases v_{j-2}.
@@ -413,8 +416,7 @@ class EgPipeline {
       try {
         KOT_CUDA(cudaSetDevice(a.device));
         const auto t0 = clk::now();
-        eg_step(a, gin, Xin, s_, out.g, out.X);
-        KOT_CUDA(cudaStreamSynchronize(a.st));
+        eg_step_parallel(a, p_.aux3(), gin, Xin, s_, out.g, out.X);
         out.eg_ms = ms_since(t0);
         prof_host("host.pipe_eg", out.eg_ms);
       } catch (const Cancelled&) {

@@ -12,6 +12,7 @@
 //   CG           linalg.py:117-162   → fused single-CTA update kernel
 //   newton       newton.py:116-195
 #include <mutex>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -60,10 +61,12 @@ Problem::~Problem() {
   }
   aux_.reset();
   aux2_.reset();
+  aux3_.reset();
   crit_.reset();
   if (crit_done) cudaEventDestroy(crit_done);
   if (crit_after) cudaEventDestroy(crit_after);
   if (crit_dx_done) cudaEventDestroy(crit_dx_done);
+  if (ev_half) cudaEventDestroy(ev_half);
   eig.reset();
   for (double* p : owned) dev_free(p);
   host_free_pinned(hsc, 64 * sizeof(double));
@@ -83,7 +86,7 @@ constexpr int kPoolPerOrder = 2;
 void problem_release(std::unique_ptr<Problem> p) {
   if (!p) return;
   if (p->nccl_comm != nullptr || p->emul_world > 1) return;  // destroyed (unique_ptr goes out of scope)
-  for (Problem* c : {p.get(), p->aux_.get(), p->aux2_.get(), p->crit_.get()})
+  for (Problem* c : {p.get(), p->aux_.get(), p->aux2_.get(), p->aux3_.get(), p->crit_.get()})
     if (c && c->st) KOT_CUDA(cudaStreamSynchronize(c->st));
   std::lock_guard<std::mutex> lk(g_pool_mu);
   int same = 0;
@@ -92,7 +95,7 @@ void problem_release(std::unique_ptr<Problem> p) {
 }
 
 static void refresh_children(Problem& p) {
-  for (Problem* c : {p.aux_.get(), p.aux2_.get(), p.crit_.get()}) {
+  for (Problem* c : {p.aux_.get(), p.aux2_.get(), p.aux3_.get(), p.crit_.get()}) {
     if (!c) continue;
     c->l1 = p.l1;
     c->l2 = p.l2;
@@ -882,6 +885,52 @@ void eg_step(Problem& p, const double* g, const double* X, double s, double* g_o
   proj(p, dc, nullptr, X_out);
 }
 
+void eg_step_parallel(Problem& p, Problem& c, const double* g, const double* X, double s, double* g_out,
+                      double* X_out) {
+  ProfScope ps("eg_step", p.st);
+  Bufs& b = p.bufs();
+  const int n = p.n;
+  Decomp dc{b.Pe, b.vale, 0};
+  // field at v: g_vec = ∇f(γ) − Φ(X)   (eg.py:27-31);  γ½ = γ − s g_vec
+  phi_partials(p, X);
+  finalize(p, FIN_RES, g, true, nullptr, 0.0, b.e1);
+  axpby(p, n, 1.0, g, -s, b.e1, b.e2);
+  if (!p.ev_half) KOT_CUDA(cudaEventCreateWithFlags(&p.ev_half, cudaEventDisableTiming));
+  KOT_CUDA(cudaEventRecord(p.ev_half, p.st));
+  // second projection on c:  X_out = Π(X − s (Φ*(γ½) + λ₁I))
+  std::exception_ptr err = nullptr;
+  std::thread helper([&] {
+    try {
+      KOT_CUDA(cudaSetDevice(c.device));
+      KOT_CUDA(cudaStreamWaitEvent(c.st, p.ev_half, 0));
+      Decomp dc2{c.M2, c.M3, 0};
+      phi_adjoint_ex(c, b.e2, c.M1, -s, X, 1.0, c.l1);
+      eigh(c, c.M1, dc2, true);
+      if (c.eig) c.eig->check_cancel(c.st);
+      proj(c, dc2, nullptr, X_out);
+      KOT_CUDA(cudaStreamSynchronize(c.st));
+    } catch (...) {
+      err = std::current_exception();
+    }
+  });
+  try {
+    // first projection on p:  X½ = Π(X − s (Φ*(γ) + λ₁I)), then g_out = γ − s (∇f(γ½) − Φ(X½))
+    phi_adjoint_ex(p, g, p.M1, -s, X, 1.0, p.l1);
+    eigh(p, p.M1, dc, true);
+    if (p.eig) p.eig->check_cancel(p.st);
+    proj(p, dc, nullptr, b.Xh);
+    phi_partials(p, b.Xh);
+    finalize(p, FIN_RES, b.e2, true, nullptr, 0.0, b.e1);
+    axpby(p, n, 1.0, g, -s, b.e1, g_out);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+  } catch (...) {
+    helper.join();
+    throw;
+  }
+  helper.join();
+  if (err) std::rethrow_exception(err);
+}
+
 static void make_context(Problem& src, std::unique_ptr<Problem>& dst, bool high_priority = false,
                          bool with_eig = true) {
   KOT_CUDA(cudaSetDevice(src.device));
@@ -938,6 +987,14 @@ Problem& Problem::aux2() {
     aux2_->lane = 2;  // residual thread of the EG pipeline
   }
   return *aux2_;
+}
+
+Problem& Problem::aux3() {
+  if (!aux3_) {
+    make_context(*this, aux3_, eg_high_priority(n));
+    aux3_->lane = 1;  // EG step, second projection
+  }
+  return *aux3_;
 }
 
 Problem& Problem::aux() {

@@ -79,14 +79,16 @@ struct Problem {
   double* ygather = nullptr;  // shard_block·world doubles
   int emul_world = 1;          // test hook: all row blocks in turn on one device, no NCCL
   double* shard_tmp = nullptr;  // (⌊ℓ/2⌋+1)·ℓ block partial of T̃ (emulation only)
-  std::unique_ptr<Problem> aux_, aux2_, crit_;
+  std::unique_ptr<Problem> aux_, aux2_, aux3_, crit_;
   Problem& aux();
   Problem& aux2();
+  Problem& aux3();  // second EG-step context: the step's second projection runs beside the first
   // high-priority context for the speculative Newton criterion (no eigensolver workspace):
   // its stream, scratch, outputs (crit_dg, crit_dX, crit_e1) and completion event
   Problem& crit();
   double *crit_dg = nullptr, *crit_dX = nullptr, *crit_e1 = nullptr;
   cudaEvent_t crit_done = nullptr, crit_after = nullptr, crit_dx_done = nullptr;
+  cudaEvent_t ev_half = nullptr;  // eg_step_parallel: γ½ ready
   bool with_eig = true;
   double* alloc(long count);
   void init_scratch();
@@ -117,6 +119,10 @@ double residual_parts(Problem& p, const double* g, const double* X, double* r1, 
 double residual_parts_origin(Problem& p, const double* g, const double* X, double* r1, double* r2, Decomp& dc);
 void middle_operator(Problem& p, const Decomp& dc, double mu, const double* v, double* out);
 void eg_step(Problem& p, const double* g, const double* X, double s, double* g_out, double* X_out);
+// Same values as eg_step; the second projection Π(X − s(Φ*(γ½) + λ₁I)) needs γ½ but not X½
+// (eg.py:34-41), so it runs on context c (its own host thread) concurrently with the first one.
+void eg_step_parallel(Problem& p, Problem& c, const double* g, const double* X, double s, double* g_out,
+                      double* X_out);
 
 // structure-reduced middle operator (the CG matvec of the solver)
 struct MvCtx {
