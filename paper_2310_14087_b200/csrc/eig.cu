@@ -654,14 +654,15 @@ void eig_pipeline_active(int delta) { g_pipelines += delta; }
 static int trd_grid_cap(int lane) {
   static const int cap = std::min(env_int("KOT_TRD_GRID", kNumSMs), kNumSMs);
   // With an EG pipeline running, four cooperative grids can be in flight — Newton chain 96, the EG
-  // step's two projections (run side by side, eg_step_parallel) 64 each, residual at v 48 CTAs — and
+  // step's two projections (run side by side, eg_step_parallel) 48 each, residual at v 32 CTAs — and
   // they fit co-resident in the 2 × 148 slots, so no chain queues at the gate behind another's panel
-  // (probe cfg3 with parallel EG projections: 96/96/64 → 10.2, 96/64/64 → 10.5, 96/64/48 → 11.0,
-  // 112/56/48 → 10.7, 128/48/48 → 11.0, 148/48/48 → 10.9 it/s).  Alone, lane 0 uses every SM.
+  // (probe cfg3 with parallel EG projections: 96/96/64 → 10.2, 96/64/64 → 10.5, 96/64/48 → 10.7–11.0,
+  // 112/56/48 → 10.7, 128/48/48 → 11.0, 96/64/32 → 10.8, 96/48/32 → 11.1, 96/32/32 → 11.1 it/s: the
+  // EG chain has slack, ≈ 58 vs 90 ms per iteration).  Alone, lane 0 uses every SM.
   static const int cap_fg = std::min(env_int("KOT_TRD_GRID_FG", 96), cap);
-  static const int cap_bg = std::min(env_int("KOT_TRD_GRID_BG", 64), cap);
+  static const int cap_bg = std::min(env_int("KOT_TRD_GRID_BG", 48), cap);
   // lane 2 = the EG pipeline's residual thread, lane 1 = its EG-step threads
-  static const int cap_bg2 = std::min(env_int("KOT_TRD_GRID_BG2", 48), cap);
+  static const int cap_bg2 = std::min(env_int("KOT_TRD_GRID_BG2", 32), cap);
   if (lane == 0) return g_pipelines.load() > 0 ? cap_fg : cap;
   return lane == 2 ? cap_bg2 : cap_bg;
 }
