@@ -503,7 +503,7 @@ int kot_eg_step(kot_problem* h, const double* gamma, const double* x, double ste
     const long nn = (long)p.n * p.n;
     up(p, b.gv, gamma, p.n);
     up(p, b.Xv, x, nn);
-    kot::eg_step(p, b.gv, b.Xv, stepsize, b.gt, b.Xt);
+    kot::eg_step_parallel(p, p.aux3(), b.gv, b.Xv, stepsize, b.gt, b.Xt);  // the solver's EG step
     down(p, gamma_out, b.gt, p.n);
     down(p, x_out, b.Xt, nn);
     KOT_CUDA(cudaStreamSynchronize(p.st));
