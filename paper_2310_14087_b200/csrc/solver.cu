@@ -416,7 +416,18 @@ class EgPipeline {
       try {
         KOT_CUDA(cudaSetDevice(a.device));
         const auto t0 = clk::now();
-        eg_step_parallel(a, p_.aux3(), gin, Xin, s_, out.g, out.X);
+        // the step's two projections side by side (default) or in sequence (KOT_EG_PARALLEL=0: fewer
+        // concurrent cooperative grids, for many solves sharing one GPU)
+        static const bool par = [] {
+          const char* e = std::getenv("KOT_EG_PARALLEL");
+          return !(e && std::atoi(e) == 0);
+        }();
+        if (par) {
+          eg_step_parallel(a, p_.aux3(), gin, Xin, s_, out.g, out.X);
+        } else {
+          eg_step(a, gin, Xin, s_, out.g, out.X);
+          KOT_CUDA(cudaStreamSynchronize(a.st));
+        }
         out.eg_ms = ms_since(t0);
         prof_host("host.pipe_eg", out.eg_ms);
       } catch (const Cancelled&) {
