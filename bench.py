@@ -286,7 +286,9 @@ def run_gpu(args):
     torch.cuda.synchronize()
     barrier(world)
     l0 = _lib.launch_count()
-    _lib.profile_enable(True)
+    # roofline scopes only (mode 2): timing every library scope costs ~14 % of the iteration rate;
+    # KOT_BENCH_PROFILE=full records every phase (diagnostics, slower)
+    _lib.profile_enable(not args.no_profile, 1 if os.environ.get("KOT_BENCH_PROFILE") == "full" else 2)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
@@ -360,6 +362,8 @@ def run_gpu(args):
                 "algorithmic": "per launch: sum over its 32 columns of one lower-triangle read of the "
                                "trailing matrix, 8*m(m+1)/2 B",
                 "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"],
+                "sampled": None if os.environ.get("KOT_BENCH_PROFILE") == "full" else
+                "1 in 16 launches (time and algorithmic bytes of the same launches)",
                 "note": "latency-bound: 2 grid barriers + ~4 dependent L2 round trips per column"}
     if roof is None and "eig.q2" in prof:  # two-stage path (l >= 3000): the tensor-core Q2 back-transform
         e = prof["eig.q2"]
@@ -377,9 +381,13 @@ def run_gpu(args):
         roof_gemm = {"kernel": "gemm_dmma_kernel (mma.sync m8n8k4 f64, all shapes)", "bound": "tensor",
                      "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
                      "traffic": None, "peak_source": "measured DMMA microbenchmark (MEASURED_PEAKS.json has no FP64)",
-                     "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"]}
+                     "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"],
+                     "sampled": None if os.environ.get("KOT_BENCH_PROFILE") == "full" else "1 in 128 launches"}
+    full = os.environ.get("KOT_BENCH_PROFILE") == "full"
     phases = {k: {"ms_per_step": v["ms"] / max(done, 1), "calls_per_step": v["calls"] / max(done, 1),
-                  **({"tflops": v["flops"] / (v["ms"] * 1e-3) / 1e12} if v["flops"] and v["ms"] else {})}
+                  **({"tflops": v["flops"] / (v["ms"] * 1e-3) / 1e12} if v["flops"] and v["ms"] else {}),
+                  **({"sampled": {"gemm_dmma": "1 in 128 launches", "sytrd_panel": "1 in 16 launches"}[k]}
+                     if k in ("gemm_dmma", "sytrd_panel") and not full else {})}
               for k, v in prof.items()}
 
     # ---------------- CPU baseline (oracle port, bounded sample)
@@ -489,6 +497,7 @@ def main():
     ap.add_argument("--profile", default="paper", choices=["paper", "tight"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-6 leg")
+    ap.add_argument("--no-profile", action="store_true", help="diagnostic: no phase profiler in the timed region")
     ap.add_argument("--batch", type=int, default=16, help="cfg5: number of problems")
     ap.add_argument("--concurrency", type=int, default=6, help="cfg5: concurrent solves per GPU")
     ap.add_argument("--tol", type=float, default=1e-6, help="cfg5: residual tolerance")

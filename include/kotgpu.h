@@ -145,7 +145,7 @@ typedef struct {
   double flops;   /* algorithmic FLOPs (0 where not applicable) */
   double bytes;   /* algorithmic HBM/L2 bytes (0 where not applicable) */
 } kot_prof_entry;
-int kot_profile_enable(int on);      /* resets the counters */
+int kot_profile_enable(int on);  /* 0 off, 1 every scope, 2 roofline scopes only (cheap); resets the counters */
 int kot_profile_read(kot_prof_entry* out, int cap);  /* returns #entries */
 
 /* ---- operators (host buffers in/out; per-kernel parity) ----------------- */

@@ -188,8 +188,10 @@ def launch_count() -> int:
     return int(lib().kot_launch_count())
 
 
-def profile_enable(on: bool = True) -> None:
-    lib().kot_profile_enable(1 if on else 0)
+def profile_enable(on: bool = True, mode: int = 1) -> None:
+    """mode 1: every library scope; mode 2: only the roofline scopes (sytrd panels, Q2, 1/16 of the
+    GEMM launches) — cheap enough to leave on inside a timed region."""
+    lib().kot_profile_enable(mode if on else 0)
 
 
 def profile_read() -> dict:

@@ -337,7 +337,8 @@ void gemm_launch_tiled(const GemmShape& s, const Epi& epi, cudaStream_t st) {
   if (s.M <= 0 || s.N <= 0) return;
   if (BM != BN) kot_require(!s.sym_tiles, KOT_EINVAL, "symmetric tiling needs square CTA tiles");
   constexpr int smem = GTile<BM, BN>::SMEM;
-  ProfScope prof("gemm_dmma", st, prof_enabled() ? gemm_alg_flops(s, BM, BN) : 0.0);
+  ProfScope prof("gemm_dmma", st);
+  if (prof.tok >= 0) prof.flops = gemm_alg_flops(s, BM, BN);  // only for recorded (sampled) launches
   const int tiles = gemm_grid(s, BM, BN);
   const dim3 grid(tiles, s.ksplit > 1 ? s.ksplit : 1);
   if (gemm_vec2_ok(s)) {
