@@ -253,7 +253,8 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
     __syncthreads();
     for (int q = threadIdx.x; q < BM; q += G_THREADS) {
       const int r = m0 + q;
-      if (r < s.M) epi.rowdot_store(tn, r, red[q] + red[BM + q]);
+      // split-K: every K share writes its own partial row block (row-dots are linear in the product)
+      if (r < s.M) epi.rowdot_store(tn + (int)blockIdx.y * tiles_n_grid, r, red[q] + red[BM + q]);
     }
   } else if (s.ksplit > 1) {
     double* ws = s.ws + (long)blockIdx.y * s.M * n_static;

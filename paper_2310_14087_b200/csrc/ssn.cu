@@ -578,6 +578,7 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
   const double* Bs = m.Bs;  // columns of the T̃-row block (the smaller sign block)
   const double* Bo = m.Bo;  // columns of the other block
   const long ld = m.ldp;
+  int rd_tiles = 0;
   if (ks > 0 && ns > 0) {
     GemmShape s = make_shape(ks, ns, n, Bs, ld, Bo, ld);
     s.kscale = v;
@@ -590,12 +591,21 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
     if (mv_split > 1 && (long)mv_split * s.M * s.N <= p.splitws_cap) s.ksplit = mv_split;
     gemm_launch<true, false>(s, EpiMvOff{b.Ct, n, m.dc.vals, k, m.pos ? 1 : 0, m.mu}, p.st);
     GemmShape s2 = make_shape(n, ks, ns, Bo, ld, b.Ct, n);
+    // optional split-K on the row-dot GEMM (each K share adds its own partial rows, summed in fixed
+    // order by finalize); KOT_MV2_SPLIT=2 measured neutral inside the solver (12.66 vs 12.68 it/s)
+    static const int mv2_split = [] {
+      const char* e = std::getenv("KOT_MV2_SPLIT");
+      return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    s2.ksplit = (mv2_split > 1 && (long)mv2_split * ceil_div(ks, GB_N) <= ceil_div(n, GB_N) && ns >= 256 * mv2_split)
+                    ? mv2_split : 1;
     gemm_launch<false, true>(s2, EpiRowDot{Bs, ld, p.partial, n}, p.st);
+    rd_tiles = ceil_div(ks, GB_N) * s2.ksplit;
   }
   FinArgs f;
   f.n = n;
   f.mode = FIN_MATVEC_B;
-  f.tiles = (ks > 0 && ns > 0) ? ceil_div(ks, GB_N) : 0;
+  f.tiles = (ks > 0 && ns > 0) ? rd_tiles : 0;
   f.tri = 0;
   f.Q = p.Q;
   f.G2 = m.H;

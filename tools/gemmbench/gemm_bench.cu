@@ -43,6 +43,8 @@ int main() {
   run<false, true>(2000, 2000, 2000, 10, A, B, C, "NT square 2000");
   run<false, false>(4096, 4096, 4096, 5, A, B, C, "NN square 4096");
   run<true, false>(1000, 2000, 2000, 10, A, B, C, "TN matvec C (k=1000)");
+  run<true, false>(1000, 1000, 2000, 20, A, B, C, "TN H-form GEMM1 split3", 3, W);
+  run<false, true>(2000, 1000, 1000, 20, A, B, C, "NT H-form GEMM2");
   run<false, true>(2000, 1000, 2000, 10, A, B, C, "NT matvec F (k=1000)");
   run<true, false>(100, 2000, 2000, 10, A, B, C, "TN C k=100");
   run<true, false>(100, 2000, 2000, 10, A, B, C, "TN C k=100 split", 8, W);
