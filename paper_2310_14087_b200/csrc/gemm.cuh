@@ -63,6 +63,7 @@ struct GemmShape {
   const int* dN;
   const int* dK;
   const int* dKstart;
+  const double* skipf = nullptr;  // nullable: the launch is a no-op when *skipf != 0 (batched CG)
   int sym_tiles;  // enumerate only tiles with tm <= tn (symmetric outputs)
   // split-K: grid.y = ksplit partial products written to ws[split][M][N] (ld N),
   // then reduced in fixed order by splitk_reduce_kernel (deterministic).
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
   using T = GTile<BM, BN>;
   static_assert(!Epi::kRowDot || BN == GB_N, "row-dot partials are per 64-column tile");
   extern __shared__ __align__(16) double gsm[];
+  if (s.skipf != nullptr && *s.skipf != 0.0) return;
   const int tiles_n_grid = (s.N + BN - 1) / BN;  // grid layout uses the static bound
   const int n_static = s.N;                        // … and so does the split-K partial layout
   if (s.dN) s.N = *s.dN;
@@ -288,7 +290,8 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
 
 template <class Epi>
 __global__ void splitk_reduce_kernel(int M, int N, int splits, int sym_tiles, const double* __restrict__ ws,
-                                     Epi epi, const int* __restrict__ dN) {
+                                     Epi epi, const int* __restrict__ dN, const double* skipf) {
+  if (skipf != nullptr && *skipf != 0.0) return;
   // ws layout [split][M][N] with the static N; columns ≥ *dN (device-side N) were not computed
   const int n_act = dN ? *dN : N;
   const long total = (long)M * N;
@@ -356,7 +359,7 @@ void gemm_launch_tiled(const GemmShape& s, const Epi& epi, cudaStream_t st) {
     if (s.ksplit > 1) {
       const long total = (long)s.M * s.N;
       splitk_reduce_kernel<Epi><<<(int)std::min<long>((total + 255) / 256, 4L * 148 * 8), 256, 0, st>>>(
-          s.M, s.N, s.ksplit, s.sym_tiles, s.ws, epi, s.dN);
+          s.M, s.N, s.ksplit, s.sym_tiles, s.ws, epi, s.dN, s.skipf);
       KOT_LAUNCH_CHECK();
     }
   }

@@ -32,6 +32,8 @@ static double ms_since(clk::time_point t0) {
 constexpr int CG_THREADS = 1024;
 // scalar slots in p.dsc used by CG
 constexpr int SC_RR = 8, SC_BN = 9, SC_PAP = 10, SC_RES = 11, SC_FLAG = 12;
+// batched CG (device-side stopping): done flag, completed steps, target residual, step limit
+constexpr int SC_DONE = 13, SC_IT = 14, SC_TARGET = 15, SC_MAXIT = 16;
 
 __global__ void __launch_bounds__(CG_THREADS) cg_init_kernel(int n, const double* __restrict__ b, double* x,
                                                              double* r, double* pv, double* sc) {
@@ -53,8 +55,12 @@ __global__ void __launch_bounds__(CG_THREADS) cg_init_kernel(int n, const double
 
 // one CG update after ap = A p (linalg.py:142-161)
 __global__ void __launch_bounds__(CG_THREADS) cg_step_kernel(int n, double* x, double* r, double* pv,
-                                                             const double* __restrict__ ap, double* sc) {
+                                                             const double* __restrict__ ap, double* sc,
+                                                             int batched) {
   __shared__ double sh[32];
+  // batched mode: the stopping test of cg_solve runs here (same arithmetic, same order); once it
+  // fires, this and every later launch of the batch (matvec kernels included) is a no-op
+  if (batched && sc[SC_DONE] != 0.0) return;
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += pv[i] * ap[i];
   const double pap = block_sum(s, sh);
@@ -62,11 +68,17 @@ __global__ void __launch_bounds__(CG_THREADS) cg_step_kernel(int n, double* x, d
   __syncthreads();
   if (threadIdx.x == 0) sc[SC_PAP] = pap;
   if (!isfinite(pap)) {
-    if (threadIdx.x == 0) sc[SC_FLAG] = 1.0;
+    if (threadIdx.x == 0) {
+      sc[SC_FLAG] = 1.0;
+      sc[SC_DONE] = 1.0;
+    }
     return;
   }
   if (pap <= 0.0) {
-    if (threadIdx.x == 0) sc[SC_FLAG] = 2.0;
+    if (threadIdx.x == 0) {
+      sc[SC_FLAG] = 2.0;
+      sc[SC_DONE] = 1.0;
+    }
     return;
   }
   const double alpha = rr / pap;
@@ -86,7 +98,19 @@ __global__ void __launch_bounds__(CG_THREADS) cg_step_kernel(int n, double* x, d
     sc[SC_RES] = res;
     sc[SC_RR] = rrn;
     sc[SC_FLAG] = isfinite(res) ? 0.0 : 3.0;
+    if (batched) {
+      const double it = sc[SC_IT] + 1.0;
+      sc[SC_IT] = it;
+      if (!isfinite(res) || res <= sc[SC_TARGET] || it >= sc[SC_MAXIT]) sc[SC_DONE] = 1.0;
+    }
   }
+}
+
+__global__ void cg_arm_kernel(double* sc, double target, int max_iter) {
+  sc[SC_DONE] = 0.0;
+  sc[SC_IT] = 0.0;
+  sc[SC_TARGET] = target;
+  sc[SC_MAXIT] = (double)max_iter;
 }
 
 struct CgOut {
@@ -108,13 +132,44 @@ static CgOut cg_solve(Problem& p, const MvCtx& mv, const double* rhs, double tol
   const double target = tol * p.hsc[SC_BN];
   double res = p.hsc[SC_BN];
   if (res <= target) return {0, res};
+  // Batched stopping (H-form matvec): B iterations are enqueued per host check and the device applies
+  // the stopping rule (cg_step_kernel, batched mode) — the launches after the stop are no-ops — so
+  // the host waits once per B steps instead of after every step; identical arithmetic and results.
+  static const int kBatch = [] {
+    const char* e = std::getenv("KOT_CG_BATCH");
+    return e ? std::max(1, std::atoi(e)) : 4;
+  }();
+  if (!mv.direct && mv.hform && kBatch > 1) {
+    cg_arm_kernel<<<1, 1, 0, p.st>>>(p.dsc, target, max_iter);
+    KOT_LAUNCH_CHECK();
+    const double* done = p.dsc + SC_DONE;
+    int launched = 0;
+    for (;;) {
+      for (int bq = 0; bq < kBatch && launched < max_iter; ++bq, ++launched) {
+        middle_operator_fast(p, mv, b.cp, b.cap, done);
+        cg_step_kernel<<<1, CG_THREADS, 0, p.st>>>(n, b.cx, b.cr, b.cp, b.cap, p.dsc, 1);
+        KOT_LAUNCH_CHECK();
+      }
+      fetch(p, SC_MAXIT + 1);
+      const bool stop = p.hsc[SC_DONE] != 0.0 || launched >= max_iter;
+      const int it = (int)p.hsc[SC_IT];
+      if (stop) {
+        const int flag = (int)p.hsc[SC_FLAG];
+        if (flag == 1) throw KotError(KOT_ECG, "non-finite curvature in conjugate gradient");
+        if (flag == 3) throw KotError(KOT_ECG, "non-finite residual in conjugate gradient");
+        return {it, it > 0 ? p.hsc[SC_RES] : res};  // flag 2: the last completed step's residual
+      }
+      res = p.hsc[SC_RES];
+      if (abort && (*abort)()) return {it, res, true};
+    }
+  }
   int it = 0;
   for (it = 1; it <= max_iter; ++it) {
     if (mv.direct)
       middle_operator(p, mv.dc, mv.mu, b.cp, b.cap);
     else
       middle_operator_fast(p, mv, b.cp, b.cap);
-    cg_step_kernel<<<1, CG_THREADS, 0, p.st>>>(n, b.cx, b.cr, b.cp, b.cap, p.dsc);
+    cg_step_kernel<<<1, CG_THREADS, 0, p.st>>>(n, b.cx, b.cr, b.cp, b.cap, p.dsc, 0);
     KOT_LAUNCH_CHECK();
     fetch(p, 16);
     const int flag = (int)p.hsc[SC_FLAG];

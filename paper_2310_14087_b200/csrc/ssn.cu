@@ -329,10 +329,12 @@ struct FinArgs {
   const double* r1v;
   double l2, mu, phsign;
   double* out;
+  const double* skipf = nullptr;  // nullable: no-op when *skipf != 0 (batched CG)
 };
 
 // warp per row: GEMV row of Q (coalesced) + fixed-order sum of the Φ partials.
 __global__ void finalize_kernel(FinArgs f) {
+  if (f.skipf != nullptr && *f.skipf != 0.0) return;
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int r = f.r0 + blockIdx.x * warps + (threadIdx.x >> 5); r < f.r1; r += gridDim.x * warps) {
@@ -568,7 +570,8 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allo
 
 // y = Qv/(2λ₂) + μv + (Hv)/μ + Σ_{a∈α, b∈ᾱ} 2ξ_ab (B_{:,a}∘B_{:,b})·C_ab,  C = Bᵀdiag(v)B
 // (one process, no row blocks): two DMMA GEMMs of 2·k(ℓ−k)·ℓ FLOPs each + two GEMVs.
-static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, double* out) {
+static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, double* out,
+                                  const double* skipf) {
   const int n = p.n, k = m.dc.k;
   const int ks = m.pos ? k : n - k;  // rows of T̃ (the smaller sign block)
   const int ns = n - ks;
@@ -582,6 +585,7 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
   if (ks > 0 && ns > 0) {
     GemmShape s = make_shape(ks, ns, n, Bs, ld, Bo, ld);
     s.kscale = v;
+    s.skipf = skipf;
     s.ws = p.splitws;
     s.ksplit = choose_ksplit(s, p.splitws_cap);
     static const int mv_split = [] {
@@ -591,6 +595,7 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
     if (mv_split > 1 && (long)mv_split * s.M * s.N <= p.splitws_cap) s.ksplit = mv_split;
     gemm_launch<true, false>(s, EpiMvOff{b.Ct, n, m.dc.vals, k, m.pos ? 1 : 0, m.mu}, p.st);
     GemmShape s2 = make_shape(n, ks, ns, Bo, ld, b.Ct, n);
+    s2.skipf = skipf;
     // optional split-K on the row-dot GEMM (each K share adds its own partial rows, summed in fixed
     // order by finalize); KOT_MV2_SPLIT=2 measured neutral inside the solver (12.66 vs 12.68 it/s)
     static const int mv2_split = [] {
@@ -609,6 +614,7 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
   f.tri = 0;
   f.Q = p.Q;
   f.G2 = m.H;
+  f.skipf = skipf;
   f.u = v;
   f.partial = f.tiles > 0 ? p.partial : nullptr;
   f.z = p.z;
@@ -623,7 +629,7 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
   KOT_LAUNCH_CHECK();
 }
 
-void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* out) {
+void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* out, const double* skipf) {
   const int n = p.n, k = m.dc.k;
   const int ks = m.pos ? k : n - k;
   const bool nccl = p.nccl_comm != nullptr;
@@ -631,9 +637,10 @@ void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* o
   const double nn = n, own = nccl ? p.row1 - p.row0 : n;
   Bufs& b = p.bufs();
   if (m.hform) {
-    middle_operator_hform(p, m, v, out);
+    middle_operator_hform(p, m, v, out, skipf);
     return;
   }
+  kot_require(skipf == nullptr, KOT_EINVAL, "batched CG needs the H-form matvec");
   ProfScope ps("matvec", p.st, 4.0 * ks * nn * own + 2.0 * nn * own);
   const double* Bsub = m.pos ? m.B : m.B + k;
   if (ks > 0) {

@@ -144,7 +144,9 @@ void problem_unshard(Problem& p);
 void problem_shard_emulate(Problem& p, int world);
 void shard_allreduce_sum(Problem& p, double* buf, long count);
 void shard_allgather(Problem& p, double* buf, long block);
-void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* out);
+// skipf (nullable): every launch is a no-op once *skipf != 0 (batched CG, H form only)
+void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* out,
+                          const double* skipf = nullptr);
 
 struct NewtonOut {
   int cg_iters, met, attempts;
