@@ -96,6 +96,19 @@ void EigWork::ensure_two_stage() {
   KOT_CUDA(cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming));
 }
 
+void EigWork::ensure_tfactors() {
+  if (Tall) return;
+  const int nblk = std::max(1, (n - 1 + 127) / 128);
+  Tall = static_cast<double*>(dev_alloc(sizeof(double) * 128L * 128 * nblk));
+  Sside = static_cast<double*>(dev_alloc(sizeof(double) * 128L * 128));
+  ws_t = static_cast<double*>(dev_alloc(sizeof(double) * 16L * 128 * 128));
+  int lo = 0, hi = 0;
+  KOT_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  KOT_CUDA(cudaStreamCreateWithPriority(&st_t, cudaStreamNonBlocking, hi));
+  KOT_CUDA(cudaEventCreateWithFlags(&ev_t0, cudaEventDisableTiming));
+  KOT_CUDA(cudaEventCreateWithFlags(&ev_t1, cudaEventDisableTiming));
+}
+
 EigWork::~EigWork() {
   for (double* p : {A, Vall, X, d, e, tau, xv, yv, part, partn, Tf, W1, Q, Qw, Qnd, Dl, Uw, zs, ds, dlam, wv, what, lam,
                     dfv, rotcs, rho, splitws, gpart, Vq2, Tq2, tq2})
@@ -104,6 +117,13 @@ EigWork::~EigWork() {
     cudaStreamSynchronize(st2);
     cudaStreamDestroy(st2);
   }
+  if (st_t) {
+    cudaStreamSynchronize(st_t);
+    cudaStreamDestroy(st_t);
+  }
+  if (ev_t0) cudaEventDestroy(ev_t0);
+  if (ev_t1) cudaEventDestroy(ev_t1);
+  for (double* q : {Tall, Sside, ws_t}) dev_free(q);
   if (ev_w) cudaEventDestroy(ev_w);
   if (ev_rest) cudaEventDestroy(ev_rest);
   dev_free(gcnt);
@@ -1590,32 +1610,46 @@ __global__ void count_pos_kernel(const double* vals, int n, int* k) {
 // reflectors (I − V T Vᵀ), last block first: W1 = Vᵀ P (split-K), W2 = T W1,
 // P −= V W2.
 // dcols (nullable, device): only the first *dcols columns of P are transformed.
+// T factor of every 128-reflector block (S = VᵀV, larft) on w.st_t: nothing here depends on the
+// tridiagonal eigenvectors, so it runs beside stedc and ormtr only waits for w.ev_t1.
+static void tfactors_async(int n, EigWork& w, cudaStream_t st) {
+  w.ensure_tfactors();
+  const int nref = n - 1;
+  const int nblk = (nref + ORM_NB - 1) / ORM_NB;
+  KOT_CUDA(cudaEventRecord(w.ev_t0, st));
+  KOT_CUDA(cudaStreamWaitEvent(w.st_t, w.ev_t0, 0));
+  for (int bi = 0; bi < nblk; ++bi) {
+    const int p0 = bi * ORM_NB;
+    const int nb = std::min(ORM_NB, nref - p0);
+    const int r0 = p0 + 1;
+    const double* Vp = w.Vall + (long)r0 * n + p0;
+    GemmShape s = make_shape(nb, nb, n - r0, Vp, n, Vp, n);  // S = Vᵀ V (symmetric, one triangle mirrored)
+    s.sym_tiles = 1;
+    s.ws = w.ws_t;
+    s.ksplit = choose_ksplit(s, 16L * 128 * 128);
+    gemm_launch<true, false>(s, EpiSymMirror{w.Sside, nb, 1.0, nullptr, 0.0, 0.0}, w.st_t);
+    ProfScope pl("orm.larft", w.st_t);
+    ensure_smem_attr((const void*)larft_kernel, LARFT_SMEM);
+    larft_kernel<<<ceil_div(nb, LARFT_THREADS / 32), LARFT_THREADS, LARFT_SMEM, w.st_t>>>(
+        w.Sside, w.tau + p0, nb, w.Tall + (long)bi * ORM_NB * ORM_NB);
+    KOT_LAUNCH_CHECK();
+  }
+  KOT_CUDA(cudaEventRecord(w.ev_t1, w.st_t));
+}
+
 static void ormtr(int n, EigWork& w, double* P, cudaStream_t st, const int* dcols = nullptr) {
   const int nref = n - 1;  // reflectors 0..n-2
   const int nblk = (nref + ORM_NB - 1) / ORM_NB;
-  double* S = w.Tf + ORM_NB * ORM_NB;
-  double* T = w.Tf;
   double* W1 = w.W1;
   double* W2 = w.W1 + (long)ORM_NB * n;
+  KOT_CUDA(cudaStreamWaitEvent(st, w.ev_t1, 0));  // T factors (tfactors_async)
   for (int bi = nblk - 1; bi >= 0; --bi) {
     const int p0 = bi * ORM_NB;
     const int nb = std::min(ORM_NB, nref - p0);
     const int r0 = p0 + 1;
     const int mrows = n - r0;
     const double* Vp = w.Vall + (long)r0 * n + p0;  // mrows × nb (ld n), zero above each unit entry
-    {  // S = Vᵀ V  (symmetric, one triangle mirrored)
-      GemmShape s = make_shape(nb, nb, mrows, Vp, n, Vp, n);
-      s.sym_tiles = 1;
-      s.ws = w.splitws;
-      s.ksplit = choose_ksplit(s, w.splitws_cap);
-      gemm_launch<true, false>(s, EpiSymMirror{S, nb, 1.0, nullptr, 0.0, 0.0}, st);
-    }
-    {
-      ProfScope pl("orm.larft", st);
-      ensure_smem_attr((const void*)larft_kernel, LARFT_SMEM);
-      larft_kernel<<<ceil_div(nb, LARFT_THREADS / 32), LARFT_THREADS, LARFT_SMEM, st>>>(S, w.tau + p0, nb, T);
-      KOT_LAUNCH_CHECK();
-    }
+    const double* T = w.Tall + (long)bi * ORM_NB * ORM_NB;
     {  // W1 = Vᵀ P[r0:, :]
       GemmShape s = make_shape(nb, n, mrows, Vp, n, P + (long)r0 * n, n);
       s.dN = dcols;
@@ -1739,6 +1773,7 @@ void syevd_device(const double* Z, int n, double* P, double* vals, int* dk, EigW
     else
       one_stage_tridiag(Z, n, w, st, lane);
     w.check_cancel(st);
+    tfactors_async(n, w, st);
     {
       ProfScope ps("eig.stedc", st);
       stedc(n, w, st);

@@ -31,6 +31,11 @@ struct EigWork {
   int* gcnt = nullptr;
   double *Vq2 = nullptr, *tq2 = nullptr, *Tq2 = nullptr;  // two-stage: stage-2 reflectors, τ, group T
   cudaStream_t st2 = nullptr;  // two-stage: look-ahead stream
+  // back-transform T factors, computed on st_t beside the tridiagonal eigensolve (ormtr only waits)
+  double *Tall = nullptr, *Sside = nullptr, *ws_t = nullptr;
+  cudaStream_t st_t = nullptr;
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+  void ensure_tfactors();
   cudaEvent_t ev_w = nullptr, ev_rest = nullptr;
   long splitws_cap = 0;
   const std::atomic<bool>* cancel = nullptr;  // set: throw Cancelled at the next panel boundary
@@ -38,6 +43,7 @@ struct EigWork {
     if (cancel && cancel->load(std::memory_order_relaxed)) {
       cudaStreamSynchronize(st);  // in-flight grids retire before any gate slot is released
       if (st2) cudaStreamSynchronize(st2);
+      if (st_t) cudaStreamSynchronize(st_t);
       throw Cancelled{};
     }
   }
