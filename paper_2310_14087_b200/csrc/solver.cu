@@ -113,6 +113,29 @@ __global__ void cg_arm_kernel(double* sc, double target, int max_iter) {
   sc[SC_MAXIT] = (double)max_iter;
 }
 
+// CG iterations enqueued per host check (KOT_CG_BATCH, test hook kot_debug_cg_batch; 1 = a host
+// check after every iteration) and whether the EG step runs its two projections side by side
+// (KOT_EG_PARALLEL, kot_debug_eg_parallel)
+static std::atomic<int> g_cg_batch{-1}, g_eg_parallel{-1};
+static int cg_batch() {
+  int v = g_cg_batch.load();
+  if (v < 0) {
+    const char* e = std::getenv("KOT_CG_BATCH");
+    v = e ? std::max(1, std::atoi(e)) : 4;
+    g_cg_batch = v;
+  }
+  return v;
+}
+static bool eg_parallel() {
+  int v = g_eg_parallel.load();
+  if (v < 0) {
+    const char* e = std::getenv("KOT_EG_PARALLEL");
+    v = (e && std::atoi(e) == 0) ? 0 : 1;
+    g_eg_parallel = v;
+  }
+  return v != 0;
+}
+
 struct CgOut {
   int iters;
   double res;
@@ -135,10 +158,7 @@ static CgOut cg_solve(Problem& p, const MvCtx& mv, const double* rhs, double tol
   // Batched stopping (H-form matvec): B iterations are enqueued per host check and the device applies
   // the stopping rule (cg_step_kernel, batched mode) — the launches after the stop are no-ops — so
   // the host waits once per B steps instead of after every step; identical arithmetic and results.
-  static const int kBatch = [] {
-    const char* e = std::getenv("KOT_CG_BATCH");
-    return e ? std::max(1, std::atoi(e)) : 4;
-  }();
+  const int kBatch = cg_batch();
   if (!mv.direct && mv.hform && kBatch > 1) {
     cg_arm_kernel<<<1, 1, 0, p.st>>>(p.dsc, target, max_iter);
     KOT_LAUNCH_CHECK();
@@ -473,11 +493,7 @@ class EgPipeline {
         const auto t0 = clk::now();
         // the step's two projections side by side (default) or in sequence (KOT_EG_PARALLEL=0: fewer
         // concurrent cooperative grids, for many solves sharing one GPU)
-        static const bool par = [] {
-          const char* e = std::getenv("KOT_EG_PARALLEL");
-          return !(e && std::atoi(e) == 0);
-        }();
-        if (par) {
+        if (eg_parallel()) {
           eg_step_parallel(a, p_.aux3(), gin, Xin, s_, out.g, out.X);
         } else {
           eg_step(a, gin, Xin, s_, out.g, out.X);
@@ -884,3 +900,13 @@ IterRecord iterate_once(Problem& p, const SolverCfg& cfg, const ReplayIn& in, Re
 }
 
 }  // namespace kot
+
+extern "C" int kot_debug_cg_batch(int batch) {  // test hook: CG iterations per host check (≥ 1)
+  kot::g_cg_batch = batch >= 1 ? batch : 1;
+  return 0;
+}
+
+extern "C" int kot_debug_eg_parallel(int on) {  // test hook: EG projections side by side (1) or in sequence
+  kot::g_eg_parallel = on ? 1 : 0;
+  return 0;
+}

@@ -390,6 +390,28 @@ def test_solve_report_serialises_exactly(cfg1, tmp_path):
     assert back.trace == rep.trace == RP.read_trace_csv(str(tmp_path / "t.csv"))
 
 
+@pytest.mark.parametrize("hook,values", [("kot_debug_cg_batch", (1, 4, 7)), ("kot_debug_eg_parallel", (0, 1))])
+def test_schedule_variants_are_bit_identical(hook, values):
+    """Batched CG stopping (device-side test, B iterations per host check) and the parallel EG
+    projections only change the schedule: the solve must be bit-identical for every setting."""
+    from paper_2310_14087_b200 import _lib
+    f = getattr(_lib.lib(), hook)
+    pd = _cfg5_like(7, 700)
+    step = 0.5 / (np.linalg.norm(pd.q_mat) / (2 * pd.lambda2) + np.linalg.norm(pd.pair_gram()))
+    cfg = K.SolverConfig(eg=EgConfig(step), residual_tol=1e-12, max_iter=6)
+    reps = []
+    try:
+        for v in values:
+            f(v)
+            reps.append(K.solve(pd, cfg))
+    finally:
+        f(values[-1] if hook == "kot_debug_eg_parallel" else 4)
+    for r in reps[1:]:
+        assert np.array_equal(r.gamma_hat, reps[0].gamma_hat) and np.array_equal(r.x_hat, reps[0].x_hat)
+        assert [(t.res_accepted, t.res_eg, t.cg_iters) for t in r.trace] == \
+               [(t.res_accepted, t.res_eg, t.cg_iters) for t in reps[0].trace]
+
+
 def test_lockstep_replay_cfg1(cfg1):
     """one GPU iteration from each saved oracle state.
 
