@@ -15,6 +15,7 @@
 // by restricting the K range per output tile.
 #pragma once
 #include <algorithm>
+#include <type_traits>
 #include "common.cuh"
 #include "prof.cuh"
 
@@ -211,25 +212,38 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
     const double* as = As + stage * T::ATILE;
     const double* bs = Bs + stage * T::BTILE;
     const double* ks = Ks + stage * GB_K;
+    // the K-scaling multiply only exists in the instantiation that needs it (uniform branch)
+    auto mma_stage = [&](auto has_kscale) {
+      constexpr bool kKS = decltype(has_kscale)::value;
 #pragma unroll
-    for (int kk = 0; kk < GB_K; kk += 4) {
-      double a[T::MI], b[T::NJ];
-      const double kscl = (s.kscale != nullptr) ? ks[kk + t] : 1.0;
+      for (int kk = 0; kk < GB_K; kk += 4) {
+        double a[T::MI], b[T::NJ];
+        double kscl = 1.0;
+        if constexpr (kKS) kscl = ks[kk + t];
 #pragma unroll
-      for (int i = 0; i < T::MI; i++) {
-        const int m = wm + i * 8 + g;
-        a[i] = (TA ? as[(kk + t) * T::PADM + m] : as[m * G_PADK + kk + t]) * kscl;
+        for (int i = 0; i < T::MI; i++) {
+          const int m = wm + i * 8 + g;
+          const double av = TA ? as[(kk + t) * T::PADM + m] : as[m * G_PADK + kk + t];
+          if constexpr (kKS)
+            a[i] = av * kscl;
+          else
+            a[i] = av;
+        }
+#pragma unroll
+        for (int j = 0; j < T::NJ; j++) {
+          const int n = wn + j * 8 + g;
+          b[j] = TB ? bs[n * G_PADK + kk + t] : bs[(kk + t) * T::PADN + n];
+        }
+#pragma unroll
+        for (int i = 0; i < T::MI; i++)
+#pragma unroll
+          for (int j = 0; j < T::NJ; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
       }
-#pragma unroll
-      for (int j = 0; j < T::NJ; j++) {
-        const int n = wn + j * 8 + g;
-        b[j] = TB ? bs[n * G_PADK + kk + t] : bs[(kk + t) * T::PADN + n];
-      }
-#pragma unroll
-      for (int i = 0; i < T::MI; i++)
-#pragma unroll
-        for (int j = 0; j < T::NJ; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-    }
+    };
+    if (s.kscale != nullptr)
+      mma_stage(std::true_type{});
+    else
+      mma_stage(std::false_type{});
   }
   cp_async_wait<0>();
 
