@@ -252,6 +252,18 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
   ProfScope ps("newton", p.st);
   // filt = r2 + 𝒯[r2];  a1 = −r1 − Φ(filt)/(μ+1);  ã2 = −filt/(μ+1)   (newton.py:161-163)
   auto ppre = std::make_unique<ProfScope>("newton.prologue", p.st);
+  // B = R·P, its packed sign blocks and H depend only on the decomposition: built on the criterion
+  // context's (idle) stream beside 𝒯[r2] and the right-hand side, joined before the first matvec
+  Problem& q = p.crit();
+  if (!p.ev_mv0) {
+    KOT_CUDA(cudaEventCreateWithFlags(&p.ev_mv0, cudaEventDisableTiming));
+    KOT_CUDA(cudaEventCreateWithFlags(&p.ev_mv1, cudaEventDisableTiming));
+  }
+  KOT_CUDA(cudaEventRecord(p.ev_mv0, p.st));
+  KOT_CUDA(cudaStreamWaitEvent(q.st, p.ev_mv0, 0));
+  MvCtx mv;
+  matvec_prepare(p, dc, mu, mv, true, q.st);
+  KOT_CUDA(cudaEventRecord(p.ev_mv1, q.st));
   spectral_filter(p, dc, r2, p.M2, mu, 0);
   axpby(p, nn, 1.0, r2, 1.0, p.M2, b.filt);
   phi_partials(p, b.filt);
@@ -260,10 +272,8 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
   double rel = cfg.has_cg_tol ? cfg.cg_tol : cfg.tau * std::min(1.0, cfg.kappa * rn);
   const double a1n = dev_norm(p, b.a1, n);
   KOT_CUDA(cudaMemsetAsync(b.sol, 0, sizeof(double) * n, p.st));
-  MvCtx mv;
-  matvec_prepare(p, dc, mu, mv);
+  KOT_CUDA(cudaStreamWaitEvent(p.st, p.ev_mv1, 0));
   ppre.reset();
-  Problem& q = p.crit();
   NewtonOut out{0, 0, 0, INFINITY, 0.0, 0.0};
   const auto t0 = clk::now();
   bool pending = false;  // criterion of attempt `att − 1` in flight on q

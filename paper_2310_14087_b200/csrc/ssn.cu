@@ -67,6 +67,8 @@ Problem::~Problem() {
   if (crit_after) cudaEventDestroy(crit_after);
   if (crit_dx_done) cudaEventDestroy(crit_dx_done);
   if (ev_half) cudaEventDestroy(ev_half);
+  if (ev_mv0) cudaEventDestroy(ev_mv0);
+  if (ev_mv1) cudaEventDestroy(ev_mv1);
   eig.reset();
   for (double* p : owned) dev_free(p);
   host_free_pinned(hsc, 64 * sizeof(double));
@@ -507,7 +509,9 @@ static std::vector<std::pair<int, int>> row_blocks(const Problem& p) {
   return v;
 }
 
-void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allow_hform) {
+void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allow_hform,
+                    cudaStream_t stream) {
+  const cudaStream_t st = stream ? stream : p.st;
   const int n = p.n;
   Bufs& b = p.bufs();
   m.dc = dc;
@@ -531,7 +535,7 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allo
       GemmShape s = make_shape(r1 - r0, n, n, p.R + (long)r0 * n, n, dc.P, n);
       s.kb_m = 1;
       s.kstart = r0;
-      gemm_launch<false, false>(s, EpiAxpby{b.Bm + (long)r0 * n, n, 1.0, 0.0}, p.st);
+      gemm_launch<false, false>(s, EpiAxpby{b.Bm + (long)r0 * n, n, 1.0, 0.0}, st);
     }
   }
   if (m.hform) {
@@ -540,7 +544,7 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allo
     const int k = dc.k, ks = m.pos ? k : n - k, ns = n - ks;
     const int ksp = ks + (ks & 1), nsp = ns + (ns & 1);
     m.ldp = ksp + nsp;
-    pack_blocks_kernel<<<ew_grid((long)n * m.ldp), 256, 0, p.st>>>(b.Bm, n, k, m.pos ? 1 : 0, ksp, m.ldp, b.Bp);
+    pack_blocks_kernel<<<ew_grid((long)n * m.ldp), 256, 0, st>>>(b.Bm, n, k, m.pos ? 1 : 0, ksp, m.ldp, b.Bp);
     KOT_LAUNCH_CHECK();
     m.Bs = b.Bp;
     m.Bo = b.Bp + ksp;
@@ -548,12 +552,12 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allo
     // W∘(Bᵀdiag(v)B) is the constant 1/μ, so its share of Φ(𝒯[Φ*(v)])_i = Σ_j v_j (b_iα·b_jα)²/μ
     // is the GEMV (H v)/μ, and only the α×ᾱ block remains for the two GEMMs of every matvec.
     if (k == 0) {
-      KOT_CUDA(cudaMemsetAsync(m.H, 0, sizeof(double) * n * n, p.st));
+      KOT_CUDA(cudaMemsetAsync(m.H, 0, sizeof(double) * n * n, st));
     } else {
       const double* Ba = m.pos ? m.Bs : m.Bo;
       GemmShape s = make_shape(n, n, k, Ba, m.ldp, Ba, m.ldp);
       s.sym_tiles = 1;
-      gemm_launch<false, true>(s, EpiSquareMirror{m.H, n}, p.st);
+      gemm_launch<false, true>(s, EpiSquareMirror{m.H, n}, st);
     }
     return;
   }
@@ -564,7 +568,7 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allo
     s.kb_m = 1;
     s.kb_n = 1;
     s.sym_tiles = 1;
-    gemm_launch<false, true>(s, EpiSquareMirror{p.G2, n}, p.st);
+    gemm_launch<false, true>(s, EpiSquareMirror{p.G2, n}, st);
   }
 }
 

@@ -89,6 +89,7 @@ struct Problem {
   double *crit_dg = nullptr, *crit_dX = nullptr, *crit_e1 = nullptr;
   cudaEvent_t crit_done = nullptr, crit_after = nullptr, crit_dx_done = nullptr;
   cudaEvent_t ev_half = nullptr;  // eg_step_parallel: γ½ ready
+  cudaEvent_t ev_mv0 = nullptr, ev_mv1 = nullptr;  // newton_direction: matvec_prepare on the crit stream
   bool with_eig = true;
   double* alloc(long count);
   void init_scratch();
@@ -136,7 +137,9 @@ struct MvCtx {
   const double *Bs = nullptr, *Bo = nullptr;  // H form: packed smaller / other sign block of B
   long ldp = 0;
 };
-void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allow_hform = true);
+// stream (nullable): where B, its packed sign blocks and H are built (default p.st)
+void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allow_hform = true,
+                    cudaStream_t stream = nullptr);
 // shard.cu
 void nccl_unique_id(char* out128);
 void problem_shard(Problem& p, const char* id128, int rank, int world);
