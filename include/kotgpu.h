@@ -148,6 +148,13 @@ typedef struct {
 int kot_profile_enable(int on);  /* 0 off, 1 every scope, 2 roofline scopes only (cheap); resets the counters */
 int kot_profile_read(kot_prof_entry* out, int cap);  /* returns #entries */
 
+/* ---- test / diagnostic hooks (process-wide; not part of the drop-in surface) ---- */
+int kot_debug_eig_stages(int stages);   /* 0 automatic, 1 one-stage, 2 two-stage, 3 two-stage in background */
+int kot_debug_cg_batch(int batch);      /* CG iterations enqueued per host check (>= 1; default 4) */
+int kot_debug_eg_parallel(int on);      /* EG-step projections side by side (1, default) or in sequence */
+int kot_debug_sytrd_timing(int on, unsigned long long* out8);  /* panel-kernel segment timers (ns) */
+int kot_debug_tail_timing(int on, unsigned long long* out8);   /* cluster-tail segment timers (ns) */
+
 /* ---- operators (host buffers in/out; per-kernel parity) ----------------- */
 
 /* gram_matrix (kernels.py:61-73), square form: out = exp(-|a_i-a_j|^2/(2 bw)), unit diag. */
