@@ -77,6 +77,11 @@ _SIGS = {
     "kot_problem_shard_info": (C.c_int, [C.c_void_p, iptr, iptr, iptr, iptr]),
     "kot_profile_enable": (C.c_int, [C.c_int]),
     "kot_profile_read": (C.c_int, [C.POINTER(ProfEntryC), C.c_int]),
+    "kot_debug_eig_stages": (C.c_int, [C.c_int]),
+    "kot_debug_cg_batch": (C.c_int, [C.c_int]),
+    "kot_debug_eg_parallel": (C.c_int, [C.c_int]),
+    "kot_debug_sytrd_timing": (C.c_int, [C.c_int, C.POINTER(C.c_ulonglong)]),
+    "kot_debug_tail_timing": (C.c_int, [C.c_int, C.POINTER(C.c_ulonglong)]),
     "kot_gram": (C.c_int, [dptr, C.c_int, C.c_int, C.c_double, C.c_int, dptr]),
     "kot_cholesky_psd": (C.c_int, [dptr, C.c_int, C.c_int, dptr, dptr]),
     "kot_sym_eig": (C.c_int, [dptr, C.c_int, C.c_int, dptr, dptr, iptr]),
