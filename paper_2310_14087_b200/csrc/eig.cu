@@ -368,13 +368,30 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
     for (int s = threadIdx.x; s < m; s += blockDim.x) vsh[s] = (s == 0) ? 1.0 : vsh[s] * scale;
     __syncthreads();
     double pt1 = 0.0, pt2 = 0.0, pyv = 0.0;  // lane t accumulates t1_t, t2_t
-#pragma unroll
-    for (int q = 0; q < TRD_RPW; ++q) {
-      const int r = rbase + q * NW;
-      if (r <= c || r >= n) continue;
+    // per own row: V/W bookkeeping once its symv result y is known
+    auto finish_row = [&](int q, int r, double y) {
       const double vr = vsh[r - c - 1];
+      yreg[q] = y;
+      if (lane == jj) Vs[wid][q][jj] = vr;
+      if (lane == 0) {
+        if (r == c + 1) a.yv[r] = y;
+        V[(long)r * LDX + jj] = vr;
+        V2[(long)r * LDX + jj] = vr;
+        a.Vall[(long)r * n + c] = (tau == 0.0) ? 0.0 : vr;  // H = I: no reflector for the back-transform
+        pyv += y * vr;
+      }
+      if (lane < jj) {
+        pt1 += Ws[wid][q][lane] * vr;
+        pt2 += Vs[wid][q][lane] * vr;
+      }
+    };
+    // L2-latency bound: 16-byte loads, 16 in flight per lane — from one row, or 8 + 8 from two rows
+    // of the same warp (same length m and 16-byte phase s0 when n is even), so a warp with several
+    // rows needs half the dependent round trips
+    const bool pair_ok = (n & 1) == 0;
+    // one row's symv (16 loads in flight per lane)
+    auto symv_row = [&](int q, int r) {
       const double* Ar = a.A + (long)r * n + c + 1;
-      // L2-latency bound: 16-byte loads, 8 in flight per lane (16 doubles)
       double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       const int s0 = (int)((reinterpret_cast<uintptr_t>(Ar) >> 3) & 1);  // peel to 16 B alignment
       if (s0 && lane == 0 && m > 0) acc[0] = Ar[0] * vsh[0];
@@ -409,18 +426,66 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
       if (((m - s0) & 1) && lane == 0) acc[1] += Ar[m - 1] * vsh[m - 1];
       double y = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
       y = warp_sum(y);
-      yreg[q] = y;
-      if (lane == jj) Vs[wid][q][jj] = vr;
-      if (lane == 0) {
-        if (r == c + 1) a.yv[r] = y;
-        V[(long)r * LDX + jj] = vr;
-        V2[(long)r * LDX + jj] = vr;
-        a.Vall[(long)r * n + c] = (tau == 0.0) ? 0.0 : vr;  // H = I: no reflector for the back-transform
-        pyv += y * vr;
-      }
-      if (lane < jj) {
-        pt1 += Ws[wid][q][lane] * vr;
-        pt2 += Vs[wid][q][lane] * vr;
+      finish_row(q, r, y);
+    };
+    // two rows of this warp together (8 + 8 loads in flight per lane)
+    auto symv_pair = [&](int q, int r, int r1) {
+        const double* Ar0 = a.A + (long)r * n + c + 1;
+        const double* Ar1 = a.A + (long)r1 * n + c + 1;
+        double acc0[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        double acc1[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        const int s0 = (int)((reinterpret_cast<uintptr_t>(Ar0) >> 3) & 1);
+        if (s0 && lane == 0 && m > 0) {
+          acc0[0] = Ar0[0] * vsh[0];
+          acc1[0] = Ar1[0] * vsh[0];
+        }
+        const int m2 = (m - s0) >> 1;
+        const double2* A20 = reinterpret_cast<const double2*>(Ar0 + s0);
+        const double2* A21 = reinterpret_cast<const double2*>(Ar1 + s0);
+        const double* vb = vsh + s0;
+        int qq = lane;
+        for (; qq + 7 * 32 < m2; qq += 8 * 32) {
+          double2 av0[8], av1[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            av0[u] = __ldcg(A20 + qq + u * 32);
+            av1[u] = __ldcg(A21 + qq + u * 32);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int s = 2 * (qq + u * 32);
+            acc0[u] += av0[u].x * vb[s] + av0[u].y * vb[s + 1];
+            acc1[u] += av1[u].x * vb[s] + av1[u].y * vb[s + 1];
+          }
+        }
+        for (; qq < m2; qq += 32) {
+          const double2 a0 = A20[qq], a1 = A21[qq];
+          acc0[0] += a0.x * vb[2 * qq] + a0.y * vb[2 * qq + 1];
+          acc1[0] += a1.x * vb[2 * qq] + a1.y * vb[2 * qq + 1];
+        }
+        if (((m - s0) & 1) && lane == 0) {
+          acc0[1] += Ar0[m - 1] * vsh[m - 1];
+          acc1[1] += Ar1[m - 1] * vsh[m - 1];
+        }
+        double y0 = ((acc0[0] + acc0[1]) + (acc0[2] + acc0[3])) + ((acc0[4] + acc0[5]) + (acc0[6] + acc0[7]));
+        double y1 = ((acc1[0] + acc1[1]) + (acc1[2] + acc1[3])) + ((acc1[4] + acc1[5]) + (acc1[6] + acc1[7]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          y0 += __shfl_xor_sync(0xffffffffu, y0, o);
+          y1 += __shfl_xor_sync(0xffffffffu, y1, o);
+        }
+        finish_row(q, r, y0);
+        finish_row(q + 1, r1, y1);
+    };
+#pragma unroll
+    for (int q = 0; q < TRD_RPW; q += 2) {
+      const int r = rbase + q * NW, r1 = r + NW;
+      const bool v0 = r > c && r < n, v1 = r1 > c && r1 < n;
+      if (v0 && v1 && pair_ok) {
+        symv_pair(q, r, r1);
+      } else {
+        if (v0) symv_row(q, r);
+        if (v1) symv_row(q + 1, r1);
       }
     }
     sred[wid][lane] = pt1;
