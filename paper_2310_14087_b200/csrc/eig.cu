@@ -553,8 +553,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) sytrd_tail_kernel(TailArgs a)
   const int nrows = (m0 - g + TAIL_CL - 1) / TAIL_CL;  // own rows r = g + 16 q, q < nrows
   const int ld = m0 + (m0 & 1);
   double* Aloc = tsm;                               // nrows × ld
-  double* vfull = Aloc + (long)TAIL_RPC * ld;       // m0
-  double* wfull = vfull + ld;                       // m0 (y, then w)
+  double* vwbuf = Aloc + (long)TAIL_RPC * ld;       // by column parity: [v | w], 2 × 2 × ld
   __shared__ double pub_x[TAIL_RPC];                // own rows' column entries (read by the cluster)
   __shared__ double pub_y[TAIL_RPC];                // own rows' symv results
   __shared__ double pub_n;                          // own partial Σ x_r², r ≥ c+2
@@ -578,12 +577,22 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) sytrd_tail_kernel(TailArgs a)
     tseg[i] += t_ - tl;                     \
     tl = t_;                                \
   }
+  // The rank-2 update of column c, A_rs −= v_r w_s + w_r v_s (r, s > c), is deferred into column c+1:
+  // column c+1 is published with it applied on the fly, and the rest is applied inside column c+1's
+  // symv pass (one read + one write of the own rows per column instead of a symv read plus a separate
+  // read-modify-write).  Same expressions, same order: bit-identical to the undeferred update.
+  bool pend = false;  // column c−1's update is still to be applied (uniform over the cluster)
   for (int c = 0; c + 1 < m0; ++c) {
-    // (A) publish own entries of column c below the diagonal and the partial norm
+    double* vn = vwbuf + (c & 1) * 2L * ld;  // v of column c, then its w
+    double* wn = vn + ld;
+    const double* vp = vwbuf + ((c + 1) & 1) * 2L * ld;  // column c−1's
+    const double* wp = vp + ld;
+    // (A) publish own entries of column c below the diagonal (pending update applied) and the partial norm
     double pn = 0.0;
     for (int q = tid; q < nrows; q += TAIL_THREADS) {
       const int r = g + TAIL_CL * q;
-      const double x = Aloc[(long)q * ld + c];
+      double x = Aloc[(long)q * ld + c];
+      if (pend && r >= c) x = x - vp[r] * wp[c] - wp[r] * vp[c];
       pub_x[q] = x;
       if (r >= c + 2) pn += x * x;
       if (r == c) a.d[c0 + c] = x;
@@ -627,37 +636,81 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) sytrd_tail_kernel(TailArgs a)
 #pragma unroll
     for (int u = 0; u < XPT; ++u) {
       const int r = c + 1 + tid + u * TAIL_THREADS;
-      if (r < m0) vfull[r] = (r == c + 1) ? 1.0 : xr[u] * scale;
+      if (r < m0) vn[r] = (r == c + 1) ? 1.0 : xr[u] * scale;
     }
     __syncthreads();
     TAIL_MARK(2)
     for (int q = tid; q < nrows; q += TAIL_THREADS) {
       const int r = g + TAIL_CL * q;
-      if (r > c) a.Vall[(long)(c0 + r) * n + c0 + c] = (tau == 0.0) ? 0.0 : vfull[r];
+      if (r > c) a.Vall[(long)(c0 + r) * n + c0 + c] = (tau == 0.0) ? 0.0 : vn[r];
     }
     TAIL_MARK(3)
-    if (tau == 0.0) {
+    if (tau == 0.0) {  // H = I: no symv and no new update; apply the pending one on its own
+      if (pend) {
+        for (int q = wid; q < nrows; q += TAIL_THREADS / 32) {
+          const int r = g + TAIL_CL * q;
+          if (r <= c) continue;
+          double* Ar = Aloc + (long)q * ld;
+          const double vr = vp[r], wr = wp[r];
+          for (int s = c + 1 + lane; s < m0; s += 32) Ar[s] = Ar[s] - vr * wp[s] - wr * vp[s];
+        }
+      }
+      pend = false;
+      __syncthreads();
       cl.sync();  // keep the two-barrier rhythm (pub_x is rewritten next column)
       continue;
     }
-    // (C) y_r = Σ_{s>c} A_rs v_s for own rows r > c (two rows per warp pass, lane-strided fixed order)
+    // (C) pending update fused with y_r = Σ_{s>c} A_rs v_s for own rows r > c (two rows per warp
+    // pass, lane-strided fixed order)
     for (int q0 = wid; q0 < nrows; q0 += 2 * (TAIL_THREADS / 32)) {
       const int q1 = q0 + TAIL_THREADS / 32;
       const bool h0 = g + TAIL_CL * q0 > c, h1 = q1 < nrows && g + TAIL_CL * q1 > c;
-      const double* A0 = Aloc + (long)q0 * ld;
-      const double* A1 = Aloc + (long)(h1 ? q1 : q0) * ld;
+      if (!h0 && !h1) continue;
+      double* A0 = Aloc + (long)q0 * ld;
+      double* A1 = Aloc + (long)(h1 ? q1 : q0) * ld;
       double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
       int s = c + 1 + lane;
-      for (; s + 32 < m0; s += 64) {
-        const double v0 = vfull[s], v1 = vfull[s + 32];
-        a0 += A0[s] * v0;
-        a1 += A0[s + 32] * v1;
-        b0 += A1[s] * v0;
-        b1 += A1[s + 32] * v1;
-      }
-      if (s < m0) {
-        a0 += A0[s] * vfull[s];
-        b0 += A1[s] * vfull[s];
+      if (pend) {
+        const int r0 = g + TAIL_CL * q0, r1 = h1 ? g + TAIL_CL * q1 : r0;
+        const double v0r = vp[r0], w0r = wp[r0], v1r = vp[r1], w1r = wp[r1];
+        for (; s + 32 < m0; s += 64) {
+          const double ws0 = wp[s], ws1 = wp[s + 32], us0 = vp[s], us1 = vp[s + 32];
+          const double e00 = A0[s] - v0r * ws0 - w0r * us0, e01 = A0[s + 32] - v0r * ws1 - w0r * us1;
+          const double e10 = A1[s] - v1r * ws0 - w1r * us0, e11 = A1[s + 32] - v1r * ws1 - w1r * us1;
+          if (h0) {
+            A0[s] = e00;
+            A0[s + 32] = e01;
+          }
+          if (h1) {
+            A1[s] = e10;
+            A1[s + 32] = e11;
+          }
+          const double x0 = vn[s], x1 = vn[s + 32];
+          a0 += e00 * x0;
+          a1 += e01 * x1;
+          b0 += e10 * x0;
+          b1 += e11 * x1;
+        }
+        if (s < m0) {
+          const double e0 = A0[s] - v0r * wp[s] - w0r * vp[s];
+          const double e1 = A1[s] - v1r * wp[s] - w1r * vp[s];
+          if (h0) A0[s] = e0;
+          if (h1) A1[s] = e1;
+          a0 += e0 * vn[s];
+          b0 += e1 * vn[s];
+        }
+      } else {
+        for (; s + 32 < m0; s += 64) {
+          const double v0 = vn[s], v1 = vn[s + 32];
+          a0 += A0[s] * v0;
+          a1 += A0[s + 32] * v1;
+          b0 += A1[s] * v0;
+          b1 += A1[s + 32] * v1;
+        }
+        if (s < m0) {
+          a0 += A0[s] * vn[s];
+          b0 += A1[s] * vn[s];
+        }
       }
       double t0 = a0 + a1, t1 = b0 + b1;
 #pragma unroll
@@ -684,40 +737,32 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) sytrd_tail_kernel(TailArgs a)
 #pragma unroll
     for (int u = 0; u < XPT; ++u) {
       const int r = c + 1 + tid + u * TAIL_THREADS;
-      if (r < m0) pyv += yr[u] * vfull[r];
+      if (r < m0) pyv += yr[u] * vn[r];
     }
     const double yv = tail_block_sum(pyv, red);
     const double alpha2 = -0.5 * tau * (tau * yv);
 #pragma unroll
     for (int u = 0; u < XPT; ++u) {
       const int r = c + 1 + tid + u * TAIL_THREADS;
-      if (r < m0) wfull[r] = tau * yr[u] + alpha2 * vfull[r];
+      if (r < m0) wn[r] = tau * yr[u] + alpha2 * vn[r];
     }
+    pend = true;
     __syncthreads();
     TAIL_MARK(6)
-    // (E) A_rs −= v_r w_s + w_r v_s on own rows r > c, columns s > c
-    for (int q = wid; q < nrows; q += TAIL_THREADS / 32) {
-      const int r = g + TAIL_CL * q;
-      if (r <= c) continue;
-      double* Ar = Aloc + (long)q * ld;
-      const double vr = vfull[r], wr = wfull[r];
-      int s = c + 1 + lane;
-      for (; s + 96 < m0; s += 128) {
-        double t[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) t[u] = Ar[s + 32 * u] - vr * wfull[s + 32 * u] - wr * vfull[s + 32 * u];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) Ar[s + 32 * u] = t[u];
-      }
-      for (; s < m0; s += 32) Ar[s] = Ar[s] - vr * wfull[s] - wr * vfull[s];
-    }
-    __syncthreads();
-    TAIL_MARK(7)
   }
   if (timing)
     for (int i = 0; i < 8; ++i) a.dbg[i] += tseg[i];
 #undef TAIL_MARK
-  if (g == (m0 - 1) % TAIL_CL && tid == 0) a.d[n - 1] = Aloc[(long)((m0 - 1) / TAIL_CL) * ld + m0 - 1];
+  if (g == (m0 - 1) % TAIL_CL && tid == 0) {
+    const int r = m0 - 1;
+    double x = Aloc[(long)((m0 - 1) / TAIL_CL) * ld + r];
+    if (pend && m0 >= 2) {  // the last column's update (c = m0 − 2) on the last diagonal entry
+      const double* vp = vwbuf + ((m0 - 2) & 1) * 2L * ld;
+      const double* wp = vp + ld;
+      x = x - vp[r] * wp[r] - wp[r] * vp[r];
+    }
+    a.d[n - 1] = x;
+  }
   cl.sync();  // no CTA leaves while its shared memory may still be read
 }
 
@@ -810,7 +855,7 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
   }
   if (c0 < n) {
     const int m0 = n - c0;
-    const size_t smem = sizeof(double) * ((size_t)TAIL_RPC * (m0 + 1) + 2L * (m0 + 1));
+    const size_t smem = sizeof(double) * ((size_t)TAIL_RPC * (m0 + 1) + 4L * (m0 + 1));
     ensure_smem_attr((const void*)sytrd_tail_kernel, (int)smem, true);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(TAIL_CL);
