@@ -520,6 +520,7 @@ constexpr int TAIL_CL = 16;
 constexpr int TAIL_THREADS = 512;
 constexpr int TAIL_MAX = 640;                   // rows per CTA ≤ 40: 40 × 640 × 8 B = 200 KB of smem
 constexpr int TAIL_RPC = TAIL_MAX / TAIL_CL;    // 40
+static_assert(TAIL_RPC <= 3 * (TAIL_THREADS / 32), "tail_rows_pass takes at most 3 rows per warp");
 
 struct TailArgs {
   const double* A;  // n × n (ld n), trailing block at (c0, c0) fully updated and symmetric
@@ -543,6 +544,76 @@ __device__ __forceinline__ double tail_block_sum(double v, double* sh) {
 #pragma unroll
   for (int w = 0; w < TAIL_THREADS / 32; ++w) t += sh[w];
   return t;
+}
+
+// R own rows of one warp (R warp-uniform): the pending rank-2 update applied in place (if pend) fused
+// with y_r = Σ_{s>c} A_rs v_s.  Per row: lane-strided, two interleaved partial sums, butterfly — the
+// same arithmetic whichever warp or R a row lands in.
+template <int R>
+__device__ __forceinline__ void tail_rows_pass(double* Aloc, int ld, int q0, int g, int c, int m0, bool pend,
+                                               const double* vp, const double* wp, const double* vn,
+                                               double* pub_y, int lane) {
+  double* A[R];
+  double vr[R], wr[R], a0[R], a1[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int q = q0 + j * (TAIL_THREADS / 32);
+    const int r = g + TAIL_CL * q;
+    A[j] = Aloc + (long)q * ld;
+    vr[j] = pend ? vp[r] : 0.0;
+    wr[j] = pend ? wp[r] : 0.0;
+    a0[j] = 0.0;
+    a1[j] = 0.0;
+  }
+  int s = c + 1 + lane;
+  if (pend) {
+    for (; s + 32 < m0; s += 64) {
+      const double ws0 = wp[s], ws1 = wp[s + 32], us0 = vp[s], us1 = vp[s + 32];
+      const double x0 = vn[s], x1 = vn[s + 32];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const double e0 = A[j][s] - vr[j] * ws0 - wr[j] * us0;
+        const double e1 = A[j][s + 32] - vr[j] * ws1 - wr[j] * us1;
+        A[j][s] = e0;
+        A[j][s + 32] = e1;
+        a0[j] += e0 * x0;
+        a1[j] += e1 * x1;
+      }
+    }
+    if (s < m0) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const double e = A[j][s] - vr[j] * wp[s] - wr[j] * vp[s];
+        A[j][s] = e;
+        a0[j] += e * vn[s];
+      }
+    }
+  } else {
+    for (; s + 32 < m0; s += 64) {
+      const double x0 = vn[s], x1 = vn[s + 32];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        a0[j] += A[j][s] * x0;
+        a1[j] += A[j][s + 32] * x1;
+      }
+    }
+    if (s < m0) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) a0[j] += A[j][s] * vn[s];
+    }
+  }
+  double t[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) t[j] = a0[j] + a1[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) t[j] += __shfl_xor_sync(0xffffffffu, t[j], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) pub_y[q0 + j * (TAIL_THREADS / 32)] = t[j];
+  }
 }
 
 __global__ void __launch_bounds__(TAIL_THREADS, 1) sytrd_tail_kernel(TailArgs a) {
@@ -660,68 +731,18 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) sytrd_tail_kernel(TailArgs a)
       cl.sync();  // keep the two-barrier rhythm (pub_x is rewritten next column)
       continue;
     }
-    // (C) pending update fused with y_r = Σ_{s>c} A_rs v_s for own rows r > c (two rows per warp
-    // pass, lane-strided fixed order)
-    for (int q0 = wid; q0 < nrows; q0 += 2 * (TAIL_THREADS / 32)) {
-      const int q1 = q0 + TAIL_THREADS / 32;
-      const bool h0 = g + TAIL_CL * q0 > c, h1 = q1 < nrows && g + TAIL_CL * q1 > c;
-      if (!h0 && !h1) continue;
-      double* A0 = Aloc + (long)q0 * ld;
-      double* A1 = Aloc + (long)(h1 ? q1 : q0) * ld;
-      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-      int s = c + 1 + lane;
-      if (pend) {
-        const int r0 = g + TAIL_CL * q0, r1 = h1 ? g + TAIL_CL * q1 : r0;
-        const double v0r = vp[r0], w0r = wp[r0], v1r = vp[r1], w1r = wp[r1];
-        for (; s + 32 < m0; s += 64) {
-          const double ws0 = wp[s], ws1 = wp[s + 32], us0 = vp[s], us1 = vp[s + 32];
-          const double e00 = A0[s] - v0r * ws0 - w0r * us0, e01 = A0[s + 32] - v0r * ws1 - w0r * us1;
-          const double e10 = A1[s] - v1r * ws0 - w1r * us0, e11 = A1[s + 32] - v1r * ws1 - w1r * us1;
-          if (h0) {
-            A0[s] = e00;
-            A0[s + 32] = e01;
-          }
-          if (h1) {
-            A1[s] = e10;
-            A1[s + 32] = e11;
-          }
-          const double x0 = vn[s], x1 = vn[s + 32];
-          a0 += e00 * x0;
-          a1 += e01 * x1;
-          b0 += e10 * x0;
-          b1 += e11 * x1;
-        }
-        if (s < m0) {
-          const double e0 = A0[s] - v0r * wp[s] - w0r * vp[s];
-          const double e1 = A1[s] - v1r * wp[s] - w1r * vp[s];
-          if (h0) A0[s] = e0;
-          if (h1) A1[s] = e1;
-          a0 += e0 * vn[s];
-          b0 += e1 * vn[s];
-        }
-      } else {
-        for (; s + 32 < m0; s += 64) {
-          const double v0 = vn[s], v1 = vn[s + 32];
-          a0 += A0[s] * v0;
-          a1 += A0[s + 32] * v1;
-          b0 += A1[s] * v0;
-          b1 += A1[s + 32] * v1;
-        }
-        if (s < m0) {
-          a0 += A0[s] * vn[s];
-          b0 += A1[s] * vn[s];
-        }
-      }
-      double t0 = a0 + a1, t1 = b0 + b1;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        t0 += __shfl_xor_sync(0xffffffffu, t0, o);
-        t1 += __shfl_xor_sync(0xffffffffu, t1, o);
-      }
-      if (lane == 0) {
-        if (h0) pub_y[q0] = t0;
-        if (h1) pub_y[q1] = t1;
-      }
+    // (C) pending update fused with y_r = Σ_{s>c} A_rs v_s for own rows r > c: the live rows
+    // q ≥ qlo spread over the warps (warp w: qlo + w + 16 j), one pass of up to 3 rows per warp
+    {
+      const int qlo = (c + 1 - g + TAIL_CL - 1) / TAIL_CL > 0 ? (c + 1 - g + TAIL_CL - 1) / TAIL_CL : 0;
+      const int q0 = qlo + wid;
+      const int nr = q0 < nrows ? (nrows - q0 + TAIL_THREADS / 32 - 1) / (TAIL_THREADS / 32) : 0;
+      if (nr == 1)
+        tail_rows_pass<1>(Aloc, ld, q0, g, c, m0, pend, vp, wp, vn, pub_y, lane);
+      else if (nr == 2)
+        tail_rows_pass<2>(Aloc, ld, q0, g, c, m0, pend, vp, wp, vn, pub_y, lane);
+      else if (nr >= 3)
+        tail_rows_pass<3>(Aloc, ld, q0, g, c, m0, pend, vp, wp, vn, pub_y, lane);
     }
     TAIL_MARK(4)
     cl.sync();
