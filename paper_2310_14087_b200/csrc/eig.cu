@@ -550,9 +550,10 @@ __device__ __forceinline__ double tail_block_sum(double v, double* sh) {
 // with y_r = Σ_{s>c} A_rs v_s.  Per row: lane-strided, two interleaved partial sums, butterfly — the
 // same arithmetic whichever warp or R a row lands in.
 template <int R>
-__device__ __forceinline__ void tail_rows_pass(double* Aloc, int ld, int q0, int g, int c, int m0, bool pend,
+__device__ __forceinline__ void tail_rows_pass(double* Aloc, int ld, int q0, int c, int m0, bool pend,
                                                const double* vp, const double* wp, const double* vn,
-                                               double* pub_y, int lane) {
+                                               double* yslot, int g, int lane) {
+  cg::cluster_group cl = cg::this_cluster();
   double* A[R];
   double vr[R], wr[R], a0[R], a1[R];
 #pragma unroll
@@ -610,9 +611,10 @@ __device__ __forceinline__ void tail_rows_pass(double* Aloc, int ld, int q0, int
 #pragma unroll
     for (int j = 0; j < R; ++j) t[j] += __shfl_xor_sync(0xffffffffu, t[j], o);
   }
-  if (lane == 0) {
+  // (the butterfly leaves the same bits in every lane) lane k < 16 pushes y_r into CTA k's slot
+  if (lane < TAIL_CL) {
 #pragma unroll
-    for (int j = 0; j < R; ++j) pub_y[q0 + j * (TAIL_THREADS / 32)] = t[j];
+    for (int j = 0; j < R; ++j) cl.map_shared_rank(yslot, lane)[g + TAIL_CL * (q0 + j * (TAIL_THREADS / 32))] = t[j];
   }
 }
 
@@ -625,9 +627,12 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) sytrd_tail_kernel(TailArgs a)
   const int ld = m0 + (m0 & 1);
   double* Aloc = tsm;                               // nrows × ld
   double* vwbuf = Aloc + (long)TAIL_RPC * ld;       // by column parity: [v | w], 2 × 2 × ld
-  __shared__ double pub_x[TAIL_RPC];                // own rows' column entries (read by the cluster)
-  __shared__ double pub_y[TAIL_RPC];                // own rows' symv results
-  __shared__ double pub_n;                          // own partial Σ x_r², r ≥ c+2
+  // Push model: every CTA stores its rows' column entries, partial norm and symv results straight into
+  // every CTA's shared memory (remote stores before the cluster barrier), so each consumer reads them
+  // locally after it: x_r lands in v's slot of the column (scaled in place), y_r in w's slot, the
+  // partial norms in nfull[rank].  The slots are dead when written: the column's v / w buffers last
+  // held column c−2's, and every CTA is past the barrier that ends their last use.
+  __shared__ double nfull[TAIL_CL];
   __shared__ double red[TAIL_THREADS / 32];
   __shared__ double scal[3];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -664,27 +669,30 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) sytrd_tail_kernel(TailArgs a)
       const int r = g + TAIL_CL * q;
       double x = Aloc[(long)q * ld + c];
       if (pend && r >= c) x = x - vp[r] * wp[c] - wp[r] * vp[c];
-      pub_x[q] = x;
+      if (r > c) {
+#pragma unroll
+        for (int k = 0; k < TAIL_CL; ++k) cl.map_shared_rank(vn, k)[r] = x;
+      }
       if (r >= c + 2) pn += x * x;
       if (r == c) a.d[c0 + c] = x;
     }
     pn = tail_block_sum(pn, red);
-    if (tid == 0) pub_n = pn;
+    if (tid < TAIL_CL) cl.map_shared_rank(nfull, tid)[g] = pn;
     TAIL_MARK(0)
     cl.sync();
     TAIL_MARK(1)
-    // (B) gather the column (registers first: one DSMEM round trip), Householder scalars (dlarfg)
-    // identically in every CTA, then v = x·scale with v_{c+1} = 1
+    // (B) the column is local now (pushed into vn), Householder scalars (dlarfg) identically in every
+    // CTA, then v = x·scale in place with v_{c+1} = 1
     constexpr int XPT = (TAIL_MAX + TAIL_THREADS - 1) / TAIL_THREADS;
     double xr[XPT];
 #pragma unroll
     for (int u = 0; u < XPT; ++u) {
       const int r = c + 1 + tid + u * TAIL_THREADS;
-      xr[u] = (r < m0) ? cl.map_shared_rank(pub_x, r % TAIL_CL)[r / TAIL_CL] : 0.0;
+      xr[u] = (r < m0) ? vn[r] : 0.0;
     }
-    const double alpha = cl.map_shared_rank(pub_x, (c + 1) % TAIL_CL)[(c + 1) / TAIL_CL];
+    const double alpha = vn[c + 1];  // read by every thread before the barrier below
     if (wid == 0) {
-      double t = (lane < TAIL_CL) ? *cl.map_shared_rank(&pub_n, lane) : 0.0;
+      double t = (lane < TAIL_CL) ? nfull[lane] : 0.0;
       t = warp_sum(t);  // fixed order over the 16 ranks
       if (lane == 0) scal[0] = t;
     }
@@ -728,7 +736,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) sytrd_tail_kernel(TailArgs a)
       }
       pend = false;
       __syncthreads();
-      cl.sync();  // keep the two-barrier rhythm (pub_x is rewritten next column)
+      cl.sync();  // keep the two-barrier rhythm
       continue;
     }
     // (C) pending update fused with y_r = Σ_{s>c} A_rs v_s for own rows r > c: the live rows
@@ -738,11 +746,11 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) sytrd_tail_kernel(TailArgs a)
       const int q0 = qlo + wid;
       const int nr = q0 < nrows ? (nrows - q0 + TAIL_THREADS / 32 - 1) / (TAIL_THREADS / 32) : 0;
       if (nr == 1)
-        tail_rows_pass<1>(Aloc, ld, q0, g, c, m0, pend, vp, wp, vn, pub_y, lane);
+        tail_rows_pass<1>(Aloc, ld, q0, c, m0, pend, vp, wp, vn, wn, g, lane);
       else if (nr == 2)
-        tail_rows_pass<2>(Aloc, ld, q0, g, c, m0, pend, vp, wp, vn, pub_y, lane);
+        tail_rows_pass<2>(Aloc, ld, q0, c, m0, pend, vp, wp, vn, wn, g, lane);
       else if (nr >= 3)
-        tail_rows_pass<3>(Aloc, ld, q0, g, c, m0, pend, vp, wp, vn, pub_y, lane);
+        tail_rows_pass<3>(Aloc, ld, q0, c, m0, pend, vp, wp, vn, wn, g, lane);
     }
     TAIL_MARK(4)
     cl.sync();
@@ -753,7 +761,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) sytrd_tail_kernel(TailArgs a)
 #pragma unroll
     for (int u = 0; u < XPT; ++u) {
       const int r = c + 1 + tid + u * TAIL_THREADS;
-      yr[u] = (r < m0) ? cl.map_shared_rank(pub_y, r % TAIL_CL)[r / TAIL_CL] : 0.0;
+      yr[u] = (r < m0) ? wn[r] : 0.0;  // pushed by the row's owner
     }
 #pragma unroll
     for (int u = 0; u < XPT; ++u) {
