@@ -28,7 +28,9 @@ enum {
   KOT_ENUMERICS = 4,    /* SolverNumericsError        solver.py:28-33 (partial trace returned) */
   KOT_ECG = 5,          /* FloatingPointError         linalg.py:146,156 */
   KOT_ECUDA = 6,        /* CUDA runtime failure */
-  KOT_EASSERT = 7       /* AssertionError             psdcone.py:77 */
+  KOT_EASSERT = 7,      /* AssertionError             psdcone.py:77 */
+  KOT_ECALLBACK = 8     /* the on_iteration callback returned nonzero (solver.py:170-181: an observer
+                           exception propagates and ends the solve) */
 };
 
 typedef struct kot_problem kot_problem;
@@ -64,8 +66,9 @@ typedef struct {
   double total_ms;
 } kot_report;
 
-/* on_iteration observer (solver.py:76-86, 170-181); host copies of w, r, dw. */
-typedef void (*kot_iter_cb)(void* user, int iteration, const double* w_gamma, const double* w_x,
+/* on_iteration observer (solver.py:76-86, 170-181); host copies of w, r, dw.  A nonzero return
+ * stops the solve with KOT_ECALLBACK (the Python shim re-raises the observer's exception). */
+typedef int (*kot_iter_cb)(void* user, int iteration, const double* w_gamma, const double* w_x,
                             const double* r_gamma, const double* r_x, double mu, double theta,
                             const double* dw_gamma, const double* dw_x, int criterion_met);
 
@@ -135,6 +138,13 @@ void* kot_problem_stream(kot_problem* p);
  * NCCL (libnccl.so.2) is dlopen'ed on first use. */
 int kot_nccl_unique_id(char* out128);
 int kot_problem_shard(kot_problem* p, const char* id128, int rank, int world);
+/* Same row sharding over a caller-supplied host data plane (gloo, MPI, …) instead of NCCL: the
+ * library stages the exchanged device buffers through pinned host memory and calls fn on the thread
+ * that called kot_solve.  op 0: in-place sum over ranks of `count` doubles; op 1: in-place
+ * all-gather, rank g's `block` doubles at buf + g·block (count = block·world).  fn returns 0 on
+ * success.  Used where ranks share a GPU (tests) or NCCL is unavailable. */
+typedef int (*kot_comm_fn)(void* user, int op, double* buf, long count, long block, int rank, int world);
+int kot_problem_shard_host(kot_problem* p, kot_comm_fn fn, void* user, int rank, int world);
 int kot_problem_shard_info(const kot_problem* p, int* rank, int* world, int* row0, int* row1);
 
 /* ---- phase profiler (CUDA events around library phases; off by default) --- */

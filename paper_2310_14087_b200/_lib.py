@@ -47,7 +47,9 @@ class ProfEntryC(C.Structure):
                 ("bytes", C.c_double)]
 
 
-IterCB = C.CFUNCTYPE(None, C.c_void_p, C.c_int, dptr, dptr, dptr, dptr, C.c_double, C.c_double, dptr, dptr,
+CommFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, dptr, C.c_long, C.c_long, C.c_int, C.c_int)
+
+IterCB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, dptr, dptr, dptr, dptr, C.c_double, C.c_double, dptr, dptr,
                      C.c_int)
 
 # name -> (restype, argtypes)
@@ -74,6 +76,7 @@ _SIGS = {
     "kot_problem_stream": (C.c_void_p, [C.c_void_p]),
     "kot_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "kot_problem_shard": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_int]),
+    "kot_problem_shard_host": (C.c_int, [C.c_void_p, CommFn, C.c_void_p, C.c_int, C.c_int]),
     "kot_problem_shard_info": (C.c_int, [C.c_void_p, iptr, iptr, iptr, iptr]),
     "kot_profile_enable": (C.c_int, [C.c_int]),
     "kot_profile_read": (C.c_int, [C.POINTER(ProfEntryC), C.c_int]),
@@ -150,6 +153,10 @@ class CudaError(RuntimeError):
     pass
 
 
+class CallbackError(RuntimeError):
+    """Status 8: the on_iteration callback failed (the shim re-raises the observer's own exception)."""
+
+
 def check(status: int, trace=None):
     if status == 0:
         return
@@ -166,6 +173,8 @@ def check(status: int, trace=None):
         raise FloatingPointError(msg)
     if status == 7:
         raise AssertionError(msg)
+    if status == 8:
+        raise CallbackError(msg)
     raise CudaError(msg)
 
 

@@ -118,18 +118,40 @@ def run_local(seeds: Sequence[int], solve_fn: Callable[[int], BatchResult], conc
     return [out[s] for s in seeds]
 
 
-def gather_to_root(results: list[BatchResult], l: int, world: int, rank: int, device=None  # noqa: E741
-                   ) -> list[BatchResult] | None:
-    """Gather fixed-size records to rank 0 (one all_gather of a padded [max_per_rank, HEADER+ℓ] block)."""
+def run_and_gather(seeds: Sequence[int], solve_fn: Callable[[int], BatchResult], concurrency: int, l: int,  # noqa: E741
+                   world: int, rank: int, device=None) -> list[BatchResult] | None:
+    """run_local on this rank's seeds, then gather_to_root — a local failure still joins the collective."""
+    res: list[BatchResult] = []
+    err: BaseException | None = None
+    try:
+        res = run_local(seeds, solve_fn, concurrency)
+    except Exception as e:  # noqa: BLE001 — re-raised on every rank by gather_to_root
+        err = e
+    return gather_to_root(res, l, world, rank, device=device, error=err)
+
+
+def gather_to_root(results: list[BatchResult], l: int, world: int, rank: int, device=None,  # noqa: E741
+                   error: BaseException | None = None) -> list[BatchResult] | None:
+    """Gather fixed-size records to rank 0 (one all_gather of a padded [max_per_rank, HEADER+ℓ] block).
+
+    Every rank takes part even when its own solves failed (``error``): the failure is all-reduced
+    first and then raised on every rank, so no rank is left waiting in the collective."""
     recs = np.stack([pack(r, l) for r in results]) if results else np.zeros((0, HEADER + l))
     if world == 1:
+        if error is not None:
+            raise error
         return [unpack(r) for r in recs]
     import torch
     import torch.distributed as dist
 
-    cnt = torch.tensor([recs.shape[0]], dtype=torch.int64, device=device)
-    dist.all_reduce(cnt, op=dist.ReduceOp.MAX)  # per-rank shard sizes differ by the σ-group dealing
-    per = max(int(cnt.item()), 1)
+    # [records on this rank, failed] — per-rank shard sizes differ by the σ-group dealing
+    cnt = torch.tensor([recs.shape[0], 1 if error is not None else 0], dtype=torch.int64, device=device)
+    dist.all_reduce(cnt, op=dist.ReduceOp.MAX)
+    if int(cnt[1].item()):
+        if error is not None:
+            raise error
+        raise RuntimeError("a batch member failed on another rank")
+    per = max(int(cnt[0].item()), 1)
     buf = np.full((per, HEADER + l), np.nan)
     buf[:recs.shape[0]] = recs
     t = torch.from_numpy(buf)

@@ -237,6 +237,15 @@ int kot_problem_shard(kot_problem* h, const char* id128, int rank, int world) {
   });
 }
 
+int kot_problem_shard_host(kot_problem* h, kot_comm_fn fn, void* user, int rank, int world) {
+  return guarded([&] {
+    if (world <= 1)
+      kot::problem_unshard(*h->p);
+    else
+      kot::problem_shard_host(*h->p, fn, user, rank, world);
+  });
+}
+
 int kot_problem_shard_info(const kot_problem* h, int* rank, int* world, int* row0, int* row1) {
   return guarded([&] {
     const kot::Problem& p = *h->p;

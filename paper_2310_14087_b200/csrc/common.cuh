@@ -20,6 +20,7 @@ enum Status : int {
   KOT_ECG = 5,           // FloatingPointError in CG (linalg.py:146,156)
   KOT_ECUDA = 6,
   KOT_EASSERT = 7,       // AssertionError (psdcone.py:77)
+  KOT_ECALLBACK = 8,     // the on_iteration observer raised (solver.py:170-181: propagates, ends the solve)
 };
 
 struct KotError : public std::runtime_error {

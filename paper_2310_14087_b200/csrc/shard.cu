@@ -79,11 +79,44 @@ void problem_shard_emulate(Problem& p, int world) {
   if (world > 1 && !p.shard_tmp) p.shard_tmp = p.alloc((long)(p.n / 2 + 1) * p.n);
 }
 
+// Host data plane: the caller supplies the two collectives on host buffers (op 0: in-place sum over
+// ranks of `count` doubles; op 1: in-place all-gather, rank g's `block` doubles at buf + g·block).
+// Same row blocks and arithmetic as the NCCL path; the device data is staged through pinned memory.
+void problem_shard_host(Problem& p, int (*fn)(void*, int, double*, long, long, int, int), void* user, int rank,
+                        int world) {
+  kot_require(fn != nullptr && world >= 1 && rank >= 0 && rank < world, KOT_EINVAL, "invalid rank/world");
+  problem_unshard(p);
+  p.host_comm = fn;
+  p.host_comm_user = user;
+  p.shard_rank = rank;
+  p.shard_world = world;
+  p.shard_block = (p.n + world - 1) / world;
+  p.row0 = std::min(p.n, rank * p.shard_block);
+  p.row1 = std::min(p.n, p.row0 + p.shard_block);
+  if (!p.ygather) p.ygather = p.alloc((long)p.shard_block * world);
+  const long cap = std::max((long)p.n * p.n, (long)p.shard_block * world);
+  if (p.host_comm_cap < cap) {
+    if (p.host_comm_buf) host_free_pinned(p.host_comm_buf, sizeof(double) * p.host_comm_cap);
+    p.host_comm_buf = static_cast<double*>(host_alloc_pinned(sizeof(double) * cap));
+    p.host_comm_cap = cap;
+  }
+}
+
+static void host_collective(Problem& p, int op, double* buf, long count, long block) {
+  KOT_CUDA(cudaMemcpyAsync(p.host_comm_buf, buf, sizeof(double) * count, cudaMemcpyDeviceToHost, p.st));
+  KOT_CUDA(cudaStreamSynchronize(p.st));
+  const int rc = p.host_comm(p.host_comm_user, op, p.host_comm_buf, count, block, p.shard_rank, p.shard_world);
+  kot_require(rc == 0, KOT_ECUDA, "host data-plane collective failed");
+  KOT_CUDA(cudaMemcpyAsync(buf, p.host_comm_buf, sizeof(double) * count, cudaMemcpyHostToDevice, p.st));
+}
+
 void problem_unshard(Problem& p) {
   if (p.nccl_comm) {
     nccl().CommDestroy((ncclComm_t)p.nccl_comm);
     p.nccl_comm = nullptr;
   }
+  p.host_comm = nullptr;
+  p.host_comm_user = nullptr;
   p.shard_world = 1;
   p.shard_rank = 0;
   p.emul_world = 1;
@@ -92,12 +125,14 @@ void problem_unshard(Problem& p) {
 }
 
 void shard_allreduce_sum(Problem& p, double* buf, long count) {
+  if (p.host_comm) return host_collective(p, 0, buf, count, 0);
   nccl_check(nccl().AllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, (ncclComm_t)p.nccl_comm, p.st),
              "ncclAllReduce");
 }
 
 // in place: rank g's block sits at buf + g·block; afterwards every rank holds all blocks
 void shard_allgather(Problem& p, double* buf, long block) {
+  if (p.host_comm) return host_collective(p, 1, buf, block * p.shard_world, block);
   nccl_check(nccl().AllGather(buf + (long)p.shard_rank * block, buf, (size_t)block, ncclDouble,
                               (ncclComm_t)p.nccl_comm, p.st),
              "ncclAllGather");

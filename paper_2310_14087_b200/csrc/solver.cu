@@ -304,7 +304,18 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
     out.cg_ms = ms_since(t0);
   };
   const std::function<bool()> abort_if_met = [&]() { return resolve(false) && pending_met; };
+  // Row-sharded problems: each CG matvec is a collective, so every rank must run the same number of
+  // them.  The speculative abort polls the criterion's completion (timing-dependent per rank), hence
+  // no speculation there: attempt a+1 starts only after attempt a's criterion is known (same result).
+  const bool may_speculate = !p.sharded();
   for (int att = 0; att <= cfg.cg_restarts; ++att) {
+    if (pending && !may_speculate) {
+      resolve(true);
+      if (pending_met) {
+        finish();
+        return out;
+      }
+    }
     const bool speculative = pending;
     CgOut c{0, 0.0};
     bool ran = false;
@@ -664,8 +675,9 @@ static bool loop_body(Problem& p, const SolverCfg& cfg, LoopState& s, int k, Ite
     KOT_CUDA(cudaMemcpyAsync(hp->dg.data(), b.dg, sizeof(double) * n, cudaMemcpyDeviceToHost, p.st));
     KOT_CUDA(cudaMemcpyAsync(hp->dx.data(), b.dX, sizeof(double) * nn, cudaMemcpyDeviceToHost, p.st));
     KOT_CUDA(cudaStreamSynchronize(p.st));
-    cb(user, k, hp->wg.data(), hp->wx.data(), hp->rg.data(), hp->rx.data(), mu, s.theta, hp->dg.data(),
-       hp->dx.data(), st.met);
+    if (cb(user, k, hp->wg.data(), hp->wx.data(), hp->rg.data(), hp->rx.data(), mu, s.theta, hp->dg.data(),
+           hp->dx.data(), st.met) != 0)
+      throw KotError(KOT_ECALLBACK, "on_iteration observer raised");
   }
   // damping update from the trial point, whether or not it is kept (solver.py:224-226)
   dev_reduce(p, b.r1t, b.dg, n, 0, false);

@@ -53,7 +53,7 @@ void Problem::init_scratch() {
 
 Problem::~Problem() {
   if (st) cudaStreamSynchronize(st);
-  if (nccl_comm) {
+  if (nccl_comm || host_comm) {
     try {
       problem_unshard(*this);
     } catch (...) {
@@ -72,6 +72,7 @@ Problem::~Problem() {
   eig.reset();
   for (double* p : owned) dev_free(p);
   host_free_pinned(hsc, 64 * sizeof(double));
+  if (host_comm_buf) host_free_pinned(host_comm_buf, sizeof(double) * host_comm_cap);
   dev_free(dk);
   host_free_pinned(hk, 16 * sizeof(int));
   if (st) cudaStreamDestroy(st);
@@ -87,7 +88,7 @@ constexpr int kPoolPerOrder = 2;
 
 void problem_release(std::unique_ptr<Problem> p) {
   if (!p) return;
-  if (p->nccl_comm != nullptr || p->emul_world > 1) return;  // destroyed (unique_ptr goes out of scope)
+  if (p->sharded() || p->emul_world > 1) return;  // destroyed (unique_ptr goes out of scope)
   for (Problem* c : {p.get(), p->aux_.get(), p->aux2_.get(), p->aux3_.get(), p->crit_.get()})
     if (c && c->st) KOT_CUDA(cudaStreamSynchronize(c->st));
   std::lock_guard<std::mutex> lk(g_pool_mu);
@@ -498,7 +499,7 @@ struct EpiSquareMirror {
 // block in turn under the single-device emulation hook (emul_world > 1), else [0, n).
 static std::vector<std::pair<int, int>> row_blocks(const Problem& p) {
   std::vector<std::pair<int, int>> v;
-  if (p.nccl_comm) {
+  if (p.sharded()) {
     v.emplace_back(p.row0, p.row1);
   } else if (p.emul_world > 1) {
     const int blk = (p.n + p.emul_world - 1) / p.emul_world;
@@ -528,7 +529,7 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allo
     const char* e = std::getenv("KOT_MATVEC");
     return e != nullptr && std::string(e) == "full";
   }();
-  m.hform = allow_hform && !full && p.nccl_comm == nullptr && p.emul_world <= 1;
+  m.hform = allow_hform && !full && !p.sharded() && p.emul_world <= 1;
   m.H = b.Hm;
   for (const auto& [r0, r1] : row_blocks(p)) {  // B = R P for the row blocks this process owns
     if (r1 > r0) {  // R upper triangular: the K range starts at the block's first row
@@ -636,7 +637,7 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
 void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* out, const double* skipf) {
   const int n = p.n, k = m.dc.k;
   const int ks = m.pos ? k : n - k;
-  const bool nccl = p.nccl_comm != nullptr;
+  const bool nccl = p.sharded();  // NCCL or the caller's host data plane
   const auto blocks = row_blocks(p);
   const double nn = n, own = nccl ? p.row1 - p.row0 : n;
   Bufs& b = p.bufs();

@@ -75,6 +75,12 @@ struct Problem {
   // which the EG safeguard chain runs concurrently with the Newton chain
   // row sharding of the CG matvec (config 4): NCCL communicator and this rank's row block
   void* nccl_comm = nullptr;
+  // host data plane (kot_problem_shard_host): the caller's collectives on host buffers (gloo, MPI…)
+  int (*host_comm)(void* user, int op, double* buf, long count, long block, int rank, int world) = nullptr;
+  void* host_comm_user = nullptr;
+  double* host_comm_buf = nullptr;  // pinned staging, max(k·ℓ, block·world) doubles
+  long host_comm_cap = 0;
+  bool sharded() const { return nccl_comm != nullptr || host_comm != nullptr; }
   int shard_rank = 0, shard_world = 1, shard_block = 0, row0 = 0, row1 = -1;
   double* ygather = nullptr;  // shard_block·world doubles
   int emul_world = 1;          // test hook: all row blocks in turn on one device, no NCCL
@@ -145,6 +151,8 @@ void nccl_unique_id(char* out128);
 void problem_shard(Problem& p, const char* id128, int rank, int world);
 void problem_unshard(Problem& p);
 void problem_shard_emulate(Problem& p, int world);
+void problem_shard_host(Problem& p, int (*fn)(void*, int, double*, long, long, int, int), void* user, int rank,
+                        int world);
 void shard_allreduce_sum(Problem& p, double* buf, long count);
 void shard_allgather(Problem& p, double* buf, long block);
 // skipf (nullable): every launch is a no-op once *skipf != 0 (batched CG, H form only)
@@ -182,7 +190,7 @@ double dev_norm(Problem& p, const double* x, long count);
 double dev_dot(Problem& p, const double* x, const double* y, long count);
 
 // ---- solver
-typedef void (*IterCallback)(void* user, int iteration, const double* w_gamma, const double* w_x,
+typedef int (*IterCallback)(void* user, int iteration, const double* w_gamma, const double* w_x,
                              const double* r_gamma, const double* r_x, double mu, double theta,
                              const double* dw_gamma, const double* dw_x, int criterion_met);
 struct SolveResult {

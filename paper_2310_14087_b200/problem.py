@@ -105,8 +105,24 @@ class ProblemData:
     spec_y: KernelSpec | None = None
     spec_xy: KernelSpec | None = None
     jitter: float = 0.0
-    _dev: DeviceProblem | None = field(default=None, repr=False)
-    _kmat: np.ndarray | None = field(default=None, repr=False)
+    # device-resident copy and pair Gram: never copied by dataclasses.replace (init=False), dropped
+    # whenever a field they were built from is reassigned (__setattr__ below)
+    _dev: DeviceProblem | None = field(default=None, init=False, repr=False, compare=False)
+    _kmat: np.ndarray | None = field(default=None, init=False, repr=False, compare=False)
+
+    # fields the uploaded instance is built from / the pair Gram depends on
+    _DEVICE_FIELDS = frozenset({"q_mat", "z", "q_sq", "chol_upper", "lambda1", "lambda2", "embed_sum", "jitter"})
+    _KMAT_FIELDS = frozenset({"filling", "spec_xy", "chol_upper"})
+
+    def __setattr__(self, name, value):
+        # Reassigning a data field invalidates the device copy (the reference ProblemData is a plain
+        # mutable dataclass).  Arrays are uploaded as they are at the first GPU call: mutate them in
+        # place only before that, or reassign the field (or call release_device()) afterwards.
+        if name in ProblemData._DEVICE_FIELDS and "_dev" in self.__dict__:
+            object.__setattr__(self, "_dev", None)
+        if name in ProblemData._KMAT_FIELDS and "_kmat" in self.__dict__:
+            object.__setattr__(self, "_kmat", None)
+        object.__setattr__(self, name, value)
 
     def __post_init__(self) -> None:
         self.q_mat = symmetrize(np.asarray(self.q_mat, dtype=float))

@@ -57,6 +57,52 @@ def shard_rows(pd, group=None, device: int | None = None) -> tuple[int, int]:
     return shard_info(pd)[2:]
 
 
+def host_collective(op: int, arr, block: int, rank: int, world: int, group=None) -> None:
+    """The host data plane of kot_problem_shard_host on a float64 host array, in place.
+
+    op 0: sum over the ranks of ``group``; op 1: all-gather of every rank's ``block`` values
+    (rank g's at ``arr[g·block:(g+1)·block]``)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(arr)  # shares memory (the library's pinned staging buffer)
+    if op == 0:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    elif op == 1:
+        parts = [torch.empty(block, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, t[rank * block:(rank + 1) * block].clone(), group=group)
+        t.copy_(torch.cat(parts))
+    else:
+        raise ValueError(f"unknown collective {op}")
+
+
+def shard_rows_host(pd, group=None, device: int | None = None) -> tuple[int, int]:
+    """Collective: the same row split as :func:`shard_rows`, with the two exchanges (sum of T̃,
+    gather of y) carried by ``group``'s own collectives on host tensors (e.g. a gloo group) instead of
+    NCCL — for ranks that share one GPU (tests) or hosts without NCCL.  Returns this rank's block."""
+    import numpy as np
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dp = pd.device_problem(device)
+    if world == 1:
+        _lib.check(_lib.lib().kot_problem_shard(dp.handle, None, 0, 1))
+        return 0, pd.n
+
+    def comm(_user, op, buf, count, block, rk, wd):
+        try:
+            host_collective(op, np.ctypeslib.as_array(buf, shape=(count,)), block, rk, wd, group)
+            return 0
+        except Exception:  # reported as a status by the library
+            return 1
+
+    cb = _lib.CommFn(comm)
+    dp._comm_cb = cb  # keep the trampoline alive as long as the device problem
+    _lib.check(_lib.lib().kot_problem_shard_host(dp.handle, cb, None, rank, world))
+    return shard_info(pd)[2:]
+
+
 def shard_info(pd) -> tuple[int, int, int, int]:
     """(rank, world, r0, r1) of the device problem."""
     v = [C.c_int() for _ in range(4)]

@@ -122,6 +122,7 @@ def _run(pd: ProblemData, cfg: SolverConfig, on_iteration, pure_eg: bool, want_x
                                           cfg.max_iter, C.byref(rep))
     else:
         cb = _lib.IterCB(0)
+        raised: list[BaseException] = []
         if on_iteration is not None:
             def _cb(user, k, wg, wx, rg, rx, mu, theta, dg, dx, met):
                 def vec(p):
@@ -130,11 +131,18 @@ def _run(pd: ProblemData, cfg: SolverConfig, on_iteration, pure_eg: bool, want_x
                 def mat(p):
                     return np.ctypeslib.as_array(p, shape=(n, n)).copy()
 
-                on_iteration(IterationProbe(k, IteratePair(vec(wg), mat(wx)), IteratePair(vec(rg), mat(rx)),
-                                            float(mu), float(theta), IteratePair(vec(dg), mat(dx)), bool(met)))
+                try:
+                    on_iteration(IterationProbe(k, IteratePair(vec(wg), mat(wx)), IteratePair(vec(rg), mat(rx)),
+                                                float(mu), float(theta), IteratePair(vec(dg), mat(dx)), bool(met)))
+                except BaseException as e:  # noqa: BLE001 — re-raised below, as the reference propagates it
+                    raised.append(e)
+                    return 1
+                return 0
             cb = _lib.IterCB(_cb)
         st = _lib.lib().kot_solve(dp.handle, C.byref(c), cb, None, _lib.ptr(gamma), _lib.ptr(x), trace,
                                   cfg.max_iter, C.byref(rep))
+        if raised:  # the observer's exception ends the solve (reference solver.py:170-181)
+            raise raised[0]
     recs = [_record(trace[i]) for i in range(min(rep.iterations, cfg.max_iter))]
     _lib.check(st, recs)
     for r in recs:

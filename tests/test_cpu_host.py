@@ -243,6 +243,79 @@ def test_multiprocess_gather_gloo():
         assert it == ref.iterations and np.array_equal(gam, ref.gamma_hat)
 
 
+def _failing_gather_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2310_14087_b200.batch import run_and_gather, shard
+
+    def solve(s):
+        if rank == 1:
+            raise FloatingPointError("member diverged")
+        return fake_result(s)
+    try:
+        run_and_gather(shard(list(range(11)), world, rank), solve, 2, 6, world, rank)
+        q.put((rank, "no error"))
+    except FloatingPointError as e:
+        q.put((rank, f"local: {e}"))
+    except RuntimeError as e:
+        q.put((rank, f"remote: {e}"))
+    dist.destroy_process_group()
+
+
+def test_multiprocess_gather_propagates_member_failure():
+    """a rank whose member solve raises still joins the collective, and every rank raises
+    (no rank is left blocked in all_gather)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_failing_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got[1] == "local: member diverged"
+    assert got[0].startswith("remote:")
+
+
+def _host_plane_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2310_14087_b200.rowshard import host_collective
+    a = np.arange(6, dtype=float) * (rank + 1)
+    host_collective(0, a, 0, rank, world)
+    g = np.full(3 * world, -1.0)
+    g[3 * rank:3 * rank + 3] = [10 * rank, 10 * rank + 1, 10 * rank + 2]
+    host_collective(1, g, 3, rank, world)
+    q.put((rank, a.tolist(), g.tolist()))
+    dist.destroy_process_group()
+
+
+def test_host_data_plane_collectives_gloo():
+    """kot_problem_shard_host's two collectives (sum of T̃, gather of y) over a gloo group, in place on
+    the library's staging buffer: identical on every rank."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_host_plane_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=120) for _ in range(3))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, a, g in got:
+        assert a == (np.arange(6) * 6.0).tolist()
+        assert g == [0, 1, 2, 10, 11, 12, 20, 21, 22]
+
+
 # ------------------------------------------------------ row sharding (config 4)
 
 def test_row_blocks_partition():
