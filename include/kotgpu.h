@@ -80,10 +80,11 @@ int kot_problem_create(const double* q, const double* z, double q_sq, const doub
                        double jitter, int device, kot_problem** out);
 
 /* assemble() on device (problem.py:135-169): Gaussian Grams, mean embeddings,
- * embedding norms, pair Gram K and its jittered Cholesky factor. */
+ * embedding norms, pair Gram K and its jittered Cholesky factor.  bw_x / bw_y / bw_xy are
+ * spec_x / spec_y / spec_xy.bandwidth_sq (equal under build_kernel_specs, problem.py:126-132). */
 int kot_assemble(const double* xs, int n_mu, const double* ys, int n_nu, const double* xt,
-                 const double* yt, int l, int d, double bandwidth_sq, double lambda1, double lambda2,
-                 int device, kot_problem** out);
+                 const double* yt, int l, int d, double bw_x, double bw_y, double bw_xy, double lambda1,
+                 double lambda2, int device, kot_problem** out);
 
 int kot_problem_info(const kot_problem* p, int* l, double* q_sq, double* jitter, double* lambda1,
                      double* lambda2, int* has_embed);
@@ -169,6 +170,14 @@ int kot_debug_tail_timing(int on, unsigned long long* out8);   /* cluster-tail s
 
 /* gram_matrix (kernels.py:61-73), square form: out = exp(-|a_i-a_j|^2/(2 bw)), unit diag. */
 int kot_gram(const double* pts, int n, int d, double bandwidth_sq, int device, double* out);
+/* gram_matrix (kernels.py:61-73), rectangular form: out[i][j] = exp(-|a_i-b_j|^2/(2 bw)), m × p. */
+int kot_gram_rect(const double* a, int m, const double* b, int p, int d, double bandwidth_sq, int device,
+                  double* out);
+/* mean_embedding (kernels.py:83-87): out[j] = mean_i k(s_i, q_j), the n × m Gram never stored. */
+int kot_mean_embedding(const double* samples, int n, const double* queries, int m, int d, double bandwidth_sq,
+                       int device, double* out);
+/* embedding_norm_sq (kernels.py:90-94): mean of the n × n sample Gram. */
+int kot_embedding_norm_sq(const double* samples, int n, int d, double bandwidth_sq, int device, double* out);
 /* cholesky_psd (linalg.py:91-114). */
 int kot_cholesky_psd(const double* k, int n, int device, double* r_upper, double* jitter);
 /* sym_eig (linalg.py:60-83): descending eigenvalues, eigvecs in columns, n_pos. */
@@ -179,11 +188,44 @@ int kot_proj_psd(const double* z, int n, int device, double* out);
  * mode 0: eliminator with mu; mode 1: projection Jacobian.  path: -1 auto, 0 POS, 1 NONPOS. */
 int kot_spectral_apply(const double* z, int n, int device, int mode, double mu, int path,
                        const double* s, double* out);
+/* The same operators at a GIVEN decomposition (eigvecs in columns, eigenvalues descending, the first
+ * n_pos strictly positive — a SpectralDecomp): mode 0 apply_eliminator(make_eliminator(coeffs, mu), s)
+ * (psdcone.py:103-151), 1 apply_proj_jacobian(coeffs, s) (:94-100), 2 proj_from_decomp (:52-59; s unused). */
+int kot_spectral_apply_decomp(const double* vecs, const double* vals, int n, int n_pos, int device, int mode,
+                              double mu, int path, const double* s, double* out);
+/* apply_jacobian (problem.py:222-236) at a decomposition: top = Qdγ/(2λ₂) + μdγ − Φ(dX),
+ * bottom = M[Φ*(dγ) − dX] + (1+μ)dX. */
+int kot_apply_jacobian(kot_problem* p, const double* vecs, const double* vals, int n_pos, double mu,
+                       const double* dgamma, const double* dx, double* top, double* bottom);
+/* cg_solve (linalg.py:117-162) for a host matvec callable: the CG recurrence runs on the device, each
+ * matvec calls fn(user, p, ap) on host copies (nonzero return → KOT_ECALLBACK).  Same stopping rule
+ * (‖r‖ ≤ tol·‖rhs‖), pᵀAp ≤ 0 → iters−1, non-finite → KOT_ECG. */
+typedef int (*kot_matvec_fn)(void* user, const double* p, double* ap);
+int kot_cg_solve(kot_matvec_fn fn, void* user, const double* rhs, int n, double tol, int max_iter, int device,
+                 double* x_out, int* iters, double* res);
+/* middle_operator(pd, make_eliminator(proj_jacobian_coeffs(decomp), mu), mu) (newton.py:116-128)
+ * applied to v, at a given decomposition (the solver's structure-reduced evaluation). */
+int kot_middle_operator_decomp(kot_problem* p, const double* vecs, const double* vals, int n_pos, double mu,
+                               const double* v, double* out);
+/* cg_solve on that middle operator, entirely on the device (the fused CG of the Newton step). */
+int kot_cg_solve_middle(kot_problem* p, const double* vecs, const double* vals, int n_pos, double mu,
+                        const double* rhs, double tol, int max_iter, double* x_out, int* iters, double* res);
+/* newton_direction(pd, r, ctx, cfg) (newton.py:144-195) with ctx = newton_context(decomp, r.norm(),
+ * theta), mu = theta·r.norm(). */
+int kot_newton_direction_decomp(kot_problem* p, const kot_solver_cfg* cfg, const double* r1, const double* r2,
+                                const double* vecs, const double* vals, int n_pos, double mu, double* dgamma,
+                                double* dx, int* cg_iters, int* criterion_met, double* crit_lhs,
+                                double* crit_rhs);
 int kot_phi_forward(kot_problem* p, const double* x, double* out);      /* problem.py:172-177 */
 int kot_phi_adjoint(kot_problem* p, const double* gamma, double* out);  /* problem.py:180-185 */
-/* residual_parts (problem.py:204-214): r1, r2, eigenvalues of Z, n_pos, ||r||. */
+/* objective_grad (problem.py:188-189): (Qγ − z)/(2λ₂); dir = 1: objective_grad_dir (:239-241), Qd/(2λ₂). */
+int kot_objective_grad(kot_problem* p, const double* gamma, int dir, double* out);
+/* constraint_matrix (problem.py:199-201): Φ*(γ) + λ₁I. */
+int kot_constraint_matrix(kot_problem* p, const double* gamma, double* out);
+/* residual_parts (problem.py:204-214): r1, r2, eigenvalues of Z (descending), n_pos, ||r||, and
+ * the eigenvectors (nullable: the SpectralDecomp's host copy). */
 int kot_residual_parts(kot_problem* p, const double* gamma, const double* x, double* r1, double* r2,
-                       double* eigvals, int* n_pos, double* res_norm);
+                       double* eigvals, int* n_pos, double* res_norm, double* eigvecs);
 /* middle_operator (newton.py:116-128) at the context of w with damping theta.
  * form 0: structure-reduced B = R·P form used by the solver (same-sign block as (G_a∘G_a)v/mu);
  * 1: reference form Φ(𝒯[Φ*(v)]); 2: structure-reduced, whole sign block in the GEMMs (row-sharded layout). */

@@ -192,19 +192,23 @@ class Problem:
         return self.z.shape[0]
 
 
-def assemble(xs, ys, xt, yt, l1, l2, bw_sq) -> tuple[Problem, np.ndarray]:
-    """problem.py:135-169 (+ build_kernel_specs :126-132, one bandwidth).
+def assemble(xs, ys, xt, yt, l1, l2, bw_sq, bw_y=None, bw_xy=None) -> tuple[Problem, np.ndarray]:
+    """problem.py:135-169 (+ build_kernel_specs :126-132: one bandwidth unless bw_y / bw_xy are given,
+    i.e. spec_x, spec_y, spec_xy with their own bandwidth_sq).
 
     Returns the problem and the pair-kernel Gram K (for the EG stepsize rule).
     """
     if l1 <= 0.0 or l2 <= 0.0:
         raise ValueError("lambda1 and lambda2 must be positive")
-    q = gaussian_gram(bw_sq, xt) + gaussian_gram(bw_sq, yt)
-    emb = mean_embedding(bw_sq, xs, xt) + mean_embedding(bw_sq, ys, yt)
+    bw_x = bw_sq
+    bw_y = bw_sq if bw_y is None else bw_y
+    bw_xy = bw_sq if bw_xy is None else bw_xy
+    q = gaussian_gram(bw_x, xt) + gaussian_gram(bw_y, yt)
+    emb = mean_embedding(bw_x, xs, xt) + mean_embedding(bw_y, ys, yt)
     cost = np.sum((xt - yt) ** 2, axis=1)
     z = emb - l2 * cost
-    q_sq = embedding_norm_sq(bw_sq, xs) + embedding_norm_sq(bw_sq, ys)
-    kmat = gaussian_gram(bw_sq, np.hstack([xt, yt]))
+    q_sq = embedding_norm_sq(bw_x, xs) + embedding_norm_sq(bw_y, ys)
+    kmat = gaussian_gram(bw_xy, np.hstack([xt, yt]))
     r, jit = cholesky_psd(kmat)
     return Problem(q=q, z=z, q_sq=q_sq, r=r, l1=l1, l2=l2, embed=emb, xt=xt, yt=yt,
                    bw_sq=bw_sq, jitter=jit), kmat

@@ -11,11 +11,12 @@ from paper_2310_14087_b200.newton import NewtonConfig
 from paper_2310_14087_b200.problem import (FillingPoints, IteratePair, ProblemData, assemble, build_kernel_specs,
                                            objective, ot_estimate)
 from paper_2310_14087_b200.solver import SolverConfig, SolverReport, solve, solve_pure_eg
+from paper_2310_14087_b200.datagen import MixtureSpec, sample_mixture, sobol_points
 
 __version__ = "0.1.0"
 
 __all__ = [
     "KernelSpec", "SampleSet", "FillingPoints", "IteratePair", "ProblemData", "assemble", "build_kernel_specs",
     "SolverConfig", "SolverReport", "solve", "solve_pure_eg", "NewtonConfig", "EgConfig", "objective",
-    "ot_estimate",
+    "ot_estimate", "MixtureSpec", "sample_mixture", "sobol_points",
 ]

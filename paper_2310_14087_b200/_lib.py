@@ -47,6 +47,8 @@ class ProfEntryC(C.Structure):
                 ("bytes", C.c_double)]
 
 
+MatvecFn = C.CFUNCTYPE(C.c_int, C.c_void_p, dptr, dptr)
+
 CommFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, dptr, C.c_long, C.c_long, C.c_int, C.c_int)
 
 IterCB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, dptr, dptr, dptr, dptr, C.c_double, C.c_double, dptr, dptr,
@@ -59,7 +61,7 @@ _SIGS = {
     "kot_problem_create": (C.c_int, [dptr, dptr, C.c_double, dptr, dptr, C.c_int, C.c_double, C.c_double,
                                      C.c_double, C.c_int, C.POINTER(C.c_void_p)]),
     "kot_assemble": (C.c_int, [dptr, C.c_int, dptr, C.c_int, dptr, dptr, C.c_int, C.c_int, C.c_double, C.c_double,
-                               C.c_double, C.c_int, C.POINTER(C.c_void_p)]),
+                               C.c_double, C.c_double, C.c_double, C.c_int, C.POINTER(C.c_void_p)]),
     "kot_problem_info": (C.c_int, [C.c_void_p, iptr, dptr, dptr, dptr, dptr, iptr]),
     "kot_problem_download": (C.c_int, [C.c_void_p, dptr, dptr, dptr, dptr, dptr]),
     "kot_problem_destroy": (None, [C.c_void_p]),
@@ -92,7 +94,22 @@ _SIGS = {
     "kot_spectral_apply": (C.c_int, [dptr, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, dptr, dptr]),
     "kot_phi_forward": (C.c_int, [C.c_void_p, dptr, dptr]),
     "kot_phi_adjoint": (C.c_int, [C.c_void_p, dptr, dptr]),
-    "kot_residual_parts": (C.c_int, [C.c_void_p, dptr, dptr, dptr, dptr, dptr, iptr, dptr]),
+    "kot_residual_parts": (C.c_int, [C.c_void_p, dptr, dptr, dptr, dptr, dptr, iptr, dptr, dptr]),
+    "kot_objective_grad": (C.c_int, [C.c_void_p, dptr, C.c_int, dptr]),
+    "kot_constraint_matrix": (C.c_int, [C.c_void_p, dptr, dptr]),
+    "kot_gram_rect": (C.c_int, [dptr, C.c_int, dptr, C.c_int, C.c_int, C.c_double, C.c_int, dptr]),
+    "kot_mean_embedding": (C.c_int, [dptr, C.c_int, dptr, C.c_int, C.c_int, C.c_double, C.c_int, dptr]),
+    "kot_embedding_norm_sq": (C.c_int, [dptr, C.c_int, C.c_int, C.c_double, C.c_int, dptr]),
+    "kot_spectral_apply_decomp": (C.c_int, [dptr, dptr, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                            dptr, dptr]),
+    "kot_apply_jacobian": (C.c_int, [C.c_void_p, dptr, dptr, C.c_int, C.c_double, dptr, dptr, dptr, dptr]),
+    "kot_cg_solve": (C.c_int, [MatvecFn, C.c_void_p, dptr, C.c_int, C.c_double, C.c_int, C.c_int, dptr, iptr,
+                               dptr]),
+    "kot_cg_solve_middle": (C.c_int, [C.c_void_p, dptr, dptr, C.c_int, C.c_double, dptr, C.c_double, C.c_int,
+                                      dptr, iptr, dptr]),
+    "kot_middle_operator_decomp": (C.c_int, [C.c_void_p, dptr, dptr, C.c_int, C.c_double, dptr, dptr]),
+    "kot_newton_direction_decomp": (C.c_int, [C.c_void_p, C.POINTER(SolverCfgC), dptr, dptr, dptr, dptr, C.c_int,
+                                              C.c_double, dptr, dptr, iptr, iptr, dptr, dptr]),
     "kot_middle_operator": (C.c_int, [C.c_void_p, dptr, dptr, C.c_double, dptr, C.c_int, dptr, dptr]),
     "kot_newton_direction": (C.c_int, [C.c_void_p, C.POINTER(SolverCfgC), dptr, dptr, C.c_double, dptr, dptr,
                                        iptr, iptr, dptr, dptr]),

@@ -75,11 +75,12 @@ int kot_problem_create(const double* q, const double* z, double q_sq, const doub
 }
 
 int kot_assemble(const double* xs, int n_mu, const double* ys, int n_nu, const double* xt, const double* yt, int l,
-                 int d, double bandwidth_sq, double lambda1, double lambda2, int device, kot_problem** out) {
+                 int d, double bw_x, double bw_y, double bw_xy, double lambda1, double lambda2, int device,
+                 kot_problem** out) {
   return guarded([&] {
     auto h = new kot_problem();
     try {
-      h->p = kot::problem_assemble(xs, n_mu, ys, n_nu, xt, yt, l, d, bandwidth_sq, lambda1, lambda2, device);
+      h->p = kot::problem_assemble(xs, n_mu, ys, n_nu, xt, yt, l, d, bw_x, bw_y, bw_xy, lambda1, lambda2, device);
     } catch (...) {
       delete h;
       throw;
@@ -273,6 +274,15 @@ static void down(kot::Problem& p, double* h, const double* d, long count) {
   KOT_CUDA(cudaMemcpyAsync(h, d, count * 8, cudaMemcpyDeviceToHost, p.st));
 }
 
+// Upload a host SpectralDecomp into p's (Pw, valw).
+static kot::Decomp up_decomp(kot::Problem& p, const double* vecs, const double* vals, int n_pos) {
+  kot::kot_require(n_pos >= 0 && n_pos <= p.n, kot::KOT_EINVAL, "invalid decomposition");
+  kot::Bufs& b = p.bufs();
+  up(p, b.Pw, vecs, (long)p.n * p.n);
+  up(p, b.valw, vals, p.n);
+  return kot::Decomp{b.Pw, b.valw, n_pos};
+}
+
 // A scratch problem for the matrix-only entry points (no instance data needed).
 static std::unique_ptr<kot::Problem> scratch_problem(int n, int device) {
   std::vector<double> zeros(1, 0.0);
@@ -291,6 +301,60 @@ int kot_gram(const double* pts, int n, int d, double bandwidth_sq, int device, d
     KOT_CUDA(cudaMemcpyAsync(dp.p, pts, (long)n * d * 8, cudaMemcpyHostToDevice, st));
     kot::gram_square(dp.p, dp.p, n, d, bandwidth_sq, bandwidth_sq, 1, false, dout.p, st);
     KOT_CUDA(cudaMemcpyAsync(out, dout.p, (long)n * n * 8, cudaMemcpyDeviceToHost, st));
+    KOT_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+  });
+}
+
+int kot_gram_rect(const double* a, int m, const double* b, int p, int d, double bandwidth_sq, int device,
+                  double* out) {
+  return guarded([&] {
+    kot::kot_require(bandwidth_sq > 0.0, kot::KOT_EINVAL, "bandwidth_sq must be positive");
+    kot::kot_require(m >= 0 && p >= 0 && d >= 1, kot::KOT_EINVAL, "invalid shapes");
+    KOT_CUDA(cudaSetDevice(device));
+    if (m == 0 || p == 0) return;
+    cudaStream_t st;
+    KOT_CUDA(cudaStreamCreate(&st));
+    DevBuf da((long)m * d), db((long)p * d), dout((long)m * p);
+    KOT_CUDA(cudaMemcpyAsync(da.p, a, (long)m * d * 8, cudaMemcpyHostToDevice, st));
+    KOT_CUDA(cudaMemcpyAsync(db.p, b, (long)p * d * 8, cudaMemcpyHostToDevice, st));
+    kot::gram_rect(da.p, m, db.p, p, d, bandwidth_sq, dout.p, st);
+    KOT_CUDA(cudaMemcpyAsync(out, dout.p, (long)m * p * 8, cudaMemcpyDeviceToHost, st));
+    KOT_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+  });
+}
+
+int kot_mean_embedding(const double* samples, int n, const double* queries, int m, int d, double bandwidth_sq,
+                       int device, double* out) {
+  return guarded([&] {
+    kot::kot_require(bandwidth_sq > 0.0, kot::KOT_EINVAL, "bandwidth_sq must be positive");
+    kot::kot_require(n >= 1, kot::KOT_EINVAL, "sample set is empty");
+    KOT_CUDA(cudaSetDevice(device));
+    if (m == 0) return;
+    cudaStream_t st;
+    KOT_CUDA(cudaStreamCreate(&st));
+    DevBuf ds((long)n * d), dq((long)m * d), dout(m);
+    KOT_CUDA(cudaMemcpyAsync(ds.p, samples, (long)n * d * 8, cudaMemcpyHostToDevice, st));
+    KOT_CUDA(cudaMemcpyAsync(dq.p, queries, (long)m * d * 8, cudaMemcpyHostToDevice, st));
+    kot::mean_embedding_device(ds.p, n, dq.p, m, d, bandwidth_sq, dout.p, st);
+    KOT_CUDA(cudaMemcpyAsync(out, dout.p, (long)m * 8, cudaMemcpyDeviceToHost, st));
+    KOT_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+  });
+}
+
+int kot_embedding_norm_sq(const double* samples, int n, int d, double bandwidth_sq, int device, double* out) {
+  return guarded([&] {
+    kot::kot_require(bandwidth_sq > 0.0, kot::KOT_EINVAL, "bandwidth_sq must be positive");
+    kot::kot_require(n >= 1, kot::KOT_EINVAL, "sample set is empty");
+    KOT_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    KOT_CUDA(cudaStreamCreate(&st));
+    DevBuf ds((long)n * d), scratch(n + 1), dout(1);
+    KOT_CUDA(cudaMemcpyAsync(ds.p, samples, (long)n * d * 8, cudaMemcpyHostToDevice, st));
+    kot::embedding_norm_sq_device(ds.p, n, d, bandwidth_sq, scratch.p, dout.p, st);
+    KOT_CUDA(cudaMemcpyAsync(out, dout.p, 8, cudaMemcpyDeviceToHost, st));
     KOT_CUDA(cudaStreamSynchronize(st));
     cudaStreamDestroy(st);
   });
@@ -402,6 +466,147 @@ int kot_spectral_apply(const double* z, int n, int device, int mode, double mu, 
   });
 }
 
+int kot_spectral_apply_decomp(const double* vecs, const double* vals, int n, int n_pos, int device, int mode,
+                              double mu, int path, const double* s, double* out) {
+  return guarded([&] {
+    kot::kot_require(n >= 1 && n_pos >= 0 && n_pos <= n, kot::KOT_EINVAL, "invalid decomposition");
+    kot::kot_require(mode >= 0 && mode <= 2, kot::KOT_EINVAL, "invalid mode");
+    if (mode == 0) kot::kot_require(mu > 0.0, kot::KOT_EINVAL, "regularization mu must be positive");
+    auto p = scratch_problem(n, device);
+    kot::Bufs& b = p->bufs();
+    const long nn = (long)n * n;
+    up(*p, b.Pw, vecs, nn);
+    up(*p, b.valw, vals, n);
+    const kot::Decomp dc{b.Pw, b.valw, n_pos};
+    if (mode == 2) {
+      if (n_pos == 0)
+        KOT_CUDA(cudaMemsetAsync(b.Xv, 0, sizeof(double) * nn, p->st));
+      else
+        kot::proj(*p, dc, nullptr, b.Xv);
+    } else {
+      up(*p, b.Xw, s, nn);
+      kot::spectral_filter(*p, dc, b.Xw, b.Xv, mu, mode, path);
+    }
+    down(*p, out, b.Xv, nn);
+    KOT_CUDA(cudaStreamSynchronize(p->st));
+  });
+}
+
+int kot_apply_jacobian(kot_problem* h, const double* vecs, const double* vals, int n_pos, double mu,
+                       const double* dgamma, const double* dx, double* top, double* bottom) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    const int n = p.n;
+    kot::kot_require(n_pos >= 0 && n_pos <= n, kot::KOT_EINVAL, "invalid decomposition");
+    KOT_CUDA(cudaSetDevice(p.device));
+    kot::Bufs& b = p.bufs();
+    const long nn = (long)n * n;
+    const kot::Decomp dc = up_decomp(p, vecs, vals, n_pos);
+    up(p, b.dg, dgamma, n);
+    up(p, b.dX, dx, nn);
+    KOT_CUDA(cudaMemsetAsync(b.e3, 0, sizeof(double) * n, p.st));
+    KOT_CUDA(cudaMemsetAsync(b.Xv, 0, sizeof(double) * nn, p.st));
+    // top = Qdγ/(2λ₂) + μdγ − Φ(dX);  bottom = M[Φ*(dγ) − dX] + (1+μ)dX   (problem.py:222-236)
+    kot::phi_partials(p, b.dX);
+    kot::finalize(p, kot::FIN_JTOP, b.dg, true, b.e3, mu, b.e1);
+    kot::phi_adjoint_ex(p, b.dg, p.M1, 1.0, b.dX, -1.0, 0.0);
+    kot::spectral_filter(p, dc, p.M1, p.M2, mu, 1);
+    kot::jac_bottom(p, nn, p.M2, b.dX, mu, b.Xv, p.M1);
+    down(p, top, b.e1, n);
+    down(p, bottom, p.M1, nn);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+  });
+}
+
+int kot_cg_solve(kot_matvec_fn fn, void* user, const double* rhs, int n, double tol, int max_iter, int device,
+                 double* x_out, int* iters, double* res) {
+  return guarded([&] {
+    kot::kot_require(fn != nullptr && n >= 1, kot::KOT_EINVAL, "invalid operator");
+    kot::kot_require(max_iter >= 1, kot::KOT_EINVAL, "max_iter must be >= 1");
+    auto p = scratch_problem(n, device);
+    kot::Bufs& b = p->bufs();
+    std::vector<double> hp(n), hap(n);
+    up(*p, b.e1, rhs, n);
+    const kot::CgResult r = kot::cg_solve_op(*p, b.e1, tol, max_iter, [&](const double* pv, double* ap) {
+      down(*p, hp.data(), pv, n);
+      KOT_CUDA(cudaStreamSynchronize(p->st));
+      kot::kot_require(fn(user, hp.data(), hap.data()) == 0, kot::KOT_ECALLBACK, "matvec callback raised");
+      up(*p, ap, hap.data(), n);
+    }, b.e2);
+    down(*p, x_out, b.e2, n);
+    KOT_CUDA(cudaStreamSynchronize(p->st));
+    *iters = r.iters;
+    *res = r.res;
+  });
+}
+
+int kot_cg_solve_middle(kot_problem* h, const double* vecs, const double* vals, int n_pos, double mu,
+                        const double* rhs, double tol, int max_iter, double* x_out, int* iters, double* res) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    kot::kot_require(mu > 0.0, kot::KOT_EINVAL, "regularization mu must be positive");
+    kot::Bufs& b = p.bufs();
+    const kot::Decomp dc = up_decomp(p, vecs, vals, n_pos);
+    kot::MvCtx mv;
+    kot::matvec_prepare(p, dc, mu, mv, true);
+    up(p, b.e1, rhs, p.n);
+    const kot::CgResult r = kot::cg_solve_op(p, b.e1, tol, max_iter, [&](const double* pv, double* ap) {
+      kot::middle_operator_fast(p, mv, pv, ap);
+    }, b.e2);
+    down(p, x_out, b.e2, p.n);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+    *iters = r.iters;
+    *res = r.res;
+  });
+}
+
+int kot_middle_operator_decomp(kot_problem* h, const double* vecs, const double* vals, int n_pos, double mu,
+                               const double* v, double* out) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    kot::kot_require(mu > 0.0, kot::KOT_EINVAL, "regularization mu must be positive");
+    kot::Bufs& b = p.bufs();
+    const kot::Decomp dc = up_decomp(p, vecs, vals, n_pos);
+    kot::MvCtx mv;
+    kot::matvec_prepare(p, dc, mu, mv, true);
+    up(p, b.e2, v, p.n);
+    kot::middle_operator_fast(p, mv, b.e2, b.e1);
+    down(p, out, b.e1, p.n);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+  });
+}
+
+int kot_newton_direction_decomp(kot_problem* h, const kot_solver_cfg* cfg, const double* r1, const double* r2,
+                                const double* vecs, const double* vals, int n_pos, double mu, double* dgamma,
+                                double* dx, int* cg_iters, int* criterion_met, double* crit_lhs, double* crit_rhs) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    const kot::SolverCfg c = to_cfg(cfg);
+    check_cfg(c);
+    kot::kot_require(mu > 0.0, kot::KOT_EINVAL, "regularization mu must be positive");
+    kot::Bufs& b = p.bufs();
+    const long nn = (long)p.n * p.n;
+    const kot::Decomp dc = up_decomp(p, vecs, vals, n_pos);
+    up(p, b.r1w, r1, p.n);
+    up(p, b.r2w, r2, nn);
+    // r.norm() = ‖r1‖₂ + ‖r2‖_F (problem.py:56-57)
+    const double rn = kot::dev_norm(p, b.r1w, p.n) + kot::dev_norm(p, b.r2w, nn);
+    kot::kot_require(rn > 0.0, kot::KOT_EINVAL, "direction requires a nonzero residual");
+    kot::NewtonOut o = kot::newton_direction(p, b.r1w, b.r2w, rn, dc, mu, c, b.dg, b.dX);
+    kot::newton_resolve(p, rn, c, o);
+    down(p, dgamma, b.dg, p.n);
+    down(p, dx, b.dX, nn);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+    *cg_iters = o.cg_iters;
+    *criterion_met = o.met;
+    *crit_lhs = o.lhs;
+    *crit_rhs = o.rhs;
+  });
+}
+
 int kot_phi_forward(kot_problem* h, const double* x, double* out) {
   return guarded([&] {
     kot::Problem& p = *h->p;
@@ -428,8 +633,40 @@ int kot_phi_adjoint(kot_problem* h, const double* gamma, double* out) {
   });
 }
 
+// objective_grad (problem.py:188-189): (Qγ − z)/(2λ₂);  mode 1 objective_grad_dir (:239-241): Qd/(2λ₂)
+int kot_objective_grad(kot_problem* h, const double* gamma, int dir, double* out) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    kot::Bufs& b = p.bufs();
+    up(p, b.e1, gamma, p.n);
+    if (dir) {
+      KOT_CUDA(cudaMemsetAsync(b.e3, 0, sizeof(double) * p.n, p.st));
+      kot::finalize(p, kot::FIN_JTOP, b.e1, false, b.e3, 0.0, b.e2);  // Qd/(2λ₂) + 0·d − 0 + 0
+    } else {
+      kot::finalize(p, kot::FIN_GRAD, b.e1, false, nullptr, 0.0, b.e2);
+    }
+    down(p, out, b.e2, p.n);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+  });
+}
+
+// constraint_matrix (problem.py:199-201): Φ*(γ) + λ₁I
+int kot_constraint_matrix(kot_problem* h, const double* gamma, double* out) {
+  return guarded([&] {
+    kot::Problem& p = *h->p;
+    KOT_CUDA(cudaSetDevice(p.device));
+    kot::Bufs& b = p.bufs();
+    const long nn = (long)p.n * p.n;
+    up(p, b.e1, gamma, p.n);
+    kot::phi_adjoint_ex(p, b.e1, b.Xh, 1.0, nullptr, 0.0, p.l1);
+    down(p, out, b.Xh, nn);
+    KOT_CUDA(cudaStreamSynchronize(p.st));
+  });
+}
+
 int kot_residual_parts(kot_problem* h, const double* gamma, const double* x, double* r1, double* r2, double* eigvals,
-                       int* n_pos, double* res_norm) {
+                       int* n_pos, double* res_norm, double* eigvecs) {
   return guarded([&] {
     kot::Problem& p = *h->p;
     KOT_CUDA(cudaSetDevice(p.device));
@@ -442,6 +679,7 @@ int kot_residual_parts(kot_problem* h, const double* gamma, const double* x, dou
     if (r1) down(p, r1, b.r1w, p.n);
     if (r2) down(p, r2, b.r2w, nn);
     if (eigvals) down(p, eigvals, dc.vals, p.n);
+    if (eigvecs) down(p, eigvecs, dc.P, nn);
     KOT_CUDA(cudaStreamSynchronize(p.st));
     if (n_pos) *n_pos = dc.k;
     if (res_norm) *res_norm = res;

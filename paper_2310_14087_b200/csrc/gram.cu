@@ -91,7 +91,7 @@ __global__ void gram_square_kernel(const double* __restrict__ P0, const double* 
 // .mean(axis=0) on a C-contiguous array does.
 __global__ void embed_kernel(const double* __restrict__ xs, int nx, const double* __restrict__ ys, int ny,
                              const double* __restrict__ xt, const double* __restrict__ yt, int l, int d,
-                             double twobw, double lambda2, double* __restrict__ embed,
+                             double twobw_x, double twobw_y, double lambda2, double* __restrict__ embed,
                              double* __restrict__ z) {
   extern __shared__ double sh[];  // staged sample chunk: [CH][d]
   const int CH = 64;
@@ -102,6 +102,7 @@ __global__ void embed_kernel(const double* __restrict__ xs, int nx, const double
     const double* S = set ? ys : xs;
     const double* F = set ? yt : xt;
     const int ns = set ? ny : nx;
+    const double twobw = set ? twobw_y : twobw_x;
     if (j < l)
       for (int k = 0; k < d; ++k) fj[k] = F[(long)j * d + k];
     double acc = 0.0;
@@ -185,21 +186,104 @@ void gram_square(const double* P0, const double* P1, int n, int d, double bw0, d
   KOT_LAUNCH_CHECK();
 }
 
+// Rectangular Gram: one thread per output entry, 32×8 tiles with both point tiles in shared memory.
+__global__ void gram_rect_kernel(const double* __restrict__ A, int m, const double* __restrict__ B, int p, int d,
+                                 double twobw, double* __restrict__ out) {
+  extern __shared__ double gsh[];
+  const int LD = d + 1;
+  double* sa = gsh;            // 8 rows of A
+  double* sb = gsh + 8 * LD;   // 32 rows of B
+  const int i0 = blockIdx.y * 8, j0 = blockIdx.x * 32;
+  for (int e = threadIdx.x; e < 8 * d; e += blockDim.x) {
+    const int r = e / d, k = e % d;
+    sa[r * LD + k] = (i0 + r < m) ? A[(long)(i0 + r) * d + k] : 0.0;
+  }
+  for (int e = threadIdx.x; e < 32 * d; e += blockDim.x) {
+    const int r = e / d, k = e % d;
+    sb[r * LD + k] = (j0 + r < p) ? B[(long)(j0 + r) * d + k] : 0.0;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int i = i0 + ty, j = j0 + tx;
+  if (i < m && j < p) out[(long)i * p + j] = exp(-sqdist_seq(sa + ty * LD, sb + tx * LD, d) / twobw);
+}
+
+void gram_rect(const double* A, int m, const double* B, int p, int d, double bw, double* out, cudaStream_t st) {
+  kot_require(d >= 1 && d <= GMAXD, KOT_EINVAL, "point dimension must be in [1, 128]");
+  if (m == 0 || p == 0) return;
+  const size_t smem = 40 * (d + 1) * sizeof(double);
+  gram_rect_kernel<<<dim3(ceil_div(p, 32), ceil_div(m, 8)), 256, smem, st>>>(A, m, B, p, d, 2.0 * bw, out);
+  KOT_LAUNCH_CHECK();
+}
+
+// out[j] = mean_i k(S_i, F_j): the column mean of the n × m Gram accumulated row by row (numpy's
+// .mean(axis=0) order), never materialised.
+__global__ void mean_embed_kernel(const double* __restrict__ S, int n, const double* __restrict__ F, int m, int d,
+                                  double twobw, double* __restrict__ out) {
+  extern __shared__ double sh[];  // staged sample chunk: [CH][d]
+  const int CH = 64;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  double fj[GMAXD];
+  if (j < m)
+    for (int k = 0; k < d; ++k) fj[k] = F[(long)j * d + k];
+  double acc = 0.0;
+  for (int c0 = 0; c0 < n; c0 += CH) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < CH * d; e += blockDim.x) {
+      const int r = e / d, k = e % d;
+      sh[e] = (c0 + r < n) ? S[(long)(c0 + r) * d + k] : 0.0;
+    }
+    __syncthreads();
+    if (j < m) {
+      const int cn = min(CH, n - c0);
+      for (int r = 0; r < cn; ++r) acc = __dadd_rn(acc, exp(-sqdist_seq(sh + r * d, fj, d) / twobw));
+    }
+  }
+  if (j < m) out[j] = acc / n;
+}
+
+__global__ void mean_parts_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double a = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a += part[i];
+  a = block_sum(a, red);
+  if (threadIdx.x == 0) out[0] = a / ((double)n * n);
+}
+
+void mean_embedding_device(const double* S, int n, const double* F, int m, int d, double bw, double* out,
+                           cudaStream_t st) {
+  kot_require(d >= 1 && d <= GMAXD, KOT_EINVAL, "point dimension must be in [1, 128]");
+  kot_require(n >= 1, KOT_EINVAL, "sample set is empty");
+  if (m == 0) return;
+  mean_embed_kernel<<<ceil_div(m, 128), 128, 64 * d * sizeof(double), st>>>(S, n, F, m, d, 2.0 * bw, out);
+  KOT_LAUNCH_CHECK();
+}
+
+void embedding_norm_sq_device(const double* S, int n, int d, double bw, double* scratch, double* out,
+                              cudaStream_t st) {
+  kot_require(d >= 1 && d <= GMAXD, KOT_EINVAL, "point dimension must be in [1, 128]");
+  kot_require(n >= 1, KOT_EINVAL, "sample set is empty");
+  gram_sum_kernel<<<n, 256, 0, st>>>(S, n, d, 2.0 * bw, scratch);
+  KOT_LAUNCH_CHECK();
+  mean_parts_kernel<<<1, 256, 0, st>>>(scratch, n, out);
+  KOT_LAUNCH_CHECK();
+}
+
 void assemble_device(const double* xs, int nx, const double* ys, int ny, const double* xt, const double* yt,
-                     int l, int d, double bw, double lambda2, double* Q, double* Kmat, double* embed,
-                     double* z, double* q_sq, double* scratch, cudaStream_t st) {
+                     int l, int d, double bw_x, double bw_y, double bw_xy, double lambda2, double* Q, double* Kmat,
+                     double* embed, double* z, double* q_sq, double* scratch, cudaStream_t st) {
   kot_require(d <= GMAXD / 2 && d >= 1, KOT_EINVAL, "point dimension must be in [1, 64]");
-  // Q = G(xt) + G(yt): unit diagonals sum to 2.
-  gram_square(xt, yt, l, d, bw, bw, 2, false, Q, st);
+  // Q = G_x(xt) + G_y(yt): unit diagonals sum to 2.
+  gram_square(xt, yt, l, d, bw_x, bw_y, 2, false, Q, st);
   // K on [xt yt] ∈ R^{2d}
-  gram_square(xt, yt, l, d, bw, bw, 1, true, Kmat, st);
+  gram_square(xt, yt, l, d, bw_xy, bw_xy, 1, true, Kmat, st);
   const int thr = 128;
-  embed_kernel<<<ceil_div(l, thr), thr, 64 * d * sizeof(double), st>>>(xs, nx, ys, ny, xt, yt, l, d,
-                                                                       2.0 * bw, lambda2, embed, z);
+  embed_kernel<<<ceil_div(l, thr), thr, 64 * d * sizeof(double), st>>>(xs, nx, ys, ny, xt, yt, l, d, 2.0 * bw_x,
+                                                                       2.0 * bw_y, lambda2, embed, z);
   KOT_LAUNCH_CHECK();
-  gram_sum_kernel<<<nx, 256, 0, st>>>(xs, nx, d, 2.0 * bw, scratch);
+  gram_sum_kernel<<<nx, 256, 0, st>>>(xs, nx, d, 2.0 * bw_x, scratch);
   KOT_LAUNCH_CHECK();
-  gram_sum_kernel<<<ny, 256, 0, st>>>(ys, ny, d, 2.0 * bw, scratch + nx);
+  gram_sum_kernel<<<ny, 256, 0, st>>>(ys, ny, d, 2.0 * bw_y, scratch + nx);
   KOT_LAUNCH_CHECK();
   sum_parts_kernel<<<1, 256, 0, st>>>(scratch, nx, scratch + nx, ny, q_sq);
   KOT_LAUNCH_CHECK();

@@ -9,8 +9,15 @@ namespace kot {
 void gram_square(const double* P0, const double* P1, int n, int d, double bw0, double bw1, int nsets, bool pair,
                  double* out, cudaStream_t st);
 void assemble_device(const double* xs, int nx, const double* ys, int ny, const double* xt, const double* yt, int l,
-                     int d, double bw, double lambda2, double* Q, double* Kmat, double* embed, double* z,
-                     double* q_sq, double* scratch, cudaStream_t st);
+                     int d, double bw_x, double bw_y, double bw_xy, double lambda2, double* Q, double* Kmat,
+                     double* embed, double* z, double* q_sq, double* scratch, cudaStream_t st);
+// rectangular Gram out[i][j] = k(a_i, b_j) (m × p); column means of the n × m sample/query Gram;
+// mean of the n × n sample Gram (unit diagonal) — kernels.py:61-94
+void gram_rect(const double* A, int m, const double* B, int p, int d, double bw, double* out, cudaStream_t st);
+void mean_embedding_device(const double* S, int n, const double* F, int m, int d, double bw, double* out,
+                           cudaStream_t st);
+void embedding_norm_sq_device(const double* S, int n, int d, double bw, double* scratch, double* out,
+                              cudaStream_t st);
 
 void evaluate_map_device(const double* xs, int n, const double* xt, const double* gamma, int l, const double* qs,
                          int m, int d, double bw, double lambda2, double* u, double* tmap, cudaStream_t st);

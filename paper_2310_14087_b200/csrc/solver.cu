@@ -207,6 +207,41 @@ static CgOut cg_solve(Problem& p, const MvCtx& mv, const double* rhs, double tol
   return {it, res};
 }
 
+// linalg.cg_solve (linalg.py:117-162) for any operator `apply(p_dev, ap_dev)` on p's stream: the same
+// recurrence, stopping rule and error conditions as the solver's CG (cg_init/cg_step kernels).
+CgResult cg_solve_op(Problem& p, const double* rhs, double tol, int max_iter,
+                     const std::function<void(const double*, double*)>& apply, double* x_out) {
+  Bufs& b = p.bufs();
+  const int n = p.n;
+  kot_require(max_iter >= 1, KOT_EINVAL, "max_iter must be >= 1");
+  cg_init_kernel<<<1, CG_THREADS, 0, p.st>>>(n, rhs, b.cx, b.cr, b.cp, p.dsc);
+  KOT_LAUNCH_CHECK();
+  fetch(p, 16);
+  const double target = tol * p.hsc[SC_BN];
+  double res = p.hsc[SC_BN];
+  int it = 0;
+  if (res > target) {
+    for (it = 1; it <= max_iter; ++it) {
+      apply(b.cp, b.cap);
+      cg_step_kernel<<<1, CG_THREADS, 0, p.st>>>(n, b.cx, b.cr, b.cp, b.cap, p.dsc, 0);
+      KOT_LAUNCH_CHECK();
+      fetch(p, 16);
+      const int flag = (int)p.hsc[SC_FLAG];
+      if (flag == 1) throw KotError(KOT_ECG, "non-finite curvature in conjugate gradient");
+      if (flag == 2) {  // p collapsed to numerical zero on an SPD operator
+        it -= 1;
+        break;
+      }
+      res = p.hsc[SC_RES];
+      if (flag == 3) throw KotError(KOT_ECG, "non-finite residual in conjugate gradient");
+      if (res <= target) break;
+    }
+    if (it > max_iter) it = max_iter;
+  }
+  KOT_CUDA(cudaMemcpyAsync(x_out, b.cx, sizeof(double) * n, cudaMemcpyDeviceToDevice, p.st));
+  return {it, res};
+}
+
 // --------------------------------------------------------------- Newton
 
 // Criterion ‖(J+μI)dw + r‖ ≤ τ min(1, κ‖r‖‖dw‖) for dw = (sol, ã2 − 𝒯[Φ*(sol)]) (newton.py:131-141,

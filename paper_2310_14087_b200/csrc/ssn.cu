@@ -177,10 +177,10 @@ std::unique_ptr<Problem> problem_from_host(const double* q, const double* z, dou
 }
 
 std::unique_ptr<Problem> problem_assemble(const double* xs, int nx, const double* ys, int ny, const double* xt,
-                                          const double* yt, int l, int d, double bw, double l1, double l2,
-                                          int device) {
+                                          const double* yt, int l, int d, double bw_x, double bw_y, double bw_xy,
+                                          double l1, double l2, int device) {
   kot_require(l1 > 0.0 && l2 > 0.0, KOT_EINVAL, "lambda1 and lambda2 must be positive");
-  kot_require(bw > 0.0, KOT_EINVAL, "bandwidth_sq must be positive");
+  kot_require(bw_x > 0.0 && bw_y > 0.0 && bw_xy > 0.0, KOT_EINVAL, "bandwidth_sq must be positive");
   kot_require(nx >= 1 && ny >= 1, KOT_EINVAL, "sample set is empty");
   auto p = make_problem(l, device);
   p->l1 = l1;
@@ -201,7 +201,7 @@ std::unique_ptr<Problem> problem_assemble(const double* xs, int nx, const double
   if (!p->kmat_buf) p->kmat_buf = p->alloc(nn);
   p->Kmat = p->kmat_buf;
   double* scratch = tscratch.p;
-  assemble_device(dxs, nx, dys, ny, dxt, dyt, l, d, bw, l2, p->Q, p->Kmat, p->embed, p->z, p->dsc, scratch, p->st);
+  assemble_device(dxs, nx, dys, ny, dxt, dyt, l, d, bw_x, bw_y, bw_xy, l2, p->Q, p->Kmat, p->embed, p->z, p->dsc, scratch, p->st);
   KOT_CUDA(cudaMemcpyAsync(p->hsc, p->dsc, sizeof(double), cudaMemcpyDeviceToHost, p->st));
   KOT_CUDA(cudaStreamSynchronize(p->st));
   p->q_sq = p->hsc[0];

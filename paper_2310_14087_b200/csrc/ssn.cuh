@@ -1,6 +1,7 @@
 // Device-resident SSN problem and operators (reference problem.py, psdcone.py,
 // newton.py, eg.py, solver.py).
 #pragma once
+#include <functional>
 #include <memory>
 #include <vector>
 
@@ -109,7 +110,8 @@ void problem_release(std::unique_ptr<Problem> p);
 std::unique_ptr<Problem> problem_from_host(const double* q, const double* z, double q_sq, const double* r,
                                            const double* embed, int n, double l1, double l2, double jitter, int device);
 std::unique_ptr<Problem> problem_assemble(const double* xs, int nx, const double* ys, int ny, const double* xt,
-                                          const double* yt, int l, int d, double bw, double l1, double l2, int device);
+                                          const double* yt, int l, int d, double bw_x, double bw_y, double bw_xy,
+                                          double l1, double l2, int device);
 
 // ---- operators (device pointers in/out, all on p.st)
 void phi_forward(Problem& p, const double* X, double* out);
@@ -164,6 +166,12 @@ struct NewtonOut {
   double lhs, rhs, cg_ms;
   bool crit_pending = false;  // met/lhs/rhs of the last attempt still in flight: newton_resolve
 };
+struct CgResult {
+  int iters;
+  double res;
+};
+CgResult cg_solve_op(Problem& p, const double* rhs, double tol, int max_iter,
+                     const std::function<void(const double*, double*)>& apply, double* x_out);
 NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, double res_norm, const Decomp& dc,
                            double mu, const SolverCfg& cfg, double* dg, double* dX);
 // completes met / lhs / rhs of a direction whose last criterion was left running (res_norm as passed

@@ -3,13 +3,15 @@
 Reference: ``pkg/src/kot/linalg.py``.  ``sym_eig`` is the hand-written
 sytrd + divide-and-conquer + back-transform eigensolver (csrc/eig.cu);
 ``cholesky_psd`` the blocked DMMA Cholesky with the same jitter ladder
-(csrc/chol.cu).  The reference's Python-callable ``cg_solve`` has no device
-equivalent: CG runs fused inside the device Newton step (csrc/solver.cu).
+(csrc/chol.cu); ``cg_solve`` runs the CG recurrence on the device — entirely so
+for the solver's own middle operator (``newton.middle_operator``), with one
+host round trip per matvec for an arbitrary Python callable.
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass
+from typing import Callable
 
 import numpy as np
 
@@ -61,6 +63,52 @@ def sym_eig(z, device: int | None = None) -> SpectralDecomp:
                                       _lib.ptr(vecs), _lib.ptr(vals), _lib.C.byref(k)))
     kk = int(k.value)
     return SpectralDecomp(eigvecs=vecs, eigvals=vals, pos_idx=np.arange(kk), nonpos_idx=np.arange(kk, n))
+
+
+def cg_solve(apply: Callable[[np.ndarray], np.ndarray], rhs, tol: float, max_iter: int,
+             device: int | None = None) -> tuple[np.ndarray, int, float]:
+    """Conjugate gradient for an SPD operator (linalg.py:117-162): stops once the recursive residual
+    ‖r‖ ≤ tol·‖rhs‖ or after ``max_iter`` matvecs; pᵀAp ≤ 0 ends it one step early; NaN/Inf raise
+    FloatingPointError.
+
+    ``apply`` built by :func:`paper_2310_14087_b200.newton.middle_operator` runs wholly on the GPU
+    (the solver's fused CG); any other callable is evaluated on host copies of p, with the CG vector
+    algebra on the device."""
+    if max_iter < 1:
+        raise ValueError("max_iter must be >= 1")
+    b = _lib.f64(rhs)
+    n = b.shape[0]
+    x = np.empty(n)
+    iters, res = _lib.C.c_int(0), _lib.C.c_double(0.0)
+    dev = getattr(apply, "_kot_middle", None)
+    if dev is not None:  # (ProblemData, SpectralDecomp, mu): everything stays in HBM
+        pd, dc, mu = dev
+        _lib.check(_lib.lib().kot_cg_solve_middle(pd.device_problem().handle, _lib.ptr(_lib.f64(dc.eigvecs)),
+                                                  _lib.ptr(_lib.f64(dc.eigvals)), dc.n_pos, float(mu), _lib.ptr(b),
+                                                  float(tol), int(max_iter), _lib.ptr(x), _lib.C.byref(iters),
+                                                  _lib.C.byref(res)))
+        return x, int(iters.value), float(res.value)
+    raised: list[BaseException] = []
+
+    def _mv(_user, p, ap):
+        try:
+            out = np.asarray(apply(np.ctypeslib.as_array(p, shape=(n,)).copy()), dtype=float)
+            if out.shape != (n,):
+                raise ValueError(f"operator returned shape {out.shape}, expected ({n},)")
+            np.ctypeslib.as_array(ap, shape=(n,))[:] = out
+            return 0
+        except BaseException as e:  # noqa: BLE001 — re-raised below
+            raised.append(e)
+            return 1
+
+    cb = _lib.MatvecFn(_mv)
+    st = _lib.lib().kot_cg_solve(cb, None, _lib.ptr(b), n, float(tol), int(max_iter),
+                                 _lib.default_device() if device is None else device, _lib.ptr(x),
+                                 _lib.C.byref(iters), _lib.C.byref(res))
+    if raised:
+        raise raised[0]
+    _lib.check(st)
+    return x, int(iters.value), float(res.value)
 
 
 def cholesky_psd(k, device: int | None = None) -> CholeskyFactor:

@@ -13,7 +13,9 @@ from dataclasses import dataclass
 import numpy as np
 
 from paper_2310_14087_b200 import _lib
-from paper_2310_14087_b200.problem import IteratePair, ProblemData
+from paper_2310_14087_b200.linalg import SpectralDecomp
+from paper_2310_14087_b200.problem import IteratePair, ProblemData, residual_parts
+from paper_2310_14087_b200.psdcone import NewtonEliminator, ProjJacobianCoeffs, make_eliminator, proj_jacobian_coeffs
 
 
 @dataclass(frozen=True)
@@ -48,6 +50,17 @@ class NewtonConfig:
 
 
 @dataclass(frozen=True)
+class NewtonContext:
+    """Per-iteration spectral objects at the current iterate (newton.py:74-82)."""
+
+    decomp: SpectralDecomp
+    coeffs: ProjJacobianCoeffs
+    eliminator: NewtonEliminator
+    mu: float
+    theta: float
+
+
+@dataclass(frozen=True)
 class NewtonStep:
     """newton.py:85-92."""
 
@@ -70,6 +83,54 @@ def cfg_struct(newton: NewtonConfig, eg_stepsize: float = 0.01, residual_tol: fl
     c.eg_stepsize, c.residual_tol = float(eg_stepsize), float(residual_tol)
     c.max_iter, c.safeguard_every = int(max_iter), int(safeguard_every)
     return c
+
+
+def newton_context(decomp: SpectralDecomp, res_norm: float, theta: float) -> NewtonContext:
+    """μ = θ‖r‖ and the spectral operators at the decomposition (newton.py:95-107)."""
+    if res_norm <= 0.0:
+        raise ValueError("context requires a nonzero residual")
+    mu = theta * res_norm
+    coeffs = proj_jacobian_coeffs(decomp)
+    return NewtonContext(decomp=decomp, coeffs=coeffs, eliminator=make_eliminator(coeffs, mu), mu=mu, theta=theta)
+
+
+def newton_context_at(pd: ProblemData, w: IteratePair, theta: float) -> NewtonContext:
+    """Evaluate the residual at ``w`` (on the GPU) and build its context (newton.py:110-113)."""
+    r, decomp = residual_parts(pd, w)
+    return newton_context(decomp, r.norm(), theta)
+
+
+def middle_operator(pd: ProblemData, elim: NewtonEliminator, mu: float):
+    """SPD operator of the reduced system v ↦ Qv/(2λ₂) + μv + Φ(𝒯[Φ*(v)]) (newton.py:116-128).
+
+    The returned callable evaluates on the GPU (the solver's structure-reduced form); passed to
+    :func:`paper_2310_14087_b200.linalg.cg_solve` it runs the whole CG in HBM."""
+    dc = elim.coeffs.decomp
+    vecs, vals = _lib.f64(dc.eigvecs), _lib.f64(dc.eigvals)
+
+    def apply(v):
+        vv = _lib.f64(v, (pd.n,))
+        out = np.empty(pd.n)
+        _lib.check(_lib.lib().kot_middle_operator_decomp(pd.device_problem().handle, _lib.ptr(vecs), _lib.ptr(vals),
+                                                         dc.n_pos, float(mu), _lib.ptr(vv), _lib.ptr(out)))
+        return out
+
+    apply._kot_middle = (pd, dc, float(mu))
+    return apply
+
+
+def newton_direction(pd: ProblemData, r: IteratePair, ctx: NewtonContext, cfg: NewtonConfig) -> NewtonStep:
+    """Algorithm 1 (newton.py:144-195) at ``ctx`` for the residual ``r``, on the GPU."""
+    r1, r2 = _lib.f64(r.gamma, (pd.n,)), _lib.f64(r.x_mat, (pd.n, pd.n))
+    dc = ctx.decomp
+    dg, dx = np.empty(pd.n), np.empty((pd.n, pd.n))
+    it, met, lhs, rhs = C.c_int(), C.c_int(), C.c_double(), C.c_double()
+    c = cfg_struct(cfg)
+    _lib.check(_lib.lib().kot_newton_direction_decomp(
+        pd.device_problem().handle, C.byref(c), _lib.ptr(r1), _lib.ptr(r2), _lib.ptr(_lib.f64(dc.eigvecs)),
+        _lib.ptr(_lib.f64(dc.eigvals)), dc.n_pos, float(ctx.mu), _lib.ptr(dg), _lib.ptr(dx), C.byref(it),
+        C.byref(met), C.byref(lhs), C.byref(rhs)))
+    return NewtonStep(IteratePair(dg, dx), int(it.value), bool(met.value), float(lhs.value), float(rhs.value))
 
 
 def middle_operator_at(pd: ProblemData, w: IteratePair, theta: float, v, form: str = "reduced"

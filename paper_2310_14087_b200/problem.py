@@ -178,16 +178,15 @@ def assemble(samples_mu: SampleSet, samples_nu: SampleSet, filling: FillingPoint
     for spec, dim in ((spec_x, d), (spec_y, d), (spec_xy, 2 * d)):
         if spec.input_dim != dim:
             raise ValueError(f"kernel expects dimension {spec.input_dim}, got {dim}")
-    if not (spec_x.bandwidth_sq == spec_y.bandwidth_sq == spec_xy.bandwidth_sq):
-        raise NotImplementedError("the device assembly uses one bandwidth (build_kernel_specs)")
     xs, ys = _lib.f64(samples_mu.points), _lib.f64(samples_nu.points)
     if xs.shape[1] != d or ys.shape[1] != d:
         raise ValueError("sample dimension mismatch")
     dev = _lib.default_device() if device is None else device
     h = C.c_void_p(0)
     _lib.check(_lib.lib().kot_assemble(_lib.ptr(xs), xs.shape[0], _lib.ptr(ys), ys.shape[0], _lib.ptr(xt),
-                                       _lib.ptr(yt), l, d, float(spec_x.bandwidth_sq), float(lambda1),
-                                       float(lambda2), dev, C.byref(h)))
+                                       _lib.ptr(yt), l, d, float(spec_x.bandwidth_sq), float(spec_y.bandwidth_sq),
+                                       float(spec_xy.bandwidth_sq), float(lambda1), float(lambda2), dev,
+                                       C.byref(h)))
     dp = DeviceProblem(h.value, dev)
     q, z, r, emb, kmat = np.empty((l, l)), np.empty(l), np.empty((l, l)), np.empty(l), np.empty((l, l))
     _lib.check(_lib.lib().kot_problem_download(dp.handle, _lib.ptr(q), _lib.ptr(z), _lib.ptr(r), _lib.ptr(emb),
@@ -240,22 +239,53 @@ def ot_estimate(pd: ProblemData, gamma_hat) -> float:
     return float(out.value)
 
 
-@dataclass(frozen=True)
-class ResidualInfo:
-    """Spectral summary of the decomposition computed inside residual_parts (device-resident)."""
+def objective_grad(pd: ProblemData, gamma) -> np.ndarray:
+    """(Qγ − z)/(2λ₂) (problem.py:188-189)."""
+    g = _lib.f64(gamma, (pd.n,))
+    out = np.empty(pd.n)
+    _lib.check(_lib.lib().kot_objective_grad(pd.device_problem().handle, _lib.ptr(g), 0, _lib.ptr(out)))
+    return out
 
-    eigvals: np.ndarray
-    n_pos: int
+
+def objective_grad_dir(pd: ProblemData, dgamma) -> np.ndarray:
+    """Qd/(2λ₂) (problem.py:239-241)."""
+    g = _lib.f64(dgamma, (pd.n,))
+    out = np.empty(pd.n)
+    _lib.check(_lib.lib().kot_objective_grad(pd.device_problem().handle, _lib.ptr(g), 1, _lib.ptr(out)))
+    return out
 
 
-def residual_parts(pd: ProblemData, w: IteratePair) -> tuple[IteratePair, ResidualInfo]:
-    """(r1, r2) and the spectrum of Z = sym(X) − (Φ*(γ)+λ₁I) (problem.py:204-214)."""
+def constraint_matrix(pd: ProblemData, gamma) -> np.ndarray:
+    """Φ*(γ) + λ₁I, the matrix whose positive semidefiniteness the dual constrains (problem.py:199-201)."""
+    g = _lib.f64(gamma, (pd.n,))
+    out = np.empty((pd.n, pd.n))
+    _lib.check(_lib.lib().kot_constraint_matrix(pd.device_problem().handle, _lib.ptr(g), _lib.ptr(out)))
+    return out
+
+
+def residual_parts(pd: ProblemData, w: IteratePair) -> tuple[IteratePair, SpectralDecomp]:
+    """(r1, r2) and the eigendecomposition of Z = sym(X) − (Φ*(γ)+λ₁I) (problem.py:204-214)."""
     g, x = _lib.f64(w.gamma, (pd.n,)), _lib.f64(w.x_mat, (pd.n, pd.n))
-    r1, r2, ev = np.empty(pd.n), np.empty((pd.n, pd.n)), np.empty(pd.n)
+    r1, r2, ev, vecs = np.empty(pd.n), np.empty((pd.n, pd.n)), np.empty(pd.n), np.empty((pd.n, pd.n))
     k, res = C.c_int(), C.c_double()
     _lib.check(_lib.lib().kot_residual_parts(pd.device_problem().handle, _lib.ptr(g), _lib.ptr(x), _lib.ptr(r1),
-                                             _lib.ptr(r2), _lib.ptr(ev), C.byref(k), C.byref(res)))
-    return IteratePair(r1, r2), ResidualInfo(ev, int(k.value))
+                                             _lib.ptr(r2), _lib.ptr(ev), C.byref(k), C.byref(res),
+                                             _lib.ptr(vecs)))
+    kk = int(k.value)
+    return IteratePair(r1, r2), SpectralDecomp(eigvecs=vecs, eigvals=ev, pos_idx=np.arange(kk),
+                                               nonpos_idx=np.arange(kk, pd.n))
+
+
+def apply_jacobian(pd: ProblemData, coeffs, mu: float, dw: IteratePair) -> IteratePair:
+    """Regularized generalized Jacobian (J + μI)dw at ``coeffs``' decomposition (problem.py:222-236):
+    top = Qdγ/(2λ₂) + μdγ − Φ(dX), bottom = M[Φ*(dγ) − dX] + (1+μ)dX."""
+    dc = coeffs.decomp
+    dg, dx = _lib.f64(dw.gamma, (pd.n,)), _lib.f64(dw.x_mat, (pd.n, pd.n))
+    top, bottom = np.empty(pd.n), np.empty((pd.n, pd.n))
+    _lib.check(_lib.lib().kot_apply_jacobian(pd.device_problem().handle, _lib.ptr(_lib.f64(dc.eigvecs)),
+                                             _lib.ptr(_lib.f64(dc.eigvals)), dc.n_pos, float(mu), _lib.ptr(dg),
+                                             _lib.ptr(dx), _lib.ptr(top), _lib.ptr(bottom)))
+    return IteratePair(top, bottom)
 
 
 def evaluate_map(pd: ProblemData, samples_mu: SampleSet, gamma_hat, queries) -> tuple[np.ndarray, np.ndarray]:
@@ -288,5 +318,6 @@ def residual(pd: ProblemData, w: IteratePair) -> IteratePair:
 
 
 __all__ = ["FillingPoints", "IteratePair", "ProblemData", "DeviceProblem", "SpectralDecomp", "zero_pair",
-           "build_kernel_specs", "assemble", "phi_forward", "phi_adjoint", "objective", "ot_estimate",
-           "residual_parts", "residual", "ResidualInfo", "evaluate_map", "potential_and_map"]
+           "build_kernel_specs", "assemble", "phi_forward", "phi_adjoint", "objective", "objective_grad",
+           "objective_grad_dir", "constraint_matrix", "ot_estimate", "residual_parts", "residual",
+           "apply_jacobian", "evaluate_map", "potential_and_map"]

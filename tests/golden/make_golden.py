@@ -221,6 +221,73 @@ def gen_small():
     print("small fixtures written")
 
 
+def gen_api():
+    """Reference outputs for the rest of the public surface (kernels, datagen, psdcone decomposition
+    API, apply_jacobian / criterion values, cg_solve, solve_pure_eg, distinct-bandwidth assemble)."""
+    from kot import datagen as kdat
+    from kot import kernels as kker
+    out = {}
+    # datagen (host input generation, datagen.py:49-132)
+    out["mix_points"] = kot.sample_mixture(kdat.default_mixture(3, 4, 7), 50).points
+    fp = kot.sobol_points(6, 37, -1.0, 1.0)
+    out["sobol_xt"], out["sobol_yt"] = fp.x_tilde, fp.y_tilde
+    out["sobol_nat"] = kdat.sobol_natural(5, 3, 20)
+    # kernels (kernels.py:54-94)
+    rng = np.random.default_rng(99)
+    a, b = rng.uniform(-1, 1, (40, 3)), rng.uniform(-1, 1, (25, 3))
+    spec = kker.KernelSpec(0.3, 3)
+    out.update({"k_a": a, "k_b": b, "k_bw": np.float64(0.3), "k_rect": kker.gram_matrix(spec, a, b),
+                "k_square": kker.gram_matrix(spec, a),
+                "k_mean": kker.mean_embedding(spec, kot.SampleSet(a), b),
+                "k_mean_at": np.float64(kker.mean_embedding_at(spec, kot.SampleSet(a), b[3])),
+                "k_norm": np.float64(kker.embedding_norm_sq(spec, kot.SampleSet(a))),
+                "k_eval": np.float64(kker.kernel_eval(spec, a[0], b[0]))})
+    # assemble with three different bandwidths (problem.py:135-169)
+    wl = configs.config1()
+    sx, sy, sxy = kker.KernelSpec(0.25, 2), kker.KernelSpec(0.4, 2), kker.KernelSpec(0.6, 4)
+    pd3 = kprob.assemble(kot.SampleSet(wl.xs), kot.SampleSet(wl.ys), kprob.FillingPoints(wl.xt, wl.yt),
+                         wl.lambda1, wl.lambda2, sx, sy, sxy)
+    out.update(_pd_arrays(pd3, "bw3_"))
+    # operators at cfg1's replay state 10 through the decomposition API
+    sx, sy, sxy = kprob.build_kernel_specs(wl.d, wl.bandwidth_sq)
+    pd = kprob.assemble(kot.SampleSet(wl.xs), kot.SampleSet(wl.ys), kprob.FillingPoints(wl.xt, wl.yt),
+                        wl.lambda1, wl.lambda2, sx, sy, sxy)
+    cfg1 = dict(np.load(os.path.join(HERE, "cfg1.npz")))
+    w = kprob.IteratePair(cfg1["op_g"], cfg1["op_x"])
+    r, dc = kprob.residual_parts(pd, w)
+    ctx = knew.newton_context(dc, r.norm(), float(cfg1["op_theta"]))
+    dw = kprob.IteratePair(cfg1["op_dir_dg"], cfg1["op_dir_dx"])
+    jd = kprob.apply_jacobian(pd, ctx.coeffs, ctx.mu, dw)
+    out.update({"jac_top": jd.gamma, "jac_bottom": jd.x_mat,
+                "crit_lhs": np.float64((jd + r).norm()),
+                "crit_rhs": np.float64(0.5 * min(1.0, 0.1 * r.norm() * dw.norm())),
+                "grad": kprob.objective_grad(pd, cfg1["op_g"]),
+                "grad_dir": kprob.objective_grad_dir(pd, cfg1["op_v"]),
+                "cmat": kprob.constraint_matrix(pd, cfg1["op_g"])})
+    st = knew.newton_direction(pd, r, ctx, knew.NewtonConfig(cg_tol=1e-13, cg_max=3000, cg_restarts=0))
+    out.update({"dirc_dg": st.dw.gamma, "dirc_dx": st.dw.x_mat, "dirc_rhs": np.float64(st.crit_rhs)})
+    # cg_solve (linalg.py:117-162): the middle operator and a plain SPD matrix
+    x, it, res = klin.cg_solve(knew.middle_operator(pd, ctx.eliminator, ctx.mu), cfg1["op_v"], 1e-12, 500)
+    out.update({"cgm_x": x, "cgm_iters": np.int64(it), "cgm_res": np.float64(res)})
+    m = rng.standard_normal((30, 30))
+    spd = m @ m.T / 30 + 0.1 * np.eye(30)
+    rhs = rng.standard_normal(30)
+    x, it, res = klin.cg_solve(lambda v: spd @ v, rhs, 1e-10, 200)
+    out.update({"cg_a": spd, "cg_b": rhs, "cg_x": x, "cg_iters": np.int64(it), "cg_res": np.float64(res)})
+    # solve_pure_eg (solver.py:236-289)
+    step = float(cfg1["eg_stepsize"])
+    rep = ksol.solve_pure_eg(pd, ksol.SolverConfig(eg=keg.EgConfig(stepsize=step), residual_tol=1e-12, max_iter=30))
+    out.update({"peg_gamma": rep.gamma_hat, "peg_x": rep.x_hat, "peg_iters": np.int64(rep.iterations),
+                "peg_res": np.array([t.res_accepted for t in rep.trace])})
+    np.savez_compressed(os.path.join(HERE, "api.npz"), **out)
+    print("api fixtures written")
+
+
 if __name__ == "__main__":
-    gen_small()
-    gen_cfg1()
+    which = sys.argv[1:] or ["small", "cfg1", "api"]
+    if "small" in which:
+        gen_small()
+    if "cfg1" in which:
+        gen_cfg1()
+    if "api" in which:
+        gen_api()
