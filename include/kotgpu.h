@@ -122,6 +122,8 @@ int kot_session_begin(kot_problem* p, const kot_solver_cfg* cfg, kot_session** o
 int kot_session_step(kot_session* s, int iters, kot_iter_record* recs /* nullable */, int* done);
 int kot_session_result(kot_session* s, double* gamma_out, double* x_out, kot_report* out);
 void kot_session_end(kot_session* s);
+/* loop state between two iterations (any pointer may be NULL): w, the safeguard iterate v, theta */
+int kot_session_state(kot_session* s, double* w_gamma, double* w_x, double* v_gamma, double* v_x, double* theta);
 /* the cudaStream_t (as void*) every kernel of this problem is launched on */
 void* kot_problem_stream(kot_problem* p);
 

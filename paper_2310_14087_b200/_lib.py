@@ -75,6 +75,7 @@ _SIGS = {
     "kot_session_step": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(IterRecordC), iptr]),
     "kot_session_result": (C.c_int, [C.c_void_p, dptr, dptr, C.POINTER(ReportC)]),
     "kot_session_end": (None, [C.c_void_p]),
+    "kot_session_state": (C.c_int, [C.c_void_p, dptr, dptr, dptr, dptr, dptr]),
     "kot_problem_stream": (C.c_void_p, [C.c_void_p]),
     "kot_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "kot_problem_shard": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_int]),

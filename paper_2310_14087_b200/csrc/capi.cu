@@ -215,6 +215,13 @@ int kot_session_result(kot_session* s, double* gamma_out, double* x_out, kot_rep
   });
 }
 
+int kot_session_state(kot_session* s, double* w_gamma, double* w_x, double* v_gamma, double* v_x, double* theta) {
+  return guarded([&] {
+    KOT_CUDA(cudaSetDevice(s->h->p->device));
+    kot::session_state(*s->s, w_gamma, w_x, v_gamma, v_x, theta);
+  });
+}
+
 void kot_session_end(kot_session* s) {
   if (!s) return;
   kot::session_end(s->s);

@@ -6,6 +6,7 @@
 // Control flow, tie-breaking and error conditions follow the reference line
 // by line; all vectors/matrices stay in HBM and only the scalars that steer
 // the control flow (norms, pAp, flags) cross to the host.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
@@ -925,6 +926,27 @@ void session_result(Session& se, double* gamma, double* x, SolveResult& out) {
   if (x) KOT_CUDA(cudaMemcpyAsync(x, b.Xw, sizeof(double) * (long)p.n * p.n, cudaMemcpyDeviceToHost, p.st));
   KOT_CUDA(cudaStreamSynchronize(p.st));
   out.total_ms = 0.0;
+}
+
+// Loop state between two iterations: w, the current safeguard iterate v (the slot consumed by the
+// last iteration; (0, 0) before the first) and θ — the oracle's State(w, v, θ) for a CPU replay.
+void session_state(Session& se, double* wg, double* wx, double* vg, double* vx, double* theta) {
+  Problem& p = *se.p;
+  Bufs& b = p.bufs();
+  const int n = p.n;
+  const long nn = (long)n * n;
+  if (wg) KOT_CUDA(cudaMemcpyAsync(wg, b.gw, sizeof(double) * n, cudaMemcpyDeviceToHost, p.st));
+  if (wx) KOT_CUDA(cudaMemcpyAsync(wx, b.Xw, sizeof(double) * nn, cudaMemcpyDeviceToHost, p.st));
+  const EgSlot* v = se.s.vslot;
+  if (v) {
+    if (vg) KOT_CUDA(cudaMemcpyAsync(vg, v->g, sizeof(double) * n, cudaMemcpyDeviceToHost, p.st));
+    if (vx) KOT_CUDA(cudaMemcpyAsync(vx, v->X, sizeof(double) * nn, cudaMemcpyDeviceToHost, p.st));
+  } else {
+    if (vg) std::fill(vg, vg + n, 0.0);
+    if (vx) std::fill(vx, vx + nn, 0.0);
+  }
+  KOT_CUDA(cudaStreamSynchronize(p.st));
+  if (theta) *theta = se.s.theta;
 }
 
 void session_end(Session* se) { delete se; }

@@ -228,5 +228,6 @@ Session* session_begin(Problem& p, const SolverCfg& cfg);
 int session_step(Session& se, int iters, IterRecord* recs);
 void session_result(Session& se, double* gamma, double* x, SolveResult& out);
 void session_end(Session* se);
+void session_state(Session& se, double* wg, double* wx, double* vg, double* vx, double* theta);
 
 }  // namespace kot

@@ -216,6 +216,15 @@ class Session:
         return SolverReport(gamma, x, ot, float(rep.residual_norm), CONVERGED if rep.converged else MAX_ITER,
                             list(self.records), float("nan"))
 
+    def state(self):
+        """(w, v, θ) between two iterations (host copies)."""
+        n = self.pd.n
+        wg, wx, vg, vx = np.empty(n), np.empty((n, n)), np.empty(n), np.empty((n, n))
+        th = C.c_double()
+        _lib.check(_lib.lib().kot_session_state(self._h, _lib.ptr(wg), _lib.ptr(wx), _lib.ptr(vg), _lib.ptr(vx),
+                                                C.byref(th)))
+        return IteratePair(wg, wx), IteratePair(vg, vx), float(th.value)
+
     def close(self):
         if self._h:
             _lib.lib().kot_session_end(self._h)
