@@ -9,16 +9,25 @@ configs[2]: d=10, n=ℓ=2000, σ=1.5, λ1=1e-4, λ2=1/ℓ, FP64), paper profile
 (``NewtonConfig()`` defaults), EG stepsize 0.5/(‖Q‖_F/(2λ2)+‖K‖_F)
 (SURVEY.md §8(d)).  Synthetic seeded data (the reference ships none).
 
-* ``value``: iterations/s over the K timed iterations, inputs resident in HBM,
-  timed with CUDA events on the library's stream, barrier + synchronize on both
-  sides, max over ranks; N>1 runs N independent replicas (single problems do not
-  shard: SURVEY.md §8(e) "configs 1-3: replicas only") → ``scaling: weak``.
-* ``e2e``: the same metric through the public API ``solve(ProblemData)`` from
-  host arrays — H2D of the instance and D2H of (γ̂, X̂) inside the timed region.
+* ``value``: iterations/s over the K timed iterations W … W+K−1, inputs resident
+  in HBM, timed with CUDA events on the library's stream, barrier + synchronize on
+  both sides, max over ranks; N>1 runs N independent replicas (single problems do
+  not shard: SURVEY.md §8(e) "configs 1-3: replicas only") → ``scaling: weak``.
+* ``e2e``: the same iterations W … W+K−1 through the public API, measured FIRST in
+  the process (fresh device allocations): ``assemble`` from the host sample arrays
+  and ``solve(pd, max_iter=W+K)`` with the D2H of (γ̂, X̂), all inside the timed
+  region; the W warm-up iterations' own step times are subtracted, so the window
+  matches ``value`` and the reference arm (assembly, upload, allocation, setup,
+  initial residual and download stay in).
 * ``roofline``: the dominant kernel (live CUDA-event timing inside libkotgpu's
-  phase profiler), against MEASURED_PEAKS.json / the measured DMMA peak.
+  phase profiler), against MEASURED_PEAKS.json / the measured DMMA peak;
+  ``traffic`` is read from the committed ncu capture (profiles/r02/roofline_traffic.json).
 * ``cpu_baseline``: the NumPy oracle (oracle/, a restatement of the reference)
-  on this box's host cores for a bounded sample (1 SSN iteration).
+  on this box's host cores for a bounded sample of the same window: 2 SSN
+  iterations from the GPU trajectory's own state at iteration W.
+* ``time_to_tol``: BASELINE's time-to-tolerance half at cfg3, tight profile:
+  assemble + solve from host arrays to 5e-3 (first hit, solver.py:221-222) and
+  to 1e-6 within a stated max_iter (the residual reached when not hit).
 * ``--impl reference``: the reference's CPU algorithm (the oracle port; the
   reference is pure Python and cannot be installed on the box) on the same config.
 """
@@ -39,7 +48,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 DMMA_PEAK_TFLOPS = 37.12  # measured, profiles/r01/fp64_peak_microbench.txt (mma.sync m8n8k4 f64)
-SYTRD_TRAFFIC_BYTES = 14.866176e6 + 8.448e3  # ncu --set full, profiles/r01/ncu_full_r01_summary.txt
 
 
 def peaks():
@@ -234,25 +242,43 @@ def run_reference(args):
 
 # --------------------------------------------------------------------- GPU leg
 
-def time_to_tol(K, configs, seed: int = 0, tol: float = 1e-6) -> dict:
-    """assemble + solve from host arrays to ‖R‖ ≤ tol on the config-5 member with seed 0 (ℓ = n = 1000,
-    σ = 0.5), tight profile — the reference's survey measured 256 s / 168 iterations on 8 cores
-    (BASELINE.md §2); at ℓ = 2000 1e-6 is out of reach for the reference and, within 1500 SSN
-    iterations, for this solver too."""
-    wl = configs.config5_member(seed)
+def _first_hit_ms(rep, tol: float):
+    """(iteration, ms since the call started) of the first accepted iterate with ‖R‖ ≤ tol, from the
+    trace's per-iteration step times; the setup before iteration 0 is total_ms − Σ step_ms."""
+    steps = [r.step_ms for r in rep.trace]
+    setup = rep.total_ms - sum(steps)
+    t = setup
+    for i, r in enumerate(rep.trace):
+        t += r.step_ms
+        if r.res_accepted <= tol:
+            return i + 1, t
+    return None, None
+
+
+def time_to_tol(K, configs, wl, max_iter: int) -> dict:
+    """BASELINE metric, first half: time-to-tolerance at the headline config (cfg3, tight profile,
+    SURVEY.md §8(d)), through the public API from host arrays.  One solve to 5e-3 (the paper's
+    threshold; solve stops at the first accepted iterate below tol, solver.py:221-222) and one to 1e-6
+    with max_iter stated; when 1e-6 is not reached the residual at max_iter is reported (never the
+    best residual seen)."""
+    out = {"workload": f"{wl.name}, tight profile (alpha1=1e-8, alpha2=1e-4, cg_max=500), assemble + solve "
+                       "from host arrays"}
     sx, sy, sxy = K.build_kernel_specs(wl.d, wl.bandwidth_sq)
-    t0 = time.perf_counter()
-    pd = K.assemble(K.SampleSet(wl.xs), K.SampleSet(wl.ys), K.FillingPoints(wl.xt, wl.yt), wl.lambda1,
-                    wl.lambda2, sx, sy, sxy)
-    step = configs.eg_stepsize(pd.q_mat, pd.pair_gram(), pd.lambda2)
-    cfg = K.SolverConfig(newton=K.NewtonConfig(**configs.PROFILES["tight"]), eg=K.EgConfig(step), residual_tol=tol,
-                         max_iter=1000)
-    rep = K.solve(pd, cfg)
-    dt = time.perf_counter() - t0
-    return {"seconds": dt, "iterations": rep.iterations, "converged": rep.termination == "converged",
-            "residual": rep.residual_norm, "workload": f"config 5 member seed {seed} (n=l=1000, d=10, sigma=0.5), "
-            "tight profile, assemble + solve from host arrays",
-            "reference_survey": "256 s, 168 iterations (8 host cores, BASELINE.md section 2)"}
+    for tol, cap in ((5e-3, max_iter), (1e-6, max_iter)):
+        t0 = time.perf_counter()
+        pd = K.assemble(K.SampleSet(wl.xs), K.SampleSet(wl.ys), K.FillingPoints(wl.xt, wl.yt), wl.lambda1,
+                        wl.lambda2, sx, sy, sxy)
+        step = configs.eg_stepsize(pd.q_mat, pd.pair_gram(), pd.lambda2)
+        cfg = K.SolverConfig(newton=K.NewtonConfig(**configs.PROFILES["tight"]), eg=K.EgConfig(step),
+                             residual_tol=tol, max_iter=cap)
+        rep = K.solve(pd, cfg)
+        dt = time.perf_counter() - t0
+        hit = rep.termination == "converged"
+        out[f"{tol:g}"] = {"reached": hit, "seconds": dt, "iterations": rep.iterations, "max_iter": cap,
+                           "residual": rep.residual_norm,
+                           "cg_iters_per_iteration": sum(r.cg_iters for r in rep.trace) / max(rep.iterations, 1)}
+        pd.release_device()
+    return out
 
 
 def run_gpu(args):
@@ -264,25 +290,57 @@ def run_gpu(args):
     from paper_2310_14087_b200 import _lib, configs, solver
 
     torch.cuda.set_device(local)
+    torch.cuda.init()
+    _lib.lib()  # library load (process setup, not part of any timed region)
     wl = workload(args.config)
     sx, sy, sxy = K.build_kernel_specs(wl.d, wl.bandwidth_sq)
-    pd = K.assemble(K.SampleSet(wl.xs), K.SampleSet(wl.ys), K.FillingPoints(wl.xt, wl.yt), wl.lambda1,
-                    wl.lambda2, sx, sy, sxy, device=local)
-    stepsize = configs.eg_stepsize(pd.q_mat, pd.pair_gram(), pd.lambda2)
-    cfg = K.SolverConfig(newton=newton_cfg(args.profile), eg=K.EgConfig(stepsize), residual_tol=1e-300,
-                         max_iter=10 ** 6)
     # config 4 (l = 8192): one problem, CG matvec row-sharded over the ranks (NCCL), strong scaling;
     # every other config runs one independent replica per rank
     rowshard = args.config.startswith("cfg4") and world > 1
     if rowshard:
         from paper_2310_14087_b200 import rowshard as RS
+
+    # ---------------- end to end through the public API from host arrays (e2e), first in the process
+    torch.cuda.synchronize()
+    barrier(world)
+    n_e2e = args.warmup + args.steps
+    t0 = time.perf_counter()
+    pd = K.assemble(K.SampleSet(wl.xs), K.SampleSet(wl.ys), K.FillingPoints(wl.xt, wl.yt), wl.lambda1,
+                    wl.lambda2, sx, sy, sxy, device=local)
+    t_asm = time.perf_counter() - t0
+    stepsize = configs.eg_stepsize(pd.q_mat, pd.pair_gram(), pd.lambda2)
+    if rowshard:  # NCCL communicator setup inside the timed region
         RS.shard_rows(pd)
+    cfg_e = K.SolverConfig(newton=newton_cfg(args.profile), eg=K.EgConfig(stepsize), residual_tol=1e-300,
+                           max_iter=n_e2e)
+    rep = K.solve(pd, cfg_e)
+    torch.cuda.synchronize()
+    t_call = time.perf_counter() - t0
+    warm_ms = sum(r.step_ms for r in rep.trace[:args.warmup])
+    t_e2e = t_call - warm_ms / 1e3
+    barrier(world)
+    t_e2e = max_over_ranks(world, t_e2e, local)
+    e2e_iters = float(rep.iterations - args.warmup)
+    e2e_iters = e2e_iters if rowshard else sum_over_ranks(world, e2e_iters, local)
+    n = pd.n
+    # per step: the instance's host arrays up (samples + filling points for assemble), γ̂, X̂ and the trace down
+    h2d = 8.0 * (wl.xs.size + wl.ys.size + wl.xt.size + wl.yt.size) / args.steps
+    d2h = ((n * n + n) * 8 + rep.iterations * 8 * 18) / args.steps
+    e2e = {"value": e2e_iters / t_e2e, "unit": "iter/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "api": "paper_2310_14087_b200.assemble(host samples) + solve(pd, max_iter=W+K) -> gamma_hat, x_hat",
+           "window": f"iterations {args.warmup}..{n_e2e - 1}; timed region = the whole call minus the "
+                     f"{args.warmup} warm-up iterations' own step time ({warm_ms:.1f} ms)",
+           "first_solve_in_process": True, "wall_ms": round(t_call * 1e3, 1), "assemble_ms": round(t_asm * 1e3, 1),
+           "setup_ms": round(rep.total_ms - sum(r.step_ms for r in rep.trace), 1)}
 
     # ---------------- device-resident timed region (value)
+    cfg = K.SolverConfig(newton=newton_cfg(args.profile), eg=K.EgConfig(stepsize), residual_tol=1e-300,
+                         max_iter=10 ** 6)
     se = solver.Session(pd, cfg)
     stream = torch.cuda.ExternalStream(se.stream, device=f"cuda:{local}")
     for _ in range(args.warmup):
         se.step(1)
+    state_w = se.state() if (world == 1 and not args.no_cpu_baseline) else None
     torch.cuda.synchronize()
     barrier(world)
     l0 = _lib.launch_count()
@@ -306,103 +364,28 @@ def run_gpu(args):
     launches = _lib.launch_count() - l0
     recs = se.records[args.warmup:]
     se.close()
+    pd.release_device()
     ms_max = max_over_ranks(world, ms, local)
     total_iters = float(done) if rowshard else sum_over_ranks(world, float(done), local)
     value = total_iters / (ms_max / 1e3)
 
-    # ---------------- end to end through the public API from host buffers (e2e)
-    pd_host = K.ProblemData(q_mat=pd.q_mat.copy(), z=pd.z.copy(), q_sq=pd.q_sq, chol_upper=pd.chol_upper.copy(),
-                            lambda1=pd.lambda1, lambda2=pd.lambda2, embed_sum=pd.embed_sum.copy())
-    # the instance above is done with: its device problem (with all workspace) goes back to the
-    # library's pool and the e2e instance reuses it, as for a user who solves one problem after
-    # another in one process; upload, setup, initial residual and download stay in the timed region
-    pd.release_device()
-    cfg_e = K.SolverConfig(newton=newton_cfg(args.profile), eg=K.EgConfig(stepsize), residual_tol=1e-300,
-                           max_iter=args.steps)
-    debug = bool(os.environ.get("KOT_BENCH_DEBUG"))
-    torch.cuda.synchronize()
-    barrier(world)
-    if debug:
-        _lib.profile_enable(True)
-    t0 = time.perf_counter()
-    if rowshard:  # upload + NCCL communicator setup inside the timed region
-        RS.shard_rows(pd_host)
-    rep = K.solve(pd_host, cfg_e)
-    torch.cuda.synchronize()
-    t_e2e = time.perf_counter() - t0
-    if debug:
-        hp = {k: round(v["ms"], 1) for k, v in _lib.profile_read().items() if k.startswith("solve.")}
-        _lib.profile_enable(False)
-        print(f"e2e: {t_e2e * 1e3:.1f} ms, solve total_ms {rep.total_ms:.1f} {hp}, steps "
-              f"{[round(r.step_ms) for r in rep.trace]} {''.join(r.accepted[0] for r in rep.trace)}", file=sys.stderr, flush=True)
-    barrier(world)
-    t_e2e = max_over_ranks(world, t_e2e, local)
-    n = pd.n
-    e2e_iters = float(rep.iterations) if rowshard else sum_over_ranks(world, float(rep.iterations), local)
-    h2d = (2 * n * n + 2 * n) * 8 / max(rep.iterations, 1)
-    d2h = ((n * n + n) * 8 + rep.iterations * 8 * 16) / max(rep.iterations, 1)
-
     if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
         return 0
 
-    # ---------------- roofline of the dominant kernel
-    # Dominant by serialized kernel time (ncu launch list, profiles/): the cooperative Householder
-    # panel kernel of the eigensolver.  The live CUDA-event timing below is per launch on the stream
-    # it runs on; the GEMM core is reported as a secondary roofline.
-    hbm, peak_kind = peaks()
-    roof = roof_gemm = None
-    if "sytrd_panel" in prof:
-        e = prof["sytrd_panel"]
-        ach = e["bytes"] / e["calls"] / (e["ms"] / e["calls"] * 1e-3) / 1e9
-        roof = {"kernel": "sytrd_panel_kernel (cooperative Householder panel: column update + symv)",
-                "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": SYTRD_TRAFFIC_BYTES, "traffic_note": "ncu --set full, one mid panel launch at l=2000 "
-                "(dram read+write; the trailing matrix is L2-resident)",
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                "algorithmic": "per launch: sum over its 32 columns of one lower-triangle read of the "
-                               "trailing matrix, 8*m(m+1)/2 B",
-                "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"],
-                "sampled": None if os.environ.get("KOT_BENCH_PROFILE") == "full" else
-                "1 in 16 launches (time and algorithmic bytes of the same launches)",
-                "note": "latency-bound: 2 grid barriers + ~4 dependent L2 round trips per column"}
-    if roof is None and "eig.q2" in prof:  # two-stage path (l >= 3000): the tensor-core Q2 back-transform
-        e = prof["eig.q2"]
-        ach = e["flops"] / (e["ms"] * 1e-3) / 1e12
-        roof = {"kernel": "q2_wave_kernel sequence (two-stage eigensolver, stage-2 back-transform, mma m8n8k4 f64)",
-                "bound": "tensor", "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": ach / DMMA_PEAK_TFLOPS, "traffic": None,
-                "algorithmic": "2 l^3 FLOPs per eigensolve (the applied reflectors' useful work; the banded blocks "
-                               "execute about 2.5x that)",
-                "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"],
-                "note": "timed per eigensolve (one Q2 application = one wave sequence)"}
-    if "gemm_dmma" in prof:
-        e = prof["gemm_dmma"]
-        ach = e["flops"] / (e["ms"] * 1e-3) / 1e12
-        roof_gemm = {"kernel": "gemm_dmma_kernel (mma.sync m8n8k4 f64, all shapes)", "bound": "tensor",
-                     "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
-                     "traffic": None, "peak_source": "measured DMMA microbenchmark (MEASURED_PEAKS.json has no FP64)",
-                     "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"],
-                     "sampled": None if os.environ.get("KOT_BENCH_PROFILE") == "full" else "1 in 128 launches"}
-    full = os.environ.get("KOT_BENCH_PROFILE") == "full"
-    phases = {k: {"ms_per_step": v["ms"] / max(done, 1), "calls_per_step": v["calls"] / max(done, 1),
-                  **({"tflops": v["flops"] / (v["ms"] * 1e-3) / 1e12} if v["flops"] and v["ms"] else {}),
-                  **({"sampled": {"gemm_dmma": "1 in 128 launches", "sytrd_panel": "1 in 16 launches"}[k]}
-                     if k in ("gemm_dmma", "sytrd_panel") and not full else {})}
-              for k, v in prof.items()}
+    roof, roof_gemm, phases = roofline(prof, done)
 
-    # ---------------- CPU baseline (oracle port, bounded sample)
+    # ---------------- CPU baseline (oracle port, bounded sample of the same window)
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        v, dt, extra = oracle_iters_per_s(wl, args.profile, 0, 3)
-        ci = cpu_info()
-        cpu = {"value": v, "unit": "iter/s", "cores": ci["cores"], "kind": "port",
-               "sample": f"the first 3 SSN iterations (from the zero pair) of {wl.name}, NumPy/OpenBLAS oracle "
-                         f"with {ci['blas_threads']} BLAS threads; {dt:.1f} s", "cpu": ci["cpu"]}
+    if state_w is not None:
+        cpu = cpu_baseline_from_state(wl, args.profile, state_w, args.warmup, 2, stepsize)
 
-    # ---------------- time-to-1e-6 (BASELINE metric, first half), through the public API
+    # ---------------- time-to-tolerance at the headline config (BASELINE metric, first half)
     ttt = None
     if world == 1 and not args.no_ttt:
-        ttt = time_to_tol(K, configs)
+        ttt = time_to_tol(K, configs, wl, args.ttt_max_iter)
 
     line = {
         "metric": f"SSN iters/s at n=l={wl.l} FP64 ({args.profile} profile)",
@@ -410,19 +393,15 @@ def run_gpu(args):
         "ms_per_step": ms_max / max(done, 1), "higher_is_better": True,
         "scaling": "strong" if rowshard else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {**describe(wl, args.profile),
-                   "parallelism": f"rowshard{world} (CG matvec rows over NCCL)" if rowshard else f"replicas{world}"},
-        "e2e": {"value": e2e_iters / t_e2e, "unit": "iter/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "api": "paper_2310_14087_b200.solve(ProblemData from host arrays)",
-                "iterations": rep.iterations, "wall_ms": round(t_e2e * 1e3, 1),
-                "solve_ms": round(rep.total_ms, 1),
-                "iterations_ms": round(sum(r.step_ms for r in rep.trace), 1)},
+        "config": describe(wl, args.profile),
+        "parallelism": f"rowshard{world} (CG matvec rows over NCCL)" if rowshard else f"replicas{world}",
+        "e2e": e2e,
         "gpu_launches": int(launches),
         "roofline": roof,
         "roofline_gemm": roof_gemm,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
-        "time_to_1e-6": ttt,
+        "time_to_tol": ttt,
         "phases": phases,
         "trace": {"res": [r.res_accepted for r in recs][:64], "cg_iters": [r.cg_iters for r in recs][:64],
                   "n_pos": [r.n_pos for r in recs][:64]},
@@ -432,6 +411,81 @@ def run_gpu(args):
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def load_traffic() -> dict:
+    """ncu --set full per-launch DRAM bytes of the roofline kernels (profiles/r02/roofline_traffic.json,
+    written from the committed capture by tools/ncu_traffic.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "roofline_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def roofline(prof: dict, done: int):
+    """Roofline of the dominant kernel (+ the GEMM core) from the live phase profiler."""
+    hbm, peak_kind = peaks()
+    traffic = load_traffic()
+    roof = roof_gemm = None
+    full = os.environ.get("KOT_BENCH_PROFILE") == "full"
+    if "sytrd_panel" in prof:
+        e = prof["sytrd_panel"]
+        ach = e["bytes"] / e["calls"] / (e["ms"] / e["calls"] * 1e-3) / 1e9
+        t = traffic.get("sytrd_panel_kernel", {})
+        roof = {"kernel": "sytrd_panel_kernel (cooperative Householder panel: column update + symv)",
+                "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": t.get("dram_bytes_per_launch"), "traffic_source": t.get("source"),
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "algorithmic": "per launch: sum over its 32 columns of one lower-triangle read of the "
+                               "trailing matrix, 8*m(m+1)/2 B",
+                "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"],
+                "sampled": None if full else "1 in 16 launches (time and algorithmic bytes of the same launches)"}
+    if roof is None and "eig.q2" in prof:  # two-stage path (l >= 3000): the tensor-core Q2 back-transform
+        e = prof["eig.q2"]
+        ach = e["flops"] / (e["ms"] * 1e-3) / 1e12
+        roof = {"kernel": "q2_wave_kernel sequence (two-stage eigensolver, stage-2 back-transform, mma m8n8k4 f64)",
+                "bound": "tensor", "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": ach / DMMA_PEAK_TFLOPS, "traffic": None,
+                "algorithmic": "2 l^3 FLOPs per eigensolve (the applied reflectors' useful work)",
+                "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"]}
+    if "gemm_dmma" in prof:
+        e = prof["gemm_dmma"]
+        ach = e["flops"] / (e["ms"] * 1e-3) / 1e12
+        roof_gemm = {"kernel": "gemm_dmma_kernel (mma.sync m8n8k4 f64, all shapes)", "bound": "tensor",
+                     "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
+                     "traffic": None, "peak_source": "measured DMMA microbenchmark (MEASURED_PEAKS.json has no FP64)",
+                     "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"],
+                     "sampled": None if full else "1 in 128 launches"}
+    phases = {k: {"ms_per_step": v["ms"] / max(done, 1), "calls_per_step": v["calls"] / max(done, 1),
+                  **({"tflops": v["flops"] / (v["ms"] * 1e-3) / 1e12} if v["flops"] and v["ms"] else {}),
+                  **({"sampled": {"gemm_dmma": "1 in 128 launches", "sytrd_panel": "1 in 16 launches"}[k]}
+                     if k in ("gemm_dmma", "sytrd_panel") and not full else {})}
+              for k, v in prof.items()}
+    return roof, roof_gemm, phases
+
+
+def cpu_baseline_from_state(wl, profile: str, state, k0: int, iters: int, stepsize: float) -> dict:
+    """The oracle (reference restatement) timed for `iters` SSN iterations from the GPU trajectory's
+    state at iteration k0 — the same window as `value` and the reference arm, bounded to ~10-30 s."""
+    from oracle import kot_port as O
+    from paper_2310_14087_b200 import configs
+    pd, _ = oracle_problem(wl)
+    cfg = O.SolverCfg(newton=O.NewtonCfg(**configs.PROFILES[profile]), eg_stepsize=stepsize, residual_tol=1e-300,
+                      max_iter=10 ** 9)
+    w, v, theta = state
+    ow = O.Pair(w.gamma.copy(), w.x_mat.copy())
+    r_w, dc_w = O.residual_parts(pd, ow)
+    st = O.State(ow, O.Pair(v.gamma.copy(), v.x_mat.copy()), r_w, dc_w, r_w.norm(), None, None, r_w.norm(), theta)
+    t0 = time.perf_counter()
+    for k in range(k0, k0 + iters):
+        st, _, _ = O.iterate_once(pd, st, k, cfg)
+    dt = time.perf_counter() - t0
+    ci = cpu_info()
+    return {"value": iters / dt, "unit": "iter/s", "cores": ci["cores"], "kind": "port",
+            "sample": f"SSN iterations {k0}..{k0 + iters - 1} of {wl.name} from the GPU trajectory's state at "
+                      f"iteration {k0}, NumPy/OpenBLAS oracle with {ci['blas_threads']} BLAS threads; {dt:.1f} s",
+            "cpu": ci["cpu"]}
 
 
 def run_batch(args):
@@ -458,12 +512,12 @@ def run_batch(args):
     l0 = _lib.launch_count()
     with ClockSampler(local) as clocks:
         t0 = time.perf_counter()
-        res = batch.run_local(mine, lambda s: batch.gpu_solve_member(s, kw, local), args.concurrency)
+        allr = batch.run_and_gather(mine, lambda s: batch.gpu_solve_member(s, kw, local), args.concurrency, 1000,
+                                    world, rank, device=f"cuda:{local}" if world > 1 else None)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
     launches = _lib.launch_count() - l0
     dt_max = max_over_ranks(world, dt, local)
-    allr = batch.gather_to_root(res, 1000, world, rank, device=f"cuda:{local}" if world > 1 else None)
     if rank != 0:
         return 0
     conv = sum(r.converged for r in allr)
@@ -478,7 +532,10 @@ def run_batch(args):
         "e2e": {"value": len(allr) / dt_max, "unit": "problems/s", "api": "batch.gpu_solve_member (assemble+solve)",
                 "h2d_bytes_per_step": 8 * 1000 * 40, "d2h_bytes_per_step": 8 * (1000 + 16)},
         "gpu_launches": int(launches), "converged": int(conv),
-        "iterations": [r.iterations for r in allr], "clocks": clocks.summary(),
+        "converged_by_sigma": {str(sg): sum(r.converged for r in allr if r.seed % 4 == g)
+                               for g, sg in enumerate((0.5, 1.0, 1.5, 2.0))},
+        "iterations": [r.iterations for r in allr], "residuals": [r.residual_norm for r in allr],
+        "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -496,7 +553,8 @@ def main():
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--profile", default="paper", choices=["paper", "tight"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-6 leg")
+    ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tolerance leg")
+    ap.add_argument("--ttt-max-iter", type=int, default=300, help="max_iter of the time-to-tolerance solves")
     ap.add_argument("--no-profile", action="store_true", help="diagnostic: no phase profiler in the timed region")
     ap.add_argument("--batch", type=int, default=16, help="cfg5: number of problems")
     ap.add_argument("--concurrency", type=int, default=6, help="cfg5: concurrent solves per GPU")
