@@ -164,6 +164,7 @@ int kot_profile_read(kot_prof_entry* out, int cap);  /* returns #entries */
 /* ---- test / diagnostic hooks (process-wide; not part of the drop-in surface) ---- */
 int kot_debug_eig_stages(int stages);   /* 0 automatic, 1 one-stage, 2 two-stage, 3 two-stage in background */
 int kot_debug_cg_batch(int batch);      /* CG iterations enqueued per host check (>= 1; default 4) */
+int kot_debug_gemm_tma(int mode);       /* 1: TMA-staged DMMA GEMM core (default), 0: the cp.async core */
 int kot_debug_eg_parallel(int on);      /* EG-step projections side by side (1, default) or in sequence */
 int kot_debug_sytrd_timing(int on, unsigned long long* out8);  /* panel-kernel segment timers (ns) */
 int kot_debug_tail_timing(int on, unsigned long long* out8);   /* cluster-tail segment timers (ns) */

@@ -379,8 +379,32 @@ void gemm_launch_tiled(const GemmShape& s, const Epi& epi, cudaStream_t st) {
   }
 }
 
+}  // namespace kot
+#include "gemm_tma.cuh"
+namespace kot {
+
+// TMA path on/off (KOT_GEMM_TMA=0 forces the cp.async core; kot_debug_gemm_tma switches at run time)
+inline std::atomic<int>& gemm_tma_mode() {
+  static std::atomic<int> mode{[] {
+    const char* e = std::getenv("KOT_GEMM_TMA");
+    return e ? std::atoi(e) : 1;
+  }()};
+  return mode;
+}
+
 template <bool TA, bool TB, class Epi>
 void gemm_launch(const GemmShape& s, const Epi& epi, cudaStream_t st) {
+  const int mode = gemm_tma_mode().load(std::memory_order_relaxed);
+  // the TMA core from a tile's worth of K on; small / device-sized launches keep the cp.async core
+  // (measured on B200, tools/gemmbench/gemm_tma_bench.cu: 64×64 CTA tiles of four 32×32 warps for
+  // everything — NN 2000³ 32.7 TF/s vs 27.2 on the cp.async core, cuBLAS 33.0 — except the row-dot
+  // products, whose tall M×(k) shapes prefer 128×64 with eight warps: CG matvec GEMM2 27.8 vs 22.5)
+  if (mode > 0 && s.K >= 2 * TMA_BK && (long)s.M * s.N >= 64L * 64) {
+    const bool tall = Epi::kRowDot && !s.sym_tiles && s.M >= 1024;
+    if (tall ? gemm_launch_tma<TA, TB, 128, 64, 32, 32, 4>(s, epi, st)
+             : gemm_launch_tma<TA, TB, 64, 64, 32, 32, 4>(s, epi, st))
+      return;
+  }
   gemm_launch_tiled<TA, TB, GB_M, GB_N>(s, epi, st);
 }
 

@@ -980,6 +980,11 @@ IterRecord iterate_once(Problem& p, const SolverCfg& cfg, const ReplayIn& in, Re
 
 }  // namespace kot
 
+extern "C" int kot_debug_gemm_tma(int mode) {  // test hook: 1 TMA-staged GEMM core (default), 0 cp.async core
+  kot::gemm_tma_mode().store(mode);
+  return 0;
+}
+
 extern "C" int kot_debug_cg_batch(int batch) {  // test hook: CG iterations per host check (≥ 1)
   kot::g_cg_batch = batch >= 1 ? batch : 1;
   return 0;

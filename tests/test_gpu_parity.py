@@ -711,3 +711,29 @@ def test_two_stage_iteration_replay_converged_cg(two_stage, cfg1):
         assert rel(w2.gamma, ost.w.g) <= 1e-8, i
         assert rel(w2.x_mat, ost.w.x) <= 1e-8, i
         assert rel(v2.x_mat, ost.v.x) <= 1e-9, i
+
+
+@pytest.mark.parametrize("n", [700, 701])
+def test_gemm_cores_agree(n):
+    """The TMA-staged DMMA core (default) and the cp.async core compute the same products: Φ* is
+    bit-identical (same k order per element), Φ's fused row-dot sums the tile's columns in the TMA
+    fragment order (≤1e-15), and a short solve agrees (odd orders fall back to the cp.async core)."""
+    from paper_2310_14087_b200 import _lib
+    f = _lib.lib().kot_debug_gemm_tma
+    d = random_problem_arrays(5, n=n)
+    pd = GP.ProblemData(q_mat=d["q"], z=d["z"], q_sq=d["q_sq"], chol_upper=d["r"], lambda1=d["l1"], lambda2=d["l2"])
+    rng = np.random.default_rng(n)
+    g = rng.standard_normal(n)
+    x = random_symmetric(rng, n)
+    cfg = K.SolverConfig(eg=EgConfig(0.05), residual_tol=1e-12, max_iter=3)
+    out = []
+    try:
+        for mode in (0, 1):
+            f(mode)
+            out.append((GP.phi_adjoint(pd, g), GP.phi_forward(pd, x), K.solve(pd, cfg)))
+    finally:
+        f(1)
+    (a0, p0, r0), (a1, p1, r1) = out
+    assert np.array_equal(a0, a1) and rel(p1, p0) <= 1e-15
+    assert rel(r1.gamma_hat, r0.gamma_hat) <= 1e-10
+    assert [t.cg_iters for t in r1.trace] == [t.cg_iters for t in r0.trace]
