@@ -819,9 +819,12 @@ static int trd_grid_cap(int lane) {
   // 112/56/48 → 10.7, 128/48/48 → 11.0, 96/64/32 → 10.8, 96/48/32 → 11.1, 96/32/32 → 11.1 it/s: the
   // EG chain has slack, ≈ 58 vs 90 ms per iteration).  Alone, lane 0 uses every SM.
   static const int cap_fg = std::min(env_int("KOT_TRD_GRID_FG", 96), cap);
-  static const int cap_bg = std::min(env_int("KOT_TRD_GRID_BG", 48), cap);
+  // Round 2, with the TMA GEMM core: thinner EG-chain grids leave CTA slots (registers) to the Newton
+  // chain's CG GEMMs, whose CTAs co-reside with panel CTAs on the same SMs (cfg3: 48/32 → 24/16
+  // CTAs: Newton direction 42.1 → 38.5 ms, 13.9 → 14.6 it/s; the EG chain, 51 → 56 ms, keeps slack).
+  static const int cap_bg = std::min(env_int("KOT_TRD_GRID_BG", 24), cap);
   // lane 2 = the EG pipeline's residual thread, lane 1 = its EG-step threads
-  static const int cap_bg2 = std::min(env_int("KOT_TRD_GRID_BG2", 32), cap);
+  static const int cap_bg2 = std::min(env_int("KOT_TRD_GRID_BG2", 16), cap);
   if (lane == 0) return g_pipelines.load() > 0 ? cap_fg : cap;
   return lane == 2 ? cap_bg2 : cap_bg;
 }

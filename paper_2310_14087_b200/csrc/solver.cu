@@ -246,10 +246,19 @@ CgResult cg_solve_op(Problem& p, const double* rhs, double tol, int max_iter,
 // --------------------------------------------------------------- Newton
 
 // Criterion ‖(J+μI)dw + r‖ ≤ τ min(1, κ‖r‖‖dw‖) for dw = (sol, ã2 − 𝒯[Φ*(sol)]) (newton.py:131-141,
-// problem.py:222-236), enqueued on the criterion context q after `after` (recorded on p's stream):
-// dw into q.crit_dg / q.crit_dX, the four squared norms into q.hsc[0..3], completion = q.crit_done.
-static void criterion_enqueue(Problem& p, Problem& q, const double* r1, const double* r2, const Decomp& dc,
-                              double mu) {
+// problem.py:222-236).  With that dw the two blocks of (J+μI)dw + r are, exactly (Lemma 1):
+//   top    = Q sol/(2λ₂) + μ sol − Φ(ã2 − 𝒯Φ*(sol)) + r1 = A·sol − a1   (A: the middle operator,
+//            a1 = −r1 + Φ(ã2)), i.e. minus the true residual of the reduced system;
+//   bottom = M[Φ*(sol) − dX] + (1+μ)dX + r2 = 0, because dX = −((1+μ)I − M)⁻¹(r2 + MΦ*(sol)) and
+//            ã2 = −((1+μ)I − M)⁻¹ r2 (M, 𝒯 share the eigenbasis, 𝒯 = M((1+μ)I − M)⁻¹).
+// So lhs = ‖a1 − A·sol‖₂: the next attempt's right-hand side, which the main stream computes anyway
+// (`rhs_next`), or one matvec on the criterion context after the last attempt.  The reference
+// evaluates the same quantity through apply_jacobian (Φ, Φ*, a dense M, four GEMM chains); the two
+// differ by rounding only.  dw itself (needed for ‖dw‖ and as the step) is built here as before.
+// Enqueued on the criterion context q after `crit_after` (recorded on p's stream): dw into
+// q.crit_dg / q.crit_dX, the norms into q.hsc[0..3], completion = q.crit_done.
+static void criterion_enqueue(Problem& p, Problem& q, const Decomp& dc, double mu, const MvCtx& mv,
+                              const double* rhs_next, cudaEvent_t rhs_ready) {
   Bufs& b = p.bufs();
   const int n = p.n;
   const long nn = (long)n * n;
@@ -261,13 +270,18 @@ static void criterion_enqueue(Problem& p, Problem& q, const double* r1, const do
   spectral_filter(q, dc, q.M1, q.M2, mu, 0);
   axpby(q, nn, 1.0, b.a2t, -1.0, q.M2, q.crit_dX);
   KOT_CUDA(cudaEventRecord(q.crit_dx_done, q.st));  // dw is complete; the norms below feed the record
-  phi_partials(q, q.crit_dX);
-  finalize(q, FIN_JTOP, q.crit_dg, true, r1, mu, q.crit_e1);
-  phi_adjoint_ex(q, q.crit_dg, q.M1, 1.0, q.crit_dX, -1.0, 0.0);  // Φ*(dγ) − dX
-  spectral_filter(q, dc, q.M1, q.M2, mu, 1);                       // M[·]
-  jac_bottom(q, nn, q.M2, q.crit_dX, mu, r2, q.M1);
-  dev_reduce(q, q.crit_e1, nullptr, n, 0, true);
-  dev_reduce(q, q.M1, nullptr, nn, 1, true);
+  const double* top;
+  if (rhs_next) {  // a1 − A·sol, from the main stream
+    KOT_CUDA(cudaStreamWaitEvent(q.st, rhs_ready, 0));
+    top = rhs_next;
+  } else {  // after the last attempt: the (H-form) matvec here, off the critical path
+    if (!q.mv_ct) q.mv_ct = q.alloc(nn);
+    middle_operator_fast(q, mv, q.crit_dg, q.crit_e1);
+    axpby(q, n, 1.0, b.a1, -1.0, q.crit_e1, q.crit_e1);
+    top = q.crit_e1;
+  }
+  dev_reduce(q, top, nullptr, n, 0, true);
+  KOT_CUDA(cudaMemsetAsync(q.dsc + 1, 0, sizeof(double), q.st));  // bottom block: identically zero
   dev_reduce(q, q.crit_dg, nullptr, n, 2, true);
   dev_reduce(q, q.crit_dX, nullptr, nn, 3, true);
   KOT_CUDA(cudaMemcpyAsync(q.hsc, q.dsc, sizeof(double) * 4, cudaMemcpyDeviceToHost, q.st));
@@ -294,6 +308,7 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
   if (!p.ev_mv0) {
     KOT_CUDA(cudaEventCreateWithFlags(&p.ev_mv0, cudaEventDisableTiming));
     KOT_CUDA(cudaEventCreateWithFlags(&p.ev_mv1, cudaEventDisableTiming));
+    KOT_CUDA(cudaEventCreateWithFlags(&p.ev_rhs, cudaEventDisableTiming));
   }
   KOT_CUDA(cudaEventRecord(p.ev_mv0, p.st));
   KOT_CUDA(cudaStreamWaitEvent(q.st, p.ev_mv0, 0));
@@ -342,8 +357,12 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
   const std::function<bool()> abort_if_met = [&]() { return resolve(false) && pending_met; };
   // Row-sharded problems: each CG matvec is a collective, so every rank must run the same number of
   // them.  The speculative abort polls the criterion's completion (timing-dependent per rank), hence
-  // no speculation there: attempt a+1 starts only after attempt a's criterion is known (same result).
+  // no speculation there: attempt a+1 starts only after attempt a's criterion is known (same result);
+  // and the last attempt's lhs matvec (a collective) runs on the main stream, in program order.
   const bool may_speculate = !p.sharded();
+  // right-hand sides of attempts ≥ 1 (a1 − A·sol), alternating so that attempt a+2 never overwrites
+  // the vector attempt a's criterion still reads (that criterion is resolved before a+2 starts)
+  double* rhs_buf[2] = {b.rhs, b.corr};
   for (int att = 0; att <= cfg.cg_restarts; ++att) {
     if (pending && !may_speculate) {
       resolve(true);
@@ -356,15 +375,7 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
     CgOut c{0, 0.0};
     bool ran = false;
     try {
-      const double* rhs = b.a1;
-      if (att) {
-        if (mv.direct)
-          middle_operator(p, dc, mu, b.sol, b.e3);
-        else
-          middle_operator_fast(p, mv, b.sol, b.e3);
-        axpby(p, n, 1.0, b.a1, -1.0, b.e3, b.rhs);
-        rhs = b.rhs;
-      }
+      const double* rhs = att ? rhs_buf[att & 1] : b.a1;
       const double bn = dev_norm(p, rhs, n);
       if (bn > 0.0 && a1n > 0.0) {
         c = cg_solve(p, mv, rhs, rel * a1n / bn, cfg.cg_max, speculative ? &abort_if_met : nullptr);
@@ -390,9 +401,21 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
       axpby(p, n, 1.0, b.sol, 1.0, b.cx, b.sol);
       out.cg_iters += c.iters;
     }
-    criterion_enqueue(p, q, r1, r2, dc, mu);
+    const bool last = att == cfg.cg_restarts;
+    const double* rhs_next = nullptr;
+    if (!last || !may_speculate || !mv.hform) {  // a1 − A·sol: attempt att+1's rhs and this criterion's lhs
+      double* rn_buf = rhs_buf[(att + 1) & 1];
+      if (mv.direct)
+        middle_operator(p, dc, mu, b.sol, b.e3);
+      else
+        middle_operator_fast(p, mv, b.sol, b.e3);
+      axpby(p, n, 1.0, b.a1, -1.0, b.e3, rn_buf);
+      KOT_CUDA(cudaEventRecord(p.ev_rhs, p.st));
+      rhs_next = rn_buf;
+    }
+    criterion_enqueue(p, q, dc, mu, mv, rhs_next, p.ev_rhs);
     pending = true;
-    if (att == cfg.cg_restarts) break;
+    if (last) break;
     rel /= 10.0;
   }
   // The last attempt's criterion only feeds the record (met, lhs, rhs): dw is taken as soon as it is

@@ -69,6 +69,7 @@ Problem::~Problem() {
   if (ev_half) cudaEventDestroy(ev_half);
   if (ev_mv0) cudaEventDestroy(ev_mv0);
   if (ev_mv1) cudaEventDestroy(ev_mv1);
+  if (ev_rhs) cudaEventDestroy(ev_rhs);
   eig.reset();
   for (double* p : owned) dev_free(p);
   host_free_pinned(hsc, 64 * sizeof(double));
@@ -582,7 +583,7 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
   const int ns = n - ks;
   const double nn = n;
   ProfScope ps("matvec", p.st, 4.0 * ks * (double)ns * nn + 4.0 * nn * nn);
-  Bufs& b = p.bufs();
+  double* Ct = p.mv_ct ? p.mv_ct : p.bufs().Ct;
   const double* Bs = m.Bs;  // columns of the T̃-row block (the smaller sign block)
   const double* Bo = m.Bo;  // columns of the other block
   const long ld = m.ldp;
@@ -595,11 +596,11 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
     s.ksplit = choose_ksplit(s, p.splitws_cap);
     static const int mv_split = [] {
       const char* e = std::getenv("KOT_MV_SPLIT");
-      return e ? std::atoi(e) : 3;
+      return e ? std::atoi(e) : 1;  // TMA core: no split-K on the H-form GEMM1 (14.08 vs 13.85 it/s)
     }();
     if (mv_split > 1 && (long)mv_split * s.M * s.N <= p.splitws_cap) s.ksplit = mv_split;
-    gemm_launch<true, false>(s, EpiMvOff{b.Ct, n, m.dc.vals, k, m.pos ? 1 : 0, m.mu}, p.st);
-    GemmShape s2 = make_shape(n, ks, ns, Bo, ld, b.Ct, n);
+    gemm_launch<true, false>(s, EpiMvOff{Ct, n, m.dc.vals, k, m.pos ? 1 : 0, m.mu}, p.st);
+    GemmShape s2 = make_shape(n, ks, ns, Bo, ld, Ct, n);
     s2.skipf = skipf;
     // optional split-K on the row-dot GEMM (each K share adds its own partial rows, summed in fixed
     // order by finalize); KOT_MV2_SPLIT=2 measured neutral inside the solver (12.66 vs 12.68 it/s)

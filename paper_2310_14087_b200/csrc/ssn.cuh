@@ -94,9 +94,11 @@ struct Problem {
   // its stream, scratch, outputs (crit_dg, crit_dX, crit_e1) and completion event
   Problem& crit();
   double *crit_dg = nullptr, *crit_dX = nullptr, *crit_e1 = nullptr;
+  double* mv_ct = nullptr;  // criterion context: its own T̃ (ℓ×ℓ) for the H-form matvec (no full Bufs)
   cudaEvent_t crit_done = nullptr, crit_after = nullptr, crit_dx_done = nullptr;
   cudaEvent_t ev_half = nullptr;  // eg_step_parallel: γ½ ready
   cudaEvent_t ev_mv0 = nullptr, ev_mv1 = nullptr;  // newton_direction: matvec_prepare on the crit stream
+  cudaEvent_t ev_rhs = nullptr;                    // newton_direction: next attempt's rhs ready
   bool with_eig = true;
   double* alloc(long count);
   void init_scratch();
