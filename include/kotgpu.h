@@ -161,6 +161,10 @@ typedef struct {
 int kot_profile_enable(int on);  /* 0 off, 1 every scope, 2 roofline scopes only (cheap); resets the counters */
 int kot_profile_read(kot_prof_entry* out, int cap);  /* returns #entries */
 
+/* Process-wide cap on the CTAs of every tridiagonalisation panel grid (0 = all SMs): several concurrent
+ * solves sharing one GPU (batches of independent problems) run faster on thin grids. */
+int kot_set_panel_grid_cap(int cap);
+
 /* ---- test / diagnostic hooks (process-wide; not part of the drop-in surface) ---- */
 int kot_debug_eig_stages(int stages);   /* 0 automatic, 1 one-stage, 2 two-stage, 3 two-stage in background */
 int kot_debug_cg_batch(int batch);      /* CG iterations enqueued per host check (>= 1; default 4) */

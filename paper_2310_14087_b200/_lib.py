@@ -87,6 +87,7 @@ _SIGS = {
     "kot_debug_cg_batch": (C.c_int, [C.c_int]),
     "kot_debug_eg_parallel": (C.c_int, [C.c_int]),
     "kot_debug_gemm_tma": (C.c_int, [C.c_int]),
+    "kot_set_panel_grid_cap": (C.c_int, [C.c_int]),
     "kot_debug_sytrd_timing": (C.c_int, [C.c_int, C.POINTER(C.c_ulonglong)]),
     "kot_debug_tail_timing": (C.c_int, [C.c_int, C.POINTER(C.c_ulonglong)]),
     "kot_gram": (C.c_int, [dptr, C.c_int, C.c_int, C.c_double, C.c_int, dptr]),

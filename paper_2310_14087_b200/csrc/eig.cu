@@ -810,21 +810,29 @@ static int env_int(const char* name, int dflt) {
 static std::atomic<int> g_pipelines{0};
 void eig_pipeline_active(int delta) { g_pipelines += delta; }
 
+// Process-wide cap on every panel grid (KOT_TRD_GRID, or kot_set_panel_grid_cap at run time): several
+// concurrent solves (config-5 batches) share the GPU better with thin grids.
+static std::atomic<int> g_trd_cap{-1};
+void set_panel_grid_cap(int cap) { g_trd_cap = cap > 0 ? std::min(cap, kNumSMs) : kNumSMs; }
 static int trd_grid_cap(int lane) {
-  static const int cap = std::min(env_int("KOT_TRD_GRID", kNumSMs), kNumSMs);
+  if (g_trd_cap.load() < 0) g_trd_cap = std::min(env_int("KOT_TRD_GRID", kNumSMs), kNumSMs);
+  const int cap = g_trd_cap.load();
   // With an EG pipeline running, four cooperative grids can be in flight — Newton chain 96, the EG
   // step's two projections (run side by side, eg_step_parallel) 48 each, residual at v 32 CTAs — and
   // they fit co-resident in the 2 × 148 slots, so no chain queues at the gate behind another's panel
   // (probe cfg3 with parallel EG projections: 96/96/64 → 10.2, 96/64/64 → 10.5, 96/64/48 → 10.7–11.0,
   // 112/56/48 → 10.7, 128/48/48 → 11.0, 96/64/32 → 10.8, 96/48/32 → 11.1, 96/32/32 → 11.1 it/s: the
   // EG chain has slack, ≈ 58 vs 90 ms per iteration).  Alone, lane 0 uses every SM.
-  static const int cap_fg = std::min(env_int("KOT_TRD_GRID_FG", 96), cap);
+  static const int fg = env_int("KOT_TRD_GRID_FG", 96);
+  const int cap_fg = std::min(fg, cap);
   // Round 2, with the TMA GEMM core: thinner EG-chain grids leave CTA slots (registers) to the Newton
   // chain's CG GEMMs, whose CTAs co-reside with panel CTAs on the same SMs (cfg3: 48/32 → 24/16
   // CTAs: Newton direction 42.1 → 38.5 ms, 13.9 → 14.6 it/s; the EG chain, 51 → 56 ms, keeps slack).
-  static const int cap_bg = std::min(env_int("KOT_TRD_GRID_BG", 24), cap);
+  static const int bg = env_int("KOT_TRD_GRID_BG", 24);
+  const int cap_bg = std::min(bg, cap);
   // lane 2 = the EG pipeline's residual thread, lane 1 = its EG-step threads
-  static const int cap_bg2 = std::min(env_int("KOT_TRD_GRID_BG2", 16), cap);
+  static const int bg2 = env_int("KOT_TRD_GRID_BG2", 16);
+  const int cap_bg2 = std::min(bg2, cap);
   if (lane == 0) return g_pipelines.load() > 0 ? cap_fg : cap;
   return lane == 2 ? cap_bg2 : cap_bg;
 }
@@ -1517,6 +1525,47 @@ struct EpiColMap {
   __device__ void rowdot_store(int, int, double) const {}
 };
 
+// All merges of one D&C level in ONE launch (grid.z = merge): the shape of each group — the top rows
+// (M = n1, K = c12) or the bottom rows (M = n2, K range [c1, K)) of Qnd·U, N = K non-deflated
+// columns — is read from the merge descriptor and the device meta, as the per-merge launches did.
+struct EpiColMapGroup {
+  static constexpr bool kRowDot = false;
+  double* Q;
+  long ldq;
+  const int* colmap;
+  const MergeDesc* md;
+  const int* meta;
+  const double* Qnd;
+  const double* U;
+  int bottom;
+  int o = 0, roff = 0;
+  __device__ void adapt(GemmShape& s, int z) {
+    const MergeDesc m = md[z];
+    const int nn = m.n1 + m.n2, ld = nn + (nn & 1);
+    const int* mt = meta + MS * z;
+    s.lda = s.ldb = ld;
+    s.B = U + m.off;
+    s.N = mt[0];
+    o = m.o;
+    if (!bottom) {
+      s.A = Qnd + m.off;
+      s.M = m.n1;
+      s.K = mt[4];
+      s.kstart = 0;
+      roff = 0;
+    } else {
+      s.A = Qnd + m.off + (long)m.n1 * ld;
+      s.M = m.n2;
+      s.K = mt[0];
+      s.kstart = mt[3];
+      roff = m.n1;
+    }
+  }
+  __device__ void store(int r, int c, double v) const { Q[(long)(o + roff + r) * ldq + o + colmap[o + c]] = v; }
+  __device__ double rowdot_weight(int, int) const { return 0; }
+  __device__ void rowdot_store(int, int, double) const {}
+};
+
 struct DcNode {
   int o, n, depth;
   bool leaf;
@@ -1646,27 +1695,25 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
     KOT_LAUNCH_CHECK();
     dc_copy_deflated_kernel<<<dim3(64, nm), 256, 0, st>>>(dms, dmeta, w.Qw, w.Q, n, colmap);
     KOT_LAUNCH_CHECK();
-    for (int i = 0; i < nm; ++i) {
-      // Q_new = Qnd·U with Qnd's columns ordered (top-only | mixed | bottom-only): the top rows only
-      // see the first c12 columns, the bottom rows only the last K − c1 (dlaed3 structure).  K, c1,
-      // c12 are read on the device; the grids are sized for K ≤ n_m.
-      const int n1 = ms[i].n1, n2 = ms[i].n2, nn = n1 + n2;
-      const int ld = nn + (nn & 1);
-      const double* Qnd = w.Qnd + ms[i].off;
-      const double* U = w.Uw + ms[i].off;
-      const int* mt = dmeta + MS * i;
-      {
-        GemmShape s = make_shape(n1, nn, nn, Qnd, ld, U, ld);
-        s.dN = mt;       // K
-        s.dK = mt + 4;   // c12
-        gemm_launch<false, true>(s, EpiColMap{w.Q, n, ms[i].o, 0, colmap}, st);
+    // Q_new = Qnd·U with Qnd's columns ordered (top-only | mixed | bottom-only): the top rows only
+    // see the first c12 columns, the bottom rows only the last K − c1 (dlaed3 structure).  K, c1, c12
+    // are read on the device; every merge of the level in one grouped launch per row half (the top-only
+    // columns are exact zeros in the bottom rows, so an aligned K start is harmless there).
+    {
+      int mmax = 0, nnmax = 0;
+      for (auto& mm : ms) {
+        mmax = std::max(mmax, std::max(mm.n1, mm.n2));
+        nnmax = std::max(nnmax, mm.n1 + mm.n2);
       }
-      {  // the top-only columns are exact zeros in the bottom rows, so an aligned K start is harmless
-        GemmShape s = make_shape(n2, nn, nn, Qnd + (long)n1 * ld, ld, U, ld);
-        s.dN = mt;
-        s.dK = mt;       // K
-        s.dKstart = mt + 3;  // c1
-        gemm_launch<false, true>(s, EpiColMap{w.Q, n, ms[i].o, n1, colmap}, st);
+      const int tiles = ceil_div(mmax, GB_M) * ceil_div(nnmax, GB_N);
+      constexpr int smem = GTile<GB_M, GB_N>::SMEM;
+      auto k = gemm_dmma_kernel<false, true, 2, EpiColMapGroup>;
+      ensure_smem_attr((const void*)k, smem);
+      for (int half = 0; half < 2; ++half) {
+        GemmShape s = make_shape(mmax, nnmax, nnmax, w.Qnd, nnmax, w.Uw, nnmax);  // rewritten per group
+        k<<<dim3(tiles, 1, nm), G_THREADS, smem, st>>>(s, EpiColMapGroup{w.Q, n, colmap, dms, dmeta, w.Qnd, w.Uw,
+                                                                        half});
+        KOT_LAUNCH_CHECK();
       }
     }
   }

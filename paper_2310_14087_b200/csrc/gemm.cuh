@@ -113,6 +113,11 @@ __device__ __forceinline__ void load_tile(double* sm, int pad, const double* g, 
   }
 }
 
+template <class E, class = void>
+struct EpiHasAdapt : std::false_type {};
+template <class E>
+struct EpiHasAdapt<E, std::void_t<decltype(&E::adapt)>> : std::true_type {};
+
 // Epilogue interface:
 //   static constexpr bool kRowDot;            // use the fused row-dot path
 //   __device__ void store(int r, int c, double v) const;          (kRowDot == false)
@@ -129,6 +134,8 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
   if (s.dN) s.N = *s.dN;
   if (s.dK) s.K = *s.dK;
   if (s.dKstart) s.kstart = *s.dKstart;
+  // grouped launches: the epilogue rewrites the shape (and itself) for group blockIdx.z
+  if constexpr (EpiHasAdapt<Epi>::value) epi.adapt(s, blockIdx.z);
   double* As = gsm;
   double* Bs = gsm + G_STAGES * T::ATILE;
   double* Ks = gsm + G_STAGES * (T::ATILE + T::BTILE);

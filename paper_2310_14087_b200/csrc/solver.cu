@@ -1003,6 +1003,14 @@ IterRecord iterate_once(Problem& p, const SolverCfg& cfg, const ReplayIn& in, Re
 
 }  // namespace kot
 
+namespace kot {
+void set_panel_grid_cap(int cap);
+}
+extern "C" int kot_set_panel_grid_cap(int cap) {  // 0: default (all SMs)
+  kot::set_panel_grid_cap(cap);
+  return 0;
+}
+
 extern "C" int kot_debug_gemm_tma(int mode) {  // test hook: 1 TMA-staged GEMM core (default), 0 cp.async core
   kot::gemm_tma_mode().store(mode);
   return 0;
