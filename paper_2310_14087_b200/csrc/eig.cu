@@ -1711,8 +1711,10 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
       ensure_smem_attr((const void*)k, smem);
       for (int half = 0; half < 2; ++half) {
         GemmShape s = make_shape(mmax, nnmax, nnmax, w.Qnd, nnmax, w.Uw, nnmax);  // rewritten per group
-        k<<<dim3(tiles, 1, nm), G_THREADS, smem, st>>>(s, EpiColMapGroup{w.Q, n, colmap, dms, dmeta, w.Qnd, w.Uw,
-                                                                        half});
+        const int cap = gemm_cta_cap();
+        const int ctas = cap > 0 ? std::max(1, std::min(tiles, cap / nm)) : tiles;
+        k<<<dim3(ctas, 1, nm), G_THREADS, smem, st>>>(s, EpiColMapGroup{w.Q, n, colmap, dms, dmeta, w.Qnd, w.Uw,
+                                                                       half}, tiles);
         KOT_LAUNCH_CHECK();
       }
     }

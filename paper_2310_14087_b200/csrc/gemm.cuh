@@ -27,6 +27,15 @@ namespace kot {
 #ifndef KOT_GEMM_BK
 #define KOT_GEMM_BK 8
 #endif
+// CTAs a GEMM launch from the calling host thread may use (0 = one per tile).  The solver's background
+// chains (EG pipeline threads) set a cap so that their GEMMs never fill every SM slot: the Newton
+// chain's CG kernels, launched one after another, then find free slots instead of queueing behind
+// a background GEMM's waves.
+inline int& gemm_cta_cap() {
+  static thread_local int cap = 0;
+  return cap;
+}
+
 constexpr int GB_M = 64, GB_N = 64, GB_K = KOT_GEMM_BK, G_STAGES = KOT_GEMM_STAGES, G_THREADS = 128;
 constexpr int G_PADK = GB_K + 4;  // stride ≡ 4 (mod 16) doubles → conflict-free fragment loads
 // CTA tile BM×BN, 4 warps as 2×2, each (BM/2)×(BN/2).  64×64 is used everywhere: 64×128 / 128×64
@@ -124,7 +133,7 @@ struct EpiHasAdapt<E, std::void_t<decltype(&E::adapt)>> : std::true_type {};
 //   __device__ double rowdot_weight(int r, int c) const;          (kRowDot == true)
 //   __device__ void rowdot_store(int tn, int r, double partial) const;
 template <bool TA, bool TB, int VEC, class Epi, int BM = GB_M, int BN = GB_N>
-__global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi epi) {
+__global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi epi, int ntiles) {
   using T = GTile<BM, BN>;
   static_assert(!Epi::kRowDot || BN == GB_N, "row-dot partials are per 64-column tile");
   extern __shared__ __align__(16) double gsm[];
@@ -140,171 +149,175 @@ __global__ void __launch_bounds__(G_THREADS) gemm_dmma_kernel(GemmShape s, Epi e
   double* Bs = gsm + G_STAGES * T::ATILE;
   double* Ks = gsm + G_STAGES * (T::ATILE + T::BTILE);
 
-  const int tiles_m = (s.M + BM - 1) / BM;
-  const int tiles_n = (s.N + BN - 1) / BN;
-  int tm, tn;
-  if (s.sym_tiles) {
-    int t = blockIdx.x;
-    tm = 0;
-    while (t >= tiles_n_grid - tm) {
-      t -= tiles_n_grid - tm;
-      ++tm;
+  // tiles in a loop: a launch may use fewer CTAs than tiles (gemm_cta_cap)
+  for (int bx = blockIdx.x; bx < ntiles; bx += gridDim.x) {
+  __syncthreads();  // the previous tile's epilogue may still read the staging buffers
+    const int tiles_m = (s.M + BM - 1) / BM;
+    const int tiles_n = (s.N + BN - 1) / BN;
+    int tm, tn;
+    if (s.sym_tiles) {
+      int t = bx;
+      tm = 0;
+      while (t >= tiles_n_grid - tm) {
+        t -= tiles_n_grid - tm;
+        ++tm;
+      }
+      tn = tm + t;
+    } else {
+      tm = bx % tiles_m;
+      tn = bx / tiles_m;
     }
-    tn = tm + t;
-  } else {
-    tm = blockIdx.x % tiles_m;
-    tn = blockIdx.x / tiles_m;
-  }
-  if (tm >= tiles_m || tn >= tiles_n) return;
-  const int m0 = tm * BM, n0 = tn * BN;
+    if (tm >= tiles_m || tn >= tiles_n) continue;
+    const int m0 = tm * BM, n0 = tn * BN;
 
-  int kbeg = 0, kend = s.K;
-  if (s.kb_m) kbeg = max(kbeg, m0);
-  if (s.kb_n) kbeg = max(kbeg, n0);
-  kbeg = max(kbeg, s.kstart);
-  if (s.ke_m) kend = min(kend, m0 + BM);
-  if (s.ke_n) kend = min(kend, n0 + BN);
-  kbeg = (kbeg / GB_K) * GB_K;
-  int nkt = kend > kbeg ? (kend - kbeg + GB_K - 1) / GB_K : 0;
-  if (s.ksplit > 1) {  // this CTA's share of the K tiles
-    const int per = (nkt + s.ksplit - 1) / s.ksplit;
-    const int t0 = blockIdx.y * per;
-    kbeg += t0 * GB_K;
-    nkt = max(0, min(per, nkt - t0));
-  }
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * T::WM, wn = (warp & 1) * T::WN;
-
-  double acc[T::MI][T::NJ][2];
-#pragma unroll
-  for (int i = 0; i < T::MI; i++)
-#pragma unroll
-    for (int j = 0; j < T::NJ; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  auto issue = [&](int kt, int stage) {
-    const int k0 = kbeg + kt * GB_K;
-    double* as = As + stage * T::ATILE;
-    double* bs = Bs + stage * T::BTILE;
-    if (TA)  // A stored K×M: tile rows k, cols m
-      load_tile<GB_K, BM, VEC>(as, T::PADM, s.A, s.lda, k0, m0, s.K, s.M);
-    else
-      load_tile<BM, GB_K, VEC>(as, G_PADK, s.A, s.lda, m0, k0, s.M, s.K);
-    if (TB)  // B stored N×K
-      load_tile<BN, GB_K, VEC>(bs, G_PADK, s.B, s.ldb, n0, k0, s.N, s.K);
-    else
-      load_tile<GB_K, BN, VEC>(bs, T::PADN, s.B, s.ldb, k0, n0, s.K, s.N);
-    if (s.kscale != nullptr && threadIdx.x < GB_K) {
-      const int k = k0 + threadIdx.x;
-      cp_async_8(Ks + stage * GB_K + threadIdx.x, k < s.K ? s.kscale + k : s.kscale, k < s.K ? 8 : 0);
+    int kbeg = 0, kend = s.K;
+    if (s.kb_m) kbeg = max(kbeg, m0);
+    if (s.kb_n) kbeg = max(kbeg, n0);
+    kbeg = max(kbeg, s.kstart);
+    if (s.ke_m) kend = min(kend, m0 + BM);
+    if (s.ke_n) kend = min(kend, n0 + BN);
+    kbeg = (kbeg / GB_K) * GB_K;
+    int nkt = kend > kbeg ? (kend - kbeg + GB_K - 1) / GB_K : 0;
+    if (s.ksplit > 1) {  // this CTA's share of the K tiles
+      const int per = (nkt + s.ksplit - 1) / s.ksplit;
+      const int t0 = blockIdx.y * per;
+      kbeg += t0 * GB_K;
+      nkt = max(0, min(per, nkt - t0));
     }
-  };
 
-#pragma unroll
-  for (int st = 0; st < G_STAGES - 1; ++st) {
-    if (st < nkt) issue(st, st);
-    cp_async_commit();
-  }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = (warp >> 1) * T::WM, wn = (warp & 1) * T::WN;
 
-  for (int kt = 0; kt < nkt; ++kt) {
-    cp_async_wait<G_STAGES - 2>();
-    __syncthreads();
-    {
-      const int nk = kt + G_STAGES - 1;
-      if (nk < nkt) issue(nk, nk % G_STAGES);
-      cp_async_commit();
-    }
-    const int stage = kt % G_STAGES;
-    const double* as = As + stage * T::ATILE;
-    const double* bs = Bs + stage * T::BTILE;
-    const double* ks = Ks + stage * GB_K;
-    // the K-scaling multiply only exists in the instantiation that needs it (uniform branch)
-    auto mma_stage = [&](auto has_kscale) {
-      constexpr bool kKS = decltype(has_kscale)::value;
-#pragma unroll
-      for (int kk = 0; kk < GB_K; kk += 4) {
-        double a[T::MI], b[T::NJ];
-        double kscl = 1.0;
-        if constexpr (kKS) kscl = ks[kk + t];
-#pragma unroll
-        for (int i = 0; i < T::MI; i++) {
-          const int m = wm + i * 8 + g;
-          const double av = TA ? as[(kk + t) * T::PADM + m] : as[m * G_PADK + kk + t];
-          if constexpr (kKS)
-            a[i] = av * kscl;
-          else
-            a[i] = av;
-        }
-#pragma unroll
-        for (int j = 0; j < T::NJ; j++) {
-          const int n = wn + j * 8 + g;
-          b[j] = TB ? bs[n * G_PADK + kk + t] : bs[(kk + t) * T::PADN + n];
-        }
-#pragma unroll
-        for (int i = 0; i < T::MI; i++)
-#pragma unroll
-          for (int j = 0; j < T::NJ; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    double acc[T::MI][T::NJ][2];
+  #pragma unroll
+    for (int i = 0; i < T::MI; i++)
+  #pragma unroll
+      for (int j = 0; j < T::NJ; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    auto issue = [&](int kt, int stage) {
+      const int k0 = kbeg + kt * GB_K;
+      double* as = As + stage * T::ATILE;
+      double* bs = Bs + stage * T::BTILE;
+      if (TA)  // A stored K×M: tile rows k, cols m
+        load_tile<GB_K, BM, VEC>(as, T::PADM, s.A, s.lda, k0, m0, s.K, s.M);
+      else
+        load_tile<BM, GB_K, VEC>(as, G_PADK, s.A, s.lda, m0, k0, s.M, s.K);
+      if (TB)  // B stored N×K
+        load_tile<BN, GB_K, VEC>(bs, G_PADK, s.B, s.ldb, n0, k0, s.N, s.K);
+      else
+        load_tile<GB_K, BN, VEC>(bs, T::PADN, s.B, s.ldb, k0, n0, s.K, s.N);
+      if (s.kscale != nullptr && threadIdx.x < GB_K) {
+        const int k = k0 + threadIdx.x;
+        cp_async_8(Ks + stage * GB_K + threadIdx.x, k < s.K ? s.kscale + k : s.kscale, k < s.K ? 8 : 0);
       }
     };
-    if (s.kscale != nullptr)
-      mma_stage(std::true_type{});
-    else
-      mma_stage(std::false_type{});
-  }
-  cp_async_wait<0>();
 
-  if constexpr (Epi::kRowDot) {
-    // partial[r] = Σ_{c in this tile} acc(r,c)·E(r,c): 4-lane shuffle + 2-warp smem combine.
-    __syncthreads();
-    double* red = gsm;  // reuse: [2][BM]
-#pragma unroll
-    for (int i = 0; i < T::MI; i++) {
-      const int r = m0 + wm + i * 8 + g;
-      double p = 0.0;
-#pragma unroll
-      for (int j = 0; j < T::NJ; j++)
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int c = n0 + wn + j * 8 + 2 * t + h;
-          if (r < s.M && c < s.N) p += acc[i][j][h] * epi.rowdot_weight(r, c);
-        }
-      p += __shfl_xor_sync(0xffffffffu, p, 1);
-      p += __shfl_xor_sync(0xffffffffu, p, 2);
-      if (t == 0) red[(warp & 1) * BM + wm + i * 8 + g] = p;
+  #pragma unroll
+    for (int st = 0; st < G_STAGES - 1; ++st) {
+      if (st < nkt) issue(st, st);
+      cp_async_commit();
     }
-    __syncthreads();
-    for (int q = threadIdx.x; q < BM; q += G_THREADS) {
-      const int r = m0 + q;
-      // split-K: every K share writes its own partial row block (row-dots are linear in the product)
-      if (r < s.M) epi.rowdot_store(tn + (int)blockIdx.y * tiles_n_grid, r, red[q] + red[BM + q]);
-    }
-  } else if (s.ksplit > 1) {
-    double* ws = s.ws + (long)blockIdx.y * s.M * n_static;
-#pragma unroll
-    for (int i = 0; i < T::MI; i++) {
-      const int r = m0 + wm + i * 8 + g;
-      if (r >= s.M) continue;
-#pragma unroll
-      for (int j = 0; j < T::NJ; j++)
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int c = n0 + wn + j * 8 + 2 * t + h;
-          if (c < s.N) ws[(long)r * n_static + c] = acc[i][j][h];
+
+    for (int kt = 0; kt < nkt; ++kt) {
+      cp_async_wait<G_STAGES - 2>();
+      __syncthreads();
+      {
+        const int nk = kt + G_STAGES - 1;
+        if (nk < nkt) issue(nk, nk % G_STAGES);
+        cp_async_commit();
+      }
+      const int stage = kt % G_STAGES;
+      const double* as = As + stage * T::ATILE;
+      const double* bs = Bs + stage * T::BTILE;
+      const double* ks = Ks + stage * GB_K;
+      // the K-scaling multiply only exists in the instantiation that needs it (uniform branch)
+      auto mma_stage = [&](auto has_kscale) {
+        constexpr bool kKS = decltype(has_kscale)::value;
+  #pragma unroll
+        for (int kk = 0; kk < GB_K; kk += 4) {
+          double a[T::MI], b[T::NJ];
+          double kscl = 1.0;
+          if constexpr (kKS) kscl = ks[kk + t];
+  #pragma unroll
+          for (int i = 0; i < T::MI; i++) {
+            const int m = wm + i * 8 + g;
+            const double av = TA ? as[(kk + t) * T::PADM + m] : as[m * G_PADK + kk + t];
+            if constexpr (kKS)
+              a[i] = av * kscl;
+            else
+              a[i] = av;
+          }
+  #pragma unroll
+          for (int j = 0; j < T::NJ; j++) {
+            const int n = wn + j * 8 + g;
+            b[j] = TB ? bs[n * G_PADK + kk + t] : bs[(kk + t) * T::PADN + n];
+          }
+  #pragma unroll
+          for (int i = 0; i < T::MI; i++)
+  #pragma unroll
+            for (int j = 0; j < T::NJ; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
         }
+      };
+      if (s.kscale != nullptr)
+        mma_stage(std::true_type{});
+      else
+        mma_stage(std::false_type{});
     }
-  } else {
-#pragma unroll
-    for (int i = 0; i < T::MI; i++) {
-      const int r = m0 + wm + i * 8 + g;
-      if (r >= s.M) continue;
-#pragma unroll
-      for (int j = 0; j < T::NJ; j++)
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int c = n0 + wn + j * 8 + 2 * t + h;
-          if (c < s.N) epi.store(r, c, acc[i][j][h]);
-        }
+    cp_async_wait<0>();
+
+    if constexpr (Epi::kRowDot) {
+      // partial[r] = Σ_{c in this tile} acc(r,c)·E(r,c): 4-lane shuffle + 2-warp smem combine.
+      __syncthreads();
+      double* red = gsm;  // reuse: [2][BM]
+  #pragma unroll
+      for (int i = 0; i < T::MI; i++) {
+        const int r = m0 + wm + i * 8 + g;
+        double p = 0.0;
+  #pragma unroll
+        for (int j = 0; j < T::NJ; j++)
+  #pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int c = n0 + wn + j * 8 + 2 * t + h;
+            if (r < s.M && c < s.N) p += acc[i][j][h] * epi.rowdot_weight(r, c);
+          }
+        p += __shfl_xor_sync(0xffffffffu, p, 1);
+        p += __shfl_xor_sync(0xffffffffu, p, 2);
+        if (t == 0) red[(warp & 1) * BM + wm + i * 8 + g] = p;
+      }
+      __syncthreads();
+      for (int q = threadIdx.x; q < BM; q += G_THREADS) {
+        const int r = m0 + q;
+        // split-K: every K share writes its own partial row block (row-dots are linear in the product)
+        if (r < s.M) epi.rowdot_store(tn + (int)blockIdx.y * tiles_n_grid, r, red[q] + red[BM + q]);
+      }
+    } else if (s.ksplit > 1) {
+      double* ws = s.ws + (long)blockIdx.y * s.M * n_static;
+  #pragma unroll
+      for (int i = 0; i < T::MI; i++) {
+        const int r = m0 + wm + i * 8 + g;
+        if (r >= s.M) continue;
+  #pragma unroll
+        for (int j = 0; j < T::NJ; j++)
+  #pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int c = n0 + wn + j * 8 + 2 * t + h;
+            if (c < s.N) ws[(long)r * n_static + c] = acc[i][j][h];
+          }
+      }
+    } else {
+  #pragma unroll
+      for (int i = 0; i < T::MI; i++) {
+        const int r = m0 + wm + i * 8 + g;
+        if (r >= s.M) continue;
+  #pragma unroll
+        for (int j = 0; j < T::NJ; j++)
+  #pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int c = n0 + wn + j * 8 + 2 * t + h;
+            if (c < s.N) epi.store(r, c, acc[i][j][h]);
+          }
+      }
     }
   }
 }
@@ -365,15 +378,17 @@ void gemm_launch_tiled(const GemmShape& s, const Epi& epi, cudaStream_t st) {
   ProfScope prof("gemm_dmma", st);
   if (prof.tok >= 0) prof.flops = gemm_alg_flops(s, BM, BN);  // only for recorded (sampled) launches
   const int tiles = gemm_grid(s, BM, BN);
-  const dim3 grid(tiles, s.ksplit > 1 ? s.ksplit : 1);
+  const int cap = gemm_cta_cap();
+  const int ctas = cap > 0 ? std::max(1, std::min(tiles, cap / std::max(s.ksplit, 1))) : tiles;
+  const dim3 grid(ctas, s.ksplit > 1 ? s.ksplit : 1);
   if (gemm_vec2_ok(s)) {
     auto k = gemm_dmma_kernel<TA, TB, 2, Epi, BM, BN>;
     ensure_smem_attr((const void*)k, smem);
-    k<<<grid, G_THREADS, smem, st>>>(s, epi);
+    k<<<grid, G_THREADS, smem, st>>>(s, epi, tiles);
   } else {
     auto k = gemm_dmma_kernel<TA, TB, 1, Epi, BM, BN>;
     ensure_smem_attr((const void*)k, smem);
-    k<<<grid, G_THREADS, smem, st>>>(s, epi);
+    k<<<grid, G_THREADS, smem, st>>>(s, epi, tiles);
   }
   KOT_LAUNCH_CHECK();
   if constexpr (!Epi::kRowDot) {

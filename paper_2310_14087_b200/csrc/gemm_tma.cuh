@@ -27,6 +27,7 @@ namespace kot {
 
 constexpr int TMA_BK = 16;
 
+
 using TmaEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -134,10 +135,54 @@ __device__ __forceinline__ uint32_t tile_off(int r, int k) {
     return (uint32_t)(r * 128 + (((k >> 1) ^ (r & 7)) << 4) + (k & 1) * 8);
 }
 
+// Output tile t of the launch (symmetric launches enumerate the tiles with tm <= tn); false if t is
+// outside the matrix.  The K range follows the triangular-structure and split-K rules of the core.
+struct TmaTile {
+  int m0, n0, tn, kbeg, nkt;
+};
+template <int BM, int BN>
+__device__ __forceinline__ bool tma_tile(const GemmShape& s, int t, int tiles_m, int tiles_n, TmaTile& o) {
+  int tm, tn;
+  if (s.sym_tiles) {
+    tm = 0;
+    while (t >= tiles_n - tm) {
+      t -= tiles_n - tm;
+      ++tm;
+    }
+    tn = tm + t;
+  } else {
+    tm = t % tiles_m;
+    tn = t / tiles_m;
+  }
+  if (tm >= tiles_m || tn >= tiles_n) return false;
+  o.m0 = tm * BM;
+  o.n0 = tn * BN;
+  o.tn = tn;
+  int kbeg = 0, kend = s.K;
+  if (s.kb_m) kbeg = max(kbeg, o.m0);
+  if (s.kb_n) kbeg = max(kbeg, o.n0);
+  kbeg = max(kbeg, s.kstart);
+  if (s.ke_m) kend = min(kend, o.m0 + BM);
+  if (s.ke_n) kend = min(kend, o.n0 + BN);
+  kbeg = (kbeg / TMA_BK) * TMA_BK;
+  int nkt = kend > kbeg ? (kend - kbeg + TMA_BK - 1) / TMA_BK : 0;
+  if (s.ksplit > 1) {
+    const int per = (nkt + s.ksplit - 1) / s.ksplit;
+    const int t0 = blockIdx.y * per;
+    kbeg += t0 * TMA_BK;
+    nkt = max(0, min(per, nkt - t0));
+  }
+  o.kbeg = kbeg;
+  o.nkt = nkt;
+  return true;
+}
+
+// Tiles are processed in a loop (tile = blockIdx.x, += gridDim.x): a launch may use fewer CTAs than
+// tiles (gemm_cta_cap, background solver chains), the ring and its phases carry across tiles.
 template <bool TA, bool TB, int BM, int BN, int WM, int WN, int ST, class Epi>
 __global__ void __launch_bounds__(((BM / WM) * (BN / WN) + 1) * 32)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                    const __grid_constant__ CUtensorMap mapK, GemmShape s, Epi epi) {
+                    const __grid_constant__ CUtensorMap mapK, GemmShape s, Epi epi, int ntiles) {
   constexpr int NWN = BN / WN, NWC = (BM / WM) * NWN;  // consumer warps
   constexpr int MI = WM / 8, NJ = WN / 8;
   constexpr uint32_t A_BYTES = BM * TMA_BK * 8, B_BYTES = BN * TMA_BK * 8;
@@ -150,38 +195,10 @@ __global__ void __launch_bounds__(((BM / WM) * (BN / WN) + 1) * 32)
   double* Ks = reinterpret_cast<double*>(Bs + ST * B_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(Ks + ST * TMA_BK);
   uint64_t* empty = full + ST;
+  double* red = reinterpret_cast<double*>(empty + ST);  // [NWN][BM] row-dot combine (not in the ring)
 
   if (s.skipf != nullptr && *s.skipf != 0.0) return;
   const int tiles_n = (s.N + BN - 1) / BN, tiles_m = (s.M + BM - 1) / BM;
-  int tm, tn;
-  if (s.sym_tiles) {
-    int t = blockIdx.x;
-    tm = 0;
-    while (t >= tiles_n - tm) {
-      t -= tiles_n - tm;
-      ++tm;
-    }
-    tn = tm + t;
-  } else {
-    tm = blockIdx.x % tiles_m;
-    tn = blockIdx.x / tiles_m;
-  }
-  if (tm >= tiles_m || tn >= tiles_n) return;
-  const int m0 = tm * BM, n0 = tn * BN;
-  int kbeg = 0, kend = s.K;
-  if (s.kb_m) kbeg = max(kbeg, m0);
-  if (s.kb_n) kbeg = max(kbeg, n0);
-  kbeg = max(kbeg, s.kstart);
-  if (s.ke_m) kend = min(kend, m0 + BM);
-  if (s.ke_n) kend = min(kend, n0 + BN);
-  kbeg = (kbeg / TMA_BK) * TMA_BK;
-  int nkt = kend > kbeg ? (kend - kbeg + TMA_BK - 1) / TMA_BK : 0;
-  if (s.ksplit > 1) {
-    const int per = (nkt + s.ksplit - 1) / s.ksplit;
-    const int t0 = blockIdx.y * per;
-    kbeg += t0 * TMA_BK;
-    nkt = max(0, min(per, nkt - t0));
-  }
   const bool has_ks = s.kscale != nullptr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -196,143 +213,155 @@ __global__ void __launch_bounds__(((BM / WM) * (BN / WN) + 1) * 32)
   if (warp == NWC) {  // ---------------- producer: one elected lane issues the TMA copies
     if (lane == 0) {
       const uint32_t bytes = A_BYTES + B_BYTES + (has_ks ? TMA_BK * 8 : 0);
-      for (int kt = 0; kt < nkt; ++kt) {
-        const int q = kt % ST;
-        if (kt >= ST) mbar_wait(empty + q, ((kt / ST) & 1) ^ 1);
-        mbar_expect_tx(full + q, bytes);
-        const int k0 = kbeg + kt * TMA_BK;
-        if constexpr (TA) {
+      int g = 0;  // k-tiles issued so far (ring position across tiles)
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        TmaTile tl;
+        if (!tma_tile<BM, BN>(s, t, tiles_m, tiles_n, tl)) continue;
+        for (int kt = 0; kt < tl.nkt; ++kt, ++g) {
+          const int q = g % ST;
+          if (g >= ST) mbar_wait(empty + q, ((g / ST) & 1) ^ 1);
+          mbar_expect_tx(full + q, bytes);
+          const int k0 = tl.kbeg + kt * TMA_BK;
+          if constexpr (TA) {
 #pragma unroll
-          for (int sub = 0; sub < BM / 16; ++sub) tma_load_2d(As + q * A_BYTES + sub * 2048, &mapA, m0 + 16 * sub, k0, full + q);
-        } else {
-          tma_load_2d(As + q * A_BYTES, &mapA, k0, m0, full + q);
-        }
-        if constexpr (!TB) {
+            for (int sub = 0; sub < BM / 16; ++sub)
+              tma_load_2d(As + q * A_BYTES + sub * 2048, &mapA, tl.m0 + 16 * sub, k0, full + q);
+          } else {
+            tma_load_2d(As + q * A_BYTES, &mapA, k0, tl.m0, full + q);
+          }
+          if constexpr (!TB) {
 #pragma unroll
-          for (int sub = 0; sub < BN / 16; ++sub) tma_load_2d(Bs + q * B_BYTES + sub * 2048, &mapB, n0 + 16 * sub, k0, full + q);
-        } else {
-          tma_load_2d(Bs + q * B_BYTES, &mapB, k0, n0, full + q);
+            for (int sub = 0; sub < BN / 16; ++sub)
+              tma_load_2d(Bs + q * B_BYTES + sub * 2048, &mapB, tl.n0 + 16 * sub, k0, full + q);
+          } else {
+            tma_load_2d(Bs + q * B_BYTES, &mapB, k0, tl.n0, full + q);
+          }
+          if (has_ks) tma_load_1d(Ks + q * TMA_BK, &mapK, k0, full + q);
         }
-        if (has_ks) tma_load_1d(Ks + q * TMA_BK, &mapK, k0, full + q);
       }
     }
     return;
   }
 
   // ---------------- consumers
-  const int g = lane >> 2, t = lane & 3;
+  const int g8 = lane >> 2, t = lane & 3;
   const int wm = (warp / NWN) * WM, wn = (warp % NWN) * WN;
-  double acc[MI][NJ][2];
+  int g = 0;  // k-tiles consumed so far
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    TmaTile tl;
+    if (!tma_tile<BM, BN>(s, tile, tiles_m, tiles_n, tl)) continue;
+    double acc[MI][NJ][2];
 #pragma unroll
-  for (int i = 0; i < MI; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  for (int kt = 0; kt < nkt; ++kt) {
-    const int q = kt % ST;
-    mbar_wait(full + q, (kt / ST) & 1);
-    const uint32_t as = smem_u32(As + q * A_BYTES);
-    const uint32_t bs = smem_u32(Bs + q * B_BYTES);
-    const double* ks = Ks + q * TMA_BK;
-    auto step = [&](auto kks, auto has_kscale) {
-      constexpr int kk = decltype(kks)::value;
-      constexpr bool kKS = decltype(has_kscale)::value;
-      const int k = kk + t;
-      double a[MI], b[NJ];
-      double kscl = 1.0;
-      if constexpr (kKS) kscl = lds64(smem_u32(ks + k));
+    for (int kt = 0; kt < tl.nkt; ++kt, ++g) {
+      const int q = g % ST;
+      mbar_wait(full + q, (g / ST) & 1);
+      const uint32_t as = smem_u32(As + q * A_BYTES);
+      const uint32_t bs = smem_u32(Bs + q * B_BYTES);
+      const double* ks = Ks + q * TMA_BK;
+      auto step = [&](auto kks, auto has_kscale) {
+        constexpr int kk = decltype(kks)::value;
+        constexpr bool kKS = decltype(has_kscale)::value;
+        const int k = kk + t;
+        double a[MI], b[NJ];
+        double kscl = 1.0;
+        if constexpr (kKS) kscl = lds64(smem_u32(ks + k));
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const double av = lds64(as + tile_off<TA>(wm + frag_row<TA>(i, g8), k));
+          if constexpr (kKS)
+            a[i] = av * kscl;
+          else
+            a[i] = av;
+        }
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) b[j] = lds64(bs + tile_off<!TB>(wn + frag_row<!TB>(j, g8), k));
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      };
+      auto stage = [&](auto has_kscale) {
+        step(std::integral_constant<int, 0>{}, has_kscale);
+        step(std::integral_constant<int, 4>{}, has_kscale);
+        step(std::integral_constant<int, 8>{}, has_kscale);
+        step(std::integral_constant<int, 12>{}, has_kscale);
+      };
+      if (has_ks)
+        stage(std::true_type{});
+      else
+        stage(std::false_type{});
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + q);
+    }
+
+    // ---------------- epilogue (same semantics as gemm_dmma_kernel)
+    const int m0 = tl.m0, n0 = tl.n0;
+    auto row_of = [&](int i) { return m0 + wm + frag_row<TA>(i, g8); };
+    auto col_of = [&](int j, int h) { return n0 + wn + frag_row<!TB>(j, 2 * t + h); };
+    if constexpr (Epi::kRowDot) {
+      // partial[r] = Σ_{c in this 64-column tile} acc(r,c)·E(r,c): 4-lane shuffle + cross-warp smem combine
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
-        const double av = lds64(as + tile_off<TA>(wm + frag_row<TA>(i, g), k));
-        if constexpr (kKS)
-          a[i] = av * kscl;
-        else
-          a[i] = av;
+        const int r = row_of(i);
+        double p = 0.0;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = col_of(j, h);
+            if (r < s.M && c < s.N) p += acc[i][j][h] * epi.rowdot_weight(r, c);
+          }
+        p += __shfl_xor_sync(0xffffffffu, p, 1);
+        p += __shfl_xor_sync(0xffffffffu, p, 2);
+        if (t == 0) red[(warp % NWN) * BM + (r - m0)] = p;
       }
+      asm volatile("bar.sync 1, %0;\n" ::"r"(NWC * 32) : "memory");
+      for (int qq = threadIdx.x; qq < BM; qq += NWC * 32) {
+        const int r = m0 + qq;
+        double v = 0.0;
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) b[j] = lds64(bs + tile_off<!TB>(wn + frag_row<!TB>(j, g), k));
+        for (int w = 0; w < NWN; ++w) v += red[w * BM + qq];
+        if (r < s.M) epi.rowdot_store(tl.tn + (int)blockIdx.y * tiles_n, r, v);
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"r"(NWC * 32) : "memory");  // red is reused by the next tile
+    } else if (s.ksplit > 1) {
+      double* ws = s.ws + (long)blockIdx.y * s.M * s.N;
 #pragma unroll
-      for (int i = 0; i < MI; ++i)
+      for (int i = 0; i < MI; ++i) {
+        const int r = row_of(i);
+        if (r >= s.M) continue;
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-    };
-    auto stage = [&](auto has_kscale) {
-      step(std::integral_constant<int, 0>{}, has_kscale);
-      step(std::integral_constant<int, 4>{}, has_kscale);
-      step(std::integral_constant<int, 8>{}, has_kscale);
-      step(std::integral_constant<int, 12>{}, has_kscale);
-    };
-    if (has_ks)
-      stage(std::true_type{});
-    else
-      stage(std::false_type{});
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + q);
-  }
-
-  // ---------------- epilogue (same semantics as gemm_dmma_kernel)
-  auto row_of = [&](int i) { return m0 + wm + frag_row<TA>(i, g); };
-  auto col_of = [&](int j, int h) { return n0 + wn + frag_row<!TB>(j, 2 * t + h); };
-  if constexpr (Epi::kRowDot) {
-    // partial[r] = Σ_{c in this 64-column tile} acc(r,c)·E(r,c): 4-lane shuffle + cross-warp smem combine.
-    asm volatile("bar.sync 1, %0;\n" ::"r"(NWC * 32) : "memory");  // every consumer is done with the ring
-    double* red = reinterpret_cast<double*>(tsm);  // [NWN][BM]
+        for (int j = 0; j < NJ; ++j)
 #pragma unroll
-    for (int i = 0; i < MI; ++i) {
-      const int r = row_of(i);
-      double p = 0.0;
+          for (int h = 0; h < 2; ++h) {
+            const int c = col_of(j, h);
+            if (c < s.N) ws[(long)r * s.N + c] = acc[i][j][h];
+          }
+      }
+    } else {
 #pragma unroll
-      for (int j = 0; j < NJ; ++j)
+      for (int i = 0; i < MI; ++i) {
+        const int r = row_of(i);
+        if (r >= s.M) continue;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = col_of(j, h);
-          if (r < s.M && c < s.N) p += acc[i][j][h] * epi.rowdot_weight(r, c);
-        }
-      p += __shfl_xor_sync(0xffffffffu, p, 1);
-      p += __shfl_xor_sync(0xffffffffu, p, 2);
-      if (t == 0) red[(warp % NWN) * BM + (r - m0)] = p;
-    }
-    asm volatile("bar.sync 1, %0;\n" ::"r"(NWC * 32) : "memory");
-    for (int qq = threadIdx.x; qq < BM; qq += NWC * 32) {
-      const int r = m0 + qq;
-      double v = 0.0;
+        for (int j = 0; j < NJ; ++j)
 #pragma unroll
-      for (int w = 0; w < NWN; ++w) v += red[w * BM + qq];
-      if (r < s.M) epi.rowdot_store(tn + (int)blockIdx.y * tiles_n, r, v);
-    }
-  } else if (s.ksplit > 1) {
-    double* ws = s.ws + (long)blockIdx.y * s.M * s.N;
-#pragma unroll
-    for (int i = 0; i < MI; ++i) {
-      const int r = row_of(i);
-      if (r >= s.M) continue;
-#pragma unroll
-      for (int j = 0; j < NJ; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = col_of(j, h);
-          if (c < s.N) ws[(long)r * s.N + c] = acc[i][j][h];
-        }
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < MI; ++i) {
-      const int r = row_of(i);
-      if (r >= s.M) continue;
-#pragma unroll
-      for (int j = 0; j < NJ; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = col_of(j, h);
-          if (c < s.N) epi.store(r, c, acc[i][j][h]);
-        }
+          for (int h = 0; h < 2; ++h) {
+            const int c = col_of(j, h);
+            if (c < s.N) epi.store(r, c, acc[i][j][h]);
+          }
+      }
     }
   }
 }
 
 template <int BM, int BN, int ST>
 constexpr int tma_smem_bytes() {
-  return ST * (BM + BN) * TMA_BK * 8 + ST * TMA_BK * 8 + 2 * ST * 8 + 1024;
+  return ST * (BM + BN) * TMA_BK * 8 + ST * TMA_BK * 8 + 2 * ST * 8 + BM * (BN / 32) * 8 + 1024;
 }
 
 // TMA-staged launch; returns false (nothing launched) when the operands do not qualify (device-side
@@ -359,10 +388,12 @@ bool gemm_launch_tma(const GemmShape& s, const Epi& epi, cudaStream_t st) {
   if (prof.tok >= 0) prof.flops = gemm_alg_flops(s, BM, BN);
   const int tm = (s.M + BM - 1) / BM, tn = (s.N + BN - 1) / BN;
   const int tiles = s.sym_tiles ? tm * (tm + 1) / 2 : tm * tn;
-  const dim3 grid(tiles, s.ksplit > 1 ? s.ksplit : 1);
+  const int cap = gemm_cta_cap();
+  const int ctas = cap > 0 ? std::max(1, std::min(tiles, cap / std::max(s.ksplit, 1))) : tiles;
+  const dim3 grid(ctas, s.ksplit > 1 ? s.ksplit : 1);
   auto k = gemm_tma_kernel<TA, TB, BM, BN, WM, WN, ST, Epi>;
   ensure_smem_attr((const void*)k, smem);
-  k<<<grid, threads, smem, st>>>(ma, mb, mk, s, epi);
+  k<<<grid, threads, smem, st>>>(ma, mb, mk, s, epi, tiles);
   KOT_LAUNCH_CHECK();
   if constexpr (!Epi::kRowDot) {
     if (s.ksplit > 1) {

@@ -137,6 +137,87 @@ static bool eg_parallel() {
   return v != 0;
 }
 
+// Experimental (KOT_L2_PERSIST=<MB>): keep the CG matvec's packed sign blocks of B resident in L2
+// (access-policy window on the Newton stream) while the EG chain's eigensolves stream through L2.
+struct L2Window {
+  cudaStream_t st = nullptr;
+  L2Window(Problem& p, const MvCtx& mv) {
+    static const long mb = [] {
+      const char* e = std::getenv("KOT_L2_PERSIST");
+      return e ? std::atol(e) : 0L;
+    }();
+    if (mb <= 0 || !mv.hform) return;
+    static std::once_flag once;
+    std::call_once(once, [] { cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mb << 20); });
+    cudaStreamAttrValue a{};
+    a.accessPolicyWindow.base_ptr = const_cast<double*>(mv.Bs);
+    a.accessPolicyWindow.num_bytes = std::min<size_t>((size_t)mb << 20, sizeof(double) * (size_t)p.n * mv.ldp);
+    a.accessPolicyWindow.hitRatio = 1.0f;
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    if (cudaStreamSetAttribute(p.st, cudaStreamAttributeAccessPolicyWindow, &a) == cudaSuccess) st = p.st;
+    (void)cudaGetLastError();
+  }
+  ~L2Window() {
+    if (!st) return;
+    cudaStreamAttrValue a{};
+    a.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
+    cudaCtxResetPersistingL2Cache();
+    (void)cudaGetLastError();
+  }
+};
+
+// CUDA-graph replay of the batched CG steps (KOT_CG_GRAPH=0: direct launches).
+static bool cg_graphs() {
+  static const bool v = [] {
+    const char* e = std::getenv("KOT_CG_GRAPH");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return v;
+}
+
+// The graph of one batch for the current matvec context; re-captured when the context changes (one
+// Newton step: new decomposition, μ, sign blocks), updated in place when the topology allows it.
+template <class F>
+static void cg_graph_launch(Problem& p, const MvCtx& mv, int batch, F&& enqueue) {
+  CgGraph& g = p.cg_graph;
+  const CgGraphKey key{mv.Bs, mv.Bo, mv.ldp, mv.H, mv.dc.vals, mv.dc.k, mv.pos, mv.mu, batch};
+  if (!g.exec || !(g.key == key)) {
+    const long l0 = g_kot_launches.load();
+    cudaGraph_t graph = nullptr;
+    prof_capturing() = true;
+    KOT_CUDA(cudaStreamBeginCapture(p.st, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue();
+    } catch (...) {
+      cudaStreamEndCapture(p.st, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      prof_capturing() = false;
+      throw;
+    }
+    KOT_CUDA(cudaStreamEndCapture(p.st, &graph));
+    prof_capturing() = false;
+    g.kernels = g_kot_launches.load() - l0;
+    g_kot_launches -= g.kernels;  // counted when the graph runs
+    bool updated = false;
+    if (g.exec) {
+      cudaGraphExecUpdateResultInfo info{};
+      updated = cudaGraphExecUpdate(g.exec, graph, &info) == cudaSuccess;
+      if (!updated) {
+        (void)cudaGetLastError();
+        cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+      }
+    }
+    if (!updated) KOT_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+    KOT_CUDA(cudaGraphDestroy(graph));
+    g.key = key;
+  }
+  KOT_CUDA(cudaGraphLaunch(g.exec, p.st));
+  g_kot_launches += g.kernels;
+}
+
 struct CgOut {
   int iters;
   double res;
@@ -164,13 +245,23 @@ static CgOut cg_solve(Problem& p, const MvCtx& mv, const double* rhs, double tol
     cg_arm_kernel<<<1, 1, 0, p.st>>>(p.dsc, target, max_iter);
     KOT_LAUNCH_CHECK();
     const double* done = p.dsc + SC_DONE;
-    int launched = 0;
-    for (;;) {
-      for (int bq = 0; bq < kBatch && launched < max_iter; ++bq, ++launched) {
+    auto enqueue_batch = [&]() {
+      for (int bq = 0; bq < kBatch; ++bq) {
         middle_operator_fast(p, mv, b.cp, b.cap, done);
         cg_step_kernel<<<1, CG_THREADS, 0, p.st>>>(n, b.cx, b.cr, b.cp, b.cap, p.dsc, 1);
         KOT_LAUNCH_CHECK();
       }
+    };
+    int launched = 0;
+    for (;;) {
+      // The device applies the stopping rule (launches after the stop are no-ops, the step limit is
+      // SC_MAXIT), so every batch is the same kernel sequence: after the first batch (which also
+      // sets every kernel attribute) it is replayed as one CUDA graph per Newton step.
+      if (launched == 0 || !cg_graphs())
+        enqueue_batch();
+      else
+        cg_graph_launch(p, mv, kBatch, enqueue_batch);
+      launched += kBatch;
       fetch(p, SC_MAXIT + 1);
       const bool stop = p.hsc[SC_DONE] != 0.0 || launched >= max_iter;
       const int it = (int)p.hsc[SC_IT];
@@ -325,6 +416,7 @@ NewtonOut newton_direction(Problem& p, const double* r1, const double* r2, doubl
   KOT_CUDA(cudaMemsetAsync(b.sol, 0, sizeof(double) * n, p.st));
   KOT_CUDA(cudaStreamWaitEvent(p.st, p.ev_mv1, 0));
   ppre.reset();
+  L2Window l2w(p, mv);
   NewtonOut out{0, 0, 0, INFINITY, 0.0, 0.0};
   const auto t0 = clk::now();
   bool pending = false;  // criterion of attempt `att − 1` in flight on q
@@ -477,6 +569,15 @@ static void copy_state(Problem& p, Bufs& b, Decomp& dw, const Decomp& dv) {
 // steps, thread B: residual at v_j), and the solve loop consumes slot j at the
 // iteration whose safeguard step produces v_j.  Same operations, same values,
 // same acceptance logic; only the schedule changes (3 concurrent chains).
+// CTAs per GEMM launch on the EG-chain threads (KOT_BG_GEMM_CTAS; 0 = uncapped): see gemm_cta_cap.
+static int bg_gemm_ctas() {
+  static const int v = [] {
+    const char* e = std::getenv("KOT_BG_GEMM_CTAS");
+    return e ? std::max(0, std::atoi(e)) : 0;
+  }();
+  return v;
+}
+
 struct EgSlot {
   double *g = nullptr, *X = nullptr, *r1 = nullptr, *r2 = nullptr, *P = nullptr, *vals = nullptr;
   int k = 0;
@@ -558,6 +659,7 @@ class EgPipeline {
   std::thread ta_, tb_;
 
   void run_steps(Problem& a) {
+    gemm_cta_cap() = bg_gemm_ctas();
     for (int j = 1;; ++j) {
       {
         std::unique_lock<std::mutex> lk(mu_);
@@ -597,6 +699,7 @@ class EgPipeline {
   }
 
   void run_residuals(Problem& b) {
+    gemm_cta_cap() = bg_gemm_ctas();
     for (int j = 1;; ++j) {
       {
         std::unique_lock<std::mutex> lk(mu_);
@@ -667,6 +770,7 @@ static bool loop_body(Problem& p, const SolverCfg& cfg, LoopState& s, int k, Ite
     Problem& a = p.aux();
     eg_thread = std::thread([&]() {
       try {
+        gemm_cta_cap() = bg_gemm_ctas();
         KOT_CUDA(cudaSetDevice(a.device));
         auto t0 = clk::now();
         eg_step(a, b.gv, b.Xv, cfg.eg_stepsize, b.gv, b.Xv);

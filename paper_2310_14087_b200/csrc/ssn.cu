@@ -70,6 +70,7 @@ Problem::~Problem() {
   if (ev_mv0) cudaEventDestroy(ev_mv0);
   if (ev_mv1) cudaEventDestroy(ev_mv1);
   if (ev_rhs) cudaEventDestroy(ev_rhs);
+  if (cg_graph.exec) cudaGraphExecDestroy(cg_graph.exec);
   eig.reset();
   for (double* p : owned) dev_free(p);
   host_free_pinned(hsc, 64 * sizeof(double));
@@ -922,8 +923,10 @@ void eg_step_parallel(Problem& p, Problem& c, const double* g, const double* X, 
   KOT_CUDA(cudaEventRecord(p.ev_half, p.st));
   // second projection on c:  X_out = Π(X − s (Φ*(γ½) + λ₁I))
   std::exception_ptr err = nullptr;
+  const int cta_cap = gemm_cta_cap();  // a background caller's GEMM cap applies to its helper too
   std::thread helper([&] {
     try {
+      gemm_cta_cap() = cta_cap;
       KOT_CUDA(cudaSetDevice(c.device));
       KOT_CUDA(cudaStreamWaitEvent(c.st, p.ev_half, 0));
       Decomp dc2{c.M2, c.M3, 0};

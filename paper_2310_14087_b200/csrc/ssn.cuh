@@ -43,6 +43,26 @@ struct Bufs {
   double* Bp;            // n×(n+2): B's sign blocks packed [smaller | other], 16-B aligned
 };
 
+// CUDA graph of one batch of CG steps (solver.cu) and the matvec context it was captured for.
+struct CgGraphKey {
+  const double *Bs = nullptr, *Bo = nullptr;
+  long ldp = 0;
+  const double *H = nullptr, *vals = nullptr;
+  int k = -1;
+  bool pos = false;
+  double mu = 0.0;
+  int batch = 0;
+  bool operator==(const CgGraphKey& o) const {
+    return Bs == o.Bs && Bo == o.Bo && ldp == o.ldp && H == o.H && vals == o.vals && k == o.k && pos == o.pos &&
+           mu == o.mu && batch == o.batch;
+  }
+};
+struct CgGraph {
+  cudaGraphExec_t exec = nullptr;
+  CgGraphKey key;
+  long kernels = 0;
+};
+
 struct Problem {
   int n = 0;
   int device = 0;
@@ -98,7 +118,8 @@ struct Problem {
   cudaEvent_t crit_done = nullptr, crit_after = nullptr, crit_dx_done = nullptr;
   cudaEvent_t ev_half = nullptr;  // eg_step_parallel: γ½ ready
   cudaEvent_t ev_mv0 = nullptr, ev_mv1 = nullptr;  // newton_direction: matvec_prepare on the crit stream
-  cudaEvent_t ev_rhs = nullptr;                    // newton_direction: next attempt's rhs ready
+  cudaEvent_t ev_rhs = nullptr;
+  CgGraph cg_graph;                    // newton_direction: next attempt's rhs ready
   bool with_eig = true;
   double* alloc(long count);
   void init_scratch();
