@@ -422,7 +422,9 @@ void gemm_launch(const GemmShape& s, const Epi& epi, cudaStream_t st) {
   // everything — NN 2000³ 32.7 TF/s vs 27.2 on the cp.async core, cuBLAS 33.0 — except the row-dot
   // products, whose tall M×(k) shapes prefer 128×64 with eight warps: CG matvec GEMM2 27.8 vs 22.5)
   if (mode > 0 && s.K >= 2 * TMA_BK && (long)s.M * s.N >= 64L * 64) {
-    const bool tall = Epi::kRowDot && !s.sym_tiles && s.M >= 1024;
+    // 128×64 CTAs hold one SM each (288 threads × 122 registers): only when there are enough of them
+    const long tiles128 = (long)((s.M + 127) / 128) * ((s.N + 63) / 64) * std::max(s.ksplit, 1);
+    const bool tall = Epi::kRowDot && !s.sym_tiles && s.M >= 1024 && tiles128 >= 200;
     if (tall ? gemm_launch_tma<TA, TB, 128, 64, 32, 32, 4>(s, epi, st)
              : gemm_launch_tma<TA, TB, 64, 64, 32, 32, 4>(s, epi, st))
       return;

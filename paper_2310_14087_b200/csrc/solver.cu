@@ -30,7 +30,9 @@ static double ms_since(clk::time_point t0) {
 
 // ------------------------------------------------------------------- CG
 
-constexpr int CG_THREADS = 1024;
+// 256, not 1024: the single-CTA update must fit beside the resident panel and GEMM CTAs of the other
+// chains (a 1024-thread CTA needs a nearly empty SM and waited for one inside the solver)
+constexpr int CG_THREADS = 256;
 // scalar slots in p.dsc used by CG
 constexpr int SC_RR = 8, SC_BN = 9, SC_PAP = 10, SC_RES = 11, SC_FLAG = 12;
 // batched CG (device-side stopping): done flag, completed steps, target residual, step limit

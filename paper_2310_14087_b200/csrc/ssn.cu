@@ -575,6 +575,15 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allo
   }
 }
 
+// CTAs a CG-matvec GEMM should have to fill every SM (KOT_MV_CTAS, default 2.5 per SM)
+static int mv_target_ctas() {
+  static const int v = [] {
+    const char* e = std::getenv("KOT_MV_CTAS");
+    return e ? std::max(1, std::atoi(e)) : (5 * kNumSMs) / 2;
+  }();
+  return v;
+}
+
 // y = Qv/(2λ₂) + μv + (Hv)/μ + Σ_{a∈α, b∈ᾱ} 2ξ_ab (B_{:,a}∘B_{:,b})·C_ab,  C = Bᵀdiag(v)B
 // (one process, no row blocks): two DMMA GEMMs of 2·k(ℓ−k)·ℓ FLOPs each + two GEMVs.
 static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, double* out,
@@ -595,11 +604,16 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
     s.skipf = skipf;
     s.ws = p.splitws;
     s.ksplit = choose_ksplit(s, p.splitws_cap);
+    // split-K so that the launch has enough CTAs to spread over every SM: the sign-block split k
+    // moves every iteration, and e.g. 162 tiles on 148 SMs leave 14 SMs with twice the work (ncu:
+    // tensor pipe 61 % active); KOT_MV_SPLIT forces a factor
     static const int mv_split = [] {
       const char* e = std::getenv("KOT_MV_SPLIT");
-      return e ? std::atoi(e) : 1;  // TMA core: no split-K on the H-form GEMM1 (14.08 vs 13.85 it/s)
+      return e ? std::atoi(e) : 0;
     }();
-    if (mv_split > 1 && (long)mv_split * s.M * s.N <= p.splitws_cap) s.ksplit = mv_split;
+    const int t1 = ceil_div(ks, GB_M) * ceil_div(ns, GB_N);
+    const int sp1 = mv_split > 0 ? mv_split : std::min(4, std::max(1, ceil_div(mv_target_ctas(), t1)));
+    if (sp1 > 1 && (long)sp1 * s.M * s.N <= p.splitws_cap) s.ksplit = sp1;
     gemm_launch<true, false>(s, EpiMvOff{Ct, n, m.dc.vals, k, m.pos ? 1 : 0, m.mu}, p.st);
     GemmShape s2 = make_shape(n, ks, ns, Bo, ld, Ct, n);
     s2.skipf = skipf;
@@ -607,10 +621,11 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
     // order by finalize); KOT_MV2_SPLIT=2 measured neutral inside the solver (12.66 vs 12.68 it/s)
     static const int mv2_split = [] {
       const char* e = std::getenv("KOT_MV2_SPLIT");
-      return e ? std::max(1, std::atoi(e)) : 1;
+      return e ? std::max(0, std::atoi(e)) : 0;
     }();
-    s2.ksplit = (mv2_split > 1 && (long)mv2_split * ceil_div(ks, GB_N) <= ceil_div(n, GB_N) && ns >= 256 * mv2_split)
-                    ? mv2_split : 1;
+    const int t2 = ceil_div(n, GB_M) * ceil_div(ks, GB_N);
+    const int sp2 = mv2_split > 0 ? mv2_split : std::min(2, std::max(1, ceil_div(mv_target_ctas(), t2)));
+    s2.ksplit = (sp2 > 1 && (long)sp2 * ceil_div(ks, GB_N) <= ceil_div(n, GB_N) && ns >= 256 * sp2) ? sp2 : 1;
     gemm_launch<false, true>(s2, EpiRowDot{Bs, ld, p.partial, n}, p.st);
     rd_tiles = ceil_div(ks, GB_N) * s2.ksplit;
   }
