@@ -331,7 +331,8 @@ def run_gpu(args):
            "window": f"iterations {args.warmup}..{n_e2e - 1}; timed region = the whole call minus the "
                      f"{args.warmup} warm-up iterations' own step time ({warm_ms:.1f} ms)",
            "first_solve_in_process": True, "wall_ms": round(t_call * 1e3, 1), "assemble_ms": round(t_asm * 1e3, 1),
-           "setup_ms": round(rep.total_ms - sum(r.step_ms for r in rep.trace), 1)}
+           "setup_ms": round(rep.total_ms - sum(r.step_ms for r in rep.trace), 1),
+           "step_ms": [round(r.step_ms, 1) for r in rep.trace]}
 
     # ---------------- device-resident timed region (value)
     cfg = K.SolverConfig(newton=newton_cfg(args.profile), eg=K.EgConfig(stepsize), residual_tol=1e-300,

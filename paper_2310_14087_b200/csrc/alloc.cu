@@ -16,9 +16,26 @@ std::mutex g_mu;
 std::map<int, cudaStream_t> g_alloc_stream;              // per device, non-blocking
 std::map<size_t, std::vector<void*>> g_pinned_free;     // size → cached pinned buffers
 
+// Optional (KOT_CARVEOUT=1; default off, measured): the kernels with large dynamic shared memory (GEMM
+// cores, sytrd panel / tail, D&C, two-stage) prefer the maximum shared-memory carveout.  An SM takes a CTA only if its
+// current L1/shared split leaves room: under per-kernel defaults an SM brought up for a 64 KB panel
+// CTA could not take the CG GEMMs' CTAs beside it (measured with idle 64 KB CTAs on another stream:
+// Newton chain 27.3 → 30.7 ms; with the max-shared preference 28.6).  Kernels without dynamic shared
+// memory keep the default (max L1): a device-wide PreferShared cost the eigensolver its L1 (trial
+// residual 27.5 → 28.6 ms).  Inside the solver the per-kernel preference is neutral to slightly worse
+// (cfg3 15.1 vs 15.3 it/s), so it stays off.
+bool carveout_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("KOT_CARVEOUT");
+    return e && std::atoi(e) > 0;
+  }();
+  return on;
+}
+
 cudaStream_t alloc_stream_locked(int dev) {
   auto it = g_alloc_stream.find(dev);
   if (it != g_alloc_stream.end()) return it->second;
+
   cudaMemPool_t pool;
   KOT_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
   unsigned long long keep = ~0ull;  // never trim the pool behind our back
@@ -177,6 +194,8 @@ void ensure_smem_attr(const void* func, int bytes, bool nonportable_cluster) {
   std::lock_guard<std::mutex> lk(g_mu);
   int& have = g_smem_attr[{dev, func}];
   if (have >= bytes && have > 0) return;
+  if (carveout_on() && have == 0)
+    KOT_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
   if (nonportable_cluster) KOT_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   if (bytes > 48 * 1024) KOT_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   have = std::max(bytes, 1);
