@@ -44,9 +44,15 @@ struct Cancelled {};
 // Every kernel launch of the library goes through KOT_LAUNCH_CHECK (counted:
 // kot_launch_count() backs bench.py's "gpu_launches").
 extern std::atomic<long long> g_kot_launches;
+// launches by the calling thread (graph capture counts its own kernels with it)
+inline long long& thread_launches() {
+  static thread_local long long n = 0;
+  return n;
+}
 #define KOT_LAUNCH_CHECK()                     \
   do {                                         \
     ::kot::g_kot_launches.fetch_add(1);        \
+    ++::kot::thread_launches();                \
     KOT_CUDA(cudaGetLastError());              \
   } while (0)
 

@@ -932,83 +932,98 @@ __global__ void dc_split_kernel(double* d, const double* e, const int* splits, i
   }
 }
 
-// Leaves: implicit QL (tqli) on a ≤32 tridiagonal, one warp per leaf.  Every
-// lane runs the scalar recurrence redundantly; lane k owns row k of Z.
-__global__ void dc_leaf_kernel(double* d, const double* e, const int* leaf_off, const int* leaf_len, int nleaves,
-                               double* Q, int ldq, int* err) {
-  const int leaf = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+// Leaves: implicit QL (tqli) on a ≤32 tridiagonal, one warp per leaf, without local memory: lane i
+// holds d[i], e[i] in registers (the recurrence reads them by warp broadcast, only lanes i, i+1 write),
+// every lane runs the scalar recurrence redundantly (identical values), and the eigenvector matrix
+// lives in shared memory column-major (column i = 32 consecutive doubles, lane k owns row k), so each
+// rotation is two conflict-free shared accesses per lane.  Same arithmetic as the textbook tqli
+// (dlaeq-free, the leaves are ≤ 32), eigenvalues finally ranked ascending (ties by index).
+constexpr int LEAF_WARPS = 4;
+__global__ void __launch_bounds__(32 * LEAF_WARPS) dc_leaf_kernel(double* d, const double* e, const int* leaf_off,
+                                                                   const int* leaf_len, int nleaves, double* Q,
+                                                                   int ldq, int* err) {
+  __shared__ double zsh[LEAF_WARPS][DC_LEAF * DC_LEAF];
+  const int w = threadIdx.x >> 5;
+  const int leaf = blockIdx.x * LEAF_WARPS + w;
   if (leaf >= nleaves) return;
   const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
   const int o = leaf_off[leaf], m = leaf_len[leaf];
-  double dd[DC_LEAF], ee[DC_LEAF], z[DC_LEAF];
-  for (int i = 0; i < m; ++i) {
-    dd[i] = d[o + i];
-    ee[i] = (i < m - 1) ? e[o + i] : 0.0;
-    z[i] = (i == lane) ? 1.0 : 0.0;
-  }
-  for (int l = 0; l < m; ++l) {
+  double* Z = zsh[w];  // Z[i*32 + k] = row k, column i
+  double D = lane < m ? d[o + lane] : 0.0;
+  double E = lane < m - 1 ? e[o + lane] : 0.0;
+  for (int i = 0; i < m; ++i) Z[i * 32 + lane] = (i == lane) ? 1.0 : 0.0;
+  __syncwarp();
+  auto dget = [&](int i) { return __shfl_sync(full, D, i); };
+  auto eget = [&](int i) { return __shfl_sync(full, E, i); };
+  bool failed = false;
+  for (int l = 0; l < m && !failed; ++l) {
     int iter = 0, mm;
     do {
       for (mm = l; mm < m - 1; ++mm) {
-        const double sd = fabs(dd[mm]) + fabs(dd[mm + 1]);
-        if (fabs(ee[mm]) + sd == sd) break;
+        const double sd = fabs(dget(mm)) + fabs(dget(mm + 1));
+        if (fabs(eget(mm)) + sd == sd) break;
       }
       if (mm != l) {
         if (iter++ == 60) {
-          if (lane == 0) atomicExch(err, 1);
+          failed = true;
           break;
         }
-        double g = (dd[l + 1] - dd[l]) / (2.0 * ee[l]);
+        const double el = eget(l), dl = dget(l);
+        double g = (dget(l + 1) - dl) / (2.0 * el);
         double r = hypot(g, 1.0);
-        g = dd[mm] - dd[l] + ee[l] / (g + copysign(r, g));
+        g = dget(mm) - dl + el / (g + copysign(r, g));
         double s = 1.0, c = 1.0, p = 0.0;
         int i;
+        bool early = false;
         for (i = mm - 1; i >= l; --i) {
-          double f = s * ee[i];
-          const double b = c * ee[i];
+          const double ei = eget(i), di = dget(i), dip = dget(i + 1);
+          double f = s * ei;
+          const double b = c * ei;
           r = hypot(f, g);
-          ee[i + 1] = r;
+          if (lane == i + 1) E = r;
           if (r == 0.0) {
-            dd[i + 1] -= p;
-            ee[mm] = 0.0;
+            if (lane == i + 1) D = dip - p;
+            if (lane == mm) E = 0.0;
+            early = true;
             break;
           }
           s = f / r;
           c = g / r;
-          g = dd[i + 1] - p;
-          r = (dd[i] - g) * s + 2.0 * c * b;
+          g = dip - p;
+          r = (di - g) * s + 2.0 * c * b;
           p = s * r;
-          dd[i + 1] = g + p;
+          if (lane == i + 1) D = g + p;
           g = c * r - b;
-          f = z[i + 1];
-          z[i + 1] = s * z[i] + c * f;
-          z[i] = c * z[i] - s * f;
+          const double z0 = Z[i * 32 + lane], z1 = Z[(i + 1) * 32 + lane];
+          Z[(i + 1) * 32 + lane] = s * z0 + c * z1;
+          Z[i * 32 + lane] = c * z0 - s * z1;
         }
-        if (r == 0.0 && i >= l) continue;
-        dd[l] -= p;
-        ee[l] = g;
-        ee[mm] = 0.0;
+        if (early) continue;
+        if (lane == l) {
+          D -= p;
+          E = g;
+        }
+        if (lane == mm) E = 0.0;
       }
     } while (mm != l);
   }
-  // ascending selection sort (lane-redundant on dd, each lane permutes its row)
-  for (int i = 0; i < m - 1; ++i) {
-    int kmin = i;
-    for (int j = i + 1; j < m; ++j)
-      if (dd[j] < dd[kmin]) kmin = j;
-    if (kmin != i) {
-      const double t = dd[i];
-      dd[i] = dd[kmin];
-      dd[kmin] = t;
-      const double tz = z[i];
-      z[i] = z[kmin];
-      z[kmin] = tz;
-    }
+  if (failed) {
+    if (lane == 0) atomicExch(err, 1);
+    return;
   }
-  if (lane < m)
-    for (int i = 0; i < m; ++i) Q[(long)(o + lane) * ldq + o + i] = z[i];
-  if (lane == 0)
-    for (int i = 0; i < m; ++i) d[o + i] = dd[i];
+  __syncwarp();
+  // ascending order: rank of lane's eigenvalue (ties broken by index), eigenvector columns follow
+  int rank = 0;
+  for (int j = 0; j < m; ++j) {
+    const double dj = dget(j);
+    rank += (dj < D) || (dj == D && j < lane);
+  }
+  if (lane < m) d[o + rank] = D;
+  for (int i = 0; i < m; ++i) {
+    const int ri = __shfl_sync(full, rank, i);
+    if (lane < m) Q[(long)(o + lane) * ldq + o + ri] = Z[i * 32 + lane];
+  }
 }
 
 constexpr int MS = 8;  // meta ints per merge: K, ndefl, nrot, c1 (top-only), c12 (top-only + mixed)
@@ -1628,7 +1643,7 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
   }
   const int nleaves = (int)loff.size();
   ProfScope ps_leaf("dc.leaf", st);
-  dc_leaf_kernel<<<ceil_div(nleaves, 4), 128, 0, st>>>(w.d, w.e, dloff, dllen, nleaves, w.Q, n, err);
+  dc_leaf_kernel<<<ceil_div(nleaves, LEAF_WARPS), 32 * LEAF_WARPS, 0, st>>>(w.d, w.e, dloff, dllen, nleaves, w.Q, n, err);
   KOT_LAUNCH_CHECK();
   // all levels' merge descriptors uploaded once; each level gets its own meta region, so the
   // whole merge tree runs without a host round trip (kernels read K from device memory)

@@ -186,7 +186,7 @@ static void cg_graph_launch(Problem& p, const MvCtx& mv, int batch, F&& enqueue)
   CgGraph& g = p.cg_graph;
   const CgGraphKey key{mv.Bs, mv.Bo, mv.ldp, mv.H, mv.dc.vals, mv.dc.k, mv.pos, mv.mu, batch};
   if (!g.exec || !(g.key == key)) {
-    const long l0 = g_kot_launches.load();
+    const long long l0 = thread_launches();
     cudaGraph_t graph = nullptr;
     prof_capturing() = true;
     KOT_CUDA(cudaStreamBeginCapture(p.st, cudaStreamCaptureModeThreadLocal));
@@ -200,8 +200,8 @@ static void cg_graph_launch(Problem& p, const MvCtx& mv, int batch, F&& enqueue)
     }
     KOT_CUDA(cudaStreamEndCapture(p.st, &graph));
     prof_capturing() = false;
-    g.kernels = g_kot_launches.load() - l0;
-    g_kot_launches -= g.kernels;  // counted when the graph runs
+    g.kernels = thread_launches() - l0;  // this thread's captured kernels (other threads keep launching)
+    g_kot_launches -= g.kernels;        // counted when the graph runs
     bool updated = false;
     if (g.exec) {
       cudaGraphExecUpdateResultInfo info{};

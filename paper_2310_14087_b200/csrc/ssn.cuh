@@ -60,7 +60,7 @@ struct CgGraphKey {
 struct CgGraph {
   cudaGraphExec_t exec = nullptr;
   CgGraphKey key;
-  long kernels = 0;
+  long long kernels = 0;
 };
 
 struct Problem {
