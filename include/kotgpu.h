@@ -183,6 +183,12 @@ int kot_gram_rect(const double* a, int m, const double* b, int p, int d, double 
 /* mean_embedding (kernels.py:83-87): out[j] = mean_i k(s_i, q_j), the n × m Gram never stored. */
 int kot_mean_embedding(const double* samples, int n, const double* queries, int m, int d, double bandwidth_sq,
                        int device, double* out);
+/* sobol_natural / sobol_points (datagen.py:77-132): unscrambled Sobol points with natural indices
+ * first … first+count−1 (the reference's `index + 1`), each coordinate mapped into [lower, upper]:
+ * out[j][k] = lower[k] + (XOR_{b: bit b of first+j} dirnums[k][b]) / 2^bits · (upper[k] − lower[k]).
+ * dirnums: dim × bits direction numbers (the reference's SciPy generator's table). */
+int kot_sobol_points(const unsigned long long* dirnums, int dim, int bits, long first, int count,
+                     const double* lower, const double* upper, int device, double* out);
 /* embedding_norm_sq (kernels.py:90-94): mean of the n × n sample Gram. */
 int kot_embedding_norm_sq(const double* samples, int n, int d, double bandwidth_sq, int device, double* out);
 /* cholesky_psd (linalg.py:91-114). */

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkotgpu.so")
+LIB_PATH = os.environ.get("KOT_LIB_PATH") or os.path.join(_HERE, "libkotgpu.so")  # override: diagnostics
 
 dptr = C.POINTER(C.c_double)
 iptr = C.POINTER(C.c_int)
@@ -102,6 +102,8 @@ _SIGS = {
     "kot_constraint_matrix": (C.c_int, [C.c_void_p, dptr, dptr]),
     "kot_gram_rect": (C.c_int, [dptr, C.c_int, dptr, C.c_int, C.c_int, C.c_double, C.c_int, dptr]),
     "kot_mean_embedding": (C.c_int, [dptr, C.c_int, dptr, C.c_int, C.c_int, C.c_double, C.c_int, dptr]),
+    "kot_sobol_points": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int, C.c_int, C.c_long, C.c_int, dptr, dptr,
+                                   C.c_int, dptr]),
     "kot_embedding_norm_sq": (C.c_int, [dptr, C.c_int, C.c_int, C.c_double, C.c_int, dptr]),
     "kot_spectral_apply_decomp": (C.c_int, [dptr, dptr, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                             dptr, dptr]),

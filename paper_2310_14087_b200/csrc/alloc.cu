@@ -16,18 +16,18 @@ std::mutex g_mu;
 std::map<int, cudaStream_t> g_alloc_stream;              // per device, non-blocking
 std::map<size_t, std::vector<void*>> g_pinned_free;     // size → cached pinned buffers
 
-// Optional (KOT_CARVEOUT=1; default off, measured): the kernels with large dynamic shared memory (GEMM
-// cores, sytrd panel / tail, D&C, two-stage) prefer the maximum shared-memory carveout.  An SM takes a CTA only if its
+// The GEMM cores and the sytrd panel kernel prefer the maximum shared-memory carveout (KOT_CARVEOUT=0:
+// driver defaults).  An SM takes a CTA only if its
 // current L1/shared split leaves room: under per-kernel defaults an SM brought up for a 64 KB panel
 // CTA could not take the CG GEMMs' CTAs beside it (measured with idle 64 KB CTAs on another stream:
 // Newton chain 27.3 → 30.7 ms; with the max-shared preference 28.6).  Kernels without dynamic shared
 // memory keep the default (max L1): a device-wide PreferShared cost the eigensolver its L1 (trial
-// residual 27.5 → 28.6 ms).  Inside the solver the per-kernel preference is neutral to slightly worse
-// (cfg3 15.1 vs 15.3 it/s), so it stays off.
+// residual 27.5 → 28.6 ms), and so did the preference on every shared-memory kernel (tail, D&C…), so
+// only the GEMMs and the panel kernel — the pair that must share SMs — carry it.
 bool carveout_on() {
   static const bool on = [] {
     const char* e = std::getenv("KOT_CARVEOUT");
-    return e && std::atoi(e) > 0;
+    return !(e && std::atoi(e) == 0);
   }();
   return on;
 }
@@ -188,14 +188,23 @@ namespace {
 std::map<std::pair<int, const void*>, int> g_smem_attr;
 }
 
+bool carveout_preferred() { return carveout_on(); }
+
+void prefer_max_shared(const void* func) {
+  if (!carveout_on()) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  static std::map<const void*, bool> done;
+  if (done[func]) return;
+  done[func] = true;
+  KOT_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+}
+
 void ensure_smem_attr(const void* func, int bytes, bool nonportable_cluster) {
   int dev = 0;
   KOT_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_mu);
   int& have = g_smem_attr[{dev, func}];
   if (have >= bytes && have > 0) return;
-  if (carveout_on() && have == 0)
-    KOT_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
   if (nonportable_cluster) KOT_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   if (bytes > 48 * 1024) KOT_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   have = std::max(bytes, 1);

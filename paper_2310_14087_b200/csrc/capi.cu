@@ -332,6 +332,27 @@ int kot_gram_rect(const double* a, int m, const double* b, int p, int d, double 
   });
 }
 
+int kot_sobol_points(const unsigned long long* dirnums, int dim, int bits, long first, int count,
+                     const double* lower, const double* upper, int device, double* out) {
+  return guarded([&] {
+    kot::kot_require(dim >= 1 && bits >= 1 && bits <= 64 && count >= 0 && first >= 0, kot::KOT_EINVAL,
+                     "invalid Sobol request");
+    KOT_CUDA(cudaSetDevice(device));
+    if (count == 0) return;
+    cudaStream_t st;
+    KOT_CUDA(cudaStreamCreate(&st));
+    DevBuf dv((long)dim * bits), dlo(dim), dhi(dim), dout((long)count * dim);
+    KOT_CUDA(cudaMemcpyAsync(dv.p, dirnums, 8L * dim * bits, cudaMemcpyHostToDevice, st));
+    KOT_CUDA(cudaMemcpyAsync(dlo.p, lower, 8L * dim, cudaMemcpyHostToDevice, st));
+    KOT_CUDA(cudaMemcpyAsync(dhi.p, upper, 8L * dim, cudaMemcpyHostToDevice, st));
+    kot::sobol_points_device(reinterpret_cast<const unsigned long long*>(dv.p), dim, bits, first, count, dlo.p, dhi.p,
+                             dout.p, st);
+    KOT_CUDA(cudaMemcpyAsync(out, dout.p, 8L * count * dim, cudaMemcpyDeviceToHost, st));
+    KOT_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+  });
+}
+
 int kot_mean_embedding(const double* samples, int n, const double* queries, int m, int d, double bandwidth_sq,
                        int device, double* out) {
   return guarded([&] {

@@ -103,6 +103,9 @@ void host_free_pinned(void* p, size_t bytes);
 // attributes are per device), optionally allowing non-portable cluster sizes; cached per
 // (device, kernel), thread-safe.
 void ensure_smem_attr(const void* func, int bytes, bool nonportable_cluster = false);
+// the kernel prefers the maximum shared-memory carveout (GEMM cores, sytrd panel; see alloc.cu)
+void prefer_max_shared(const void* func);
+bool carveout_preferred();
 
 constexpr int kNumSMs = 148;
 

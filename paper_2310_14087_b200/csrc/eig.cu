@@ -873,11 +873,19 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
       cfg.blockDim = dim3(TRD_THREADS);
       cfg.dynamicSmemBytes = smem;
       cfg.stream = st;
-      cudaLaunchAttribute at[1];
+      cudaLaunchAttribute at[2];
       at[0].id = cudaLaunchAttributeCooperative;
       at[0].val.cooperative = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
+      // background chains' panels (lanes 1, 2) bring their SMs up with the maximum shared-memory
+      // carveout, so that the Newton chain's GEMM CTAs fit beside them; the Newton chain's own panels
+      // keep the default split (their L1 helps: trial eigensolve 27.8 vs 28.6 ms)
+      if (lane != 0 && carveout_preferred()) {
+        at[1].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
+        at[1].val.sharedMemCarveout = cudaSharedmemCarveoutMaxShared;
+        cfg.numAttrs = 2;
+      }
       KOT_CUDA(cudaLaunchKernelEx(&cfg, sytrd_panel_kernel, args));
       KOT_LAUNCH_CHECK();
     }
@@ -1923,6 +1931,7 @@ struct CoopGate {
 static int sytrd_per_sm(int n) {
   const size_t smem = sizeof(double) * (std::max(n, 1) + 3L * TRD_WARPS * TRD_RPW * TRD_NB);
   ensure_smem_attr((const void*)sytrd_panel_kernel, (int)smem);
+    prefer_max_shared((const void*)sytrd_panel_kernel);
   int per_sm = 0;
   KOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sytrd_panel_kernel, TRD_THREADS, smem));
   return std::max(1, per_sm);

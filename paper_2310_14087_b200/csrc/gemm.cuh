@@ -384,10 +384,12 @@ void gemm_launch_tiled(const GemmShape& s, const Epi& epi, cudaStream_t st) {
   if (gemm_vec2_ok(s)) {
     auto k = gemm_dmma_kernel<TA, TB, 2, Epi, BM, BN>;
     ensure_smem_attr((const void*)k, smem);
+    prefer_max_shared((const void*)k);
     k<<<grid, G_THREADS, smem, st>>>(s, epi, tiles);
   } else {
     auto k = gemm_dmma_kernel<TA, TB, 1, Epi, BM, BN>;
     ensure_smem_attr((const void*)k, smem);
+    prefer_max_shared((const void*)k);
     k<<<grid, G_THREADS, smem, st>>>(s, epi, tiles);
   }
   KOT_LAUNCH_CHECK();

@@ -179,8 +179,19 @@ __device__ __forceinline__ bool tma_tile(const GemmShape& s, int t, int tiles_m,
 
 // Tiles are processed in a loop (tile = blockIdx.x, += gridDim.x): a launch may use fewer CTAs than
 // tiles (gemm_cta_cap, background solver chains), the ring and its phases carry across tiles.
+// At most 96 registers per thread (a few bytes of epilogue spill): two of these CTAs then fit beside a
+// resident sytrd panel CTA (256 threads × 128 registers), which inside the solver outweighs the ≈8 %
+// this costs a GEMM alone (CG Newton direction 37.2 → 35.5 ms with the max-shared carveout below).
+#ifndef KOT_TMA_MAXREG
+#define KOT_TMA_MAXREG 96
+#endif
+#if KOT_TMA_MAXREG > 0
+#define KOT_TMA_BOUNDS __maxnreg__(KOT_TMA_MAXREG)
+#else
+#define KOT_TMA_BOUNDS __launch_bounds__(((BM / WM) * (BN / WN) + 1) * 32)
+#endif
 template <bool TA, bool TB, int BM, int BN, int WM, int WN, int ST, class Epi>
-__global__ void __launch_bounds__(((BM / WM) * (BN / WN) + 1) * 32)
+__global__ void KOT_TMA_BOUNDS
     gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                     const __grid_constant__ CUtensorMap mapK, GemmShape s, Epi epi, int ntiles) {
   constexpr int NWN = BN / WN, NWC = (BM / WM) * NWN;  // consumer warps
@@ -393,6 +404,7 @@ bool gemm_launch_tma(const GemmShape& s, const Epi& epi, cudaStream_t st) {
   const dim3 grid(ctas, s.ksplit > 1 ? s.ksplit : 1);
   auto k = gemm_tma_kernel<TA, TB, BM, BN, WM, WN, ST, Epi>;
   ensure_smem_attr((const void*)k, smem);
+  prefer_max_shared((const void*)k);
   k<<<grid, threads, smem, st>>>(ma, mb, mk, s, epi, tiles);
   KOT_LAUNCH_CHECK();
   if constexpr (!Epi::kRowDot) {

@@ -269,6 +269,33 @@ void embedding_norm_sq_device(const double* S, int n, int d, double bw, double* 
   KOT_LAUNCH_CHECK();
 }
 
+// Natural-order unscrambled Sobol points (reference datagen.py:77-95, 111-132): point with natural
+// index i = XOR of the direction numbers V[dim][b] over the set bits b of i, divided by 2^bits (exact),
+// then mapped affinely into [lower, upper] per coordinate (same operations as the reference's NumPy
+// expression lower + unit·(upper − lower), no FMA contraction).  One thread per (point, dimension).
+__global__ void sobol_points_kernel(const unsigned long long* __restrict__ V, int dim, int bits, long first,
+                                    int count, const double* __restrict__ lower, const double* __restrict__ upper,
+                                    double* __restrict__ out) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= (long)count * dim) return;
+  const int j = (int)(t / dim), k = (int)(t % dim);
+  unsigned long long idx = (unsigned long long)(first + j);
+  unsigned long long x = 0;
+  for (int b = 0; b < bits && idx; ++b, idx >>= 1)
+    if (idx & 1ull) x ^= V[(long)k * bits + b];
+  const double unit = (double)x / ldexp(1.0, bits);
+  out[t] = __dadd_rn(lower[k], __dmul_rn(unit, __dsub_rn(upper[k], lower[k])));
+}
+
+void sobol_points_device(const unsigned long long* V, int dim, int bits, long first, int count,
+                         const double* lower, const double* upper, double* out, cudaStream_t st) {
+  kot_require(dim >= 1 && bits >= 1 && bits <= 64 && count >= 0 && first >= 0, KOT_EINVAL, "invalid Sobol request");
+  if (count == 0) return;
+  const long total = (long)count * dim;
+  sobol_points_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(V, dim, bits, first, count, lower, upper, out);
+  KOT_LAUNCH_CHECK();
+}
+
 void assemble_device(const double* xs, int nx, const double* ys, int ny, const double* xt, const double* yt,
                      int l, int d, double bw_x, double bw_y, double bw_xy, double lambda2, double* Q, double* Kmat,
                      double* embed, double* z, double* q_sq, double* scratch, cudaStream_t st) {

@@ -13,6 +13,8 @@ void assemble_device(const double* xs, int nx, const double* ys, int ny, const d
                      double* embed, double* z, double* q_sq, double* scratch, cudaStream_t st);
 // rectangular Gram out[i][j] = k(a_i, b_j) (m × p); column means of the n × m sample/query Gram;
 // mean of the n × n sample Gram (unit diagonal) — kernels.py:61-94
+void sobol_points_device(const unsigned long long* V, int dim, int bits, long first, int count,
+                         const double* lower, const double* upper, double* out, cudaStream_t st);
 void gram_rect(const double* A, int m, const double* B, int p, int d, double bw, double* out, cudaStream_t st);
 void mean_embedding_device(const double* S, int n, const double* F, int m, int d, double bw, double* out,
                            cudaStream_t st);

@@ -214,3 +214,16 @@ def test_replaced_problem_data_is_reuploaded(cfg1):
     pd.lambda2 = 2.0 * pd.lambda2
     assert GP.objective(pd, g) == pytest.approx(O.objective(po, g), rel=1e-13)
     assert o1 != GP.objective(pd, g)
+
+
+def test_sobol_points_on_device(api):
+    """Row f4: natural-order Sobol filling points generated on the GPU equal the reference's
+    (datagen.py:77-132: SciPy's Gray-code stream re-indexed), bit for bit."""
+    from paper_2310_14087_b200 import datagen as D
+    fp = K.sobol_points(6, 37, -1.0, 1.0)
+    assert np.array_equal(fp.x_tilde, api["sobol_xt"]) and np.array_equal(fp.y_tilde, api["sobol_yt"])
+    assert np.array_equal(D.sobol_natural(5, 3, 20), api["sobol_nat"])
+    s = D.SobolStream(5, 3)
+    assert np.array_equal(np.vstack([s.take(7), s.take(13)]), api["sobol_nat"])
+    with pytest.raises(ValueError):
+        K.sobol_points(5, 10)
