@@ -881,7 +881,7 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
       // background chains' panels (lanes 1, 2) bring their SMs up with the maximum shared-memory
       // carveout, so that the Newton chain's GEMM CTAs fit beside them; the Newton chain's own panels
       // keep the default split (their L1 helps: trial eigensolve 27.8 vs 28.6 ms)
-      if (lane != 0 && carveout_preferred()) {
+      if ((lane != 0 || background_thread()) && carveout_preferred()) {
         at[1].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
         at[1].val.sharedMemCarveout = cudaSharedmemCarveoutMaxShared;
         cfg.numAttrs = 2;
@@ -1931,7 +1931,6 @@ struct CoopGate {
 static int sytrd_per_sm(int n) {
   const size_t smem = sizeof(double) * (std::max(n, 1) + 3L * TRD_WARPS * TRD_RPW * TRD_NB);
   ensure_smem_attr((const void*)sytrd_panel_kernel, (int)smem);
-    prefer_max_shared((const void*)sytrd_panel_kernel);
   int per_sm = 0;
   KOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sytrd_panel_kernel, TRD_THREADS, smem));
   return std::max(1, per_sm);

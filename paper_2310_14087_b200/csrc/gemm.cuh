@@ -31,6 +31,13 @@ namespace kot {
 // chains (EG pipeline threads) set a cap so that their GEMMs never fill every SM slot: the Newton
 // chain's CG kernels, launched one after another, then find free slots instead of queueing behind
 // a background GEMM's waves.
+// The calling host thread runs a background chain (the EG pipeline): its GEMMs and panels bring SMs up
+// with the maximum shared-memory carveout (per launch), so the Newton chain's kernels fit beside them.
+inline bool& background_thread() {
+  static thread_local bool bg = false;
+  return bg;
+}
+
 inline int& gemm_cta_cap() {
   static thread_local int cap = 0;
   return cap;
@@ -381,17 +388,26 @@ void gemm_launch_tiled(const GemmShape& s, const Epi& epi, cudaStream_t st) {
   const int cap = gemm_cta_cap();
   const int ctas = cap > 0 ? std::max(1, std::min(tiles, cap / std::max(s.ksplit, 1))) : tiles;
   const dim3 grid(ctas, s.ksplit > 1 ? s.ksplit : 1);
-  if (gemm_vec2_ok(s)) {
-    auto k = gemm_dmma_kernel<TA, TB, 2, Epi, BM, BN>;
+  auto launch = [&](auto k) {
     ensure_smem_attr((const void*)k, smem);
-    prefer_max_shared((const void*)k);
-    k<<<grid, G_THREADS, smem, st>>>(s, epi, tiles);
-  } else {
-    auto k = gemm_dmma_kernel<TA, TB, 1, Epi, BM, BN>;
-    ensure_smem_attr((const void*)k, smem);
-    prefer_max_shared((const void*)k);
-    k<<<grid, G_THREADS, smem, st>>>(s, epi, tiles);
-  }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(G_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    if (background_thread() && carveout_preferred()) {
+      at[0].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
+      at[0].val.sharedMemCarveout = cudaSharedmemCarveoutMaxShared;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+    }
+    KOT_CUDA(cudaLaunchKernelEx(&cfg, k, s, epi, tiles));
+  };
+  if (gemm_vec2_ok(s))
+    launch(gemm_dmma_kernel<TA, TB, 2, Epi, BM, BN>);
+  else
+    launch(gemm_dmma_kernel<TA, TB, 1, Epi, BM, BN>);
   KOT_LAUNCH_CHECK();
   if constexpr (!Epi::kRowDot) {
     if (s.ksplit > 1) {

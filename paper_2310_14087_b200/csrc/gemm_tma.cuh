@@ -404,8 +404,21 @@ bool gemm_launch_tma(const GemmShape& s, const Epi& epi, cudaStream_t st) {
   const dim3 grid(ctas, s.ksplit > 1 ? s.ksplit : 1);
   auto k = gemm_tma_kernel<TA, TB, BM, BN, WM, WN, ST, Epi>;
   ensure_smem_attr((const void*)k, smem);
-  prefer_max_shared((const void*)k);
-  k<<<grid, threads, smem, st>>>(ma, mb, mk, s, epi, tiles);
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    if (background_thread() && carveout_preferred()) {  // see background_thread (gemm.cuh)
+      at[0].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
+      at[0].val.sharedMemCarveout = cudaSharedmemCarveoutMaxShared;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+    }
+    KOT_CUDA(cudaLaunchKernelEx(&cfg, k, ma, mb, mk, s, epi, tiles));
+  }
   KOT_LAUNCH_CHECK();
   if constexpr (!Epi::kRowDot) {
     if (s.ksplit > 1) {

@@ -662,6 +662,7 @@ class EgPipeline {
 
   void run_steps(Problem& a) {
     gemm_cta_cap() = bg_gemm_ctas();
+    background_thread() = true;
     for (int j = 1;; ++j) {
       {
         std::unique_lock<std::mutex> lk(mu_);
@@ -702,6 +703,7 @@ class EgPipeline {
 
   void run_residuals(Problem& b) {
     gemm_cta_cap() = bg_gemm_ctas();
+    background_thread() = true;
     for (int j = 1;; ++j) {
       {
         std::unique_lock<std::mutex> lk(mu_);
@@ -773,6 +775,7 @@ static bool loop_body(Problem& p, const SolverCfg& cfg, LoopState& s, int k, Ite
     eg_thread = std::thread([&]() {
       try {
         gemm_cta_cap() = bg_gemm_ctas();
+        background_thread() = true;
         KOT_CUDA(cudaSetDevice(a.device));
         auto t0 = clk::now();
         eg_step(a, b.gv, b.Xv, cfg.eg_stepsize, b.gv, b.Xv);

@@ -939,9 +939,11 @@ void eg_step_parallel(Problem& p, Problem& c, const double* g, const double* X, 
   // second projection on c:  X_out = Π(X − s (Φ*(γ½) + λ₁I))
   std::exception_ptr err = nullptr;
   const int cta_cap = gemm_cta_cap();  // a background caller's GEMM cap applies to its helper too
+  const bool bg = background_thread();
   std::thread helper([&] {
     try {
       gemm_cta_cap() = cta_cap;
+      background_thread() = bg;
       KOT_CUDA(cudaSetDevice(c.device));
       KOT_CUDA(cudaStreamWaitEvent(c.st, p.ev_half, 0));
       Decomp dc2{c.M2, c.M3, 0};
