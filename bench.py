@@ -509,7 +509,7 @@ def batch_leg(world: int, rank: int, local: int, n_problems: int, tol: float, ma
     # several solves share the GPU: thinner cooperative panel grids let their eigensolves run side by
     # side (16 problems x 100 iterations, cluster tail: 0.73 problems/s at 64 CTAs, 0.85 at 48, 0.89 at
     # 32, 0.90 at 24; concurrency 4-12 equal)
-    _lib.lib().kot_set_panel_grid_cap(32)
+    _lib.lib().kot_set_panel_grid_cap(int(os.environ.get("KOT_BATCH_GRID", "32")))
     seeds = list(range(n_problems))
     mine = batch.shard(seeds, world, rank)
     kw = dict(profile=profile, residual_tol=tol, max_iter=max_iter)

@@ -77,7 +77,7 @@ EigWork::EigWork(int n_) : n(n_) {
   alloc(&lam, n);
   alloc(&dfv, n);
   alloc(&rotcs, 2L * n);
-  alloc(&rho, n);
+  alloc(&rho, n + 1);  // merge ρ's, then the tridiagonal's max norm at [n]
   ibuf = static_cast<int*>(dev_alloc(sizeof(int) * (8L * n + 64)));
   dbuf = dev_alloc(16L * n + 4096 + 64L * n);
   hbuf = static_cast<int*>(host_alloc_pinned(sizeof(int) * (12L * n + 512)));
@@ -929,9 +929,26 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
 
 // ======================================================== tridiagonal D&C
 
-// Subtract the rank-one couplings at every split point (dlaed0): d[s], d[s+1] -= |e[s]|.
-__global__ void dc_split_kernel(double* d, const double* e, const int* splits, int ns) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// Subtract the rank-one couplings at every split point (dlaed0): d[s], d[s+1] -= |e[s]|.  First the
+// tridiagonal's max norm (dstedc's orgnrm, over the couplings as given) goes to *scale: LAPACK runs
+// the D&C on T/orgnrm, so its deflation tolerance 8·eps·max(d_max, z_max) mixes an O(1) d with the
+// unit-norm z; the merges use 8·eps·max(d_max, orgnrm·z_max), the same test without rescaling T
+// (a matrix of norm 1e-8 deflated at an absolute 1.8e-15 before: 3.7e-7 relative projection error).
+constexpr int DC_SPLIT_THREADS = 256;
+__global__ void __launch_bounds__(DC_SPLIT_THREADS) dc_split_kernel(double* d, const double* e, int n,
+                                                                  const int* splits, int ns, double* scale) {
+  __shared__ double red[DC_SPLIT_THREADS / 32];
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    mx = fmax(mx, fabs(d[i]));
+    if (i < n - 1) mx = fmax(mx, fabs(e[i]));
+  }
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int w = 0; w < DC_SPLIT_THREADS / 32; ++w) mx = fmax(mx, red[w]);
+  *scale = mx;
   for (int i = 0; i < ns; ++i) {
     const int s = splits[i];
     const double r = fabs(e[s]);
@@ -1078,7 +1095,7 @@ __device__ __forceinline__ int rank_le(const double* a, int n, double v) {  // #
 __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
     const MergeDesc* md, const double* Q, int ldq, const double* d, const double* e, double* zs, double* ds,
     double* dlam, double* wv, double* dfv, double* rotcs, double* rho_out, int* perm, int* ndcol, int* dcol,
-    int* rot, int* meta, int* pidx) {
+    int* rot, int* meta, int* pidx, const double* tscale) {
   extern __shared__ double psm[];
   __shared__ double red[32];
   const MergeDesc m = md[blockIdx.x];
@@ -1117,7 +1134,7 @@ __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
     dmax = fmax(dmax, red[16 + w]);
   }
   const double rho = fabs(2.0 * esplit);
-  const double tol = 8.0 * DEPS * fmax(dmax, zmax);
+  const double tol = 8.0 * DEPS * fmax(dmax, *tscale * zmax);  // dlaed2's test on T/orgnrm
   int* NDC = ndcol + o;
   int* DC = dcol + o;
   int* RT = rot + 2 * o;
@@ -1646,7 +1663,7 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
   const int* dloff = d_packed + splits.size();
   const int* dllen = dloff + loff.size();
   if (!splits.empty()) {
-    dc_split_kernel<<<1, 1, 0, st>>>(w.d, w.e, dsplit, (int)splits.size());
+    dc_split_kernel<<<1, DC_SPLIT_THREADS, 0, st>>>(w.d, w.e, n, dsplit, (int)splits.size(), w.rho + n);
     KOT_LAUNCH_CHECK();
   }
   const int nleaves = (int)loff.size();
@@ -1692,7 +1709,7 @@ static void stedc(int n, EigWork& w, cudaStream_t st) {
       ensure_smem_attr((const void*)dc_merge_prep_kernel, (int)smem);
       dc_merge_prep_kernel<<<nm, DC_PREP_THREADS, smem, st>>>(dms, w.Q, n, w.d, w.e, w.zs, w.ds, w.dlam, w.wv,
                                                               w.dfv, w.rotcs, w.rho, perm, ndcol, dcol, rot, dmeta,
-                                                              pidx);
+                                                              pidx, w.rho + n);
       KOT_LAUNCH_CHECK();
     }
     {

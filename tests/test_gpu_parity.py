@@ -84,6 +84,27 @@ def test_sym_eig_structured(n, kind):
     assert np.linalg.norm((p * dc.eigvals) @ p.T - z) <= 1e-12 * nz * n
 
 
+@pytest.mark.parametrize("scale", [1e-8, 1.0, 1e8])
+def test_sym_eig_scale_invariant(scale):
+    """A nearly diagonal matrix with a few positive eigenvalues (the first EG argument of a config-5
+    member has this shape at norm ~1e-8): D&C deflation is relative to the tridiagonal's norm, as in
+    dstedc, so the decomposition and the PSD projection are accurate at any scale."""
+    n = 600
+    rng = np.random.default_rng(11)
+    base = np.diag(-1.0 - rng.random(n))
+    base[:12, :12] += np.diag(1.2 + rng.random(12))
+    e = rng.standard_normal((n, n)) * 1e-6
+    z = scale * (base + 0.5 * (e + e.T))
+    dc = GL.sym_eig(z)
+    nz = np.linalg.norm(z, 2)
+    ref = np.sort(np.linalg.eigvalsh(z))[::-1]
+    assert np.max(np.abs(dc.eigvals - ref)) <= 1e-13 * nz
+    p = dc.eigvecs
+    assert np.max(np.abs((p * dc.eigvals) @ p.T - z)) <= 1e-13 * nz
+    proj = GC.proj_psd(z)
+    assert rel(proj, O.proj_psd(z)) <= 1e-12
+
+
 def test_sym_eig_kats():
     # test_linalg.py:13-44
     d = GL.sym_eig(np.diag([2.0, -1.0]))

@@ -181,3 +181,23 @@ def test_paper_profile_first_iteration_cfg3(cfg3):
     assert rec.cg_iters == cfg3.rec0.cg_iters and rec.accepted == cfg3.rec0.accepted
     assert rec.res_accepted == pytest.approx(cfg3.rec0.res_accepted, rel=1e-9)
     assert rel(w2.gamma, cfg3.st1.w.g) <= 1e-9
+
+
+@pytest.mark.parametrize("which", ["cfg5_sigma0.5", "cfg5_sigma2.0", "cfg4_l1024"])
+def test_lockstep_replay_converged_cg_cfg4_cfg5(which):
+    """The remaining BASELINE families: config-5 members (ℓ = n = 1000, d = 10) at the smallest and the
+    largest bandwidth of the σ sweep, and the config-4 recipe (d = 64 embeddings) at ℓ = 1024 —
+    iterations 0 and 1 of the paper trajectory replayed with the Newton system solved to 1e-13.  The
+    σ = 0.5 member's first EG argument has norm ~1e-8 and caught an absolute D&C deflation tolerance
+    (3.7e-7 relative error in the projected X before the fix; test_sym_eig_scale_invariant)."""
+    if which.startswith("cfg5"):
+        seed = 0 if which.endswith("0.5") else 3  # σ = [0.5, 1, 1.5, 2][seed % 4]
+        inst = Instance(configs.config5_member(seed))
+    else:
+        inst = Instance(configs.config4(n=1024))
+    gcfg, ocfg = inst.cfgs(dict(cg_tol=CG_TOL, cg_max=3000, cg_restarts=0))
+    _, opaper = inst.cfgs({})
+    st = O.initial_state(inst.po, opaper)
+    for k in range(2):
+        _replay(inst, st, k, gcfg, ocfg)
+        st, _, _ = O.iterate_once(inst.po, st, k, opaper)
