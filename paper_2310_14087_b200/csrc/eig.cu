@@ -1168,6 +1168,10 @@ __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
     __syncthreads();
     csum[threadIdx.x] = cnt;
   }
+  // the dlaed2 close-pair test of every non-small j against its predecessor with the ORIGINAL values:
+  // the sequential scan below reuses it wherever the predecessor was not itself rotated (then Z[pj],
+  // D[pj] are still the original values, so the test is the same expression on the same inputs)
+  unsigned long long fl = 0;  // bit j − j0: the test fired (chunk ≤ 64, i.e. n ≤ 64·DC_PREP_THREADS)
   for (int j = j0; j < j1; ++j) {
     if (rho * fabs(Z[j]) <= tol) continue;
     const int pj = prevnz[j];
@@ -1177,9 +1181,18 @@ __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
     const double t = D[j] - D[pj];
     c /= tau;
     s = -s / tau;
-    if (fabs(t * c * s) <= tol) trig_sh = 1;
+    if (fabs(t * c * s) <= tol) {
+      trig_sh = 1;
+      fl |= 1ull << ((j - j0) & 63);
+    }
   }
   __syncthreads();
+  if (trig_sh) {  // prevnz is dead: it becomes the origin mask (bit 2 = the precomputed test fired)
+    const bool exact = chunk <= 64;
+    for (int j = j0; j < j1; ++j)
+      prevnz[j] = ((P[j] < n1) ? 1 : 2) | ((!exact || ((fl >> (j - j0)) & 1ull)) ? 4 : 0);
+    __syncthreads();
+  }
   if (!trig_sh) {
     __shared__ int ctop[DC_PREP_THREADS];
     int tops = 0;
@@ -1226,8 +1239,11 @@ __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
   }
   if (threadIdx.x != 0) return;
   rho_out[blockIdx.x] = rho;
-  int* mask = prevnz;  // origin of each sorted column: 1 top child, 2 bottom child, 3 mixed by rotation
-  for (int j = 0; j < n; ++j) mask[j] = (P[j] < n1) ? 1 : 2;
+  // origin of each sorted column: 1 top child, 2 bottom child, 3 mixed by rotation (bits 0-1); bit 2:
+  // the close-pair test against the original predecessor fired (a superset flag when chunk > 64)
+  int* mask = prevnz;
+  if (rho * zmax <= tol)
+    for (int j = 0; j < n; ++j) mask[j] = (P[j] < n1) ? 1 : 2;
   int K = 0, nd = 0, nr = 0;
   if (rho * zmax <= tol) {
     for (int k = 0; k < n; ++k) {
@@ -1237,6 +1253,7 @@ __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
     }
   } else {
     int pj = -1;
+    bool pj_rot = false;  // Z[pj], D[pj] were changed by a rotation (the precomputed test does not apply)
     for (int j = 0; j < n; ++j) {
       if (rho * fabs(Z[j]) <= tol) {
         DC[nd] = j;
@@ -1245,6 +1262,15 @@ __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
         continue;
       }
       if (pj < 0) {
+        pj = j;
+        pj_rot = false;
+        continue;
+      }
+      if (!pj_rot && !(mask[j] & 4)) {  // no deflation (same verdict as the test below)
+        NDC[K] = pj;
+        DL[K] = D[pj];
+        WV[K] = Z[pj];
+        ++K;
         pj = j;
         continue;
       }
@@ -1256,7 +1282,7 @@ __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
       if (fabs(t * c * s) <= tol) {
         Z[j] = tau;
         Z[pj] = 0.0;
-        mask[j] |= mask[pj];
+        mask[j] = (mask[j] & 3) | (mask[pj] & 3);
         RT[2 * nr] = pj;
         RT[2 * nr + 1] = j;
         RCS[2 * nr] = c;
@@ -1269,12 +1295,14 @@ __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
         DFV[nd] = D[pj];
         ++nd;
         pj = j;
+        pj_rot = true;
       } else {
         NDC[K] = pj;
         DL[K] = D[pj];
         WV[K] = Z[pj];
         ++K;
         pj = j;
+        pj_rot = false;
       }
     }
     if (pj >= 0) {
@@ -1300,13 +1328,13 @@ __global__ void __launch_bounds__(DC_PREP_THREADS) dc_merge_prep_kernel(
   {  // GEMM order of the secular columns: top-only, mixed, bottom-only
     int c1 = 0, c2 = 0;
     for (int k = 0; k < K; ++k) {
-      const int mk = mask[NDC[k]];
+      const int mk = mask[NDC[k]] & 3;
       c1 += (mk == 1);
       c2 += (mk == 3);
     }
     int i1 = 0, i2 = c1, i3 = c1 + c2;
     for (int k = 0; k < K; ++k) {
-      const int mk = mask[NDC[k]];
+      const int mk = mask[NDC[k]] & 3;
       pidx[o + k] = (mk == 1) ? i1++ : (mk == 3) ? i2++ : i3++;
     }
     meta[MS * blockIdx.x + 3] = c1;

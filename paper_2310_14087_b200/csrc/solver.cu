@@ -988,12 +988,14 @@ SolveResult solve(Problem& p, const SolverCfg& cfg, IterCallback cb, void* user,
     out.status = KOT_ENUMERICS;
     return out;
   }
+  const auto t_fin = clk::now();
   const double* gfin = pure_eg ? b.gv : b.gw;
   const double* xfin = pure_eg ? b.Xv : b.Xw;
   if (p.has_embed) out.ot_estimate = (p.q_sq - dev_dot(p, gfin, p.embed, n)) / (2.0 * p.l2);
   if (gamma_out) KOT_CUDA(cudaMemcpyAsync(gamma_out, gfin, sizeof(double) * n, cudaMemcpyDeviceToHost, p.st));
   if (x_out) KOT_CUDA(cudaMemcpyAsync(x_out, xfin, sizeof(double) * nn, cudaMemcpyDeviceToHost, p.st));
   KOT_CUDA(cudaStreamSynchronize(p.st));
+  prof_host("solve.download", ms_since(t_fin));
   out.total_ms = ms_since(t_start);
   return out;
 }
