@@ -102,12 +102,17 @@ void problem_shard_host(Problem& p, int (*fn)(void*, int, double*, long, long, i
   }
 }
 
-static void host_collective(Problem& p, int op, double* buf, long count, long block) {
-  KOT_CUDA(cudaMemcpyAsync(p.host_comm_buf, buf, sizeof(double) * count, cudaMemcpyDeviceToHost, p.st));
-  KOT_CUDA(cudaStreamSynchronize(p.st));
+static void host_collective(Problem& p, int op, double* buf, long count, long block, cudaStream_t st) {
+  if (p.host_comm_cap < count) {  // the split H form gathers whole row blocks of B
+    if (p.host_comm_buf) host_free_pinned(p.host_comm_buf, sizeof(double) * p.host_comm_cap);
+    p.host_comm_buf = static_cast<double*>(host_alloc_pinned(sizeof(double) * count));
+    p.host_comm_cap = count;
+  }
+  KOT_CUDA(cudaMemcpyAsync(p.host_comm_buf, buf, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
+  KOT_CUDA(cudaStreamSynchronize(st));
   const int rc = p.host_comm(p.host_comm_user, op, p.host_comm_buf, count, block, p.shard_rank, p.shard_world);
   kot_require(rc == 0, KOT_ECUDA, "host data-plane collective failed");
-  KOT_CUDA(cudaMemcpyAsync(buf, p.host_comm_buf, sizeof(double) * count, cudaMemcpyHostToDevice, p.st));
+  KOT_CUDA(cudaMemcpyAsync(buf, p.host_comm_buf, sizeof(double) * count, cudaMemcpyHostToDevice, st));
 }
 
 void problem_unshard(Problem& p) {
@@ -124,18 +129,32 @@ void problem_unshard(Problem& p) {
   p.row1 = p.n;
 }
 
-void shard_allreduce_sum(Problem& p, double* buf, long count) {
-  if (p.host_comm) return host_collective(p, 0, buf, count, 0);
-  nccl_check(nccl().AllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, (ncclComm_t)p.nccl_comm, p.st),
+// Every rank receives the same sum (NCCL's ring / tree and the host collectives return one result to
+// all ranks), so the ranks keep taking identical control decisions.
+void shard_allreduce_sum(Problem& p, double* buf, long count, cudaStream_t st) {
+  if (p.host_comm) return host_collective(p, 0, buf, count, 0, st);
+  nccl_check(nccl().AllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, (ncclComm_t)p.nccl_comm, st),
              "ncclAllReduce");
 }
+void shard_allreduce_sum(Problem& p, double* buf, long count) { shard_allreduce_sum(p, buf, count, p.st); }
 
 // in place: rank g's block sits at buf + g·block; afterwards every rank holds all blocks
-void shard_allgather(Problem& p, double* buf, long block) {
-  if (p.host_comm) return host_collective(p, 1, buf, block * p.shard_world, block);
+void shard_allgather(Problem& p, double* buf, long block, cudaStream_t st) {
+  if (p.host_comm) return host_collective(p, 1, buf, block * p.shard_world, block, st);
   nccl_check(nccl().AllGather(buf + (long)p.shard_rank * block, buf, (size_t)block, ncclDouble,
-                              (ncclComm_t)p.nccl_comm, p.st),
+                              (ncclComm_t)p.nccl_comm, st),
              "ncclAllGather");
+}
+void shard_allgather(Problem& p, double* buf, long block) { shard_allgather(p, buf, block, p.st); }
+
+FoldedRows folded_rows(int n, int g, int world) {
+  FoldedRows f;
+  f.blk = (n + 2 * world - 1) / (2 * world);
+  f.a0 = std::min(n, g * f.blk);
+  f.a1 = std::min(n, f.a0 + f.blk);
+  f.b0 = std::min(n, (2 * world - 1 - g) * f.blk);
+  f.b1 = std::min(n, f.b0 + f.blk);
+  return f;
 }
 
 }  // namespace kot

@@ -243,7 +243,7 @@ static CgOut cg_solve(Problem& p, const MvCtx& mv, const double* rhs, double tol
   // the stopping rule (cg_step_kernel, batched mode) — the launches after the stop are no-ops — so
   // the host waits once per B steps instead of after every step; identical arithmetic and results.
   const int kBatch = cg_batch();
-  if (!mv.direct && mv.hform && kBatch > 1) {
+  if (!mv.direct && mv.hform && !mv.split && kBatch > 1) {
     cg_arm_kernel<<<1, 1, 0, p.st>>>(p.dsc, target, max_iter);
     KOT_LAUNCH_CHECK();
     const double* done = p.dsc + SC_DONE;

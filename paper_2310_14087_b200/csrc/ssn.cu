@@ -335,6 +335,9 @@ struct FinArgs {
   double l2, mu, phsign;
   double* out;
   const double* skipf = nullptr;  // nullable: no-op when *skipf != 0 (batched CG)
+  // split H form: only the rows in [own0, own1) ∪ [own2, own3) take the Q / H GEMVs and μv (this
+  // rank's share); the other rows get the mixed-block partials alone (summed over ranks afterwards)
+  int split_rows = 0, own0 = 0, own1 = 0, own2 = 0, own3 = 0;
 };
 
 // warp per row: GEMV row of Q (coalesced) + fixed-order sum of the Φ partials.
@@ -344,6 +347,15 @@ __global__ void finalize_kernel(FinArgs f) {
   const int lane = threadIdx.x & 31;
   for (int r = f.r0 + blockIdx.x * warps + (threadIdx.x >> 5); r < f.r1; r += gridDim.x * warps) {
     double qv = 0.0, ph = 0.0, gv = 0.0;
+    const bool own = !f.split_rows || (r >= f.own0 && r < f.own1) || (r >= f.own2 && r < f.own3);
+    if (!own) {  // split H form, another rank's row: the mixed-block partials only
+      if (f.partial) {
+        for (int tn = lane; tn < f.tiles; tn += 32) ph += f.partial[(long)tn * f.n + r];
+        ph = warp_sum(ph);
+      }
+      if (lane == 0) f.out[r] = ph;
+      continue;
+    }
     if (f.Q) {
       const double* qr = f.Q + (long)r * f.n;
       for (int c = lane; c < f.n; c += 32) qv += qr[c] * f.u[c];
@@ -473,8 +485,10 @@ struct EpiMvOff {
   const double* vals;
   int k, pos;
   double mu;
+  int coff = 0;  // column offset of this launch inside the mixed block (split H form); C is pre-offset
   __device__ void store(int r, int c, double v) const {
-    const double sa = pos ? vals[r] : vals[c], sb = pos ? vals[k + c] : vals[k + r];
+    const int cg = c + coff;
+    const double sa = pos ? vals[r] : vals[cg], sb = pos ? vals[k + cg] : vals[k + r];
     const double eta = sa / (sa - sb);
     C[(long)r * ldc + c] = 2.0 * ((eta / (mu + 1.0 - eta)) * v);
   }
@@ -493,6 +507,16 @@ struct EpiSquareMirror {
     C[(long)r * ldc + c] = o;
     C[(long)c * ldc + r] = o;
   }
+  __device__ double rowdot_weight(int, int) const { return 0; }
+  __device__ void rowdot_store(int, int, double) const {}
+};
+
+// Rows [r0, r0 + M) of H = G_α∘G_α (split H form: this rank's rows only).
+struct EpiSquareRows {
+  static constexpr bool kRowDot = false;
+  double* C;  // row r0 of H
+  long ldc;
+  __device__ void store(int r, int c, double v) const { C[(long)r * ldc + c] = v * v; }
   __device__ double rowdot_weight(int, int) const { return 0; }
   __device__ void rowdot_store(int, int, double) const {}
 };
@@ -531,15 +555,45 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allo
     const char* e = std::getenv("KOT_MATVEC");
     return e != nullptr && std::string(e) == "full";
   }();
-  m.hform = allow_hform && !full && !p.sharded() && p.emul_world <= 1;
+  const int world = p.sharded() ? p.shard_world : p.emul_world;
+  m.hform = allow_hform && !full;
+  m.split = m.hform && world > 1;
+  m.world = m.split ? world : 1;
   m.H = b.Hm;
-  for (const auto& [r0, r1] : row_blocks(p)) {  // B = R P for the row blocks this process owns
-    if (r1 > r0) {  // R upper triangular: the K range starts at the block's first row
-      GemmShape s = make_shape(r1 - r0, n, n, p.R + (long)r0 * n, n, dc.P, n);
-      s.kb_m = 1;
-      s.kstart = r0;
-      gemm_launch<false, false>(s, EpiAxpby{b.Bm + (long)r0 * n, n, 1.0, 0.0}, st);
+  // B = R P; R upper triangular: a row block's K range starts at its first row
+  auto b_rows = [&](int r0, int r1, double* dst) {
+    if (r1 <= r0) return;
+    GemmShape s = make_shape(r1 - r0, n, n, p.R + (long)r0 * n, n, dc.P, n);
+    s.kb_m = 1;
+    s.kstart = r0;
+    gemm_launch<false, false>(s, EpiAxpby{dst, n, 1.0, 0.0}, st);
+  };
+  if (m.split && p.sharded()) {
+    // every rank needs all of B (both GEMMs contract over all rows): each computes its two folded row
+    // blocks (equal shares of R's triangle) into its slots of the gather-order staging (slot g: block
+    // g, slot N+g: block 2N−1−g), two all-gathers, then B in natural row order
+    const int N = world, g = p.shard_rank;
+    const FoldedRows f = folded_rows(n, g, N);
+    const long slot = (long)f.blk * n;
+    if (p.shard_stage_cap < 2L * N * slot) {
+      p.shard_stage = p.alloc(2L * N * slot);
+      p.shard_stage_cap = 2L * N * slot;
     }
+    double* S = p.shard_stage;
+    b_rows(f.a0, f.a1, S + g * slot);
+    b_rows(f.b0, f.b1, S + (long)(N + g) * slot);
+    shard_allgather(p, S, slot, st);
+    shard_allgather(p, S + (long)N * slot, slot, st);
+    const long first = std::min<long>(n, (long)N * f.blk);  // blocks 0..N−1 are contiguous in both
+    KOT_CUDA(cudaMemcpyAsync(b.Bm, S, sizeof(double) * first * n, cudaMemcpyDeviceToDevice, st));
+    for (int h = 0; h < N; ++h) {
+      const FoldedRows fh = folded_rows(n, h, N);
+      if (fh.b1 > fh.b0)
+        KOT_CUDA(cudaMemcpyAsync(b.Bm + (long)fh.b0 * n, S + (long)(N + h) * slot,
+                                 sizeof(double) * (fh.b1 - fh.b0) * n, cudaMemcpyDeviceToDevice, st));
+    }
+  } else {
+    for (const auto& [r0, r1] : row_blocks(p)) b_rows(r0, r1, b.Bm + (long)r0 * n);
   }
   if (m.hform) {
     // The sign blocks of B packed side by side with even widths, so that every operand of the
@@ -556,6 +610,17 @@ void matvec_prepare(Problem& p, const Decomp& dc, double mu, MvCtx& m, bool allo
     // is the GEMV (H v)/μ, and only the α×ᾱ block remains for the two GEMMs of every matvec.
     if (k == 0) {
       KOT_CUDA(cudaMemsetAsync(m.H, 0, sizeof(double) * n * n, st));
+    } else if (m.split) {  // only the rows of this rank's folded blocks (every block under emulation)
+      const double* Ba = m.pos ? m.Bs : m.Bo;
+      for (int g = 0; g < world; ++g) {
+        if (p.sharded() && g != p.shard_rank) continue;
+        const FoldedRows f = folded_rows(n, g, world);
+        for (const auto& [r0, r1] : {std::make_pair(f.a0, f.a1), std::make_pair(f.b0, f.b1)}) {
+          if (r1 <= r0) continue;
+          GemmShape s = make_shape(r1 - r0, n, k, Ba + (long)r0 * m.ldp, m.ldp, Ba, m.ldp);
+          gemm_launch<false, true>(s, EpiSquareRows{m.H + (long)r0 * n, n}, st);
+        }
+      }
     } else {
       const double* Ba = m.pos ? m.Bs : m.Bo;
       GemmShape s = make_shape(n, n, k, Ba, m.ldp, Ba, m.ldp);
@@ -586,16 +651,26 @@ static int mv_target_ctas() {
 
 // y = Qv/(2λ₂) + μv + (Hv)/μ + Σ_{a∈α, b∈ᾱ} 2ξ_ab (B_{:,a}∘B_{:,b})·C_ab,  C = Bᵀdiag(v)B
 // (one process, no row blocks): two DMMA GEMMs of 2·k(ℓ−k)·ℓ FLOPs each + two GEMVs.
+// Split H form, rank g of N: the columns [c0, c1) of the mixed block (both GEMMs; even bounds keep
+// every operand 16-byte aligned) — the y partials over all ℓ rows — plus the Q / H GEMVs and μv on the
+// rows of g's folded blocks; the ranks' vectors add up to the unsplit matvec.
+static void split_cols(int ns, int g, int world, int& c0, int& c1) {
+  c0 = (int)(((long)ns * g / world) & ~1L);
+  c1 = g == world - 1 ? ns : (int)(((long)ns * (g + 1) / world) & ~1L);
+}
+
 static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, double* out,
-                                  const double* skipf) {
+                                  const double* skipf, int part = 0) {
   const int n = p.n, k = m.dc.k;
   const int ks = m.pos ? k : n - k;  // rows of T̃ (the smaller sign block)
-  const int ns = n - ks;
+  int c0 = 0, c1 = n - ks;
+  if (m.split) split_cols(n - ks, part, m.world, c0, c1);
+  const int ns = c1 - c0;  // this launch's columns of the other block
   const double nn = n;
-  ProfScope ps("matvec", p.st, 4.0 * ks * (double)ns * nn + 4.0 * nn * nn);
+  ProfScope ps("matvec", p.st, 4.0 * ks * (double)ns * nn + 4.0 * nn * nn / m.world);
   double* Ct = p.mv_ct ? p.mv_ct : p.bufs().Ct;
-  const double* Bs = m.Bs;  // columns of the T̃-row block (the smaller sign block)
-  const double* Bo = m.Bo;  // columns of the other block
+  const double* Bs = m.Bs;       // columns of the T̃-row block (the smaller sign block)
+  const double* Bo = m.Bo + c0;  // this launch's columns of the other block
   const long ld = m.ldp;
   int rd_tiles = 0;
   if (ks > 0 && ns > 0) {
@@ -614,8 +689,8 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
     const int t1 = ceil_div(ks, GB_M) * ceil_div(ns, GB_N);
     const int sp1 = mv_split > 0 ? mv_split : std::min(4, std::max(1, ceil_div(mv_target_ctas(), t1)));
     if (sp1 > 1 && (long)sp1 * s.M * s.N <= p.splitws_cap) s.ksplit = sp1;
-    gemm_launch<true, false>(s, EpiMvOff{Ct, n, m.dc.vals, k, m.pos ? 1 : 0, m.mu}, p.st);
-    GemmShape s2 = make_shape(n, ks, ns, Bo, ld, Ct, n);
+    gemm_launch<true, false>(s, EpiMvOff{Ct + c0, n, m.dc.vals, k, m.pos ? 1 : 0, m.mu, c0}, p.st);
+    GemmShape s2 = make_shape(n, ks, ns, Bo, ld, Ct + c0, n);
     s2.skipf = skipf;
     // optional split-K on the row-dot GEMM (each K share adds its own partial rows, summed in fixed
     // order by finalize); KOT_MV2_SPLIT=2 measured neutral inside the solver (12.66 vs 12.68 it/s)
@@ -647,6 +722,14 @@ static void middle_operator_hform(Problem& p, const MvCtx& m, const double* v, d
   f.out = out;
   f.r0 = 0;
   f.r1 = n;
+  if (m.split) {
+    const FoldedRows fr = folded_rows(n, part, m.world);
+    f.split_rows = 1;
+    f.own0 = fr.a0;
+    f.own1 = fr.a1;
+    f.own2 = fr.b0;
+    f.own3 = fr.b1;
+  }
   finalize_kernel<<<std::min(ceil_div(n, 8), 8 * kNumSMs), 256, 0, p.st>>>(f);
   KOT_LAUNCH_CHECK();
 }
@@ -658,6 +741,21 @@ void middle_operator_fast(Problem& p, const MvCtx& m, const double* v, double* o
   const auto blocks = row_blocks(p);
   const double nn = n, own = nccl ? p.row1 - p.row0 : n;
   Bufs& b = p.bufs();
+  if (m.hform && m.split) {
+    kot_require(skipf == nullptr, KOT_EINVAL, "the split H form runs the CG without batching");
+    if (nccl) {  // this rank's share, then Σ over ranks (ℓ doubles)
+      middle_operator_hform(p, m, v, out, nullptr, p.shard_rank);
+      shard_allreduce_sum(p, out, n, p.st);
+    } else {  // emulation: every rank's share in turn, summed in rank order
+      if (!p.mv_y) p.mv_y = p.alloc(n);
+      middle_operator_hform(p, m, v, out, nullptr, 0);
+      for (int g = 1; g < m.world; ++g) {
+        middle_operator_hform(p, m, v, p.mv_y, nullptr, g);
+        axpby(p, n, 1.0, out, 1.0, p.mv_y, out);
+      }
+    }
+    return;
+  }
   if (m.hform) {
     middle_operator_hform(p, m, v, out, skipf);
     return;

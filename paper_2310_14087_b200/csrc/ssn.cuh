@@ -106,6 +106,9 @@ struct Problem {
   double* ygather = nullptr;  // shard_block·world doubles
   int emul_world = 1;          // test hook: all row blocks in turn on one device, no NCCL
   double* shard_tmp = nullptr;  // (⌊ℓ/2⌋+1)·ℓ block partial of T̃ (emulation only)
+  double* shard_stage = nullptr;  // 2N·⌈ℓ/2N⌉ rows of B in gather order (split H form, sharded)
+  long shard_stage_cap = 0;
+  double* mv_y = nullptr;         // ℓ: one emulated rank's partial y (split H form, emulation)
   std::unique_ptr<Problem> aux_, aux2_, aux3_, crit_;
   Problem& aux();
   Problem& aux2();
@@ -162,7 +165,12 @@ struct MvCtx {
   double mu = 0.0;
   bool pos = true;
   bool direct = false;  // diagnostic: KOT_MATVEC=direct uses the reference Φ*→𝒯→Φ chain
-  bool hform = false;   // same-sign block as a GEMV with H = G_α∘G_α (unsharded; KOT_MATVEC=full: off)
+  bool hform = false;   // same-sign block as a GEMV with H = G_α∘G_α (KOT_MATVEC=full: off)
+  // H form split over ranks (row-sharded problems, or the single-device emulation hook): rank g owns
+  // the columns [c0_g, c1_g) of the mixed sign block (both GEMMs), the rows of its folded row blocks for
+  // the H/Q GEMVs, and the ranks' partial y vectors are summed (one all-reduce of ℓ doubles per matvec)
+  bool split = false;
+  int world = 1;
   double* B = nullptr;
   double* H = nullptr;
   const double *Bs = nullptr, *Bo = nullptr;  // H form: packed smaller / other sign block of B
@@ -178,6 +186,15 @@ void problem_unshard(Problem& p);
 void problem_shard_emulate(Problem& p, int world);
 void problem_shard_host(Problem& p, int (*fn)(void*, int, double*, long, long, int, int), void* user, int rank,
                         int world);
+// collectives of a sharded problem on stream st (NCCL, or the host data plane)
+void shard_allreduce_sum(Problem& p, double* buf, long count, cudaStream_t st);
+void shard_allgather(Problem& p, double* buf, long block, cudaStream_t st);
+// folded row blocks of rank g of N: [a0,a1) = block g and [b0,b1) = block 2N−1−g of ⌈ℓ/2N⌉ rows each,
+// so that every rank gets the same share of R's upper triangle (row i costs ℓ − i in B = R·P)
+struct FoldedRows {
+  int blk, a0, a1, b0, b1;
+};
+FoldedRows folded_rows(int n, int g, int world);
 void shard_allreduce_sum(Problem& p, double* buf, long count);
 void shard_allgather(Problem& p, double* buf, long block);
 // skipf (nullable): every launch is a no-op once *skipf != 0 (batched CG, H form only)

@@ -1,7 +1,9 @@
 """Row-sharded solve (BASELINE config 4's split) run by TWO processes on the one B200, exchanging
 through the host data plane (kot_problem_shard_host over a gloo group) — the world_size-2 evidence
-for the sharded CG matvec.  The ranks' kernels never wait on one another (the collectives are host
-calls between kernel sequences), so co-locating them on one GPU is safe.  Every rank must return the
+for the sharded CG matvec (split H form: each rank's mixed-block columns and folded H/Q rows, one
+all-reduce of ℓ doubles per matvec, B = R·P from folded row blocks plus two all-gathers).  The ranks'
+kernels never wait on one another (the collectives are host calls between kernel sequences), so
+co-locating them on one GPU is safe.  Every rank must return the
 same result, and that result must match the unsharded solve (converged CG: ≤1e-10), including with
 CG restarts (no speculative CG when sharded, so both ranks run the same collectives)."""
 
@@ -86,6 +88,6 @@ def test_two_process_row_sharded_solve(n):
         if name == "converged":
             assert np.linalg.norm(g0 - r.gamma_hat) <= 1e-10 * np.linalg.norm(r.gamma_hat)
             assert np.allclose(res0, [t.res_accepted for t in r.trace], rtol=1e-10)
-        else:  # capped CG with restarts: the sharded (blocked) matvec rounds differently from the unsharded
-            # H-form, so only the envelope of 3 capped-CG iterations is compared
+        else:  # capped CG with restarts: the split H form sums the ranks' partial vectors in another
+            # order than the unsharded matvec, so only the envelope of 3 capped-CG iterations is compared
             assert np.allclose(res0, [t.res_accepted for t in r.trace], rtol=1e-3)

@@ -566,10 +566,13 @@ def test_evaluate_map(cfg1):
 
 @pytest.mark.parametrize("world", [2, 3, 7])
 @pytest.mark.parametrize("shift", [-5.0, 5.0])
-def test_row_sharded_middle_operator(cfg1, world, shift):
-    """The row-block decomposition of the structure-reduced matvec (rowshard.py), every block
-    computed in turn on one device (the single-GPU hook of kot_problem_shard), vs the oracle, for
-    the POS and NONPOS branches and block sizes that do not align with the GEMM tiles."""
+@pytest.mark.parametrize("form", ["reduced", "blocked"])
+def test_row_sharded_middle_operator(cfg1, world, shift, form):
+    """The sharded decompositions of the structure-reduced matvec (rowshard.py), every rank's share
+    computed in turn on one device (the single-GPU hook of kot_problem_shard), vs the oracle, for the
+    POS and NONPOS branches and shares that do not align with the GEMM tiles: "reduced" = the split
+    H form (mixed-block columns + folded H/Q rows per rank, partial vectors summed), "blocked" = the
+    legacy row-block layout (partial T̃ summed)."""
     from paper_2310_14087_b200 import rowshard
     pd = gpu_pd(cfg1)
     po = oracle_pd(cfg1)
@@ -578,7 +581,7 @@ def test_row_sharded_middle_operator(cfg1, world, shift):
     x = cfg1["op_x"] + shift * np.eye(pd.n) * np.abs(np.diag(cfg1["op_x"])).mean()
     g = cfg1["op_g"]
     v = rng.standard_normal(pd.n)
-    out, mu = GN.middle_operator_at(pd, GP.IteratePair(g, x), 0.7, v)
+    out, mu = GN.middle_operator_at(pd, GP.IteratePair(g, x), 0.7, v, form=form)
     r, dc = O.residual_parts(po, O.Pair(g, x))
     ctx = O.newton_context(dc, r.norm(), 0.7)
     ref = O.middle_operator(po, ctx.op, ctx.mu)(v)
