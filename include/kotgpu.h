@@ -172,6 +172,10 @@ int kot_debug_gemm_tma(int mode);       /* 1: TMA-staged DMMA GEMM core (default
 int kot_debug_eg_parallel(int on);      /* EG-step projections side by side (1, default) or in sequence */
 int kot_debug_sytrd_timing(int on, unsigned long long* out8);  /* panel-kernel segment timers (ns) */
 int kot_debug_tail_timing(int on, unsigned long long* out8);   /* cluster-tail segment timers (ns) */
+int kot_debug_mid_timing(int on, unsigned long long* out8);    /* grid-resident mid-kernel segment timers (ns) */
+/* grid-resident sytrd mid kernel: mode 0 off, 1 latency-critical eigensolves (default), 2 every eigensolve;
+ * tail = trailing columns handed to the cluster tail (0: none); a negative value leaves a setting unchanged */
+int kot_debug_trd_mid(int mode, int tail);
 
 /* ---- operators (host buffers in/out; per-kernel parity) ----------------- */
 

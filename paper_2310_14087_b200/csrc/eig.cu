@@ -127,6 +127,9 @@ EigWork::~EigWork() {
   if (ev_w) cudaEventDestroy(ev_w);
   if (ev_rest) cudaEventDestroy(ev_rest);
   dev_free(gcnt);
+  dev_free(mid_x);
+  dev_free(mid_err);
+  if (mid_err_host) host_free_pinned(mid_err_host, sizeof(int));
   dev_free(ibuf);
   dev_free(dbuf);
   host_free_pinned(hbuf, sizeof(int) * (12L * n + 512));
@@ -797,6 +800,22 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) sytrd_tail_kernel(TailArgs a)
 
 __global__ void set_last_diag_kernel(const double* A, int n, double* d) { d[n - 1] = A[(long)(n - 1) * n + n - 1]; }
 
+}  // namespace kot
+#include "sytrd_mid.cuh"
+namespace kot {
+
+void EigWork::ensure_mid() {
+  if (mid_x) return;
+  const size_t bytes = sizeof(MidSector) * 2 * MID_REP_MAX * kNumSMs * MID_SPC;
+  mid_x = dev_alloc(bytes);
+  mid_err = static_cast<int*>(dev_alloc(sizeof(int)));
+  mid_err_host = static_cast<int*>(host_alloc_pinned(sizeof(int)));
+  *mid_err_host = 0;
+  KOT_CUDA(cudaMemset(mid_x, 0, bytes));
+  KOT_CUDA(cudaMemset(mid_err, 0, sizeof(int)));
+}
+
+
 unsigned long long* g_trd_dbg = nullptr;  // set by kot_debug_sytrd_timing
 
 // CTAs of the cooperative panel kernel (≤ one per SM).  KOT_TRD_GRID caps every
@@ -843,6 +862,34 @@ static int trd_grid(int rows, int lane) {
   return g;
 }
 
+// Grid-resident mid kernel: KOT_TRD_MID = 0 off, 1 (default) for latency-critical eigensolves, 2 for
+// every eigensolve (tests); KOT_TRD_MID_TAIL = trailing columns handed to the cluster tail (0: none).
+static std::atomic<int> g_mid_mode{-1};
+static std::atomic<int> g_mid_tail{-1};
+static std::atomic<int> g_mid_rep{4};  // replicas of the exchange sectors (KOT_TRD_MID_REP)
+static int mid_mode() {
+  if (g_mid_mode.load() < 0) {
+    const char* e = std::getenv("KOT_TRD_MID");
+    g_mid_mode = e ? std::max(0, std::atoi(e)) : 1;
+    const char* t = std::getenv("KOT_TRD_MID_TAIL");
+    g_mid_tail = t ? std::max(0, std::atoi(t)) : 0;
+    const char* r = std::getenv("KOT_TRD_MID_REP");
+    if (r) g_mid_rep = std::min(std::max(1, std::atoi(r)), MID_REP_MAX);
+  }
+  return g_mid_mode.load();
+}
+static size_t mid_smem_max() {
+  static const size_t v = [] {
+    int dev = 0, optin = 0;
+    KOT_CUDA(cudaGetDevice(&dev));
+    KOT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa;
+    KOT_CUDA(cudaFuncGetAttributes(&fa, (const void*)sytrd_mid_kernel));
+    return (size_t)optin - fa.sharedSizeBytes;
+  }();
+  return v;
+}
+
 static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane) {
   KOT_CUDA(cudaMemcpyAsync(w.A, Z, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
   KOT_CUDA(cudaMemsetAsync(w.Vall, 0, sizeof(double) * n * n, st));
@@ -851,8 +898,23 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
     return !(e && std::atoi(e) == 0);
   }();
   // columns [c0, n) go to the cluster-resident tail kernel (c0 on a panel boundary)
-  const int c0 = !use_tail ? n : (n <= TAIL_MAX ? 0 : ceil_div(n - TAIL_MAX, TRD_NB) * TRD_NB);
-  for (int p0 = 0; p0 < std::min(c0, n - 1); p0 += TRD_NB) {
+  int c0 = !use_tail ? n : (n <= TAIL_MAX ? 0 : ceil_div(n - TAIL_MAX, TRD_NB) * TRD_NB);
+  // columns [cm, cm + mid_cols) go to the grid-resident mid kernel: a latency-critical eigensolve
+  // (lane 0, not a background chain) whose grid's shared memory holds clearly more than the tail's 640
+  int cm = n, mid_cols = 0, Gm = 0;
+  const int mode = mid_mode();
+  if (mode > 0 && n >= 3 && ((lane == 0 && !background_thread()) || mode >= 2)) {
+    Gm = std::min(trd_grid_cap(lane), kNumSMs);
+    const int cap = mid_capacity(Gm, mid_smem_max());
+    if (cap >= TAIL_MAX + 256 && (n > TAIL_MAX || mode >= 2)) {
+      cm = n <= cap ? 0 : ceil_div(n - cap, TRD_NB) * TRD_NB;
+      const int m0 = n - cm;
+      const int keep = use_tail ? std::min(g_mid_tail.load(), TAIL_MAX) : 0;  // columns left to the tail
+      mid_cols = keep >= 2 && m0 - keep >= 1 ? m0 - keep : m0 - 1;
+      c0 = mid_cols == m0 - 1 ? n : cm + mid_cols;
+    }
+  }
+  for (int p0 = 0; p0 < std::min(std::min(c0, cm), n - 1); p0 += TRD_NB) {
     const int nb = std::min(TRD_NB, n - 1 - p0);
     w.check_cancel(st);
     KOT_CUDA(cudaMemsetAsync(w.X, 0, sizeof(double) * n * 3 * TRD_NB, st));
@@ -901,6 +963,34 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
       gemm_launch<false, true>(s, epi, st);
     }
   }
+  if (mid_cols > 0) {
+    const int m0 = n - cm;
+    const int rpc = ceil_div(m0, Gm), ld = m0 + (m0 & 1);
+    const size_t smem = sizeof(double) * ((size_t)rpc * ld + 4L * ld);
+    ensure_smem_attr((const void*)sytrd_mid_kernel, (int)mid_smem_max());  // static + dynamic may pass 48 KB below it
+    w.ensure_mid();
+    w.mid_seq = (w.mid_seq + 1) & 0xfffffu;
+    if (w.mid_seq == 0) w.mid_seq = 1;
+    MidArgs ma{w.A, n, cm, mid_cols, w.d, w.e, w.tau, w.Vall, static_cast<MidSector*>(w.mid_x),
+               g_mid_rep.load(), w.mid_seq << 12, w.mid_err, g_mid_dbg};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(Gm);
+    cfg.blockDim = dim3(MID_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;  // co-residency: the CTAs spin on each other's slots
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    double bytes = 0.0;
+    for (int c = cm; c < cm + mid_cols; ++c) bytes += 8.0 * 0.5 * (double)(n - c - 1) * (n - c);
+    ProfScope ps("sytrd_mid", st, 0.0, bytes);
+    KOT_CUDA(cudaLaunchKernelEx(&cfg, sytrd_mid_kernel, ma));
+    KOT_LAUNCH_CHECK();
+    KOT_CUDA(cudaMemcpyAsync(w.mid_err_host, w.mid_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    w.mid_used = true;
+  }
   if (c0 < n) {
     const int m0 = n - c0;
     const size_t smem = sizeof(double) * ((size_t)TAIL_RPC * (m0 + 1) + 4L * (m0 + 1));
@@ -921,7 +1011,7 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
     ProfScope ps("sytrd_tail", st);
     KOT_CUDA(cudaLaunchKernelEx(&cfg, sytrd_tail_kernel, ta));
     KOT_LAUNCH_CHECK();
-  } else {
+  } else if (mid_cols == 0) {
     set_last_diag_kernel<<<1, 1, 0, st>>>(w.A, n, w.d);
     KOT_LAUNCH_CHECK();
   }
@@ -2010,6 +2100,10 @@ static void one_stage_tridiag(const double* Z, int n, EigWork& w, cudaStream_t s
   CoopGate gate(total, trd_grid(n, lane), trd_grid(n, 0), lane);
   sytrd(Z, n, w, st, lane);
   KOT_CUDA(cudaStreamSynchronize(st));  // the gate is held until the grids have retired
+  if (w.mid_used) {
+    w.mid_used = false;
+    kot_require(*w.mid_err_host == 0, KOT_EEIG, "sytrd mid kernel: an exchange timed out (grid not co-resident)");
+  }
 }
 
 void tridiag_device(const double* Z, int n, EigWork& w, cudaStream_t st, int stages) {
@@ -2098,4 +2192,31 @@ extern "C" int kot_debug_sytrd_timing(int on, unsigned long long* out8) {
 extern "C" int kot_debug_eig_stages(int stages) {
   kot::g_eig_stages = (stages >= 0 && stages <= 3) ? stages : 0;
   return 0;
+}
+
+// test hook: mode 0 off / 1 latency-critical eigensolves / 2 every eigensolve; tail = trailing columns
+// handed to the cluster tail (0: the mid kernel runs to the last column); negative = leave unchanged
+extern "C" int kot_debug_trd_mid(int mode, int tail) {
+  kot::mid_mode();
+  if (mode >= 0) kot::g_mid_mode = mode;
+  if (tail >= 0) kot::g_mid_tail = tail;
+  return 0;
+}
+
+extern "C" int kot_debug_mid_timing(int on, unsigned long long* out8) {
+  using namespace kot;
+  try {
+    if (on) {
+      if (!g_mid_dbg) KOT_CUDA(cudaMalloc(&g_mid_dbg, 8 * sizeof(unsigned long long)));
+      KOT_CUDA(cudaMemset(g_mid_dbg, 0, 8 * sizeof(unsigned long long)));
+    } else if (g_mid_dbg) {
+      KOT_CUDA(cudaDeviceSynchronize());
+      KOT_CUDA(cudaMemcpy(out8, g_mid_dbg, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      cudaFree(g_mid_dbg);
+      g_mid_dbg = nullptr;
+    }
+    return 0;
+  } catch (const KotError& e) {
+    return e.code;
+  }
 }

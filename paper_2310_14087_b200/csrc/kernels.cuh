@@ -45,6 +45,12 @@ struct EigWork {
   cudaStream_t st_t = nullptr;
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
   void ensure_tfactors();
+  // grid-resident sytrd mid kernel: tagged exchange slots, launch sequence number, error flag
+  void* mid_x = nullptr;
+  int *mid_err = nullptr, *mid_err_host = nullptr;
+  unsigned mid_seq = 0;
+  bool mid_used = false;
+  void ensure_mid();
   cudaEvent_t ev_w = nullptr, ev_rest = nullptr;
   long splitws_cap = 0;
   const std::atomic<bool>* cancel = nullptr;  // set: throw Cancelled at the next panel boundary
