@@ -866,7 +866,7 @@ static int trd_grid(int rows, int lane) {
 // every eigensolve (tests); KOT_TRD_MID_TAIL = trailing columns handed to the cluster tail (0: none).
 static std::atomic<int> g_mid_mode{-1};
 static std::atomic<int> g_mid_tail{-1};
-static std::atomic<int> g_mid_rep{4};  // replicas of the exchange sectors (KOT_TRD_MID_REP)
+static std::atomic<int> g_mid_rep{1};  // replicas of the exchange sectors (KOT_TRD_MID_REP)
 static int mid_mode() {
   if (g_mid_mode.load() < 0) {
     const char* e = std::getenv("KOT_TRD_MID");
@@ -972,7 +972,8 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
     w.mid_seq = (w.mid_seq + 1) & 0xfffffu;
     if (w.mid_seq == 0) w.mid_seq = 1;
     MidArgs ma{w.A, n, cm, mid_cols, w.d, w.e, w.tau, w.Vall, static_cast<MidSector*>(w.mid_x),
-               g_mid_rep.load(), w.mid_seq << 12, w.mid_err, g_mid_dbg};
+               g_mid_rep.load(), w.mid_seq << 12, w.mid_err, g_mid_dbg, g_mid_trace, g_mid_trace_c0,
+               g_mid_trace_cta};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(Gm);
     cfg.blockDim = dim3(MID_THREADS);
@@ -2214,6 +2215,28 @@ extern "C" int kot_debug_mid_timing(int on, unsigned long long* out8) {
       KOT_CUDA(cudaMemcpy(out8, g_mid_dbg, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
       cudaFree(g_mid_dbg);
       g_mid_dbg = nullptr;
+    }
+    return 0;
+  } catch (const KotError& e) {
+    return e.code;
+  }
+}
+
+// clock64 stamps of the mid kernel: [8 columns from c0][16 warps][16 points] of CTA `cta` (on = 1 arms, 0 reads)
+extern "C" int kot_debug_mid_trace(int on, int c0, int cta, long long* out) {
+  using namespace kot;
+  const size_t bytes = sizeof(long long) * MID_TRACE_COLS * MID_WARPS * MID_TRACE_PTS;
+  try {
+    if (on) {
+      if (!g_mid_trace) KOT_CUDA(cudaMalloc(&g_mid_trace, bytes));
+      KOT_CUDA(cudaMemset(g_mid_trace, 0, bytes));
+      g_mid_trace_c0 = c0;
+      g_mid_trace_cta = cta;
+    } else if (g_mid_trace) {
+      KOT_CUDA(cudaDeviceSynchronize());
+      KOT_CUDA(cudaMemcpy(out, g_mid_trace, bytes, cudaMemcpyDeviceToHost));
+      cudaFree(g_mid_trace);
+      g_mid_trace = nullptr;
     }
     return 0;
   } catch (const KotError& e) {

@@ -78,6 +78,6 @@ for n in (2000, 1000):
     L.kot_debug_mid_timing(1, buf)
     linalg.sym_eig(z)
     L.kot_debug_mid_timing(0, buf)
-    names = ["C:update+symv", "publish", "gather", "finish w, x, house, v"]
+    names = ["symv pass", "publish + update", "gather + finish"]
     for nm, v in zip(names, buf):
         print(f"  mid {nm:26s} {v / 1e6:8.3f} ms")
