@@ -97,7 +97,22 @@ __device__ __forceinline__ double mid_sum16(const double* r) {
          (((e.x + e.y) + (f.x + f.y)) + ((g.x + g.y) + (h.x + h.y)));
 }
 
-// The row passes run on a 2-D warp grid: WR = ⌈live rows / 4⌉ row groups × WC = 16 / WR column chunks;
+// three warp sums at once by a transposed butterfly (6 adds instead of 15): the totals of a, b, c end
+// up in lanes 0, 8 and 16
+__device__ __forceinline__ double mid_warp_sum3(double a, double b, double c, int lane) {
+  const bool h16 = lane & 16, h8 = lane & 8;
+  double k0 = h16 ? c : a, k1 = h16 ? 0.0 : b;
+  k0 += __shfl_xor_sync(0xffffffffu, h16 ? a : c, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, h16 ? b : 0.0, 16);
+  double t = (h8 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, h8 ? k0 : k1, 8);
+  t += __shfl_xor_sync(0xffffffffu, t, 4);
+  t += __shfl_xor_sync(0xffffffffu, t, 2);
+  t += __shfl_xor_sync(0xffffffffu, t, 1);
+  return t;
+}
+
+// The row passes run on a 2-D warp grid: WR = ⌈live rows / 4⌉ row groups × WC = 15 / WR column chunks
+// (warp 15 is kept out of them: it derives the Householder scalars beside the symv pass);
 // warp (rg, cc) handles the 4 rows q0 … q0+3 (clamped to the last row; `nr` of them exist) on the
 // double2 columns [i0, i1) counted from column `base` (even).
 //
@@ -259,19 +274,23 @@ __global__ void __launch_bounds__(MID_THREADS, 1) sytrd_mid_kernel(MidArgs a) {
   unsigned long long tl = timing ? gtimer() : 0;
   const bool tracing = a.trace != nullptr && g == a.trace_cta && lane == 0;
 #endif
-  // Exchange c (c = −1 … cend−1) finishes column c (its w) and builds column c+1 (x, Householder
-  // scalars, v); c = −1 only distributes column 0 (τ = 0, v = 0).
-  double tau = 0.0;            // τ of column c
-  double t1 = 0.0, t2 = 0.0;   // w_{c−1}·v_c and v_{c−1}·v_c over the live range (rows > c)
-  int qlo = 0;                 // first live row of the CTA (r > c)
+  // Exchange c (c = −1 … cend−1) finishes column c (its w) and builds column c+1 (the unscaled x̃ and
+  // the sums its Householder scalars need); c = −1 only distributes column 0 (τ = 0, v = 0).
+  //
+  // The scalars of column c (β, τ, 1/(α − β): a chain of ~100 dependent instructions) stay off the
+  // critical path: the symv runs on the UNSCALED column, v = s (x̃ − β e_{c+1}) with s = 1/(α − β) gives
+  // Â v = s (Â x̃ − β Â[:, c+1]), and warp 15 derives the scalars beside the pass; x̃ is scaled into v
+  // (and the reflector stored) while warp 0 publishes.
+  double tau = 0.0;  // τ of column c
+  int qlo = 0;       // first live row of the CTA (r > c)
   // 2-D warp grid of the row passes, recomputed when the number of row groups changes
-  int WR = -1, WC = MID_WARPS, winv = 0, wrg = 0, wcc = 0;
+  int WR = -1, WC = MID_WARPS - 1, winv = 0, wrg = 0, wcc = 0;
 #pragma unroll 1
   for (int c = -1; c < cend; ++c) {
     const int par = c & 1;
-    double* vn = vwbuf + par * 2L * ld;  // v of column c, then (w slot) its w
+    double* vn = vwbuf + par * 2L * ld;  // x̃ then v of column c, and (w slot) its y then w
     double* wn = vn + ld;
-    double* vq = vwbuf + (par ^ 1) * 2L * ld;  // column c−1's v and w (update in flight), then column c+1's v
+    double* vq = vwbuf + (par ^ 1) * 2L * ld;  // column c−1's v and w (update in flight), then column c+1's x̃
     const double* wp = vq + ld;
     const unsigned long long tag = (unsigned long long)a.epoch0 + (unsigned)(c + 2);
     MidSector* xb = a.xchg + (long)par * a.nrep * G * MID_SPC;
@@ -285,7 +304,7 @@ __global__ void __launch_bounds__(MID_THREADS, 1) sytrd_mid_kernel(MidArgs a) {
       const int wr = (nlive + MID_RG - 1) / MID_RG;
       if (wr != WR) {  // rare: a row group died
         WR = wr;
-        WC = WR > 0 ? MID_WARPS / WR : MID_WARPS;  // column chunks (WR ≤ 5: at least 3)
+        WC = WR > 0 ? (MID_WARPS - 1) / WR : MID_WARPS - 1;  // column chunks (WR ≤ 5: at least 3)
         wrg = wid / WC;
         wcc = wid - wrg * WC;
         winv = 65536 / WC + 1;
@@ -295,16 +314,58 @@ __global__ void __launch_bounds__(MID_THREADS, 1) sytrd_mid_kernel(MidArgs a) {
     const int chunk = ((n2 * winv) >> 16) + 1;  // ≥ ⌈n2 / WC⌉
     const int i0 = wcc * chunk, i1 = min(n2, i0 + chunk);
     const int wq0 = qlo + wrg * MID_RG, wnr = min(MID_RG, nrows - wq0);
-    // (1) ŷ_r = Σ_{s>c} Â_rs v_s over the stale rows
+    // (1) z_r = Σ_{s>c} Â_rs x̃_s over the stale rows (warps 0 … 14) ∥ dlarfg of column c (warp 15)
     if (c >= 0) {
       if (wact) mid_symv_pass(Aloc, ld, wq0, wnr, nrows - 1, qlo, base, i0, i1, vn, wcc, ypart, lane);
+      if (wid == MID_WARPS - 1) {
+        // lanes 0..2 reduce the three sums; lane 0: β = −sign(α)‖(α, x)‖, τ = (β − α)/β = 1 + |α|/‖·‖,
+        // 1/(α − β) = sign(α)/(|α| + ‖·‖) with one rsqrt and one reciprocal
+        const double s = lane < 3 ? mid_sum16(red2[lane]) : 0.0;
+        const double xn2 = __shfl_sync(0xffffffffu, s, 0);
+        const double swx = __shfl_sync(0xffffffffu, s, 1), svx = __shfl_sync(0xffffffffu, s, 2);
+        if (lane == 0) {
+          const double alpha = vn[c + 1];
+          double beta, tn, scale;
+          if (xn2 == 0.0) {  // dlarfg: H = I
+            tn = 0.0;
+            beta = alpha;
+            scale = 1.0;
+          } else {
+            const double s2 = fma(alpha, alpha, xn2), aa = fabs(alpha);
+            double nrm, rn;
+            if (s2 > 1e-280 && s2 < 1e280) {  // far from over/underflow: straight from the sum of squares
+              rn = rsqrt(s2);
+              nrm = s2 * rn;
+              nrm = fma(0.5 * rn, fma(-nrm, nrm, s2), nrm);  // one Newton step: sqrt to the last bit or two
+              rn = fma(rn, fma(-nrm, rn, 1.0), rn);           // and its reciprocal
+            } else {  // dlapy2
+              nrm = hypot(alpha, sqrt(xn2));
+              rn = 1.0 / nrm;
+            }
+            beta = -copysign(nrm, alpha);
+            tn = fma(aa, rn, 1.0);
+            scale = copysign(1.0 / (aa + nrm), alpha);
+          }
+          scal[0] = tn;
+          scal[1] = scale;
+          scal[2] = beta;
+          scal[6] = pend ? wp[c + 1] + scale * swx : 0.0;  // w_{c−1}·v_c over the rows > c
+          scal[7] = pend ? vq[c + 1] + scale * svx : 0.0;  // v_{c−1}·v_c
+          if (g == 0) {
+            a.e[c0 + c] = beta;
+            a.tau[c0 + c] = tn;
+          }
+        }
+      }
       MID_TR(1)
       __syncthreads();
+      tau = scal[0];
     }
     MID_TR(2)
     MID_MARK(0)
-    // (2) publish y_r = ŷ_r − v'_r t1 − w'_r t2 and p_r = A_{r,c+1} − τ y_r (update c−1 applied on the
-    // fly; v', w' = column c−1's): warp 0 packs row triples into sectors
+    // (2) warp 0 publishes y_r = s (z_r − β Â_{r,c+1}) − v'_r t1 − w'_r t2 and p_r = A_{r,c+1} − τ y_r
+    // (update c−1 applied on the fly; v', w' = column c−1's) as row triples packed into sectors; the
+    // other warps scale x̃ into v and store the reflector
     if (wid == 0) {
       if (lane < nrows) {
         double y = 0.0, pv = 0.0;
@@ -322,11 +383,11 @@ __global__ void __launch_bounds__(MID_THREADS, 1) sytrd_mid_kernel(MidArgs a) {
               y2 += pb.x;
               y3 += pb.y;
             }
-            y = (y0 + y1) + (y2 + y3);
+            y = scal[1] * (((y0 + y1) + (y2 + y3)) - scal[2] * ac);
           }
           if (pend) {
             const double vr = vq[r], wr = wp[r];
-            y = y - vr * t1 - wr * t2;
+            y = y - vr * scal[6] - wr * scal[7];
             ac = ac - vr * wp[c + 1] - wr * vq[c + 1];
           }
           pv = ac - tau * y;
@@ -340,12 +401,19 @@ __global__ void __launch_bounds__(MID_THREADS, 1) sytrd_mid_kernel(MidArgs a) {
         const double v0 = src[3 * pj], v1 = src[3 * pj + 1], v2 = src[3 * pj + 2];
         for (int rp = 0; rp < a.nrep; ++rp) mid_put(xb + ((long)rp * G + g) * MID_SPC + pk, v0, v1, v2, tag);
       }
+    } else if (c >= 0) {
+      const double scale = scal[1];
+#pragma unroll 1
+      for (int r = c + 1 + tid - 32; r < m0; r += MID_THREADS - 32) vn[r] = (r == c + 1) ? 1.0 : vn[r] * scale;
     }
     MID_TR(3)
-    // (3) while the exchange is in flight: the rows catch up with column c−1's update (after a barrier,
-    // so that the update's shared-memory traffic does not slow the publishing warp down)
+    __syncthreads();
+    if (c >= 0 && tid < nrows) {
+      const int r = g + G * tid;
+      if (r > c) a.Vall[(long)(c0 + r) * n + c0 + c] = (tau == 0.0) ? 0.0 : vn[r];
+    }
+    // (3) while the exchange is in flight: the rows catch up with column c−1's update
     if (pend) {
-      __syncthreads();
       if (wact) mid_update_pass(Aloc, ld, wq0, wnr, nrows - 1, g, G, base, i0, i1, vq, wp, lane);
       MID_TR(4)
       __syncthreads();  // vq (column c−1's v) is free from here on
@@ -383,7 +451,7 @@ __global__ void __launch_bounds__(MID_THREADS, 1) sytrd_mid_kernel(MidArgs a) {
     }
     MID_TR(5)
     __syncthreads();
-    // (5) w = τ y + α₂ v (α₂ = −½ τ² yᵀv) finishes column c; x_{c+1} = p − κ v, κ = τ y_{c+1} + 2 α₂.
+    // (5) w = τ y + α₂ v (α₂ = −½ τ² yᵀv) finishes column c; x̃_{c+1} = p − κ v, κ = τ y_{c+1} + 2 α₂.
     // Thread t takes rows cc + t, cc + t + 512, …; y sits in wn, p in vq, and both are rewritten in place.
     const int cc = c + 1;
     double pyv = 0.0;
@@ -404,82 +472,22 @@ __global__ void __launch_bounds__(MID_THREADS, 1) sytrd_mid_kernel(MidArgs a) {
       const double w = tau * wn[r] + alpha2 * v;
       const double x = vq[r] - kappa * v;
       wn[r] = w;
-      vq[r] = x;
+      if (r == cc) {  // the diagonal entry; the symv pass may start on it (even column): it must not count
+        if (g == 0) a.d[c0 + cc] = x;
+        vq[r] = 0.0;
+      } else {
+        vq[r] = x;
+      }
       if (r >= cc + 2) {
         pn += x * x;
         pwx += w * x;
         pvx += v * x;
       }
     }
-    pn = warp_sum(pn);
-    pwx = warp_sum(pwx);
-    pvx = warp_sum(pvx);
-    if (lane == 0) {
-      red2[0][wid] = pn;
-      red2[1][wid] = pwx;
-      red2[2][wid] = pvx;
-    }
+    const double t3 = mid_warp_sum3(pn, pwx, pvx, lane);
+    if ((lane & 7) == 0 && lane < 24) red2[lane >> 3][wid] = t3;
     __syncthreads();
     MID_TR(7)
-    if (wid == 0) {
-      // lanes 0..2 reduce the three sums; dlarfg on lane 0 with one rsqrt and one reciprocal:
-      // β = −sign(α)‖(α, x)‖, τ = (β − α)/β = 1 + |α|/‖·‖, 1/(α − β) = sign(α)/(|α| + ‖·‖)
-      const double s = lane < 3 ? mid_sum16(red2[lane]) : 0.0;
-      const double xn2 = __shfl_sync(0xffffffffu, s, 0);
-      const double swx = __shfl_sync(0xffffffffu, s, 1), svx = __shfl_sync(0xffffffffu, s, 2);
-      if (lane == 0) {
-        const double alpha = vq[cc + 1 < m0 ? cc + 1 : cc];
-        double beta, tn, scale;
-        if (xn2 == 0.0 || cc + 1 >= m0) {  // dlarfg: H = I
-          tn = 0.0;
-          beta = alpha;
-          scale = 1.0;
-        } else {
-          const double s2 = fma(alpha, alpha, xn2), aa = fabs(alpha);
-          double nrm, rn;
-          if (s2 > 1e-280 && s2 < 1e280) {  // far from over/underflow: straight from the sum of squares
-            rn = rsqrt(s2);
-            nrm = s2 * rn;
-            nrm = fma(0.5 * rn, fma(-nrm, nrm, s2), nrm);  // one Newton step: sqrt to the last bit or two
-            rn = fma(rn, fma(-nrm, rn, 1.0), rn);           // and its reciprocal
-          } else {  // dlapy2
-            nrm = hypot(alpha, sqrt(xn2));
-            rn = 1.0 / nrm;
-          }
-          beta = -copysign(nrm, alpha);
-          tn = fma(aa, rn, 1.0);
-          const double dsum = aa + nrm;
-          double rd = 1.0 / dsum;
-          scale = copysign(rd, alpha);
-        }
-        scal[0] = tn;
-        scal[1] = scale;
-        scal[6] = cc + 1 < m0 ? wn[cc + 1 < m0 ? cc + 1 : cc] + scale * swx : 0.0;  // w_c·v_{c+1}
-        scal[7] = cc + 1 < m0 ? vn[cc + 1 < m0 ? cc + 1 : cc] + scale * svx : 0.0;  // v_c·v_{c+1}
-        if (g == 0) {
-          a.d[c0 + cc] = vq[cc];
-          if (cc < cend) {
-            a.e[c0 + cc] = beta;
-            a.tau[c0 + cc] = tn;
-          }
-        }
-      }
-    }
-    MID_TR(13)
-    __syncthreads();
-    MID_TR(8)
-    tau = scal[0];
-    t1 = scal[6];
-    t2 = scal[7];
-    const double scale = scal[1];
-#pragma unroll 1
-    for (int r = cc + tid; r < m0; r += MID_THREADS)
-      vq[r] = (r == cc) ? 0.0 : (r == cc + 1) ? 1.0 : vq[r] * scale;  // entry cc masks the even start
-    __syncthreads();
-    if (tid < nrows && cc < cend) {
-      const int r = g + G * tid;
-      if (r > cc) a.Vall[(long)(c0 + r) * n + c0 + cc] = (tau == 0.0) ? 0.0 : vq[r];
-    }
     MID_TR(9)
     MID_MARK(2)
   }
