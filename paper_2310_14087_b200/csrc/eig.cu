@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cfloat>
+#include <chrono>
 #include <condition_variable>
 #include <mutex>
 #include <vector>
@@ -129,7 +130,7 @@ EigWork::~EigWork() {
   dev_free(gcnt);
   dev_free(mid_x);
   dev_free(mid_err);
-  if (mid_err_host) host_free_pinned(mid_err_host, sizeof(int));
+  if (mid_err_host) host_free_pinned(mid_err_host, 2 * sizeof(int));
   dev_free(ibuf);
   dev_free(dbuf);
   host_free_pinned(hbuf, sizeof(int) * (12L * n + 512));
@@ -809,8 +810,9 @@ void EigWork::ensure_mid() {
   const size_t bytes = sizeof(MidSector) * 2 * MID_REP_MAX * kNumSMs * MID_SPC;
   mid_x = dev_alloc(bytes);
   mid_err = static_cast<int*>(dev_alloc(sizeof(int)));
-  mid_err_host = static_cast<int*>(host_alloc_pinned(sizeof(int)));
-  *mid_err_host = 0;
+  mid_err_host = static_cast<int*>(host_alloc_pinned(2 * sizeof(int)));
+  mid_err_host[0] = mid_err_host[1] = 0;
+  mid_resident = reinterpret_cast<unsigned*>(mid_err_host + 1);
   KOT_CUDA(cudaMemset(mid_x, 0, bytes));
   KOT_CUDA(cudaMemset(mid_err, 0, sizeof(int)));
 }
@@ -833,6 +835,10 @@ void eig_pipeline_active(int delta) { g_pipelines += delta; }
 // concurrent solves (config-5 batches) share the GPU better with thin grids.
 static std::atomic<int> g_trd_cap{-1};
 void set_panel_grid_cap(int cap) { g_trd_cap = cap > 0 ? std::min(cap, kNumSMs) : kNumSMs; }
+static int trd_grid_cap_all() {
+  if (g_trd_cap.load() < 0) g_trd_cap = std::min(env_int("KOT_TRD_GRID", kNumSMs), kNumSMs);
+  return g_trd_cap.load();
+}
 static int trd_grid_cap(int lane) {
   if (g_trd_cap.load() < 0) g_trd_cap = std::min(env_int("KOT_TRD_GRID", kNumSMs), kNumSMs);
   const int cap = g_trd_cap.load();
@@ -862,6 +868,77 @@ static int trd_grid(int rows, int lane) {
   return g;
 }
 
+// Cooperative sytrd grids from different streams/host threads must never need
+// more co-resident CTAs than the SMs can hold at once (their blocks spin on a
+// grid barrier).  This process-wide gate accounts CTA slots (occupancy × SMs):
+// a grid is admitted when its CTAs fit, and background grids (lane ≠ 0) may
+// only use what is left after reserving one full lane-0 grid, so a Newton-chain
+// eigensolve never queues behind the EG pipeline.
+//
+// The grid-resident mid kernel needs WHOLE SMs (one 220 KB CTA each) and its CTAs spin on each other
+// from the first column on, so it must never wait for SMs behind a stream of small background CTAs:
+// its owner first makes the gate exclusive (no new background grid is admitted, the ones in flight
+// retire — a panel launch lasts under a millisecond), launches, waits until the kernel reports every
+// CTA resident (its first exchange completed), and then re-opens the gate with the slots of its SMs
+// accounted, so the background chains' grids go on beside it on the remaining SMs.
+namespace {
+std::mutex g_coop_mu;
+std::condition_variable g_coop_cv;
+int g_coop_used = 0;
+int g_coop_fg = 0;      // lane-0 grids in flight
+bool g_coop_excl = false;  // an exclusive owner is waiting or launching: no new admissions
+struct CoopGate {
+  int slots, lane, total, limit_bg;
+  CoopGate(int total_, int want, int reserve, int lane_) : slots(want), lane(lane_), total(total_) {
+    static const bool yield_bg = [] {  // diagnostic: background grids wait while a lane-0 grid runs
+      const char* e = std::getenv("KOT_COOP_YIELD");
+      return e && std::atoi(e) > 0;
+    }();
+    std::unique_lock<std::mutex> lk(g_coop_mu);
+    limit_bg = total - reserve;
+    const int limit = (lane == 0) ? total : limit_bg;
+    g_coop_cv.wait(lk, [&] {
+      if (g_coop_excl) return false;
+      if (lane != 0 && yield_bg && g_coop_fg > 0) return false;
+      return g_coop_used + want <= limit || g_coop_used == 0;
+    });
+    g_coop_used += want;
+    if (lane == 0) ++g_coop_fg;
+  }
+  // no other grid in flight and none admitted until exclusive_end
+  void exclusive_begin() {
+    // (the caller's own grids have retired: its slots go back while it waits, so that two owners
+    // cannot block each other)
+    std::unique_lock<std::mutex> lk(g_coop_mu);
+    g_coop_used -= slots;
+    g_coop_cv.notify_all();
+    g_coop_cv.wait(lk, [&] { return !g_coop_excl; });
+    g_coop_excl = true;
+    g_coop_cv.wait(lk, [&] { return g_coop_used == 0; });
+    g_coop_used += slots;
+  }
+  // the owner's kernel is resident on `sms` whole SMs: account them and admit the others again
+  void exclusive_end(int sms, int per_sm) {
+    {
+      std::lock_guard<std::mutex> lk(g_coop_mu);
+      const int hold = std::max(slots, limit_bg - per_sm * (kNumSMs - sms));
+      g_coop_used += hold - slots;
+      slots = hold;
+      g_coop_excl = false;
+    }
+    g_coop_cv.notify_all();
+  }
+  ~CoopGate() {
+    {
+      std::lock_guard<std::mutex> lk(g_coop_mu);
+      g_coop_used -= slots;
+      if (lane == 0) --g_coop_fg;
+    }
+    g_coop_cv.notify_all();
+  }
+};
+}  // namespace
+
 // Grid-resident mid kernel: KOT_TRD_MID = 0 off, 1 (default) for latency-critical eigensolves, 2 for
 // every eigensolve (tests); KOT_TRD_MID_TAIL = trailing columns handed to the cluster tail (0: none).
 static std::atomic<int> g_mid_mode{-1};
@@ -890,7 +967,7 @@ static size_t mid_smem_max() {
   return v;
 }
 
-static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane) {
+static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane, CoopGate* gate, int per_sm) {
   KOT_CUDA(cudaMemcpyAsync(w.A, Z, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
   KOT_CUDA(cudaMemsetAsync(w.Vall, 0, sizeof(double) * n * n, st));
   static const bool use_tail = [] {
@@ -904,7 +981,11 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
   int cm = n, mid_cols = 0, Gm = 0;
   const int mode = mid_mode();
   if (mode > 0 && n >= 3 && ((lane == 0 && !background_thread()) || mode >= 2)) {
-    Gm = std::min(trd_grid_cap(lane), kNumSMs);
+    // beside an EG pipeline the mid kernel takes KOT_TRD_MID_GRID whole SMs (default 96) and the
+    // background chains keep the others; alone, every SM
+    static const int mid_grid_shared = env_int("KOT_TRD_MID_GRID", 96);
+    Gm = std::min(g_pipelines.load() > 0 && lane == 0 ? std::min(mid_grid_shared, trd_grid_cap_all()) : trd_grid_cap(lane),
+                  kNumSMs);
     const int cap = mid_capacity(Gm, mid_smem_max());
     if (cap >= TAIL_MAX + 256 && (n > TAIL_MAX || mode >= 2)) {
       cm = n <= cap ? 0 : ceil_div(n - cap, TRD_NB) * TRD_NB;
@@ -972,7 +1053,7 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
     w.mid_seq = (w.mid_seq + 1) & 0xfffffu;
     if (w.mid_seq == 0) w.mid_seq = 1;
     MidArgs ma{w.A, n, cm, mid_cols, w.d, w.e, w.tau, w.Vall, static_cast<MidSector*>(w.mid_x),
-               g_mid_rep.load(), w.mid_seq << 12, w.mid_err, g_mid_dbg, g_mid_trace, g_mid_trace_c0,
+               g_mid_rep.load(), w.mid_seq << 12, w.mid_err, w.mid_resident, g_mid_dbg, g_mid_trace, g_mid_trace_c0,
                g_mid_trace_cta};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(Gm);
@@ -986,9 +1067,25 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane)
     cfg.numAttrs = 1;
     double bytes = 0.0;
     for (int c = cm; c < cm + mid_cols; ++c) bytes += 8.0 * 0.5 * (double)(n - c - 1) * (n - c);
-    ProfScope ps("sytrd_mid", st, 0.0, bytes);
-    KOT_CUDA(cudaLaunchKernelEx(&cfg, sytrd_mid_kernel, ma));
-    KOT_LAUNCH_CHECK();
+    // other cooperative grids may be in flight (EG pipeline, concurrent solves): launch exclusively
+    const bool shared_gpu = gate != nullptr && (g_pipelines.load() > 0 || lane != 0 || background_thread());
+    if (shared_gpu) {
+      KOT_CUDA(cudaStreamSynchronize(st));  // our own panels have retired
+      gate->exclusive_begin();
+    }
+    {
+      ProfScope ps("sytrd_mid", st, 0.0, bytes);
+      KOT_CUDA(cudaLaunchKernelEx(&cfg, sytrd_mid_kernel, ma));
+      KOT_LAUNCH_CHECK();
+    }
+    if (shared_gpu) {
+      // every CTA is resident once CTA 0 has completed the first exchange
+      const auto t0 = std::chrono::steady_clock::now();
+      while (*reinterpret_cast<volatile unsigned*>(w.mid_resident) != ma.epoch0) {
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(4)) break;  // the kernel's own timeout reports
+      }
+      gate->exclusive_end(Gm, per_sm);
+    }
     KOT_CUDA(cudaMemcpyAsync(w.mid_err_host, w.mid_err, sizeof(int), cudaMemcpyDeviceToHost, st));
     w.mid_used = true;
   }
@@ -2026,44 +2123,6 @@ __global__ void eig1_kernel(const double* Z, double* P, double* vals) {
   P[0] = 1.0;
 }
 
-// Cooperative sytrd grids from different streams/host threads must never need
-// more co-resident CTAs than the SMs can hold at once (their blocks spin on a
-// grid barrier).  This process-wide gate accounts CTA slots (occupancy × SMs):
-// a grid is admitted when its CTAs fit, and background grids (lane ≠ 0) may
-// only use what is left after reserving one full lane-0 grid, so a Newton-chain
-// eigensolve never queues behind the EG pipeline.
-namespace {
-std::mutex g_coop_mu;
-std::condition_variable g_coop_cv;
-int g_coop_used = 0;
-int g_coop_fg = 0;  // lane-0 grids in flight
-struct CoopGate {
-  int slots, lane;
-  CoopGate(int total, int want, int reserve, int lane_) : slots(want), lane(lane_) {
-    static const bool yield_bg = [] {  // diagnostic: background grids wait while a lane-0 grid runs
-      const char* e = std::getenv("KOT_COOP_YIELD");
-      return e && std::atoi(e) > 0;
-    }();
-    std::unique_lock<std::mutex> lk(g_coop_mu);
-    const int limit = (lane == 0) ? total : total - reserve;
-    g_coop_cv.wait(lk, [&] {
-      if (lane != 0 && yield_bg && g_coop_fg > 0) return false;
-      return g_coop_used + want <= limit || g_coop_used == 0;
-    });
-    g_coop_used += want;
-    if (lane == 0) ++g_coop_fg;
-  }
-  ~CoopGate() {
-    {
-      std::lock_guard<std::mutex> lk(g_coop_mu);
-      g_coop_used -= slots;
-      if (lane == 0) --g_coop_fg;
-    }
-    g_coop_cv.notify_all();
-  }
-};
-}  // namespace
-
 static int sytrd_per_sm(int n) {
   const size_t smem = sizeof(double) * (std::max(n, 1) + 3L * TRD_WARPS * TRD_RPW * TRD_NB);
   ensure_smem_attr((const void*)sytrd_panel_kernel, (int)smem);
@@ -2099,7 +2158,7 @@ static void one_stage_tridiag(const double* Z, int n, EigWork& w, cudaStream_t s
   ProfScope ps("eig.sytrd", st, 4.0 / 3.0 * n * (double)n * n);
   const int total = sytrd_per_sm(n) * kNumSMs;
   CoopGate gate(total, trd_grid(n, lane), trd_grid(n, 0), lane);
-  sytrd(Z, n, w, st, lane);
+  sytrd(Z, n, w, st, lane, &gate, total / kNumSMs);
   KOT_CUDA(cudaStreamSynchronize(st));  // the gate is held until the grids have retired
   if (w.mid_used) {
     w.mid_used = false;

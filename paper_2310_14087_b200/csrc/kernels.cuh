@@ -48,6 +48,7 @@ struct EigWork {
   // grid-resident sytrd mid kernel: tagged exchange slots, launch sequence number, error flag
   void* mid_x = nullptr;
   int *mid_err = nullptr, *mid_err_host = nullptr;
+  unsigned* mid_resident = nullptr;  // host-mapped: the kernel's epoch once every CTA is resident
   unsigned mid_seq = 0;
   bool mid_used = false;
   void ensure_mid();

@@ -61,6 +61,7 @@ struct MidArgs {
   int nrep;
   unsigned epoch0;
   int* err;                 // set to 1 when a gather timed out
+  unsigned* resident;       // host-mapped: CTA 0 stores epoch0 after its first gather (every CTA is resident)
   unsigned long long* dbg;  // nullable: per-segment ns accumulated by CTA 0 thread 0
   long long* trace;         // nullable: clock64 stamps [MID_TRACE_COLS][MID_WARPS][MID_TRACE_PTS] of CTA trace_cta
   int trace_c0, trace_cta;
@@ -451,6 +452,10 @@ __global__ void __launch_bounds__(MID_THREADS, 1) sytrd_mid_kernel(MidArgs a) {
     }
     MID_TR(5)
     __syncthreads();
+    if (c == -1 && g == 0 && tid == 0) {  // every producer has published: the whole grid is resident
+      *reinterpret_cast<volatile unsigned*>(a.resident) = a.epoch0;
+      __threadfence_system();
+    }
     // (5) w = τ y + α₂ v (α₂ = −½ τ² yᵀv) finishes column c; x̃_{c+1} = p − κ v, κ = τ y_{c+1} + 2 α₂.
     // Thread t takes rows cc + t, cc + t + 512, …; y sits in wn, p in vq, and both are rewritten in place.
     const int cc = c + 1;
