@@ -385,7 +385,7 @@ def run_gpu(args):
             dist.destroy_process_group()
         return 0
 
-    roof, roof_gemm, phases = roofline(prof, done)
+    roof, roof_gemm, roof_mid, phases = roofline(prof, done)
 
     # ---------------- CPU baseline (oracle port, bounded sample of the same window)
     cpu = None
@@ -409,6 +409,7 @@ def run_gpu(args):
         "gpu_launches": int(launches),
         "roofline": roof,
         "roofline_gemm": roof_gemm,
+        "roofline_mid": roof_mid,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
         "time_to_tol": ttt,
@@ -452,6 +453,19 @@ def roofline(prof: dict, done: int):
                                "trailing matrix, 8*m(m+1)/2 B",
                 "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"],
                 "sampled": None if full else "1 in 16 launches (time and algorithmic bytes of the same launches)"}
+    roof_mid = None
+    if "sytrd_mid" in prof:  # the Newton chain's eigensolves: the trailing block resident in shared memory
+        e = prof["sytrd_mid"]
+        ach = e["bytes"] / e["calls"] / (e["ms"] / e["calls"] * 1e-3) / 1e9
+        t = traffic.get("sytrd_mid_kernel", {})
+        roof_mid = {"kernel": "sytrd_mid_kernel (grid-resident unblocked Householder: one tagged-sector all-gather "
+                              "per column, the trailing block in shared memory)",
+                    "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                    "traffic": t.get("dram_bytes_per_launch"), "traffic_source": t.get("source"),
+                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                    "algorithmic": "per launch: sum over its columns of one lower-triangle read of the trailing "
+                                   "matrix, 8*m(m+1)/2 B (served from shared memory: the block is read from HBM once)",
+                    "avg_launch_ms": e["ms"] / e["calls"], "launches": e["calls"]}
     if roof is None and "eig.q2" in prof:  # two-stage path (l >= 3000): the tensor-core Q2 back-transform
         e = prof["eig.q2"]
         ach = e["flops"] / (e["ms"] * 1e-3) / 1e12
@@ -473,7 +487,7 @@ def roofline(prof: dict, done: int):
                   **({"sampled": {"gemm_dmma": "1 in 128 launches", "sytrd_panel": "1 in 16 launches"}[k]}
                      if k in ("gemm_dmma", "sytrd_panel") and not full else {})}
               for k, v in prof.items()}
-    return roof, roof_gemm, phases
+    return roof, roof_gemm, roof_mid, phases
 
 
 def cpu_baseline_from_state(wl, profile: str, state, k0: int, iters: int, stepsize: float) -> dict:

@@ -97,6 +97,11 @@ void EigWork::ensure_two_stage() {
   KOT_CUDA(cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming));
 }
 
+void EigWork::ensure_panel_events() {
+  if (ev_panel[0]) return;
+  for (auto& e : ev_panel) KOT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
 void EigWork::ensure_tfactors() {
   if (Tall) return;
   const int nblk = std::max(1, (n - 1 + 127) / 128);
@@ -122,6 +127,8 @@ EigWork::~EigWork() {
     cudaStreamSynchronize(st_t);
     cudaStreamDestroy(st_t);
   }
+  for (auto e : ev_panel)
+    if (e) cudaEventDestroy(e);
   if (ev_t0) cudaEventDestroy(ev_t0);
   if (ev_t1) cudaEventDestroy(ev_t1);
   for (double* q : {Tall, Sside, ws_t}) dev_free(q);
@@ -887,6 +894,7 @@ std::condition_variable g_coop_cv;
 int g_coop_used = 0;
 int g_coop_fg = 0;      // lane-0 grids in flight
 bool g_coop_excl = false;  // an exclusive owner is waiting or launching: no new admissions
+std::atomic<bool> g_coop_excl_hint{false};  // lock-free mirror, polled by the panel loops
 struct CoopGate {
   int slots, lane, total, limit_bg;
   CoopGate(int total_, int want, int reserve, int lane_) : slots(want), lane(lane_), total(total_) {
@@ -914,7 +922,22 @@ struct CoopGate {
     g_coop_cv.notify_all();
     g_coop_cv.wait(lk, [&] { return !g_coop_excl; });
     g_coop_excl = true;
+    g_coop_excl_hint = true;
     g_coop_cv.wait(lk, [&] { return g_coop_used == 0; });
+    g_coop_used += slots;
+  }
+  // Called by the other chains between two panel launches: when an exclusive owner waits, let the
+  // grids in flight retire, give the slots back and come back once the owner's kernel is resident
+  // (a gate is otherwise held for a whole tridiagonalisation, tens of milliseconds).
+  void yield_to_exclusive(cudaStream_t st) {
+    if (!g_coop_excl_hint.load(std::memory_order_relaxed)) return;
+    KOT_CUDA(cudaStreamSynchronize(st));
+    std::unique_lock<std::mutex> lk(g_coop_mu);
+    if (!g_coop_excl) return;
+    g_coop_used -= slots;
+    g_coop_cv.notify_all();
+    const int limit = (lane == 0) ? total : limit_bg;
+    g_coop_cv.wait(lk, [&] { return !g_coop_excl && (g_coop_used + slots <= limit || g_coop_used == 0); });
     g_coop_used += slots;
   }
   // the owner's kernel is resident on `sms` whole SMs: account them and admit the others again
@@ -925,6 +948,7 @@ struct CoopGate {
       g_coop_used += hold - slots;
       slots = hold;
       g_coop_excl = false;
+      g_coop_excl_hint = false;
     }
     g_coop_cv.notify_all();
   }
@@ -995,9 +1019,22 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane,
       c0 = mid_cols == m0 - 1 ? n : cm + mid_cols;
     }
   }
+  const bool throttle = gate != nullptr && (lane != 0 || background_thread()) && mode > 0 && g_pipelines.load() > 0;
+  static const int depth = std::min(env_int("KOT_TRD_THROTTLE", 2), 8);  // panels enqueued ahead of the GPU
+  if (throttle) w.ensure_panel_events();
   for (int p0 = 0; p0 < std::min(std::min(c0, cm), n - 1); p0 += TRD_NB) {
     const int nb = std::min(TRD_NB, n - 1 - p0);
     w.check_cancel(st);
+    if (gate) {
+      // background chains stay within a few panels of the GPU, so that they reach this point (and can
+      // yield to a mid kernel's exclusive window) within a millisecond or two instead of having the
+      // whole tridiagonalisation enqueued
+      if (throttle) {
+        const int pi = p0 / TRD_NB;
+        if (pi >= depth) KOT_CUDA(cudaEventSynchronize(w.ev_panel[pi % depth]));
+      }
+      gate->yield_to_exclusive(st);
+    }
     KOT_CUDA(cudaMemsetAsync(w.X, 0, sizeof(double) * n * 3 * TRD_NB, st));
     const int rows = n - p0;
     const int G = trd_grid(rows, lane);
@@ -1043,6 +1080,7 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane,
       EpiSymMirror epi{C, n, -1.0, C, 1.0, 0.0};
       gemm_launch<false, true>(s, epi, st);
     }
+    if (throttle) KOT_CUDA(cudaEventRecord(w.ev_panel[(p0 / TRD_NB) % depth], st));
   }
   if (mid_cols > 0) {
     const int m0 = n - cm;
@@ -1069,9 +1107,13 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane,
     for (int c = cm; c < cm + mid_cols; ++c) bytes += 8.0 * 0.5 * (double)(n - c - 1) * (n - c);
     // other cooperative grids may be in flight (EG pipeline, concurrent solves): launch exclusively
     const bool shared_gpu = gate != nullptr && (g_pipelines.load() > 0 || lane != 0 || background_thread());
+    const auto tx0 = std::chrono::steady_clock::now();
     if (shared_gpu) {
       KOT_CUDA(cudaStreamSynchronize(st));  // our own panels have retired
+      const auto tx1 = std::chrono::steady_clock::now();
       gate->exclusive_begin();
+      prof_host("host.mid_sync", std::chrono::duration<double, std::milli>(tx1 - tx0).count());
+      prof_host("host.mid_excl", std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tx1).count());
     }
     {
       ProfScope ps("sytrd_mid", st, 0.0, bytes);
@@ -1084,12 +1126,14 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane,
       while (*reinterpret_cast<volatile unsigned*>(w.mid_resident) != ma.epoch0) {
         if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(4)) break;  // the kernel's own timeout reports
       }
+      prof_host("host.mid_resident", std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
       gate->exclusive_end(Gm, per_sm);
     }
     KOT_CUDA(cudaMemcpyAsync(w.mid_err_host, w.mid_err, sizeof(int), cudaMemcpyDeviceToHost, st));
     w.mid_used = true;
   }
   if (c0 < n) {
+    if (gate) gate->yield_to_exclusive(st);
     const int m0 = n - c0;
     const size_t smem = sizeof(double) * ((size_t)TAIL_RPC * (m0 + 1) + 4L * (m0 + 1));
     ensure_smem_attr((const void*)sytrd_tail_kernel, (int)smem, true);

@@ -52,6 +52,8 @@ struct EigWork {
   unsigned mid_seq = 0;
   bool mid_used = false;
   void ensure_mid();
+  cudaEvent_t ev_panel[8] = {};  // panel-loop throttle of the background chains
+  void ensure_panel_events();
   cudaEvent_t ev_w = nullptr, ev_rest = nullptr;
   long splitws_cap = 0;
   const std::atomic<bool>* cancel = nullptr;  // set: throw Cancelled at the next panel boundary

@@ -44,6 +44,7 @@ bool wanted(const char* name) {
   if (g_mode != 2) return true;
   if (std::strcmp(name, "sytrd_panel") == 0) return (g_trd_seen++ & 15) == 0;
   if (std::strcmp(name, "eig.q2") == 0) return true;
+  if (std::strcmp(name, "sytrd_mid") == 0) return true;  // one launch per latency-critical eigensolve
   if (std::strcmp(name, "gemm_dmma") == 0) return (g_gemm_seen++ & 127) == 0;
   return false;
 }

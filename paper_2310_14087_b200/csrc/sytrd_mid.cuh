@@ -334,18 +334,29 @@ __global__ void __launch_bounds__(MID_THREADS, 1) sytrd_mid_kernel(MidArgs a) {
           } else {
             const double s2 = fma(alpha, alpha, xn2), aa = fabs(alpha);
             double nrm, rn;
-            if (s2 > 1e-280 && s2 < 1e280) {  // far from over/underflow: straight from the sum of squares
-              rn = rsqrt(s2);
+            double rd;
+            if (s2 > 1e-280 && s2 < 1e280) {  // far from over/underflow: straight from the sum of squares,
+              // hardware seeds + Newton steps (a short dependent chain; results within an ulp or two)
+              asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rn) : "d"(s2));
+              const double hs = 0.5 * s2;
+              rn = rn * fma(-hs * rn, rn, 1.5);
+              rn = rn * fma(-hs * rn, rn, 1.5);
               nrm = s2 * rn;
-              nrm = fma(0.5 * rn, fma(-nrm, nrm, s2), nrm);  // one Newton step: sqrt to the last bit or two
-              rn = fma(rn, fma(-nrm, rn, 1.0), rn);           // and its reciprocal
+              nrm = fma(0.5 * rn, fma(-nrm, nrm, s2), nrm);
+              rn = fma(rn, fma(-nrm, rn, 1.0), rn);
+              const double dsum = aa + nrm;
+              asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(dsum));
+              rd = fma(rd, fma(-dsum, rd, 1.0), rd);
+              rd = fma(rd, fma(-dsum, rd, 1.0), rd);
+              rd = fma(rd, fma(-dsum, rd, 1.0), rd);
             } else {  // dlapy2
               nrm = hypot(alpha, sqrt(xn2));
               rn = 1.0 / nrm;
+              rd = 1.0 / (aa + nrm);
             }
             beta = -copysign(nrm, alpha);
             tn = fma(aa, rn, 1.0);
-            scale = copysign(1.0 / (aa + nrm), alpha);
+            scale = copysign(rd, alpha);
           }
           scal[0] = tn;
           scal[1] = scale;

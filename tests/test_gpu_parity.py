@@ -633,6 +633,86 @@ def test_row_sharded_iteration_replay(cfg1):
         assert rel(w2.x_mat, ost.w.x) <= 1e-8, i
 
 
+# ------------------------------------------- grid-resident sytrd mid kernel (sytrd_mid.cuh)
+
+@pytest.fixture
+def mid_everywhere():
+    """Force the grid-resident mid kernel for every order (default: latency-critical eigensolves with a
+    trailing block larger than the cluster tail's)."""
+    from paper_2310_14087_b200 import _lib
+    f = _lib.lib().kot_debug_trd_mid
+    yield f
+    f(1, 0)
+
+
+def _check_decomposition(z, tol=1e-12):
+    n = z.shape[0]
+    dc = GL.sym_eig(z)
+    ref = np.sort(np.linalg.eigvalsh(z))[::-1]
+    nz = max(np.abs(ref).max(), 1e-300)
+    p = dc.eigvecs
+    assert np.max(np.abs(dc.eigvals - ref)) <= tol * nz * max(1.0, n / 100)
+    assert np.max(np.abs(p.T @ p - np.eye(n))) <= tol * max(1.0, n / 100)
+    assert np.max(np.abs((p * dc.eigvals) @ p.T - z)) <= tol * nz * max(1.0, n / 100)
+    return dc
+
+
+@pytest.mark.parametrize("tail", [0, 200, 640])
+@pytest.mark.parametrize("n", [3, 4, 33, 148, 149, 257, 641, 999, 1000])
+def test_mid_kernel_sym_eig(mid_everywhere, n, tail):
+    """Every column through the mid kernel (tail = 0) or handed over to the cluster tail for the last
+    `tail` columns; odd and even orders (padding column), fewer rows than CTAs, one row triple."""
+    mid_everywhere(2, tail)
+    rng = np.random.default_rng(1000 * tail + n)
+    _check_decomposition(random_symmetric(rng, n))
+
+
+@pytest.mark.parametrize("n", [1500, 1776, 1777, 2000])
+def test_mid_kernel_large_orders(mid_everywhere, n):
+    """Orders around the resident-block capacity (1776 on 148 SMs): panels first, then the mid kernel."""
+    mid_everywhere(1, 0)
+    rng = np.random.default_rng(n)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    vals = np.concatenate([np.linspace(1, 100, n // 2), -np.linspace(1e-4, 1, n - n // 2)])
+    z = (q * vals) @ q.T
+    _check_decomposition(0.5 * (z + z.T))
+
+
+def test_mid_kernel_identity_reflectors(mid_everywhere):
+    """Columns with H = I (τ = 0): a diagonal matrix, and a block matrix mixing both kinds of column."""
+    mid_everywhere(2, 0)
+    rng = np.random.default_rng(5)
+    _check_decomposition(np.diag(rng.standard_normal(700)))
+    b = np.zeros((800, 800))
+    x = rng.standard_normal((400, 400))
+    b[:400, :400] = (x + x.T) / 2
+    b[600:, 600:] = np.eye(200) * 3.0
+    _check_decomposition(b)
+
+
+@pytest.mark.parametrize("scale", [1e-145, 1e-8, 1e8, 1e150])
+def test_mid_kernel_scales(mid_everywhere, scale):
+    """dlarfg from the sum of squares (hardware rsqrt / reciprocal seeds + Newton steps) and its dlapy2
+    branch for sums of squares near over/underflow (below 1e-145 the divide-and-conquer stage itself
+    loses accuracy to underflow, with or without this kernel)."""
+    mid_everywhere(2, 0)
+    rng = np.random.default_rng(9)
+    _check_decomposition(scale * random_symmetric(rng, 300), tol=1e-11 if scale < 1e-100 else 1e-12)
+
+
+def test_mid_kernel_is_deterministic(mid_everywhere):
+    """The tagged-sector exchange never delivers a torn or stale payload: repeated eigensolves of the
+    same matrix are bit-identical (every CTA derives the same scalars from the same gathered vectors)."""
+    mid_everywhere(1, 0)
+    rng = np.random.default_rng(21)
+    z = random_symmetric(rng, 1400)
+    first = GL.sym_eig(z)
+    for _ in range(20):
+        again = GL.sym_eig(z)
+        assert np.array_equal(first.eigvals, again.eigvals)
+        assert np.array_equal(first.eigvecs, again.eigvecs)
+
+
 # ------------------------------------------- two-stage tridiagonalisation (eig2.cu)
 
 def _tridiag(z, stages):
