@@ -1,16 +1,17 @@
-"""Row sharding of the Newton-CG matvec across GPUs (BASELINE config 4, ℓ = 8192).
+"""Sharding of the Newton-CG matvec across GPUs (BASELINE config 4, ℓ = 8192).
 
 SURVEY.md §8(e).  The reference's middle operator (newton.py:70-95,
-psdcone.py:113-121) applied through B = R·P is a sum over the rows i of B:
+psdcone.py:113-121) applied through B = R·P in the split H form:
 
-    T̃ = W∘(B_αᵀ diag(v) B) = Σ_g W∘(B_{g,α}ᵀ diag(v_g) B_g)
-    y_i = Σ_a (B T̃ᵀ)_ia B_ia
+    Φ(𝒯[Φ*(v)])_i = (H v)_i/μ + 2 Σ_{a∈s, b∈s̄} B_ia B_ib ξ_ab C_ab,   C = B_sᵀ diag(v) B_s̄
 
-so rank g keeps the row block [g·⌈ℓ/N⌉, (g+1)·⌈ℓ/N⌉) of B, computes its
-partial T̃ (one DMMA GEMM), the partials are summed with one NCCL all-reduce
-(k·ℓ doubles) and each rank forms its own y rows, all-gathered (ℓ doubles).
-Everything else (eigensolve, Φ, EG, CG vectors) stays replicated, so every
-rank takes identical control decisions and returns identical results.
+Rank g takes a column range of the mixed-sign block (both DMMA GEMMs) and its two folded
+row blocks (g and 2N−1−g of 2N) of the H / Q GEMVs; the partial y vectors are summed with
+one all-reduce of ℓ doubles per matvec.  Once per Newton step every rank forms its folded
+row blocks of B = R·P (equal shares of R's triangle) and two all-gathers complete B.
+Everything else (eigensolve, Φ, EG, CG vectors) stays replicated, so every rank takes
+identical control decisions and returns identical results.  ``row_block`` / ``shard_info``
+report the contiguous block of the legacy "blocked" form (``kot_middle_operator(form=2)``).
 
 The NCCL communicator is created by the library itself from an ncclUniqueId
 that rank 0 draws and ``torch.distributed`` broadcasts (any process group,
