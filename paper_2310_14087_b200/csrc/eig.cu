@@ -979,6 +979,26 @@ static int mid_mode() {
   }
   return g_mid_mode.load();
 }
+// the mid kernel needs one resident 512-thread CTA with the maximum shared memory per SM: if the
+// device or its configuration cannot provide that, the panel + tail path is used
+static bool mid_supported() {
+  static const bool ok = [] {
+    int dev = 0, sms = 0, per_sm = 0, coop = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    if (sms < kNumSMs || !coop) return false;
+    if (cudaFuncSetAttribute((const void*)sytrd_mid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sytrd_mid_kernel, MID_THREADS, 200 * 1024) !=
+            cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return per_sm >= 1;
+  }();
+  return ok;
+}
 static size_t mid_smem_max() {
   static const size_t v = [] {
     int dev = 0, optin = 0;
@@ -1004,7 +1024,7 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane,
   // (lane 0, not a background chain) whose grid's shared memory holds clearly more than the tail's 640
   int cm = n, mid_cols = 0, Gm = 0;
   const int mode = mid_mode();
-  if (mode > 0 && n >= 3 && ((lane == 0 && !background_thread()) || mode >= 2)) {
+  if (mode > 0 && n >= 3 && ((lane == 0 && !background_thread()) || mode >= 2) && mid_supported()) {
     // beside an EG pipeline the mid kernel takes KOT_TRD_MID_GRID whole SMs (default 96) and the
     // background chains keep the others; alone, every SM
     static const int mid_grid_shared = env_int("KOT_TRD_MID_GRID", 96);
