@@ -186,7 +186,7 @@ __device__ __forceinline__ void mid_update_pass(double* Aloc, int ld, int q0, in
 
 // Segment timers / per-warp clock stamps (kot_debug_mid_timing, kot_debug_mid_trace) are compiled in
 // only with -DKOT_MID_TRACE: the column loop has to stay inside the SM's instruction cache (≈ 32 KB
-// measured, tools/microbench/icache_bench_gen.cu — past it a lone warp runs at 17 cycles per
+// measured, tools/microbench/icache_bench_gen.py — past it a lone warp runs at 17 cycles per
 // instruction), and single-warp sections pay every instruction-fetch miss in full.
 #ifdef KOT_MID_TRACE
 #define MID_TR(k)                                                                                       \
