@@ -375,7 +375,7 @@ def run_gpu(args):
 
     # ---------------- config-5 batch (BASELINE metric, third half): every rank takes part
     batch_res = None
-    if not args.no_batch and not rowshard:
+    if not args.no_batch and not rowshard and args.config == "cfg3":  # part of the default (headline) run
         batch_res, _, _ = batch_leg(world, rank, local, args.batch, args.tol, args.max_iter, "tight",
                                     args.concurrency)
 
@@ -394,7 +394,7 @@ def run_gpu(args):
 
     # ---------------- time-to-tolerance at the headline config (BASELINE metric, first half)
     ttt = None
-    if world == 1 and not args.no_ttt:
+    if world == 1 and not args.no_ttt and args.config == "cfg3":  # the headline config (minutes at cfg4)
         ttt = time_to_tol(K, configs, wl, args.ttt_max_iter)
 
     line = {
