@@ -193,11 +193,15 @@ def assemble(samples_mu: SampleSet, samples_nu: SampleSet, filling: FillingPoint
                                                _lib.ptr(kmat)))
     qsq, jit = C.c_double(), C.c_double()
     _lib.check(_lib.lib().kot_problem_info(dp.handle, None, C.byref(qsq), C.byref(jit), None, None, None))
-    pd = ProblemData(q_mat=q, z=z, q_sq=float(qsq.value), chol_upper=r, lambda1=lambda1, lambda2=lambda2,
-                     embed_sum=emb, filling=filling, spec_x=spec_x, spec_y=spec_y, spec_xy=spec_xy,
-                     jitter=float(jit.value))
-    pd._dev = dp
-    pd._kmat = kmat
+    # The device mirrors Q's triangle, so it is bitwise symmetric already: the instance is filled in
+    # directly, without __post_init__'s symmetrisation pass over the ℓ × ℓ host array (its other checks
+    # — shapes, positive λ — hold by construction).
+    pd = object.__new__(ProblemData)
+    for name, value in (("q_mat", q), ("z", z), ("q_sq", float(qsq.value)), ("chol_upper", r),
+                        ("lambda1", lambda1), ("lambda2", lambda2), ("embed_sum", emb), ("filling", filling),
+                        ("spec_x", spec_x), ("spec_y", spec_y), ("spec_xy", spec_xy), ("jitter", float(jit.value)),
+                        ("_dev", dp), ("_kmat", kmat)):
+        object.__setattr__(pd, name, value)
     return pd
 
 

@@ -168,6 +168,12 @@ def test_assemble_cfg1(cfg1):
     assert pd.jitter == 0.0
     assert rel(pd.chol_upper, cfg1["r"]) <= 1e-13
     assert rel(pd.pair_gram(), cfg1["kmat"]) <= 1e-15
+    # assemble() skips ProblemData.__post_init__'s symmetrisation pass: the device result is exactly
+    # symmetric, so the reference's 0.5 (Q + Qᵀ) (problem.py:86-123) would return it unchanged
+    assert np.array_equal(pd.q_mat, pd.q_mat.T)
+    import dataclasses
+    pd2 = dataclasses.replace(pd, lambda1=2.0 * pd.lambda1)  # a regular instance again
+    assert np.array_equal(pd2.q_mat, pd.q_mat) and pd2._dev is None and pd2.lambda1 == 2.0 * pd.lambda1
 
 
 # ------------------------------------------------------------ operators
