@@ -178,6 +178,11 @@ int kot_debug_mid_timing(int on, unsigned long long* out8);    /* grid-resident 
 int kot_debug_trd_mid(int mode, int tail);
 /* clock64 stamps of the mid kernel, [8 columns from c0][16 warps][16 points] of CTA cta (on = 1 arms, 0 reads) */
 int kot_debug_mid_trace(int on, int c0, int cta, long long* out);
+/* host-only (no GPU): largest order of the mid kernel's resident block for `grid` CTAs with smem_max bytes
+ * of dynamic shared memory each; a self-test of the cooperative-grid gate (background panel loops that
+ * yield, a foreground thread opening exclusive windows): windows completed, or < 0 on a violation */
+int kot_debug_mid_capacity(int grid, long smem_max);
+int kot_debug_gate_selftest(int nbg, int ms);
 
 /* ---- operators (host buffers in/out; per-kernel parity) ----------------- */
 

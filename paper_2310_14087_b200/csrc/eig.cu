@@ -26,6 +26,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "gemm.cuh"
@@ -931,7 +932,7 @@ struct CoopGate {
   // (a gate is otherwise held for a whole tridiagonalisation, tens of milliseconds).
   void yield_to_exclusive(cudaStream_t st) {
     if (!g_coop_excl_hint.load(std::memory_order_relaxed)) return;
-    KOT_CUDA(cudaStreamSynchronize(st));
+    if (st) KOT_CUDA(cudaStreamSynchronize(st));  // (no stream: the host-only self-test)
     std::unique_lock<std::mutex> lk(g_coop_mu);
     if (!g_coop_excl) return;
     g_coop_used -= slots;
@@ -2365,4 +2366,67 @@ extern "C" int kot_debug_mid_trace(int on, int c0, int cta, long long* out) {
   } catch (const KotError& e) {
     return e.code;
   }
+}
+
+// ---- host-only hooks (no GPU needed): shared-memory capacity rule and a gate self-test ----
+
+// largest order of the mid kernel's resident block for a grid of G CTAs with smem_max bytes of dynamic
+// shared memory per CTA
+extern "C" int kot_debug_mid_capacity(int grid, long smem_max) {
+  if (grid < 1 || smem_max < 0) return -1;
+  return kot::mid_capacity(grid, (size_t)smem_max);
+}
+
+// Exercises the cooperative-grid gate for `ms` milliseconds with `nbg` background threads (panel loops
+// that yield between panels) and one foreground thread that opens exclusive windows.  Returns the
+// number of exclusive windows completed, or a negative code: −1 a background grid was in flight inside
+// a window before its re-opening, −2 the slot accounting did not return to zero, −3 no window opened.
+extern "C" int kot_debug_gate_selftest(int nbg, int ms) {
+  using namespace kot;
+  using clk = std::chrono::steady_clock;
+  const int total = 2 * kNumSMs;
+  std::atomic<bool> stop{false};
+  std::atomic<int> in_panel{0}, bad{0}, windows{0};
+  std::atomic<bool> window_closed{false};
+  std::vector<std::thread> th;
+  for (int t = 0; t < nbg; ++t)
+    th.emplace_back([&, t] {
+      while (!stop.load()) {
+        CoopGate g(total, t % 2 ? 16 : 24, 96, 1 + t % 2);
+        for (int p = 0; p < 40 && !stop.load(); ++p) {
+          g.yield_to_exclusive(nullptr);
+          ++in_panel;
+          if (window_closed.load()) ++bad;  // admitted while a window was closed
+          std::this_thread::sleep_for(std::chrono::microseconds(30));
+          --in_panel;
+        }
+      }
+    });
+  std::thread fg([&] {
+    while (!stop.load()) {
+      CoopGate g(total, 96, 96, 0);
+      std::this_thread::sleep_for(std::chrono::microseconds(200));  // its own panels
+      g.exclusive_begin();
+      // Background threads sample window_closed after their yield: give one that passed its yield
+      // point just before the window its 30 µs panel, then nobody may be inside.
+      window_closed = true;
+      std::this_thread::sleep_for(std::chrono::microseconds(100));
+      if (in_panel.load() != 0) ++bad;
+      window_closed = false;
+      g.exclusive_end(96, 2);
+      std::this_thread::sleep_for(std::chrono::microseconds(300));  // the resident kernel, others beside it
+      ++windows;
+    }
+  });
+  std::this_thread::sleep_for(std::chrono::milliseconds(ms));
+  stop = true;
+  fg.join();
+  for (auto& t : th) t.join();
+  (void)clk::now();
+  if (bad.load() != 0) return -1;
+  {
+    std::lock_guard<std::mutex> lk(g_coop_mu);
+    if (g_coop_used != 0 || g_coop_fg != 0 || g_coop_excl) return -2;
+  }
+  return windows.load() > 0 ? windows.load() : -3;
 }

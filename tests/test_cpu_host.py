@@ -42,6 +42,35 @@ def test_debug_hook_exported():
     assert hasattr(_lib.lib(), "kot_debug_sytrd_timing")
 
 
+def test_mid_kernel_capacity_rule():
+    """Order of the trailing block the grid-resident sytrd kernel keeps in shared memory: (rows + 4
+    vectors) × 8 B per CTA, at most 18 rows per CTA (csrc/sytrd_mid.cuh: mid_capacity; host-only hook)."""
+    from paper_2310_14087_b200 import _lib
+    f = _lib.lib().kot_debug_mid_capacity
+    smem = 228352  # 227 KB opt-in maximum minus the kernel's 4 KB of static shared memory
+    assert f(148, smem) == 1776 and f(96, smem) == 1440  # DESIGN.md §3: ℓ = 2000 alone / beside an EG pipeline
+    for g in (1, 16, 52, 96, 148):
+        m0 = f(g, smem)
+        rpc, ld = -(-m0 // g), m0 + (m0 & 1)
+        assert rpc <= 18 and (rpc + 4) * ld * 8 <= smem
+        m1 = m0 + 1  # one more column does not fit
+        rpc1, ld1 = -(-m1 // g), m1 + (m1 & 1)
+        assert rpc1 > 18 or (rpc1 + 4) * ld1 * 8 > smem or m1 > 2048
+    assert [f(g, smem) for g in (16, 24, 52, 96, 148)] == sorted(f(g, smem) for g in (16, 24, 52, 96, 148))
+    assert f(148, 0) == 0 and f(0, smem) == -1
+
+
+@pytest.mark.timeout(120)
+def test_cooperative_gate_exclusive_windows():
+    """The gate that admits cooperative eigensolver grids (csrc/eig.cu: CoopGate), host logic only: three
+    background panel loops that yield between panels and one foreground thread opening exclusive
+    windows (the mid kernel's launch protocol).  No background panel may be in flight inside a window,
+    nobody deadlocks, and the slot accounting returns to zero."""
+    from paper_2310_14087_b200 import _lib
+    windows = _lib.lib().kot_debug_gate_selftest(3, 400)
+    assert windows > 10, windows
+
+
 def test_ctypes_struct_layouts_match_c(tmp_path):
     """Compile a probe against include/kotgpu.h with gcc and compare sizes/offsets with ctypes."""
     import ctypes as C
