@@ -170,6 +170,43 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// dlarfg scalars from α and Σx² (the part of the column below α): β = −sign(α)‖(α, x)‖,
+// τ = (β − α)/β = 1 + |α|/‖·‖, 1/(α − β) = sign(α)/(|α| + ‖·‖).  Far from over/underflow the norm comes
+// straight from the sum of squares with hardware rsqrt / reciprocal seeds and Newton steps — a short
+// dependent chain (FP64 sqrt, hypot and two divisions cost ≈ 1 µs when a whole CTA waits for one
+// thread, or when every thread runs them); dlapy2 otherwise.  Results within an ulp or two of dlarfg's.
+__device__ __forceinline__ void dlarfg_scalars(double alpha, double xn2, double& beta, double& tau, double& scale) {
+  if (xn2 == 0.0) {  // H = I
+    tau = 0.0;
+    beta = alpha;
+    scale = 1.0;
+    return;
+  }
+  const double s2 = fma(alpha, alpha, xn2), aa = fabs(alpha);
+  double nrm, rn, rd;
+  if (s2 > 1e-280 && s2 < 1e280) {
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rn) : "d"(s2));
+    const double hs = 0.5 * s2;
+    rn = rn * fma(-hs * rn, rn, 1.5);
+    rn = rn * fma(-hs * rn, rn, 1.5);
+    nrm = s2 * rn;
+    nrm = fma(0.5 * rn, fma(-nrm, nrm, s2), nrm);
+    rn = fma(rn, fma(-nrm, rn, 1.0), rn);
+    const double dsum = aa + nrm;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(dsum));
+    rd = fma(rd, fma(-dsum, rd, 1.0), rd);
+    rd = fma(rd, fma(-dsum, rd, 1.0), rd);
+    rd = fma(rd, fma(-dsum, rd, 1.0), rd);
+  } else {
+    nrm = hypot(alpha, sqrt(xn2));
+    rn = 1.0 / nrm;
+    rd = 1.0 / (aa + nrm);
+  }
+  beta = -copysign(nrm, alpha);
+  tau = fma(aa, rn, 1.0);
+  scale = copysign(rd, alpha);
+}
+
 // One cooperative launch per NB=32 panel.  Each warp owns up to TRD_RPW rows
 // (r ≡ global-warp-id mod #warps, r ≥ p0); their V/W panel rows and the panel
 // columns of A live in shared memory for the whole panel, the symv results in
@@ -356,15 +393,7 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) sytrd_panel_kernel(TrdArgs a) 
       if (lane == 0) {
         const double xn2 = s;
         double beta, tau, scale;
-        if (xn2 == 0.0) {  // dlarfg: H = I
-          tau = 0.0;
-          beta = alpha;
-          scale = 1.0;
-        } else {
-          beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
-          tau = (beta - alpha) / beta;
-          scale = 1.0 / (alpha - beta);
-        }
+        dlarfg_scalars(alpha, xn2, beta, tau, scale);
         scal_sh[0] = tau;
         scal_sh[1] = scale;
         if (blockIdx.x == 0) {
@@ -711,15 +740,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) sytrd_tail_kernel(TailArgs a)
     __syncthreads();
     const double xn2 = scal[0];
     double beta, tau, scale;
-    if (xn2 == 0.0) {  // dlarfg: H = I
-      tau = 0.0;
-      beta = alpha;
-      scale = 1.0;
-    } else {
-      beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
-      tau = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
-    }
+    dlarfg_scalars(alpha, xn2, beta, tau, scale);  // every thread, identically
     if (g == 0 && tid == 0) {
       a.e[c0 + c] = beta;
       a.tau[c0 + c] = tau;
@@ -1109,8 +1130,7 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane,
     const size_t smem = sizeof(double) * ((size_t)rpc * ld + 4L * ld);
     ensure_smem_attr((const void*)sytrd_mid_kernel, (int)mid_smem_max());  // static + dynamic may pass 48 KB below it
     w.ensure_mid();
-    w.mid_seq = (w.mid_seq + 1) & 0xfffffu;
-    if (w.mid_seq == 0) w.mid_seq = 1;
+    ++w.mid_seq;  // 64-bit launch epoch: a tag never repeats within a buffer's lifetime
     MidArgs ma{w.A, n, cm, mid_cols, w.d, w.e, w.tau, w.Vall, static_cast<MidSector*>(w.mid_x),
                g_mid_rep.load(), w.mid_seq << 12, w.mid_err, w.mid_resident, g_mid_dbg, g_mid_trace, g_mid_trace_c0,
                g_mid_trace_cta};
@@ -1144,7 +1164,7 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane,
     if (shared_gpu) {
       // every CTA is resident once CTA 0 has completed the first exchange
       const auto t0 = std::chrono::steady_clock::now();
-      while (*reinterpret_cast<volatile unsigned*>(w.mid_resident) != ma.epoch0) {
+      while (*reinterpret_cast<volatile unsigned*>(w.mid_resident) != (unsigned)ma.epoch0) {
         if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(4)) break;  // the kernel's own timeout reports
       }
       prof_host("host.mid_resident", std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());

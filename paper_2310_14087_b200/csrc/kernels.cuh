@@ -49,7 +49,7 @@ struct EigWork {
   void* mid_x = nullptr;
   int *mid_err = nullptr, *mid_err_host = nullptr;
   unsigned* mid_resident = nullptr;  // host-mapped: the kernel's epoch once every CTA is resident
-  unsigned mid_seq = 0;
+  unsigned long long mid_seq = 0;
   bool mid_used = false;
   void ensure_mid();
   cudaEvent_t ev_panel[8] = {};  // panel-loop throttle of the background chains

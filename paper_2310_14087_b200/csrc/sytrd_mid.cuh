@@ -59,7 +59,7 @@ struct MidArgs {
   double* Vall;      // reflector c (global index) in column c, rows > c; v_{c+1} = 1
   MidSector* xchg;   // [2 parities][nrep][G][MID_SPC] tagged sectors
   int nrep;
-  unsigned epoch0;
+  unsigned long long epoch0;  // launch sequence number << 12: tags = epoch0 + column + 2
   int* err;                 // set to 1 when a gather timed out
   unsigned* resident;       // host-mapped: CTA 0 stores epoch0 after its first gather (every CTA is resident)
   unsigned long long* dbg;  // nullable: per-segment ns accumulated by CTA 0 thread 0
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(MID_THREADS, 1) sytrd_mid_kernel(MidArgs a) {
     double* wn = vn + ld;
     double* vq = vwbuf + (par ^ 1) * 2L * ld;  // column c−1's v and w (update in flight), then column c+1's x̃
     const double* wp = vq + ld;
-    const unsigned long long tag = (unsigned long long)a.epoch0 + (unsigned)(c + 2);
+    const unsigned long long tag = a.epoch0 + (unsigned)(c + 2);
     MidSector* xb = a.xchg + (long)par * a.nrep * G * MID_SPC;
     const bool pend = c >= 1;  // the rows still lack column c−1's rank-2 update
     MID_TR(0)
@@ -327,37 +327,7 @@ __global__ void __launch_bounds__(MID_THREADS, 1) sytrd_mid_kernel(MidArgs a) {
         if (lane == 0) {
           const double alpha = vn[c + 1];
           double beta, tn, scale;
-          if (xn2 == 0.0) {  // dlarfg: H = I
-            tn = 0.0;
-            beta = alpha;
-            scale = 1.0;
-          } else {
-            const double s2 = fma(alpha, alpha, xn2), aa = fabs(alpha);
-            double nrm, rn;
-            double rd;
-            if (s2 > 1e-280 && s2 < 1e280) {  // far from over/underflow: straight from the sum of squares,
-              // hardware seeds + Newton steps (a short dependent chain; results within an ulp or two)
-              asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rn) : "d"(s2));
-              const double hs = 0.5 * s2;
-              rn = rn * fma(-hs * rn, rn, 1.5);
-              rn = rn * fma(-hs * rn, rn, 1.5);
-              nrm = s2 * rn;
-              nrm = fma(0.5 * rn, fma(-nrm, nrm, s2), nrm);
-              rn = fma(rn, fma(-nrm, rn, 1.0), rn);
-              const double dsum = aa + nrm;
-              asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(dsum));
-              rd = fma(rd, fma(-dsum, rd, 1.0), rd);
-              rd = fma(rd, fma(-dsum, rd, 1.0), rd);
-              rd = fma(rd, fma(-dsum, rd, 1.0), rd);
-            } else {  // dlapy2
-              nrm = hypot(alpha, sqrt(xn2));
-              rn = 1.0 / nrm;
-              rd = 1.0 / (aa + nrm);
-            }
-            beta = -copysign(nrm, alpha);
-            tn = fma(aa, rn, 1.0);
-            scale = copysign(rd, alpha);
-          }
+          dlarfg_scalars(alpha, xn2, beta, tn, scale);
           scal[0] = tn;
           scal[1] = scale;
           scal[2] = beta;
@@ -464,7 +434,7 @@ __global__ void __launch_bounds__(MID_THREADS, 1) sytrd_mid_kernel(MidArgs a) {
     MID_TR(5)
     __syncthreads();
     if (c == -1 && g == 0 && tid == 0) {  // every producer has published: the whole grid is resident
-      *reinterpret_cast<volatile unsigned*>(a.resident) = a.epoch0;
+      *reinterpret_cast<volatile unsigned*>(a.resident) = (unsigned)a.epoch0;
       __threadfence_system();
     }
     // (5) w = τ y + α₂ v (α₂ = −½ τ² yᵀv) finishes column c; x̃_{c+1} = p − κ v, κ = τ y_{c+1} + 2 α₂.
