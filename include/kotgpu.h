@@ -176,6 +176,9 @@ int kot_debug_mid_timing(int on, unsigned long long* out8);    /* grid-resident 
 /* grid-resident sytrd mid kernel: mode 0 off, 1 latency-critical eigensolves (default), 2 every eigensolve;
  * tail = trailing columns handed to the cluster tail (0: none); a negative value leaves a setting unchanged */
 int kot_debug_trd_mid(int mode, int tail);
+/* the mid kernel's head launch (the columns only every SM together can hold, before the launch that leaves
+ * SMs to the other chains): 0 off, 1 beside an EG pipeline (default), 2 also for standalone eigensolves */
+int kot_debug_trd_mid_head(int mode);
 /* clock64 stamps of the mid kernel, [8 columns from c0][16 warps][16 points] of CTA cta (on = 1 arms, 0 reads) */
 int kot_debug_mid_trace(int on, int c0, int cta, long long* out);
 /* host-only (no GPU): largest order of the mid kernel's resident block for `grid` CTAs with smem_max bytes

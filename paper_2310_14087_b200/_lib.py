@@ -92,6 +92,7 @@ _SIGS = {
     "kot_debug_tail_timing": (C.c_int, [C.c_int, C.POINTER(C.c_ulonglong)]),
     "kot_debug_mid_timing": (C.c_int, [C.c_int, C.POINTER(C.c_ulonglong)]),
     "kot_debug_trd_mid": (C.c_int, [C.c_int, C.c_int]),
+    "kot_debug_trd_mid_head": (C.c_int, [C.c_int]),
     "kot_debug_mid_trace": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_longlong)]),
     "kot_debug_mid_capacity": (C.c_int, [C.c_int, C.c_long]),
     "kot_debug_gate_selftest": (C.c_int, [C.c_int, C.c_int]),

@@ -989,6 +989,7 @@ struct CoopGate {
 // every eigensolve (tests); KOT_TRD_MID_TAIL = trailing columns handed to the cluster tail (0: none).
 static std::atomic<int> g_mid_mode{-1};
 static std::atomic<int> g_mid_tail{-1};
+static std::atomic<int> g_mid_head{-1};  // head launch on every SM beside an EG pipeline (KOT_TRD_MID_HEAD)
 static std::atomic<int> g_mid_rep{1};  // replicas of the exchange sectors (KOT_TRD_MID_REP)
 static int mid_mode() {
   if (g_mid_mode.load() < 0) {
@@ -1045,13 +1046,19 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane,
   // columns [cm, cm + mid_cols) go to the grid-resident mid kernel: a latency-critical eigensolve
   // (lane 0, not a background chain) whose grid's shared memory holds clearly more than the tail's 640
   int cm = n, mid_cols = 0, Gm = 0;
+  int ch = n, Gh = 0;  // head launch: columns [ch, cm) on Gh CTAs (ch = cm: none)
   const int mode = mid_mode();
   if (mode > 0 && n >= 3 && ((lane == 0 && !background_thread()) || mode >= 2) && mid_supported()) {
     // beside an EG pipeline the mid kernel takes KOT_TRD_MID_GRID whole SMs (default 96) and the
     // background chains keep the others; alone, every SM
     static const int mid_grid_shared = env_int("KOT_TRD_MID_GRID", 96);
-    Gm = std::min(g_pipelines.load() > 0 && lane == 0 ? std::min(mid_grid_shared, trd_grid_cap_all()) : trd_grid_cap(lane),
-                  kNumSMs);
+    if (g_mid_head.load() < 0) {
+      const char* e = std::getenv("KOT_TRD_MID_HEAD");
+      g_mid_head = e ? std::min(std::max(std::atoi(e), 0), 2) : 1;
+    }
+    // (2: the solver's two-launch schedule also for standalone eigensolves — tests)
+    const bool shared_like = (g_pipelines.load() > 0 || g_mid_head.load() == 2) && lane == 0 && !background_thread();
+    Gm = std::min(shared_like ? std::min(mid_grid_shared, trd_grid_cap_all()) : trd_grid_cap(lane), kNumSMs);
     const int cap = mid_capacity(Gm, mid_smem_max());
     if (cap >= TAIL_MAX + 256 && (n > TAIL_MAX || mode >= 2)) {
       cm = n <= cap ? 0 : ceil_div(n - cap, TRD_NB) * TRD_NB;
@@ -1059,12 +1066,25 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane,
       const int keep = use_tail ? std::min(g_mid_tail.load(), TAIL_MAX) : 0;  // columns left to the tail
       mid_cols = keep >= 2 && m0 - keep >= 1 ? m0 - keep : m0 - 1;
       c0 = mid_cols == m0 - 1 ? n : cm + mid_cols;
+      // Beside an EG pipeline the columns between what every SM could hold and what Gm SMs hold (224 … 560
+      // at ℓ = 2000) would go to the panel kernel at ≈ 19 µs per column: a *head* launch on every SM takes
+      // them instead (the background chains wait ≈ 1.6 ms longer at the gate) and hands its block over.
+      if (g_mid_head.load() >= 1 && shared_like) {
+        const int Gall = std::min(trd_grid_cap_all(), kNumSMs);
+        const int caph = mid_capacity(Gall, mid_smem_max());
+        if (Gall > Gm && caph >= cap + 2 * TRD_NB && n > cap) {
+          ch = n <= caph ? 0 : ceil_div(n - caph, TRD_NB) * TRD_NB;
+          Gh = Gall;
+          if (cm - ch < 2) ch = cm;  // nothing worth a launch
+        }
+      }
     }
   }
+  if (ch > cm) ch = cm;
   const bool throttle = gate != nullptr && (lane != 0 || background_thread()) && mode > 0 && g_pipelines.load() > 0;
   static const int depth = std::min(env_int("KOT_TRD_THROTTLE", 2), 8);  // panels enqueued ahead of the GPU
   if (throttle) w.ensure_panel_events();
-  for (int p0 = 0; p0 < std::min(std::min(c0, cm), n - 1); p0 += TRD_NB) {
+  for (int p0 = 0; p0 < std::min(std::min(c0, ch), n - 1); p0 += TRD_NB) {
     const int nb = std::min(TRD_NB, n - 1 - p0);
     w.check_cancel(st);
     if (gate) {
@@ -1125,27 +1145,34 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane,
     if (throttle) KOT_CUDA(cudaEventRecord(w.ev_panel[(p0 / TRD_NB) % depth], st));
   }
   if (mid_cols > 0) {
-    const int m0 = n - cm;
-    const int rpc = ceil_div(m0, Gm), ld = m0 + (m0 & 1);
-    const size_t smem = sizeof(double) * ((size_t)rpc * ld + 4L * ld);
     ensure_smem_attr((const void*)sytrd_mid_kernel, (int)mid_smem_max());  // static + dynamic may pass 48 KB below it
     w.ensure_mid();
-    ++w.mid_seq;  // 64-bit launch epoch: a tag never repeats within a buffer's lifetime
-    MidArgs ma{w.A, n, cm, mid_cols, w.d, w.e, w.tau, w.Vall, static_cast<MidSector*>(w.mid_x),
-               g_mid_rep.load(), w.mid_seq << 12, w.mid_err, w.mid_resident, g_mid_dbg, g_mid_trace, g_mid_trace_c0,
-               g_mid_trace_cta};
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(Gm);
-    cfg.blockDim = dim3(MID_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;  // co-residency: the CTAs spin on each other's slots
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    double bytes = 0.0;
-    for (int c = cm; c < cm + mid_cols; ++c) bytes += 8.0 * 0.5 * (double)(n - c - 1) * (n - c);
+    // columns [cs, cs + cols) of the block starting at cs on G CTAs; returns the launch epoch
+    auto launch_mid = [&](int G, int cs, int cols) {
+      const int m0 = n - cs;
+      const int rpc = ceil_div(m0, G), ld = m0 + (m0 & 1);
+      const size_t smem = sizeof(double) * ((size_t)rpc * ld + 4L * ld);
+      ++w.mid_seq;  // 64-bit launch epoch: a tag never repeats within a buffer's lifetime
+      MidArgs ma{w.A, n, cs, cols, w.d, w.e, w.tau, w.Vall, static_cast<MidSector*>(w.mid_x),
+                 g_mid_rep.load(), w.mid_seq << 12, w.mid_err, w.mid_resident, g_mid_dbg, g_mid_trace,
+                 g_mid_trace_c0, g_mid_trace_cta};
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(MID_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;  // co-residency: the CTAs spin on each other's slots
+      at[0].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      double bytes = 0.0;
+      for (int c = cs; c < cs + cols; ++c) bytes += 8.0 * 0.5 * (double)(n - c - 1) * (n - c);
+      ProfScope ps("sytrd_mid", st, 0.0, bytes);
+      KOT_CUDA(cudaLaunchKernelEx(&cfg, sytrd_mid_kernel, ma));
+      KOT_LAUNCH_CHECK();
+      return ma.epoch0;
+    };
     // other cooperative grids may be in flight (EG pipeline, concurrent solves): launch exclusively
     const bool shared_gpu = gate != nullptr && (g_pipelines.load() > 0 || lane != 0 || background_thread());
     const auto tx0 = std::chrono::steady_clock::now();
@@ -1156,15 +1183,12 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane,
       prof_host("host.mid_sync", std::chrono::duration<double, std::milli>(tx1 - tx0).count());
       prof_host("host.mid_excl", std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tx1).count());
     }
-    {
-      ProfScope ps("sytrd_mid", st, 0.0, bytes);
-      KOT_CUDA(cudaLaunchKernelEx(&cfg, sytrd_mid_kernel, ma));
-      KOT_LAUNCH_CHECK();
-    }
+    if (ch < cm) launch_mid(Gh, ch, cm - ch);  // head: every SM, hands the block from column cm on back
+    const unsigned long long epoch = launch_mid(Gm, cm, mid_cols);
     if (shared_gpu) {
       // every CTA is resident once CTA 0 has completed the first exchange
       const auto t0 = std::chrono::steady_clock::now();
-      while (*reinterpret_cast<volatile unsigned*>(w.mid_resident) != (unsigned)ma.epoch0) {
+      while (*reinterpret_cast<volatile unsigned*>(w.mid_resident) != (unsigned)epoch) {
         if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(4)) break;  // the kernel's own timeout reports
       }
       prof_host("host.mid_resident", std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
@@ -2449,4 +2473,10 @@ extern "C" int kot_debug_gate_selftest(int nbg, int ms) {
     if (g_coop_used != 0 || g_coop_fg != 0 || g_coop_excl) return -2;
   }
   return windows.load() > 0 ? windows.load() : -3;
+}
+
+// test hook: 0 no head launch, 1 beside an EG pipeline (default), 2 also for standalone eigensolves
+extern "C" int kot_debug_trd_mid_head(int mode) {
+  kot::g_mid_head = (mode >= 0 && mode <= 2) ? mode : 1;
+  return 0;
 }

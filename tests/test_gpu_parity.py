@@ -684,6 +684,21 @@ def test_mid_kernel_large_orders(mid_everywhere, n):
     _check_decomposition(0.5 * (z + z.T))
 
 
+@pytest.mark.parametrize("n", [1500, 2000, 2300])
+def test_mid_kernel_head_launch(mid_everywhere, n):
+    """The solver's schedule beside an EG pipeline, forced for a standalone eigensolve: panels, a head
+    launch on every SM that hands its block over, then the launch on 96 SMs."""
+    from paper_2310_14087_b200 import _lib
+    mid_everywhere(1, 0)
+    head = _lib.lib().kot_debug_trd_mid_head
+    head(2)
+    try:
+        rng = np.random.default_rng(n + 1)
+        _check_decomposition(random_symmetric(rng, n))
+    finally:
+        head(1)
+
+
 def test_mid_kernel_identity_reflectors(mid_everywhere):
     """Columns with H = I (τ = 0): a diagonal matrix, and a block matrix mixing both kinds of column."""
     mid_everywhere(2, 0)
