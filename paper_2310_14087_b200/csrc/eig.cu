@@ -882,10 +882,12 @@ static int trd_grid_cap(int lane) {
   // Round 2, with the TMA GEMM core: thinner EG-chain grids leave CTA slots (registers) to the Newton
   // chain's CG GEMMs, whose CTAs co-reside with panel CTAs on the same SMs (cfg3: 48/32 → 24/16
   // CTAs: Newton direction 42.1 → 38.5 ms, 13.9 → 14.6 it/s; the EG chain, 51 → 56 ms, keeps slack).
-  static const int bg = env_int("KOT_TRD_GRID_BG", 24);
+  // With the mid kernel on the Newton chain the EG chain became the longer one: 32 / 32 (cfg3 16.55–16.65
+  // it/s, tight profile 15.25) against 24 / 16 (16.26–16.33, 15.15), 48 / 16 (16.6, 15.0), 48 / 32 (16.5, 15.1).
+  static const int bg = env_int("KOT_TRD_GRID_BG", 32);
   const int cap_bg = std::min(bg, cap);
   // lane 2 = the EG pipeline's residual thread, lane 1 = its EG-step threads
-  static const int bg2 = env_int("KOT_TRD_GRID_BG2", 16);
+  static const int bg2 = env_int("KOT_TRD_GRID_BG2", 32);
   const int cap_bg2 = std::min(bg2, cap);
   if (lane == 0) return g_pipelines.load() > 0 ? cap_fg : cap;
   return lane == 2 ? cap_bg2 : cap_bg;
