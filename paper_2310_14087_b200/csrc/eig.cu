@@ -14,7 +14,7 @@
 //      Gu–Eisenstat recomputation of z for orthogonal eigenvectors, and the
 //      eigenvector update as a DMMA GEMM with a column-scatter epilogue.
 //   3. ormtr  — back-transform P = Q_H·Q_T with compact-WY blocks
-//      (I − V T Vᵀ), three DMMA GEMMs per panel.
+//      (I − V T Vᵀ), two DMMA GEMMs per block (V·T formed beside the D&C).
 //   4. descending order + k = #(σ > 0)  (strict, zero → ᾱ, linalg.py:74-83).
 // Consumers (proj, 𝒯, M) are basis-invariant, so eigenvector signs and the
 // basis inside clusters may differ from LAPACK.
@@ -108,6 +108,7 @@ void EigWork::ensure_tfactors() {
   const int nblk = std::max(1, (n - 1 + 127) / 128);
   Tall = static_cast<double*>(dev_alloc(sizeof(double) * 128L * 128 * nblk));
   Sside = static_cast<double*>(dev_alloc(sizeof(double) * 128L * 128));
+  VT = static_cast<double*>(dev_alloc(sizeof(double) * (long)n * n));
   ws_t = static_cast<double*>(dev_alloc(sizeof(double) * 16L * 128 * 128));
   int lo = 0, hi = 0;
   KOT_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -132,7 +133,7 @@ EigWork::~EigWork() {
     if (e) cudaEventDestroy(e);
   if (ev_t0) cudaEventDestroy(ev_t0);
   if (ev_t1) cudaEventDestroy(ev_t1);
-  for (double* q : {Tall, Sside, ws_t}) dev_free(q);
+  for (double* q : {Tall, Sside, ws_t, VT}) dev_free(q);
   if (ev_w) cudaEventDestroy(ev_w);
   if (ev_rest) cudaEventDestroy(ev_rest);
   dev_free(gcnt);
@@ -2191,6 +2192,11 @@ static void tfactors_async(int n, EigWork& w, cudaStream_t st) {
     larft_kernel<<<ceil_div(nb, LARFT_THREADS / 32), LARFT_THREADS, LARFT_SMEM, w.st_t>>>(
         w.Sside, w.tau + p0, nb, w.Tall + (long)bi * ORM_NB * ORM_NB);
     KOT_LAUNCH_CHECK();
+    // VT = V·T (T upper triangular, zero below the diagonal): the back-transform then needs two GEMMs
+    // per block, P −= (V T)(Vᵀ P), instead of three
+    double* VTp = w.VT + (long)r0 * n + p0;
+    gemm_launch<false, false>(make_shape(n - r0, nb, nb, Vp, n, w.Tall + (long)bi * ORM_NB * ORM_NB, nb),
+                              EpiAxpby{VTp, n, 1.0, 0.0}, w.st_t);
   }
   KOT_CUDA(cudaEventRecord(w.ev_t1, w.st_t));
 }
@@ -2199,15 +2205,14 @@ static void ormtr(int n, EigWork& w, double* P, cudaStream_t st, const int* dcol
   const int nref = n - 1;  // reflectors 0..n-2
   const int nblk = (nref + ORM_NB - 1) / ORM_NB;
   double* W1 = w.W1;
-  double* W2 = w.W1 + (long)ORM_NB * n;
-  KOT_CUDA(cudaStreamWaitEvent(st, w.ev_t1, 0));  // T factors (tfactors_async)
+  KOT_CUDA(cudaStreamWaitEvent(st, w.ev_t1, 0));  // T factors and V·T (tfactors_async)
   for (int bi = nblk - 1; bi >= 0; --bi) {
     const int p0 = bi * ORM_NB;
     const int nb = std::min(ORM_NB, nref - p0);
     const int r0 = p0 + 1;
     const int mrows = n - r0;
     const double* Vp = w.Vall + (long)r0 * n + p0;  // mrows × nb (ld n), zero above each unit entry
-    const double* T = w.Tall + (long)bi * ORM_NB * ORM_NB;
+    const double* VTp = w.VT + (long)r0 * n + p0;   // V·T of the block (tfactors_async)
     {  // W1 = Vᵀ P[r0:, :]
       GemmShape s = make_shape(nb, n, mrows, Vp, n, P + (long)r0 * n, n);
       s.dN = dcols;
@@ -2215,14 +2220,8 @@ static void ormtr(int n, EigWork& w, double* P, cudaStream_t st, const int* dcol
       s.ksplit = choose_ksplit(s, w.splitws_cap);
       gemm_launch<true, false>(s, EpiAxpby{W1, n, 1.0, 0.0}, st);
     }
-    {  // W2 = T W1   (T upper triangular: K range starts at the row tile)
-      GemmShape s = make_shape(nb, n, nb, T, nb, W1, n);
-      s.dN = dcols;
-      s.kb_m = 1;
-      gemm_launch<false, false>(s, EpiAxpby{W2, n, 1.0, 0.0}, st);
-    }
-    {  // P[r0:, :] −= V W2
-      GemmShape s = make_shape(mrows, n, nb, Vp, n, W2, n);
+    {  // P[r0:, :] −= (V T) W1
+      GemmShape s = make_shape(mrows, n, nb, VTp, n, W1, n);
       s.dN = dcols;
       gemm_launch<false, false>(s, EpiAxpby{P + (long)r0 * n, n, -1.0, 1.0}, st);
     }

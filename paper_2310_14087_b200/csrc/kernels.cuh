@@ -41,7 +41,7 @@ struct EigWork {
   double *Vq2 = nullptr, *tq2 = nullptr, *Tq2 = nullptr;  // two-stage: stage-2 reflectors, τ, group T
   cudaStream_t st2 = nullptr;  // two-stage: look-ahead stream
   // back-transform T factors, computed on st_t beside the tridiagonal eigensolve (ormtr only waits)
-  double *Tall = nullptr, *Sside = nullptr, *ws_t = nullptr;
+  double *Tall = nullptr, *Sside = nullptr, *ws_t = nullptr, *VT = nullptr;  // VT = V·T per block (ormtr layout)
   cudaStream_t st_t = nullptr;
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
   void ensure_tfactors();
