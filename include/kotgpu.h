@@ -165,6 +165,12 @@ int kot_profile_read(kot_prof_entry* out, int cap);  /* returns #entries */
  * solves sharing one GPU (batches of independent problems) run faster on thin grids. */
 int kot_set_panel_grid_cap(int cap);
 
+/* Process set-up of a long-running service: grows the library's device memory pool by `bytes` once (the
+ * bytes go straight back to the pool, which never trims).  Without it the first solve of a process pays the
+ * driver's mapping of the pool (4 … 300 ms for the ≈ 3.5 GB of an l = 2000 problem, depending on what ran on
+ * the GPU before); every problem, workspace and context is still allocated by the calls that need them. */
+int kot_reserve(int device, unsigned long long bytes);
+
 /* ---- test / diagnostic hooks (process-wide; not part of the drop-in surface) ---- */
 int kot_debug_eig_stages(int stages);   /* 0 automatic, 1 one-stage, 2 two-stage, 3 two-stage in background */
 int kot_debug_cg_batch(int batch);      /* CG iterations enqueued per host check (>= 1; default 4) */

@@ -12,11 +12,12 @@ from paper_2310_14087_b200.problem import (FillingPoints, IteratePair, ProblemDa
                                            objective, ot_estimate)
 from paper_2310_14087_b200.solver import SolverConfig, SolverReport, solve, solve_pure_eg
 from paper_2310_14087_b200.datagen import MixtureSpec, sample_mixture, sobol_points
+from paper_2310_14087_b200._lib import reserve_device_memory  # extension: pool set-up of a service process
 
 __version__ = "0.1.0"
 
 __all__ = [
     "KernelSpec", "SampleSet", "FillingPoints", "IteratePair", "ProblemData", "assemble", "build_kernel_specs",
     "SolverConfig", "SolverReport", "solve", "solve_pure_eg", "NewtonConfig", "EgConfig", "objective",
-    "ot_estimate", "MixtureSpec", "sample_mixture", "sobol_points",
+    "ot_estimate", "MixtureSpec", "sample_mixture", "sobol_points", "reserve_device_memory",
 ]

@@ -88,6 +88,7 @@ _SIGS = {
     "kot_debug_eg_parallel": (C.c_int, [C.c_int]),
     "kot_debug_gemm_tma": (C.c_int, [C.c_int]),
     "kot_set_panel_grid_cap": (C.c_int, [C.c_int]),
+    "kot_reserve": (C.c_int, [C.c_int, C.c_ulonglong]),
     "kot_debug_sytrd_timing": (C.c_int, [C.c_int, C.POINTER(C.c_ulonglong)]),
     "kot_debug_tail_timing": (C.c_int, [C.c_int, C.POINTER(C.c_ulonglong)]),
     "kot_debug_mid_timing": (C.c_int, [C.c_int, C.POINTER(C.c_ulonglong)]),
@@ -224,6 +225,12 @@ def ptr(a: np.ndarray | None):
 
 def default_device() -> int:
     return int(os.environ.get("KOT_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+
+
+def reserve_device_memory(nbytes: int, device: int | None = None) -> None:
+    """Process set-up of a long-running service: grow the library's device memory pool by ``nbytes``
+    once (kot_reserve).  The first solve of a process otherwise pays the driver's mapping of the pool."""
+    check(lib().kot_reserve(default_device() if device is None else device, int(nbytes)))
 
 
 def launch_count() -> int:

@@ -137,6 +137,24 @@ void* dev_alloc(size_t bytes) {
   return p;
 }
 
+// Grows the device memory pool once (process set-up of a long-running service): `bytes` are allocated
+// from the library's pool and given back to it; the pool never trims (release threshold = max), so later
+// allocations find mapped memory.  Without it the first solve of a process pays the driver's mapping of
+// the pool — 4 to 300 ms for the ≈ 3.5 GB of an ℓ = 2000 problem, depending on what ran on the GPU before.
+void dev_reserve(size_t bytes) {
+  int dev = 0;
+  KOT_CUDA(cudaGetDevice(&dev));
+  cudaStream_t s;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    s = alloc_stream_locked(dev);
+  }
+  void* p = nullptr;
+  KOT_CUDA(cudaMallocAsync(&p, bytes > 0 ? bytes : 8, s));
+  KOT_CUDA(cudaFreeAsync(p, s));
+  KOT_CUDA(cudaStreamSynchronize(s));
+}
+
 void dev_free(void* p) {
   if (!p) return;
   int dev = 0;

@@ -60,6 +60,13 @@ const char* kot_last_error(void) { return g_last_error.c_str(); }
 
 long long kot_launch_count(void) { return kot::g_kot_launches.load(); }
 
+int kot_reserve(int device, unsigned long long bytes) {
+  return guarded([&] {
+    KOT_CUDA(cudaSetDevice(device));
+    kot::dev_reserve((size_t)bytes);
+  });
+}
+
 int kot_problem_create(const double* q, const double* z, double q_sq, const double* r_upper, const double* embed,
                        int l, double lambda1, double lambda2, double jitter, int device, kot_problem** out) {
   return guarded([&] {

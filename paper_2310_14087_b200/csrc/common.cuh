@@ -96,6 +96,7 @@ inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
 void* dev_alloc(size_t bytes);
 int canary_check_all(const char* where);  // KOT_CANARY=1: guard-byte check of every live allocation
 void dev_free(void* p);
+void dev_reserve(size_t bytes);  // grow the pool once (kot_reserve)
 void* host_alloc_pinned(size_t bytes);
 void host_free_pinned(void* p, size_t bytes);
 

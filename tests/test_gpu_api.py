@@ -227,3 +227,18 @@ def test_sobol_points_on_device(api):
     assert np.array_equal(np.vstack([s.take(7), s.take(13)]), api["sobol_nat"])
     with pytest.raises(ValueError):
         K.sobol_points(5, 10)
+
+
+def test_reserve_device_memory_grows_the_pool_once():
+    """kot_reserve: process set-up of a service; a second call of the same size is
+    served from the pool, and solves afterwards are unaffected."""
+    import time
+    import paper_2310_14087_b200 as K2
+    K2.reserve_device_memory(256 << 20)
+    t0 = time.perf_counter()
+    K2.reserve_device_memory(256 << 20)
+    assert time.perf_counter() - t0 < 0.5
+    with pytest.raises(Exception):
+        K2.reserve_device_memory(1 << 50)  # more than the device has: reported, not fatal
+    z = np.diag([2.0, -1.0, 0.5])
+    assert np.allclose(np.sort(GL.sym_eig(z).eigvals), [-1.0, 0.5, 2.0])
