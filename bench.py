@@ -541,8 +541,9 @@ def batch_leg(world: int, rank: int, local: int, n_problems: int, tol: float, ma
 
     # several solves share the GPU: thinner cooperative panel grids let their eigensolves run side by
     # side (16 problems x 100 iterations, cluster tail: 0.73 problems/s at 64 CTAs, 0.85 at 48, 0.89 at
-    # 32, 0.90 at 24; concurrency 4-12 equal)
-    _lib.lib().kot_set_panel_grid_cap(int(os.environ.get("KOT_BATCH_GRID", "32")))
+    # 32, 0.90 at 24; concurrency 4-12 equal).  Round 2, 160 members to tol 5e-3, two runs each: 2.68 problems/s
+    # at 16 CTAs, 2.74 at 20, 2.75-2.77 at 24, 2.61-2.62 at 32; concurrency 5 / 6 / 8 equal.
+    _lib.lib().kot_set_panel_grid_cap(int(os.environ.get("KOT_BATCH_GRID", "24")))
     seeds = list(range(n_problems))
     mine = batch.shard(seeds, world, rank)
     kw = dict(profile=profile, residual_tol=tol, max_iter=max_iter)
