@@ -1084,7 +1084,15 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane,
     }
   }
   if (ch > cm) ch = cm;
-  const bool throttle = gate != nullptr && (lane != 0 || background_thread()) && mode > 0 && g_pipelines.load() > 0;
+  // Under a batch's panel-grid cap (several solves share the GPU) every chain is throttled, the Newton
+  // chains included: short queues interleave the solves more evenly (config-5 batch 2.77 → 2.81 problems/s;
+  // without any throttle 2.70).  KOT_TRD_THROTTLE_ALL=0 restricts it to the background chains again.
+  static const bool throttle_all = [] {
+    const char* e = std::getenv("KOT_TRD_THROTTLE_ALL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const bool throttle = gate != nullptr && mode > 0 && g_pipelines.load() > 0 &&
+                        (lane != 0 || background_thread() || (throttle_all && trd_grid_cap_all() < kNumSMs));
   static const int depth = std::min(env_int("KOT_TRD_THROTTLE", 2), 8);  // panels enqueued ahead of the GPU
   if (throttle) w.ensure_panel_events();
   for (int p0 = 0; p0 < std::min(std::min(c0, ch), n - 1); p0 += TRD_NB) {
