@@ -17,8 +17,13 @@
 // bit-identical decisions.  The all-gather goes through TAGGED 32-byte sectors in global memory
 // ({3 doubles, tag}: one 256-bit store, one 256-bit load — the sector is L2's access granule, the
 // tag validates the payload, so a consumer polls the data itself; no grid barrier, no flag round
-// trip).  Every sector is written to R replicas and a CTA reads replica blockIdx mod R, otherwise
-// 148 SMs would poll the same cache lines of a few L2 slices.
+// trip).  A sector can be written to R replicas with a CTA reading replica blockIdx mod R
+// (KOT_TRD_MID_REP); measured, one copy is fastest — the exchange costs the all-to-all skew of 148
+// CTAs (≈ 2300–2800 cycles, tools/microbench/hop_bench.cu), not hot L2 lines — so R = 1 by default.
+//
+// The Householder scalars of a column stay off the critical path: the symv runs on the UNSCALED column
+// (Â v = s (Â x̃ − β Â[:, c+1]), s = 1/(α − β)) while warp 15 derives β, τ, s, and x̃ is scaled into v
+// while warp 0 publishes.  The column loop is kept small enough for the SM's instruction cache.
 //
 // The shared-memory copy runs ONE rank-2 update behind (dlatrd with a panel of one): column c's symv
 // is a read-only pass over the stale rows, corrected per row with the two dot products w_{c−1}·v_c
@@ -36,7 +41,6 @@ namespace kot {
 constexpr int MID_THREADS = 512;
 constexpr int MID_WARPS = MID_THREADS / 32;
 constexpr int MID_MAX = 2048;                     // order of the resident block
-constexpr int MID_XPT = MID_MAX / MID_THREADS;    // vector entries per thread
 constexpr int MID_RPC_MAX = 18;                   // rows per CTA
 constexpr int MID_NTR_MAX = MID_RPC_MAX / 3;      // row triples per CTA
 constexpr int MID_SPC = 2 * MID_NTR_MAX;          // sector stride per CTA (y triples, then p triples)
