@@ -1187,10 +1187,19 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane,
     // other cooperative grids may be in flight (EG pipeline, concurrent solves): launch exclusively
     const bool shared_gpu = gate != nullptr && (g_pipelines.load() > 0 || lane != 0 || background_thread());
     const auto tx0 = std::chrono::steady_clock::now();
+    struct WindowGuard {  // a failed launch must not leave the gate closed for the other chains
+      CoopGate* g = nullptr;
+      int per_sm = 1;
+      ~WindowGuard() {
+        if (g) g->exclusive_end(0, per_sm);
+      }
+    } window;
     if (shared_gpu) {
       KOT_CUDA(cudaStreamSynchronize(st));  // our own panels have retired
       const auto tx1 = std::chrono::steady_clock::now();
       gate->exclusive_begin();
+      window.g = gate;
+      window.per_sm = per_sm;
       prof_host("host.mid_sync", std::chrono::duration<double, std::milli>(tx1 - tx0).count());
       prof_host("host.mid_excl", std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tx1).count());
     }
@@ -1203,6 +1212,7 @@ static void sytrd(const double* Z, int n, EigWork& w, cudaStream_t st, int lane,
         if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(4)) break;  // the kernel's own timeout reports
       }
       prof_host("host.mid_resident", std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+      window.g = nullptr;
       gate->exclusive_end(Gm, per_sm);
     }
     KOT_CUDA(cudaMemcpyAsync(w.mid_err_host, w.mid_err, sizeof(int), cudaMemcpyDeviceToHost, st));
